@@ -1,0 +1,105 @@
+"""Per-client profile estimates (oracle; test infrastructure only).
+
+PAPER.md Table 1 (§2.2) lists the metrics Protea's UtilMonitor
+tracks; the hot path keeps VRAM (-> exact peak device bytes of the client's
+arena slot) and CUDA_time (-> device-timed training time, a measurement:
+"parity unpinned").  P:217 (§3.3): get_properties() reports "does this client
+use a GPU? How much VRAM is the training making use of? ... How long did it
+take to do the training".  Eq. (1) (§3.4):
+
+    num_gpus = vram_measured_for_single_worker / total_vram_in_system
+
+Definitions (DESIGN.md "Profiler" table; readings R2, R3, R21):
+  S_k      = E * ceil(n_k / B_k)
+  FLOPs_k  = E * n_k * f(model, w),   f = 2 * (fwd MACs + wgrad MACs + dgrad
+             MACs without the first layer's dgrad), per sample
+  HWM_k    = sum of align256(buffer bytes) over the slot layout below (the
+             arena is a bump allocator; nothing is freed inside a round)
+  q_k      = ceil(1024 * slot_k / sum_g C_g)   (Eq. (1) in units of 1/1024,
+             rounded up: SPEC D-7)
+"""
+from __future__ import annotations
+
+import math
+
+from .sgd import MLP, CNN, RESNET8, cnn_channels, n_params
+
+ALIGN = 256
+
+
+def align256(x: int) -> int:
+    return (x + ALIGN - 1) // ALIGN * ALIGN
+
+
+def local_steps(n: int, batch: int, epochs: int) -> int:
+    return epochs * math.ceil(n / batch)
+
+
+def macs_per_sample(model, width_q=4, classes=10):
+    """[(layer, MACs of one forward pass for one sample)] in forward order."""
+    if model == MLP:
+        return [("fc1", 784 * 64), ("fc2", 64 * classes)]
+    if model == CNN:
+        c1, c2, f = cnn_channels(width_q)
+        return [("conv1", 32 * 32 * c1 * 5 * 5 * 3),
+                ("conv2", 16 * 16 * c2 * 5 * 5 * c1),
+                ("fc1", 64 * c2 * f),
+                ("fc2", f * classes)]
+    if model == RESNET8:
+        return [("conv0", 32 * 32 * 16 * 9 * 3),
+                ("b1a", 32 * 32 * 16 * 9 * 16), ("b1b", 32 * 32 * 16 * 9 * 16),
+                ("b2a", 16 * 16 * 32 * 9 * 16), ("b2b", 16 * 16 * 32 * 9 * 32),
+                ("b3a", 8 * 8 * 64 * 9 * 32), ("b3b", 8 * 8 * 64 * 9 * 64),
+                ("fc", 64 * classes)]
+    raise ValueError(model)
+
+
+def flops_per_sample(model, width_q=4, classes=10) -> int:
+    layers = macs_per_sample(model, width_q, classes)
+    fwd = sum(m for _, m in layers)
+    wgrad = fwd
+    dgrad = sum(m for _, m in layers[1:])
+    return 2 * (fwd + wgrad + dgrad)
+
+
+def client_flops(n, epochs, model, width_q=4, classes=10) -> int:
+    return epochs * n * flops_per_sample(model, width_q, classes)
+
+
+def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
+    """[(buffer, bytes)] of one client's arena slot.
+
+    elem_bytes = 4 in fp32-verify mode, 2 in bf16 mode (activation storage).
+    """
+    b, e = batch, elem_bytes
+    P = n_params(model, width_q, classes)
+    out = [("params", 4 * P), ("perm", 4 * epochs * n), ("stats", 64)]
+    if model == MLP:
+        out += [("h1", b * 64 * e), ("dz1", b * 64 * 4)]
+    elif model == CNN:
+        c1, c2, f = cnn_channels(width_q)
+        out += [("a1", b * 256 * c1 * e), ("i1", b * 256 * c1),
+                ("a2", b * 64 * c2 * e), ("i2", b * 64 * c2),
+                ("h", b * f * e), ("dh", b * f * 4),
+                ("dz2", b * 256 * c2 * e), ("dz1", b * 1024 * c1 * e)]
+    elif model == RESNET8:
+        out += [("a0", b * 1024 * 16 * e),
+                ("r1", b * 1024 * 16 * e), ("o1", b * 1024 * 16 * e),
+                ("r2", b * 256 * 32 * e), ("o2", b * 256 * 32 * e),
+                ("r3", b * 64 * 64 * e), ("o3", b * 64 * 64 * e),
+                ("gap", b * 64 * e), ("dgap", b * 64 * 4),
+                ("g0", b * 1024 * 16 * e), ("g1", b * 1024 * 16 * e), ("g2", b * 1024 * 16 * e)]
+    else:
+        raise ValueError(model)
+    return out
+
+
+def hwm_bytes(model, width_q, classes, batch, n, epochs, elem_bytes) -> int:
+    return sum(align256(sz) for _, sz in slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes))
+
+
+def eq1_q1024(slot_bytes: int, total_capacity: int) -> int:
+    """Eq. (1) as an integer count of 1/1024 GPU (rounded up, SPEC D-7)."""
+    if total_capacity <= 0:
+        raise ValueError("no GPU capacity")
+    return -(-1024 * slot_bytes // total_capacity)

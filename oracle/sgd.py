@@ -1,0 +1,298 @@
+"""Local SGD of one client, float64 (oracle; test infrastructure only).
+
+PAPER.md never states the local training recipe: clients "finish training"
+(§3.2), ResNet-18 / LEAF CNN are named (§4.1) and batch sizes vary
+per client (§4.3).  The recipe below is DESIGN.md reading R10 (SURVEY
+§8(c).2), followed step by step:
+
+ 1. x = u8 / 255.
+ 2. epoch permutation pi_{k,e} (oracle/splitmix.py); `shuffle=False` = identity.
+ 3. batch j = pi[jB, min((j+1)B, n)), the last partial batch kept.
+ 4. forward: conv kxk zero-pad "same" (stride s), ReLU y=max(x,0) with
+    ReLU'(0)=0, max-pool 2x2/2 whose backward routes to the FIRST maximum in
+    row-major window order (strict >), FC y = x W^T + b.
+ 5. loss = mean over the actual batch |beta| of CE(softmax(z), y), softmax
+    stabilised by the row max; dz = (softmax - onehot)/|beta|.
+ 6. backward per layer in reverse: dX = dY W with the pre-update W,
+    dW = dY^T X, db = sum_rows dY; no dX for layer 1.
+ 7. plain SGD W <- W - lr dW, b <- b - lr db (no momentum / weight decay).
+ 8. repeat for E epochs; the client returns (w_k, n_k).
+
+Models (reading R11):
+  MLP 784-64-10;
+  CNN-w: conv5x5 3->32w, ReLU, pool2; conv5x5 32w->64w, ReLU, pool2;
+         FC 64w*64 -> 512w, ReLU; FC 512w -> classes;
+  ResNet-8 (He et al. 6n+2, n=1): conv3x3 3->16, ReLU; 3 basic blocks
+         (16, 32, 64 channels; stride 2 at blocks 2,3; option-A shortcut =
+         subsample x[:, ::2, ::2] and zero-pad the new channels at the END);
+         global average pool; FC 64 -> classes.  Conv biases, no BatchNorm.
+
+Layouts: activations NHWC; conv weights [Cout, k, k, Cin]; FC weights
+[out, in]; the CNN's FC1 input is the NHWC flatten of [8, 8, C2].  Flat
+parameter order: per layer W then b, layers in forward order.
+
+Convolution here is written as an explicit im2col + matmul (a library matmul
+used as one step); pooling and its backward are written out per window.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .splitmix import epoch_perm
+
+MLP, CNN, RESNET8 = 0, 1, 2
+
+
+# ---------------------------------------------------------------------------
+# model tables (the oracle's own copy)
+# ---------------------------------------------------------------------------
+def cnn_channels(width_q):
+    w = width_q / 4.0
+    return int(round(32 * w)), int(round(64 * w)), int(round(512 * w))
+
+
+def layer_shapes(model, width_q=4, classes=10):
+    """List of (name, W shape, b shape)."""
+    if model == MLP:
+        return [("fc1", (64, 784), (64,)), ("fc2", (classes, 64), (classes,))]
+    if model == CNN:
+        c1, c2, f = cnn_channels(width_q)
+        return [("conv1", (c1, 5, 5, 3), (c1,)), ("conv2", (c2, 5, 5, c1), (c2,)),
+                ("fc1", (f, 64 * c2), (f,)), ("fc2", (classes, f), (classes,))]
+    if model == RESNET8:
+        return [("conv0", (16, 3, 3, 3), (16,)),
+                ("b1a", (16, 3, 3, 16), (16,)), ("b1b", (16, 3, 3, 16), (16,)),
+                ("b2a", (32, 3, 3, 16), (32,)), ("b2b", (32, 3, 3, 32), (32,)),
+                ("b3a", (64, 3, 3, 32), (64,)), ("b3b", (64, 3, 3, 64), (64,)),
+                ("fc", (classes, 64), (classes,))]
+    raise ValueError(model)
+
+
+def n_params(model, width_q=4, classes=10):
+    return sum(int(np.prod(w)) + int(np.prod(b)) for _, w, b in layer_shapes(model, width_q, classes))
+
+
+def unpack(flat, model, width_q=4, classes=10):
+    p, off = {}, 0
+    for name, ws, bs in layer_shapes(model, width_q, classes):
+        nw, nb = int(np.prod(ws)), int(np.prod(bs))
+        p[name + ".W"] = flat[off:off + nw].reshape(ws)
+        off += nw
+        p[name + ".b"] = flat[off:off + nb].reshape(bs)
+        off += nb
+    assert off == flat.size
+    return p
+
+
+def pack(p, model, width_q=4, classes=10):
+    return np.concatenate([np.concatenate([p[n + ".W"].ravel(), p[n + ".b"].ravel()])
+                           for n, _, _ in layer_shapes(model, width_q, classes)])
+
+
+def input_shape(model):
+    return (28, 28, 1) if model == MLP else (32, 32, 3)
+
+
+# ---------------------------------------------------------------------------
+# layer primitives
+# ---------------------------------------------------------------------------
+def im2col(x, k, stride, pad):
+    """x [n,H,W,C] -> cols [n,Ho,Wo,k,k,C] with zero padding."""
+    n, H, W, C = x.shape
+    Ho = (H + 2 * pad - k) // stride + 1
+    Wo = (W + 2 * pad - k) // stride + 1
+    xp = np.zeros((n, H + 2 * pad, W + 2 * pad, C), dtype=x.dtype)
+    xp[:, pad:pad + H, pad:pad + W, :] = x
+    cols = np.empty((n, Ho, Wo, k, k, C), dtype=x.dtype)
+    for ky in range(k):
+        for kx in range(k):
+            cols[:, :, :, ky, kx, :] = xp[:, ky:ky + stride * Ho:stride, kx:kx + stride * Wo:stride, :]
+    return cols
+
+
+def col2im(dcols, x_shape, k, stride, pad):
+    """Adjoint of im2col: scatter-add dcols [n,Ho,Wo,k,k,C] into dx [n,H,W,C]."""
+    n, H, W, C = x_shape
+    Ho, Wo = dcols.shape[1], dcols.shape[2]
+    dxp = np.zeros((n, H + 2 * pad, W + 2 * pad, C), dtype=dcols.dtype)
+    for ky in range(k):
+        for kx in range(k):
+            dxp[:, ky:ky + stride * Ho:stride, kx:kx + stride * Wo:stride, :] += dcols[:, :, :, ky, kx, :]
+    return dxp[:, pad:pad + H, pad:pad + W, :]
+
+
+def conv_fwd(x, Wt, b, stride, pad):
+    co, k = Wt.shape[0], Wt.shape[1]
+    cols = im2col(x, k, stride, pad)
+    n, Ho, Wo = cols.shape[:3]
+    z = cols.reshape(n * Ho * Wo, -1) @ Wt.reshape(co, -1).T + b
+    return z.reshape(n, Ho, Wo, co), cols
+
+
+def conv_bwd(dz, x_shape, cols, Wt, stride, pad, need_dx):
+    co, k = Wt.shape[0], Wt.shape[1]
+    dzm = dz.reshape(-1, co)
+    dW = (dzm.T @ cols.reshape(dzm.shape[0], -1)).reshape(Wt.shape)
+    db = dzm.sum(axis=0)
+    dx = None
+    if need_dx:
+        dcols = (dzm @ Wt.reshape(co, -1)).reshape(cols.shape)
+        dx = col2im(dcols, x_shape, k, stride, pad)
+    return dW, db, dx
+
+
+def relu(z):
+    return np.maximum(z, 0.0)
+
+
+def pool2_fwd(r):
+    """2x2/2 max pool of r [n,H,W,C]; returns (pooled, argmax q in 0..3).
+    Window order q = 2*dy + dx (row-major); the first maximum wins (strict >)."""
+    n, H, W, C = r.shape
+    win = [r[:, dy::2, dx::2, :] for dy in (0, 1) for dx in (0, 1)]
+    best = win[0].copy()
+    arg = np.zeros(best.shape, dtype=np.int64)
+    for q in (1, 2, 3):
+        upd = win[q] > best
+        best = np.where(upd, win[q], best)
+        arg = np.where(upd, q, arg)
+    return best, arg
+
+
+def pool2_bwd(dp, arg, shape):
+    dr = np.zeros(shape, dtype=dp.dtype)
+    for q in range(4):
+        dy, dx = divmod(q, 2)
+        dr[:, dy::2, dx::2, :] = np.where(arg == q, dp, 0.0)
+    return dr
+
+
+def softmax_ce(z, y):
+    """Mean CE over the batch and dz = (softmax - onehot)/|beta|."""
+    nb = z.shape[0]
+    m = z.max(axis=1, keepdims=True)
+    e = np.exp(z - m)
+    s = e.sum(axis=1, keepdims=True)
+    p = e / s
+    loss = float(np.mean(np.log(s[:, 0]) + m[:, 0] - z[np.arange(nb), y]))
+    dz = p.copy()
+    dz[np.arange(nb), y] -= 1.0
+    return loss, dz / nb
+
+
+# ---------------------------------------------------------------------------
+# per-model loss + gradient
+# ---------------------------------------------------------------------------
+def loss_and_grad(p, model, xb, yb):
+    """xb float64 [nb, H, W, C] in [0,1]; returns (loss, grads dict)."""
+    g = {}
+    nb = xb.shape[0]
+    if model == MLP:
+        x = xb.reshape(nb, -1)
+        z1 = x @ p["fc1.W"].T + p["fc1.b"]
+        h1 = relu(z1)
+        z2 = h1 @ p["fc2.W"].T + p["fc2.b"]
+        loss, dz2 = softmax_ce(z2, yb)
+        g["fc2.W"], g["fc2.b"] = dz2.T @ h1, dz2.sum(0)
+        dh1 = dz2 @ p["fc2.W"]
+        dz1 = dh1 * (z1 > 0)
+        g["fc1.W"], g["fc1.b"] = dz1.T @ x, dz1.sum(0)
+        return loss, g
+    if model == CNN:
+        z1, cols1 = conv_fwd(xb, p["conv1.W"], p["conv1.b"], 1, 2)
+        a1, arg1 = pool2_fwd(relu(z1))
+        z2, cols2 = conv_fwd(a1, p["conv2.W"], p["conv2.b"], 1, 2)
+        a2, arg2 = pool2_fwd(relu(z2))
+        f = a2.reshape(nb, -1)
+        z3 = f @ p["fc1.W"].T + p["fc1.b"]
+        h = relu(z3)
+        z4 = h @ p["fc2.W"].T + p["fc2.b"]
+        loss, dz4 = softmax_ce(z4, yb)
+        g["fc2.W"], g["fc2.b"] = dz4.T @ h, dz4.sum(0)
+        dz3 = (dz4 @ p["fc2.W"]) * (z3 > 0)
+        g["fc1.W"], g["fc1.b"] = dz3.T @ f, dz3.sum(0)
+        da2 = (dz3 @ p["fc1.W"]).reshape(a2.shape)
+        dz2 = pool2_bwd(da2, arg2, z2.shape) * (z2 > 0)
+        g["conv2.W"], g["conv2.b"], da1 = conv_bwd(dz2, a1.shape, cols2, p["conv2.W"], 1, 2, True)
+        dz1 = pool2_bwd(da1, arg1, z1.shape) * (z1 > 0)
+        g["conv1.W"], g["conv1.b"], _ = conv_bwd(dz1, xb.shape, cols1, p["conv1.W"], 1, 2, False)
+        return loss, g
+    if model == RESNET8:
+        z0, cols0 = conv_fwd(xb, p["conv0.W"], p["conv0.b"], 1, 1)
+        a0 = relu(z0)
+        caches = []
+        a = a0
+        for blk, stride in (("b1", 1), ("b2", 2), ("b3", 2)):
+            za, colsa = conv_fwd(a, p[blk + "a.W"], p[blk + "a.b"], stride, 1)
+            ra = relu(za)
+            zb, colsb = conv_fwd(ra, p[blk + "b.W"], p[blk + "b.b"], 1, 1)
+            cout = zb.shape[3]
+            if stride == 1 and a.shape[3] == cout:
+                sc = a
+            else:
+                sub = a[:, ::2, ::2, :]
+                sc = np.zeros(sub.shape[:3] + (cout,))
+                sc[..., :sub.shape[3]] = sub
+            s = zb + sc
+            out = relu(s)
+            caches.append((blk, stride, a, za, colsa, ra, colsb, s))
+            a = out
+        gap = a.mean(axis=(1, 2))
+        z = gap @ p["fc.W"].T + p["fc.b"]
+        loss, dz = softmax_ce(z, yb)
+        g["fc.W"], g["fc.b"] = dz.T @ gap, dz.sum(0)
+        dgap = dz @ p["fc.W"]
+        HW = a.shape[1] * a.shape[2]
+        dout = np.broadcast_to(dgap[:, None, None, :] / HW, a.shape).copy()
+        for blk, stride, a_in, za, colsa, ra, colsb, s in reversed(caches):
+            ds = dout * (s > 0)
+            g[blk + "b.W"], g[blk + "b.b"], dra = conv_bwd(ds, ra.shape, colsb, p[blk + "b.W"], 1, 1, True)
+            dza = dra * (za > 0)
+            g[blk + "a.W"], g[blk + "a.b"], da_in = conv_bwd(dza, a_in.shape, colsa, p[blk + "a.W"], stride, 1, True)
+            if stride == 1 and a_in.shape[3] == ds.shape[3]:
+                da_in = da_in + ds
+            else:
+                da_in[:, ::2, ::2, :] += ds[..., :a_in.shape[3]]
+            dout = da_in
+        dz0 = dout * (z0 > 0)
+        g["conv0.W"], g["conv0.b"], _ = conv_bwd(dz0, xb.shape, cols0, p["conv0.W"], 1, 1, False)
+        return loss, g
+    raise ValueError(model)
+
+
+def flat_loss_and_grad(w, model, width_q, classes, xb, yb):
+    p = unpack(np.asarray(w, dtype=np.float64), model, width_q, classes)
+    loss, g = loss_and_grad(p, model, xb, yb)
+    return loss, pack(g, model, width_q, classes)
+
+
+# ---------------------------------------------------------------------------
+# local SGD
+# ---------------------------------------------------------------------------
+def steps(n, batch, epochs):
+    return epochs * math.ceil(n / batch)
+
+
+def local_sgd(w0, model, width_q, classes, x_u8, y, batch, epochs, lr, seed, rnd, client_id,
+              shuffle=True, max_steps=None):
+    """Run one client's local SGD; returns (w_k float64, losses list)."""
+    w = np.array(w0, dtype=np.float64)
+    n = x_u8.shape[0]
+    H, W, C = input_shape(model)
+    xf = x_u8.reshape(n, H, W, C).astype(np.float64) / 255.0
+    nbat = math.ceil(n / batch)
+    losses = []
+    done = 0
+    for e in range(epochs):
+        perm = epoch_perm(n, seed, rnd, client_id, e) if shuffle else list(range(n))
+        for j in range(nbat):
+            if max_steps is not None and done >= max_steps:
+                return w, losses
+            idx = perm[j * batch:min((j + 1) * batch, n)]
+            loss, gflat = flat_loss_and_grad(w, model, width_q, classes, xf[idx], y[idx])
+            w = w - lr * gflat
+            losses.append(loss)
+            done += 1
+    return w, losses
