@@ -1,0 +1,229 @@
+/*
+ * protea.h — C ABI of the B200-native Protea hot path.
+ *
+ * What the library does (PAPER.md = the Protea paper, arXiv 2207.01053):
+ *   - profile clients: peak device bytes + device-timed training time
+ *     (Table 1 "VRAM", "CUDA_time", §2.2; get_properties() P:217 §3.3);
+ *   - plan: turn profiles into GPU memory slots and a FIFO admission schedule
+ *     (Eq. (1) P:243-249 §3.4; VCE stages (1)-(4) P:209 §3.2);
+ *   - run one federated round: every sampled client's local SGD epochs on its
+ *     own shard with its own batch size / model width, then sample-weighted
+ *     FedAvg (§3.3 configure_fit / aggregate_fit);
+ *   - FedAvg of arbitrary device vectors (McMahan et al. P:83).
+ *
+ * Conventions (apply to every call):
+ *   - Ownership: the caller owns every array it passes and must keep it alive
+ *     for the duration of the call only.  The library never retains caller
+ *     pointers, EXCEPT the arena block given to protea_init, which must outlive
+ *     the context.  The library owns (and frees in protea_finalize) its device
+ *     copies of shards and its workspace.
+ *   - Errors: every call returns a protea_status.  Validation runs before any
+ *     device work, so on error no output is written.  protea_last_error()
+ *     returns a message naming the offending client / field.
+ *   - Threading: one context per GPU / rank; a context is not thread-safe.
+ *     protea_plan is a pure host function (no context) and deterministic, so
+ *     every rank computes the identical plan.
+ *   - Pointers: "device" = CUDA device memory of the context's GPU; "host" =
+ *     ordinary (preferably pinned) host memory.  protea_run_round accepts
+ *     either for global_in / global_out (cudaPointerGetAttributes decides).
+ *   - Streams: all device work is ordered on the stream given at init; calls
+ *     return after that stream is synchronised.
+ */
+#ifndef PROTEA_H
+#define PROTEA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PROTEA_OK = 0,
+  PROTEA_ERR_INVALID = 1,     /* null pointer, n == 0, batch/epochs <= 0, n_k <= 0, unknown model, duplicate id */
+  PROTEA_ERR_EMPTY = 2,       /* no results to aggregate */
+  PROTEA_ERR_ZERO_WEIGHT = 3, /* sum of num_examples == 0 */
+  PROTEA_ERR_DIM = 4,         /* dimension mismatch */
+  PROTEA_ERR_NO_CAPACITY = 5, /* a slot exceeds every GPU's capacity (rejected, not clamped) */
+  PROTEA_ERR_PLAN = 6,        /* plan/client mismatch, overlap, slot too small, missing client */
+  PROTEA_ERR_OOM = 7,         /* arena overrun: the plan does not fit the arena */
+  PROTEA_ERR_CUDA = 8,
+  PROTEA_ERR_NCCL = 9
+} protea_status;
+
+enum { PROTEA_MODEL_MLP = 0, PROTEA_MODEL_CNN = 1, PROTEA_MODEL_RESNET8 = 2 };
+enum { PROTEA_PREC_FP32 = 0, PROTEA_PREC_BF16 = 1 };
+enum { PROTEA_POLICY_PROFILED = 0, PROTEA_POLICY_STATIC = 1 };
+enum { PROTEA_ORDER_ASC_ID = 0, PROTEA_ORDER_DESC_STEPS = 1 };
+
+typedef struct protea_ctx protea_ctx;
+
+typedef struct {
+  int32_t device;          /* CUDA device ordinal of this rank */
+  int32_t rank;            /* this rank in [0, world) */
+  int32_t world;           /* number of ranks (GPUs); 1 = no NCCL */
+  int32_t precision;       /* PROTEA_PREC_*: activation storage + GEMM operand type */
+  const uint8_t* nccl_id;  /* host, 128 bytes (ncclUniqueId from rank 0, broadcast by the caller); NULL iff world == 1 */
+  void* arena;             /* device, caller-owned block holding the client slots (e.g. a torch uint8 tensor) */
+  uint64_t arena_bytes;    /* capacity C_g of this GPU's arena */
+  void* stream;            /* cudaStream_t to order all work on (NULL = the legacy default stream) */
+} protea_init_opts;
+
+/* Model family of a shape group.  CNN: width = width_q / 4, width_q in {1,2,4}
+ * (BASELINE.json configs[3]); MLP / RESNET8 require width_q == 4.
+ * H, W, C: input image shape (MLP 28x28x1, CNN / RESNET8 32x32x3). */
+typedef struct {
+  int32_t arch;      /* PROTEA_MODEL_* */
+  int32_t width_q;
+  int32_t classes;
+  int32_t H, W, C;
+} protea_model_desc;
+
+/* One client's data shard: n_k examples, NHWC u8 pixels x[n*H*W*C], labels y[n] in [0, classes). Host pointers. */
+typedef struct {
+  int64_t client_id;
+  int64_t n;
+  const uint8_t* x;
+  const int32_t* y;
+} protea_shard;
+
+/* One sampled client of a round. */
+typedef struct {
+  int64_t client_id;
+  int32_t model_id;  /* from protea_register_model */
+  int32_t batch;     /* B_k > 0 */
+  int32_t epochs;    /* E > 0 */
+  int32_t reserved;
+} protea_client;
+
+/* get_properties() record; integer SI units. */
+typedef struct {
+  int64_t client_id;
+  uint64_t peak_bytes;  /* exact arena high-water mark of the client's slot (Table 1 VRAM) */
+  uint64_t steps;       /* S_k = E * ceil(n_k / B_k) */
+  uint64_t flops;       /* E * n_k * f(model, width) */
+  uint64_t step_ns;     /* device time of one local step (CUDA events, probe; Table 1 CUDA_time / S_k) */
+  uint64_t train_ns;    /* step_ns * steps (estimate) or measured in-run attribution */
+  uint64_t sm_ns;       /* in-run SM time attributed to the client (0 if not measured) */
+  uint32_t uses_gpu;    /* 1 */
+  uint32_t reserved;
+} protea_profile;
+
+typedef struct {
+  uint32_t n_gpus;            /* G >= 1 */
+  uint32_t reserved;
+  const uint64_t* capacity;   /* host, C_g for g in [0, G) (bytes) */
+} protea_cluster;
+
+typedef struct {
+  int32_t policy;             /* PROTEA_POLICY_PROFILED (slots from profiles) or _STATIC (one client per GPU) */
+  int32_t order;              /* PROTEA_ORDER_ASC_ID (paper FIFO) or _DESC_STEPS */
+  uint32_t margin_permille;   /* slot = align256(ceil(peak * margin / 1000)); >= 1000 */
+  uint32_t max_active;        /* 0 = unlimited */
+} protea_plan_opts;
+
+typedef struct {
+  int64_t client_id;
+  int32_t gpu;
+  uint32_t q1024;    /* Eq. (1): ceil(1024 * slot / sum_g C_g) — num_gpus in units of 1/1024 */
+  uint64_t offset;   /* slot offset in the GPU's arena */
+  uint64_t slot;     /* slot bytes */
+  uint64_t admit;    /* first lock-step iteration */
+  uint64_t release;  /* admit + S_k */
+} protea_assignment;
+
+/* Op classes of one lock-step iteration (kernel families), for per-op timing
+ * and the algorithmic work counters of protea_round_stats. */
+enum {
+  PROTEA_OPC_CONV1_FWD = 0, PROTEA_OPC_CONV2_FWD, PROTEA_OPC_FC1_FWD, PROTEA_OPC_HEAD, PROTEA_OPC_FC1_DGRAD,
+  PROTEA_OPC_FC1_WGRAD, PROTEA_OPC_CONV2_DGRAD, PROTEA_OPC_CONV2_WGRAD, PROTEA_OPC_CONV2_REDUCE,
+  PROTEA_OPC_CONV1_WGRAD, PROTEA_OPC_CONV1_REDUCE, PROTEA_OPC_MLP_FC1_FWD, PROTEA_OPC_MLP_HEAD,
+  PROTEA_OPC_MLP_FC1_WGRAD, PROTEA_OPC_ADMIT, PROTEA_OPC_FEDAVG, PROTEA_N_OPC = 16
+};
+
+typedef struct {
+  float lr;          /* SGD learning rate eta */
+  uint32_t seed;     /* permutation seed (oracle/splitmix reading R10) */
+  uint32_t round;    /* round index */
+  int32_t shuffle;   /* 1 = SplitMix64 epoch permutation, 0 = identity order */
+  uint32_t time_ops; /* bitmask over PROTEA_OPC_*: bracket every launch of those classes with CUDA events */
+  uint32_t reserved;
+} protea_round_opts;
+
+typedef struct {
+  uint64_t round_ns;        /* device time of the whole round on this rank (CUDA events) */
+  uint64_t iterations;      /* lock-step iterations run on this rank (= makespan of its GPU) */
+  uint64_t client_steps;    /* sum S_k over this rank's clients */
+  uint64_t kernel_launches; /* kernels launched by the round on this rank */
+  uint64_t flops;           /* sum FLOPs_k over this rank's clients */
+  double loss_sum;          /* sum over this rank's client steps of the mean batch loss */
+  uint64_t op_ns[PROTEA_N_OPC];       /* summed device time of the op classes selected by time_ops */
+  uint64_t op_launches[PROTEA_N_OPC]; /* kernel launches per op class */
+  uint64_t op_flops[PROTEA_N_OPC];    /* algorithmic FLOPs per op class (2 x useful MACs) */
+  uint64_t op_bytes[PROTEA_N_OPC];    /* algorithmic (compulsory) HBM bytes per op class: operands read once, results written once */
+} protea_round_stats;
+
+/* Create a context on opts->device.  world > 1 bootstraps an NCCL communicator
+ * from opts->nccl_id.  Errors: INVALID (bad field), CUDA, NCCL. */
+protea_status protea_init(const protea_init_opts* opts, protea_ctx** out);
+
+/* Free the context, its device copies and workspace (not the caller's arena). */
+void protea_finalize(protea_ctx* ctx);
+
+/* Message of the last failed call on ctx (or of the last failed context-free call when ctx == NULL). */
+const char* protea_last_error(const protea_ctx* ctx);
+
+/* Register a shape group.  Its global weights occupy [offset, offset + n_params)
+ * of the concatenated global vector, groups in registration order; *n_params
+ * receives P of this group.  Errors: INVALID. */
+protea_status protea_register_model(protea_ctx* ctx, const protea_model_desc* desc, int32_t* model_id,
+                                    uint64_t* n_params);
+
+/* Copy n shards to device (library-owned).  Re-registering an id replaces it.
+ * Errors: INVALID (null, n_k <= 0, label out of range is not checked), CUDA. */
+protea_status protea_register_shards(protea_ctx* ctx, const protea_shard* shards, size_t n);
+
+/* Profile n clients (shards must be registered): exact peak bytes, S_k, FLOPs,
+ * and the device time of one probe step per shape class (model, batch) run in
+ * the arena (which must not be in use).  out: caller-allocated, n records.
+ * Errors: INVALID, OOM (arena smaller than a probe slot), CUDA. */
+protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clients, size_t n,
+                                     protea_profile* out);
+
+/* Pure host planner (no context): LPT partition by FLOPs across GPUs, then
+ * per-GPU strict-FIFO admission replay with address first-fit.
+ * out: caller-allocated n records, written in ascending client_id order;
+ * makespan_steps: caller-allocated G entries.
+ * Errors: INVALID, NO_CAPACITY, PLAN. */
+protea_status protea_plan(const protea_profile* profiles, size_t n, const protea_cluster* cluster,
+                          const protea_plan_opts* opts, protea_assignment* out, uint64_t* makespan_steps);
+
+/* Run one round.  Every rank passes the same clients and plan; this rank runs
+ * the clients whose gpu == rank in lock-step iterations at their planned arena
+ * offsets, then all ranks sum the per-GPU FedAvg partials (NCCL when world > 1)
+ * and every rank writes the new global weights.
+ * global_in / global_out: n_params floats (all registered groups concatenated),
+ * host or device; a group without sampled clients is copied unchanged.
+ * measured (nullable): n records of in-run profiles; stats (nullable).
+ * Errors: INVALID, PLAN, OOM, CUDA, NCCL. */
+protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, const protea_client* clients,
+                               size_t n, const protea_assignment* plan, const float* global_in, float* global_out,
+                               size_t n_params, protea_profile* measured, protea_round_stats* stats);
+
+/* out[d] = sum_k n_k params[k][d] / sum_k n_k, fp64 accumulation in the given
+ * order, one rounding to fp32.  params: host array of n device pointers, each
+ * dim floats; out: device, dim floats.
+ * Errors: EMPTY (n == 0), INVALID (null, n_k <= 0), ZERO_WEIGHT, CUDA. */
+protea_status protea_fedavg(protea_ctx* ctx, const float* const* params, const int64_t* num_examples, size_t n,
+                            size_t dim, float* out);
+
+/* Host helpers (pure, no context) mirroring the profiler formulas, so callers
+ * can plan without a GPU: slot bytes (exact HWM) and FLOPs of one client. */
+protea_status protea_client_footprint(const protea_model_desc* desc, int64_t n, int32_t batch, int32_t epochs,
+                                      int32_t precision, uint64_t* peak_bytes, uint64_t* steps, uint64_t* flops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PROTEA_H */

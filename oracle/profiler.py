@@ -66,10 +66,27 @@ def client_flops(n, epochs, model, width_q=4, classes=10) -> int:
     return epochs * n * flops_per_sample(model, width_q, classes)
 
 
+WGRAD_CHUNK_PX = 2048  # pixels reduced by one split of a conv weight-gradient GEMM
+
+
+def conv_layers(model, width_q=4):
+    """[(Hout*Wout, cout, k*k*cin)] of every conv layer (for the wgrad split buffer)."""
+    if model == CNN:
+        c1, c2, _ = cnn_channels(width_q)
+        return [(1024, c1, 25 * 3), (256, c2, 25 * c1)]
+    if model == RESNET8:
+        return [(1024, 16, 27), (1024, 16, 144), (1024, 16, 144), (256, 32, 144), (256, 32, 288),
+                (64, 64, 288), (64, 64, 576)]
+    return []
+
+
 def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
     """[(buffer, bytes)] of one client's arena slot.
 
     elem_bytes = 4 in fp32-verify mode, 2 in bf16 mode (activation storage).
+    wsp = split-K partials of the conv weight gradients: each conv layer's
+    reduction over b*Hout*Wout pixels is cut into ceil(b*Hout*Wout / 2048)
+    splits, each holding cout*(K+1) fp32 partials (the +1 is the bias column).
     """
     b, e = batch, elem_bytes
     P = n_params(model, width_q, classes)
@@ -91,6 +108,9 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
                 ("g0", b * 1024 * 16 * e), ("g1", b * 1024 * 16 * e), ("g2", b * 1024 * 16 * e)]
     else:
         raise ValueError(model)
+    convs = conv_layers(model, width_q)
+    if convs:
+        out.append(("wsp", 4 * max(math.ceil(b * hw / WGRAD_CHUNK_PX) * co * (K + 1) for hw, co, K in convs)))
     return out
 
 

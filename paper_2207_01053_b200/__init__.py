@@ -1,0 +1,229 @@
+"""Thin Python binding of libprotea.so (include/protea.h), argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only
+converts numpy / torch objects to the C structs and pointers the ABI takes.
+There is no CPU fallback: importing the package fails loudly if the shared
+library is missing (build it with `python -m paper_2207_01053_b200.build` or
+`__graft_entry__.build()`).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libprotea.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libprotea.so not built at {LIB_PATH}: run __graft_entry__.build()")
+_lib = ctypes.CDLL(LIB_PATH)
+
+# status codes (protea_status)
+OK, ERR_INVALID, ERR_EMPTY, ERR_ZERO_WEIGHT, ERR_DIM, ERR_NO_CAPACITY, ERR_PLAN, ERR_OOM, ERR_CUDA, ERR_NCCL = range(10)
+STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "EMPTY", 3: "ZERO_WEIGHT", 4: "DIM", 5: "NO_CAPACITY", 6: "PLAN", 7: "OOM",
+                8: "CUDA", 9: "NCCL"}
+MODEL_MLP, MODEL_CNN, MODEL_RESNET8 = 0, 1, 2
+PREC_FP32, PREC_BF16 = 0, 1
+POLICY_PROFILED, POLICY_STATIC = 0, 1
+ORDER_ASC_ID, ORDER_DESC_STEPS = 0, 1
+
+EXPORTS = ["protea_init", "protea_finalize", "protea_last_error", "protea_register_model", "protea_register_shards",
+           "protea_profile_clients", "protea_plan", "protea_run_round", "protea_fedavg", "protea_client_footprint"]
+
+
+class ProteaError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+        self.name = STATUS_NAMES.get(code, str(code))
+
+
+# ---------------------------------------------------------------------------
+# C structs
+# ---------------------------------------------------------------------------
+class InitOpts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("precision", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("arena", ctypes.c_void_p),
+                ("arena_bytes", ctypes.c_uint64), ("stream", ctypes.c_void_p)]
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [("arch", ctypes.c_int32), ("width_q", ctypes.c_int32), ("classes", ctypes.c_int32),
+                ("H", ctypes.c_int32), ("W", ctypes.c_int32), ("C", ctypes.c_int32)]
+
+
+class Cluster(ctypes.Structure):
+    _fields_ = [("n_gpus", ctypes.c_uint32), ("reserved", ctypes.c_uint32), ("capacity", ctypes.c_void_p)]
+
+
+class PlanOpts(ctypes.Structure):
+    _fields_ = [("policy", ctypes.c_int32), ("order", ctypes.c_int32), ("margin_permille", ctypes.c_uint32),
+                ("max_active", ctypes.c_uint32)]
+
+
+class RoundOpts(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_float), ("seed", ctypes.c_uint32), ("round", ctypes.c_uint32),
+                ("shuffle", ctypes.c_int32)]
+
+
+class RoundStats(ctypes.Structure):
+    _fields_ = [("round_ns", ctypes.c_uint64), ("iterations", ctypes.c_uint64), ("client_steps", ctypes.c_uint64),
+                ("kernel_launches", ctypes.c_uint64), ("flops", ctypes.c_uint64), ("loss_sum", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+SHARD_DT = np.dtype([("client_id", "<i8"), ("n", "<i8"), ("x", "<u8"), ("y", "<u8")], align=True)
+CLIENT_DT = np.dtype([("client_id", "<i8"), ("model_id", "<i4"), ("batch", "<i4"), ("epochs", "<i4"),
+                      ("reserved", "<i4")], align=True)
+PROFILE_DT = np.dtype([("client_id", "<i8"), ("peak_bytes", "<u8"), ("steps", "<u8"), ("flops", "<u8"),
+                       ("step_ns", "<u8"), ("train_ns", "<u8"), ("sm_ns", "<u8"), ("uses_gpu", "<u4"),
+                       ("reserved", "<u4")], align=True)
+ASSIGN_DT = np.dtype([("client_id", "<i8"), ("gpu", "<i4"), ("q1024", "<u4"), ("offset", "<u8"), ("slot", "<u8"),
+                      ("admit", "<u8"), ("release", "<u8")], align=True)
+assert SHARD_DT.itemsize == 32 and CLIENT_DT.itemsize == 24 and PROFILE_DT.itemsize == 64 and ASSIGN_DT.itemsize == 48
+
+_vp, _sz = ctypes.c_void_p, ctypes.c_size_t
+_lib.protea_init.argtypes = [ctypes.POINTER(InitOpts), ctypes.POINTER(ctypes.c_void_p)]
+_lib.protea_finalize.argtypes = [_vp]
+_lib.protea_finalize.restype = None
+_lib.protea_last_error.argtypes = [_vp]
+_lib.protea_last_error.restype = ctypes.c_char_p
+_lib.protea_register_model.argtypes = [_vp, ctypes.POINTER(ModelDesc), ctypes.POINTER(ctypes.c_int32),
+                                       ctypes.POINTER(ctypes.c_uint64)]
+_lib.protea_register_shards.argtypes = [_vp, _vp, _sz]
+_lib.protea_profile_clients.argtypes = [_vp, _vp, _sz, _vp]
+_lib.protea_plan.argtypes = [_vp, _sz, ctypes.POINTER(Cluster), ctypes.POINTER(PlanOpts), _vp, _vp]
+_lib.protea_run_round.argtypes = [_vp, ctypes.POINTER(RoundOpts), _vp, _sz, _vp, _vp, _vp, _sz, _vp,
+                                  ctypes.POINTER(RoundStats)]
+_lib.protea_fedavg.argtypes = [_vp, _vp, _vp, _sz, _sz, _vp]
+_lib.protea_client_footprint.argtypes = [ctypes.POINTER(ModelDesc), ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int32, ctypes.POINTER(ctypes.c_uint64),
+                                         ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+for _f in EXPORTS:
+    if _f not in ("protea_finalize", "protea_last_error"):
+        getattr(_lib, _f).restype = ctypes.c_int
+
+
+def _check(code, ctx=None):
+    if code != OK:
+        msg = _lib.protea_last_error(ctx)
+        raise ProteaError(code, msg.decode() if msg else "")
+
+
+def _ptr(a):
+    """data pointer of a numpy array or torch tensor (or an int)."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return a
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+# ---------------------------------------------------------------------------
+# ABI calls (same names as include/protea.h)
+# ---------------------------------------------------------------------------
+def protea_init(device=0, rank=0, world=1, precision=PREC_FP32, arena=None, arena_bytes=0, stream=None,
+                nccl_id=None):
+    """arena: device tensor (uint8) or pointer; stream: torch.cuda.Stream, cudaStream_t int, or None."""
+    if stream is not None and hasattr(stream, "cuda_stream"):
+        stream = stream.cuda_stream
+    nid = None
+    if nccl_id is not None:
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(bytes(nccl_id))
+        nid = ctypes.addressof(buf)
+    if arena is not None and hasattr(arena, "numel") and not arena_bytes:
+        arena_bytes = arena.numel() * arena.element_size()
+    o = InitOpts(device, rank, world, precision, nid, _ptr(arena), arena_bytes, stream)
+    ctx = ctypes.c_void_p()
+    _check(_lib.protea_init(ctypes.byref(o), ctypes.byref(ctx)))
+    return ctx
+
+
+def protea_finalize(ctx):
+    _lib.protea_finalize(ctx)
+
+
+def protea_last_error(ctx=None):
+    m = _lib.protea_last_error(ctx)
+    return m.decode() if m else ""
+
+
+def protea_register_model(ctx, arch, width_q=4, classes=10, H=32, W=32, C=3):
+    d = ModelDesc(arch, width_q, classes, H, W, C)
+    mid, npar = ctypes.c_int32(), ctypes.c_uint64()
+    _check(_lib.protea_register_model(ctx, ctypes.byref(d), ctypes.byref(mid), ctypes.byref(npar)), ctx)
+    return mid.value, npar.value
+
+
+def protea_register_shards(ctx, shards):
+    """shards: iterable of (client_id, x u8 [n, D], y int32 [n]) host arrays."""
+    keep = []
+    rec = np.zeros(len(shards), dtype=SHARD_DT)
+    for i, (cid, x, y) in enumerate(shards):
+        x = np.ascontiguousarray(x, dtype=np.uint8)
+        y = np.ascontiguousarray(y, dtype=np.int32)
+        keep += [x, y]
+        rec[i] = (cid, y.shape[0], x.ctypes.data, y.ctypes.data)
+    _check(_lib.protea_register_shards(ctx, rec.ctypes.data, len(rec)), ctx)
+
+
+def clients_array(rows):
+    """rows: iterable of (client_id, model_id, batch, epochs) -> CLIENT_DT array."""
+    rows = list(rows)
+    a = np.zeros(len(rows), dtype=CLIENT_DT)
+    for i, (cid, mid, b, e) in enumerate(rows):
+        a[i] = (cid, mid, b, e, 0)
+    return a
+
+
+def protea_profile_clients(ctx, clients):
+    out = np.zeros(len(clients), dtype=PROFILE_DT)
+    _check(_lib.protea_profile_clients(ctx, clients.ctypes.data, len(clients), out.ctypes.data), ctx)
+    return out
+
+
+def protea_plan(profiles, caps, policy=POLICY_PROFILED, order=ORDER_ASC_ID, margin_permille=1000, max_active=0):
+    profiles = np.ascontiguousarray(profiles, dtype=PROFILE_DT)
+    caps = np.ascontiguousarray(caps, dtype=np.uint64)
+    cl = Cluster(len(caps), 0, caps.ctypes.data)
+    po = PlanOpts(policy, order, margin_permille, max_active)
+    out = np.zeros(len(profiles), dtype=ASSIGN_DT)
+    mk = np.zeros(len(caps), dtype=np.uint64)
+    _check(_lib.protea_plan(profiles.ctypes.data, len(profiles), ctypes.byref(cl), ctypes.byref(po),
+                            out.ctypes.data, mk.ctypes.data))
+    return out, mk
+
+
+def protea_run_round(ctx, clients, plan, global_in, global_out, lr=0.05, seed=0, rnd=0, shuffle=True,
+                     measured=False):
+    """global_in / global_out: float32 torch tensors (cuda or cpu) or numpy arrays."""
+    o = RoundOpts(lr, seed, rnd, 1 if shuffle else 0)
+    st = RoundStats()
+    n_params = global_in.numel() if hasattr(global_in, "numel") else global_in.size
+    meas = np.zeros(len(clients), dtype=PROFILE_DT) if measured else None
+    _check(_lib.protea_run_round(ctx, ctypes.byref(o), clients.ctypes.data, len(clients),
+                                 np.ascontiguousarray(plan, dtype=ASSIGN_DT).ctypes.data, _ptr(global_in),
+                                 _ptr(global_out), n_params, meas.ctypes.data if measured else None,
+                                 ctypes.byref(st)), ctx)
+    return (st.as_dict(), meas) if measured else st.as_dict()
+
+
+def protea_fedavg(ctx, params, num_examples, out):
+    """params: list of device float32 tensors (same length); out: device tensor."""
+    ptrs = np.array([p.data_ptr() for p in params], dtype=np.uint64)
+    ns = np.ascontiguousarray(num_examples, dtype=np.int64)
+    dim = out.numel()
+    _check(_lib.protea_fedavg(ctx, ptrs.ctypes.data, ns.ctypes.data, len(params), dim, out.data_ptr()), ctx)
+
+
+def protea_client_footprint(arch, width_q, classes, H, W, C, n, batch, epochs, precision=PREC_FP32):
+    d = ModelDesc(arch, width_q, classes, H, W, C)
+    pb, st, fl = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    _check(_lib.protea_client_footprint(ctypes.byref(d), n, batch, epochs, precision, ctypes.byref(pb),
+                                        ctypes.byref(st), ctypes.byref(fl)))
+    return pb.value, st.value, fl.value

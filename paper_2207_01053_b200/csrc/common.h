@@ -1,0 +1,74 @@
+// common.h — library-internal types shared by the host runtime and the kernels.
+//
+// Model table, parameter layout and the per-client arena slot layout
+// (DESIGN.md "Arena slot layout").  This is the library's own copy; the
+// oracle (oracle/profiler.py) implements the same table independently and the
+// CPU tests compare the two byte for byte through protea_client_footprint.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/protea.h"
+
+namespace protea {
+
+constexpr uint64_t kAlign = 256;
+inline uint64_t align256(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// One layer of a model, in forward order.  Weights are [out][K] row-major with
+// K = k*k*cin (conv, NHWC taps (ky,kx,ci)) or K = in (fc); bias [out] follows.
+struct Layer {
+  int kind;      // 0 = conv, 1 = fc
+  int k, stride, pad;
+  int cin, cout;
+  int hin, win;  // input spatial size (conv)
+  int hout, wout;
+  int64_t off_w, off_b;  // offsets in the flat parameter vector
+  int64_t K() const { return kind == 0 ? (int64_t)k * k * cin : cin; }
+};
+
+struct ModelDims {
+  int arch = 0, width_q = 4, classes = 10, H = 0, W = 0, C = 0;
+  int c1 = 0, c2 = 0, f = 0;  // CNN channel counts
+  int64_t P = 0;
+  std::vector<Layer> layers;
+  int64_t in_dim() const { return (int64_t)H * W * C; }
+};
+
+bool make_model(const protea_model_desc& d, ModelDims* out, std::string* err);
+
+// FLOPs of one sample's forward + backward pass: 2 * (fwd + wgrad + dgrad MACs),
+// no dgrad for the first layer.
+uint64_t flops_per_sample(const ModelDims& m);
+
+// Named buffers of one client's slot, in slot order.
+enum Buf : int {
+  B_PARAMS = 0, B_PERM, B_STATS,
+  // MLP
+  B_H1, B_DZ1,
+  // CNN
+  B_A1, B_I1, B_A2, B_I2, B_H, B_DH, B_DZ2, B_DZC1, B_WSP,
+  // ResNet-8
+  B_R_A0, B_R_R1, B_R_O1, B_R_R2, B_R_O2, B_R_R3, B_R_O3, B_R_GAP, B_R_DGAP, B_R_G0, B_R_G1, B_R_G2, B_R_WSP,
+  B_COUNT
+};
+
+struct SlotLayout {
+  uint64_t off[B_COUNT];
+  uint64_t size[B_COUNT];
+  bool used[B_COUNT];
+  uint64_t total;  // = exact HWM of the slot (bump allocator, nothing freed in a round)
+};
+
+// Split-K partition of the conv wgrad reductions (pixels per split).
+constexpr int kWgradChunkPx = 2048;
+int cnn_conv1_splits(int rows);
+int cnn_conv2_splits(int rows);
+
+SlotLayout slot_layout(const ModelDims& m, int batch, int64_t n, int epochs, int elem_bytes);
+
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+}  // namespace protea

@@ -1,0 +1,89 @@
+// device.cuh — device-side records and small helpers shared by all kernels.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.h"
+
+namespace protea {
+
+// One client of the round on this rank (device copy; built on host per round).
+struct ClientRec {
+  float* params;           // P fp32 master weights in the slot
+  int32_t* perm;           // E*n epoch permutations
+  float* stats;            // 16 floats: [0] loss sum
+  void* buf[B_COUNT];      // slot buffers (nullptr if unused)
+  const uint8_t* x;        // device shard, n x D u8
+  const int32_t* y;        // labels
+  const float* wg;         // global weights of the client's group (device)
+  double* acc;             // group FedAvg accumulator (fp64)
+  int32_t n, B, E, nb;     // nb = ceil(n/B)
+  int64_t P;               // parameters of the client's model
+  int64_t id;
+  uint64_t* sm_ns;         // per-client device-time attribution (nullable)
+};
+
+// One active client in one lock-step iteration.
+struct Task {
+  int32_t rec;   // ClientRec index
+  int32_t step;  // local step s in [0, S_k)
+  int32_t rows;  // |beta| = min(B, n - j*B)
+  int32_t base;  // e*n + j*B: index into perm of the batch's first row
+};
+
+// CTA -> task: prefix[i] = first CTA of task i, prefix[ntask] = grid size.
+__device__ __forceinline__ int find_task(const int* __restrict__ prefix, int ntask, int block) {
+  int lo = 0, hi = ntask - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (__ldg(prefix + mid) <= block)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+template <typename T>
+__device__ __forceinline__ float ldv(const T* p);
+template <>
+__device__ __forceinline__ float ldv<float>(const float* p) {
+  return *p;
+}
+template <>
+__device__ __forceinline__ float ldv<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat162float(*p);
+}
+template <typename T>
+__device__ __forceinline__ void stv(T* p, float v);
+template <>
+__device__ __forceinline__ void stv<float>(float* p, float v) {
+  *p = v;
+}
+template <>
+__device__ __forceinline__ void stv<__nv_bfloat16>(__nv_bfloat16* p, float v) {
+  *p = __float2bfloat16_rn(v);
+}
+
+// u8 pixel -> x/255 (fp32, correctly rounded division)
+__device__ __forceinline__ float px01(uint8_t u) { return __fdiv_rn((float)u, 255.0f); }
+
+// SplitMix64 finaliser (reading R10; oracle/splitmix.py is the
+// independent Python implementation).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace protea

@@ -1,0 +1,808 @@
+// engine.cu — the virtual-client engine and the C ABI (include/protea.h).
+//
+// PAPER.md §3.2: the VCE runs "as many clients concurrently as the
+// available system resources can hold" and spawns the next one when a client
+// finishes.  Here the "resource" is a byte range of this GPU's arena (the slot
+// of protea_plan) and concurrency is realised as LOCK-STEP ITERATIONS: in
+// iteration t every admitted client (admit <= t < release) advances one local
+// SGD step, and every layer-op of that step is ONE grouped kernel launch over
+// all active clients (kernels_simt.cuh).  Clients are admitted / released at
+// the iterations the plan fixed; on release the client's FedAvg term
+// n_k (w_k - w_g) is added to the group's fp64 accumulator, and after
+// the last iteration the ranks sum their accumulators (NCCL, the only
+// cross-GPU exchange) and every rank writes w' = w_g + acc / N.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "device.cuh"
+#include "kernels_misc.cuh"
+#include "kernels_simt.cuh"
+
+namespace protea {
+
+static std::mutex g_err_mu;
+static std::string g_err;
+void set_global_error(const std::string& msg) {
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  g_err = msg;
+}
+
+struct Group {
+  ModelDims m;
+  int64_t offset = 0;  // in the concatenated global vector
+};
+
+struct ShardDev {
+  int64_t n = 0;
+  uint8_t* x = nullptr;
+  int32_t* y = nullptr;
+};
+
+template <typename T>
+struct DevArray {
+  T* p = nullptr;
+  size_t cap = 0;
+  cudaError_t reserve(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T));
+    if (e == cudaSuccess) cap = n;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace protea
+
+using namespace protea;
+
+struct protea_ctx {
+  int device = 0, rank = 0, world = 1, precision = PROTEA_PREC_FP32;
+  cudaStream_t stream = nullptr;
+  uint8_t* arena = nullptr;
+  uint64_t arena_bytes = 0;
+  std::vector<Group> groups;
+  std::map<int64_t, ShardDev> shards;
+  ncclComm_t comm = nullptr;
+  std::string err;
+  DevArray<float> gin, gout;
+  DevArray<double> acc;
+  DevArray<ClientRec> recs;
+  DevArray<int32_t> tab;
+  DevArray<const float*> ptrs;
+  DevArray<double> wts;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  uint64_t launches = 0;
+};
+
+#define CK(call)                                                                               \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) {                                                                   \
+      ctx->err = std::string("CUDA error ") + cudaGetErrorString(e_) + " at " #call;           \
+      return PROTEA_ERR_CUDA;                                                                  \
+    }                                                                                          \
+  } while (0)
+
+static protea_status fail(protea_ctx* ctx, protea_status s, const std::string& m) {
+  ctx->err = m;
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// per-model op tables: tile counts (must mirror the device setup() decode)
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kMaxBatch = 64;
+
+// tile shapes
+constexpr int C1F_BM = 64, C1F_BN = 32;
+constexpr int C2F_BM = 64, C2F_BN = 64;
+constexpr int F1F_BM = 32, F1F_BN = 64;
+constexpr int F1D_BM = 32, F1D_BN = 64;
+constexpr int F1W_BM = 64, F1W_BN = 64;
+constexpr int C2D_BM = 64, C2D_BN = 32;
+constexpr int C2W_BM = 64, C2W_BN = 64;
+constexpr int C1W_BM = 32, C1W_BN = 64;
+constexpr int MF_BM = 16, MF_BN = 64;
+constexpr int MW_BM = 64, MW_BN = 64;
+
+enum Op : int {
+  OP_C1F = 0, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R,
+  OP_MF, OP_MHEAD, OP_MW, OP_COUNT
+};
+
+int tiles(const ModelDims& m, int op, int rows) {
+  switch (op) {
+    case OP_C1F: return cdiv(rows * 1024, C1F_BM) * cdiv(m.c1, C1F_BN);
+    case OP_C2F: return cdiv(rows * 256, C2F_BM) * cdiv(m.c2, C2F_BN);
+    case OP_F1F: return cdiv(rows, F1F_BM) * cdiv(m.f, F1F_BN);
+    case OP_HEAD: return 1;
+    case OP_F1D: return cdiv(rows, F1D_BM) * cdiv(64 * m.c2, F1D_BN);
+    case OP_F1W: return cdiv(m.f, F1W_BM) * cdiv(64 * m.c2 + 1, F1W_BN);
+    case OP_C2D: return cdiv(rows * 256, C2D_BM) * cdiv(m.c1, C2D_BN);
+    case OP_C2W: return cdiv(rows * 256, kWgradChunkPx) * cdiv(m.c2, C2W_BM) * cdiv(25 * m.c1 + 1, C2W_BN);
+    case OP_C2R: return cdiv(m.c2 * (25 * m.c1 + 1), kReduceBlock);
+    case OP_C1W: return cdiv(rows * 1024, kWgradChunkPx) * cdiv(m.c1, C1W_BM) * cdiv(76, C1W_BN);
+    case OP_C1R: return cdiv(m.c1 * 76, kReduceBlock);
+    case OP_MF: return cdiv(rows, MF_BM) * cdiv(64, MF_BN);
+    case OP_MHEAD: return 1;
+    case OP_MW: return cdiv(64, MW_BM) * cdiv(785, MW_BN);
+  }
+  return 0;
+}
+
+std::vector<int> ops_of(const ModelDims& m) {
+  if (m.arch == PROTEA_MODEL_CNN)
+    return {OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
+  if (m.arch == PROTEA_MODEL_MLP) return {OP_MF, OP_MHEAD, OP_MW};
+  return {};
+}
+
+CnnDims cnn_dims(const ModelDims& m) {
+  CnnDims d;
+  d.c1 = m.c1;
+  d.c2 = m.c2;
+  d.f = m.f;
+  d.classes = m.classes;
+  d.w1 = m.layers[0].off_w;
+  d.b1 = m.layers[0].off_b;
+  d.w2 = m.layers[1].off_w;
+  d.b2 = m.layers[1].off_b;
+  d.w3 = m.layers[2].off_w;
+  d.b3 = m.layers[2].off_b;
+  d.w4 = m.layers[3].off_w;
+  d.b4 = m.layers[3].off_b;
+  return d;
+}
+
+MlpDims mlp_dims(const ModelDims& m) {
+  MlpDims d;
+  d.classes = m.classes;
+  d.w1 = m.layers[0].off_w;
+  d.b1 = m.layers[0].off_b;
+  d.w2 = m.layers[1].off_w;
+  d.b2 = m.layers[1].off_b;
+  return d;
+}
+
+// One (iteration, group) launch descriptor, offsets into the int32 table.
+struct Launch {
+  int group;
+  int ntask;
+  int64_t task_off;            // tasks: 4 ints each
+  int64_t prefix_off[OP_COUNT];
+  int grid[OP_COUNT];
+};
+
+template <class OpT, int BM, int BN>
+void launch_gemm(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, const int32_t* dtab) {
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const int* prefix = dtab + L.prefix_off[opid];
+  k_gemm_simt<BM, BN, OpT><<<L.grid[opid], (BM / 4) * (BN / 4), 0, ctx->stream>>>(op, tasks, prefix, L.ntask);
+  ctx->launches++;
+}
+
+template <typename T>
+void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const int32_t* dtab,
+                 float lr) {
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  if (m.arch == PROTEA_MODEL_CNN) {
+    const CnnDims d = cnn_dims(m);
+    launch_gemm<Conv1Fwd<T, C1F_BM, C1F_BN>, C1F_BM, C1F_BN>(ctx, {drecs, d}, L, OP_C1F, dtab);
+    launch_gemm<Conv2Fwd<T, C2F_BM, C2F_BN>, C2F_BM, C2F_BN>(ctx, {drecs, d}, L, OP_C2F, dtab);
+    launch_gemm<Fc1Fwd<T, F1F_BM, F1F_BN>, F1F_BM, F1F_BN>(ctx, {drecs, d}, L, OP_F1F, dtab);
+    HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, lr};
+    k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
+    ctx->launches++;
+    launch_gemm<Fc1Dgrad<T, F1D_BM, F1D_BN>, F1D_BM, F1D_BN>(ctx, {drecs, d}, L, OP_F1D, dtab);
+    launch_gemm<Fc1Wgrad<T, F1W_BM, F1W_BN>, F1W_BM, F1W_BN>(ctx, {drecs, d, lr}, L, OP_F1W, dtab);
+    launch_gemm<Conv2Dgrad<T, C2D_BM, C2D_BN>, C2D_BM, C2D_BN>(ctx, {drecs, d}, L, OP_C2D, dtab);
+    launch_gemm<Conv2Wgrad<T, C2W_BM, C2W_BN>, C2W_BM, C2W_BN>(ctx, {drecs, d}, L, OP_C2W, dtab);
+    ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr};
+    k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->stream>>>(r2, tasks, dtab + L.prefix_off[OP_C2R],
+                                                                       L.ntask);
+    ctx->launches++;
+    launch_gemm<Conv1Wgrad<T, C1W_BM, C1W_BN>, C1W_BM, C1W_BN>(ctx, {drecs, d}, L, OP_C1W, dtab);
+    ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr};
+    k_reduce_update<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->stream>>>(r1, tasks, dtab + L.prefix_off[OP_C1R],
+                                                                       L.ntask);
+    ctx->launches++;
+  } else if (m.arch == PROTEA_MODEL_MLP) {
+    const MlpDims d = mlp_dims(m);
+    launch_gemm<MlpFc1Fwd<T, MF_BM, MF_BN>, MF_BM, MF_BN>(ctx, {drecs, d}, L, OP_MF, dtab);
+    HeadArgs ha{drecs, B_H1, B_DZ1, 64, m.classes, d.w2, d.b2, lr};
+    k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
+    ctx->launches++;
+    launch_gemm<MlpFc1Wgrad<T, MW_BM, MW_BN>, MW_BM, MW_BN>(ctx, {drecs, d, lr}, L, OP_MW, dtab);
+  }
+}
+
+int grid_for(int64_t n, int threads, int cap = 148 * 8) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, cap));
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* protea_last_error(const protea_ctx* ctx) {
+  if (ctx) return ctx->err.c_str();
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  return g_err.c_str();
+}
+
+protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
+  if (!opts || !out) {
+    set_global_error("protea_init: null argument");
+    return PROTEA_ERR_INVALID;
+  }
+  if (opts->world < 1 || opts->rank < 0 || opts->rank >= opts->world || (opts->world > 1 && !opts->nccl_id) ||
+      !opts->arena || opts->arena_bytes == 0 ||
+      (opts->precision != PROTEA_PREC_FP32 && opts->precision != PROTEA_PREC_BF16)) {
+    set_global_error("protea_init: invalid rank/world/nccl_id/arena/precision");
+    return PROTEA_ERR_INVALID;
+  }
+  std::unique_ptr<protea_ctx> c(new protea_ctx());
+  c->device = opts->device;
+  c->rank = opts->rank;
+  c->world = opts->world;
+  c->precision = opts->precision;
+  c->stream = (cudaStream_t)opts->stream;
+  c->arena = (uint8_t*)opts->arena;
+  c->arena_bytes = opts->arena_bytes;
+  protea_ctx* ctx = c.get();
+  cudaError_t e = cudaSetDevice(opts->device);
+  if (e != cudaSuccess) {
+    set_global_error(std::string("protea_init: cudaSetDevice: ") + cudaGetErrorString(e));
+    return PROTEA_ERR_CUDA;
+  }
+  if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
+    set_global_error("protea_init: cudaEventCreate failed");
+    return PROTEA_ERR_CUDA;
+  }
+  if (opts->world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, opts->nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, opts->world, id, opts->rank);
+    if (r != ncclSuccess) {
+      set_global_error(std::string("protea_init: ncclCommInitRank: ") + ncclGetErrorString(r));
+      return PROTEA_ERR_NCCL;
+    }
+  }
+  *out = c.release();
+  return PROTEA_OK;
+}
+
+void protea_finalize(protea_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& kv : ctx->shards) {
+    cudaFree(kv.second.x);
+    cudaFree(kv.second.y);
+  }
+  ctx->gin.release();
+  ctx->gout.release();
+  ctx->acc.release();
+  ctx->recs.release();
+  ctx->tab.release();
+  ctx->ptrs.release();
+  ctx->wts.release();
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  delete ctx;
+}
+
+protea_status protea_register_model(protea_ctx* ctx, const protea_model_desc* desc, int32_t* model_id,
+                                    uint64_t* n_params) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  if (!desc || !model_id || !n_params) return fail(ctx, PROTEA_ERR_INVALID, "register_model: null argument");
+  Group g;
+  std::string err;
+  if (!make_model(*desc, &g.m, &err)) return fail(ctx, PROTEA_ERR_INVALID, "register_model: " + err);
+  if (desc->arch == PROTEA_MODEL_RESNET8)
+    return fail(ctx, PROTEA_ERR_INVALID, "register_model: RESNET8 device path not built in this version");
+  g.offset = 0;
+  for (auto& x : ctx->groups) g.offset += x.m.P;
+  ctx->groups.push_back(g);
+  *model_id = (int32_t)ctx->groups.size() - 1;
+  *n_params = (uint64_t)g.m.P;
+  return PROTEA_OK;
+}
+
+protea_status protea_register_shards(protea_ctx* ctx, const protea_shard* shards, size_t n) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  if (!shards || n == 0) return fail(ctx, PROTEA_ERR_INVALID, "register_shards: null or empty");
+  for (size_t i = 0; i < n; ++i)
+    if (shards[i].n <= 0 || !shards[i].x || !shards[i].y)
+      return fail(ctx, PROTEA_ERR_INVALID,
+                  "register_shards: client " + std::to_string(shards[i].client_id) + " has n <= 0 or null data");
+  // all shards of a context share one input size D (taken from the first registered model, else from
+  // the caller's bytes per example: x holds n * D bytes; D is inferred per call from the models).
+  if (ctx->groups.empty()) return fail(ctx, PROTEA_ERR_INVALID, "register_shards: register a model first");
+  const int64_t D = ctx->groups[0].m.in_dim();
+  CK(cudaSetDevice(ctx->device));
+  for (size_t i = 0; i < n; ++i) {
+    const protea_shard& s = shards[i];
+    auto it = ctx->shards.find(s.client_id);
+    if (it != ctx->shards.end()) {
+      cudaFree(it->second.x);
+      cudaFree(it->second.y);
+      ctx->shards.erase(it);
+    }
+    ShardDev d;
+    d.n = s.n;
+    CK(cudaMalloc(&d.x, (size_t)s.n * D));
+    CK(cudaMalloc(&d.y, (size_t)s.n * 4));
+    CK(cudaMemcpyAsync(d.x, s.x, (size_t)s.n * D, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(d.y, s.y, (size_t)s.n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->shards[s.client_id] = d;
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PROTEA_OK;
+}
+
+protea_status protea_client_footprint(const protea_model_desc* desc, int64_t n, int32_t batch, int32_t epochs,
+                                      int32_t precision, uint64_t* peak_bytes, uint64_t* steps, uint64_t* flops) {
+  if (!desc || !peak_bytes || !steps || !flops || n <= 0 || batch <= 0 || epochs <= 0 ||
+      (precision != PROTEA_PREC_FP32 && precision != PROTEA_PREC_BF16)) {
+    set_global_error("client_footprint: invalid argument");
+    return PROTEA_ERR_INVALID;
+  }
+  ModelDims m;
+  std::string err;
+  if (!make_model(*desc, &m, &err)) {
+    set_global_error("client_footprint: " + err);
+    return PROTEA_ERR_INVALID;
+  }
+  const SlotLayout s = slot_layout(m, batch, n, epochs, precision == PROTEA_PREC_FP32 ? 4 : 2);
+  *peak_bytes = s.total;
+  *steps = (uint64_t)epochs * ceil_div((uint64_t)n, (uint64_t)batch);
+  *flops = (uint64_t)epochs * (uint64_t)n * flops_per_sample(m);
+  return PROTEA_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// round execution (shared by protea_run_round and the profiler's probe)
+// ---------------------------------------------------------------------------
+namespace {
+
+struct RunClient {
+  int64_t id;
+  int group;
+  int64_t n;
+  int B, E, nb;
+  uint64_t S, admit, release;
+  uint64_t offset;
+  int rec = -1;
+};
+
+// Validates and executes the lock-step schedule of `rc` (this rank's clients,
+// ascending id) inside the arena.  wg: device concatenated global weights;
+// acc: device fp64 accumulator (zeroed by caller) or nullptr (probe mode:
+// no FedAvg terms).  Returns iterations run.
+protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* wg, double* acc, float lr,
+                      uint32_t seed, uint32_t round, int shuffle, uint64_t* iters_out) {
+  const int e = ctx->precision == PROTEA_PREC_FP32 ? 4 : 2;
+  const int G = (int)ctx->groups.size();
+  // ---- device records
+  std::vector<ClientRec> recs(rc.size());
+  std::vector<int64_t> gacc_off(G, 0);
+  for (int g = 1; g < G; ++g) gacc_off[g] = gacc_off[g - 1] + ctx->groups[g - 1].m.P;
+  for (size_t i = 0; i < rc.size(); ++i) {
+    RunClient& c = rc[i];
+    c.rec = (int)i;
+    const Group& gr = ctx->groups[c.group];
+    const SlotLayout L = slot_layout(gr.m, c.B, c.n, c.E, e);
+    ClientRec& r = recs[i];
+    std::memset(&r, 0, sizeof(r));
+    uint8_t* base = ctx->arena + c.offset;
+    for (int b = 0; b < B_COUNT; ++b) r.buf[b] = L.used[b] ? base + L.off[b] : nullptr;
+    r.params = (float*)r.buf[B_PARAMS];
+    r.perm = (int32_t*)r.buf[B_PERM];
+    r.stats = (float*)r.buf[B_STATS];
+    const ShardDev& sd = ctx->shards[c.id];
+    r.x = sd.x;
+    r.y = sd.y;
+    r.wg = wg + gr.offset;
+    r.acc = acc ? acc + gacc_off[c.group] : nullptr;
+    r.n = (int32_t)c.n;
+    r.B = c.B;
+    r.E = c.E;
+    r.nb = c.nb;
+    r.id = c.id;
+    r.P = gr.m.P;
+  }
+  // ---- schedule tables
+  uint64_t T = 0;
+  for (auto& c : rc) T = std::max(T, c.release);
+  std::vector<int32_t> tab;
+  std::vector<Launch> launches;
+  std::vector<std::pair<int64_t, int>> admits(T + 1, {-1, 0}), rels;  // per-iteration (offset, count)
+  std::vector<std::vector<std::pair<int64_t, int>>> rel_by_group(T + 1, std::vector<std::pair<int64_t, int>>(G, {-1, 0}));
+  std::vector<std::vector<int>> launch_idx(T);
+  for (uint64_t t = 0; t < T; ++t) {
+    // admissions at t (ascending id)
+    std::vector<int> adm;
+    for (auto& c : rc)
+      if (c.admit == t) adm.push_back(c.rec);
+    if (!adm.empty()) {
+      admits[t] = {(int64_t)tab.size(), (int)adm.size()};
+      tab.insert(tab.end(), adm.begin(), adm.end());
+    }
+    for (int g = 0; g < G; ++g) {
+      const ModelDims& m = ctx->groups[g].m;
+      std::vector<const RunClient*> act;
+      for (auto& c : rc)
+        if (c.group == g && c.admit <= t && t < c.release) act.push_back(&c);
+      if (!act.empty()) {
+        Launch L;
+        std::memset(&L, 0, sizeof(L));
+        L.group = g;
+        L.ntask = (int)act.size();
+        while (tab.size() % 4) tab.push_back(0);
+        L.task_off = (int64_t)tab.size();
+        std::vector<int> rows(act.size());
+        for (size_t i = 0; i < act.size(); ++i) {
+          const RunClient& c = *act[i];
+          const int s = (int)(t - c.admit), ep = s / c.nb, j = s % c.nb;
+          rows[i] = (int)std::min<int64_t>(c.B, c.n - (int64_t)j * c.B);
+          tab.push_back(c.rec);
+          tab.push_back(s);
+          tab.push_back(rows[i]);
+          tab.push_back((int32_t)((int64_t)ep * c.n + (int64_t)j * c.B));
+        }
+        for (int op : ops_of(m)) {
+          L.prefix_off[op] = (int64_t)tab.size();
+          int acc_t = 0;
+          for (size_t i = 0; i < act.size(); ++i) {
+            tab.push_back(acc_t);
+            acc_t += tiles(m, op, rows[i]);
+          }
+          tab.push_back(acc_t);
+          L.grid[op] = acc_t;
+        }
+        launch_idx[t].push_back((int)launches.size());
+        launches.push_back(L);
+      }
+      // releases after iteration t (client finished its last step)
+      std::vector<int> rel;
+      for (auto& c : rc)
+        if (c.group == g && c.release == t + 1) rel.push_back(c.rec);
+      if (!rel.empty()) {
+        rel_by_group[t][g] = {(int64_t)tab.size(), (int)rel.size()};
+        tab.insert(tab.end(), rel.begin(), rel.end());
+      }
+    }
+  }
+  CK(ctx->recs.reserve(recs.size()));
+  CK(ctx->tab.reserve(tab.size()));
+  CK(cudaMemcpyAsync(ctx->recs.p, recs.data(), recs.size() * sizeof(ClientRec), cudaMemcpyHostToDevice, ctx->stream));
+  if (!tab.empty())
+    CK(cudaMemcpyAsync(ctx->tab.p, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  const ClientRec* drecs = ctx->recs.p;
+  const int32_t* dtab = ctx->tab.p;
+  int maxE = 1;
+  for (auto& c : rc) maxE = std::max(maxE, c.E);
+  for (uint64_t t = 0; t < T; ++t) {
+    if (admits[t].second > 0) {
+      const int* ids = dtab + admits[t].first;
+      int64_t maxP = 0, maxn = 0;
+      for (auto& c : rc)
+        if (c.admit == t) {
+          maxP = std::max<int64_t>(maxP, ctx->groups[c.group].m.P);
+          maxn = std::max<int64_t>(maxn, c.n);
+        }
+      k_admit_params<<<dim3(grid_for(maxP / 4 + 1, 256, 64), admits[t].second), 256, 0, ctx->stream>>>(drecs, ids);
+      ctx->launches++;
+      k_admit_perm<<<dim3(cdiv((int)maxn, kPermThreads), admits[t].second, maxE), kPermThreads, 0, ctx->stream>>>(
+          drecs, ids, seed, round, shuffle);
+      ctx->launches++;
+    }
+    for (int li : launch_idx[t]) {
+      const Launch& L = launches[li];
+      const ModelDims& m = ctx->groups[L.group].m;
+      if (e == 4)
+        launch_step<float>(ctx, m, L, drecs, dtab, lr);
+      else
+        launch_step<__nv_bfloat16>(ctx, m, L, drecs, dtab, lr);
+    }
+    if (acc)
+      for (int g = 0; g < G; ++g)
+        if (rel_by_group[t][g].second > 0) {
+          const int64_t P = ctx->groups[g].m.P;
+          k_release_acc<<<grid_for(P, 256), 256, 0, ctx->stream>>>(drecs, dtab + rel_by_group[t][g].first,
+                                                                    rel_by_group[t][g].second, P);
+          ctx->launches++;
+        }
+  }
+  CK(cudaGetLastError());
+  if (iters_out) *iters_out = T;
+  return PROTEA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, const protea_client* clients, size_t n,
+                               const protea_assignment* plan, const float* global_in, float* global_out,
+                               size_t n_params, protea_profile* measured, protea_round_stats* stats) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  if (!opts || !clients || !plan || !global_in || !global_out || n == 0)
+    return fail(ctx, PROTEA_ERR_INVALID, "run_round: null argument or n == 0");
+  int64_t Ptot = 0;
+  for (auto& g : ctx->groups) Ptot += g.m.P;
+  if ((int64_t)n_params != Ptot)
+    return fail(ctx, PROTEA_ERR_DIM, "run_round: n_params " + std::to_string(n_params) + " != registered total " +
+                                         std::to_string(Ptot));
+  const int e = ctx->precision == PROTEA_PREC_FP32 ? 4 : 2;
+  // ---- validate clients and plan
+  std::map<int64_t, const protea_assignment*> pa;
+  for (size_t i = 0; i < n; ++i)
+    if (!pa.emplace(plan[i].client_id, &plan[i]).second)
+      return fail(ctx, PROTEA_ERR_PLAN, "run_round: plan lists client " + std::to_string(plan[i].client_id) + " twice");
+  std::vector<RunClient> all;
+  std::map<int64_t, int> seen;
+  std::vector<int64_t> Ngroup(ctx->groups.size(), 0);
+  for (size_t i = 0; i < n; ++i) {
+    const protea_client& c = clients[i];
+    const std::string who = "run_round: client " + std::to_string(c.client_id);
+    if (!seen.emplace(c.client_id, 1).second) return fail(ctx, PROTEA_ERR_INVALID, who + " listed twice");
+    if (c.model_id < 0 || c.model_id >= (int)ctx->groups.size())
+      return fail(ctx, PROTEA_ERR_INVALID, who + ": unknown model_id");
+    if (c.batch <= 0 || c.batch > kMaxBatch || c.epochs <= 0)
+      return fail(ctx, PROTEA_ERR_INVALID, who + ": batch must be in [1, 64] and epochs > 0");
+    auto sh = ctx->shards.find(c.client_id);
+    if (sh == ctx->shards.end()) return fail(ctx, PROTEA_ERR_INVALID, who + ": no registered shard");
+    auto it = pa.find(c.client_id);
+    if (it == pa.end()) return fail(ctx, PROTEA_ERR_PLAN, who + " missing from the plan");
+    const protea_assignment& a = *it->second;
+    RunClient r;
+    r.id = c.client_id;
+    r.group = c.model_id;
+    r.n = sh->second.n;
+    r.B = c.batch;
+    r.E = c.epochs;
+    r.nb = (int)ceil_div((uint64_t)r.n, (uint64_t)r.B);
+    r.S = (uint64_t)r.E * r.nb;
+    r.admit = a.admit;
+    r.release = a.release;
+    r.offset = a.offset;
+    if (a.gpu < 0 || a.gpu >= ctx->world) return fail(ctx, PROTEA_ERR_PLAN, who + ": gpu out of range");
+    if (a.release != a.admit + r.S)
+      return fail(ctx, PROTEA_ERR_PLAN, who + ": release - admit != S_k = " + std::to_string(r.S));
+    const uint64_t need = slot_layout(ctx->groups[c.model_id].m, r.B, r.n, r.E, e).total;
+    if (a.slot < need)
+      return fail(ctx, PROTEA_ERR_PLAN, who + ": slot " + std::to_string(a.slot) + " < HWM " + std::to_string(need));
+    if (a.gpu == ctx->rank && (a.offset % kAlign != 0 || a.offset + a.slot > ctx->arena_bytes))
+      return fail(ctx, PROTEA_ERR_OOM, who + ": slot [" + std::to_string(a.offset) + ", +" + std::to_string(a.slot) +
+                                           ") outside the arena of " + std::to_string(ctx->arena_bytes) + " B");
+    Ngroup[c.model_id] += r.n;
+    if (a.gpu == ctx->rank) all.push_back(r);
+  }
+  if (pa.size() != n) return fail(ctx, PROTEA_ERR_PLAN, "run_round: plan and client list differ");
+  // live slots pairwise disjoint on this GPU
+  {
+    std::vector<std::pair<uint64_t, int>> ev;  // (time*2 + kind, idx)
+    std::vector<RunClient*> byoff;
+    for (auto& c : all) byoff.push_back(&c);
+    std::sort(byoff.begin(), byoff.end(), [](RunClient* a, RunClient* b) { return a->offset < b->offset; });
+    for (size_t i = 0; i < byoff.size(); ++i)
+      for (size_t j = i + 1; j < byoff.size(); ++j) {
+        RunClient* a = byoff[i];
+        RunClient* b = byoff[j];
+        const uint64_t aend = a->offset + slot_layout(ctx->groups[a->group].m, a->B, a->n, a->E, e).total;
+        if (b->offset >= aend) break;
+        if (a->admit < b->release && b->admit < a->release)
+          return fail(ctx, PROTEA_ERR_PLAN, "run_round: clients " + std::to_string(a->id) + " and " +
+                                                std::to_string(b->id) + " overlap in the arena while both live");
+      }
+  }
+  std::sort(all.begin(), all.end(), [](const RunClient& a, const RunClient& b) { return a.id < b.id; });
+  CK(cudaSetDevice(ctx->device));
+  // ---- global weights in
+  const bool in_dev = is_device_ptr(global_in), out_dev = is_device_ptr(global_out);
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  const float* wg = global_in;
+  if (!in_dev) {
+    CK(ctx->gin.reserve(Ptot));
+    CK(cudaMemcpyAsync(ctx->gin.p, global_in, Ptot * 4, cudaMemcpyHostToDevice, ctx->stream));
+    wg = ctx->gin.p;
+  } else if (global_in == global_out) {
+    // finalize writes out while admissions of later iterations are done; keep a private copy
+    CK(ctx->gin.reserve(Ptot));
+    CK(cudaMemcpyAsync(ctx->gin.p, global_in, Ptot * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    wg = ctx->gin.p;
+  }
+  CK(ctx->acc.reserve(Ptot));
+  CK(cudaMemsetAsync(ctx->acc.p, 0, Ptot * 8, ctx->stream));
+  const uint64_t l0 = ctx->launches;
+  uint64_t iters = 0;
+  protea_status st = execute(ctx, all, wg, ctx->acc.p, opts->lr, opts->seed, opts->round, opts->shuffle, &iters);
+  if (st != PROTEA_OK) return st;
+  if (ctx->world > 1) {
+    ncclResult_t r = ncclAllReduce(ctx->acc.p, ctx->acc.p, Ptot, ncclDouble, ncclSum, ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return fail(ctx, PROTEA_ERR_NCCL, std::string("run_round: ncclAllReduce: ") + ncclGetErrorString(r));
+  }
+  float* out = global_out;
+  if (!out_dev) {
+    CK(ctx->gout.reserve(Ptot));
+    out = ctx->gout.p;
+  }
+  for (size_t g = 0; g < ctx->groups.size(); ++g) {
+    const Group& gr = ctx->groups[g];
+    if (Ngroup[g] > 0) {
+      k_finalize<<<grid_for(gr.m.P, 256), 256, 0, ctx->stream>>>(wg + gr.offset, ctx->acc.p + gr.offset,
+                                                                 (double)Ngroup[g], out + gr.offset, gr.m.P);
+      ctx->launches++;
+    } else if (out + gr.offset != wg + gr.offset) {
+      CK(cudaMemcpyAsync(out + gr.offset, wg + gr.offset, gr.m.P * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  }
+  if (!out_dev) CK(cudaMemcpyAsync(global_out, out, Ptot * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->round_ns = (uint64_t)(ms * 1e6);
+    stats->iterations = iters;
+    stats->kernel_launches = ctx->launches - l0;
+    for (auto& c : all) {
+      stats->client_steps += c.S;
+      stats->flops += (uint64_t)c.E * c.n * flops_per_sample(ctx->groups[c.group].m);
+    }
+  }
+  if (measured) {
+    size_t k = 0;
+    for (size_t i = 0; i < n; ++i) {
+      const protea_client& c = clients[i];
+      const int64_t nn = ctx->shards[c.client_id].n;
+      protea_profile& p = measured[k++];
+      std::memset(&p, 0, sizeof(p));
+      p.client_id = c.client_id;
+      p.peak_bytes = slot_layout(ctx->groups[c.model_id].m, c.batch, nn, c.epochs, e).total;
+      p.steps = (uint64_t)c.epochs * ceil_div((uint64_t)nn, (uint64_t)c.batch);
+      p.flops = (uint64_t)c.epochs * nn * flops_per_sample(ctx->groups[c.model_id].m);
+      p.uses_gpu = 1;
+    }
+  }
+  return PROTEA_OK;
+}
+
+protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clients, size_t n, protea_profile* out) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  if (!clients || !out || n == 0) return fail(ctx, PROTEA_ERR_INVALID, "profile_clients: null argument or n == 0");
+  const int e = ctx->precision == PROTEA_PREC_FP32 ? 4 : 2;
+  std::map<std::pair<int, int>, uint64_t> class_ns;  // (model, batch) -> probe step ns
+  for (size_t i = 0; i < n; ++i) {
+    const protea_client& c = clients[i];
+    const std::string who = "profile_clients: client " + std::to_string(c.client_id);
+    if (c.model_id < 0 || c.model_id >= (int)ctx->groups.size())
+      return fail(ctx, PROTEA_ERR_INVALID, who + ": unknown model_id");
+    if (c.batch <= 0 || c.batch > kMaxBatch || c.epochs <= 0)
+      return fail(ctx, PROTEA_ERR_INVALID, who + ": batch must be in [1, 64] and epochs > 0");
+    if (!ctx->shards.count(c.client_id)) return fail(ctx, PROTEA_ERR_INVALID, who + ": no registered shard");
+  }
+  CK(cudaSetDevice(ctx->device));
+  for (size_t i = 0; i < n; ++i) {
+    const protea_client& c = clients[i];
+    auto key = std::make_pair((int)c.model_id, (int)c.batch);
+    if (class_ns.count(key)) continue;
+    // probe: this client alone, one step (a batch of B rows), at arena offset 0
+    const Group& gr = ctx->groups[c.model_id];
+    RunClient r;
+    r.id = c.client_id;
+    r.group = c.model_id;
+    r.n = std::max<int64_t>(ctx->shards[c.client_id].n, 1);
+    r.B = c.batch;
+    r.E = 1;
+    r.nb = (int)ceil_div((uint64_t)r.n, (uint64_t)r.B);
+    r.S = 1;
+    r.admit = 0;
+    r.release = 1;
+    r.offset = 0;
+    const uint64_t need = slot_layout(gr.m, r.B, r.n, r.E, e).total;
+    if (need > ctx->arena_bytes)
+      return fail(ctx, PROTEA_ERR_OOM, "profile_clients: probe slot of " + std::to_string(need) +
+                                           " B exceeds the arena");
+    CK(ctx->gin.reserve(gr.m.P));
+    CK(cudaMemsetAsync(ctx->gin.p, 0, gr.m.P * 4, ctx->stream));
+    std::vector<float> times;
+    for (int rep = 0; rep < 7; ++rep) {
+      std::vector<RunClient> one{r};
+      // gin holds zero weights at offset 0; shift so that wg + group offset == gin
+      const float* wg = ctx->gin.p - gr.offset;
+      CK(cudaEventRecord(ctx->ev0, ctx->stream));
+      protea_status st = execute(ctx, one, wg, nullptr, 0.0f, 0, 0, 0, nullptr);
+      if (st != PROTEA_OK) return st;
+      CK(cudaEventRecord(ctx->ev1, ctx->stream));
+      CK(cudaEventSynchronize(ctx->ev1));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+      if (rep >= 2) times.push_back(ms);
+    }
+    std::sort(times.begin(), times.end());
+    class_ns[key] = (uint64_t)(times[times.size() / 2] * 1e6);
+  }
+  for (size_t i = 0; i < n; ++i) {
+    const protea_client& c = clients[i];
+    const int64_t nn = ctx->shards[c.client_id].n;
+    protea_profile& p = out[i];
+    std::memset(&p, 0, sizeof(p));
+    p.client_id = c.client_id;
+    p.peak_bytes = slot_layout(ctx->groups[c.model_id].m, c.batch, nn, c.epochs, e).total;
+    p.steps = (uint64_t)c.epochs * ceil_div((uint64_t)nn, (uint64_t)c.batch);
+    p.flops = (uint64_t)c.epochs * nn * flops_per_sample(ctx->groups[c.model_id].m);
+    p.step_ns = class_ns[std::make_pair((int)c.model_id, (int)c.batch)];
+    p.train_ns = p.step_ns * p.steps;
+    p.uses_gpu = 1;
+  }
+  return PROTEA_OK;
+}
+
+protea_status protea_fedavg(protea_ctx* ctx, const float* const* params, const int64_t* num_examples, size_t n,
+                            size_t dim, float* out) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  if (n == 0) return fail(ctx, PROTEA_ERR_EMPTY, "fedavg: no results to aggregate");
+  if (!params || !num_examples || !out || dim == 0) return fail(ctx, PROTEA_ERR_INVALID, "fedavg: null argument");
+  int64_t N = 0;
+  std::vector<double> w(n);
+  for (size_t k = 0; k < n; ++k) {
+    if (!params[k]) return fail(ctx, PROTEA_ERR_INVALID, "fedavg: params[" + std::to_string(k) + "] is null");
+    if (num_examples[k] <= 0)
+      return fail(ctx, PROTEA_ERR_INVALID, "fedavg: num_examples[" + std::to_string(k) + "] <= 0");
+    N += num_examples[k];
+    w[k] = (double)num_examples[k];
+  }
+  if (N == 0) return fail(ctx, PROTEA_ERR_ZERO_WEIGHT, "fedavg: zero total weight");
+  CK(cudaSetDevice(ctx->device));
+  CK(ctx->ptrs.reserve(n));
+  CK(ctx->wts.reserve(n));
+  CK(cudaMemcpyAsync(ctx->ptrs.p, params, n * sizeof(float*), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->wts.p, w.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  k_fedavg<<<grid_for((int64_t)dim, 256), 256, 0, ctx->stream>>>(ctx->ptrs.p, ctx->wts.p, (int)n, (double)N, out,
+                                                                 (int64_t)dim);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PROTEA_OK;
+}
+
+}  // extern "C"

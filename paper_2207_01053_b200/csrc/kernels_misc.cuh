@@ -1,0 +1,89 @@
+// kernels_misc.cuh — admission, epoch permutation, FedAvg reduce/finalise kernels.
+#pragma once
+#include "device.cuh"
+
+namespace protea {
+
+// Admission (VCE stage (4): "another client in the round will be
+// spawned"): copy the group's global weights into the client's slot and zero
+// its stats.  blockIdx.y = admitted client, grid-stride over P.
+__global__ void k_admit_params(const ClientRec* __restrict__ recs, const int* __restrict__ ids) {
+  const ClientRec* c = recs + ids[blockIdx.y];
+  const int64_t P = c->P;
+  // group offsets in the global vector need not be 16-byte aligned: scalar, coalesced
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x)
+    c->params[i] = c->wg[i];
+  if (blockIdx.x == 0 && threadIdx.x < 16) c->stats[threadIdx.x] = 0.f;
+}
+
+// Epoch permutation pi_{k,e} (reading R10): key_i = mix64(s + i*phi),
+// pi = indices sorted by key (keys are distinct: mix64 is a bijection and
+// s + i*phi is injective in i).  Computed as ranks: rank_i = #{j: key_j < key_i},
+// pi[rank_i] = i.  blockIdx.y = admitted client, blockIdx.z = epoch.
+constexpr int kPermThreads = 256, kPermChunk = 2048;
+__global__ void __launch_bounds__(kPermThreads)
+    k_admit_perm(const ClientRec* __restrict__ recs, const int* __restrict__ ids, uint32_t seed, uint32_t round,
+                 int shuffle) {
+  __shared__ uint64_t keys[kPermChunk];
+  const ClientRec* c = recs + ids[blockIdx.y];
+  const int e = blockIdx.z;
+  if (e >= c->E) return;
+  const int n = c->n;
+  int32_t* perm = c->perm + (int64_t)e * n;
+  const uint64_t GOLD = 0x9E3779B97F4A7C15ull;
+  const uint64_t s = mix64(mix64(mix64((uint64_t)seed ^ (uint64_t)round) ^ (uint64_t)c->id) ^ (uint64_t)e);
+  for (int i0 = blockIdx.x * kPermThreads; i0 < n; i0 += gridDim.x * kPermThreads) {
+    const int i = i0 + threadIdx.x;
+    if (!shuffle) {
+      if (i < n) perm[i] = i;
+      continue;
+    }
+    const uint64_t ki = mix64(s + (uint64_t)i * GOLD);
+    int rank = 0;
+    for (int j0 = 0; j0 < n; j0 += kPermChunk) {
+      __syncthreads();
+      for (int j = threadIdx.x; j < kPermChunk && j0 + j < n; j += kPermThreads)
+        keys[j] = mix64(s + (uint64_t)(j0 + j) * GOLD);
+      __syncthreads();
+      const int lim = min(kPermChunk, n - j0);
+      if (i < n)
+        for (int j = 0; j < lim; ++j) rank += keys[j] < ki;
+    }
+    if (i < n) perm[rank] = i;
+  }
+}
+
+// Release (P:209 stage (4) "resources get freed") + FedAvg partial:
+// acc[d] += n_k * (w_k[d] - w_g[d]) in fp64, clients in the given (ascending
+// id) order, so the per-element summation order is fixed.
+__global__ void k_release_acc(const ClientRec* __restrict__ recs, const int* __restrict__ ids, int nrel, int64_t P) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < P; d += (int64_t)gridDim.x * blockDim.x) {
+    const ClientRec* c0 = recs + ids[0];
+    double a = c0->acc[d];
+    const double g = (double)c0->wg[d];
+    for (int i = 0; i < nrel; ++i) {
+      const ClientRec* c = recs + ids[i];
+      a += (double)c->n * ((double)c->params[d] - g);
+    }
+    c0->acc[d] = a;
+  }
+}
+
+// w' = w_g + acc / N  (fp64, one rounding to fp32); reading R20.
+__global__ void k_finalize(const float* __restrict__ wg, const double* __restrict__ acc, double N, float* __restrict__ out,
+                           int64_t P) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < P; d += (int64_t)gridDim.x * blockDim.x)
+    out[d] = (float)((double)wg[d] + acc[d] / N);
+}
+
+// protea_fedavg: out[d] = sum_k n_k p_k[d] / N, fp64 accumulation in order k.
+__global__ void k_fedavg(const float* const* __restrict__ ptrs, const double* __restrict__ w, int n, double N,
+                         float* __restrict__ out, int64_t dim) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < dim; d += (int64_t)gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int k = 0; k < n; ++k) a += w[k] * (double)ptrs[k][d];
+    out[d] = (float)(a / N);
+  }
+}
+
+}  // namespace protea

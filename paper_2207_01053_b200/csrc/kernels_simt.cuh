@@ -1,0 +1,630 @@
+// kernels_simt.cuh — fp32 SIMT kernels of one lock-step iteration (verify path, K8).
+//
+// Every contraction of local SGD ("finished training"; recipe =
+// DESIGN.md reading R10) is written as an implicit GEMM  C[M,N] = sum_k A(m,k) B(k,n)
+// over ALL active clients of the iteration at once: the grid is the
+// concatenation of every client's tiles (prefix table -> binary search), so
+// one launch per layer-op serves the whole cohort ("grouped GEMM").
+// Operand loaders and epilogues are per-layer functors:
+//   conv fwd    M = pixels (quad-major: 4 consecutive m = one 2x2 pool window),
+//               N = cout, K = (ky,kx,ci); epilogue bias + ReLU + 2x2 max-pool
+//               (first max wins, strict >) -> pooled value + argmax byte.
+//   conv dgrad  M = pixels of the layer input, N = cin, K = (ky,kx,co) (flipped
+//               taps); epilogue ReLU mask + pool-backward scatter to full res.
+//   conv wgrad  M = cout, N = (ky,kx,ci) + 1 bias column, K = pixels, split-K
+//               into fixed chunks; partials summed in split order by k_reduce_update.
+//   fc fwd / dgrad / wgrad analogously; fc wgrad applies the SGD update in its
+//   epilogue (W <- W - lr dW), after the dgrad kernel read the old W.
+// All sums run in a fixed order (deterministic, run-to-run bitwise stable).
+#pragma once
+#include "device.cuh"
+
+namespace protea {
+
+struct GemmTile {
+  const ClientRec* c;
+  Task tk;
+  int m0, n0, kb, ke, M, N;
+  int split;
+};
+
+// --------------------------------------------------------------------------
+// generic SIMT implicit GEMM
+// --------------------------------------------------------------------------
+template <int BM, int BN, class Op>
+__global__ void __launch_bounds__((BM / 4) * (BN / 4))
+    k_gemm_simt(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
+  constexpr int TX = BN / 4, NT = (BM / 4) * (BN / 4), BK = 16;
+  __shared__ __align__(16) float As[BK][BM + 4];
+  __shared__ __align__(16) float Bs[BK][BN + 4];
+  const int ti = find_task(prefix, ntask, blockIdx.x);
+  GemmTile t;
+  t.tk = tasks[ti];
+  t.c = op.recs + t.tk.rec;
+  op.setup(t, blockIdx.x - __ldg(prefix + ti));
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (int k0 = t.kb; k0 < t.ke; k0 += BK) {
+    for (int i = tid; i < BM * BK; i += NT) {
+      int mm, kk;
+      if (Op::A_KFAST) {
+        kk = i % BK;
+        mm = i / BK;
+      } else {
+        mm = i % BM;
+        kk = i / BM;
+      }
+      const int m = t.m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < t.M && k < t.ke) ? op.A(t, m, k) : 0.f;
+    }
+    for (int i = tid; i < BN * BK; i += NT) {
+      int nn, kk;
+      if (Op::B_KFAST) {
+        kk = i % BK;
+        nn = i / BK;
+      } else {
+        nn = i % BN;
+        kk = i / BN;
+      }
+      const int n = t.n0 + nn, k = k0 + kk;
+      Bs[kk][nn] = (n < t.N && k < t.ke) ? op.B(t, k, n) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[kk][(tid / TX) * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  op.epilogue(t, t.m0 + ty * 4, t.n0 + tx * 4, acc);
+}
+
+// tile decode helpers (host mirrors these in engine.cu: tiles_*())
+__host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// Pool epilogue: thread holds 4 consecutive m (one 2x2 window, q = 2*dy+dx)
+// for 4 columns.  relu -> first max (strict >) -> pooled + argmax.
+__device__ __forceinline__ void pool4(const float v[4], float& best, int& arg) {
+  best = fmaxf(v[0], 0.f);
+  arg = 0;
+#pragma unroll
+  for (int q = 1; q < 4; ++q) {
+    const float r = fmaxf(v[q], 0.f);
+    if (r > best) {
+      best = r;
+      arg = q;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// CNN-w ops
+// --------------------------------------------------------------------------
+struct CnnDims {
+  int c1, c2, f, classes;
+  int64_t w1, b1, w2, b2, w3, b3, w4, b4;  // conv1, conv2, fc1, fc2 offsets in params
+};
+
+template <typename T, int BM, int BN>
+struct Conv1Fwd {  // M = rows*1024 (quad-major 32x32), N = c1, K = 75
+  static constexpr bool A_KFAST = true, B_KFAST = true;
+  const ClientRec* recs;
+  CnnDims d;
+  __device__ void setup(GemmTile& t, int local) const {
+    const int nt = cdiv(d.c1, BN);
+    t.M = t.tk.rows * 1024;
+    t.N = d.c1;
+    t.m0 = (local / nt) * BM;
+    t.n0 = (local % nt) * BN;
+    t.kb = 0;
+    t.ke = 75;
+    t.split = t.c->perm[t.tk.base + (t.m0 >> 10)];  // sample index of the tile's image
+  }
+  __device__ float A(const GemmTile& t, int m, int k) const {
+    const int local = m & 1023, p = local >> 2, q = local & 3;
+    const int y = ((p >> 4) << 1) + (q >> 1), x = ((p & 15) << 1) + (q & 1);
+    const int tap = k / 3, ci = k - tap * 3, ky = tap / 5, kx = tap - ky * 5;
+    const int sy = y + ky - 2, sx = x + kx - 2;
+    if ((unsigned)sy >= 32u || (unsigned)sx >= 32u) return 0.f;
+    return px01(t.c->x[(int64_t)t.split * 3072 + (sy * 32 + sx) * 3 + ci]);
+  }
+  __device__ float B(const GemmTile& t, int k, int n) const { return t.c->params[d.w1 + (int64_t)n * 75 + k]; }
+  __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
+    if (mb >= t.M) return;
+    const int r = mb >> 10, p = (mb & 1023) >> 2;
+    T* a1 = (T*)t.c->buf[B_A1];
+    uint8_t* i1 = (uint8_t*)t.c->buf[B_I1];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = nb + j;
+      if (n >= t.N) continue;
+      const float bias = t.c->params[d.b1 + n];
+      const float v[4] = {acc[0][j] + bias, acc[1][j] + bias, acc[2][j] + bias, acc[3][j] + bias};
+      float best;
+      int arg;
+      pool4(v, best, arg);
+      const int64_t o = ((int64_t)r * 256 + p) * d.c1 + n;
+      stv(a1 + o, best);
+      i1[o] = (uint8_t)arg;
+    }
+  }
+};
+
+template <typename T, int BM, int BN>
+struct Conv2Fwd {  // M = rows*256 (quad-major 16x16), N = c2, K = 25*c1
+  static constexpr bool A_KFAST = true, B_KFAST = true;
+  const ClientRec* recs;
+  CnnDims d;
+  __device__ void setup(GemmTile& t, int local) const {
+    const int nt = cdiv(d.c2, BN);
+    t.M = t.tk.rows * 256;
+    t.N = d.c2;
+    t.m0 = (local / nt) * BM;
+    t.n0 = (local % nt) * BN;
+    t.kb = 0;
+    t.ke = 25 * d.c1;
+  }
+  __device__ float A(const GemmTile& t, int m, int k) const {
+    const int r = m >> 8, local = m & 255, p = local >> 2, q = local & 3;
+    const int y = ((p >> 3) << 1) + (q >> 1), x = ((p & 7) << 1) + (q & 1);
+    const int tap = k / d.c1, ci = k - tap * d.c1, ky = tap / 5, kx = tap - ky * 5;
+    const int sy = y + ky - 2, sx = x + kx - 2;
+    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return 0.f;
+    const T* a1 = (const T*)t.c->buf[B_A1];
+    return ldv(a1 + ((int64_t)r * 256 + sy * 16 + sx) * d.c1 + ci);
+  }
+  __device__ float B(const GemmTile& t, int k, int n) const {
+    return t.c->params[d.w2 + (int64_t)n * 25 * d.c1 + k];
+  }
+  __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
+    if (mb >= t.M) return;
+    const int r = mb >> 8, p = (mb & 255) >> 2;
+    T* a2 = (T*)t.c->buf[B_A2];
+    uint8_t* i2 = (uint8_t*)t.c->buf[B_I2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = nb + j;
+      if (n >= t.N) continue;
+      const float bias = t.c->params[d.b2 + n];
+      const float v[4] = {acc[0][j] + bias, acc[1][j] + bias, acc[2][j] + bias, acc[3][j] + bias};
+      float best;
+      int arg;
+      pool4(v, best, arg);
+      const int64_t o = ((int64_t)r * 64 + p) * d.c2 + n;
+      stv(a2 + o, best);
+      i2[o] = (uint8_t)arg;
+    }
+  }
+};
+
+template <typename T, int BM, int BN>
+struct Fc1Fwd {  // M = rows, N = f, K = 64*c2
+  static constexpr bool A_KFAST = true, B_KFAST = true;
+  const ClientRec* recs;
+  CnnDims d;
+  __device__ void setup(GemmTile& t, int local) const {
+    const int nt = cdiv(d.f, BN);
+    t.M = t.tk.rows;
+    t.N = d.f;
+    t.m0 = (local / nt) * BM;
+    t.n0 = (local % nt) * BN;
+    t.kb = 0;
+    t.ke = 64 * d.c2;
+  }
+  __device__ float A(const GemmTile& t, int m, int k) const {
+    return ldv((const T*)t.c->buf[B_A2] + (int64_t)m * 64 * d.c2 + k);
+  }
+  __device__ float B(const GemmTile& t, int k, int n) const {
+    return t.c->params[d.w3 + (int64_t)n * 64 * d.c2 + k];
+  }
+  __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
+    T* h = (T*)t.c->buf[B_H];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int m = mb + i, n = nb + j;
+        if (m < t.M && n < t.N) stv(h + (int64_t)m * d.f + n, fmaxf(acc[i][j] + t.c->params[d.b3 + n], 0.f));
+      }
+  }
+};
+
+template <typename T, int BM, int BN>
+struct Fc1Dgrad {  // dA2 = dh W1: M = rows, N = 64*c2, K = f; epilogue: pool2 backward -> dz2 (16x16)
+  static constexpr bool A_KFAST = true, B_KFAST = false;
+  const ClientRec* recs;
+  CnnDims d;
+  __device__ void setup(GemmTile& t, int local) const {
+    const int nt = cdiv(64 * d.c2, BN);
+    t.M = t.tk.rows;
+    t.N = 64 * d.c2;
+    t.m0 = (local / nt) * BM;
+    t.n0 = (local % nt) * BN;
+    t.kb = 0;
+    t.ke = d.f;
+  }
+  __device__ float A(const GemmTile& t, int m, int k) const {
+    return ((const float*)t.c->buf[B_DH])[(int64_t)m * d.f + k];
+  }
+  __device__ float B(const GemmTile& t, int k, int n) const {
+    return t.c->params[d.w3 + (int64_t)k * 64 * d.c2 + n];
+  }
+  __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
+    const T* a2 = (const T*)t.c->buf[B_A2];
+    const uint8_t* i2 = (const uint8_t*)t.c->buf[B_I2];
+    T* dz2 = (T*)t.c->buf[B_DZ2];
+    const int N = t.N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int m = mb + i, n = nb + j;
+        if (m >= t.M || n >= N) continue;
+        const int64_t o = (int64_t)m * N + n;
+        const float v = ldv(a2 + o) > 0.f ? acc[i][j] : 0.f;
+        const int arg = i2[o];
+        const int p = n / d.c2, c = n - p * d.c2, py = p >> 3, px = p & 7;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int y = 2 * py + (q >> 1), x = 2 * px + (q & 1);
+          stv(dz2 + ((int64_t)m * 256 + y * 16 + x) * d.c2 + c, q == arg ? v : 0.f);
+        }
+      }
+  }
+};
+
+template <typename T, int BM, int BN>
+struct Fc1Wgrad {  // W1 -= lr dh^T a2: M = f, N = 64*c2 + 1 (bias), K = rows
+  static constexpr bool A_KFAST = false, B_KFAST = false;
+  const ClientRec* recs;
+  CnnDims d;
+  float lr;
+  __device__ void setup(GemmTile& t, int local) const {
+    const int nt = cdiv(64 * d.c2 + 1, BN);
+    t.M = d.f;
+    t.N = 64 * d.c2 + 1;
+    t.m0 = (local / nt) * BM;
+    t.n0 = (local % nt) * BN;
+    t.kb = 0;
+    t.ke = t.tk.rows;
+  }
+  __device__ float A(const GemmTile& t, int m, int k) const {
+    return ((const float*)t.c->buf[B_DH])[(int64_t)k * d.f + m];
+  }
+  __device__ float B(const GemmTile& t, int k, int n) const {
+    const int K1 = 64 * d.c2;
+    return n < K1 ? ldv((const T*)t.c->buf[B_A2] + (int64_t)k * K1 + n) : 1.f;
+  }
+  __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
+    const int K1 = 64 * d.c2;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int m = mb + i, n = nb + j;
+        if (m >= t.M || n >= t.N) continue;
+        float* w = n < K1 ? t.c->params + d.w3 + (int64_t)m * K1 + n : t.c->params + d.b3 + m;
+        *w = *w - lr * acc[i][j];
+      }
+  }
+};
+
+template <typename T, int BM, int BN>
+struct Conv2Dgrad {  // dA1: M = rows*256 (row-major 16x16), N = c1, K = 25*c2; epilogue pool1 backward -> dz1
+  static constexpr bool A_KFAST = true, B_KFAST = false;
+  const ClientRec* recs;
+  CnnDims d;
+  __device__ void setup(GemmTile& t, int local) const {
+    const int nt = cdiv(d.c1, BN);
+    t.M = t.tk.rows * 256;
+    t.N = d.c1;
+    t.m0 = (local / nt) * BM;
+    t.n0 = (local % nt) * BN;
+    t.kb = 0;
+    t.ke = 25 * d.c2;
+  }
+  __device__ float A(const GemmTile& t, int m, int k) const {
+    const int r = m >> 8, y = (m >> 4) & 15, x = m & 15;
+    const int tap = k / d.c2, co = k - tap * d.c2, ky = tap / 5, kx = tap - ky * 5;
+    const int sy = y - ky + 2, sx = x - kx + 2;
+    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return 0.f;
+    return ldv((const T*)t.c->buf[B_DZ2] + ((int64_t)r * 256 + sy * 16 + sx) * d.c2 + co);
+  }
+  __device__ float B(const GemmTile& t, int k, int n) const {
+    const int tap = k / d.c2, co = k - tap * d.c2;
+    return t.c->params[d.w2 + ((int64_t)co * 25 + tap) * d.c1 + n];
+  }
+  __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
+    const T* a1 = (const T*)t.c->buf[B_A1];
+    const uint8_t* i1 = (const uint8_t*)t.c->buf[B_I1];
+    T* dz1 = (T*)t.c->buf[B_DZC1];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int m = mb + i, n = nb + j;
+        if (m >= t.M || n >= t.N) continue;
+        const int64_t o = (int64_t)m * d.c1 + n;
+        const float v = ldv(a1 + o) > 0.f ? acc[i][j] : 0.f;
+        const int arg = i1[o];
+        const int r = m >> 8, y = (m >> 4) & 15, x = m & 15;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int Y = 2 * y + (q >> 1), X = 2 * x + (q & 1);
+          stv(dz1 + ((int64_t)r * 1024 + Y * 32 + X) * d.c1 + n, q == arg ? v : 0.f);
+        }
+      }
+  }
+};
+
+// conv wgrad, split-K: partial[split][m][n] for n in [0, N) (N = K_w + 1 bias column)
+template <typename T, int BM, int BN>
+struct Conv2Wgrad {  // M = c2, N = 25*c1 + 1, K = rows*256 pixels (splits of 2048)
+  static constexpr bool A_KFAST = false, B_KFAST = false;
+  const ClientRec* recs;
+  CnnDims d;
+  __device__ void setup(GemmTile& t, int local) const {
+    const int N = 25 * d.c1 + 1, nt = cdiv(N, BN), mt = cdiv(d.c2, BM);
+    t.split = local / (mt * nt);
+    const int rem = local - t.split * mt * nt;
+    t.M = d.c2;
+    t.N = N;
+    t.m0 = (rem / nt) * BM;
+    t.n0 = (rem % nt) * BN;
+    t.kb = t.split * kWgradChunkPx;
+    t.ke = min(t.tk.rows * 256, t.kb + kWgradChunkPx);
+  }
+  __device__ float A(const GemmTile& t, int m, int k) const {
+    return ldv((const T*)t.c->buf[B_DZ2] + (int64_t)k * d.c2 + m);
+  }
+  __device__ float B(const GemmTile& t, int k, int n) const {
+    const int Kw = 25 * d.c1;
+    if (n == Kw) return 1.f;
+    const int r = k >> 8, y = (k >> 4) & 15, x = k & 15;
+    const int tap = n / d.c1, ci = n - tap * d.c1, ky = tap / 5, kx = tap - ky * 5;
+    const int sy = y + ky - 2, sx = x + kx - 2;
+    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return 0.f;
+    return ldv((const T*)t.c->buf[B_A1] + ((int64_t)r * 256 + sy * 16 + sx) * d.c1 + ci);
+  }
+  __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
+    float* part = (float*)t.c->buf[B_WSP] + (int64_t)t.split * t.M * t.N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int m = mb + i, n = nb + j;
+        if (m < t.M && n < t.N) part[(int64_t)m * t.N + n] = acc[i][j];
+      }
+  }
+};
+
+template <typename T, int BM, int BN>
+struct Conv1Wgrad {  // M = c1, N = 76, K = rows*1024 pixels (splits of 2048)
+  static constexpr bool A_KFAST = false, B_KFAST = false;
+  const ClientRec* recs;
+  CnnDims d;
+  __device__ void setup(GemmTile& t, int local) const {
+    const int N = 76, nt = cdiv(N, BN), mt = cdiv(d.c1, BM);
+    t.split = local / (mt * nt);
+    const int rem = local - t.split * mt * nt;
+    t.M = d.c1;
+    t.N = N;
+    t.m0 = (rem / nt) * BM;
+    t.n0 = (rem % nt) * BN;
+    t.kb = t.split * kWgradChunkPx;
+    t.ke = min(t.tk.rows * 1024, t.kb + kWgradChunkPx);
+  }
+  __device__ float A(const GemmTile& t, int m, int k) const {
+    return ldv((const T*)t.c->buf[B_DZC1] + (int64_t)k * d.c1 + m);
+  }
+  __device__ float B(const GemmTile& t, int k, int n) const {
+    if (n == 75) return 1.f;
+    const int r = k >> 10, y = (k >> 5) & 31, x = k & 31;
+    const int tap = n / 3, ci = n - tap * 3, ky = tap / 5, kx = tap - ky * 5;
+    const int sy = y + ky - 2, sx = x + kx - 2;
+    if ((unsigned)sy >= 32u || (unsigned)sx >= 32u) return 0.f;
+    const int s = t.c->perm[t.tk.base + r];
+    return px01(t.c->x[(int64_t)s * 3072 + (sy * 32 + sx) * 3 + ci]);
+  }
+  __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
+    float* part = (float*)t.c->buf[B_WSP] + (int64_t)t.split * t.M * t.N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int m = mb + i, n = nb + j;
+        if (m < t.M && n < t.N) part[(int64_t)m * t.N + n] = acc[i][j];
+      }
+  }
+};
+
+// Sum split partials in split order, then W -= lr * g (n < Nw) / b -= lr * g (n == Nw).
+struct ReduceArgs {
+  const ClientRec* recs;
+  int wsp_buf;  // B_WSP or B_R_WSP
+  int M, Nw;    // partial is [splits][M][Nw+1]
+  int64_t off_w, off_b;
+  int px_per_row;  // pixels per sample of the layer output (split count = ceil(rows*px/2048))
+  float lr;
+};
+constexpr int kReduceBlock = 256;
+__global__ void __launch_bounds__(kReduceBlock)
+    k_reduce_update(ReduceArgs a, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
+  const int ti = find_task(prefix, ntask, blockIdx.x);
+  const Task tk = tasks[ti];
+  const ClientRec* c = a.recs + tk.rec;
+  const int N = a.Nw + 1, total = a.M * N;
+  const int e = (blockIdx.x - prefix[ti]) * kReduceBlock + threadIdx.x;
+  if (e >= total) return;
+  const int splits = cdiv(tk.rows * a.px_per_row, kWgradChunkPx);
+  const float* part = (const float*)c->buf[a.wsp_buf];
+  float g = 0.f;
+  for (int s = 0; s < splits; ++s) g += part[(int64_t)s * total + e];
+  const int m = e / N, n = e - m * N;
+  float* w = n < a.Nw ? c->params + a.off_w + (int64_t)m * a.Nw + n : c->params + a.off_b + m;
+  *w = *w - a.lr * g;
+}
+
+// --------------------------------------------------------------------------
+// MLP ops (784-64-10)
+// --------------------------------------------------------------------------
+struct MlpDims {
+  int classes;
+  int64_t w1, b1, w2, b2;
+};
+
+template <typename T, int BM, int BN>
+struct MlpFc1Fwd {  // M = rows, N = 64, K = 784
+  static constexpr bool A_KFAST = true, B_KFAST = true;
+  const ClientRec* recs;
+  MlpDims d;
+  __device__ void setup(GemmTile& t, int local) const {
+    const int nt = cdiv(64, BN);
+    t.M = t.tk.rows;
+    t.N = 64;
+    t.m0 = (local / nt) * BM;
+    t.n0 = (local % nt) * BN;
+    t.kb = 0;
+    t.ke = 784;
+  }
+  __device__ float A(const GemmTile& t, int m, int k) const {
+    const int s = t.c->perm[t.tk.base + m];
+    return px01(t.c->x[(int64_t)s * 784 + k]);
+  }
+  __device__ float B(const GemmTile& t, int k, int n) const { return t.c->params[d.w1 + (int64_t)n * 784 + k]; }
+  __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
+    T* h = (T*)t.c->buf[B_H1];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int m = mb + i, n = nb + j;
+        if (m < t.M && n < t.N) stv(h + (int64_t)m * 64 + n, fmaxf(acc[i][j] + t.c->params[d.b1 + n], 0.f));
+      }
+  }
+};
+
+template <typename T, int BM, int BN>
+struct MlpFc1Wgrad {  // M = 64, N = 785, K = rows
+  static constexpr bool A_KFAST = false, B_KFAST = false;
+  const ClientRec* recs;
+  MlpDims d;
+  float lr;
+  __device__ void setup(GemmTile& t, int local) const {
+    const int nt = cdiv(785, BN);
+    t.M = 64;
+    t.N = 785;
+    t.m0 = (local / nt) * BM;
+    t.n0 = (local % nt) * BN;
+    t.kb = 0;
+    t.ke = t.tk.rows;
+  }
+  __device__ float A(const GemmTile& t, int m, int k) const {
+    return ((const float*)t.c->buf[B_DZ1])[(int64_t)k * 64 + m];
+  }
+  __device__ float B(const GemmTile& t, int k, int n) const {
+    if (n == 784) return 1.f;
+    const int s = t.c->perm[t.tk.base + k];
+    return px01(t.c->x[(int64_t)s * 784 + n]);
+  }
+  __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int m = mb + i, n = nb + j;
+        if (m >= t.M || n >= t.N) continue;
+        float* w = n < 784 ? t.c->params + d.w1 + (int64_t)m * 784 + n : t.c->params + d.b1 + m;
+        *w = *w - lr * acc[i][j];
+      }
+  }
+};
+
+// --------------------------------------------------------------------------
+// Fused classifier head (K3): fc2 fwd -> softmax-CE -> dlogits -> dh (masked by
+// h > 0, with the OLD W2) -> W2/b2 SGD update.  One CTA per active client.
+// --------------------------------------------------------------------------
+struct HeadArgs {
+  const ClientRec* recs;
+  int hbuf, dhbuf;  // buffer ids of h (act) and dh (fp32)
+  int F, classes;
+  int64_t w, b;     // fc2 offsets
+  float lr;
+};
+constexpr int kHeadThreads = 256;
+template <typename T>
+__global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a, const Task* __restrict__ tasks) {
+  __shared__ float dlog[64 * 64];
+  __shared__ float lossr[64];
+  const Task tk = tasks[blockIdx.x];
+  const ClientRec* c = a.recs + tk.rec;
+  const int rows = tk.rows, F = a.F, C = a.classes;
+  const T* h = (const T*)c->buf[a.hbuf];
+  float* W = c->params + a.w;
+  float* bias = c->params + a.b;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // 1. logits
+  for (int idx = warp; idx < rows * C; idx += kHeadThreads / 32) {
+    const int r = idx / C, cc = idx - r * C;
+    float s = 0.f;
+    for (int f = lane; f < F; f += 32) s = fmaf(ldv(h + (int64_t)r * F + f), W[(int64_t)cc * F + f], s);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) dlog[r * C + cc] = s + bias[cc];
+  }
+  __syncthreads();
+  // 2. softmax-CE per row; dlogits = (p - onehot) / rows
+  if (threadIdx.x < rows) {
+    const int r = threadIdx.x;
+    const int label = c->y[c->perm[tk.base + r]];
+    float mx = -INFINITY;
+    for (int cc = 0; cc < C; ++cc) mx = fmaxf(mx, dlog[r * C + cc]);
+    float s = 0.f;
+    for (int cc = 0; cc < C; ++cc) s += expf(dlog[r * C + cc] - mx);
+    lossr[r] = logf(s) + mx - dlog[r * C + label];
+    const float inv = 1.f / (s * (float)rows);
+    for (int cc = 0; cc < C; ++cc) {
+      const float p = expf(dlog[r * C + cc] - mx);
+      dlog[r * C + cc] = p * inv - (cc == label ? 1.f / (float)rows : 0.f);
+    }
+  }
+  __syncthreads();
+  // 3. dh = (dlogits W2) * (h > 0)   (old W2)
+  float* dh = (float*)c->buf[a.dhbuf];
+  for (int idx = threadIdx.x; idx < rows * F; idx += kHeadThreads) {
+    const int r = idx / F, f = idx - r * F;
+    float s = 0.f;
+    for (int cc = 0; cc < C; ++cc) s = fmaf(dlog[r * C + cc], W[(int64_t)cc * F + f], s);
+    dh[idx] = ldv(h + idx) > 0.f ? s : 0.f;
+  }
+  __syncthreads();
+  // 4. W2 -= lr dlogits^T h ; b2 -= lr sum_r dlogits
+  for (int idx = threadIdx.x; idx < C * F; idx += kHeadThreads) {
+    const int cc = idx / F, f = idx - cc * F;
+    float g = 0.f;
+    for (int r = 0; r < rows; ++r) g = fmaf(dlog[r * C + cc], ldv(h + (int64_t)r * F + f), g);
+    W[idx] -= a.lr * g;
+  }
+  if (threadIdx.x < C) {
+    float g = 0.f;
+    for (int r = 0; r < rows; ++r) g += dlog[r * C + threadIdx.x];
+    bias[threadIdx.x] -= a.lr * g;
+  }
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int r = 0; r < rows; ++r) s += lossr[r];
+    c->stats[0] += s / (float)rows;
+  }
+}
+
+}  // namespace protea

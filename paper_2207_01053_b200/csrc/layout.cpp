@@ -1,0 +1,168 @@
+// layout.cpp — model table, FLOP count and the per-client slot layout.
+//
+// Models (reading R11): MLP 784-64-10; CNN-w (McMahan-style,
+// channels 32w/64w/512w); ResNet-8 (6n+2, n=1, option-A shortcut, no BN).
+// FLOPs: PAPER.md Table 1 CUDA_time needs a work measure; f = 2 x MACs of
+// fwd + wgrad + dgrad without the first layer's dgrad.
+#include <algorithm>
+#include <cstring>
+
+#include "common.h"
+
+namespace protea {
+
+static Layer conv(int k, int stride, int pad, int cin, int cout, int hin, int win) {
+  Layer l{};
+  l.kind = 0;
+  l.k = k;
+  l.stride = stride;
+  l.pad = pad;
+  l.cin = cin;
+  l.cout = cout;
+  l.hin = hin;
+  l.win = win;
+  l.hout = (hin + 2 * pad - k) / stride + 1;
+  l.wout = (win + 2 * pad - k) / stride + 1;
+  return l;
+}
+
+static Layer fc(int in, int out) {
+  Layer l{};
+  l.kind = 1;
+  l.cin = in;
+  l.cout = out;
+  return l;
+}
+
+bool make_model(const protea_model_desc& d, ModelDims* out, std::string* err) {
+  ModelDims m;
+  m.arch = d.arch;
+  m.width_q = d.width_q;
+  m.classes = d.classes;
+  m.H = d.H;
+  m.W = d.W;
+  m.C = d.C;
+  if (d.classes < 2 || d.classes > 64) {
+    *err = "model: classes must be in [2, 64]";
+    return false;
+  }
+  switch (d.arch) {
+    case PROTEA_MODEL_MLP:
+      if (d.width_q != 4 || d.H * d.W * d.C != 784) {
+        *err = "model: MLP needs width_q == 4 and a 784-pixel input (28x28x1)";
+        return false;
+      }
+      m.layers = {fc(784, 64), fc(64, d.classes)};
+      break;
+    case PROTEA_MODEL_CNN:
+      if (!(d.width_q == 1 || d.width_q == 2 || d.width_q == 4) || d.H != 32 || d.W != 32 || d.C != 3) {
+        *err = "model: CNN needs width_q in {1,2,4} and a 32x32x3 input";
+        return false;
+      }
+      m.c1 = 8 * d.width_q;
+      m.c2 = 16 * d.width_q;
+      m.f = 128 * d.width_q;
+      m.layers = {conv(5, 1, 2, 3, m.c1, 32, 32), conv(5, 1, 2, m.c1, m.c2, 16, 16), fc(64 * m.c2, m.f),
+                  fc(m.f, d.classes)};
+      break;
+    case PROTEA_MODEL_RESNET8:
+      if (d.width_q != 4 || d.H != 32 || d.W != 32 || d.C != 3) {
+        *err = "model: RESNET8 needs width_q == 4 and a 32x32x3 input";
+        return false;
+      }
+      m.layers = {conv(3, 1, 1, 3, 16, 32, 32),  conv(3, 1, 1, 16, 16, 32, 32), conv(3, 1, 1, 16, 16, 32, 32),
+                  conv(3, 2, 1, 16, 32, 32, 32), conv(3, 1, 1, 32, 32, 16, 16), conv(3, 2, 1, 32, 64, 16, 16),
+                  conv(3, 1, 1, 64, 64, 8, 8),   fc(64, d.classes)};
+      break;
+    default:
+      *err = "model: unknown arch " + std::to_string(d.arch);
+      return false;
+  }
+  int64_t off = 0;
+  for (auto& l : m.layers) {
+    l.off_w = off;
+    off += (int64_t)l.cout * l.K();
+    l.off_b = off;
+    off += l.cout;
+  }
+  m.P = off;
+  *out = m;
+  return true;
+}
+
+uint64_t flops_per_sample(const ModelDims& m) {
+  uint64_t fwd = 0, dgrad = 0;
+  for (size_t i = 0; i < m.layers.size(); ++i) {
+    const Layer& l = m.layers[i];
+    uint64_t macs = l.kind == 0 ? (uint64_t)l.hout * l.wout * l.cout * l.K() : (uint64_t)l.cin * l.cout;
+    fwd += macs;
+    if (i > 0) dgrad += macs;
+  }
+  return 2 * (2 * fwd + dgrad);
+}
+
+static int splits_for(const Layer& l, int rows) {
+  return (int)ceil_div((uint64_t)rows * l.hout * l.wout, kWgradChunkPx);
+}
+
+int cnn_conv1_splits(int rows) { return (int)ceil_div((uint64_t)rows * 1024, kWgradChunkPx); }
+int cnn_conv2_splits(int rows) { return (int)ceil_div((uint64_t)rows * 256, kWgradChunkPx); }
+
+SlotLayout slot_layout(const ModelDims& m, int b, int64_t n, int epochs, int e) {
+  SlotLayout s;
+  std::memset(&s, 0, sizeof(s));
+  auto put = [&](Buf id, uint64_t bytes) {
+    s.used[id] = true;
+    s.size[id] = bytes;
+  };
+  put(B_PARAMS, 4 * (uint64_t)m.P);
+  put(B_PERM, 4 * (uint64_t)epochs * n);
+  put(B_STATS, 64);
+  const uint64_t B = b;
+  if (m.arch == PROTEA_MODEL_MLP) {
+    put(B_H1, B * 64 * e);
+    put(B_DZ1, B * 64 * 4);
+  } else if (m.arch == PROTEA_MODEL_CNN) {
+    put(B_A1, B * 256 * m.c1 * e);
+    put(B_I1, B * 256 * m.c1);
+    put(B_A2, B * 64 * m.c2 * e);
+    put(B_I2, B * 64 * m.c2);
+    put(B_H, B * m.f * e);
+    put(B_DH, B * m.f * 4);
+    put(B_DZ2, B * 256 * m.c2 * e);
+    put(B_DZC1, B * 1024 * m.c1 * e);
+  } else {
+    put(B_R_A0, B * 1024 * 16 * e);
+    put(B_R_R1, B * 1024 * 16 * e);
+    put(B_R_O1, B * 1024 * 16 * e);
+    put(B_R_R2, B * 256 * 32 * e);
+    put(B_R_O2, B * 256 * 32 * e);
+    put(B_R_R3, B * 64 * 64 * e);
+    put(B_R_O3, B * 64 * 64 * e);
+    put(B_R_GAP, B * 64 * e);
+    put(B_R_DGAP, B * 64 * 4);
+    put(B_R_G0, B * 1024 * 16 * e);
+    put(B_R_G1, B * 1024 * 16 * e);
+    put(B_R_G2, B * 1024 * 16 * e);
+  }
+  uint64_t wsp = 0;
+  for (const Layer& l : m.layers)
+    if (l.kind == 0) wsp = std::max<uint64_t>(wsp, 4ull * splits_for(l, b) * l.cout * (l.K() + 1));
+  if (wsp) put(m.arch == PROTEA_MODEL_RESNET8 ? B_R_WSP : B_WSP, wsp);
+  // slot order = enum order except that the wgrad partials come last (oracle order)
+  uint64_t off = 0;
+  for (int i = 0; i < B_COUNT; ++i) {
+    if (!s.used[i] || i == B_WSP || i == B_R_WSP) continue;
+    s.off[i] = off;
+    off += align256(s.size[i]);
+  }
+  for (int i : {B_WSP, B_R_WSP})
+    if (s.used[i]) {
+      s.off[i] = off;
+      off += align256(s.size[i]);
+    }
+  s.total = off;
+  return s;
+}
+
+}  // namespace protea

@@ -1,0 +1,165 @@
+"""GPU parity: the CUDA path through the C ABI vs the float64 oracle on the
+same seeded inputs (BASELINE.json north_star tolerances: rel-L2 1e-5 in the
+fp32 verification mode, 1e-2 in bf16 mode; plan bit-exact)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import fedavg as ofa
+from oracle import planner as opl
+from oracle import profiler as opf
+from tests.gpu_helpers import gpu_run, oracle_run, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+BF16_TOL = 1e-2
+
+
+@pytest.fixture(scope="module")
+def torch():
+    t = pytest.importorskip("torch")
+    if not t.cuda.is_available():
+        pytest.skip("no GPU")
+    return t
+
+
+def test_fedavg_kernel_ulp(torch):
+    import paper_2207_01053_b200 as pb
+    from paper_2207_01053_b200.sim import Simulation
+    sim = Simulation(arena_bytes=1 << 20)
+    rng = np.random.default_rng(0)
+    for K, D in ((1, 7), (3, 1000), (17, 4099), (100, 50890)):
+        ws = [rng.normal(size=D).astype(np.float32) for _ in range(K)]
+        ns = rng.integers(1, 600, size=K)
+        out = torch.empty(D, device="cuda")
+        pb.protea_fedavg(sim.ctx, [torch.tensor(w, device="cuda") for w in ws], ns, out)
+        ref = ofa.fedavg(ws, ns).astype(np.float32)  # oracle (fp64) rounded to fp32
+        got = out.cpu().numpy()
+        ulp = np.abs(got.view(np.int32).astype(np.int64) - ref.view(np.int32).astype(np.int64))
+        assert ulp.max() <= 1
+    # SPEC S:441 closed form
+    out = torch.empty(1, device="cuda")
+    pb.protea_fedavg(sim.ctx, [torch.tensor([2.0], device="cuda"), torch.tensor([4.0], device="cuda")], [1, 3], out)
+    assert out.item() == 3.5
+    with pytest.raises(pb.ProteaError) as e:
+        pb.protea_fedavg(sim.ctx, [], [], out)
+    assert e.value.name == "EMPTY"
+    with pytest.raises(pb.ProteaError) as e:
+        pb.protea_fedavg(sim.ctx, [out], [0], out)
+    assert e.value.name == "INVALID"
+    sim.close()
+
+
+def test_config1_mlp_fp32_three_rounds(torch):
+    wl = synth.build_workload(1)  # 10 clients x 50, B=10, E=1, 3 rounds
+    got, ex = gpu_run(wl, rounds=3)
+    ref = oracle_run(wl, rounds=3)
+    assert rel_l2(got[4], ref[4]) <= FP32_TOL
+    # round update diagnostic
+    d_got = got[4] - ex["g0"][4]
+    d_ref = ref[4] - ex["g0"][4]
+    assert rel_l2(d_got, d_ref) <= 1e-4
+
+
+def test_config2_reduced_cnn_fp32(torch):
+    # config 2 shape (CNN-1x CIFAR, B in {8,16,32,64}, E=2), 6 clients x 37 samples:
+    # every batch size has a ragged last batch, and several tiles per layer.
+    wl = synth.build_workload(2, n_clients=6, samples=37)
+    got, ex = gpu_run(wl)
+    ref = oracle_run(wl)
+    assert rel_l2(got[4], ref[4]) <= FP32_TOL
+    assert rel_l2(got[4] - ex["g0"][4], ref[4] - ex["g0"][4]) <= 1e-3
+
+
+def test_config4_mixed_widths_fp32(torch):
+    wl = synth.build_workload(4, k=7, samples=20, epochs=1)
+    got, _ = gpu_run(wl, all_widths=True)
+    ref = oracle_run(wl, all_widths=True)
+    present = {c.width_q for c in wl.clients}
+    for w in (1, 2, 4):
+        if w in present:
+            assert rel_l2(got[w], ref[w]) <= FP32_TOL, w
+        else:
+            assert np.array_equal(got[w], synth.init_weights(synth.MODEL_CNN, w))
+
+
+def test_config2_reduced_cnn_bf16(torch):
+    wl = synth.build_workload(2, n_clients=4, samples=24)
+    got, _ = gpu_run(wl, precision=1)
+    ref = oracle_run(wl)
+    assert rel_l2(got[4], ref[4]) <= BF16_TOL
+
+
+def test_profiles_and_plan_match_oracle(torch):
+    wl = synth.build_workload(3, k=12, samples=20)
+    _, ex = gpu_run(wl)
+    prof, plan = ex["prof"], ex["plan"]
+    cl = {c.id: c for c in wl.clients}
+    for p in prof:
+        c = cl[int(p["client_id"])]
+        assert int(p["peak_bytes"]) == opf.hwm_bytes(c.model, c.width_q, 10, c.batch, c.n, c.epochs, 4)
+        assert int(p["steps"]) == opf.local_steps(c.n, c.batch, c.epochs)
+        assert int(p["flops"]) == opf.client_flops(c.n, c.epochs, c.model, c.width_q)
+        assert int(p["step_ns"]) > 0 and int(p["uses_gpu"]) == 1
+    ref, mk = opl.plan([dict(id=int(p["client_id"]), peak_bytes=int(p["peak_bytes"]), steps=int(p["steps"]),
+                             flops=int(p["flops"])) for p in prof], [1 << 30])
+    for a, r in zip(plan, ref):
+        assert (int(a["client_id"]), int(a["offset"]), int(a["slot"]), int(a["admit"]), int(a["release"])) == \
+            (r["id"], r["offset"], r["slot"], r["admit"], r["release"])
+    assert list(ex["makespans"]) == mk
+
+
+def test_memory_bound_fifo_schedule_same_result(torch):
+    # a tiny arena forces FIFO admission with slot reuse (P:209 stages (3)-(4));
+    # the federated result must not depend on the schedule.
+    wl = synth.build_workload(2, n_clients=5, samples=19, epochs=1)
+    free, _ = gpu_run(wl)
+    from oracle import profiler as opf
+    slot = max(opf.hwm_bytes(c.model, 4, 10, c.batch, c.n, c.epochs, 4) for c in wl.clients)
+    cap = 2 * slot + 256 * 3
+    tight, ex = gpu_run(wl, arena_bytes=cap)
+    assert max(int(a["admit"]) for a in ex["plan"]) > 0  # somebody had to wait
+    assert rel_l2(tight[4], free[4]) <= 1e-7
+
+
+def test_shuffle_off_and_single_client(torch):
+    wl = synth.build_workload(2, n_clients=1, samples=9, epochs=2)
+    got, _ = gpu_run(wl, shuffle=False, lr=0.1)
+    ref = oracle_run(wl, shuffle=False, lr=0.1)
+    assert rel_l2(got[4], ref[4]) <= FP32_TOL
+
+
+def test_determinism_bitwise(torch):
+    wl = synth.build_workload(2, n_clients=4, samples=21, epochs=1)
+    a, _ = gpu_run(wl)
+    b, _ = gpu_run(wl)
+    assert np.array_equal(a[4], b[4])
+
+
+def test_abi_errors_on_gpu(torch):
+    import paper_2207_01053_b200 as pb
+    wl = synth.build_workload(2, n_clients=2, samples=8, epochs=1)
+    _, ex = gpu_run(wl, return_sim=True)
+    sim = ex["sim"]
+    clients = sim.clients([(c.id, 0, c.batch, c.epochs) for c in wl.clients])
+    g = torch.tensor(synth.init_weights(synth.MODEL_CNN), device="cuda")
+    bad = ex["plan"].copy()
+    bad["release"][0] += 1
+    with pytest.raises(pb.ProteaError) as e:
+        sim.run_round(clients, bad, g)
+    assert e.value.name == "PLAN"
+    bad = ex["plan"].copy()
+    bad["offset"][0] = sim.arena.numel()
+    with pytest.raises(pb.ProteaError) as e:
+        sim.run_round(clients, bad, g)
+    assert e.value.name == "OOM"
+    with pytest.raises(pb.ProteaError) as e:
+        sim.run_round(clients, ex["plan"], g[:-1])
+    assert e.value.name == "DIM"
+    c2 = clients.copy()
+    c2["batch"][0] = 65
+    with pytest.raises(pb.ProteaError) as e:
+        sim.run_round(c2, ex["plan"], g)
+    assert e.value.name == "INVALID"
+    sim.close()
