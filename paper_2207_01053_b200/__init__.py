@@ -62,17 +62,29 @@ class PlanOpts(ctypes.Structure):
                 ("max_active", ctypes.c_uint32)]
 
 
+N_OPC = 16
+OPC_NAMES = ["conv1_fwd", "conv2_fwd", "fc1_fwd", "head", "fc1_dgrad", "fc1_wgrad", "conv2_dgrad", "conv2_wgrad",
+             "conv2_reduce", "conv1_wgrad", "conv1_reduce", "mlp_fc1_fwd", "mlp_head", "mlp_fc1_wgrad", "admit",
+             "fedavg"]
+
+
 class RoundOpts(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_float), ("seed", ctypes.c_uint32), ("round", ctypes.c_uint32),
-                ("shuffle", ctypes.c_int32)]
+                ("shuffle", ctypes.c_int32), ("time_ops", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class RoundStats(ctypes.Structure):
     _fields_ = [("round_ns", ctypes.c_uint64), ("iterations", ctypes.c_uint64), ("client_steps", ctypes.c_uint64),
-                ("kernel_launches", ctypes.c_uint64), ("flops", ctypes.c_uint64), ("loss_sum", ctypes.c_double)]
+                ("kernel_launches", ctypes.c_uint64), ("flops", ctypes.c_uint64), ("loss_sum", ctypes.c_double),
+                ("op_ns", ctypes.c_uint64 * N_OPC), ("op_launches", ctypes.c_uint64 * N_OPC),
+                ("op_flops", ctypes.c_uint64 * N_OPC), ("op_bytes", ctypes.c_uint64 * N_OPC)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {}
+        for k, _ in self._fields_:
+            v = getattr(self, k)
+            d[k] = list(v) if k.startswith("op_") else v
+        return d
 
 
 SHARD_DT = np.dtype([("client_id", "<i8"), ("n", "<i8"), ("x", "<u8"), ("y", "<u8")], align=True)
@@ -200,9 +212,9 @@ def protea_plan(profiles, caps, policy=POLICY_PROFILED, order=ORDER_ASC_ID, marg
 
 
 def protea_run_round(ctx, clients, plan, global_in, global_out, lr=0.05, seed=0, rnd=0, shuffle=True,
-                     measured=False):
+                     measured=False, time_ops=0):
     """global_in / global_out: float32 torch tensors (cuda or cpu) or numpy arrays."""
-    o = RoundOpts(lr, seed, rnd, 1 if shuffle else 0)
+    o = RoundOpts(lr, seed, rnd, 1 if shuffle else 0, time_ops, 0)
     st = RoundStats()
     n_params = global_in.numel() if hasattr(global_in, "numel") else global_in.size
     meas = np.zeros(len(clients), dtype=PROFILE_DT) if measured else None

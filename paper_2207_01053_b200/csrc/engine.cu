@@ -90,7 +90,42 @@ struct protea_ctx {
   DevArray<double> wts;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint64_t launches = 0;
+  // per-op-class accounting of the current round (protea_round_stats)
+  uint32_t time_ops = 0;
+  std::vector<cudaEvent_t> evpool;
+  size_t evused = 0;
+  std::vector<int> ev_op;
+  uint64_t op_launches[PROTEA_N_OPC] = {}, op_flops[PROTEA_N_OPC] = {}, op_bytes[PROTEA_N_OPC] = {};
+  double loss_host = 0.0;
 };
+
+namespace {
+// Bracket one launch of op class `op` with CUDA events if requested.
+int op_begin(protea_ctx* ctx, int op) {
+  ctx->op_launches[op]++;
+  ctx->launches++;
+  if (!((ctx->time_ops >> op) & 1u)) return -1;
+  while (ctx->evused + 2 > ctx->evpool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    ctx->evpool.push_back(e);
+  }
+  const int i = (int)ctx->evused;
+  ctx->evused += 2;
+  ctx->ev_op.push_back(op);
+  cudaEventRecord(ctx->evpool[i], ctx->stream);
+  return i;
+}
+void op_end(protea_ctx* ctx, int i) {
+  if (i >= 0) cudaEventRecord(ctx->evpool[i + 1], ctx->stream);
+}
+void reset_ops(protea_ctx* ctx, uint32_t time_ops) {
+  ctx->time_ops = time_ops;
+  ctx->evused = 0;
+  ctx->ev_op.clear();
+  for (int i = 0; i < PROTEA_N_OPC; ++i) ctx->op_launches[i] = ctx->op_flops[i] = ctx->op_bytes[i] = 0;
+}
+}  // namespace
 
 #define CK(call)                                                                               \
   do {                                                                                         \
@@ -157,6 +192,33 @@ std::vector<int> ops_of(const ModelDims& m) {
   return {};
 }
 
+// Algorithmic work of one op for one client-step of `r` rows: FLOPs = 2 x useful
+// MACs; bytes = compulsory HBM traffic (every operand read once, every result
+// written once; weights fp32, activations e bytes).  DESIGN.md "Roofline".
+void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, uint64_t* by) {
+  const uint64_t c1 = m.c1, c2 = m.c2, f = m.f, C = m.classes;
+  const uint64_t s1 = cdiv((int)(r * 1024), kWgradChunkPx), s2 = cdiv((int)(r * 256), kWgradChunkPx);
+  uint64_t F = 0, B = 0;
+  switch (op) {
+    case OP_C1F: F = 2 * r * 1024 * c1 * 75; B = r * 3072 + 4 * c1 * 76 + r * 256 * c1 * (e + 1); break;
+    case OP_C2F: F = 2 * r * 256 * c2 * 25 * c1; B = r * 256 * c1 * e + 4 * c2 * (25 * c1 + 1) + r * 64 * c2 * (e + 1); break;
+    case OP_F1F: F = 2 * r * f * 64 * c2; B = r * 64 * c2 * e + 4 * f * (64 * c2 + 1) + r * f * e; break;
+    case OP_HEAD: F = 3 * 2 * r * C * f; B = r * f * e + 8 * C * (f + 1) + r * f * 4 + r * 4; break;
+    case OP_F1D: F = 2 * r * 64 * c2 * f; B = r * f * 4 + 4 * f * 64 * c2 + r * 64 * c2 * (e + 1) + r * 256 * c2 * e; break;
+    case OP_F1W: F = 2 * r * f * 64 * c2; B = r * f * 4 + r * 64 * c2 * e + 8 * f * (64 * c2 + 1); break;
+    case OP_C2D: F = 2 * r * 256 * c1 * 25 * c2; B = r * 256 * c2 * e + 4 * c2 * 25 * c1 + r * 256 * c1 * (e + 1) + r * 1024 * c1 * e; break;
+    case OP_C2W: F = 2 * r * 256 * c2 * 25 * c1; B = r * 256 * c2 * e + r * 256 * c1 * e + 4 * s2 * c2 * (25 * c1 + 1); break;
+    case OP_C2R: F = 0; B = 4 * s2 * c2 * (25 * c1 + 1) + 8 * c2 * (25 * c1 + 1); break;
+    case OP_C1W: F = 2 * r * 1024 * c1 * 75; B = r * 1024 * c1 * e + r * 3072 + 4 * s1 * c1 * 76; break;
+    case OP_C1R: F = 0; B = 4 * s1 * c1 * 76 + 8 * c1 * 76; break;
+    case OP_MF: F = 2 * r * 64 * 784; B = r * 784 + 4 * 64 * 785 + r * 64 * e; break;
+    case OP_MHEAD: F = 3 * 2 * r * C * 64; B = r * 64 * e + 8 * C * 65 + r * 64 * 4 + r * 4; break;
+    case OP_MW: F = 2 * r * 64 * 784; B = r * 64 * 4 + r * 784 + 8 * 64 * 785; break;
+  }
+  *fl = F;
+  *by = B;
+}
+
 CnnDims cnn_dims(const ModelDims& m) {
   CnnDims d;
   d.c1 = m.c1;
@@ -197,8 +259,9 @@ template <class OpT, int BM, int BN>
 void launch_gemm(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, const int32_t* dtab) {
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int* prefix = dtab + L.prefix_off[opid];
+  const int ev = op_begin(ctx, opid);
   k_gemm_simt<BM, BN, OpT><<<L.grid[opid], (BM / 4) * (BN / 4), 0, ctx->stream>>>(op, tasks, prefix, L.ntask);
-  ctx->launches++;
+  op_end(ctx, ev);
 }
 
 template <typename T>
@@ -211,27 +274,31 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Conv2Fwd<T, C2F_BM, C2F_BN>, C2F_BM, C2F_BN>(ctx, {drecs, d}, L, OP_C2F, dtab);
     launch_gemm<Fc1Fwd<T, F1F_BM, F1F_BN>, F1F_BM, F1F_BN>(ctx, {drecs, d}, L, OP_F1F, dtab);
     HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, lr};
+    int ev = op_begin(ctx, OP_HEAD);
     k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
-    ctx->launches++;
+    op_end(ctx, ev);
     launch_gemm<Fc1Dgrad<T, F1D_BM, F1D_BN>, F1D_BM, F1D_BN>(ctx, {drecs, d}, L, OP_F1D, dtab);
     launch_gemm<Fc1Wgrad<T, F1W_BM, F1W_BN>, F1W_BM, F1W_BN>(ctx, {drecs, d, lr}, L, OP_F1W, dtab);
     launch_gemm<Conv2Dgrad<T, C2D_BM, C2D_BN>, C2D_BM, C2D_BN>(ctx, {drecs, d}, L, OP_C2D, dtab);
     launch_gemm<Conv2Wgrad<T, C2W_BM, C2W_BN>, C2W_BM, C2W_BN>(ctx, {drecs, d}, L, OP_C2W, dtab);
     ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr};
+    ev = op_begin(ctx, OP_C2R);
     k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->stream>>>(r2, tasks, dtab + L.prefix_off[OP_C2R],
                                                                        L.ntask);
-    ctx->launches++;
+    op_end(ctx, ev);
     launch_gemm<Conv1Wgrad<T, C1W_BM, C1W_BN>, C1W_BM, C1W_BN>(ctx, {drecs, d}, L, OP_C1W, dtab);
     ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr};
+    ev = op_begin(ctx, OP_C1R);
     k_reduce_update<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->stream>>>(r1, tasks, dtab + L.prefix_off[OP_C1R],
                                                                        L.ntask);
-    ctx->launches++;
+    op_end(ctx, ev);
   } else if (m.arch == PROTEA_MODEL_MLP) {
     const MlpDims d = mlp_dims(m);
     launch_gemm<MlpFc1Fwd<T, MF_BM, MF_BN>, MF_BM, MF_BN>(ctx, {drecs, d}, L, OP_MF, dtab);
     HeadArgs ha{drecs, B_H1, B_DZ1, 64, m.classes, d.w2, d.b2, lr};
+    const int ev = op_begin(ctx, OP_MHEAD);
     k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
-    ctx->launches++;
+    op_end(ctx, ev);
     launch_gemm<MlpFc1Wgrad<T, MW_BM, MW_BN>, MW_BM, MW_BN>(ctx, {drecs, d, lr}, L, OP_MW, dtab);
   }
 }
@@ -319,6 +386,7 @@ void protea_finalize(protea_ctx* ctx) {
   ctx->tab.release();
   ctx->ptrs.release();
   ctx->wts.release();
+  for (auto e : ctx->evpool) cudaEventDestroy(e);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
@@ -357,15 +425,19 @@ protea_status protea_register_shards(protea_ctx* ctx, const protea_shard* shards
   for (size_t i = 0; i < n; ++i) {
     const protea_shard& s = shards[i];
     auto it = ctx->shards.find(s.client_id);
-    if (it != ctx->shards.end()) {
-      cudaFree(it->second.x);
-      cudaFree(it->second.y);
-      ctx->shards.erase(it);
-    }
     ShardDev d;
-    d.n = s.n;
-    CK(cudaMalloc(&d.x, (size_t)s.n * D));
-    CK(cudaMalloc(&d.y, (size_t)s.n * 4));
+    if (it != ctx->shards.end() && it->second.n == s.n) {
+      d = it->second;  // same size: refresh the device copy in place
+    } else {
+      if (it != ctx->shards.end()) {
+        cudaFree(it->second.x);
+        cudaFree(it->second.y);
+        ctx->shards.erase(it);
+      }
+      d.n = s.n;
+      CK(cudaMalloc(&d.x, (size_t)s.n * D));
+      CK(cudaMalloc(&d.y, (size_t)s.n * 4));
+    }
     CK(cudaMemcpyAsync(d.x, s.x, (size_t)s.n * D, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(d.y, s.y, (size_t)s.n * 4, cudaMemcpyHostToDevice, ctx->stream));
     ctx->shards[s.client_id] = d;
@@ -416,7 +488,7 @@ struct RunClient {
 // acc: device fp64 accumulator (zeroed by caller) or nullptr (probe mode:
 // no FedAvg terms).  Returns iterations run.
 protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* wg, double* acc, float lr,
-                      uint32_t seed, uint32_t round, int shuffle, uint64_t* iters_out) {
+                      uint32_t seed, uint32_t round, int shuffle, uint64_t* iters_out, double* loss_dev) {
   const int e = ctx->precision == PROTEA_PREC_FP32 ? 4 : 2;
   const int G = (int)ctx->groups.size();
   // ---- device records
@@ -492,6 +564,10 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
           for (size_t i = 0; i < act.size(); ++i) {
             tab.push_back(acc_t);
             acc_t += tiles(m, op, rows[i]);
+            uint64_t fl, by;
+            op_work(m, op, (uint64_t)rows[i], (uint64_t)e, &fl, &by);
+            ctx->op_flops[op] += fl;
+            ctx->op_bytes[op] += by;
           }
           tab.push_back(acc_t);
           L.grid[op] = acc_t;
@@ -527,11 +603,15 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
           maxP = std::max<int64_t>(maxP, ctx->groups[c.group].m.P);
           maxn = std::max<int64_t>(maxn, c.n);
         }
+      for (auto& c : rc)
+        if (c.admit == t) ctx->op_bytes[PROTEA_OPC_ADMIT] += 8 * (uint64_t)ctx->groups[c.group].m.P + 4 * (uint64_t)c.E * c.n;
+      int ev = op_begin(ctx, PROTEA_OPC_ADMIT);
       k_admit_params<<<dim3(grid_for(maxP / 4 + 1, 256, 64), admits[t].second), 256, 0, ctx->stream>>>(drecs, ids);
-      ctx->launches++;
+      op_end(ctx, ev);
+      ev = op_begin(ctx, PROTEA_OPC_ADMIT);
       k_admit_perm<<<dim3(cdiv((int)maxn, kPermThreads), admits[t].second, maxE), kPermThreads, 0, ctx->stream>>>(
           drecs, ids, seed, round, shuffle);
-      ctx->launches++;
+      op_end(ctx, ev);
     }
     for (int li : launch_idx[t]) {
       const Launch& L = launches[li];
@@ -545,9 +625,11 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
       for (int g = 0; g < G; ++g)
         if (rel_by_group[t][g].second > 0) {
           const int64_t P = ctx->groups[g].m.P;
+          ctx->op_bytes[PROTEA_OPC_FEDAVG] += (uint64_t)P * (20 + 4 * rel_by_group[t][g].second);
+          const int ev = op_begin(ctx, PROTEA_OPC_FEDAVG);
           k_release_acc<<<grid_for(P, 256), 256, 0, ctx->stream>>>(drecs, dtab + rel_by_group[t][g].first,
-                                                                    rel_by_group[t][g].second, P);
-          ctx->launches++;
+                                                                    rel_by_group[t][g].second, P, loss_dev);
+          op_end(ctx, ev);
         }
   }
   CK(cudaGetLastError());
@@ -649,11 +731,14 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
     CK(cudaMemcpyAsync(ctx->gin.p, global_in, Ptot * 4, cudaMemcpyDeviceToDevice, ctx->stream));
     wg = ctx->gin.p;
   }
-  CK(ctx->acc.reserve(Ptot));
-  CK(cudaMemsetAsync(ctx->acc.p, 0, Ptot * 8, ctx->stream));
+  CK(ctx->acc.reserve(Ptot + 1));
+  CK(cudaMemsetAsync(ctx->acc.p, 0, (Ptot + 1) * 8, ctx->stream));
+  reset_ops(ctx, opts->time_ops);
   const uint64_t l0 = ctx->launches;
   uint64_t iters = 0;
-  protea_status st = execute(ctx, all, wg, ctx->acc.p, opts->lr, opts->seed, opts->round, opts->shuffle, &iters);
+  double* loss_dev = ctx->acc.p + Ptot;  // one extra fp64 after the accumulators: sum of step losses
+  protea_status st =
+      execute(ctx, all, wg, ctx->acc.p, opts->lr, opts->seed, opts->round, opts->shuffle, &iters, loss_dev);
   if (st != PROTEA_OK) return st;
   if (ctx->world > 1) {
     ncclResult_t r = ncclAllReduce(ctx->acc.p, ctx->acc.p, Ptot, ncclDouble, ncclSum, ctx->comm, ctx->stream);
@@ -667,14 +752,18 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
   for (size_t g = 0; g < ctx->groups.size(); ++g) {
     const Group& gr = ctx->groups[g];
     if (Ngroup[g] > 0) {
+      ctx->op_bytes[PROTEA_OPC_FEDAVG] += 16 * (uint64_t)gr.m.P;
+      const int ev = op_begin(ctx, PROTEA_OPC_FEDAVG);
       k_finalize<<<grid_for(gr.m.P, 256), 256, 0, ctx->stream>>>(wg + gr.offset, ctx->acc.p + gr.offset,
                                                                  (double)Ngroup[g], out + gr.offset, gr.m.P);
-      ctx->launches++;
+      op_end(ctx, ev);
     } else if (out + gr.offset != wg + gr.offset) {
       CK(cudaMemcpyAsync(out + gr.offset, wg + gr.offset, gr.m.P * 4, cudaMemcpyDeviceToDevice, ctx->stream));
     }
   }
   if (!out_dev) CK(cudaMemcpyAsync(global_out, out, Ptot * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  double loss_sum = 0.0;
+  CK(cudaMemcpyAsync(&loss_sum, loss_dev, 8, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   float ms = 0.f;
@@ -684,6 +773,17 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
     stats->round_ns = (uint64_t)(ms * 1e6);
     stats->iterations = iters;
     stats->kernel_launches = ctx->launches - l0;
+    stats->loss_sum = loss_sum;
+    for (int i = 0; i < PROTEA_N_OPC; ++i) {
+      stats->op_launches[i] = ctx->op_launches[i];
+      stats->op_flops[i] = ctx->op_flops[i];
+      stats->op_bytes[i] = ctx->op_bytes[i];
+    }
+    for (size_t k = 0; k < ctx->ev_op.size(); ++k) {
+      float ems = 0.f;
+      CK(cudaEventElapsedTime(&ems, ctx->evpool[2 * k], ctx->evpool[2 * k + 1]));
+      stats->op_ns[ctx->ev_op[k]] += (uint64_t)((double)ems * 1e6);
+    }
     for (auto& c : all) {
       stats->client_steps += c.S;
       stats->flops += (uint64_t)c.E * c.n * flops_per_sample(ctx->groups[c.group].m);
@@ -744,13 +844,14 @@ protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clien
                                            " B exceeds the arena");
     CK(ctx->gin.reserve(gr.m.P));
     CK(cudaMemsetAsync(ctx->gin.p, 0, gr.m.P * 4, ctx->stream));
+    reset_ops(ctx, 0);
     std::vector<float> times;
     for (int rep = 0; rep < 7; ++rep) {
       std::vector<RunClient> one{r};
       // gin holds zero weights at offset 0; shift so that wg + group offset == gin
       const float* wg = ctx->gin.p - gr.offset;
       CK(cudaEventRecord(ctx->ev0, ctx->stream));
-      protea_status st = execute(ctx, one, wg, nullptr, 0.0f, 0, 0, 0, nullptr);
+      protea_status st = execute(ctx, one, wg, nullptr, 0.0f, 0, 0, 0, nullptr, nullptr);
       if (st != PROTEA_OK) return st;
       CK(cudaEventRecord(ctx->ev1, ctx->stream));
       CK(cudaEventSynchronize(ctx->ev1));

@@ -56,7 +56,10 @@ __global__ void __launch_bounds__(kPermThreads)
 // Release (P:209 stage (4) "resources get freed") + FedAvg partial:
 // acc[d] += n_k * (w_k[d] - w_g[d]) in fp64, clients in the given (ascending
 // id) order, so the per-element summation order is fixed.
-__global__ void k_release_acc(const ClientRec* __restrict__ recs, const int* __restrict__ ids, int nrel, int64_t P) {
+__global__ void k_release_acc(const ClientRec* __restrict__ recs, const int* __restrict__ ids, int nrel, int64_t P,
+                              double* __restrict__ loss) {
+  if (loss && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int i = 0; i < nrel; ++i) *loss += (double)recs[ids[i]].stats[0];
   for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < P; d += (int64_t)gridDim.x * blockDim.x) {
     const ClientRec* c0 = recs + ids[0];
     double a = c0->acc[d];
