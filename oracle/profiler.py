@@ -83,7 +83,8 @@ def conv_layers(model, width_q=4):
 def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
     """[(buffer, bytes)] of one client's arena slot.
 
-    elem_bytes = 4 in fp32-verify mode, 2 in bf16 mode (activation storage).
+    elem_bytes = 4 in fp32-verify mode, 2 in bf16 mode (activation storage; in
+    bf16 mode the slot also holds a bf16 shadow copy of the weights).
     wsp = split-K partials of the conv weight gradients: each conv layer's
     reduction over b*Hout*Wout pixels is cut into ceil(b*Hout*Wout / 2048)
     splits, each holding cout*(K+1) fp32 partials (the +1 is the bias column).
@@ -91,13 +92,15 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
     b, e = batch, elem_bytes
     P = n_params(model, width_q, classes)
     out = [("params", 4 * P), ("perm", 4 * epochs * n), ("stats", 64)]
+    if e == 2:
+        out.append(("wsh", 2 * P))  # bf16 shadow weights read by the tensor-core GEMMs
     if model == MLP:
-        out += [("h1", b * 64 * e), ("dz1", b * 64 * 4)]
+        out += [("h1", b * 64 * e), ("dz1", b * 64 * e)]
     elif model == CNN:
         c1, c2, f = cnn_channels(width_q)
         out += [("a1", b * 256 * c1 * e), ("i1", b * 256 * c1),
                 ("a2", b * 64 * c2 * e), ("i2", b * 64 * c2),
-                ("h", b * f * e), ("dh", b * f * 4),
+                ("h", b * f * e), ("dh", b * f * e),
                 ("dz2", b * 256 * c2 * e), ("dz1", b * 1024 * c1 * e)]
     elif model == RESNET8:
         out += [("a0", b * 1024 * 16 * e),

@@ -29,7 +29,8 @@ POLICY_PROFILED, POLICY_STATIC = 0, 1
 ORDER_ASC_ID, ORDER_DESC_STEPS = 0, 1
 
 EXPORTS = ["protea_init", "protea_finalize", "protea_last_error", "protea_register_model", "protea_register_shards",
-           "protea_profile_clients", "protea_plan", "protea_run_round", "protea_fedavg", "protea_client_footprint"]
+           "protea_profile_clients", "protea_plan", "protea_run_round", "protea_fedavg", "protea_client_footprint",
+           "protea_selftest_gemm"]
 
 
 class ProteaError(RuntimeError):
@@ -114,6 +115,7 @@ _lib.protea_fedavg.argtypes = [_vp, _vp, _vp, _sz, _sz, _vp]
 _lib.protea_client_footprint.argtypes = [ctypes.POINTER(ModelDesc), ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                          ctypes.c_int32, ctypes.POINTER(ctypes.c_uint64),
                                          ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+_lib.protea_selftest_gemm.argtypes = [_vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
 for _f in EXPORTS:
     if _f not in ("protea_finalize", "protea_last_error"):
         getattr(_lib, _f).restype = ctypes.c_int
@@ -239,3 +241,8 @@ def protea_client_footprint(arch, width_q, classes, H, W, C, n, batch, epochs, p
     _check(_lib.protea_client_footprint(ctypes.byref(d), n, batch, epochs, precision, ctypes.byref(pb),
                                         ctypes.byref(st), ctypes.byref(fl)))
     return pb.value, st.value, fl.value
+
+
+def protea_selftest_gemm(A, B, D, M, N, K, mn_major=False):
+    """include/protea_selftest.h: D = A B^T on the library's tcgen05 core (device tensors)."""
+    _check(_lib.protea_selftest_gemm(A.data_ptr(), B.data_ptr(), D.data_ptr(), M, N, K, 1 if mn_major else 0))

@@ -45,7 +45,7 @@ uint64_t flops_per_sample(const ModelDims& m);
 
 // Named buffers of one client's slot, in slot order.
 enum Buf : int {
-  B_PARAMS = 0, B_PERM, B_STATS,
+  B_PARAMS = 0, B_PERM, B_STATS, B_WSH,
   // MLP
   B_H1, B_DZ1,
   // CNN

@@ -28,6 +28,7 @@
 #include "device.cuh"
 #include "kernels_misc.cuh"
 #include "kernels_simt.cuh"
+#include "kernels_tc.cuh"
 
 namespace protea {
 
@@ -165,14 +166,27 @@ enum Op : int {
   OP_MF, OP_MHEAD, OP_MW, OP_COUNT
 };
 
-int tiles(const ModelDims& m, int op, int rows) {
+// tensor-core tile shapes (bf16 mode): M tile = 128, BN per op, STAGES-deep ring
+constexpr int TC_C2F_BN = 64, TC_C2D_BN = 32, TC_C2W_BN = 64, TC_F1F_BN = 64, TC_F1D_BN = 64, TC_F1W_BN = 256;
+constexpr int TC_STAGES = 4, TC_F1W_STAGES = 2;
+
+int tiles(const ModelDims& m, int op, int rows, bool tc) {
+  if (tc) switch (op) {
+      case OP_C2F: return rows * 2;
+      case OP_F1F: return m.f / 128;
+      case OP_F1D: return 64 * m.c2 / 128;
+      case OP_F1W: return (64 * m.c2 / 128) * cdiv(m.f, 256);
+      case OP_C2D: return rows * 2;
+      case OP_C2W: return cdiv(25 * m.c1 + 1, 128);
+      default: break;
+    }
   switch (op) {
     case OP_C1F: return cdiv(rows * 1024, C1F_BM) * cdiv(m.c1, C1F_BN);
     case OP_C2F: return cdiv(rows * 256, C2F_BM) * cdiv(m.c2, C2F_BN);
     case OP_F1F: return cdiv(rows, F1F_BM) * cdiv(m.f, F1F_BN);
     case OP_HEAD: return 1;
     case OP_F1D: return cdiv(rows, F1D_BM) * cdiv(64 * m.c2, F1D_BN);
-    case OP_F1W: return cdiv(m.f, F1W_BM) * cdiv(64 * m.c2 + 1, F1W_BN);
+    case OP_F1W: return cdiv(m.f, F1W_BM) * cdiv(64 * m.c2, F1W_BN);
     case OP_C2D: return cdiv(rows * 256, C2D_BM) * cdiv(m.c1, C2D_BN);
     case OP_C2W: return cdiv(rows * 256, kWgradChunkPx) * cdiv(m.c2, C2W_BM) * cdiv(25 * m.c1 + 1, C2W_BN);
     case OP_C2R: return cdiv(m.c2 * (25 * m.c1 + 1), kReduceBlock);
@@ -180,12 +194,14 @@ int tiles(const ModelDims& m, int op, int rows) {
     case OP_C1R: return cdiv(m.c1 * 76, kReduceBlock);
     case OP_MF: return cdiv(rows, MF_BM) * cdiv(64, MF_BN);
     case OP_MHEAD: return 1;
-    case OP_MW: return cdiv(64, MW_BM) * cdiv(785, MW_BN);
+    case OP_MW: return cdiv(64, MW_BM) * cdiv(784, MW_BN);
   }
   return 0;
 }
 
-std::vector<int> ops_of(const ModelDims& m) {
+std::vector<int> ops_of(const ModelDims& m, bool tc) {
+  if (m.arch == PROTEA_MODEL_CNN && tc)
+    return {OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_CNN)
     return {OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_MLP) return {OP_MF, OP_MHEAD, OP_MW};
@@ -201,19 +217,19 @@ void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, u
   uint64_t F = 0, B = 0;
   switch (op) {
     case OP_C1F: F = 2 * r * 1024 * c1 * 75; B = r * 3072 + 4 * c1 * 76 + r * 256 * c1 * (e + 1); break;
-    case OP_C2F: F = 2 * r * 256 * c2 * 25 * c1; B = r * 256 * c1 * e + 4 * c2 * (25 * c1 + 1) + r * 64 * c2 * (e + 1); break;
-    case OP_F1F: F = 2 * r * f * 64 * c2; B = r * 64 * c2 * e + 4 * f * (64 * c2 + 1) + r * f * e; break;
-    case OP_HEAD: F = 3 * 2 * r * C * f; B = r * f * e + 8 * C * (f + 1) + r * f * 4 + r * 4; break;
-    case OP_F1D: F = 2 * r * 64 * c2 * f; B = r * f * 4 + 4 * f * 64 * c2 + r * 64 * c2 * (e + 1) + r * 256 * c2 * e; break;
-    case OP_F1W: F = 2 * r * f * 64 * c2; B = r * f * 4 + r * 64 * c2 * e + 8 * f * (64 * c2 + 1); break;
-    case OP_C2D: F = 2 * r * 256 * c1 * 25 * c2; B = r * 256 * c2 * e + 4 * c2 * 25 * c1 + r * 256 * c1 * (e + 1) + r * 1024 * c1 * e; break;
-    case OP_C2W: F = 2 * r * 256 * c2 * 25 * c1; B = r * 256 * c2 * e + r * 256 * c1 * e + 4 * s2 * c2 * (25 * c1 + 1); break;
+    case OP_C2F: F = 2 * r * 256 * c2 * 25 * c1; B = r * 256 * c1 * e + e * c2 * 25 * c1 + 4 * c2 + r * 64 * c2 * (e + 1); break;
+    case OP_F1F: F = 2 * r * f * 64 * c2; B = r * 64 * c2 * e + e * f * 64 * c2 + 4 * f + r * f * e; break;
+    case OP_HEAD: F = 3 * 2 * r * C * f; B = r * f * e + 8 * C * (f + 1) + r * f * e + 8 * f + r * 4; break;
+    case OP_F1D: F = 2 * r * 64 * c2 * f; B = r * f * e + e * f * 64 * c2 + r * 64 * c2 * (e + 1) + r * 256 * c2 * e; break;
+    case OP_F1W: F = 2 * r * f * 64 * c2; B = r * f * e + r * 64 * c2 * e + (8 + (e == 2 ? 2 : 0)) * f * 64 * c2; break;
+    case OP_C2D: F = 2 * r * 256 * c1 * 25 * c2; B = r * 256 * c2 * e + e * c2 * 25 * c1 + r * 256 * c1 * (e + 1) + r * 1024 * c1 * e; break;
+    case OP_C2W: F = 2 * r * 256 * c2 * 25 * c1; B = r * 256 * c2 * e + r * 256 * c1 * e + (e == 2 ? 10 * c2 * (25 * c1 + 1) : 4 * s2 * c2 * (25 * c1 + 1)); break;
     case OP_C2R: F = 0; B = 4 * s2 * c2 * (25 * c1 + 1) + 8 * c2 * (25 * c1 + 1); break;
     case OP_C1W: F = 2 * r * 1024 * c1 * 75; B = r * 1024 * c1 * e + r * 3072 + 4 * s1 * c1 * 76; break;
     case OP_C1R: F = 0; B = 4 * s1 * c1 * 76 + 8 * c1 * 76; break;
     case OP_MF: F = 2 * r * 64 * 784; B = r * 784 + 4 * 64 * 785 + r * 64 * e; break;
-    case OP_MHEAD: F = 3 * 2 * r * C * 64; B = r * 64 * e + 8 * C * 65 + r * 64 * 4 + r * 4; break;
-    case OP_MW: F = 2 * r * 64 * 784; B = r * 64 * 4 + r * 784 + 8 * 64 * 785; break;
+    case OP_MHEAD: F = 3 * 2 * r * C * 64; B = r * 64 * e + 8 * C * 65 + r * 64 * e + 8 * 64 + r * 4; break;
+    case OP_MW: F = 2 * r * 64 * 784; B = r * 64 * e + r * 784 + 8 * 64 * 784; break;
   }
   *fl = F;
   *by = B;
@@ -264,6 +280,45 @@ void launch_gemm(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, cons
   op_end(ctx, ev);
 }
 
+template <int BN, int STAGES, class OpT>
+void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, const int32_t* dtab) {
+  constexpr int SMEM = tc_smem_bytes<BN, STAGES>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, OpT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const int* prefix = dtab + L.prefix_off[opid];
+  const int ev = op_begin(ctx, opid);
+  k_gemm_tc<BN, STAGES, OpT><<<L.grid[opid], kTcThreads, SMEM, ctx->stream>>>(op, tasks, prefix, L.ntask);
+  op_end(ctx, ev);
+}
+
+// bf16 mode, CNN: conv2 and fc1 (fwd / dgrad / wgrad) on tcgen05; conv1 and the head on SIMT
+void launch_step_tc(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const int32_t* dtab,
+                    float lr) {
+  typedef __nv_bfloat16 T;
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const CnnDims d = cnn_dims(m);
+  launch_gemm<Conv1Fwd<T, C1F_BM, C1F_BN>, C1F_BM, C1F_BN>(ctx, {drecs, d}, L, OP_C1F, dtab);
+  launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TcConv2Fwd{drecs, d}, L, OP_C2F, dtab);
+  launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, TcFc1Fwd{drecs, d}, L, OP_F1F, dtab);
+  HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
+  int ev = op_begin(ctx, OP_HEAD);
+  k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
+  op_end(ctx, ev);
+  launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, TcFc1Dgrad{drecs, d}, L, OP_F1D, dtab);
+  launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad{drecs, d, lr}, L, OP_F1W, dtab);
+  launch_gemm_tc<TC_C2D_BN, TC_STAGES>(ctx, TcConv2Dgrad{drecs, d}, L, OP_C2D, dtab);
+  launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, TcConv2Wgrad{drecs, d, lr}, L, OP_C2W, dtab);
+  launch_gemm<Conv1Wgrad<T, C1W_BM, C1W_BN>, C1W_BM, C1W_BN>(ctx, {drecs, d}, L, OP_C1W, dtab);
+  ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr};
+  ev = op_begin(ctx, OP_C1R);
+  k_reduce_update<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->stream>>>(r1, tasks, dtab + L.prefix_off[OP_C1R], L.ntask);
+  op_end(ctx, ev);
+}
+
 template <typename T>
 void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const int32_t* dtab,
                  float lr) {
@@ -273,7 +328,7 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Conv1Fwd<T, C1F_BM, C1F_BN>, C1F_BM, C1F_BN>(ctx, {drecs, d}, L, OP_C1F, dtab);
     launch_gemm<Conv2Fwd<T, C2F_BM, C2F_BN>, C2F_BM, C2F_BN>(ctx, {drecs, d}, L, OP_C2F, dtab);
     launch_gemm<Fc1Fwd<T, F1F_BM, F1F_BN>, F1F_BM, F1F_BN>(ctx, {drecs, d}, L, OP_F1F, dtab);
-    HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, lr};
+    HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
     int ev = op_begin(ctx, OP_HEAD);
     k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
     op_end(ctx, ev);
@@ -295,7 +350,7 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
   } else if (m.arch == PROTEA_MODEL_MLP) {
     const MlpDims d = mlp_dims(m);
     launch_gemm<MlpFc1Fwd<T, MF_BM, MF_BN>, MF_BM, MF_BN>(ctx, {drecs, d}, L, OP_MF, dtab);
-    HeadArgs ha{drecs, B_H1, B_DZ1, 64, m.classes, d.w2, d.b2, lr};
+    HeadArgs ha{drecs, B_H1, B_DZ1, 64, m.classes, d.w2, d.b2, d.b1, lr};
     const int ev = op_begin(ctx, OP_MHEAD);
     k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
     op_end(ctx, ev);
@@ -490,6 +545,7 @@ struct RunClient {
 protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* wg, double* acc, float lr,
                       uint32_t seed, uint32_t round, int shuffle, uint64_t* iters_out, double* loss_dev) {
   const int e = ctx->precision == PROTEA_PREC_FP32 ? 4 : 2;
+  const bool tc_mode = e == 2;  // bf16 mode: tensor-core GEMMs for the CNN
   const int G = (int)ctx->groups.size();
   // ---- device records
   std::vector<ClientRec> recs(rc.size());
@@ -558,12 +614,12 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
           tab.push_back(rows[i]);
           tab.push_back((int32_t)((int64_t)ep * c.n + (int64_t)j * c.B));
         }
-        for (int op : ops_of(m)) {
+        for (int op : ops_of(m, tc_mode)) {
           L.prefix_off[op] = (int64_t)tab.size();
           int acc_t = 0;
           for (size_t i = 0; i < act.size(); ++i) {
             tab.push_back(acc_t);
-            acc_t += tiles(m, op, rows[i]);
+            acc_t += tiles(m, op, rows[i], tc_mode);
             uint64_t fl, by;
             op_work(m, op, (uint64_t)rows[i], (uint64_t)e, &fl, &by);
             ctx->op_flops[op] += fl;
@@ -618,6 +674,8 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
       const ModelDims& m = ctx->groups[L.group].m;
       if (e == 4)
         launch_step<float>(ctx, m, L, drecs, dtab, lr);
+      else if (m.arch == PROTEA_MODEL_CNN)
+        launch_step_tc(ctx, m, L, drecs, dtab, lr);
       else
         launch_step<__nv_bfloat16>(ctx, m, L, drecs, dtab, lr);
     }
@@ -907,3 +965,36 @@ protea_status protea_fedavg(protea_ctx* ctx, const float* const* params, const i
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// include/protea_selftest.h
+// ---------------------------------------------------------------------------
+extern "C" protea_status protea_selftest_gemm(const void* A, const void* B, float* D, int32_t M, int32_t N,
+                                              int32_t K, int32_t mn_major) {
+  if (!A || !B || !D || M <= 0 || M % 128 || N <= 0 || N > 64 || K <= 0 || K % 64) {
+    set_global_error("selftest_gemm: need M % 128 == 0, 0 < N <= 64, K % 64 == 0, non-null pointers");
+    return PROTEA_ERR_INVALID;
+  }
+  int h[2 + 4] = {0, M / 128, 0, 0, 1, 0};  // prefix[0..1], task {rec, step, rows, base}
+  int* dtab = nullptr;
+  if (cudaMalloc(&dtab, sizeof(h)) != cudaSuccess) return PROTEA_ERR_CUDA;
+  cudaMemcpy(dtab, h, sizeof(h), cudaMemcpyHostToDevice);
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + 2);
+  constexpr int SMEM = tc_smem_bytes<64, 4>();
+  if (mn_major) {
+    TcDenseMN op{nullptr, (const bf16*)A, (const bf16*)B, D, M, N, K};
+    cudaFuncSetAttribute(k_gemm_tc<64, 4, TcDenseMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    k_gemm_tc<64, 4, TcDenseMN><<<M / 128, kTcThreads, SMEM>>>(op, tasks, dtab, 1);
+  } else {
+    TcDense op{nullptr, (const bf16*)A, (const bf16*)B, D, M, N, K};
+    cudaFuncSetAttribute(k_gemm_tc<64, 4, TcDense>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    k_gemm_tc<64, 4, TcDense><<<M / 128, kTcThreads, SMEM>>>(op, tasks, dtab, 1);
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaFree(dtab);
+  if (e != cudaSuccess) {
+    set_global_error(std::string("selftest_gemm: ") + cudaGetErrorString(e));
+    return PROTEA_ERR_CUDA;
+  }
+  return PROTEA_OK;
+}

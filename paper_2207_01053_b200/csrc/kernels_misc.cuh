@@ -11,8 +11,12 @@ __global__ void k_admit_params(const ClientRec* __restrict__ recs, const int* __
   const ClientRec* c = recs + ids[blockIdx.y];
   const int64_t P = c->P;
   // group offsets in the global vector need not be 16-byte aligned: scalar, coalesced
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x)
-    c->params[i] = c->wg[i];
+  __nv_bfloat16* sh = (__nv_bfloat16*)c->buf[B_WSH];  // bf16 mode: tensor-core shadow
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    const float w = c->wg[i];
+    c->params[i] = w;
+    if (sh) sh[i] = __float2bfloat16_rn(w);
+  }
   if (blockIdx.x == 0 && threadIdx.x < 16) c->stats[threadIdx.x] = 0.f;
 }
 

@@ -254,7 +254,7 @@ struct Fc1Dgrad {  // dA2 = dh W1: M = rows, N = 64*c2, K = f; epilogue: pool2 b
     t.ke = d.f;
   }
   __device__ float A(const GemmTile& t, int m, int k) const {
-    return ((const float*)t.c->buf[B_DH])[(int64_t)m * d.f + k];
+    return ldv((const T*)t.c->buf[B_DH] + (int64_t)m * d.f + k);
   }
   __device__ float B(const GemmTile& t, int k, int n) const {
     return t.c->params[d.w3 + (int64_t)k * 64 * d.c2 + n];
@@ -284,26 +284,25 @@ struct Fc1Dgrad {  // dA2 = dh W1: M = rows, N = 64*c2, K = f; epilogue: pool2 b
 };
 
 template <typename T, int BM, int BN>
-struct Fc1Wgrad {  // W1 -= lr dh^T a2: M = f, N = 64*c2 + 1 (bias), K = rows
+struct Fc1Wgrad {  // W1 -= lr dh^T a2: M = f, N = 64*c2, K = rows (fc1 bias: k_head)
   static constexpr bool A_KFAST = false, B_KFAST = false;
   const ClientRec* recs;
   CnnDims d;
   float lr;
   __device__ void setup(GemmTile& t, int local) const {
-    const int nt = cdiv(64 * d.c2 + 1, BN);
+    const int nt = cdiv(64 * d.c2, BN);
     t.M = d.f;
-    t.N = 64 * d.c2 + 1;
+    t.N = 64 * d.c2;
     t.m0 = (local / nt) * BM;
     t.n0 = (local % nt) * BN;
     t.kb = 0;
     t.ke = t.tk.rows;
   }
   __device__ float A(const GemmTile& t, int m, int k) const {
-    return ((const float*)t.c->buf[B_DH])[(int64_t)k * d.f + m];
+    return ldv((const T*)t.c->buf[B_DH] + (int64_t)k * d.f + m);
   }
   __device__ float B(const GemmTile& t, int k, int n) const {
-    const int K1 = 64 * d.c2;
-    return n < K1 ? ldv((const T*)t.c->buf[B_A2] + (int64_t)k * K1 + n) : 1.f;
+    return ldv((const T*)t.c->buf[B_A2] + (int64_t)k * 64 * d.c2 + n);
   }
   __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
     const int K1 = 64 * d.c2;
@@ -313,7 +312,7 @@ struct Fc1Wgrad {  // W1 -= lr dh^T a2: M = f, N = 64*c2 + 1 (bias), K = rows
       for (int j = 0; j < 4; ++j) {
         const int m = mb + i, n = nb + j;
         if (m >= t.M || n >= t.N) continue;
-        float* w = n < K1 ? t.c->params + d.w3 + (int64_t)m * K1 + n : t.c->params + d.b3 + m;
+        float* w = t.c->params + d.w3 + (int64_t)m * K1 + n;
         *w = *w - lr * acc[i][j];
       }
   }
@@ -515,25 +514,24 @@ struct MlpFc1Fwd {  // M = rows, N = 64, K = 784
 };
 
 template <typename T, int BM, int BN>
-struct MlpFc1Wgrad {  // M = 64, N = 785, K = rows
+struct MlpFc1Wgrad {  // M = 64, N = 784, K = rows (fc1 bias: k_head)
   static constexpr bool A_KFAST = false, B_KFAST = false;
   const ClientRec* recs;
   MlpDims d;
   float lr;
   __device__ void setup(GemmTile& t, int local) const {
-    const int nt = cdiv(785, BN);
+    const int nt = cdiv(784, BN);
     t.M = 64;
-    t.N = 785;
+    t.N = 784;
     t.m0 = (local / nt) * BM;
     t.n0 = (local % nt) * BN;
     t.kb = 0;
     t.ke = t.tk.rows;
   }
   __device__ float A(const GemmTile& t, int m, int k) const {
-    return ((const float*)t.c->buf[B_DZ1])[(int64_t)k * 64 + m];
+    return ldv((const T*)t.c->buf[B_DZ1] + (int64_t)k * 64 + m);
   }
   __device__ float B(const GemmTile& t, int k, int n) const {
-    if (n == 784) return 1.f;
     const int s = t.c->perm[t.tk.base + k];
     return px01(t.c->x[(int64_t)s * 784 + n]);
   }
@@ -544,7 +542,7 @@ struct MlpFc1Wgrad {  // M = 64, N = 785, K = rows
       for (int j = 0; j < 4; ++j) {
         const int m = mb + i, n = nb + j;
         if (m >= t.M || n >= t.N) continue;
-        float* w = n < 784 ? t.c->params + d.w1 + (int64_t)m * 784 + n : t.c->params + d.b1 + m;
+        float* w = t.c->params + d.w1 + (int64_t)m * 784 + n;
         *w = *w - lr * acc[i][j];
       }
   }
@@ -556,9 +554,10 @@ struct MlpFc1Wgrad {  // M = 64, N = 785, K = rows
 // --------------------------------------------------------------------------
 struct HeadArgs {
   const ClientRec* recs;
-  int hbuf, dhbuf;  // buffer ids of h (act) and dh (fp32)
+  int hbuf, dhbuf;  // buffer ids of h and dh (activation type T)
   int F, classes;
   int64_t w, b;     // fc2 offsets
+  int64_t b_prev;   // bias of the layer producing h: b_prev -= lr * sum_r dh[r]
   float lr;
 };
 constexpr int kHeadThreads = 256;
@@ -599,13 +598,20 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a, const Task* _
     }
   }
   __syncthreads();
-  // 3. dh = (dlogits W2) * (h > 0)   (old W2)
-  float* dh = (float*)c->buf[a.dhbuf];
-  for (int idx = threadIdx.x; idx < rows * F; idx += kHeadThreads) {
-    const int r = idx / F, f = idx - r * F;
-    float s = 0.f;
-    for (int cc = 0; cc < C; ++cc) s = fmaf(dlog[r * C + cc], W[(int64_t)cc * F + f], s);
-    dh[idx] = ldv(h + idx) > 0.f ? s : 0.f;
+  // 3. dh = (dlogits W2) * (h > 0)   (old W2); the previous layer's bias
+  //    gradient sum_r dh[r][f] is applied here (its SGD update, fused).
+  T* dh = (T*)c->buf[a.dhbuf];
+  float* bprev = c->params + a.b_prev;
+  for (int f = threadIdx.x; f < F; f += kHeadThreads) {
+    float gb = 0.f;
+    for (int r = 0; r < rows; ++r) {
+      float s = 0.f;
+      for (int cc = 0; cc < C; ++cc) s = fmaf(dlog[r * C + cc], W[(int64_t)cc * F + f], s);
+      s = ldv(h + (int64_t)r * F + f) > 0.f ? s : 0.f;
+      stv(dh + (int64_t)r * F + f, s);
+      gb += s;
+    }
+    bprev[f] -= a.lr * gb;
   }
   __syncthreads();
   // 4. W2 -= lr dlogits^T h ; b2 -= lr sum_r dlogits

@@ -118,17 +118,18 @@ SlotLayout slot_layout(const ModelDims& m, int b, int64_t n, int epochs, int e) 
   put(B_PARAMS, 4 * (uint64_t)m.P);
   put(B_PERM, 4 * (uint64_t)epochs * n);
   put(B_STATS, 64);
+  if (e == 2) put(B_WSH, 2 * (uint64_t)m.P);  // bf16 shadow of the weights (tensor-core operands)
   const uint64_t B = b;
   if (m.arch == PROTEA_MODEL_MLP) {
     put(B_H1, B * 64 * e);
-    put(B_DZ1, B * 64 * 4);
+    put(B_DZ1, B * 64 * e);
   } else if (m.arch == PROTEA_MODEL_CNN) {
     put(B_A1, B * 256 * m.c1 * e);
     put(B_I1, B * 256 * m.c1);
     put(B_A2, B * 64 * m.c2 * e);
     put(B_I2, B * 64 * m.c2);
     put(B_H, B * m.f * e);
-    put(B_DH, B * m.f * 4);
+    put(B_DH, B * m.f * e);
     put(B_DZ2, B * 256 * m.c2 * e);
     put(B_DZC1, B * 1024 * m.c1 * e);
   } else {

@@ -17,7 +17,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_library_exports_every_header_symbol():
-    hdr = open(os.path.join(ROOT, "include", "protea.h")).read()
+    import glob
+    hdr = "".join(open(f).read() for f in glob.glob(os.path.join(ROOT, "include", "*.h")))
     declared = set(re.findall(r"\b(protea_[a-z_0-9]+)\s*\(", hdr))
     assert declared == set(pb.EXPORTS)
     for name in declared:
