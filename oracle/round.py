@@ -19,20 +19,21 @@ from .sgd import local_sgd
 
 
 def _client_job(args):
-    (w0, model, width_q, classes, x, y, batch, epochs, lr, seed, rnd, cid, shuffle, max_steps) = args
+    (w0, model, width_q, classes, x, y, batch, epochs, lr, seed, rnd, cid, shuffle, max_steps, emul) = args
     w, losses = local_sgd(w0, model, width_q, classes, x, y, batch, epochs, lr, seed, rnd, cid,
-                          shuffle=shuffle, max_steps=max_steps)
+                          shuffle=shuffle, max_steps=max_steps, emulate_bf16=emul)
     return w, losses
 
 
-def run_round(clients, shards, global_w, lr, seed, rnd, shuffle=True, workers=0, return_clients=False):
+def run_round(clients, shards, global_w, lr, seed, rnd, shuffle=True, workers=0, return_clients=False,
+              emulate_bf16=False):
     """clients: objects with id, n, batch, epochs, model, width_q, classes.
     global_w: dict width_q -> float array.  Returns dict width_q -> float64 array."""
     jobs = []
     for c in clients:
         x, y = shards[c.id]
         jobs.append((global_w[c.width_q], c.model, c.width_q, c.classes, x, y, c.batch, c.epochs,
-                     lr, seed, rnd, c.id, shuffle, None))
+                     lr, seed, rnd, c.id, shuffle, None, emulate_bf16))
     if workers and workers > 1:
         with ProcessPoolExecutor(max_workers=workers) as ex:
             results = list(ex.map(_client_job, jobs))

@@ -185,38 +185,61 @@ def softmax_ce(z, y):
 # ---------------------------------------------------------------------------
 # per-model loss + gradient
 # ---------------------------------------------------------------------------
-def loss_and_grad(p, model, xb, yb):
-    """xb float64 [nb, H, W, C] in [0,1]; returns (loss, grads dict)."""
+def bf16(x):
+    """Round to the nearest bfloat16 (ties to even) through float32, returned as float64.
+
+    Used only by the bf16-EMULATION mode (reading R17):
+    the CUDA bf16 path stores activations / gradient operands and the tensor-core
+    weight shadow in bf16 and accumulates in fp32."""
+    f = np.asarray(x, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def loss_and_grad(p, model, xb, yb, emulate_bf16=False):
+    """xb float64 [nb, H, W, C] in [0,1]; returns (loss, grads dict).
+
+    emulate_bf16: round to bf16 exactly where the CUDA bf16 mode stores bf16
+    (pooled / hidden activations, dh, the pre-activation gradients dz, and the
+    conv2 / fc1 weights read by the tensor cores); everything else float64."""
+    q = bf16 if emulate_bf16 else (lambda v: v)
     g = {}
     nb = xb.shape[0]
     if model == MLP:
         x = xb.reshape(nb, -1)
         z1 = x @ p["fc1.W"].T + p["fc1.b"]
-        h1 = relu(z1)
+        h1 = q(relu(z1))
         z2 = h1 @ p["fc2.W"].T + p["fc2.b"]
         loss, dz2 = softmax_ce(z2, yb)
         g["fc2.W"], g["fc2.b"] = dz2.T @ h1, dz2.sum(0)
         dh1 = dz2 @ p["fc2.W"]
-        dz1 = dh1 * (z1 > 0)
-        g["fc1.W"], g["fc1.b"] = dz1.T @ x, dz1.sum(0)
+        dz1 = dh1 * (h1 > 0)
+        g["fc1.b"] = dz1.sum(0)
+        g["fc1.W"] = q(dz1).T @ x
         return loss, g
     if model == CNN:
+        W2q, W3q = q(p["conv2.W"]), q(p["fc1.W"])
         z1, cols1 = conv_fwd(xb, p["conv1.W"], p["conv1.b"], 1, 2)
         a1, arg1 = pool2_fwd(relu(z1))
-        z2, cols2 = conv_fwd(a1, p["conv2.W"], p["conv2.b"], 1, 2)
+        a1 = q(a1)
+        z2, cols2 = conv_fwd(a1, W2q, p["conv2.b"], 1, 2)
         a2, arg2 = pool2_fwd(relu(z2))
+        a2 = q(a2)
         f = a2.reshape(nb, -1)
-        z3 = f @ p["fc1.W"].T + p["fc1.b"]
-        h = relu(z3)
+        z3 = f @ W3q.T + p["fc1.b"]
+        h = q(relu(z3))
         z4 = h @ p["fc2.W"].T + p["fc2.b"]
         loss, dz4 = softmax_ce(z4, yb)
         g["fc2.W"], g["fc2.b"] = dz4.T @ h, dz4.sum(0)
-        dz3 = (dz4 @ p["fc2.W"]) * (z3 > 0)
-        g["fc1.W"], g["fc1.b"] = dz3.T @ f, dz3.sum(0)
-        da2 = (dz3 @ p["fc1.W"]).reshape(a2.shape)
-        dz2 = pool2_bwd(da2, arg2, z2.shape) * (z2 > 0)
-        g["conv2.W"], g["conv2.b"], da1 = conv_bwd(dz2, a1.shape, cols2, p["conv2.W"], 1, 2, True)
-        dz1 = pool2_bwd(da1, arg1, z1.shape) * (z1 > 0)
+        dz3 = (dz4 @ p["fc2.W"]) * (h > 0)
+        g["fc1.b"] = dz3.sum(0)
+        dz3 = q(dz3)
+        g["fc1.W"] = dz3.T @ f
+        da2 = (dz3 @ W3q).reshape(a2.shape)
+        dz2 = q(pool2_bwd(da2 * (a2 > 0), arg2, z2.shape))
+        g["conv2.W"], g["conv2.b"], da1 = conv_bwd(dz2, a1.shape, cols2, W2q, 1, 2, True)
+        dz1 = q(pool2_bwd(da1 * (a1 > 0), arg1, z1.shape))
         g["conv1.W"], g["conv1.b"], _ = conv_bwd(dz1, xb.shape, cols1, p["conv1.W"], 1, 2, False)
         return loss, g
     if model == RESNET8:
@@ -262,9 +285,9 @@ def loss_and_grad(p, model, xb, yb):
     raise ValueError(model)
 
 
-def flat_loss_and_grad(w, model, width_q, classes, xb, yb):
+def flat_loss_and_grad(w, model, width_q, classes, xb, yb, emulate_bf16=False):
     p = unpack(np.asarray(w, dtype=np.float64), model, width_q, classes)
-    loss, g = loss_and_grad(p, model, xb, yb)
+    loss, g = loss_and_grad(p, model, xb, yb, emulate_bf16)
     return loss, pack(g, model, width_q, classes)
 
 
@@ -276,7 +299,7 @@ def steps(n, batch, epochs):
 
 
 def local_sgd(w0, model, width_q, classes, x_u8, y, batch, epochs, lr, seed, rnd, client_id,
-              shuffle=True, max_steps=None):
+              shuffle=True, max_steps=None, emulate_bf16=False):
     """Run one client's local SGD; returns (w_k float64, losses list)."""
     w = np.array(w0, dtype=np.float64)
     n = x_u8.shape[0]
@@ -291,7 +314,7 @@ def local_sgd(w0, model, width_q, classes, x_u8, y, batch, epochs, lr, seed, rnd
             if max_steps is not None and done >= max_steps:
                 return w, losses
             idx = perm[j * batch:min((j + 1) * batch, n)]
-            loss, gflat = flat_loss_and_grad(w, model, width_q, classes, xf[idx], y[idx])
+            loss, gflat = flat_loss_and_grad(w, model, width_q, classes, xf[idx], y[idx], emulate_bf16)
             w = w - lr * gflat
             losses.append(loss)
             done += 1

@@ -53,11 +53,13 @@ def gpu_run(wl, rounds=1, precision=0, lr=0.05, arena_bytes=None, shuffle=True, 
     return res, extra
 
 
-def oracle_run(wl, rounds=1, lr=0.05, shuffle=True, all_widths=False, init_seed=0, g0=None, workers=0):
+def oracle_run(wl, rounds=1, lr=0.05, shuffle=True, all_widths=False, init_seed=0, g0=None, workers=0,
+               emulate_bf16=False):
     widths = widths_of(wl, all_widths)
     g = {w: v.astype(np.float64) for w, v in (g0 or init_globals(wl, widths, init_seed)).items()}
     for r in range(rounds):
-        g = orr.run_round(wl.clients, wl.shards, g, lr, wl.seed, r, shuffle=shuffle, workers=workers)
+        g = orr.run_round(wl.clients, wl.shards, g, lr, wl.seed, r, shuffle=shuffle, workers=workers,
+                          emulate_bf16=emulate_bf16)
     return g
 
 
