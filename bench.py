@@ -324,9 +324,13 @@ def main():
     by_per = dom_by / max(1, dom_n)
     alu_peak = fp32_alu_peak_tflops(pk["sm_max_mhz"])
     ridge = alu_peak * 1e12 / (pk["hbm"] * 1e9)
+    # which op classes run on tcgen05 in bf16 mode (the rest are SIMT fp32 math)
+    tc_ops = {"conv1_fwd", "conv2_fwd", "fc1_fwd", "fc1_dgrad", "fc1_wgrad", "conv2_dgrad", "conv2_wgrad",
+              "conv1_wgrad"} if prec == pb.PREC_BF16 else set()
+    on_tc = pb.OPC_NAMES[dominant] in tc_ops and pb.TC_OPS_BUILT.get(pb.OPC_NAMES[dominant], False)
     if fl_per / max(by_per, 1) >= ridge:
-        bound, achieved, peak, unit = ("alu", fl_per / avg_ns / 1e3, alu_peak, "TFLOP/s") if prec == pb.PREC_FP32 \
-            else ("tensor", fl_per / avg_ns / 1e3, pk["bf16_sus"], "TFLOP/s")
+        bound, achieved, peak, unit = ("tensor", fl_per / avg_ns / 1e3, pk["bf16_sus"], "TFLOP/s") if on_tc \
+            else ("alu", fl_per / avg_ns / 1e3, alu_peak, "TFLOP/s")
     else:
         bound, achieved, peak, unit = "hbm", by_per / avg_ns, pk["hbm"], "GB/s"
     traffic = None

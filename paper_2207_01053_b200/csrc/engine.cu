@@ -296,27 +296,38 @@ void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, c
 }
 
 // bf16 mode, CNN: conv2 and fc1 (fwd / dgrad / wgrad) on tcgen05; conv1 and the head on SIMT
-void launch_step_tc(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const int32_t* dtab,
-                    float lr) {
+template <int WQ>
+void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs,
+                      const int32_t* dtab, float lr) {
   typedef __nv_bfloat16 T;
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const CnnDims d = cnn_dims(m);
   launch_gemm<Conv1Fwd<T, C1F_BM, C1F_BN>, C1F_BM, C1F_BN>(ctx, {drecs, d}, L, OP_C1F, dtab);
-  launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TcConv2Fwd{drecs, d}, L, OP_C2F, dtab);
-  launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, TcFc1Fwd{drecs, d}, L, OP_F1F, dtab);
+  launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TcConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
+  launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, TcFc1Fwd<WQ>{drecs, d}, L, OP_F1F, dtab);
   HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
   int ev = op_begin(ctx, OP_HEAD);
   k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
   op_end(ctx, ev);
-  launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, TcFc1Dgrad{drecs, d}, L, OP_F1D, dtab);
-  launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad{drecs, d, lr}, L, OP_F1W, dtab);
-  launch_gemm_tc<TC_C2D_BN, TC_STAGES>(ctx, TcConv2Dgrad{drecs, d}, L, OP_C2D, dtab);
-  launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, TcConv2Wgrad{drecs, d, lr}, L, OP_C2W, dtab);
+  launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, TcFc1Dgrad<WQ>{drecs, d}, L, OP_F1D, dtab);
+  launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
+  launch_gemm_tc<TC_C2D_BN, TC_STAGES>(ctx, TcConv2Dgrad<WQ>{drecs, d}, L, OP_C2D, dtab);
+  launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, TcConv2Wgrad<WQ>{drecs, d, lr}, L, OP_C2W, dtab);
   launch_gemm<Conv1Wgrad<T, C1W_BM, C1W_BN>, C1W_BM, C1W_BN>(ctx, {drecs, d}, L, OP_C1W, dtab);
   ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr};
   ev = op_begin(ctx, OP_C1R);
   k_reduce_update<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->stream>>>(r1, tasks, dtab + L.prefix_off[OP_C1R], L.ntask);
   op_end(ctx, ev);
+}
+
+void launch_step_tc(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const int32_t* dtab,
+                    float lr) {
+  if (m.width_q == 1)
+    launch_step_tc_w<1>(ctx, m, L, drecs, dtab, lr);
+  else if (m.width_q == 2)
+    launch_step_tc_w<2>(ctx, m, L, drecs, dtab, lr);
+  else
+    launch_step_tc_w<4>(ctx, m, L, drecs, dtab, lr);
 }
 
 template <typename T>

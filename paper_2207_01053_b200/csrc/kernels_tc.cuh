@@ -4,19 +4,25 @@
 // Same grouped structure as kernels_simt.cuh (one launch per layer-op over every
 // active client; CTA -> (client, tile) by binary search over a prefix table),
 // but each CTA computes a 128 x BN output tile on the 5th-generation tensor
-// cores: 4 producer warps stream 64-wide K blocks of both operands into a
+// cores: 8 producer warps stream 64-wide K blocks of both operands into a
 // STAGES-deep shared-memory ring with 16-byte cp.async (the operands are
 // implicit-GEMM gathers: im2col of NHWC activations, transposed weights, ...),
-// one elected thread of warp 4 issues tcgen05.mma (M=128, N=BN, K=16, bf16 in,
-// fp32 accumulate in TMEM) and tcgen05.commit releases each stage, and the 4
-// producer warps then drain the accumulator with tcgen05.ld and run the
-// layer's fused epilogue (bias+ReLU+2x2 pool / ReLU-mask + pool-backward
-// scatter / SGD update of fp32 master + bf16 shadow weights).
+// one elected thread of warp 8 issues tcgen05.mma (M=128, N<=BN, K=16, bf16
+// in, fp32 accumulate in TMEM) and tcgen05.commit releases each stage, then the
+// 8 producer warps drain the accumulator with tcgen05.ld (warps w and w+4 share
+// TMEM lanes 32(w%4).., splitting the columns) and run the layer's fused
+// epilogue (bias+ReLU+2x2 pool / ReLU-mask + pool-backward scatter / SGD update
+// of fp32 master + bf16 shadow weights).
 //
-// Op sizes per client-step (rows = |beta|, CNN-w channels c1, c2, F; K1 = 64 c2):
-//   conv2 fwd   M = rows*256 (quad-major) N = c2    K = 25 c1      A K-major, B K-major
-//   conv2 dgrad M = rows*256              N = c1    K = 25 c2      A K-major, B MN-major
-//   conv2 wgrad M = 25 c1 + 1 (bias row)  N = c2    K = rows*256   A MN-major, B MN-major
+// Each producer thread owns fixed (row, chunk) coordinates of the tile for
+// the whole K loop, so the per-row part of the gather address (image, y, x,
+// base pointer) is computed once per tile ("pre" states); per K block only the
+// tap / channel offset changes.  Channel counts are compile-time (width WQ).
+//
+// Op sizes per client-step (rows = |beta|, CNN-w channels C1, C2, F; K1 = 64 C2):
+//   conv2 fwd   M = rows*256 (quad-major) N = C2    K = 25 C1      A K-major, B K-major
+//   conv2 dgrad M = rows*256              N = C1    K = 25 C2      A K-major, B MN-major
+//   conv2 wgrad M = 25 C1 + 1 (bias row)  N = C2    K = rows*256   A MN-major, B MN-major
 //   fc1 fwd     M = F                     N = rows  K = K1         A K-major, B K-major
 //   fc1 dgrad   M = K1                    N = rows  K = F          A MN-major, B K-major
 //   fc1 wgrad   M = K1                    N = F     K = rows       A MN-major, B MN-major
@@ -39,6 +45,9 @@ struct TcTile {
 
 __device__ __align__(16) const uint16_t kOneChunk[8] = {0x3F80, 0, 0, 0, 0, 0, 0, 0};  // bf16 {1,0,...,0}
 
+constexpr int kTcProd = 256;               // producer / epilogue threads (8 warps)
+constexpr int kTcThreads = kTcProd + 32;   // + the MMA warp
+
 template <bool MN, int R>
 __device__ __forceinline__ void chunk_coords(int q, int& i, int& j) {
   if (MN) {  // i = k row in [0,64), j = mn group in [0, R/8)
@@ -49,8 +58,6 @@ __device__ __forceinline__ void chunk_coords(int q, int& i, int& j) {
     j = (q >> 3) & 7;
   }
 }
-
-constexpr int kTcThreads = 160;
 
 template <int BN, int STAGES>
 constexpr int tc_smem_bytes() {
@@ -63,6 +70,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   constexpr int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
   constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   constexpr int LAG = (STAGES - 1) < 2 ? (STAGES - 1) : 2;
+  constexpr int NA = 1024 / kTcProd;                             // A chunks per producer thread
+  constexpr int NB = (BN * 8 + kTcProd - 1) / kTcProd;           // B chunks per producer thread
   static_assert(LAG >= 1, "need >= 2 stages");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
@@ -79,41 +88,46 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t done = bar0 + 16 * STAGES;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      tc::mbar_init(bar0 + 8 * s, 128);             // full[s]: one arrive per producer thread
+      tc::mbar_init(bar0 + 8 * s, kTcProd);         // full[s]: one arrive per producer thread
       tc::mbar_init(bar0 + 8 * (STAGES + s), 1);    // empty[s]: tcgen05.commit
     }
     tc::mbar_init(done, 1);
     tc::mbar_fence_init();
   }
-  if (warp == 4) tc::tmem_alloc(tc::smem_u32(tmem_slot), TMEM_COLS);
+  if (warp == 8) tc::tmem_alloc(tc::smem_u32(tmem_slot), TMEM_COLS);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = tc::smem_u32(smem);
 
-  if (warp < 4) {
+  if (warp < 8) {
     // ---------------- producers
     const int tid = threadIdx.x;
     const void* any = op.any(t);
+    typename Op::PA pa[NA];
+    typename Op::PB pb[NB];
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      int i, j;
+      chunk_coords<Op::A_MN, 128>(tid + kTcProd * u, i, j);
+      pa[u] = op.a_pre(t, i, j);
+    }
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      int i = 0, j = 0;
+      if (tid + kTcProd * u < BN * 8) chunk_coords<Op::B_MN, BN>(tid + kTcProd * u, i, j);
+      pb[u] = op.b_pre(t, i, j);
+    }
     for (int kb = 0; kb < t.nk; ++kb) {
       const int s = kb % STAGES;
       if (kb >= STAGES) tc::mbar_wait(bar0 + 8 * (STAGES + s), ((kb / STAGES) - 1) & 1);
       const uint32_t a_base = sbase + s * STAGE, b_base = a_base + A_BYTES;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int q = tid + 128 * u;
-        int i, j;
-        chunk_coords<Op::A_MN, 128>(q, i, j);
-        tc::cp16(a_base + 16 * q, op.a_src(t, kb, i, j), any);
-      }
+      for (int u = 0; u < NA; ++u) tc::cp16(a_base + 16 * (tid + kTcProd * u), op.a_src(t, pa[u], kb), any);
 #pragma unroll
-      for (int u = 0; u < BN * 8 / 128; ++u) {
-        const int q = tid + 128 * u;
-        int i, j;
-        chunk_coords<Op::B_MN, BN>(q, i, j);
-        tc::cp16(b_base + 16 * q, op.b_src(t, kb, i, j), any);
-      }
+      for (int u = 0; u < NB; ++u)
+        if (tid + kTcProd * u < BN * 8) tc::cp16(b_base + 16 * (tid + kTcProd * u), op.b_src(t, pb[u], kb), any);
       tc::cp_commit();
       if (kb >= LAG) {
         tc::cp_wait<LAG>();
@@ -128,14 +142,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---------------- epilogue: TMEM -> registers -> fused layer epilogue
     tc::mbar_wait(done, 0);
     tc::fence_after();
-    const int row = warp * 32 + lane;
-    for (int c0 = 0; c0 < t.n_mma; c0 += 16) {
+    const int row = (warp & 3) * 32 + lane;
+    for (int c0 = (warp >> 2) * 16; c0 < t.n_mma; c0 += 32) {
       float v[16];
-      tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+      tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
       op.epilogue(t, row, c0, v);
     }
-  } else if (warp == 4) {
-    // ---------------- MMA issuer (one thread)
+  } else {
+    // ---------------- MMA issuer (one thread of warp 8)
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_bf16(128, t.n_mma, Op::A_MN, Op::B_MN);
       for (int kb = 0; kb < t.nk; ++kb) {
@@ -159,7 +173,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 8) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, TMEM_COLS);
   }
@@ -167,34 +181,52 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
 __device__ __forceinline__ int round16(int x) { return (x + 15) & ~15; }
 
+// compile-time CNN-w channel counts for width WQ/4
+template <int WQ>
+struct CnnW {
+  static constexpr int C1 = 8 * WQ, C2 = 16 * WQ, F = 128 * WQ, K1 = 64 * C2;
+  static constexpr int L1 = WQ == 1 ? 3 : WQ == 2 ? 4 : 5;  // log2 C1
+  static constexpr int L2 = L1 + 1;                          // log2 C2
+};
+
 // --------------------------------------------------------------------------
 // CNN ops on tensor cores (bf16 activations, bf16 shadow weights B_WSH)
 // --------------------------------------------------------------------------
+template <int WQ>
 struct TcConv2Fwd {
+  typedef CnnW<WQ> W;
   static constexpr bool A_MN = false, B_MN = false;
+  struct PA { const bf16* base; int y, x, j; };
+  struct PB { const bf16* row; int j; };
   const ClientRec* recs;
   CnnDims d;
   __device__ void setup(TcTile& t, int local) const {
     t.m0 = local * 128;
     t.n0 = 0;
-    t.nk = cdiv(25 * d.c1, 64);
-    t.n_mma = round16(d.c2);
+    t.nk = (25 * W::C1 + 63) / 64;
+    t.n_mma = W::C2 < 16 ? 16 : W::C2;
   }
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
-  __device__ const void* a_src(const TcTile& t, int kb, int i, int j) const {
-    const int k = kb * 64 + 8 * j;
-    if (k >= 25 * d.c1) return nullptr;
-    const int m = t.m0 + i, r = m >> 8, local = m & 255, p = local >> 2, q = local & 3;
-    const int y = ((p >> 3) << 1) + (q >> 1), x = ((p & 7) << 1) + (q & 1);
-    const int tap = k / d.c1, ci = k - tap * d.c1, ky = tap / 5, kx = tap - ky * 5;
-    const int sy = y + ky - 2, sx = x + kx - 2;
-    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return nullptr;
-    return (const bf16*)t.c->buf[B_A1] + ((int64_t)r * 256 + sy * 16 + sx) * d.c1 + ci;
+  __device__ PA a_pre(const TcTile& t, int i, int j) const {
+    const int m = t.m0 + i, r = m >> 8, p = (m >> 2) & 63, q = m & 3;
+    return PA{(const bf16*)t.c->buf[B_A1] + (int64_t)r * 256 * W::C1, ((p >> 3) << 1) + (q >> 1),
+              ((p & 7) << 1) + (q & 1), j};
   }
-  __device__ const void* b_src(const TcTile& t, int kb, int i, int j) const {
-    const int k = kb * 64 + 8 * j;
-    if (k >= 25 * d.c1 || i >= d.c2) return nullptr;
-    return (const bf16*)t.c->buf[B_WSH] + d.w2 + (int64_t)i * 25 * d.c1 + k;
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
+    const int k = kb * 64 + 8 * s.j;
+    if (k >= 25 * W::C1) return nullptr;
+    const int tap = k >> W::L1, ci = k & (W::C1 - 1), ky = tap / 5, kx = tap - ky * 5;
+    const int sy = s.y + ky - 2, sx = s.x + kx - 2;
+    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return nullptr;
+    return s.base + (sy * 16 + sx) * W::C1 + ci;
+  }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const {
+    return PB{i < W::C2 ? (const bf16*)t.c->buf[B_WSH] + d.w2 + (int64_t)i * 25 * W::C1 : nullptr, j};
+  }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
+    const int k = kb * 64 + 8 * s.j;
+    if (!s.row || k >= 25 * W::C1) return nullptr;
+    return s.row + k;
   }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
     const int m = t.m0 + row, r = m >> 8, p = (m & 255) >> 2, q = m & 3;
@@ -204,16 +236,16 @@ struct TcConv2Fwd {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int n = c0 + j;
-      const float val = n < d.c2 ? fmaxf(v[j] + t.c->params[d.b2 + n], 0.f) : 0.f;
+      const float val = n < W::C2 ? fmaxf(v[j] + t.c->params[d.b2 + n], 0.f) : 0.f;
       const float v0 = __shfl_sync(0xffffffffu, val, base), v1 = __shfl_sync(0xffffffffu, val, base + 1);
       const float v2 = __shfl_sync(0xffffffffu, val, base + 2), v3 = __shfl_sync(0xffffffffu, val, base + 3);
-      if (q == 0 && n < d.c2) {
+      if (q == 0 && n < W::C2) {
         float best = v0;
         int arg = 0;
         if (v1 > best) { best = v1; arg = 1; }
         if (v2 > best) { best = v2; arg = 2; }
         if (v3 > best) { best = v3; arg = 3; }
-        const int64_t o = ((int64_t)r * 64 + p) * d.c2 + n;
+        const int64_t o = ((int64_t)r * 64 + p) * W::C2 + n;
         a2[o] = __float2bfloat16_rn(best);
         i2[o] = (uint8_t)arg;
       }
@@ -221,31 +253,39 @@ struct TcConv2Fwd {
   }
 };
 
+template <int WQ>
 struct TcConv2Dgrad {
+  typedef CnnW<WQ> W;
   static constexpr bool A_MN = false, B_MN = true;
+  struct PA { const bf16* base; int y, x, j; };
+  struct PB { int i, n0; };
   const ClientRec* recs;
   CnnDims d;
   __device__ void setup(TcTile& t, int local) const {
     t.m0 = local * 128;
     t.n0 = 0;
-    t.nk = cdiv(25 * d.c2, 64);
-    t.n_mma = round16(d.c1);
+    t.nk = (25 * W::C2 + 63) / 64;
+    t.n_mma = W::C1 < 16 ? 16 : W::C1;
   }
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
-  __device__ const void* a_src(const TcTile& t, int kb, int i, int j) const {
-    const int k = kb * 64 + 8 * j;
-    if (k >= 25 * d.c2) return nullptr;
-    const int m = t.m0 + i, r = m >> 8, y = (m >> 4) & 15, x = m & 15;
-    const int tap = k / d.c2, co = k - tap * d.c2, ky = tap / 5, kx = tap - ky * 5;
-    const int sy = y - ky + 2, sx = x - kx + 2;
-    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return nullptr;
-    return (const bf16*)t.c->buf[B_DZ2] + ((int64_t)r * 256 + sy * 16 + sx) * d.c2 + co;
+  __device__ PA a_pre(const TcTile& t, int i, int j) const {
+    const int m = t.m0 + i, r = m >> 8;
+    return PA{(const bf16*)t.c->buf[B_DZ2] + (int64_t)r * 256 * W::C2, (m >> 4) & 15, m & 15, j};
   }
-  __device__ const void* b_src(const TcTile& t, int kb, int i, int j) const {
-    const int k = kb * 64 + i, n0 = 8 * j;
-    if (k >= 25 * d.c2 || n0 >= d.c1) return nullptr;
-    const int tap = k / d.c2, co = k - tap * d.c2;
-    return (const bf16*)t.c->buf[B_WSH] + d.w2 + ((int64_t)co * 25 + tap) * d.c1 + n0;
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
+    const int k = kb * 64 + 8 * s.j;
+    if (k >= 25 * W::C2) return nullptr;
+    const int tap = k >> W::L2, co = k & (W::C2 - 1), ky = tap / 5, kx = tap - ky * 5;
+    const int sy = s.y - ky + 2, sx = s.x - kx + 2;
+    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return nullptr;
+    return s.base + (sy * 16 + sx) * W::C2 + co;
+  }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const { return PB{i, 8 * j}; }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
+    const int k = kb * 64 + s.i;
+    if (k >= 25 * W::C2 || s.n0 >= W::C1) return nullptr;
+    const int tap = k >> W::L2, co = k & (W::C2 - 1);
+    return (const bf16*)t.c->buf[B_WSH] + d.w2 + (co * 25 + tap) * W::C1 + s.n0;
   }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
     const int m = t.m0 + row, r = m >> 8, y = (m >> 4) & 15, x = m & 15;
@@ -255,21 +295,25 @@ struct TcConv2Dgrad {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int n = c0 + j;
-      if (n >= d.c1) continue;
-      const int64_t o = (int64_t)m * d.c1 + n;
+      if (n >= W::C1) continue;
+      const int64_t o = (int64_t)m * W::C1 + n;
       const float val = __bfloat162float(a1[o]) > 0.f ? v[j] : 0.f;
       const int arg = i1[o];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int Y = 2 * y + (q >> 1), X = 2 * x + (q & 1);
-        dz1[((int64_t)r * 1024 + Y * 32 + X) * d.c1 + n] = __float2bfloat16_rn(q == arg ? val : 0.f);
+        dz1[((int64_t)r * 1024 + Y * 32 + X) * W::C1 + n] = __float2bfloat16_rn(q == arg ? val : 0.f);
       }
     }
   }
 };
 
+template <int WQ>
 struct TcConv2Wgrad {  // full reduction in one CTA -> SGD update in the epilogue (no split-K partials)
+  typedef CnnW<WQ> W;
   static constexpr bool A_MN = true, B_MN = true;
+  struct PA { int i, dy, dx, ci, kind; };  // kind 0: gather, 1: bias ones row, 2: zero
+  struct PB { int i, n0; };
   const ClientRec* recs;
   CnnDims d;
   float lr;
@@ -277,63 +321,75 @@ struct TcConv2Wgrad {  // full reduction in one CTA -> SGD update in the epilogu
     t.m0 = local * 128;
     t.n0 = 0;
     t.nk = t.tk.rows * 4;  // rows*256 pixels / 64
-    t.n_mma = round16(d.c2);
+    t.n_mma = W::C2 < 16 ? 16 : W::C2;
   }
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
-  __device__ const void* a_src(const TcTile& t, int kb, int i, int j) const {
-    const int p = kb * 64 + i, mg = t.m0 + 8 * j, Kw = 25 * d.c1;
-    if (mg == Kw) return kOneChunk;  // bias row: db = sum_p dz
-    if (mg > Kw) return nullptr;
-    const int r = p >> 8, y = (p >> 4) & 15, x = p & 15;
-    const int tap = mg / d.c1, ci = mg - tap * d.c1, ky = tap / 5, kx = tap - ky * 5;
-    const int sy = y + ky - 2, sx = x + kx - 2;
-    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return nullptr;
-    return (const bf16*)t.c->buf[B_A1] + ((int64_t)r * 256 + sy * 16 + sx) * d.c1 + ci;
+  __device__ PA a_pre(const TcTile& t, int i, int j) const {
+    const int mg = t.m0 + 8 * j, Kw = 25 * W::C1;
+    if (mg == Kw) return PA{i, 0, 0, 0, 1};
+    if (mg > Kw) return PA{i, 0, 0, 0, 2};
+    const int tap = mg >> W::L1, ky = tap / 5, kx = tap - ky * 5;
+    return PA{i, ky - 2, kx - 2, mg & (W::C1 - 1), 0};
   }
-  __device__ const void* b_src(const TcTile& t, int kb, int i, int j) const {
-    const int p = kb * 64 + i, n0 = 8 * j;
-    if (n0 >= d.c2) return nullptr;
-    return (const bf16*)t.c->buf[B_DZ2] + (int64_t)p * d.c2 + n0;
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
+    if (s.kind) return s.kind == 1 ? (const void*)kOneChunk : nullptr;
+    const int p = kb * 64 + s.i, r = p >> 8, sy = ((p >> 4) & 15) + s.dy, sx = (p & 15) + s.dx;
+    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return nullptr;
+    return (const bf16*)t.c->buf[B_A1] + ((int64_t)r * 256 + sy * 16 + sx) * W::C1 + s.ci;
+  }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const { return PB{i, 8 * j}; }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
+    if (s.n0 >= W::C2) return nullptr;
+    return (const bf16*)t.c->buf[B_DZ2] + (int64_t)(kb * 64 + s.i) * W::C2 + s.n0;
   }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
-    const int m = t.m0 + row, Kw = 25 * d.c1;
+    const int m = t.m0 + row, Kw = 25 * W::C1;
     if (m > Kw) return;
     float* P = t.c->params;
     bf16* S = (bf16*)t.c->buf[B_WSH];
+    if (m == Kw) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int co = c0 + j;
-      if (co >= d.c2) continue;
-      if (m < Kw) {
-        const int64_t idx = d.w2 + (int64_t)co * Kw + m;
-        const float w = P[idx] - lr * v[j];
-        P[idx] = w;
-        S[idx] = __float2bfloat16_rn(w);
-      } else {
-        P[d.b2 + co] -= lr * v[j];
-      }
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < W::C2) P[d.b2 + c0 + j] -= lr * v[j];
+      return;
     }
+    float w[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) w[j] = c0 + j < W::C2 ? P[d.w2 + (int64_t)(c0 + j) * Kw + m] : 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (c0 + j < W::C2) {
+        const int64_t idx = d.w2 + (int64_t)(c0 + j) * Kw + m;
+        const float nw = w[j] - lr * v[j];
+        P[idx] = nw;
+        S[idx] = __float2bfloat16_rn(nw);
+      }
   }
 };
 
+template <int WQ>
 struct TcFc1Fwd {
+  typedef CnnW<WQ> W;
   static constexpr bool A_MN = false, B_MN = false;
+  struct PA { const bf16* p; };
+  struct PB { const bf16* p; };
   const ClientRec* recs;
   CnnDims d;
   __device__ void setup(TcTile& t, int local) const {
     t.m0 = local * 128;
     t.n0 = 0;
-    t.nk = d.c2;  // 64 c2 / 64
+    t.nk = W::K1 / 64;
     t.n_mma = round16(t.tk.rows);
   }
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
-  __device__ const void* a_src(const TcTile& t, int kb, int i, int j) const {
-    return (const bf16*)t.c->buf[B_WSH] + d.w3 + (int64_t)(t.m0 + i) * 64 * d.c2 + kb * 64 + 8 * j;
+  __device__ PA a_pre(const TcTile& t, int i, int j) const {
+    return PA{(const bf16*)t.c->buf[B_WSH] + d.w3 + (int64_t)(t.m0 + i) * W::K1 + 8 * j};
   }
-  __device__ const void* b_src(const TcTile& t, int kb, int i, int j) const {
-    if (i >= t.tk.rows) return nullptr;
-    return (const bf16*)t.c->buf[B_A2] + (int64_t)i * 64 * d.c2 + kb * 64 + 8 * j;
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const { return s.p + kb * 64; }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const {
+    return PB{i < t.tk.rows ? (const bf16*)t.c->buf[B_A2] + (int64_t)i * W::K1 + 8 * j : nullptr};
   }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const { return s.p ? s.p + kb * 64 : nullptr; }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
     const int f = t.m0 + row;
     const float b = t.c->params[d.b3 + f];
@@ -341,33 +397,37 @@ struct TcFc1Fwd {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int r = c0 + j;
-      if (r < t.tk.rows) h[(int64_t)r * d.f + f] = __float2bfloat16_rn(fmaxf(v[j] + b, 0.f));
+      if (r < t.tk.rows) h[(int64_t)r * W::F + f] = __float2bfloat16_rn(fmaxf(v[j] + b, 0.f));
     }
   }
 };
 
+template <int WQ>
 struct TcFc1Dgrad {
+  typedef CnnW<WQ> W;
   static constexpr bool A_MN = true, B_MN = false;
+  struct PA { const bf16* p; };
+  struct PB { const bf16* p; };
   const ClientRec* recs;
   CnnDims d;
   __device__ void setup(TcTile& t, int local) const {
     t.m0 = local * 128;
     t.n0 = 0;
-    t.nk = d.f / 64;
+    t.nk = W::F / 64;
     t.n_mma = round16(t.tk.rows);
   }
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
-  __device__ const void* a_src(const TcTile& t, int kb, int i, int j) const {
-    const int f = kb * 64 + i;
-    return (const bf16*)t.c->buf[B_WSH] + d.w3 + (int64_t)f * 64 * d.c2 + t.m0 + 8 * j;
+  __device__ PA a_pre(const TcTile& t, int i, int j) const {
+    return PA{(const bf16*)t.c->buf[B_WSH] + d.w3 + (int64_t)i * W::K1 + t.m0 + 8 * j};
   }
-  __device__ const void* b_src(const TcTile& t, int kb, int i, int j) const {
-    if (i >= t.tk.rows) return nullptr;
-    return (const bf16*)t.c->buf[B_DH] + (int64_t)i * d.f + kb * 64 + 8 * j;
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const { return s.p + (int64_t)kb * 64 * W::K1; }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const {
+    return PB{i < t.tk.rows ? (const bf16*)t.c->buf[B_DH] + (int64_t)i * W::F + 8 * j : nullptr};
   }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const { return s.p ? s.p + kb * 64 : nullptr; }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
-    const int n1 = t.m0 + row, K1 = 64 * d.c2;
-    const int p = n1 / d.c2, c = n1 - p * d.c2, py = p >> 3, px = p & 7;
+    const int n1 = t.m0 + row;
+    const int p = n1 >> W::L2, c = n1 & (W::C2 - 1), py = p >> 3, px = p & 7;
     const bf16* a2 = (const bf16*)t.c->buf[B_A2];
     const uint8_t* i2 = (const uint8_t*)t.c->buf[B_I2];
     bf16* dz2 = (bf16*)t.c->buf[B_DZ2];
@@ -375,52 +435,57 @@ struct TcFc1Dgrad {
     for (int j = 0; j < 16; ++j) {
       const int r = c0 + j;
       if (r >= t.tk.rows) continue;
-      const int64_t o = (int64_t)r * K1 + n1;
+      const int64_t o = (int64_t)r * W::K1 + n1;
       const float val = __bfloat162float(a2[o]) > 0.f ? v[j] : 0.f;
       const int arg = i2[o];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int y = 2 * py + (q >> 1), x = 2 * px + (q & 1);
-        dz2[((int64_t)r * 256 + y * 16 + x) * d.c2 + c] = __float2bfloat16_rn(q == arg ? val : 0.f);
+        dz2[((int64_t)r * 256 + y * 16 + x) * W::C2 + c] = __float2bfloat16_rn(q == arg ? val : 0.f);
       }
     }
   }
 };
 
+template <int WQ>
 struct TcFc1Wgrad {  // M = K1 (input features), N = F (outputs), K = rows; W <- W - lr dW
+  typedef CnnW<WQ> W;
   static constexpr bool A_MN = true, B_MN = true;
+  struct PA { const bf16* p; };
+  struct PB { const bf16* p; };
   const ClientRec* recs;
   CnnDims d;
   float lr;
   __device__ void setup(TcTile& t, int local) const {
-    const int nt = cdiv(d.f, 256);
+    const int nt = (W::F + 255) / 256;
     t.m0 = (local / nt) * 128;
     t.n0 = (local % nt) * 256;
     t.nk = 1;  // rows <= 64
-    t.n_mma = min(256, d.f - t.n0);
+    t.n_mma = W::F - t.n0 < 256 ? W::F - t.n0 : 256;
   }
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
-  __device__ const void* a_src(const TcTile& t, int kb, int i, int j) const {
-    if (i >= t.tk.rows) return nullptr;
-    return (const bf16*)t.c->buf[B_A2] + (int64_t)i * 64 * d.c2 + t.m0 + 8 * j;
+  __device__ PA a_pre(const TcTile& t, int i, int j) const {
+    return PA{i < t.tk.rows ? (const bf16*)t.c->buf[B_A2] + (int64_t)i * W::K1 + t.m0 + 8 * j : nullptr};
   }
-  __device__ const void* b_src(const TcTile& t, int kb, int i, int j) const {
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const { return s.p; }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const {
     const int n = t.n0 + 8 * j;
-    if (i >= t.tk.rows || n >= d.f) return nullptr;
-    return (const bf16*)t.c->buf[B_DH] + (int64_t)i * d.f + n;
+    return PB{i < t.tk.rows && n < W::F ? (const bf16*)t.c->buf[B_DH] + (int64_t)i * W::F + n : nullptr};
   }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const { return s.p; }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
-    const int k1 = t.m0 + row, K1 = 64 * d.c2;
-    float* P = t.c->params;
-    bf16* S = (bf16*)t.c->buf[B_WSH];
+    const int k1 = t.m0 + row;
+    float* P = t.c->params + d.w3 + k1;
+    bf16* S = (bf16*)t.c->buf[B_WSH] + d.w3 + k1;
+    const int64_t f0 = t.n0 + c0;
+    float w[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) w[j] = P[(f0 + j) * W::K1];  // 16 independent loads in flight
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const int f = t.n0 + c0 + j;
-      if (f >= d.f) continue;
-      const int64_t idx = d.w3 + (int64_t)f * K1 + k1;
-      const float w = P[idx] - lr * v[j];
-      P[idx] = w;
-      S[idx] = __float2bfloat16_rn(w);
+      const float nw = w[j] - lr * v[j];
+      P[(f0 + j) * W::K1] = nw;
+      S[(f0 + j) * W::K1] = __float2bfloat16_rn(nw);
     }
   }
 };
@@ -428,9 +493,10 @@ struct TcFc1Wgrad {  // M = K1 (input features), N = F (outputs), K = rows; W <-
 // --------------------------------------------------------------------------
 // self-test GEMM (protea_selftest_gemm): D[M,N] = A B^T with dense bf16 operands
 // --------------------------------------------------------------------------
-struct TcDense {
-  // A: K-major [M][K] (a_mn=0) or MN-major [K][M]; B likewise with N; K multiple of 64; M multiple of 128
+struct TcDense {  // A [M][K], B [N][K] (K-major)
   static constexpr bool A_MN = false, B_MN = false;
+  struct PA { const bf16* p; };
+  struct PB { const bf16* p; };
   const ClientRec* recs;
   const bf16* A;
   const bf16* B;
@@ -443,13 +509,10 @@ struct TcDense {
     t.n_mma = round16(N);
   }
   __device__ const void* any(const TcTile& t) const { return A; }
-  __device__ const void* a_src(const TcTile& t, int kb, int i, int j) const {
-    return A + (int64_t)(t.m0 + i) * K + kb * 64 + 8 * j;
-  }
-  __device__ const void* b_src(const TcTile& t, int kb, int i, int j) const {
-    if (i >= N) return nullptr;
-    return B + (int64_t)i * K + kb * 64 + 8 * j;
-  }
+  __device__ PA a_pre(const TcTile& t, int i, int j) const { return PA{A + (int64_t)(t.m0 + i) * K + 8 * j}; }
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const { return s.p + kb * 64; }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const { return PB{i < N ? B + (int64_t)i * K + 8 * j : nullptr}; }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const { return s.p ? s.p + kb * 64 : nullptr; }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
 #pragma unroll
     for (int j = 0; j < 16; ++j)
@@ -459,6 +522,8 @@ struct TcDense {
 
 struct TcDenseMN {  // A given as [K][M] (MN-major), B as [K][N] (MN-major)
   static constexpr bool A_MN = true, B_MN = true;
+  struct PA { const bf16* p; };
+  struct PB { const bf16* p; };
   const ClientRec* recs;
   const bf16* A;
   const bf16* B;
@@ -471,12 +536,13 @@ struct TcDenseMN {  // A given as [K][M] (MN-major), B as [K][N] (MN-major)
     t.n_mma = round16(N);
   }
   __device__ const void* any(const TcTile& t) const { return A; }
-  __device__ const void* a_src(const TcTile& t, int kb, int i, int j) const {
-    return A + (int64_t)(kb * 64 + i) * M + t.m0 + 8 * j;
+  __device__ PA a_pre(const TcTile& t, int i, int j) const { return PA{A + (int64_t)i * M + t.m0 + 8 * j}; }
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const { return s.p + (int64_t)kb * 64 * M; }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const {
+    return PB{8 * j < N ? B + (int64_t)i * N + 8 * j : nullptr};
   }
-  __device__ const void* b_src(const TcTile& t, int kb, int i, int j) const {
-    if (8 * j >= N) return nullptr;
-    return B + (int64_t)(kb * 64 + i) * N + 8 * j;
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
+    return s.p ? s.p + (int64_t)kb * 64 * N : nullptr;
   }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
 #pragma unroll
