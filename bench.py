@@ -274,7 +274,7 @@ def main():
     for w in range(args.warmup):
         plan, _ = pb.protea_plan(profiles, caps)
         _, st = sim.run_round(all_clients, plan, g, g2, lr=wl.lr, seed=wl.seed, rnd=rnd,
-                              time_ops=(0xFFFF if w == 0 else 0))
+                              time_ops=(0xFFFFFFFF if w == 0 else 0))
         g, g2 = g2, g
         rnd += 1
         if w == 0:
@@ -387,7 +387,7 @@ def main():
                 "detail": {"round_tflops": sum(int(f["flops"]) for f in foot) / (ms_per_step / 1e3) / 1e12,
                            "iterations_per_round": int(st["iterations"]), "host_wall_s": host_s,
                            "probe_s": probe_s, "probe_step_ns": sorted({int(p["step_ns"]) for p in probe}),
-                           "op_ms_warmup": {pb.OPC_NAMES[i]: op_stats["op_ns"][i] / 1e6 for i in range(16)
+                           "op_ms_warmup": {pb.OPC_NAMES[i]: op_stats["op_ns"][i] / 1e6 for i in range(pb.N_OPC)
                                             if op_stats and op_stats["op_ns"][i]},
                            "loss_mean_last_round": st["loss_sum"] / max(1, st["client_steps"])}}
         print(json.dumps(line), flush=True)

@@ -139,7 +139,8 @@ enum {
   PROTEA_OPC_CONV1_FWD = 0, PROTEA_OPC_CONV2_FWD, PROTEA_OPC_FC1_FWD, PROTEA_OPC_HEAD, PROTEA_OPC_FC1_DGRAD,
   PROTEA_OPC_FC1_WGRAD, PROTEA_OPC_CONV2_DGRAD, PROTEA_OPC_CONV2_WGRAD, PROTEA_OPC_CONV2_REDUCE,
   PROTEA_OPC_CONV1_WGRAD, PROTEA_OPC_CONV1_REDUCE, PROTEA_OPC_MLP_FC1_FWD, PROTEA_OPC_MLP_HEAD,
-  PROTEA_OPC_MLP_FC1_WGRAD, PROTEA_OPC_ADMIT, PROTEA_OPC_FEDAVG, PROTEA_N_OPC = 16
+  PROTEA_OPC_MLP_FC1_WGRAD, PROTEA_OPC_ADMIT, PROTEA_OPC_FEDAVG, PROTEA_OPC_STAGE_X,
+  PROTEA_N_OPC = 32 /* room for further op classes */
 };
 
 typedef struct {

@@ -220,7 +220,7 @@ def loss_and_grad(p, model, xb, yb, emulate_bf16=False):
         return loss, g
     if model == CNN:
         W2q, W3q = q(p["conv2.W"]), q(p["fc1.W"])
-        z1, cols1 = conv_fwd(xb, p["conv1.W"], p["conv1.b"], 1, 2)
+        z1, cols1 = conv_fwd(q(xb), q(p["conv1.W"]), p["conv1.b"], 1, 2)
         a1, arg1 = pool2_fwd(relu(z1))
         a1 = q(a1)
         z2, cols2 = conv_fwd(a1, W2q, p["conv2.b"], 1, 2)
@@ -240,7 +240,7 @@ def loss_and_grad(p, model, xb, yb, emulate_bf16=False):
         dz2 = q(pool2_bwd(da2 * (a2 > 0), arg2, z2.shape))
         g["conv2.W"], g["conv2.b"], da1 = conv_bwd(dz2, a1.shape, cols2, W2q, 1, 2, True)
         dz1 = q(pool2_bwd(da1 * (a1 > 0), arg1, z1.shape))
-        g["conv1.W"], g["conv1.b"], _ = conv_bwd(dz1, xb.shape, cols1, p["conv1.W"], 1, 2, False)
+        g["conv1.W"], g["conv1.b"], _ = conv_bwd(dz1, xb.shape, cols1, q(p["conv1.W"]), 1, 2, False)
         return loss, g
     if model == RESNET8:
         z0, cols0 = conv_fwd(xb, p["conv0.W"], p["conv0.b"], 1, 1)

@@ -63,13 +63,13 @@ class PlanOpts(ctypes.Structure):
                 ("max_active", ctypes.c_uint32)]
 
 
-N_OPC = 16
+N_OPC = 32
 # op classes that run on tcgen05 tensor cores in bf16 mode (CNN); the others use SIMT fp32 math
-TC_OPS_BUILT = {"conv2_fwd": True, "fc1_fwd": True, "fc1_dgrad": True, "fc1_wgrad": True, "conv2_dgrad": True,
-                "conv2_wgrad": True}
+TC_OPS_BUILT = {"conv1_fwd": True, "conv2_fwd": True, "fc1_fwd": True, "fc1_dgrad": True, "fc1_wgrad": True,
+                "conv2_dgrad": True, "conv2_wgrad": True, "conv1_wgrad": True}
 OPC_NAMES = ["conv1_fwd", "conv2_fwd", "fc1_fwd", "head", "fc1_dgrad", "fc1_wgrad", "conv2_dgrad", "conv2_wgrad",
              "conv2_reduce", "conv1_wgrad", "conv1_reduce", "mlp_fc1_fwd", "mlp_head", "mlp_fc1_wgrad", "admit",
-             "fedavg"]
+             "fedavg", "stage_x"] + [f"op{i}" for i in range(17, 32)]
 
 
 class RoundOpts(ctypes.Structure):

@@ -20,6 +20,8 @@ struct ClientRec {
   double* acc;             // group FedAvg accumulator (fp64)
   int32_t n, B, E, nb;     // nb = ceil(n/B)
   int64_t P;               // parameters of the client's model
+  int32_t c1;              // CNN conv1 channels (padded conv1 shadow in bf16 mode), else 0
+  int32_t pad_;
   int64_t id;
   uint64_t* sm_ns;         // per-client device-time attribution (nullable)
 };

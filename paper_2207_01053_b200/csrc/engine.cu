@@ -163,15 +163,19 @@ constexpr int MW_BM = 64, MW_BN = 64;
 
 enum Op : int {
   OP_C1F = 0, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R,
-  OP_MF, OP_MHEAD, OP_MW, OP_COUNT
+  OP_MF, OP_MHEAD, OP_MW, OP_ADMIT_, OP_FEDAVG_, OP_STAGE, OP_COUNT = PROTEA_N_OPC
 };
 
 // tensor-core tile shapes (bf16 mode): M tile = 128, BN per op, STAGES-deep ring
-constexpr int TC_C2F_BN = 64, TC_C2D_BN = 32, TC_C2W_BN = 64, TC_F1F_BN = 64, TC_F1D_BN = 64, TC_F1W_BN = 256;
+constexpr int TC_C1F_BN = 32, TC_C1W_BN = 32, TC_C2F_BN = 64, TC_C2D_BN = 32, TC_C2W_BN = 64, TC_F1F_BN = 64, TC_F1D_BN = 64, TC_F1W_BN = 256;
 constexpr int TC_STAGES = 4, TC_F1W_STAGES = 2;
 
 int tiles(const ModelDims& m, int op, int rows, bool tc) {
   if (tc) switch (op) {
+      case OP_STAGE: return cdiv(rows * 1296, kStageThreads);
+      case OP_C1F: return rows * 8;
+      case OP_C1W: return 2 * cdiv(rows * 1024, kWgradChunkPx);
+      case OP_C1R: return cdiv(76 * m.c1, kReduceBlock);
       case OP_C2F: return rows * 2;
       case OP_F1F: return m.f / 128;
       case OP_F1D: return 64 * m.c2 / 128;
@@ -201,7 +205,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
 
 std::vector<int> ops_of(const ModelDims& m, bool tc) {
   if (m.arch == PROTEA_MODEL_CNN && tc)
-    return {OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C1W, OP_C1R};
+    return {OP_STAGE, OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_CNN)
     return {OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_MLP) return {OP_MF, OP_MHEAD, OP_MW};
@@ -230,6 +234,7 @@ void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, u
     case OP_MF: F = 2 * r * 64 * 784; B = r * 784 + 4 * 64 * 785 + r * 64 * e; break;
     case OP_MHEAD: F = 3 * 2 * r * C * 64; B = r * 64 * e + 8 * C * 65 + r * 64 * e + 8 * 64 + r * 4; break;
     case OP_MW: F = 2 * r * 64 * 784; B = r * 64 * e + r * 784 + 8 * 64 * 784; break;
+    case OP_STAGE: F = 0; B = r * 3072 + r * 1296 * 16; break;
   }
   *fl = F;
   *by = B;
@@ -302,21 +307,25 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   typedef __nv_bfloat16 T;
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const CnnDims d = cnn_dims(m);
-  launch_gemm<Conv1Fwd<T, C1F_BM, C1F_BN>, C1F_BM, C1F_BN>(ctx, {drecs, d}, L, OP_C1F, dtab);
+  int ev = op_begin(ctx, OP_STAGE);
+  k_stage_x<<<L.grid[OP_STAGE], kStageThreads, 0, ctx->stream>>>(drecs, tasks, dtab + L.prefix_off[OP_STAGE],
+                                                                  L.ntask);
+  op_end(ctx, ev);
+  launch_gemm_tc<TC_C1F_BN, TC_STAGES>(ctx, TcConv1Fwd<WQ>{drecs, d}, L, OP_C1F, dtab);
   launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TcConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
   launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, TcFc1Fwd<WQ>{drecs, d}, L, OP_F1F, dtab);
   HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
-  int ev = op_begin(ctx, OP_HEAD);
+  ev = op_begin(ctx, OP_HEAD);
   k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
   op_end(ctx, ev);
   launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, TcFc1Dgrad<WQ>{drecs, d}, L, OP_F1D, dtab);
   launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
   launch_gemm_tc<TC_C2D_BN, TC_STAGES>(ctx, TcConv2Dgrad<WQ>{drecs, d}, L, OP_C2D, dtab);
   launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, TcConv2Wgrad<WQ>{drecs, d, lr}, L, OP_C2W, dtab);
-  launch_gemm<Conv1Wgrad<T, C1W_BM, C1W_BN>, C1W_BM, C1W_BN>(ctx, {drecs, d}, L, OP_C1W, dtab);
-  ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr};
+  launch_gemm_tc<TC_C1W_BN, TC_STAGES>(ctx, TcConv1Wgrad<WQ>{drecs, d}, L, OP_C1W, dtab);
   ev = op_begin(ctx, OP_C1R);
-  k_reduce_update<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->stream>>>(r1, tasks, dtab + L.prefix_off[OP_C1R], L.ntask);
+  k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->stream>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
+                                                                       L.ntask, m.c1, d.w1, d.b1, lr);
   op_end(ctx, ev);
 }
 
@@ -585,6 +594,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     r.nb = c.nb;
     r.id = c.id;
     r.P = gr.m.P;
+    r.c1 = gr.m.c1;
   }
   // ---- schedule tables
   uint64_t T = 0;

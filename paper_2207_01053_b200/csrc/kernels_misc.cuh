@@ -17,6 +17,12 @@ __global__ void k_admit_params(const ClientRec* __restrict__ recs, const int* __
     c->params[i] = w;
     if (sh) sh[i] = __float2bfloat16_rn(w);
   }
+  __nv_bfloat16* w1p = (__nv_bfloat16*)c->buf[B_W1P];  // conv1 shadow [c1][25][8] (ci >= 3 zero), W1 at offset 0
+  if (w1p)
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < c->c1 * 200; e += gridDim.x * blockDim.x) {
+      const int co = e / 200, tap = (e % 200) >> 3, ci = e & 7;
+      w1p[e] = __float2bfloat16_rn(ci < 3 ? c->wg[co * 75 + tap * 3 + ci] : 0.f);
+    }
   if (blockIdx.x == 0 && threadIdx.x < 16) c->stats[threadIdx.x] = 0.f;
 }
 

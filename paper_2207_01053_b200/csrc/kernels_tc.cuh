@@ -491,6 +491,170 @@ struct TcFc1Wgrad {  // M = K1 (input features), N = F (outputs), K = rows; W <-
 };
 
 // --------------------------------------------------------------------------
+// conv1 on tensor cores.  K1 (gather): the batch is staged as bf16
+// xs[r][36][36][8] = x/255 with a 2-pixel zero border and the 3 channels padded
+// to 8, so that every (pixel, tap) is one aligned 16-byte chunk.
+// --------------------------------------------------------------------------
+constexpr int kStageThreads = 256;
+__global__ void __launch_bounds__(kStageThreads)
+    k_stage_x(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, const int* __restrict__ prefix,
+              int ntask) {
+  const int ti = find_task(prefix, ntask, blockIdx.x);
+  const Task tk = tasks[ti];
+  const ClientRec* c = recs + tk.rec;
+  const int e = (blockIdx.x - __ldg(prefix + ti)) * kStageThreads + threadIdx.x;  // staged pixel index
+  if (e >= tk.rows * 1296) return;
+  const int r = e / 1296, rem = e - r * 1296, Y = rem / 36, X = rem - Y * 36;
+  const int y = Y - 2, x = X - 2;
+  uint4 out = make_uint4(0, 0, 0, 0);
+  if ((unsigned)y < 32u && (unsigned)x < 32u) {
+    const uint8_t* px = c->x + (int64_t)c->perm[tk.base + r] * 3072 + (y * 32 + x) * 3;
+    const __nv_bfloat162 v01 = __floats2bfloat162_rn(px01(px[0]), px01(px[1]));
+    const __nv_bfloat162 v2 = __floats2bfloat162_rn(px01(px[2]), 0.f);
+    out.x = *reinterpret_cast<const uint32_t*>(&v01);
+    out.y = *reinterpret_cast<const uint32_t*>(&v2);
+  }
+  reinterpret_cast<uint4*>(c->buf[B_XS])[e] = out;
+}
+
+template <int WQ>
+struct TcConv1Fwd {  // M = rows*1024 (quad-major 32x32), N = C1, K = 25 taps x 8 (ci padded) = 200 -> 256
+  typedef CnnW<WQ> W;
+  static constexpr bool A_MN = false, B_MN = false;
+  struct PA { const bf16* base; int j; };
+  struct PB { const bf16* row; int j; };
+  const ClientRec* recs;
+  CnnDims d;
+  __device__ void setup(TcTile& t, int local) const {
+    t.m0 = local * 128;
+    t.n0 = 0;
+    t.nk = 4;
+    t.n_mma = W::C1 < 16 ? 16 : W::C1;
+  }
+  __device__ const void* any(const TcTile& t) const { return t.c->params; }
+  __device__ PA a_pre(const TcTile& t, int i, int j) const {
+    const int m = t.m0 + i, r = m >> 10, p = (m >> 2) & 255, q = m & 3;
+    const int y = ((p >> 4) << 1) + (q >> 1), x = ((p & 15) << 1) + (q & 1);
+    return PA{(const bf16*)t.c->buf[B_XS] + ((int64_t)r * 1296 + y * 36 + x) * 8, j};
+  }
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
+    const int tap = kb * 8 + s.j;  // one 16-byte chunk = one tap's 8 (padded) channels
+    if (tap >= 25) return nullptr;
+    const int ky = tap / 5, kx = tap - ky * 5;
+    return s.base + (ky * 36 + kx) * 8;
+  }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const {
+    return PB{i < W::C1 ? (const bf16*)t.c->buf[B_W1P] + i * 200 : nullptr, j};
+  }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
+    const int tap = kb * 8 + s.j;
+    if (!s.row || tap >= 25) return nullptr;
+    return s.row + tap * 8;
+  }
+  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
+    const int m = t.m0 + row, r = m >> 10, p = (m & 1023) >> 2, q = m & 3;
+    const int base = (threadIdx.x & 31) & ~3;
+    bf16* a1 = (bf16*)t.c->buf[B_A1];
+    uint8_t* i1 = (uint8_t*)t.c->buf[B_I1];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int n = c0 + j;
+      const float val = n < W::C1 ? fmaxf(v[j] + t.c->params[d.b1 + n], 0.f) : 0.f;
+      const float v0 = __shfl_sync(0xffffffffu, val, base), v1 = __shfl_sync(0xffffffffu, val, base + 1);
+      const float v2 = __shfl_sync(0xffffffffu, val, base + 2), v3 = __shfl_sync(0xffffffffu, val, base + 3);
+      if (q == 0 && n < W::C1) {
+        float best = v0;
+        int arg = 0;
+        if (v1 > best) { best = v1; arg = 1; }
+        if (v2 > best) { best = v2; arg = 2; }
+        if (v3 > best) { best = v3; arg = 3; }
+        const int64_t o = ((int64_t)r * 256 + p) * W::C1 + n;
+        a1[o] = __float2bfloat16_rn(best);
+        i1[o] = (uint8_t)arg;
+      }
+    }
+  }
+};
+
+// conv1 wgrad: D[m = tap*8 + ci (+ bias row 200), n = co] = sum_p xs(p, tap, ci) dz1[p][co],
+// split-K over 2048-pixel chunks; the epilogue stores the 75 real rows + bias as
+// partial[split][76][C1] (fp32), summed in split order by k_reduce_conv1_tc.
+template <int WQ>
+struct TcConv1Wgrad {
+  typedef CnnW<WQ> W;
+  static constexpr bool A_MN = true, B_MN = true;
+  struct PA { int i, off, kind; };  // kind 0: gather (off = staged offset of the tap), 1: ones, 2: zero
+  struct PB { int i, n0; };
+  const ClientRec* recs;
+  CnnDims d;
+  __device__ void setup(TcTile& t, int local) const {
+    const int split = local >> 1;
+    t.m0 = (local & 1) * 128;
+    t.n0 = split;  // carries the split index
+    const int px = t.tk.rows * 1024 - split * kWgradChunkPx;
+    t.nk = (px < kWgradChunkPx ? px : kWgradChunkPx) / 64;
+    t.n_mma = W::C1 < 16 ? 16 : W::C1;
+  }
+  __device__ const void* any(const TcTile& t) const { return t.c->params; }
+  __device__ PA a_pre(const TcTile& t, int i, int j) const {
+    const int tap = (t.m0 >> 3) + j;
+    if (tap == 25) return PA{i, 0, 1};
+    if (tap > 25) return PA{i, 0, 2};
+    const int ky = tap / 5, kx = tap - ky * 5;
+    return PA{i, (ky * 36 + kx) * 8, 0};
+  }
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
+    if (s.kind) return s.kind == 1 ? (const void*)kOneChunk : nullptr;
+    const int p = t.n0 * kWgradChunkPx + kb * 64 + s.i, r = p >> 10, y = (p >> 5) & 31, x = p & 31;
+    return (const bf16*)t.c->buf[B_XS] + ((int64_t)r * 1296 + y * 36 + x) * 8 + s.off;
+  }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const { return PB{i, 8 * j}; }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
+    if (s.n0 >= W::C1) return nullptr;
+    const int p = t.n0 * kWgradChunkPx + kb * 64 + s.i;
+    return (const bf16*)t.c->buf[B_DZC1] + (int64_t)p * W::C1 + s.n0;
+  }
+  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
+    const int m = t.m0 + row;
+    int idx;
+    if (m == 200)
+      idx = 75;
+    else if (m < 200 && (m & 7) < 3)
+      idx = (m >> 3) * 3 + (m & 7);
+    else
+      return;
+    float* part = (float*)t.c->buf[B_WSP] + ((int64_t)t.n0 * 76 + idx) * W::C1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (c0 + j < W::C1) part[c0 + j] = v[j];
+  }
+};
+
+__global__ void __launch_bounds__(kReduceBlock)
+    k_reduce_conv1_tc(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, const int* __restrict__ prefix,
+                      int ntask, int C1, int64_t off_w, int64_t off_b, float lr) {
+  const int ti = find_task(prefix, ntask, blockIdx.x);
+  const Task tk = tasks[ti];
+  const ClientRec* c = recs + tk.rec;
+  const int total = 76 * C1;
+  const int e = (blockIdx.x - __ldg(prefix + ti)) * kReduceBlock + threadIdx.x;
+  if (e >= total) return;
+  const int splits = cdiv(tk.rows * 1024, kWgradChunkPx);
+  const float* part = (const float*)c->buf[B_WSP];
+  float g = 0.f;
+  for (int s = 0; s < splits; ++s) g += part[(int64_t)s * total + e];
+  const int idx = e / C1, co = e - idx * C1;
+  if (idx == 75) {
+    c->params[off_b + co] -= lr * g;
+  } else {
+    float* w = c->params + off_w + co * 75 + idx;
+    const float nw = *w - lr * g;
+    *w = nw;
+    ((bf16*)c->buf[B_W1P])[co * 200 + (idx / 3) * 8 + idx % 3] = __float2bfloat16_rn(nw);
+  }
+}
+
+// --------------------------------------------------------------------------
 // self-test GEMM (protea_selftest_gemm): D[M,N] = A B^T with dense bf16 operands
 // --------------------------------------------------------------------------
 struct TcDense {  // A [M][K], B [N][K] (K-major)
