@@ -58,7 +58,7 @@ def test_bf16_one_step_vs_bf16_emulated_oracle(torch, B):
     got, ex = gpu_run(wl, precision=1)
     emu = oracle_run(wl, emulate_bf16=True)
     d = rel_l2(got[4] - ex["g0"][4], emu[4] - ex["g0"][4])
-    assert d <= 2e-3, d
+    assert d <= 5e-3, d
 
 
 def test_bf16_mixed_widths(torch):
