@@ -24,6 +24,7 @@ struct ClientRec {
   int32_t pad_;
   int64_t id;
   uint64_t* sm_ns;         // per-client device-time attribution (nullable)
+  const void* tmaps;       // bf16 CNN: TM_COUNT CUtensorMaps (128 B each, global memory), else nullptr
 };
 
 // One active client in one lock-step iteration.

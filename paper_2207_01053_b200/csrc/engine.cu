@@ -11,8 +11,13 @@
 // n_k (w_k - w_g) is added to the group's fp64 accumulator, and after
 // the last iteration the ranks sum their accumulators (NCCL, the only
 // cross-GPU exchange) and every rank writes w' = w_g + acc / N.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+
+#include <array>
+#include <tuple>
 
 #include <algorithm>
 #include <cstdio>
@@ -98,7 +103,77 @@ struct protea_ctx {
   std::vector<int> ev_op;
   uint64_t op_launches[PROTEA_N_OPC] = {}, op_flops[PROTEA_N_OPC] = {}, op_bytes[PROTEA_N_OPC] = {};
   double loss_host = 0.0;
+  // TMA tensor maps per (client, slot offset, batch, group), reused across rounds
+  std::map<std::tuple<int64_t, uint64_t, int, int>, std::array<CUtensorMap, TM_COUNT>> tmap_cache;
+  DevArray<CUtensorMap> tmaps;
 };
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool tmap_encode(CUtensorMap* m, const void* addr, int rank, const uint64_t* dims, const uint64_t* strides,
+                 const uint32_t* box) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&g_encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !g_encode)
+      return false;
+  }
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(addr), (const cuuint64_t*)dims,
+                  (const cuuint64_t*)strides, (const cuuint32_t*)box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// The TMA tensor maps of one bf16-mode CNN client (see TmapId in kernels_tc.cuh).
+bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap* out) {
+  const uint64_t C1 = m.c1, C2 = m.c2, F = m.f, K1 = 64 * C2, Bk = B, R = (B + 15) & ~15;
+  const uint8_t* wsh = (const uint8_t*)r.buf[B_WSH];
+  const void* w2 = wsh + 2 * m.layers[1].off_w;
+  const void* w3 = wsh + 2 * m.layers[2].off_w;
+  bool ok = true;
+  {
+    const uint64_t d[4] = {C1, 16, 16, Bk}, st[3] = {C1 * 2, 32 * C1, 512 * C1};
+    const uint32_t b8[4] = {8, 16, 8, 1}, b4[4] = {8, 16, 4, 1};
+    ok &= tmap_encode(&out[TM_A1], r.buf[B_A1], 4, d, st, b8);
+    ok &= tmap_encode(&out[TM_A1W], r.buf[B_A1], 4, d, st, b4);
+  }
+  {
+    const uint64_t d[4] = {C2, 16, 16, Bk}, st[3] = {C2 * 2, 32 * C2, 512 * C2};
+    const uint32_t b8[4] = {8, 16, 8, 1}, b4[4] = {8, 16, 4, 1};
+    ok &= tmap_encode(&out[TM_DZ2], r.buf[B_DZ2], 4, d, st, b8);
+    ok &= tmap_encode(&out[TM_DZ2W], r.buf[B_DZ2], 4, d, st, b4);
+  }
+  {
+    const uint64_t d[2] = {25 * C1, C2}, st[1] = {50 * C1};
+    const uint32_t bx[2] = {8, (uint32_t)C2};
+    ok &= tmap_encode(&out[TM_W2F], w2, 2, d, st, bx);
+  }
+  {
+    const uint64_t d[3] = {C1, 25, C2}, st[2] = {2 * C1, 50 * C1};
+    const uint32_t bx[3] = {8, 1, (uint32_t)C2};
+    ok &= tmap_encode(&out[TM_W2D], w2, 3, d, st, bx);
+  }
+  {
+    const uint64_t d[2] = {K1, F}, st[1] = {2 * K1};
+    const uint32_t bk[2] = {8, 128}, bm[2] = {8, 64};
+    ok &= tmap_encode(&out[TM_W3K], w3, 2, d, st, bk);
+    ok &= tmap_encode(&out[TM_W3M], w3, 2, d, st, bm);
+  }
+  {
+    const uint64_t d[2] = {K1, Bk}, st[1] = {2 * K1};
+    const uint32_t bx[2] = {8, (uint32_t)R};
+    ok &= tmap_encode(&out[TM_A2], r.buf[B_A2], 2, d, st, bx);
+  }
+  {
+    const uint64_t d[2] = {F, Bk}, st[1] = {2 * F};
+    const uint32_t bx[2] = {8, (uint32_t)R};
+    ok &= tmap_encode(&out[TM_DH], r.buf[B_DH], 2, d, st, bx);
+  }
+  return ok;
+}
+}  // namespace
 
 namespace {
 // Bracket one launch of op class `op` with CUDA events if requested.
@@ -300,7 +375,21 @@ void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, c
   op_end(ctx, ev);
 }
 
-// bf16 mode, CNN: conv2 and fc1 (fwd / dgrad / wgrad) on tcgen05; conv1 and the head on SIMT
+template <class OpT>
+OpT tma_op(const ClientRec* recs, const CnnDims& d) {
+  OpT op;
+  op.recs = recs;
+  op.d = d;
+  return op;
+}
+template <class OpT>
+OpT tma_op_lr(const ClientRec* recs, const CnnDims& d, float lr) {
+  OpT op = tma_op<OpT>(recs, d);
+  op.lr = lr;
+  return op;
+}
+
+// bf16 mode, CNN: conv1, conv2 and fc1 (fwd / dgrad / wgrad) on tcgen05; the head on SIMT
 template <int WQ>
 void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs,
                       const int32_t* dtab, float lr) {
@@ -312,16 +401,16 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
                                                                   L.ntask);
   op_end(ctx, ev);
   launch_gemm_tc<TC_C1F_BN, TC_STAGES>(ctx, TcConv1Fwd<WQ>{drecs, d}, L, OP_C1F, dtab);
-  launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TcConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
-  launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, TcFc1Fwd<WQ>{drecs, d}, L, OP_F1F, dtab);
+  launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TmaConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
+  launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
   HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
   ev = op_begin(ctx, OP_HEAD);
   k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
   op_end(ctx, ev);
-  launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, TcFc1Dgrad<WQ>{drecs, d}, L, OP_F1D, dtab);
+  launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab);
   launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
-  launch_gemm_tc<TC_C2D_BN, TC_STAGES>(ctx, TcConv2Dgrad<WQ>{drecs, d}, L, OP_C2D, dtab);
-  launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, TcConv2Wgrad<WQ>{drecs, d, lr}, L, OP_C2W, dtab);
+  launch_gemm_tc<TC_C2D_BN, TC_STAGES>(ctx, tma_op<TmaConv2Dgrad<WQ>>(drecs, d), L, OP_C2D, dtab);
+  launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2Wgrad<WQ>>(drecs, d, lr), L, OP_C2W, dtab);
   launch_gemm_tc<TC_C1W_BN, TC_STAGES>(ctx, TcConv1Wgrad<WQ>{drecs, d}, L, OP_C1W, dtab);
   ev = op_begin(ctx, OP_C1R);
   k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->stream>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
@@ -595,6 +684,32 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     r.id = c.id;
     r.P = gr.m.P;
     r.c1 = gr.m.c1;
+  }
+  // ---- TMA tensor maps (bf16 CNN clients)
+  if (tc_mode) {
+    std::vector<CUtensorMap> maps;
+    std::vector<int> owner;
+    for (size_t i = 0; i < rc.size(); ++i) {
+      const ModelDims& m = ctx->groups[rc[i].group].m;
+      if (m.arch != PROTEA_MODEL_CNN) continue;
+      auto key = std::make_tuple(rc[i].id, rc[i].offset, rc[i].B, rc[i].group);
+      auto it = ctx->tmap_cache.find(key);
+      if (it == ctx->tmap_cache.end()) {
+        std::array<CUtensorMap, TM_COUNT> a;
+        if (!build_cnn_tmaps(m, recs[i], rc[i].B, a.data()))
+          return fail(ctx, PROTEA_ERR_CUDA, "run_round: cuTensorMapEncodeTiled failed for client " +
+                                               std::to_string(rc[i].id));
+        it = ctx->tmap_cache.emplace(key, a).first;
+      }
+      owner.push_back((int)i);
+      maps.insert(maps.end(), it->second.begin(), it->second.end());
+    }
+    if (!maps.empty()) {
+      CK(ctx->tmaps.reserve(maps.size()));
+      CK(cudaMemcpyAsync(ctx->tmaps.p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice,
+                         ctx->stream));
+      for (size_t k = 0; k < owner.size(); ++k) recs[owner[k]].tmaps = ctx->tmaps.p + k * TM_COUNT;
+    }
   }
   // ---- schedule tables
   uint64_t T = 0;

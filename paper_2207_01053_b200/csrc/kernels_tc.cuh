@@ -64,9 +64,24 @@ constexpr int tc_smem_bytes() {
   return STAGES * (128 * 64 * 2 + BN * 64 * 2) + (2 * STAGES + 1) * 8 + 16;
 }
 
+// Default UMMA descriptors of the cp.async layouts (see tc.cuh).
+template <bool MN, int R>
+__device__ __forceinline__ uint64_t cp_desc(uint32_t base, int ks) {
+  return MN ? tc::sdesc(base + 32 * R * ks, 16 * R, 128) : tc::sdesc(base + 256 * ks, 128, 1024);
+}
+template <class Op>
+struct has_tma {
+  template <class U>
+  static constexpr bool f(decltype(U::TMA)*) { return U::TMA; }
+  template <class U>
+  static constexpr bool f(...) { return false; }
+  static constexpr bool value = f<Op>(nullptr);
+};
+
 template <int BN, int STAGES, class Op>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_gemm_tc(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
+  constexpr bool TMA = has_tma<Op>::value;
   constexpr int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
   constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   constexpr int LAG = (STAGES - 1) < 2 ? (STAGES - 1) : 2;
@@ -88,21 +103,40 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t done = bar0 + 16 * STAGES;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      tc::mbar_init(bar0 + 8 * s, kTcProd);         // full[s]: one arrive per producer thread
+      tc::mbar_init(bar0 + 8 * s, TMA ? 1 : kTcProd);  // full[s]: TMA expect_tx, or one arrive per producer
       tc::mbar_init(bar0 + 8 * (STAGES + s), 1);    // empty[s]: tcgen05.commit
     }
     tc::mbar_init(done, 1);
     tc::mbar_fence_init();
   }
   if (warp == 8) tc::tmem_alloc(tc::smem_u32(tmem_slot), TMEM_COLS);
+  const uint32_t sbase = tc::smem_u32(smem);
+  if constexpr (TMA) {
+    if (warp < 8) {  // constant operand groups (e.g. the bias "ones" row), written once into every stage
+      for (int s = 0; s < STAGES; ++s) op.init_stage(t, smem + s * STAGE, smem + s * STAGE + A_BYTES);
+      tc::fence_proxy_async();
+    }
+  }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t sbase = tc::smem_u32(smem);
 
+  if constexpr (TMA) {
+    if (warp == 0 && lane == 0) {
+      // ---------------- TMA producer (one thread)
+      for (int kb = 0; kb < t.nk; ++kb) {
+        const int s = kb % STAGES;
+        if (kb >= STAGES) tc::mbar_wait(bar0 + 8 * (STAGES + s), ((kb / STAGES) - 1) & 1);
+        const uint32_t a_base = sbase + s * STAGE, b_base = a_base + A_BYTES;
+        tc::mbar_expect_tx(bar0 + 8 * s, op.tx_bytes(t, kb));
+        op.tma_issue(t, kb, a_base, b_base, bar0 + 8 * s);
+      }
+    }
+  }
   if (warp < 8) {
-    // ---------------- producers
+    // ---------------- cp.async producers
+    if constexpr (!TMA) {
     const int tid = threadIdx.x;
     const void* any = op.any(t);
     typename Op::PA pa[NA];
@@ -138,6 +172,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc::cp_wait<0>();
     tc::fence_proxy_async();
     for (int kb = (t.nk - LAG > 0 ? t.nk - LAG : 0); kb < t.nk; ++kb) tc::mbar_arrive(bar0 + 8 * (kb % STAGES));
+    }
 
     // ---------------- epilogue: TMEM -> registers -> fused layer epilogue
     tc::mbar_wait(done, 0);
@@ -159,10 +194,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t a_base = sbase + s * STAGE, b_base = a_base + A_BYTES;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          const uint64_t da = Op::A_MN ? tc::sdesc(a_base + 32 * 128 * ks, 16 * 128, 128)
-                                       : tc::sdesc(a_base + 256 * ks, 128, 1024);
-          const uint64_t db = Op::B_MN ? tc::sdesc(b_base + 32 * BN * ks, 16 * BN, 128)
-                                       : tc::sdesc(b_base + 256 * ks, 128, 1024);
+          uint64_t da, db;
+          if constexpr (TMA) {
+            da = op.a_desc(t, a_base, ks);
+            db = op.b_desc(t, b_base, ks);
+          } else {
+            da = cp_desc<Op::A_MN, 128>(a_base, ks);
+            db = cp_desc<Op::B_MN, BN>(b_base, ks);
+          }
           tc::mma_bf16(tmem, da, db, idesc, (kb | ks) != 0);
         }
         tc::commit(bar0 + 8 * (STAGES + s));
@@ -487,6 +526,195 @@ struct TcFc1Wgrad {  // M = K1 (input features), N = F (outputs), K = rows; W <-
       P[(f0 + j) * W::K1] = nw;
       S[(f0 + j) * W::K1] = __float2bfloat16_rn(nw);
     }
+  }
+};
+
+// --------------------------------------------------------------------------
+// TMA-fed ops.  Operand tiles are loaded by the Tensor Memory Accelerator from
+// per-client tensor maps (built on the host per slot, kept in global memory):
+// every box is "8 channels x R rows" of 16-byte rows, which lands in shared
+// memory as R consecutive 16-byte rows = UMMA canonical core matrices; conv
+// halos (zero padding) are the TMA's out-of-bounds zero fill.  This bypasses
+// L1 (the cp.async gathers above were L1TEX-throughput bound) and leaves one
+// thread issuing ~16-24 bulk copies per 64-wide K block.
+// --------------------------------------------------------------------------
+enum TmapId : int {
+  TM_A1 = 0,   // a1  [B][16][16][C1] box (8,16,8,1)   conv2 fwd A
+  TM_A1W,      // a1                box (8,16,4,1)   conv2 wgrad A
+  TM_DZ2,      // dz2 [B][16][16][C2] box (8,16,8,1) conv2 dgrad A
+  TM_DZ2W,     // dz2               box (8,16,4,1)   conv2 wgrad B
+  TM_W2F,      // W2 shadow (25C1, C2)   box (8, C2) conv2 fwd B
+  TM_W2D,      // W2 shadow (C1, 25, C2) box (8,1,C2) conv2 dgrad B
+  TM_W3K,      // W3 shadow (K1, F)      box (8,128) fc1 fwd A
+  TM_W3M,      // W3 shadow (K1, F)      box (8,64)  fc1 dgrad A
+  TM_A2,       // a2 (K1, B)             box (8,R)   fc1 fwd B
+  TM_DH,       // dh (F, B)              box (8,R)   fc1 dgrad B
+  TM_COUNT
+};
+
+__device__ __forceinline__ const void* tmap_of(const TcTile& t, int id) {
+  return reinterpret_cast<const uint8_t*>(t.c->tmaps) + 128 * id;
+}
+
+template <int WQ>
+struct TmaConv2Fwd {  // M = rows*256 (natural order, tile = 8 image rows), N = C2, K = 25 C1
+  typedef CnnW<WQ> W;
+  static constexpr bool TMA = true, A_MN = false, B_MN = false;
+  const ClientRec* recs;
+  CnnDims d;
+  __device__ void setup(TcTile& t, int local) const {
+    t.m0 = local * 128;
+    t.n0 = 0;
+    t.nk = (25 * W::C1 + 63) / 64;
+    t.n_mma = W::C2 < 16 ? 16 : W::C2;
+  }
+  __device__ void init_stage(const TcTile&, uint8_t*, uint8_t*) const {}
+  __device__ uint32_t tx_bytes(const TcTile& t, int kb) const { return 16384 + 8 * 16 * W::C2; }
+  __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
+    const int r = t.m0 >> 8, y0 = (t.m0 >> 4) & 15;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = kb * 64 + 8 * j, tap = k >> W::L1, cc = k & (W::C1 - 1), ky = tap / 5, kx = tap - ky * 5;
+      tc::tma_load_4d(a + 2048 * j, tmap_of(t, TM_A1), mbar, cc, kx - 2, tap < 25 ? y0 + ky - 2 : -64, r);
+      tc::tma_load_2d(b + 16 * W::C2 * j, tmap_of(t, TM_W2F), mbar, k, 0);
+    }
+  }
+  __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {
+    return tc::sdesc(base + 4096 * ks, 2048, 128);
+  }
+  __device__ uint64_t b_desc(const TcTile&, uint32_t base, int ks) const {
+    return tc::sdesc(base + 32 * W::C2 * ks, 16 * W::C2, 128);
+  }
+  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
+    // natural pixel order: a warp holds image rows y (lanes 0-15) and y+1 (lanes 16-31)
+    const int lane = threadIdx.x & 31, base = lane & 14;
+    const int m = t.m0 + row, r = m >> 8, y = (m >> 4) & 15, x = m & 15;
+    const bool writer = lane < 16 && (lane & 1) == 0;
+    bf16* a2 = (bf16*)t.c->buf[B_A2];
+    uint8_t* i2 = (uint8_t*)t.c->buf[B_I2];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int n = c0 + j;
+      const float val = n < W::C2 ? fmaxf(v[j] + t.c->params[d.b2 + n], 0.f) : 0.f;
+      const float v0 = __shfl_sync(0xffffffffu, val, base), v1 = __shfl_sync(0xffffffffu, val, base + 1);
+      const float v2 = __shfl_sync(0xffffffffu, val, base + 16), v3 = __shfl_sync(0xffffffffu, val, base + 17);
+      if (writer && n < W::C2) {
+        float best = v0;
+        int arg = 0;
+        if (v1 > best) { best = v1; arg = 1; }
+        if (v2 > best) { best = v2; arg = 2; }
+        if (v3 > best) { best = v3; arg = 3; }
+        const int64_t o = ((int64_t)r * 64 + (y >> 1) * 8 + (x >> 1)) * W::C2 + n;
+        a2[o] = __float2bfloat16_rn(best);
+        i2[o] = (uint8_t)arg;
+      }
+    }
+  }
+};
+
+template <int WQ>
+struct TmaConv2Dgrad : TcConv2Dgrad<WQ> {  // same GEMM and epilogue, operands by TMA
+  typedef CnnW<WQ> W;
+  static constexpr bool TMA = true;
+  __device__ void init_stage(const TcTile&, uint8_t*, uint8_t*) const {}
+  __device__ uint32_t tx_bytes(const TcTile& t, int kb) const { return 16384 + (uint32_t)t.n_mma * 128; }
+  __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
+    const int r = t.m0 >> 8, y0 = (t.m0 >> 4) & 15;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = kb * 64 + 8 * j, tap = k >> W::L2, cc = k & (W::C2 - 1), ky = tap / 5, kx = tap - ky * 5;
+      tc::tma_load_4d(a + 2048 * j, tmap_of(t, TM_DZ2), mbar, cc, 2 - kx, tap < 25 ? y0 + 2 - ky : -64, r);
+    }
+    constexpr int NTB = 64 / W::C2;  // taps per K block
+#pragma unroll
+    for (int tb = 0; tb < NTB; ++tb)
+      for (int nc = 0; nc < t.n_mma / 8; ++nc)
+        tc::tma_load_3d(b + 1024 * nc + 16 * W::C2 * tb, tmap_of(t, TM_W2D), mbar, 8 * nc, kb * NTB + tb, 0);
+  }
+  __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {
+    return tc::sdesc(base + 4096 * ks, 2048, 128);
+  }
+  __device__ uint64_t b_desc(const TcTile&, uint32_t base, int ks) const {
+    return tc::sdesc(base + 256 * ks, 128, 1024);  // MN-major: k rows at 16 B, n chunks at 1 KB
+  }
+};
+
+template <int WQ>
+struct TmaConv2Wgrad : TcConv2Wgrad<WQ> {  // same GEMM and epilogue, operands by TMA
+  typedef CnnW<WQ> W;
+  static constexpr bool TMA = true;
+  __device__ void init_stage(const TcTile& t, uint8_t* a, uint8_t* b) const {
+    // m groups at/after the bias row: constant chunks ([1,0..] per pixel, or zeros), 64 rows x 16 B each
+    for (int g = 0; g < 16; ++g) {
+      const int mg = t.m0 + 8 * g, Kw = 25 * W::C1;
+      if (mg < Kw) continue;
+      const uint4 val = mg == Kw ? make_uint4(0x3F80u, 0, 0, 0) : make_uint4(0, 0, 0, 0);
+      for (int i = threadIdx.x; i < 64; i += kTcProd) reinterpret_cast<uint4*>(a + 1024 * g)[i] = val;
+    }
+  }
+  __device__ uint32_t tx_bytes(const TcTile& t, int kb) const {
+    const int valid = (25 * W::C1 - t.m0) / 8;  // m groups loaded by TMA
+    return 1024u * (valid < 16 ? (valid < 0 ? 0 : valid) : 16) + 1024u * (W::C2 / 8);
+  }
+  __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
+    const int r = kb >> 2, y0 = (kb & 3) * 4;
+    for (int g = 0; g < 16; ++g) {
+      const int mg = t.m0 + 8 * g;
+      if (mg >= 25 * W::C1) break;
+      const int tap = mg >> W::L1, cc = mg & (W::C1 - 1), ky = tap / 5, kx = tap - ky * 5;
+      tc::tma_load_4d(a + 1024 * g, tmap_of(t, TM_A1W), mbar, cc, kx - 2, y0 + ky - 2, r);
+    }
+#pragma unroll
+    for (int nc = 0; nc < W::C2 / 8; ++nc) tc::tma_load_4d(b + 1024 * nc, tmap_of(t, TM_DZ2W), mbar, 8 * nc, 0, y0, r);
+  }
+  __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const { return tc::sdesc(base + 256 * ks, 128, 1024); }
+  __device__ uint64_t b_desc(const TcTile&, uint32_t base, int ks) const { return tc::sdesc(base + 256 * ks, 128, 1024); }
+};
+
+__device__ __forceinline__ int batch_rows16(const TcTile& t) { return (t.c->B + 15) & ~15; }
+
+template <int WQ>
+struct TmaFc1Fwd : TcFc1Fwd<WQ> {
+  typedef CnnW<WQ> W;
+  static constexpr bool TMA = true;
+  __device__ void init_stage(const TcTile&, uint8_t*, uint8_t*) const {}
+  __device__ uint32_t tx_bytes(const TcTile& t, int kb) const { return 16384 + 128 * batch_rows16(t); }
+  __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
+    const int R = batch_rows16(t);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      tc::tma_load_2d(a + 2048 * j, tmap_of(t, TM_W3K), mbar, kb * 64 + 8 * j, t.m0);
+      tc::tma_load_2d(b + 16 * R * j, tmap_of(t, TM_A2), mbar, kb * 64 + 8 * j, 0);
+    }
+  }
+  __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {
+    return tc::sdesc(base + 4096 * ks, 2048, 128);
+  }
+  __device__ uint64_t b_desc(const TcTile& t, uint32_t base, int ks) const {
+    const int R = batch_rows16(t);
+    return tc::sdesc(base + 32 * R * ks, 16 * R, 128);
+  }
+};
+
+template <int WQ>
+struct TmaFc1Dgrad : TcFc1Dgrad<WQ> {
+  typedef CnnW<WQ> W;
+  static constexpr bool TMA = true;
+  __device__ void init_stage(const TcTile&, uint8_t*, uint8_t*) const {}
+  __device__ uint32_t tx_bytes(const TcTile& t, int kb) const { return 16384 + 128 * batch_rows16(t); }
+  __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
+    const int R = batch_rows16(t);
+#pragma unroll
+    for (int g = 0; g < 16; ++g) tc::tma_load_2d(a + 1024 * g, tmap_of(t, TM_W3M), mbar, t.m0 + 8 * g, kb * 64);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tc::tma_load_2d(b + 16 * R * j, tmap_of(t, TM_DH), mbar, kb * 64 + 8 * j, 0);
+  }
+  __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {
+    return tc::sdesc(base + 256 * ks, 128, 1024);  // MN-major: k rows at 16 B, m groups at 1 KB
+  }
+  __device__ uint64_t b_desc(const TcTile& t, uint32_t base, int ks) const {
+    const int R = batch_rows16(t);
+    return tc::sdesc(base + 32 * R * ks, 16 * R, 128);
   }
 };
 
