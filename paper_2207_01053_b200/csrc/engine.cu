@@ -104,7 +104,7 @@ struct protea_ctx {
   uint64_t op_launches[PROTEA_N_OPC] = {}, op_flops[PROTEA_N_OPC] = {}, op_bytes[PROTEA_N_OPC] = {};
   double loss_host = 0.0;
   // TMA tensor maps per (client, slot offset, batch, group), reused across rounds
-  std::map<std::tuple<int64_t, uint64_t, int, int>, std::array<CUtensorMap, TM_COUNT>> tmap_cache;
+  std::map<std::tuple<uint64_t, int, int, int64_t, int>, std::array<CUtensorMap, TM_COUNT>> tmap_cache;  // (offset, B, E, n, group): everything the slot layout depends on
   DevArray<CUtensorMap> tmaps;
 };
 
@@ -692,7 +692,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     for (size_t i = 0; i < rc.size(); ++i) {
       const ModelDims& m = ctx->groups[rc[i].group].m;
       if (m.arch != PROTEA_MODEL_CNN) continue;
-      auto key = std::make_tuple(rc[i].id, rc[i].offset, rc[i].B, rc[i].group);
+      auto key = std::make_tuple(rc[i].offset, rc[i].B, rc[i].E, rc[i].n, rc[i].group);
       auto it = ctx->tmap_cache.find(key);
       if (it == ctx->tmap_cache.end()) {
         std::array<CUtensorMap, TM_COUNT> a;
