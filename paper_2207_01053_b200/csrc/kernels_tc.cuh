@@ -220,6 +220,73 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
 __device__ __forceinline__ int round16(int x) { return (x + 15) & ~15; }
 
+// Vectorised epilogue helpers: a thread owns 16 consecutive channels of one pixel.
+template <int N>  // N = 8 or 16 bf16
+__device__ __forceinline__ void st_bf16(bf16* dst, const float* v) {
+  uint32_t w[N / 2];
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    w[i] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  if (N == 16) reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+template <int N>
+__device__ __forceinline__ void ld_bf16(const bf16* src, float* v) {
+  uint4 q[2];
+  q[0] = reinterpret_cast<const uint4*>(src)[0];
+  if (N == 16) q[1] = reinterpret_cast<const uint4*>(src)[1];
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(q);
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+    v[2 * i] = __low2float(h);
+    v[2 * i + 1] = __high2float(h);
+  }
+}
+template <int N>
+__device__ __forceinline__ void st_u8(uint8_t* dst, const int* a) {
+  uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < N; ++i) w[i >> 2] |= (uint32_t)a[i] << (8 * (i & 3));
+  if (N == 16)
+    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+  else
+    *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+}
+template <int N>
+__device__ __forceinline__ void ld_u8(const uint8_t* src, int* a) {
+  uint32_t w[4];
+  if (N == 16) {
+    const uint4 q = *reinterpret_cast<const uint4*>(src);
+    w[0] = q.x, w[1] = q.y, w[2] = q.z, w[3] = q.w;
+  } else {
+    const uint2 q = *reinterpret_cast<const uint2*>(src);
+    w[0] = q.x, w[1] = q.y;
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i] = (w[i >> 2] >> (8 * (i & 3))) & 0xFF;
+}
+
+// 2x2 max-pool of a warp's 16 columns: values of the 4 window lanes (q order
+// (0,0),(0,1),(1,0),(1,1)), first maximum wins (strict >); result in the writer lane.
+__device__ __forceinline__ void pool_lanes(const float (&val)[16], int l0, int l1, int l2, int l3, float (&best)[16],
+                                           int (&arg)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float v0 = __shfl_sync(0xffffffffu, val[j], l0), v1 = __shfl_sync(0xffffffffu, val[j], l1);
+    const float v2 = __shfl_sync(0xffffffffu, val[j], l2), v3 = __shfl_sync(0xffffffffu, val[j], l3);
+    float b = v0;
+    int a = 0;
+    if (v1 > b) { b = v1; a = 1; }
+    if (v2 > b) { b = v2; a = 2; }
+    if (v3 > b) { b = v3; a = 3; }
+    best[j] = b;
+    arg[j] = a;
+  }
+}
+
 // compile-time CNN-w channel counts for width WQ/4
 template <int WQ>
 struct CnnW {
@@ -327,22 +394,20 @@ struct TcConv2Dgrad {
     return (const bf16*)t.c->buf[B_WSH] + d.w2 + (co * 25 + tap) * W::C1 + s.n0;
   }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
+    constexpr int N = W::C1 < 16 ? W::C1 : 16;  // valid channels in this 16-column chunk
     const int m = t.m0 + row, r = m >> 8, y = (m >> 4) & 15, x = m & 15;
-    const bf16* a1 = (const bf16*)t.c->buf[B_A1];
-    const uint8_t* i1 = (const uint8_t*)t.c->buf[B_I1];
+    const int64_t o = (int64_t)m * W::C1 + c0;
+    float a[N], out[N];
+    int arg[N];
+    ld_bf16<N>((const bf16*)t.c->buf[B_A1] + o, a);
+    ld_u8<N>((const uint8_t*)t.c->buf[B_I1] + o, arg);
     bf16* dz1 = (bf16*)t.c->buf[B_DZC1];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int n = c0 + j;
-      if (n >= W::C1) continue;
-      const int64_t o = (int64_t)m * W::C1 + n;
-      const float val = __bfloat162float(a1[o]) > 0.f ? v[j] : 0.f;
-      const int arg = i1[o];
+    for (int q = 0; q < 4; ++q) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int Y = 2 * y + (q >> 1), X = 2 * x + (q & 1);
-        dz1[((int64_t)r * 1024 + Y * 32 + X) * W::C1 + n] = __float2bfloat16_rn(q == arg ? val : 0.f);
-      }
+      for (int j = 0; j < N; ++j) out[j] = (arg[j] == q && a[j] > 0.f) ? v[j] : 0.f;
+      const int Y = 2 * y + (q >> 1), X = 2 * x + (q & 1);
+      st_bf16<N>(dz1 + ((int64_t)r * 1024 + Y * 32 + X) * W::C1 + c0, out);
     }
   }
 };
@@ -587,27 +652,18 @@ struct TmaConv2Fwd {  // M = rows*256 (natural order, tile = 8 image rows), N = 
   }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
     // natural pixel order: a warp holds image rows y (lanes 0-15) and y+1 (lanes 16-31)
+    constexpr int N = W::C2 < 16 ? W::C2 : 16;
     const int lane = threadIdx.x & 31, base = lane & 14;
     const int m = t.m0 + row, r = m >> 8, y = (m >> 4) & 15, x = m & 15;
-    const bool writer = lane < 16 && (lane & 1) == 0;
-    bf16* a2 = (bf16*)t.c->buf[B_A2];
-    uint8_t* i2 = (uint8_t*)t.c->buf[B_I2];
+    float val[16], best[16];
+    int arg[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int n = c0 + j;
-      const float val = n < W::C2 ? fmaxf(v[j] + t.c->params[d.b2 + n], 0.f) : 0.f;
-      const float v0 = __shfl_sync(0xffffffffu, val, base), v1 = __shfl_sync(0xffffffffu, val, base + 1);
-      const float v2 = __shfl_sync(0xffffffffu, val, base + 16), v3 = __shfl_sync(0xffffffffu, val, base + 17);
-      if (writer && n < W::C2) {
-        float best = v0;
-        int arg = 0;
-        if (v1 > best) { best = v1; arg = 1; }
-        if (v2 > best) { best = v2; arg = 2; }
-        if (v3 > best) { best = v3; arg = 3; }
-        const int64_t o = ((int64_t)r * 64 + (y >> 1) * 8 + (x >> 1)) * W::C2 + n;
-        a2[o] = __float2bfloat16_rn(best);
-        i2[o] = (uint8_t)arg;
-      }
+    for (int j = 0; j < 16; ++j) val[j] = j < N ? fmaxf(v[j] + t.c->params[d.b2 + c0 + j], 0.f) : 0.f;
+    pool_lanes(val, base, base + 1, base + 16, base + 17, best, arg);
+    if (lane < 16 && (lane & 1) == 0) {
+      const int64_t o = ((int64_t)r * 64 + (y >> 1) * 8 + (x >> 1)) * W::C2 + c0;
+      st_bf16<N>((bf16*)t.c->buf[B_A2] + o, best);
+      st_u8<N>((uint8_t*)t.c->buf[B_I2] + o, arg);
     }
   }
 };
@@ -780,26 +836,18 @@ struct TcConv1Fwd {  // M = rows*1024 (quad-major 32x32), N = C1, K = 25 taps x 
     return s.row + tap * 8;
   }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
+    constexpr int N = W::C1 < 16 ? W::C1 : 16;
     const int m = t.m0 + row, r = m >> 10, p = (m & 1023) >> 2, q = m & 3;
     const int base = (threadIdx.x & 31) & ~3;
-    bf16* a1 = (bf16*)t.c->buf[B_A1];
-    uint8_t* i1 = (uint8_t*)t.c->buf[B_I1];
+    float val[16], best[16];
+    int arg[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int n = c0 + j;
-      const float val = n < W::C1 ? fmaxf(v[j] + t.c->params[d.b1 + n], 0.f) : 0.f;
-      const float v0 = __shfl_sync(0xffffffffu, val, base), v1 = __shfl_sync(0xffffffffu, val, base + 1);
-      const float v2 = __shfl_sync(0xffffffffu, val, base + 2), v3 = __shfl_sync(0xffffffffu, val, base + 3);
-      if (q == 0 && n < W::C1) {
-        float best = v0;
-        int arg = 0;
-        if (v1 > best) { best = v1; arg = 1; }
-        if (v2 > best) { best = v2; arg = 2; }
-        if (v3 > best) { best = v3; arg = 3; }
-        const int64_t o = ((int64_t)r * 256 + p) * W::C1 + n;
-        a1[o] = __float2bfloat16_rn(best);
-        i1[o] = (uint8_t)arg;
-      }
+    for (int j = 0; j < 16; ++j) val[j] = j < N ? fmaxf(v[j] + t.c->params[d.b1 + c0 + j], 0.f) : 0.f;
+    pool_lanes(val, base, base + 1, base + 2, base + 3, best, arg);
+    if (q == 0) {
+      const int64_t o = ((int64_t)r * 256 + p) * W::C1 + c0;
+      st_bf16<N>((bf16*)t.c->buf[B_A1] + o, best);
+      st_u8<N>((uint8_t*)t.c->buf[B_I1] + o, arg);
     }
   }
 };
