@@ -34,6 +34,7 @@
 #include "kernels_misc.cuh"
 #include "kernels_simt.cuh"
 #include "kernels_tc.cuh"
+#include "kernels_conv.cuh"
 
 namespace protea {
 
@@ -135,15 +136,17 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
   bool ok = true;
   {
     const uint64_t d[4] = {C1, 16, 16, Bk}, st[3] = {C1 * 2, 32 * C1, 512 * C1};
-    const uint32_t b8[4] = {8, 16, 8, 1}, b4[4] = {8, 16, 4, 1};
+    const uint32_t b8[4] = {8, 16, 8, 1}, b4[4] = {8, 16, 4, 1}, b12[4] = {8, 16, 12, 1};
     ok &= tmap_encode(&out[TM_A1], r.buf[B_A1], 4, d, st, b8);
     ok &= tmap_encode(&out[TM_A1W], r.buf[B_A1], 4, d, st, b4);
+    ok &= tmap_encode(&out[TM_A1H], r.buf[B_A1], 4, d, st, b12);
   }
   {
     const uint64_t d[4] = {C2, 16, 16, Bk}, st[3] = {C2 * 2, 32 * C2, 512 * C2};
-    const uint32_t b8[4] = {8, 16, 8, 1}, b4[4] = {8, 16, 4, 1};
+    const uint32_t b8[4] = {8, 16, 8, 1}, b4[4] = {8, 16, 4, 1}, b12[4] = {8, 16, 12, 1};
     ok &= tmap_encode(&out[TM_DZ2], r.buf[B_DZ2], 4, d, st, b8);
     ok &= tmap_encode(&out[TM_DZ2W], r.buf[B_DZ2], 4, d, st, b4);
+    ok &= tmap_encode(&out[TM_DZ2H], r.buf[B_DZ2], 4, d, st, b12);
   }
   {
     const uint64_t d[2] = {25 * C1, C2}, st[1] = {50 * C1};
@@ -251,11 +254,11 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
       case OP_C1F: return rows * 8;
       case OP_C1W: return 2 * cdiv(rows * 1024, kWgradChunkPx);
       case OP_C1R: return cdiv(76 * m.c1, kReduceBlock);
-      case OP_C2F: return rows * 2;
+      case OP_C2F: return m.c1 >= 16 ? cdiv(rows * 2, kConvTPC) : rows * 2;  // halo kernel unless width 1/4
       case OP_F1F: return m.f / 128;
       case OP_F1D: return 64 * m.c2 / 128;
       case OP_F1W: return (64 * m.c2 / 128) * cdiv(m.f, 256);
-      case OP_C2D: return rows * 2;
+      case OP_C2D: return cdiv(rows * 2, kConvTPC);
       case OP_C2W: return cdiv(25 * m.c1 + 1, 128);
       default: break;
     }
@@ -375,6 +378,25 @@ void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, c
   op_end(ctx, ev);
 }
 
+template <int WQ, bool DGRAD>
+void launch_conv_halo(protea_ctx* ctx, const ClientRec* drecs, const CnnDims& d, const Launch& L, int opid,
+                      const int32_t* dtab) {
+  typedef HaloConv2<WQ, DGRAD> Op;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_conv_halo<WQ, DGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
+    attr = true;
+  }
+  Op op;
+  op.recs = drecs;
+  op.d = d;
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const int ev = op_begin(ctx, opid);
+  k_conv_halo<WQ, DGRAD><<<L.grid[opid], kConvThreads, Op::SMEM, ctx->stream>>>(op, tasks, dtab + L.prefix_off[opid],
+                                                                                 L.ntask);
+  op_end(ctx, ev);
+}
+
 template <class OpT>
 OpT tma_op(const ClientRec* recs, const CnnDims& d) {
   OpT op;
@@ -401,7 +423,10 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
                                                                   L.ntask);
   op_end(ctx, ev);
   launch_gemm_tc<TC_C1F_BN, TC_STAGES>(ctx, TcConv1Fwd<WQ>{drecs, d}, L, OP_C1F, dtab);
-  launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TmaConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
+  if constexpr (WQ >= 2)
+    launch_conv_halo<WQ, false>(ctx, drecs, d, L, OP_C2F, dtab);
+  else
+    launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TmaConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
   launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
   HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
   ev = op_begin(ctx, OP_HEAD);
@@ -409,7 +434,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   op_end(ctx, ev);
   launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab);
   launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
-  launch_gemm_tc<TC_C2D_BN, TC_STAGES>(ctx, tma_op<TmaConv2Dgrad<WQ>>(drecs, d), L, OP_C2D, dtab);
+  launch_conv_halo<WQ, true>(ctx, drecs, d, L, OP_C2D, dtab);
   launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2Wgrad<WQ>>(drecs, d, lr), L, OP_C2W, dtab);
   launch_gemm_tc<TC_C1W_BN, TC_STAGES>(ctx, TcConv1Wgrad<WQ>{drecs, d}, L, OP_C1W, dtab);
   ev = op_begin(ctx, OP_C1R);

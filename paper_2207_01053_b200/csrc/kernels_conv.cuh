@@ -1,0 +1,195 @@
+// kernels_conv.cuh — "halo" implicit-GEMM 5x5 convolution on tcgen05 (bf16 mode).
+//
+// conv2 fwd (M = output pixels, N = C2, K = 25 taps x C1) and conv2 dgrad
+// (M = a1 pixels, N = C1, K = 25 taps x C2) re-read every input element once
+// per tap when the im2col operand is gathered per K block.  Here a CTA owns
+// TPC consecutive 128-pixel tiles (8 image rows x 16 columns) of ONE client:
+//  * its whole weight operand (all 25 taps) is loaded once by TMA and stays
+//    resident in shared memory;
+//  * per tile (and per 32-channel group of the input) the TMA loads the input
+//    halo ONCE as 5 x-shifted copies [kx][channel chunk][12 rows][16 px][8 ch]
+//    (out-of-bounds rows / columns are the TMA's zero fill = the conv padding);
+//  * the A operand of tap (ky, kx) is then just a UMMA descriptor into copy kx
+//    starting at row ky: 128 consecutive 16-byte pixel rows (SBO = 128 B), the
+//    second 8-channel chunk of the K=16 MMA one copy further (LBO = 12*256 B);
+//  * the halo is double-buffered and the fp32 accumulator double-buffered in
+//    TMEM, so TMA, tcgen05.mma and the epilogue of the previous tile overlap.
+// Warp roles: warps 0-7 epilogue (tcgen05.ld + fused layer epilogue), warp 8
+// lane 0 TMA producer, warp 9 lane 0 MMA issuer.
+#pragma once
+#include "kernels_tc.cuh"
+
+namespace protea {
+
+constexpr int kConvTPC = 4;  // 128-pixel tiles per CTA (2 images of 16x16)
+constexpr int kConvThreads = 320;
+
+template <int CIN>  // channels of the gathered input (per 32-channel halo group)
+struct HaloGeom {
+  static constexpr int NCC = CIN < 32 ? CIN / 8 : 4;  // 8-channel chunks per halo group
+  static constexpr int GROUPS = CIN / (8 * NCC);       // halo groups per tile
+  static constexpr int ROWS = 12;                      // 8 output rows + 4 halo rows
+  static constexpr int COPY = ROWS * 16 * 16;          // bytes of one (kx, chunk) copy
+  static constexpr int BYTES = 5 * NCC * COPY;         // one halo buffer
+};
+
+// Fwd: input a1 (C1 channels), weights K-major [kchunk][C2][8]; epilogue = TmaConv2Fwd's.
+// Dgrad: input dz2 (C2 channels, flipped taps), weights MN-major [tap][C1/8][C2][8]; epilogue = TcConv2Dgrad's.
+template <int WQ, bool DGRAD>
+struct HaloConv2 {
+  typedef CnnW<WQ> W;
+  static constexpr int CIN = DGRAD ? W::C2 : W::C1;   // gathered input channels
+  static constexpr int NOUT = DGRAD ? W::C1 : W::C2;  // MMA N (valid)
+  static constexpr int N = NOUT < 16 ? 16 : NOUT;     // MMA N
+  typedef HaloGeom<CIN> G;
+  static constexpr int B_BYTES = 25 * CIN * N * 2;    // resident weights (K x N bf16)
+  static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
+  static constexpr int SMEM = B_BYTES + 2 * G::BYTES + 256;
+  const ClientRec* recs;
+  CnnDims d;
+};
+
+template <int WQ, bool DGRAD>
+__global__ void __launch_bounds__(kConvThreads, 1)
+    k_conv_halo(const HaloConv2<WQ, DGRAD> op, const Task* __restrict__ tasks, const int* __restrict__ prefix,
+                int ntask) {
+  typedef HaloConv2<WQ, DGRAD> Op;
+  typedef typename Op::G G;
+  typedef CnnW<WQ> W;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sB = smem;
+  uint8_t* sH = smem + Op::B_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * G::BYTES);
+  // barriers: 0 b_full, 1-2 h_full, 3-4 h_empty, 5-6 acc_full, 7-8 acc_empty
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int ti = find_task(prefix, ntask, blockIdx.x);
+  TcTile t;
+  t.tk = tasks[ti];
+  t.c = op.recs + t.tk.rec;
+  const int tile0 = (blockIdx.x - __ldg(prefix + ti)) * kConvTPC;
+  const int ntile = min(kConvTPC, t.tk.rows * 2 - tile0);
+  t.n_mma = Op::N;
+
+  const uint32_t bar0 = tc::smem_u32(bars);
+  const uint32_t b_full = bar0, h_full = bar0 + 8, h_empty = bar0 + 24, acc_full = bar0 + 40, acc_empty = bar0 + 56;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(b_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(h_full + 8 * i, 1);
+      tc::mbar_init(h_empty + 8 * i, 1);
+      tc::mbar_init(acc_full + 8 * i, 1);
+      tc::mbar_init(acc_empty + 8 * i, 8);
+    }
+    tc::mbar_fence_init();
+  }
+  if (warp == 9) tc::tmem_alloc(tc::smem_u32(tmem_slot), Op::TMEM_COLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sb = tc::smem_u32(sB), sh = tc::smem_u32(sH);
+  const int nstage = ntile * G::GROUPS;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      const void* tin = tmap_of(t, DGRAD ? TM_DZ2H : TM_A1H);
+      tc::mbar_expect_tx(b_full, Op::B_BYTES);
+      if (!DGRAD) {  // [kchunk][C2][8]: box (8, C2) per 8-wide K chunk
+        for (int kc = 0; kc < 25 * W::C1 / 8; ++kc)
+          tc::tma_load_2d(sb + kc * Op::N * 16, tmap_of(t, TM_W2F), b_full, 8 * kc, 0);
+      } else {  // [tap][C1/8 (padded to N/8)][C2][8]: box (8 ci, 1 tap, C2 co)
+        for (int tap = 0; tap < 25; ++tap)
+          for (int nc = 0; nc < Op::N / 8; ++nc)
+            tc::tma_load_3d(sb + (tap * (Op::N / 8) + nc) * W::C2 * 16, tmap_of(t, TM_W2D), b_full, 8 * nc, tap, 0);
+      }
+      for (int s = 0; s < nstage; ++s) {
+        const int buf = s & 1, tile = tile0 + s / G::GROUPS, grp = s % G::GROUPS;
+        if (s >= 2) tc::mbar_wait(h_empty + 8 * buf, ((s >> 1) - 1) & 1);
+        tc::mbar_expect_tx(h_full + 8 * buf, G::BYTES);
+        const int r = tile >> 1, y0 = (tile & 1) * 8;
+        const uint32_t base = sh + buf * G::BYTES;
+        for (int kx = 0; kx < 5; ++kx)
+          for (int cc = 0; cc < G::NCC; ++cc)
+            tc::tma_load_4d(base + (kx * G::NCC + cc) * G::COPY, tin, h_full + 8 * buf, 8 * (grp * G::NCC + cc),
+                            DGRAD ? 2 - kx : kx - 2, y0 - 2, r);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      const uint32_t idesc = tc::idesc_bf16(128, Op::N, false, DGRAD);
+      tc::mbar_wait(b_full, 0);
+      tc::fence_after();
+      for (int i = 0; i < ntile; ++i) {
+        const int acc = i & 1;
+        if (i >= 2) tc::mbar_wait(acc_empty + 8 * acc, ((i >> 1) - 1) & 1);
+        tc::fence_after();
+        const uint32_t dt = tmem + acc * Op::N;
+        for (int grp = 0; grp < G::GROUPS; ++grp) {
+          const int s = i * G::GROUPS + grp, buf = s & 1;
+          tc::mbar_wait(h_full + 8 * buf, (s >> 1) & 1);
+          tc::fence_after();
+          const uint32_t hb = sh + buf * G::BYTES;
+          for (int ky = 0; ky < 5; ++ky)
+            for (int kx = 0; kx < 5; ++kx) {
+              const int tap = ky * 5 + kx, row0 = DGRAD ? 4 - ky : ky;
+              for (int cp = 0; cp < G::NCC / 2; ++cp) {
+                const uint64_t da =
+                    tc::sdesc(hb + (kx * G::NCC + 2 * cp) * G::COPY + row0 * 256, G::COPY, 128);
+                uint64_t db;
+                if (!DGRAD) {  // K chunk index of (tap, channel grp*NCC + 2cp)
+                  const int kc = tap * (W::C1 / 8) + grp * G::NCC + 2 * cp;
+                  db = tc::sdesc(sb + kc * Op::N * 16, Op::N * 16, 128);
+                } else {  // k rows = co (16 of them) of tap; n groups at C2*16
+                  const int co0 = (grp * G::NCC + 2 * cp) * 8;
+                  db = tc::sdesc(sb + tap * (Op::N / 8) * W::C2 * 16 + co0 * 16, 128, W::C2 * 16);
+                }
+                tc::mma_bf16(dt, da, db, idesc, (grp | tap | cp) != 0);
+              }
+            }
+          tc::commit(h_empty + 8 * buf);
+        }
+        tc::commit(acc_full + 8 * acc);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue warps 0-7
+    for (int i = 0; i < ntile; ++i) {
+      const int acc = i & 1;
+      tc::mbar_wait(acc_full + 8 * acc, (i >> 1) & 1);
+      tc::fence_after();
+      t.m0 = (tile0 + i) * 128;
+      const int row = (warp & 3) * 32 + lane;
+      for (int c0 = (warp >> 2) * 16; c0 < Op::N; c0 += 32) {
+        float v[16];
+        tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(acc * Op::N + c0), v);
+        if (DGRAD) {
+          TcConv2Dgrad<WQ> e;
+          e.recs = op.recs;
+          e.d = op.d;
+          e.epilogue(t, row, c0, v);
+        } else {
+          TmaConv2Fwd<WQ> e;
+          e.recs = op.recs;
+          e.d = op.d;
+          e.epilogue(t, row, c0, v);
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty + 8 * acc);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, Op::TMEM_COLS);
+  }
+}
+
+}  // namespace protea

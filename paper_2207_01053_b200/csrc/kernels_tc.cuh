@@ -614,6 +614,8 @@ enum TmapId : int {
   TM_W3M,      // W3 shadow (K1, F)      box (8,64)  fc1 dgrad A
   TM_A2,       // a2 (K1, B)             box (8,R)   fc1 fwd B
   TM_DH,       // dh (F, B)              box (8,R)   fc1 dgrad B
+  TM_A1H,      // a1                box (8,16,12,1)  conv2 fwd halo (kernels_conv.cuh)
+  TM_DZ2H,     // dz2               box (8,16,12,1)  conv2 dgrad halo
   TM_COUNT
 };
 
