@@ -64,7 +64,8 @@ typedef struct {
   int32_t rank;            /* this rank in [0, world) */
   int32_t world;           /* number of ranks (GPUs); 1 = no NCCL */
   int32_t precision;       /* PROTEA_PREC_*: activation storage + GEMM operand type */
-  const uint8_t* nccl_id;  /* host, 128 bytes (ncclUniqueId from rank 0, broadcast by the caller); NULL iff world == 1 */
+  const uint8_t* nccl_id;  /* host, 128 bytes (ncclUniqueId from rank 0, broadcast by the caller); NULL: no NCCL
+                              communicator (world == 1, or caller-side reduction via partial_only rounds) */
   void* arena;             /* device, caller-owned block holding the client slots (e.g. a torch uint8 tensor) */
   uint64_t arena_bytes;    /* capacity C_g of this GPU's arena */
   void* stream;            /* cudaStream_t to order all work on (NULL = the legacy default stream) */
@@ -149,7 +150,9 @@ typedef struct {
   uint32_t round;    /* round index */
   int32_t shuffle;   /* 1 = SplitMix64 epoch permutation, 0 = identity order */
   uint32_t time_ops; /* bitmask over PROTEA_OPC_*: bracket every launch of those classes with CUDA events */
-  uint32_t reserved;
+  uint32_t partial_only; /* 1: skip the cross-rank sum and the finalisation; keep this rank's fp64 FedAvg
+                            partial (protea_round_partial) for a caller-side reduction (protea_round_finalize);
+                            global_out is not written */
 } protea_round_opts;
 
 typedef struct {
@@ -211,6 +214,20 @@ protea_status protea_plan(const protea_profile* profiles, size_t n, const protea
 protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, const protea_client* clients,
                                size_t n, const protea_assignment* plan, const float* global_in, float* global_out,
                                size_t n_params, protea_profile* measured, protea_round_stats* stats);
+
+/* Copy the fp64 FedAvg partial of the last protea_run_round (partial_only = 1) of
+ * this rank: acc[d] = sum over this rank's clients of n_k (w_k[d] - w_g[d]),
+ * n_params doubles, all groups concatenated.  dst: host or device.
+ * Errors: INVALID (no partial round recorded, size mismatch), CUDA. */
+protea_status protea_round_partial(protea_ctx* ctx, double* dst, size_t n_params);
+
+/* Finish a partial round: global_out = global_in + acc_sum / N_group per shape
+ * group (N_group = sum n_k over ALL ranks' clients of that group, recorded by
+ * the last protea_run_round; groups without clients are copied unchanged).
+ * acc_sum: the element-wise sum of every rank's partial (device or host).
+ * Errors: INVALID, DIM, CUDA. */
+protea_status protea_round_finalize(protea_ctx* ctx, const double* acc_sum, const float* global_in, float* global_out,
+                                    size_t n_params);
 
 /* out[d] = sum_k n_k params[k][d] / sum_k n_k, fp64 accumulation in the given
  * order, one rounding to fp32.  params: host array of n device pointers, each

@@ -30,7 +30,7 @@ ORDER_ASC_ID, ORDER_DESC_STEPS = 0, 1
 
 EXPORTS = ["protea_init", "protea_finalize", "protea_last_error", "protea_register_model", "protea_register_shards",
            "protea_profile_clients", "protea_plan", "protea_run_round", "protea_fedavg", "protea_client_footprint",
-           "protea_selftest_gemm"]
+           "protea_selftest_gemm", "protea_round_partial", "protea_round_finalize"]
 
 
 class ProteaError(RuntimeError):
@@ -74,7 +74,7 @@ OPC_NAMES = ["conv1_fwd", "conv2_fwd", "fc1_fwd", "head", "fc1_dgrad", "fc1_wgra
 
 class RoundOpts(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_float), ("seed", ctypes.c_uint32), ("round", ctypes.c_uint32),
-                ("shuffle", ctypes.c_int32), ("time_ops", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("shuffle", ctypes.c_int32), ("time_ops", ctypes.c_uint32), ("partial_only", ctypes.c_uint32)]
 
 
 class RoundStats(ctypes.Structure):
@@ -118,6 +118,8 @@ _lib.protea_fedavg.argtypes = [_vp, _vp, _vp, _sz, _sz, _vp]
 _lib.protea_client_footprint.argtypes = [ctypes.POINTER(ModelDesc), ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                          ctypes.c_int32, ctypes.POINTER(ctypes.c_uint64),
                                          ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+_lib.protea_round_partial.argtypes = [_vp, _vp, _sz]
+_lib.protea_round_finalize.argtypes = [_vp, _vp, _vp, _vp, _sz]
 _lib.protea_selftest_gemm.argtypes = [_vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
 for _f in EXPORTS:
     if _f not in ("protea_finalize", "protea_last_error"):
@@ -217,9 +219,9 @@ def protea_plan(profiles, caps, policy=POLICY_PROFILED, order=ORDER_ASC_ID, marg
 
 
 def protea_run_round(ctx, clients, plan, global_in, global_out, lr=0.05, seed=0, rnd=0, shuffle=True,
-                     measured=False, time_ops=0):
+                     measured=False, time_ops=0, partial_only=False):
     """global_in / global_out: float32 torch tensors (cuda or cpu) or numpy arrays."""
-    o = RoundOpts(lr, seed, rnd, 1 if shuffle else 0, time_ops, 0)
+    o = RoundOpts(lr, seed, rnd, 1 if shuffle else 0, time_ops, 1 if partial_only else 0)
     st = RoundStats()
     n_params = global_in.numel() if hasattr(global_in, "numel") else global_in.size
     meas = np.zeros(len(clients), dtype=PROFILE_DT) if measured else None
@@ -228,6 +230,17 @@ def protea_run_round(ctx, clients, plan, global_in, global_out, lr=0.05, seed=0,
                                  _ptr(global_out), n_params, meas.ctypes.data if measured else None,
                                  ctypes.byref(st)), ctx)
     return (st.as_dict(), meas) if measured else st.as_dict()
+
+
+def protea_round_partial(ctx, dst):
+    """dst: float64 tensor / array of n_params (device or host)."""
+    n = dst.numel() if hasattr(dst, "numel") else dst.size
+    _check(_lib.protea_round_partial(ctx, _ptr(dst), n), ctx)
+
+
+def protea_round_finalize(ctx, acc_sum, global_in, global_out):
+    n = global_in.numel() if hasattr(global_in, "numel") else global_in.size
+    _check(_lib.protea_round_finalize(ctx, _ptr(acc_sum), _ptr(global_in), _ptr(global_out), n), ctx)
 
 
 def protea_fedavg(ctx, params, num_examples, out):

@@ -104,6 +104,9 @@ struct protea_ctx {
   std::vector<int> ev_op;
   uint64_t op_launches[PROTEA_N_OPC] = {}, op_flops[PROTEA_N_OPC] = {}, op_bytes[PROTEA_N_OPC] = {};
   double loss_host = 0.0;
+  // partial-round state (protea_round_partial / protea_round_finalize)
+  bool have_partial = false;
+  std::vector<int64_t> last_Ngroup;
   // TMA tensor maps per (client, slot offset, batch, group), reused across rounds
   std::map<std::tuple<uint64_t, int, int, int64_t, int>, std::array<CUtensorMap, TM_COUNT>> tmap_cache;  // (offset, B, E, n, group): everything the slot layout depends on
   DevArray<CUtensorMap> tmaps;
@@ -523,7 +526,7 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
     set_global_error("protea_init: null argument");
     return PROTEA_ERR_INVALID;
   }
-  if (opts->world < 1 || opts->rank < 0 || opts->rank >= opts->world || (opts->world > 1 && !opts->nccl_id) ||
+  if (opts->world < 1 || opts->rank < 0 || opts->rank >= opts->world ||
       !opts->arena || opts->arena_bytes == 0 ||
       (opts->precision != PROTEA_PREC_FP32 && opts->precision != PROTEA_PREC_BF16)) {
     set_global_error("protea_init: invalid rank/world/nccl_id/arena/precision");
@@ -547,7 +550,7 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
     set_global_error("protea_init: cudaEventCreate failed");
     return PROTEA_ERR_CUDA;
   }
-  if (opts->world > 1) {
+  if (opts->world > 1 && opts->nccl_id) {
     ncclUniqueId id;
     std::memcpy(&id, opts->nccl_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&ctx->comm, opts->world, id, opts->rank);
@@ -959,7 +962,25 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
   protea_status st =
       execute(ctx, all, wg, ctx->acc.p, opts->lr, opts->seed, opts->round, opts->shuffle, &iters, loss_dev);
   if (st != PROTEA_OK) return st;
+  ctx->last_Ngroup = Ngroup;
+  ctx->have_partial = opts->partial_only != 0;
+  if (opts->partial_only) {
+    CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (stats) {
+      float pms = 0.f;
+      CK(cudaEventElapsedTime(&pms, ctx->ev0, ctx->ev1));
+      std::memset(stats, 0, sizeof(*stats));
+      stats->round_ns = (uint64_t)(pms * 1e6);
+      stats->iterations = iters;
+      stats->kernel_launches = ctx->launches - l0;
+      for (auto& c : all) stats->client_steps += c.S;
+    }
+    return PROTEA_OK;
+  }
   if (ctx->world > 1) {
+    if (!ctx->comm)
+      return fail(ctx, PROTEA_ERR_INVALID, "run_round: world > 1 without an NCCL communicator needs partial_only = 1");
     ncclResult_t r = ncclAllReduce(ctx->acc.p, ctx->acc.p, Ptot, ncclDouble, ncclSum, ctx->comm, ctx->stream);
     if (r != ncclSuccess) return fail(ctx, PROTEA_ERR_NCCL, std::string("run_round: ncclAllReduce: ") + ncclGetErrorString(r));
   }
@@ -1094,6 +1115,49 @@ protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clien
     p.train_ns = p.step_ns * p.steps;
     p.uses_gpu = 1;
   }
+  return PROTEA_OK;
+}
+
+protea_status protea_round_partial(protea_ctx* ctx, double* dst, size_t n_params) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  int64_t Ptot = 0;
+  for (auto& g : ctx->groups) Ptot += g.m.P;
+  if (!dst || !ctx->have_partial) return fail(ctx, PROTEA_ERR_INVALID, "round_partial: no partial round recorded");
+  if ((int64_t)n_params != Ptot) return fail(ctx, PROTEA_ERR_DIM, "round_partial: n_params mismatch");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(dst, ctx->acc.p, Ptot * 8, cudaMemcpyDefault, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PROTEA_OK;
+}
+
+protea_status protea_round_finalize(protea_ctx* ctx, const double* acc_sum, const float* global_in, float* global_out,
+                                    size_t n_params) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  if (!acc_sum || !global_in || !global_out || ctx->last_Ngroup.size() != ctx->groups.size())
+    return fail(ctx, PROTEA_ERR_INVALID, "round_finalize: null argument or no round recorded");
+  int64_t Ptot = 0;
+  for (auto& g : ctx->groups) Ptot += g.m.P;
+  if ((int64_t)n_params != Ptot) return fail(ctx, PROTEA_ERR_DIM, "round_finalize: n_params mismatch");
+  CK(cudaSetDevice(ctx->device));
+  CK(ctx->gin.reserve(Ptot));
+  CK(ctx->gout.reserve(Ptot));
+  CK(ctx->acc.reserve(Ptot + 1));
+  CK(cudaMemcpyAsync(ctx->gin.p, global_in, Ptot * 4, cudaMemcpyDefault, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->acc.p, acc_sum, Ptot * 8, cudaMemcpyDefault, ctx->stream));
+  for (size_t g = 0; g < ctx->groups.size(); ++g) {
+    const Group& gr = ctx->groups[g];
+    if (ctx->last_Ngroup[g] > 0)
+      k_finalize<<<grid_for(gr.m.P, 256), 256, 0, ctx->stream>>>(ctx->gin.p + gr.offset, ctx->acc.p + gr.offset,
+                                                                 (double)ctx->last_Ngroup[g], ctx->gout.p + gr.offset,
+                                                                 gr.m.P);
+    else
+      CK(cudaMemcpyAsync(ctx->gout.p + gr.offset, ctx->gin.p + gr.offset, gr.m.P * 4, cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+  }
+  CK(cudaMemcpyAsync(global_out, ctx->gout.p, Ptot * 4, cudaMemcpyDefault, ctx->stream));
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->have_partial = false;
   return PROTEA_OK;
 }
 

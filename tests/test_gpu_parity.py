@@ -163,3 +163,36 @@ def test_abi_errors_on_gpu(torch):
         sim.run_round(c2, ex["plan"], g)
     assert e.value.name == "INVALID"
     sim.close()
+
+
+def test_virtual_two_ranks_equal_one_rank(torch):
+    """Two rank contexts on one GPU (no NCCL), each running only its planned
+    clients with partial_only rounds; partials summed in rank order and
+    finalised must equal the single-rank round (fp64 accumulation: <= 1 ulp)."""
+    import paper_2207_01053_b200 as pb
+    from paper_2207_01053_b200.sim import Simulation
+    wl = synth.build_workload(3, k=9, samples=12, epochs=1)
+    one, ex = gpu_run(wl)
+    w0 = torch.tensor(synth.init_weights(wl.model), device="cuda")
+    P = w0.numel()
+    partials = []
+    sims = []
+    for rank in range(2):
+        sim = Simulation(arena_bytes=1 << 30, rank=rank, world=2)
+        mid = sim.register_model(synth.MODEL_CNN, 4, 10, 32, 32, 3)
+        sim.register_shards([(c.id, *wl.shards[c.id]) for c in wl.clients])
+        cl = sim.clients([(c.id, mid, c.batch, c.epochs) for c in wl.clients])
+        plan, _ = sim.plan(sim.profile(cl), caps=[1 << 30, 1 << 30])
+        sim.run_round(cl, plan, w0, torch.empty_like(w0), lr=0.05, seed=wl.seed, rnd=0, partial_only=True)
+        part = torch.empty(P, dtype=torch.float64, device="cuda")
+        pb.protea_round_partial(sim.ctx, part)
+        partials.append(part)
+        sims.append(sim)
+    acc = partials[0] + partials[1]
+    out = torch.empty_like(w0)
+    pb.protea_round_finalize(sims[0].ctx, acc, w0, out)
+    got = out.cpu().numpy()
+    ulp = np.abs(got.view(np.int32).astype(np.int64) - one[4].view(np.int32).astype(np.int64))
+    assert ulp.max() <= 1
+    for s in sims:
+        s.close()
