@@ -141,6 +141,7 @@ enum {
   PROTEA_OPC_FC1_WGRAD, PROTEA_OPC_CONV2_DGRAD, PROTEA_OPC_CONV2_WGRAD, PROTEA_OPC_CONV2_REDUCE,
   PROTEA_OPC_CONV1_WGRAD, PROTEA_OPC_CONV1_REDUCE, PROTEA_OPC_MLP_FC1_FWD, PROTEA_OPC_MLP_HEAD,
   PROTEA_OPC_MLP_FC1_WGRAD, PROTEA_OPC_ADMIT, PROTEA_OPC_FEDAVG, PROTEA_OPC_STAGE_X,
+  PROTEA_OPC_R_FWD, PROTEA_OPC_R_HEAD, PROTEA_OPC_R_DGRAD, PROTEA_OPC_R_WGRAD, PROTEA_OPC_R_REDUCE, /* ResNet-8 */
   PROTEA_N_OPC = 32 /* room for further op classes */
 };
 

@@ -69,7 +69,8 @@ TC_OPS_BUILT = {"conv1_fwd": True, "conv2_fwd": True, "fc1_fwd": True, "fc1_dgra
                 "conv2_dgrad": True, "conv2_wgrad": True, "conv1_wgrad": True}
 OPC_NAMES = ["conv1_fwd", "conv2_fwd", "fc1_fwd", "head", "fc1_dgrad", "fc1_wgrad", "conv2_dgrad", "conv2_wgrad",
              "conv2_reduce", "conv1_wgrad", "conv1_reduce", "mlp_fc1_fwd", "mlp_head", "mlp_fc1_wgrad", "admit",
-             "fedavg", "stage_x"] + [f"op{i}" for i in range(17, 32)]
+             "fedavg", "stage_x", "resnet_fwd", "resnet_head", "resnet_dgrad", "resnet_wgrad",
+             "resnet_reduce"] + [f"op{i}" for i in range(22, 32)]
 
 
 class RoundOpts(ctypes.Structure):

@@ -35,6 +35,7 @@
 #include "kernels_simt.cuh"
 #include "kernels_tc.cuh"
 #include "kernels_conv.cuh"
+#include "kernels_resnet.cuh"
 
 namespace protea {
 
@@ -244,14 +245,37 @@ constexpr int MW_BM = 64, MW_BN = 64;
 
 enum Op : int {
   OP_C1F = 0, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R,
-  OP_MF, OP_MHEAD, OP_MW, OP_ADMIT_, OP_FEDAVG_, OP_STAGE, OP_COUNT = PROTEA_N_OPC
+  OP_MF, OP_MHEAD, OP_MW, OP_ADMIT_, OP_FEDAVG_, OP_STAGE,
+  // ResNet-8 launch instances (each needs its own prefix table); stats use PROTEA_OPC_R_* classes
+  RI_F0 = 32, RI_HEAD = RI_F0 + 7, RI_D1 = RI_HEAD + 1, RI_W0 = RI_D1 + 6, RI_R0 = RI_W0 + 7, OP_COUNT = RI_R0 + 7
 };
+// ResNet-8 SIMT tile shape
+constexpr int R_BM = 64, R_BN = 32;
+const protea::Layer& rlayer(const ModelDims& m, int i) { return m.layers[i]; }
+int rsplits(const Layer& l, int rows) { return cdiv(rows * l.hout * l.wout, kWgradChunkPx); }
 
 // tensor-core tile shapes (bf16 mode): M tile = 128, BN per op, STAGES-deep ring
 constexpr int TC_C1F_BN = 32, TC_C1W_BN = 32, TC_C2F_BN = 64, TC_C2D_BN = 32, TC_C2W_BN = 64, TC_F1F_BN = 64, TC_F1D_BN = 64, TC_F1W_BN = 256;
 constexpr int TC_STAGES = 4, TC_F1W_STAGES = 2;
 
 int tiles(const ModelDims& m, int op, int rows, bool tc) {
+  if (op >= RI_F0) {
+    if (op == RI_HEAD) return 1;
+    if (op < RI_HEAD) {
+      const Layer& l = m.layers[op - RI_F0];
+      return cdiv(rows * l.hout * l.wout, R_BM) * cdiv(l.cout, R_BN);
+    }
+    if (op < RI_W0) {
+      const Layer& l = m.layers[1 + op - RI_D1];
+      return cdiv(rows * l.hin * l.win, R_BM) * cdiv(l.cin, R_BN);
+    }
+    if (op < RI_R0) {
+      const Layer& l = m.layers[op - RI_W0];
+      return rsplits(l, rows) * cdiv(l.cout, R_BM) * cdiv(9 * l.cin + 1, R_BN);
+    }
+    const Layer& l = m.layers[op - RI_R0];
+    return cdiv(l.cout * (9 * l.cin + 1), kReduceBlock);
+  }
   if (tc) switch (op) {
       case OP_STAGE: return cdiv(rows * 1296, kStageThreads);
       case OP_C1F: return rows * 8;
@@ -290,13 +314,52 @@ std::vector<int> ops_of(const ModelDims& m, bool tc) {
   if (m.arch == PROTEA_MODEL_CNN)
     return {OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_MLP) return {OP_MF, OP_MHEAD, OP_MW};
-  return {};
+  std::vector<int> v;
+  for (int i = 0; i < 7; ++i) v.push_back(RI_F0 + i);
+  v.push_back(RI_HEAD);
+  for (int i = 0; i < 6; ++i) v.push_back(RI_D1 + i);
+  for (int i = 0; i < 7; ++i) v.push_back(RI_W0 + i);
+  for (int i = 0; i < 7; ++i) v.push_back(RI_R0 + i);
+  return v;
 }
 
 // Algorithmic work of one op for one client-step of `r` rows: FLOPs = 2 x useful
 // MACs; bytes = compulsory HBM traffic (every operand read once, every result
 // written once; weights fp32, activations e bytes).  DESIGN.md "Roofline".
+void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, uint64_t* by);
+int op_class(int op) {
+  if (op < RI_F0) return op;
+  if (op < RI_HEAD) return PROTEA_OPC_R_FWD;
+  if (op == RI_HEAD) return PROTEA_OPC_R_HEAD;
+  if (op < RI_W0) return PROTEA_OPC_R_DGRAD;
+  if (op < RI_R0) return PROTEA_OPC_R_WGRAD;
+  return PROTEA_OPC_R_REDUCE;
+}
 void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, uint64_t* by) {
+  if (op >= RI_F0) {
+    uint64_t F = 0, B = 0;
+    if (op == RI_HEAD) {
+      F = 3 * 2 * r * 64 * m.classes;
+      B = r * 4096 * e * 2 + 8 * m.classes * 65 + r * 4;
+    } else if (op < RI_HEAD || op < RI_W0) {
+      const bool fwd = op < RI_HEAD;
+      const Layer& l = m.layers[fwd ? op - RI_F0 : 1 + op - RI_D1];
+      F = 2 * r * l.hout * l.wout * l.cout * 9 * l.cin;
+      B = r * (uint64_t)l.hin * l.win * l.cin * e + 4 * (uint64_t)l.cout * 9 * l.cin +
+          r * (uint64_t)l.hout * l.wout * l.cout * e * 2;
+    } else if (op < RI_R0) {
+      const Layer& l = m.layers[op - RI_W0];
+      F = 2 * r * l.hout * l.wout * l.cout * 9 * l.cin;
+      B = r * (uint64_t)l.hin * l.win * l.cin * e + r * (uint64_t)l.hout * l.wout * l.cout * e +
+          4 * (uint64_t)rsplits(l, (int)r) * l.cout * (9 * l.cin + 1);
+    } else {
+      const Layer& l = m.layers[op - RI_R0];
+      B = 4 * (uint64_t)rsplits(l, (int)r) * l.cout * (9 * l.cin + 1) + 8 * (uint64_t)l.cout * (9 * l.cin + 1);
+    }
+    *fl = F;
+    *by = B;
+    return;
+  }
   const uint64_t c1 = m.c1, c2 = m.c2, f = m.f, C = m.classes;
   const uint64_t s1 = cdiv((int)(r * 1024), kWgradChunkPx), s2 = cdiv((int)(r * 256), kWgradChunkPx);
   uint64_t F = 0, B = 0;
@@ -361,7 +424,7 @@ template <class OpT, int BM, int BN>
 void launch_gemm(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, const int32_t* dtab) {
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int* prefix = dtab + L.prefix_off[opid];
-  const int ev = op_begin(ctx, opid);
+  const int ev = op_begin(ctx, op_class(opid));
   k_gemm_simt<BM, BN, OpT><<<L.grid[opid], (BM / 4) * (BN / 4), 0, ctx->stream>>>(op, tasks, prefix, L.ntask);
   op_end(ctx, ev);
 }
@@ -456,9 +519,96 @@ void launch_step_tc(protea_ctx* ctx, const ModelDims& m, const Launch& L, const 
     launch_step_tc_w<4>(ctx, m, L, drecs, dtab, lr);
 }
 
+RConv rconv(const Layer& l) {
+  RConv c;
+  c.H = l.hin;
+  c.W = l.win;
+  c.Cin = l.cin;
+  c.Cout = l.cout;
+  c.s = l.stride;
+  c.Ho = l.hout;
+  c.Wo = l.wout;
+  c.w = l.off_w;
+  c.b = l.off_b;
+  return c;
+}
+
+// ResNet-8 step (SIMT; bf16 mode stores activations in bf16).  Buffers: a0 r1 o1 r2 o2 r3 o3, gradients
+// ping-pong g0 g1 g2; each layer's dgrad runs before its SGD update (old weights).
+template <typename T>
+void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs,
+                        const int32_t* dtab, float lr) {
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const int in_of[7] = {-1, B_R_A0, B_R_R1, B_R_O1, B_R_R2, B_R_O2, B_R_R3};
+  const int out_of[7] = {B_R_A0, B_R_R1, B_R_O1, B_R_R2, B_R_O2, B_R_R3, B_R_O3};
+  typedef RFwd<T, R_BM, R_BN> F;
+  typedef RDgrad<T, R_BM, R_BN> D;
+  typedef RWgrad<T, R_BM, R_BN> Wg;
+  for (int i = 0; i < 7; ++i) {
+    F f;
+    f.recs = drecs;
+    f.L = rconv(m.layers[i]);
+    f.in_buf = in_of[i];
+    f.out_buf = out_of[i];
+    f.res_buf = -1;
+    f.res_mode = 0;
+    f.Cres = 0;
+    if (i == 2) { f.res_buf = B_R_A0; f.res_mode = 1; }                      // block 1: identity shortcut
+    if (i == 4) { f.res_buf = B_R_O1; f.res_mode = 2; f.Cres = 16; }         // block 2: option A from o1
+    if (i == 6) { f.res_buf = B_R_O2; f.res_mode = 2; f.Cres = 32; }         // block 3: option A from o2
+    launch_gemm<F, R_BM, R_BN>(ctx, f, L, RI_F0 + i, dtab);
+  }
+  const Layer& fc = m.layers[7];
+  RHeadArgs ha{drecs, m.classes, fc.off_w, fc.off_b, lr};
+  int ev = op_begin(ctx, PROTEA_OPC_R_HEAD);
+  k_rhead<T><<<L.ntask, 256, 0, ctx->stream>>>(ha, tasks);
+  op_end(ctx, ev);
+  // backward, layer 6 (b3b) down to 1 (b1a): dgrad (dout, out, mask, add), then wgrad + reduce
+  struct Bw { int dout, out, mask, add, add_mode, cadd; };
+  const Bw bw[7] = {
+      {0, 0, 0, 0, 0, 0},                              // conv0: no dgrad
+      {B_R_G2, B_R_G0, B_R_A0, B_R_G1, 1, 16},         // b1a: dz0 = (convT(dr1) + ds1) * (a0 > 0)
+      {B_R_G1, B_R_G2, B_R_R1, -1, 0, 0},              // b1b: dr1 = convT(ds1) * (r1 > 0)
+      {B_R_G0, B_R_G1, B_R_O1, B_R_G2, 2, 32},         // b2a: ds1 = (convT_s2(dr2) + sc(ds2)) * (o1 > 0)
+      {B_R_G2, B_R_G0, B_R_R2, -1, 0, 0},              // b2b: dr2 = convT(ds2) * (r2 > 0)
+      {B_R_G1, B_R_G2, B_R_O2, B_R_G0, 2, 64},         // b3a: ds2 = (convT_s2(dr3) + sc(ds3)) * (o2 > 0)
+      {B_R_G0, B_R_G1, B_R_R3, -1, 0, 0}};             // b3b: dr3 = convT(ds3) * (r3 > 0)
+  const int wg_dout[7] = {B_R_G0, B_R_G2, B_R_G1, B_R_G0, B_R_G2, B_R_G1, B_R_G0};
+  for (int i = 6; i >= 0; --i) {
+    const Layer& l = m.layers[i];
+    if (i >= 1) {
+      D dg;
+      dg.recs = drecs;
+      dg.L = rconv(l);
+      dg.dout_buf = bw[i].dout;
+      dg.out_buf = bw[i].out;
+      dg.mask_buf = bw[i].mask;
+      dg.add_buf = bw[i].add;
+      dg.add_mode = bw[i].add_mode;
+      dg.Cadd = bw[i].cadd;
+      launch_gemm<D, R_BM, R_BN>(ctx, dg, L, RI_D1 + i - 1, dtab);
+    }
+    Wg wg;
+    wg.recs = drecs;
+    wg.L = rconv(l);
+    wg.dout_buf = wg_dout[i];
+    wg.in_buf = in_of[i];
+    launch_gemm<Wg, R_BM, R_BN>(ctx, wg, L, RI_W0 + i, dtab);
+    ReduceArgs ra{drecs, B_R_WSP, l.cout, 9 * l.cin, l.off_w, l.off_b, l.hout * l.wout, lr};
+    ev = op_begin(ctx, PROTEA_OPC_R_REDUCE);
+    k_reduce_update<<<L.grid[RI_R0 + i], kReduceBlock, 0, ctx->stream>>>(ra, tasks, dtab + L.prefix_off[RI_R0 + i],
+                                                                         L.ntask);
+    op_end(ctx, ev);
+  }
+}
+
 template <typename T>
 void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const int32_t* dtab,
                  float lr) {
+  if (m.arch == PROTEA_MODEL_RESNET8) {
+    launch_step_resnet<T>(ctx, m, L, drecs, dtab, lr);
+    return;
+  }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   if (m.arch == PROTEA_MODEL_CNN) {
     const CnnDims d = cnn_dims(m);
@@ -592,8 +742,6 @@ protea_status protea_register_model(protea_ctx* ctx, const protea_model_desc* de
   Group g;
   std::string err;
   if (!make_model(*desc, &g.m, &err)) return fail(ctx, PROTEA_ERR_INVALID, "register_model: " + err);
-  if (desc->arch == PROTEA_MODEL_RESNET8)
-    return fail(ctx, PROTEA_ERR_INVALID, "register_model: RESNET8 device path not built in this version");
   g.offset = 0;
   for (auto& x : ctx->groups) g.offset += x.m.P;
   ctx->groups.push_back(g);
@@ -786,8 +934,8 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
             acc_t += tiles(m, op, rows[i], tc_mode);
             uint64_t fl, by;
             op_work(m, op, (uint64_t)rows[i], (uint64_t)e, &fl, &by);
-            ctx->op_flops[op] += fl;
-            ctx->op_bytes[op] += by;
+            ctx->op_flops[op_class(op)] += fl;
+            ctx->op_bytes[op_class(op)] += by;
           }
           tab.push_back(acc_t);
           L.grid[op] = acc_t;

@@ -196,3 +196,19 @@ def test_virtual_two_ranks_equal_one_rank(torch):
     assert ulp.max() <= 1
     for s in sims:
         s.close()
+
+
+def test_config5_resnet8_fp32(torch):
+    # config 5 shape (ResNet-8, Dirichlet shard sizes, B in {8..64}, E=2), 5 sampled clients, small shards
+    wl = synth.build_workload(5, n_clients=200, k=5, samples=6)
+    got, ex = gpu_run(wl)
+    ref = oracle_run(wl)
+    assert rel_l2(got[4], ref[4]) <= FP32_TOL
+    assert rel_l2(got[4] - ex["g0"][4], ref[4] - ex["g0"][4]) <= 1e-3
+
+
+def test_config5_resnet8_bf16(torch):
+    wl = synth.build_workload(5, n_clients=200, k=4, samples=6)
+    got, _ = gpu_run(wl, precision=1)
+    ref = oracle_run(wl)
+    assert rel_l2(got[4], ref[4]) <= BF16_TOL
