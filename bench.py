@@ -335,9 +335,9 @@ def main():
         bound, achieved, peak, unit = "hbm", by_per / avg_ns, pk["hbm"], "GB/s"
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf):  # DRAM bytes per launch of this op from the committed ncu capture of the same command
         try:
-            traffic = json.load(open(tf)).get(pb.OPC_NAMES[dominant], {}).get(dtype)
+            traffic = json.load(open(tf)).get(pb.OPC_NAMES[dominant], {}).get(dtype, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     roof = {"kernel": pb.OPC_NAMES[dominant], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
