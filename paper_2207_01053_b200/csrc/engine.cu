@@ -255,8 +255,8 @@ const protea::Layer& rlayer(const ModelDims& m, int i) { return m.layers[i]; }
 int rsplits(const Layer& l, int rows) { return cdiv(rows * l.hout * l.wout, kWgradChunkPx); }
 
 // tensor-core tile shapes (bf16 mode): M tile = 128, BN per op, STAGES-deep ring
-constexpr int TC_C1F_BN = 32, TC_C1W_BN = 32, TC_C2F_BN = 64, TC_C2D_BN = 32, TC_C2W_BN = 64, TC_F1F_BN = 64, TC_F1D_BN = 64, TC_F1W_BN = 256;
-constexpr int TC_STAGES = 4, TC_F1W_STAGES = 2;
+constexpr int TC_C1F_BN = 32, TC_C1W_BN = 32, TC_C2F_BN = 64, TC_C2D_BN = 32, TC_C2W_BN = 64, TC_F1F_BN = 64, TC_F1D_BN = 64, TC_F1W_BN = 128;
+constexpr int TC_STAGES = 4, TC_F1W_STAGES = 1;
 
 int tiles(const ModelDims& m, int op, int rows, bool tc) {
   if (op >= RI_F0) {
@@ -284,9 +284,9 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
       case OP_C2F: return m.c1 >= 16 ? cdiv(rows * 2, kConvTPC) : rows * 2;  // halo kernel unless width 1/4
       case OP_F1F: return m.f / 128;
       case OP_F1D: return 64 * m.c2 / 128;
-      case OP_F1W: return (64 * m.c2 / 128) * cdiv(m.f, 256);
+      case OP_F1W: return (64 * m.c2 / 128) * cdiv(m.f, 128);
       case OP_C2D: return cdiv(rows * 2, kConvTPC);
-      case OP_C2W: return cdiv(25 * m.c1 + 1, 128);
+      case OP_C2W: return cdiv(rows * 256, kWgradChunkPx) * cdiv(25 * m.c1 + 1, 128);
       default: break;
     }
   switch (op) {
@@ -310,7 +310,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
 
 std::vector<int> ops_of(const ModelDims& m, bool tc) {
   if (m.arch == PROTEA_MODEL_CNN && tc)
-    return {OP_STAGE, OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C1W, OP_C1R};
+    return {OP_STAGE, OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_CNN)
     return {OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_MLP) return {OP_MF, OP_MHEAD, OP_MW};
@@ -371,8 +371,8 @@ void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, u
     case OP_F1D: F = 2 * r * 64 * c2 * f; B = r * f * e + e * f * 64 * c2 + r * 64 * c2 * (e + 1) + r * 256 * c2 * e; break;
     case OP_F1W: F = 2 * r * f * 64 * c2; B = r * f * e + r * 64 * c2 * e + (8 + (e == 2 ? 2 : 0)) * f * 64 * c2; break;
     case OP_C2D: F = 2 * r * 256 * c1 * 25 * c2; B = r * 256 * c2 * e + e * c2 * 25 * c1 + r * 256 * c1 * (e + 1) + r * 1024 * c1 * e; break;
-    case OP_C2W: F = 2 * r * 256 * c2 * 25 * c1; B = r * 256 * c2 * e + r * 256 * c1 * e + (e == 2 ? 10 * c2 * (25 * c1 + 1) : 4 * s2 * c2 * (25 * c1 + 1)); break;
-    case OP_C2R: F = 0; B = 4 * s2 * c2 * (25 * c1 + 1) + 8 * c2 * (25 * c1 + 1); break;
+    case OP_C2W: F = 2 * r * 256 * c2 * 25 * c1; B = r * 256 * c2 * e + r * 256 * c1 * e + 4 * s2 * c2 * (25 * c1 + 1); break;
+    case OP_C2R: F = 0; B = 4 * s2 * c2 * (25 * c1 + 1) + (8 + (e == 2 ? 2 : 0)) * c2 * (25 * c1 + 1); break;
     case OP_C1W: F = 2 * r * 1024 * c1 * 75; B = r * 1024 * c1 * e + r * 3072 + 4 * s1 * c1 * 76; break;
     case OP_C1R: F = 0; B = 4 * s1 * c1 * 76 + 8 * c1 * 76; break;
     case OP_MF: F = 2 * r * 64 * 784; B = r * 784 + 4 * 64 * 785 + r * 64 * e; break;
@@ -502,6 +502,10 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
   launch_conv_halo<WQ, true>(ctx, drecs, d, L, OP_C2D, dtab);
   launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2Wgrad<WQ>>(drecs, d, lr), L, OP_C2W, dtab);
+  ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr, 1};
+  ev = op_begin(ctx, OP_C2R);
+  k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->stream>>>(r2, tasks, dtab + L.prefix_off[OP_C2R], L.ntask);
+  op_end(ctx, ev);
   launch_gemm_tc<TC_C1W_BN, TC_STAGES>(ctx, TcConv1Wgrad<WQ>{drecs, d}, L, OP_C1W, dtab);
   ev = op_begin(ctx, OP_C1R);
   k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->stream>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
@@ -594,7 +598,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
     wg.dout_buf = wg_dout[i];
     wg.in_buf = in_of[i];
     launch_gemm<Wg, R_BM, R_BN>(ctx, wg, L, RI_W0 + i, dtab);
-    ReduceArgs ra{drecs, B_R_WSP, l.cout, 9 * l.cin, l.off_w, l.off_b, l.hout * l.wout, lr};
+    ReduceArgs ra{drecs, B_R_WSP, l.cout, 9 * l.cin, l.off_w, l.off_b, l.hout * l.wout, lr, 0};
     ev = op_begin(ctx, PROTEA_OPC_R_REDUCE);
     k_reduce_update<<<L.grid[RI_R0 + i], kReduceBlock, 0, ctx->stream>>>(ra, tasks, dtab + L.prefix_off[RI_R0 + i],
                                                                          L.ntask);
@@ -623,13 +627,13 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Fc1Wgrad<T, F1W_BM, F1W_BN>, F1W_BM, F1W_BN>(ctx, {drecs, d, lr}, L, OP_F1W, dtab);
     launch_gemm<Conv2Dgrad<T, C2D_BM, C2D_BN>, C2D_BM, C2D_BN>(ctx, {drecs, d}, L, OP_C2D, dtab);
     launch_gemm<Conv2Wgrad<T, C2W_BM, C2W_BN>, C2W_BM, C2W_BN>(ctx, {drecs, d}, L, OP_C2W, dtab);
-    ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr};
+    ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr, 0};
     ev = op_begin(ctx, OP_C2R);
     k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->stream>>>(r2, tasks, dtab + L.prefix_off[OP_C2R],
                                                                        L.ntask);
     op_end(ctx, ev);
     launch_gemm<Conv1Wgrad<T, C1W_BM, C1W_BN>, C1W_BM, C1W_BN>(ctx, {drecs, d}, L, OP_C1W, dtab);
-    ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr};
+    ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr, 0};
     ev = op_begin(ctx, OP_C1R);
     k_reduce_update<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->stream>>>(r1, tasks, dtab + L.prefix_off[OP_C1R],
                                                                        L.ntask);

@@ -455,6 +455,7 @@ struct ReduceArgs {
   int64_t off_w, off_b;
   int px_per_row;  // pixels per sample of the layer output (split count = ceil(rows*px/2048))
   float lr;
+  int shadow;      // 1: also write the bf16 weight shadow (bf16 mode)
 };
 constexpr int kReduceBlock = 256;
 __global__ void __launch_bounds__(kReduceBlock)
@@ -470,8 +471,14 @@ __global__ void __launch_bounds__(kReduceBlock)
   float g = 0.f;
   for (int s = 0; s < splits; ++s) g += part[(int64_t)s * total + e];
   const int m = e / N, n = e - m * N;
-  float* w = n < a.Nw ? c->params + a.off_w + (int64_t)m * a.Nw + n : c->params + a.off_b + m;
-  *w = *w - a.lr * g;
+  if (n < a.Nw) {
+    const int64_t idx = a.off_w + (int64_t)m * a.Nw + n;
+    const float nw = c->params[idx] - a.lr * g;
+    c->params[idx] = nw;
+    if (a.shadow) ((__nv_bfloat16*)c->buf[B_WSH])[idx] = __float2bfloat16_rn(nw);  // tensor-core operand copy
+  } else {
+    c->params[a.off_b + m] -= a.lr * g;
+  }
 }
 
 // --------------------------------------------------------------------------

@@ -84,10 +84,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   constexpr bool TMA = has_tma<Op>::value;
   constexpr int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
   constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  constexpr int LAG = (STAGES - 1) < 2 ? (STAGES - 1) : 2;
+  constexpr int LAG = (STAGES - 1) < 2 ? (STAGES - 1) : 2;  // STAGES == 1: single-K-block ops (LAG 0)
   constexpr int NA = 1024 / kTcProd;                             // A chunks per producer thread
   constexpr int NB = (BN * 8 + kTcProd - 1) / kTcProd;           // B chunks per producer thread
-  static_assert(LAG >= 1, "need >= 2 stages");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
@@ -555,17 +554,18 @@ template <int WQ>
 struct TcFc1Wgrad {  // M = K1 (input features), N = F (outputs), K = rows; W <- W - lr dW
   typedef CnnW<WQ> W;
   static constexpr bool A_MN = true, B_MN = true;
+  static constexpr int NT = 128;  // N tile (TMEM 128 columns -> up to 4 CTAs per SM)
   struct PA { const bf16* p; };
   struct PB { const bf16* p; };
   const ClientRec* recs;
   CnnDims d;
   float lr;
   __device__ void setup(TcTile& t, int local) const {
-    const int nt = (W::F + 255) / 256;
+    const int nt = (W::F + NT - 1) / NT;
     t.m0 = (local / nt) * 128;
-    t.n0 = (local % nt) * 256;
+    t.n0 = (local % nt) * NT;
     t.nk = 1;  // rows <= 64
-    t.n_mma = W::F - t.n0 < 256 ? W::F - t.n0 : 256;
+    t.n_mma = W::F - t.n0 < NT ? W::F - t.n0 : NT;
   }
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
   __device__ PA a_pre(const TcTile& t, int i, int j) const {
@@ -698,9 +698,18 @@ struct TmaConv2Dgrad : TcConv2Dgrad<WQ> {  // same GEMM and epilogue, operands b
 };
 
 template <int WQ>
-struct TmaConv2Wgrad : TcConv2Wgrad<WQ> {  // same GEMM and epilogue, operands by TMA
+struct TmaConv2Wgrad : TcConv2Wgrad<WQ> {  // split-K over 2048-pixel chunks -> partial[split][C2][25 C1 + 1]
   typedef CnnW<WQ> W;
   static constexpr bool TMA = true;
+  static constexpr int MT = (25 * W::C1 + 1 + 127) / 128;  // M tiles
+  __device__ void setup(TcTile& t, int local) const {
+    const int split = local / MT;
+    t.m0 = (local - split * MT) * 128;
+    t.n0 = split;
+    const int kbs = t.tk.rows * 4 - split * (kWgradChunkPx / 64);
+    t.nk = kbs < kWgradChunkPx / 64 ? kbs : kWgradChunkPx / 64;
+    t.n_mma = W::C2 < 16 ? 16 : W::C2;
+  }
   __device__ void init_stage(const TcTile& t, uint8_t* a, uint8_t* b) const {
     // m groups at/after the bias row: constant chunks ([1,0..] per pixel, or zeros), 64 rows x 16 B each
     for (int g = 0; g < 16; ++g) {
@@ -715,7 +724,7 @@ struct TmaConv2Wgrad : TcConv2Wgrad<WQ> {  // same GEMM and epilogue, operands b
     return 1024u * (valid < 16 ? (valid < 0 ? 0 : valid) : 16) + 1024u * (W::C2 / 8);
   }
   __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
-    const int r = kb >> 2, y0 = (kb & 3) * 4;
+    const int kg = t.n0 * (kWgradChunkPx / 64) + kb, r = kg >> 2, y0 = (kg & 3) * 4;
     for (int g = 0; g < 16; ++g) {
       const int mg = t.m0 + 8 * g;
       if (mg >= 25 * W::C1) break;
@@ -727,6 +736,14 @@ struct TmaConv2Wgrad : TcConv2Wgrad<WQ> {  // same GEMM and epilogue, operands b
   }
   __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const { return tc::sdesc(base + 256 * ks, 128, 1024); }
   __device__ uint64_t b_desc(const TcTile&, uint32_t base, int ks) const { return tc::sdesc(base + 256 * ks, 128, 1024); }
+  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
+    const int m = t.m0 + row, N = 25 * W::C1 + 1;
+    if (m >= N) return;
+    float* part = (float*)t.c->buf[B_WSP] + (int64_t)t.n0 * W::C2 * N + m;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (c0 + j < W::C2) part[(int64_t)(c0 + j) * N] = v[j];
+  }
 };
 
 __device__ __forceinline__ int batch_rows16(const TcTile& t) { return (t.c->B + 15) & ~15; }
