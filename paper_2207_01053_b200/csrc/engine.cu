@@ -117,7 +117,7 @@ namespace {
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 bool tmap_encode(CUtensorMap* m, const void* addr, int rank, const uint64_t* dims, const uint64_t* strides,
-                 const uint32_t* box) {
+                 const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   if (!g_encode) {
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&g_encode, cudaEnableDefault, &q) != cudaSuccess ||
@@ -126,8 +126,8 @@ bool tmap_encode(CUtensorMap* m, const void* addr, int rank, const uint64_t* dim
   }
   const cuuint32_t es[5] = {1, 1, 1, 1, 1};
   return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(addr), (const cuuint64_t*)dims,
-                  (const cuuint64_t*)strides, (const cuuint32_t*)box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  (const cuuint64_t*)strides, (const cuuint32_t*)box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -164,19 +164,19 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
   }
   {
     const uint64_t d[2] = {K1, F}, st[1] = {2 * K1};
-    const uint32_t bk[2] = {8, 128}, bm[2] = {8, 64};
-    ok &= tmap_encode(&out[TM_W3K], w3, 2, d, st, bk);
-    ok &= tmap_encode(&out[TM_W3M], w3, 2, d, st, bm);
+    const uint32_t bk[2] = {64, 128}, bm[2] = {64, 64};
+    ok &= tmap_encode(&out[TM_W3K], w3, 2, d, st, bk, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= tmap_encode(&out[TM_W3M], w3, 2, d, st, bm, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   {
     const uint64_t d[2] = {K1, Bk}, st[1] = {2 * K1};
-    const uint32_t bx[2] = {8, (uint32_t)R};
-    ok &= tmap_encode(&out[TM_A2], r.buf[B_A2], 2, d, st, bx);
+    const uint32_t bx[2] = {64, (uint32_t)R};
+    ok &= tmap_encode(&out[TM_A2], r.buf[B_A2], 2, d, st, bx, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   {
     const uint64_t d[2] = {F, Bk}, st[1] = {2 * F};
-    const uint32_t bx[2] = {8, (uint32_t)R};
-    ok &= tmap_encode(&out[TM_DH], r.buf[B_DH], 2, d, st, bx);
+    const uint32_t bx[2] = {64, (uint32_t)R};
+    ok &= tmap_encode(&out[TM_DH], r.buf[B_DH], 2, d, st, bx, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   return ok;
 }

@@ -60,8 +60,8 @@ __device__ __forceinline__ void chunk_coords(int q, int& i, int& j) {
 }
 
 template <int BN, int STAGES>
-constexpr int tc_smem_bytes() {
-  return STAGES * (128 * 64 * 2 + BN * 64 * 2) + (2 * STAGES + 1) * 8 + 16;
+constexpr int tc_smem_bytes() {  // + 1 KB to realign the dynamic window to 1024 B (128-byte-swizzle atoms)
+  return STAGES * (128 * 64 * 2 + BN * 64 * 2) + (2 * STAGES + 1) * 8 + 16 + 1024;
 }
 
 // Default UMMA descriptors of the cp.async layouts (see tc.cuh).
@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   constexpr int LAG = (STAGES - 1) < 2 ? (STAGES - 1) : 2;  // STAGES == 1: single-K-block ops (LAG 0)
   constexpr int NA = 1024 / kTcProd;                             // A chunks per producer thread
   constexpr int NB = (BN * 8 + kTcProd - 1) / kTcProd;           // B chunks per producer thread
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -610,10 +611,10 @@ enum TmapId : int {
   TM_DZ2W,     // dz2               box (8,16,4,1)   conv2 wgrad B
   TM_W2F,      // W2 shadow (25C1, C2)   box (8, C2) conv2 fwd B
   TM_W2D,      // W2 shadow (C1, 25, C2) box (8,1,C2) conv2 dgrad B
-  TM_W3K,      // W3 shadow (K1, F)      box (8,128) fc1 fwd A
-  TM_W3M,      // W3 shadow (K1, F)      box (8,64)  fc1 dgrad A
-  TM_A2,       // a2 (K1, B)             box (8,R)   fc1 fwd B
-  TM_DH,       // dh (F, B)              box (8,R)   fc1 dgrad B
+  TM_W3K,      // W3 shadow (K1, F)      box (64,128) 128B-swizzled, fc1 fwd A
+  TM_W3M,      // W3 shadow (K1, F)      box (64,64)  128B-swizzled, fc1 dgrad A (MN-major)
+  TM_A2,       // a2 (K1, B)             box (64,R)   128B-swizzled, fc1 fwd B
+  TM_DH,       // dh (F, B)              box (64,R)   128B-swizzled, fc1 dgrad B
   TM_A1H,      // a1                box (8,16,12,1)  conv2 fwd halo (kernels_conv.cuh)
   TM_DZ2H,     // dz2               box (8,16,12,1)  conv2 dgrad halo
   TM_COUNT
@@ -748,6 +749,8 @@ struct TmaConv2Wgrad : TcConv2Wgrad<WQ> {  // split-K over 2048-pixel chunks -> 
 
 __device__ __forceinline__ int batch_rows16(const TcTile& t) { return (t.c->B + 15) & ~15; }
 
+// fc1 operands are wide (K1 = 64 C2, F = 128 w): 64-element (128 B) TMA boxes with
+// 128-byte swizzle, one box per operand (or two for the MN-major W^T) per K block.
 template <int WQ>
 struct TmaFc1Fwd : TcFc1Fwd<WQ> {
   typedef CnnW<WQ> W;
@@ -755,19 +758,14 @@ struct TmaFc1Fwd : TcFc1Fwd<WQ> {
   __device__ void init_stage(const TcTile&, uint8_t*, uint8_t*) const {}
   __device__ uint32_t tx_bytes(const TcTile& t, int kb) const { return 16384 + 128 * batch_rows16(t); }
   __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
-    const int R = batch_rows16(t);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      tc::tma_load_2d(a + 2048 * j, tmap_of(t, TM_W3K), mbar, kb * 64 + 8 * j, t.m0);
-      tc::tma_load_2d(b + 16 * R * j, tmap_of(t, TM_A2), mbar, kb * 64 + 8 * j, 0);
-    }
+    tc::tma_load_2d(a, tmap_of(t, TM_W3K), mbar, kb * 64, t.m0);  // [128 f][64 k] swizzled
+    tc::tma_load_2d(b, tmap_of(t, TM_A2), mbar, kb * 64, 0);      // [R rows][64 k] swizzled
   }
   __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {
-    return tc::sdesc(base + 4096 * ks, 2048, 128);
+    return tc::sdesc_sw128(base + 32 * ks, 16, 1024);
   }
   __device__ uint64_t b_desc(const TcTile& t, uint32_t base, int ks) const {
-    const int R = batch_rows16(t);
-    return tc::sdesc(base + 32 * R * ks, 16 * R, 128);
+    return tc::sdesc_sw128(base + 32 * ks, 16, 1024);
   }
 };
 
@@ -778,18 +776,15 @@ struct TmaFc1Dgrad : TcFc1Dgrad<WQ> {
   __device__ void init_stage(const TcTile&, uint8_t*, uint8_t*) const {}
   __device__ uint32_t tx_bytes(const TcTile& t, int kb) const { return 16384 + 128 * batch_rows16(t); }
   __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
-    const int R = batch_rows16(t);
-#pragma unroll
-    for (int g = 0; g < 16; ++g) tc::tma_load_2d(a + 1024 * g, tmap_of(t, TM_W3M), mbar, t.m0 + 8 * g, kb * 64);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) tc::tma_load_2d(b + 16 * R * j, tmap_of(t, TM_DH), mbar, kb * 64 + 8 * j, 0);
+    tc::tma_load_2d(a, tmap_of(t, TM_W3M), mbar, t.m0, kb * 64);            // [64 f][64 m] swizzled
+    tc::tma_load_2d(a + 8192, tmap_of(t, TM_W3M), mbar, t.m0 + 64, kb * 64);  // next 64 m
+    tc::tma_load_2d(b, tmap_of(t, TM_DH), mbar, kb * 64, 0);                 // [R rows][64 f] swizzled
   }
   __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {
-    return tc::sdesc(base + 256 * ks, 128, 1024);  // MN-major: k rows at 16 B, m groups at 1 KB
+    return tc::sdesc_sw128(base + 2048 * ks, 8192, 1024);  // MN-major: 16 k rows per step, 64-m blocks 8 KB apart
   }
   __device__ uint64_t b_desc(const TcTile& t, uint32_t base, int ks) const {
-    const int R = batch_rows16(t);
-    return tc::sdesc(base + 32 * R * ks, 16 * R, 128);
+    return tc::sdesc_sw128(base + 32 * ks, 16, 1024);
   }
 };
 

@@ -34,6 +34,13 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   return d;                // base_offset 0, lbo_mode 0, layout_type 0 (SWIZZLE_NONE)
 }
 
+// 128-byte-swizzled operand (TMA CU_TENSOR_MAP_SWIZZLE_128B): 8-row x 128 B atoms (1024 B,
+// atom-aligned base); K-major: SBO = 1024, K steps advance the start address by 32 B
+// inside the atom; MN-major: SBO = 1024 (8 k rows), LBO = stride of 64-element MN blocks.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return sdesc(saddr, lbo, sbo) | ((uint64_t)2 << 61);
+}
+
 // ---- instruction descriptor: kind::f16, A/B bf16, D fp32
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4)                      // c_format = F32
