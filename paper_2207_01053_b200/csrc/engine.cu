@@ -293,7 +293,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
     case OP_C1F: return cdiv(rows * 1024, C1F_BM) * cdiv(m.c1, C1F_BN);
     case OP_C2F: return cdiv(rows * 256, C2F_BM) * cdiv(m.c2, C2F_BN);
     case OP_F1F: return cdiv(rows, F1F_BM) * cdiv(m.f, F1F_BN);
-    case OP_HEAD: return 1;
+    case OP_HEAD: return cdiv(m.f, kHeadSlice);
     case OP_F1D: return cdiv(rows, F1D_BM) * cdiv(64 * m.c2, F1D_BN);
     case OP_F1W: return cdiv(m.f, F1W_BM) * cdiv(64 * m.c2, F1W_BN);
     case OP_C2D: return cdiv(rows * 256, C2D_BM) * cdiv(m.c1, C2D_BN);
@@ -496,7 +496,9 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
   HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
   ev = op_begin(ctx, OP_HEAD);
-  k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
+  k_head_a<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
+  k_head_b<T><<<L.grid[OP_HEAD], kHeadSlice, 0, ctx->stream>>>(ha, tasks, dtab + L.prefix_off[OP_HEAD], L.ntask);
+  ctx->launches++;
   op_end(ctx, ev);
   launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab);
   launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
@@ -621,7 +623,9 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Fc1Fwd<T, F1F_BM, F1F_BN>, F1F_BM, F1F_BN>(ctx, {drecs, d}, L, OP_F1F, dtab);
     HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
     int ev = op_begin(ctx, OP_HEAD);
-    k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
+    k_head_a<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
+    k_head_b<T><<<L.grid[OP_HEAD], kHeadSlice, 0, ctx->stream>>>(ha, tasks, dtab + L.prefix_off[OP_HEAD], L.ntask);
+    ctx->launches++;
     op_end(ctx, ev);
     launch_gemm<Fc1Dgrad<T, F1D_BM, F1D_BN>, F1D_BM, F1D_BN>(ctx, {drecs, d}, L, OP_F1D, dtab);
     launch_gemm<Fc1Wgrad<T, F1W_BM, F1W_BN>, F1W_BM, F1W_BN>(ctx, {drecs, d, lr}, L, OP_F1W, dtab);

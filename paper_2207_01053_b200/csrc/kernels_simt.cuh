@@ -640,4 +640,95 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a, const Task* _
   }
 }
 
+// --------------------------------------------------------------------------
+// CNN head split across CTAs (the single-CTA k_head is latency bound):
+//  k_head_a (1 CTA / client): fc2 fwd, softmax-CE, dlogits -> scratch (the
+//           wgrad partial buffer, free at this point of the step), loss.
+//  k_head_b (F/64 CTAs / client): for its 64 features f: dh[:, f] (old W2
+//           column f, ReLU mask), fc1 bias SGD, W2[:, f] SGD; slice 0 also b2.
+// Every W2 column is read and written by exactly one CTA -> race free.
+// --------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kHeadThreads) k_head_a(HeadArgs a, const Task* __restrict__ tasks) {
+  __shared__ float dlog[64 * 64];
+  __shared__ float lossr[64];
+  const Task tk = tasks[blockIdx.x];
+  const ClientRec* c = a.recs + tk.rec;
+  const int rows = tk.rows, F = a.F, C = a.classes;
+  const T* h = (const T*)c->buf[a.hbuf];
+  const float* W = c->params + a.w;
+  const float* bias = c->params + a.b;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int idx = warp; idx < rows * C; idx += kHeadThreads / 32) {
+    const int r = idx / C, cc = idx - r * C;
+    float s = 0.f;
+    for (int f = lane; f < F; f += 32) s = fmaf(ldv(h + (int64_t)r * F + f), W[(int64_t)cc * F + f], s);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) dlog[r * C + cc] = s + bias[cc];
+  }
+  __syncthreads();
+  float* out = (float*)c->buf[B_WSP];
+  if (threadIdx.x < rows) {
+    const int r = threadIdx.x;
+    const int label = c->y[c->perm[tk.base + r]];
+    float mx = -INFINITY;
+    for (int cc = 0; cc < C; ++cc) mx = fmaxf(mx, dlog[r * C + cc]);
+    float s = 0.f;
+    for (int cc = 0; cc < C; ++cc) s += expf(dlog[r * C + cc] - mx);
+    lossr[r] = logf(s) + mx - dlog[r * C + label];
+    const float inv = 1.f / (s * (float)rows);
+    for (int cc = 0; cc < C; ++cc) {
+      const float p = expf(dlog[r * C + cc] - mx);
+      out[r * C + cc] = p * inv - (cc == label ? 1.f / (float)rows : 0.f);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int r = 0; r < rows; ++r) s += lossr[r];
+    c->stats[0] += s / (float)rows;
+  }
+}
+
+constexpr int kHeadSlice = 64;
+template <typename T>
+__global__ void __launch_bounds__(kHeadSlice)
+    k_head_b(HeadArgs a, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
+  __shared__ float dlog[64 * 64];
+  const int ti = find_task(prefix, ntask, blockIdx.x);
+  const Task tk = tasks[ti];
+  const ClientRec* c = a.recs + tk.rec;
+  const int slice = blockIdx.x - __ldg(prefix + ti);
+  const int rows = tk.rows, F = a.F, C = a.classes;
+  const float* dl = (const float*)c->buf[B_WSP];
+  for (int i = threadIdx.x; i < rows * C; i += kHeadSlice) dlog[i] = dl[i];
+  __syncthreads();
+  const int f = slice * kHeadSlice + threadIdx.x;
+  if (f < F) {
+    const T* h = (const T*)c->buf[a.hbuf];
+    T* dh = (T*)c->buf[a.dhbuf];
+    float* W = c->params + a.w;
+    float gb = 0.f;
+    for (int r = 0; r < rows; ++r) {
+      float s = 0.f;
+      for (int cc = 0; cc < C; ++cc) s = fmaf(dlog[r * C + cc], W[(int64_t)cc * F + f], s);
+      s = ldv(h + (int64_t)r * F + f) > 0.f ? s : 0.f;
+      stv(dh + (int64_t)r * F + f, s);
+      gb += s;
+    }
+    c->params[a.b_prev + f] -= a.lr * gb;
+    for (int cc = 0; cc < C; ++cc) {
+      float g = 0.f;
+      for (int r = 0; r < rows; ++r) g = fmaf(dlog[r * C + cc], ldv(h + (int64_t)r * F + f), g);
+      W[(int64_t)cc * F + f] -= a.lr * g;
+    }
+  }
+  if (slice == 0 && threadIdx.x < C) {
+    float g = 0.f;
+    for (int r = 0; r < rows; ++r) g += dlog[r * C + threadIdx.x];
+    c->params[a.b + threadIdx.x] -= a.lr * g;
+  }
+}
+
 }  // namespace protea
