@@ -103,7 +103,7 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
                 ("h", b * f * e), ("dh", b * f * e),
                 ("dz2", b * 256 * c2 * e), ("dz1", b * 1024 * c1 * e)]
         if e == 2:  # bf16 mode: input staged for the tensor cores + padded conv1 weight shadow
-            out += [("xs", b * 36 * 36 * 8 * 2), ("w1p", c1 * 25 * 8 * 2)]
+            out += [("xs", b * 36 * 36 * 8 * 2), ("w1p", c1 * 30 * 8 * 2)]
     elif model == RESNET8:
         out += [("a0", b * 1024 * 16 * e),
                 ("r1", b * 1024 * 16 * e), ("o1", b * 1024 * 16 * e),

@@ -173,6 +173,14 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
     const uint32_t bx[2] = {64, (uint32_t)R};
     ok &= tmap_encode(&out[TM_A2], r.buf[B_A2], 2, d, st, bx, CU_TENSOR_MAP_SWIZZLE_128B);
   }
+  if (r.buf[B_XS]) {
+    const uint64_t dx[4] = {8, 36, 36, Bk}, sx[3] = {16, 36 * 16, 1296 * 16};
+    const uint32_t bx[4] = {8, 16, 13, 1};
+    ok &= tmap_encode(&out[TM_XSH], r.buf[B_XS], 4, dx, sx, bx);
+    const uint64_t dw[2] = {240, C1}, sw[1] = {480};
+    const uint32_t bw[2] = {8, (uint32_t)(C1 < 16 ? 16 : C1)};
+    ok &= tmap_encode(&out[TM_W1P], r.buf[B_W1P], 2, dw, sw, bw);
+  }
   {
     const uint64_t d[2] = {F, Bk}, st[1] = {2 * F};
     const uint32_t bx[2] = {64, (uint32_t)R};
@@ -278,7 +286,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
   }
   if (tc) switch (op) {
       case OP_STAGE: return cdiv(rows * 1296, kStageThreads);
-      case OP_C1F: return rows * 8;
+      case OP_C1F: return cdiv(rows * 8, kConv1TPC);
       case OP_C1W: return 2 * cdiv(rows * 1024, kWgradChunkPx);
       case OP_C1R: return cdiv(76 * m.c1, kReduceBlock);
       case OP_C2F: return m.c1 >= 16 ? cdiv(rows * 2, kConvTPC) : rows * 2;  // halo kernel unless width 1/4
@@ -488,7 +496,21 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   k_stage_x<<<L.grid[OP_STAGE], kStageThreads, 0, ctx->stream>>>(drecs, tasks, dtab + L.prefix_off[OP_STAGE],
                                                                   L.ntask);
   op_end(ctx, ev);
-  launch_gemm_tc<TC_C1F_BN, TC_STAGES>(ctx, TcConv1Fwd<WQ>{drecs, d}, L, OP_C1F, dtab);
+  {
+    typedef HaloConv1<WQ> Op1;
+    static bool attr1 = false;
+    if (!attr1) {
+      cudaFuncSetAttribute(k_conv1_halo<WQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op1::SMEM);
+      attr1 = true;
+    }
+    Op1 op1;
+    op1.recs = drecs;
+    op1.d = d;
+    const int ev1 = op_begin(ctx, OP_C1F);
+    k_conv1_halo<WQ><<<L.grid[OP_C1F], kConvThreads, Op1::SMEM, ctx->stream>>>(op1, tasks,
+                                                                              dtab + L.prefix_off[OP_C1F], L.ntask);
+    op_end(ctx, ev1);
+  }
   if constexpr (WQ >= 2)
     launch_conv_halo<WQ, false>(ctx, drecs, d, L, OP_C2F, dtab);
   else

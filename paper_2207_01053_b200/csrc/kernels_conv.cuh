@@ -192,4 +192,131 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   }
 }
 
+// --------------------------------------------------------------------------
+// conv1 (3 -> C1, 5x5, 32x32 input) on the halo scheme.  Input: the staged bf16
+// batch xs[r][36][36][8] (2-pixel border and channel padding built in, one
+// 16-byte chunk per pixel).  K order = (kx, ky in 0..5, ci 8): one K=16 MMA
+// covers the tap pair (ky, ky+1) of one x-shifted halo copy, so its second
+// 8-element K chunk is simply the next halo row (LBO = 256 B); ky = 5 carries
+// zero weights.  The padded weight shadow w1p is [C1][kx 5][ky 6][8] (B_W1P).
+// Tile = 8 output rows x 16 columns (8 tiles per image); a CTA does one image.
+// --------------------------------------------------------------------------
+constexpr int kConv1TPC = 8;
+template <int WQ>
+struct HaloConv1 {
+  typedef CnnW<WQ> W;
+  static constexpr int N = W::C1 < 16 ? 16 : W::C1;
+  static constexpr int ROWS = 13, COPY = ROWS * 16 * 16, HBYTES = 5 * COPY;
+  static constexpr int B_BYTES = 30 * N * 16;
+  static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 128;
+  static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256;
+  const ClientRec* recs;
+  CnnDims d;
+};
+
+template <int WQ>
+__global__ void __launch_bounds__(kConvThreads, 1)
+    k_conv1_halo(const HaloConv1<WQ> op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
+  typedef HaloConv1<WQ> Op;
+  typedef CnnW<WQ> W;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sH = smem + Op::B_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * Op::HBYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ti = find_task(prefix, ntask, blockIdx.x);
+  TcTile t;
+  t.tk = tasks[ti];
+  t.c = op.recs + t.tk.rec;
+  const int tile0 = (blockIdx.x - __ldg(prefix + ti)) * kConv1TPC;
+  const int ntile = min(kConv1TPC, t.tk.rows * 8 - tile0);
+  t.n_mma = Op::N;
+  const uint32_t bar0 = tc::smem_u32(bars);
+  const uint32_t b_full = bar0, h_full = bar0 + 8, h_empty = bar0 + 24, acc_full = bar0 + 40, acc_empty = bar0 + 56;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(b_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(h_full + 8 * i, 1);
+      tc::mbar_init(h_empty + 8 * i, 1);
+      tc::mbar_init(acc_full + 8 * i, 1);
+      tc::mbar_init(acc_empty + 8 * i, 8);
+    }
+    tc::mbar_fence_init();
+  }
+  if (warp == 9) tc::tmem_alloc(tc::smem_u32(tmem_slot), Op::TMEM_COLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sb = tc::smem_u32(smem), sh = tc::smem_u32(sH);
+  if (warp == 8) {
+    if (lane == 0) {
+      tc::mbar_expect_tx(b_full, Op::B_BYTES);
+      for (int kc = 0; kc < 30; ++kc) tc::tma_load_2d(sb + kc * Op::N * 16, tmap_of(t, TM_W1P), b_full, 8 * kc, 0);
+      for (int i = 0; i < ntile; ++i) {
+        const int buf = i & 1, tile = tile0 + i, r = tile >> 3, y0 = ((tile >> 1) & 3) * 8, x0 = (tile & 1) * 16;
+        if (i >= 2) tc::mbar_wait(h_empty + 8 * buf, ((i >> 1) - 1) & 1);
+        tc::mbar_expect_tx(h_full + 8 * buf, Op::HBYTES);
+        for (int kx = 0; kx < 5; ++kx)  // staged coordinates: output (y, x) reads xs[y + ky][x + kx]
+          tc::tma_load_4d(sh + buf * Op::HBYTES + kx * Op::COPY, tmap_of(t, TM_XSH), h_full + 8 * buf, 0, x0 + kx, y0,
+                          r);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_bf16(128, Op::N, false, false);
+      tc::mbar_wait(b_full, 0);
+      tc::fence_after();
+      for (int i = 0; i < ntile; ++i) {
+        const int acc = i & 1, buf = i & 1;
+        if (i >= 2) tc::mbar_wait(acc_empty + 8 * acc, ((i >> 1) - 1) & 1);
+        tc::mbar_wait(h_full + 8 * buf, (i >> 1) & 1);
+        tc::fence_after();
+        const uint32_t hb = sh + buf * Op::HBYTES, dt = tmem + acc * Op::N;
+        for (int kx = 0; kx < 5; ++kx)
+          for (int p = 0; p < 3; ++p) {
+            const uint64_t da = tc::sdesc(hb + kx * Op::COPY + 2 * p * 256, 256, 128);
+            const uint64_t db = tc::sdesc(sb + (kx * 6 + 2 * p) * Op::N * 16, Op::N * 16, 128);
+            tc::mma_bf16(dt, da, db, idesc, (kx | p) != 0);
+          }
+        tc::commit(h_empty + 8 * buf);
+        tc::commit(acc_full + 8 * acc);
+      }
+    }
+    __syncwarp();
+  } else {
+    constexpr int NV = W::C1 < 16 ? W::C1 : 16;
+    bf16* a1 = (bf16*)t.c->buf[B_A1];
+    uint8_t* i1 = (uint8_t*)t.c->buf[B_I1];
+    for (int i = 0; i < ntile; ++i) {
+      const int acc = i & 1, tile = tile0 + i, r = tile >> 3, y0 = ((tile >> 1) & 3) * 8, x0 = (tile & 1) * 16;
+      tc::mbar_wait(acc_full + 8 * acc, (i >> 1) & 1);
+      tc::fence_after();
+      const int row = (warp & 3) * 32 + lane, y = y0 + (row >> 4), x = x0 + (row & 15), base = lane & 14;
+      for (int c0 = (warp >> 2) * 16; c0 < Op::N; c0 += 32) {
+        float v[16], val[16], best[16];
+        int arg[16];
+        tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(acc * Op::N + c0), v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) val[j] = j < NV ? fmaxf(v[j] + t.c->params[op.d.b1 + c0 + j], 0.f) : 0.f;
+        pool_lanes(val, base, base + 1, base + 16, base + 17, best, arg);
+        if (lane < 16 && (lane & 1) == 0) {
+          const int64_t o = ((int64_t)r * 256 + (y >> 1) * 16 + (x >> 1)) * W::C1 + c0;
+          st_bf16<NV>(a1 + o, best);
+          st_u8<NV>(i1 + o, arg);
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty + 8 * acc);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, Op::TMEM_COLS);
+  }
+}
+
 }  // namespace protea

@@ -17,11 +17,11 @@ __global__ void k_admit_params(const ClientRec* __restrict__ recs, const int* __
     c->params[i] = w;
     if (sh) sh[i] = __float2bfloat16_rn(w);
   }
-  __nv_bfloat16* w1p = (__nv_bfloat16*)c->buf[B_W1P];  // conv1 shadow [c1][25][8] (ci >= 3 zero), W1 at offset 0
+  __nv_bfloat16* w1p = (__nv_bfloat16*)c->buf[B_W1P];  // conv1 shadow [c1][kx 5][ky 6][8], W1 at offset 0
   if (w1p)
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < c->c1 * 200; e += gridDim.x * blockDim.x) {
-      const int co = e / 200, tap = (e % 200) >> 3, ci = e & 7;
-      w1p[e] = __float2bfloat16_rn(ci < 3 ? c->wg[co * 75 + tap * 3 + ci] : 0.f);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < c->c1 * 240; e += gridDim.x * blockDim.x) {
+      const int co = e / 240, rem = e % 240, kx = rem / 48, ky = (rem % 48) >> 3, ci = e & 7;
+      w1p[e] = __float2bfloat16_rn(ky < 5 && ci < 3 ? c->wg[co * 75 + (ky * 5 + kx) * 3 + ci] : 0.f);
     }
   if (blockIdx.x == 0 && threadIdx.x < 16) c->stats[threadIdx.x] = 0.f;
 }

@@ -617,6 +617,8 @@ enum TmapId : int {
   TM_DH,       // dh (F, B)              box (64,R)   128B-swizzled, fc1 dgrad B
   TM_A1H,      // a1                box (8,16,12,1)  conv2 fwd halo (kernels_conv.cuh)
   TM_DZ2H,     // dz2               box (8,16,12,1)  conv2 dgrad halo
+  TM_XSH,      // xs [B][36][36][8]  box (8,16,13,1)  conv1 halo
+  TM_W1P,      // w1p (240, C1)      box (8, N)       conv1 weights [C1][kx][ky6][8]
   TM_COUNT
 };
 
@@ -815,57 +817,6 @@ __global__ void __launch_bounds__(kStageThreads)
   reinterpret_cast<uint4*>(c->buf[B_XS])[e] = out;
 }
 
-template <int WQ>
-struct TcConv1Fwd {  // M = rows*1024 (quad-major 32x32), N = C1, K = 25 taps x 8 (ci padded) = 200 -> 256
-  typedef CnnW<WQ> W;
-  static constexpr bool A_MN = false, B_MN = false;
-  struct PA { const bf16* base; int j; };
-  struct PB { const bf16* row; int j; };
-  const ClientRec* recs;
-  CnnDims d;
-  __device__ void setup(TcTile& t, int local) const {
-    t.m0 = local * 128;
-    t.n0 = 0;
-    t.nk = 4;
-    t.n_mma = W::C1 < 16 ? 16 : W::C1;
-  }
-  __device__ const void* any(const TcTile& t) const { return t.c->params; }
-  __device__ PA a_pre(const TcTile& t, int i, int j) const {
-    const int m = t.m0 + i, r = m >> 10, p = (m >> 2) & 255, q = m & 3;
-    const int y = ((p >> 4) << 1) + (q >> 1), x = ((p & 15) << 1) + (q & 1);
-    return PA{(const bf16*)t.c->buf[B_XS] + ((int64_t)r * 1296 + y * 36 + x) * 8, j};
-  }
-  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
-    const int tap = kb * 8 + s.j;  // one 16-byte chunk = one tap's 8 (padded) channels
-    if (tap >= 25) return nullptr;
-    const int ky = tap / 5, kx = tap - ky * 5;
-    return s.base + (ky * 36 + kx) * 8;
-  }
-  __device__ PB b_pre(const TcTile& t, int i, int j) const {
-    return PB{i < W::C1 ? (const bf16*)t.c->buf[B_W1P] + i * 200 : nullptr, j};
-  }
-  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
-    const int tap = kb * 8 + s.j;
-    if (!s.row || tap >= 25) return nullptr;
-    return s.row + tap * 8;
-  }
-  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
-    constexpr int N = W::C1 < 16 ? W::C1 : 16;
-    const int m = t.m0 + row, r = m >> 10, p = (m & 1023) >> 2, q = m & 3;
-    const int base = (threadIdx.x & 31) & ~3;
-    float val[16], best[16];
-    int arg[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) val[j] = j < N ? fmaxf(v[j] + t.c->params[d.b1 + c0 + j], 0.f) : 0.f;
-    pool_lanes(val, base, base + 1, base + 2, base + 3, best, arg);
-    if (q == 0) {
-      const int64_t o = ((int64_t)r * 256 + p) * W::C1 + c0;
-      st_bf16<N>((bf16*)t.c->buf[B_A1] + o, best);
-      st_u8<N>((uint8_t*)t.c->buf[B_I1] + o, arg);
-    }
-  }
-};
-
 // conv1 wgrad: D[m = tap*8 + ci (+ bias row 200), n = co] = sum_p xs(p, tap, ci) dz1[p][co],
 // split-K over 2048-pixel chunks; the epilogue stores the 75 real rows + bias as
 // partial[split][76][C1] (fp32), summed in split order by k_reduce_conv1_tc.
@@ -940,7 +891,8 @@ __global__ void __launch_bounds__(kReduceBlock)
     float* w = c->params + off_w + co * 75 + idx;
     const float nw = *w - lr * g;
     *w = nw;
-    ((bf16*)c->buf[B_W1P])[co * 200 + (idx / 3) * 8 + idx % 3] = __float2bfloat16_rn(nw);
+    const int tap = idx / 3, ky = tap / 5, kx = tap - ky * 5;  // w1p layout [C1][kx][ky 6][8]
+    ((bf16*)c->buf[B_W1P])[co * 240 + (kx * 6 + ky) * 8 + idx % 3] = __float2bfloat16_rn(nw);
   }
 }
 

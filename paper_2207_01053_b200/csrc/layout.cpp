@@ -134,7 +134,7 @@ SlotLayout slot_layout(const ModelDims& m, int b, int64_t n, int epochs, int e) 
     put(B_DZC1, B * 1024 * m.c1 * e);
     if (e == 2) {
       put(B_XS, B * 36 * 36 * 8 * 2);        // bf16 input staged for the tensor cores: 2-px zero border, ci padded to 8
-      put(B_W1P, (uint64_t)m.c1 * 25 * 8 * 2);  // conv1 weight shadow [c1][25 taps][8 ci] bf16
+      put(B_W1P, (uint64_t)m.c1 * 30 * 8 * 2);  // conv1 weight shadow [c1][kx 5][ky 6][8 ci] bf16
     }
   } else {
     put(B_R_A0, B * 1024 * 16 * e);
