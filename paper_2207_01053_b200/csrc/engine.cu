@@ -140,17 +140,23 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
   bool ok = true;
   {
     const uint64_t d[4] = {C1, 16, 16, Bk}, st[3] = {C1 * 2, 32 * C1, 512 * C1};
-    const uint32_t b8[4] = {8, 16, 8, 1}, b4[4] = {8, 16, 4, 1}, b12[4] = {8, 16, 12, 1};
+    const uint32_t b8[4] = {8, 16, 8, 1}, b4[4] = {8, 16, 4, 1}, b12[4] = {8, 16, 12, 1}, w12[4] = {32, 16, 12, 1};
     ok &= tmap_encode(&out[TM_A1], r.buf[B_A1], 4, d, st, b8);
     ok &= tmap_encode(&out[TM_A1W], r.buf[B_A1], 4, d, st, b4);
-    ok &= tmap_encode(&out[TM_A1H], r.buf[B_A1], 4, d, st, b12);
+    if (C1 >= 32)  // halo copies: 32-channel boxes, 64-byte swizzle (HaloGeom::SW64)
+      ok &= tmap_encode(&out[TM_A1H], r.buf[B_A1], 4, d, st, w12, CU_TENSOR_MAP_SWIZZLE_64B);
+    else
+      ok &= tmap_encode(&out[TM_A1H], r.buf[B_A1], 4, d, st, b12);
   }
   {
     const uint64_t d[4] = {C2, 16, 16, Bk}, st[3] = {C2 * 2, 32 * C2, 512 * C2};
-    const uint32_t b8[4] = {8, 16, 8, 1}, b4[4] = {8, 16, 4, 1}, b12[4] = {8, 16, 12, 1};
+    const uint32_t b8[4] = {8, 16, 8, 1}, b4[4] = {8, 16, 4, 1}, b12[4] = {8, 16, 12, 1}, w12[4] = {32, 16, 12, 1};
     ok &= tmap_encode(&out[TM_DZ2], r.buf[B_DZ2], 4, d, st, b8);
     ok &= tmap_encode(&out[TM_DZ2W], r.buf[B_DZ2], 4, d, st, b4);
-    ok &= tmap_encode(&out[TM_DZ2H], r.buf[B_DZ2], 4, d, st, b12);
+    if (C2 >= 32)
+      ok &= tmap_encode(&out[TM_DZ2H], r.buf[B_DZ2], 4, d, st, w12, CU_TENSOR_MAP_SWIZZLE_64B);
+    else
+      ok &= tmap_encode(&out[TM_DZ2H], r.buf[B_DZ2], 4, d, st, b12);
   }
   {
     const uint64_t d[2] = {25 * C1, C2}, st[1] = {50 * C1};

@@ -26,6 +26,9 @@ constexpr int kConvThreads = 320;
 
 template <int CIN>  // channels of the gathered input (per 32-channel halo group)
 struct HaloGeom {
+  // CIN >= 32: one TMA box (32 ch, 16 px, 12 rows) per x-shift, 64-byte swizzled (64 B pixel rows);
+  // otherwise 8-channel boxes with 16-byte pixel rows (no swizzle).
+  static constexpr bool SW64 = CIN >= 32;
   static constexpr int NCC = CIN < 32 ? CIN / 8 : 4;  // 8-channel chunks per halo group
   static constexpr int GROUPS = CIN / (8 * NCC);       // halo groups per tile
   static constexpr int ROWS = 12;                      // 8 output rows + 4 halo rows
@@ -44,7 +47,7 @@ struct HaloConv2 {
   typedef HaloGeom<CIN> G;
   static constexpr int B_BYTES = 25 * CIN * N * 2;    // resident weights (K x N bf16)
   static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
-  static constexpr int SMEM = B_BYTES + 2 * G::BYTES + 256;
+  static constexpr int SMEM = B_BYTES + 2 * G::BYTES + 256 + 1024;  // + realignment slack
   const ClientRec* recs;
   CnnDims d;
 };
@@ -56,7 +59,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   typedef HaloConv2<WQ, DGRAD> Op;
   typedef typename Op::G G;
   typedef CnnW<WQ> W;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sB = smem;
   uint8_t* sH = smem + Op::B_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * G::BYTES);
@@ -111,10 +115,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         tc::mbar_expect_tx(h_full + 8 * buf, G::BYTES);
         const int r = tile >> 1, y0 = (tile & 1) * 8;
         const uint32_t base = sh + buf * G::BYTES;
-        for (int kx = 0; kx < 5; ++kx)
-          for (int cc = 0; cc < G::NCC; ++cc)
-            tc::tma_load_4d(base + (kx * G::NCC + cc) * G::COPY, tin, h_full + 8 * buf, 8 * (grp * G::NCC + cc),
-                            DGRAD ? 2 - kx : kx - 2, y0 - 2, r);
+        if constexpr (G::SW64) {
+          for (int kx = 0; kx < 5; ++kx)  // copy kx = [12 rows][16 px][32 ch], 64 B swizzled
+            tc::tma_load_4d(base + kx * 4 * G::COPY, tin, h_full + 8 * buf, 32 * grp, DGRAD ? 2 - kx : kx - 2,
+                            y0 - 2, r);
+        } else {
+          for (int kx = 0; kx < 5; ++kx)
+            for (int cc = 0; cc < G::NCC; ++cc)
+              tc::tma_load_4d(base + (kx * G::NCC + cc) * G::COPY, tin, h_full + 8 * buf, 8 * (grp * G::NCC + cc),
+                              DGRAD ? 2 - kx : kx - 2, y0 - 2, r);
+        }
       }
     }
   } else if (warp == 9) {
@@ -138,7 +148,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               const int tap = ky * 5 + kx, row0 = DGRAD ? 4 - ky : ky;
               for (int cp = 0; cp < G::NCC / 2; ++cp) {
                 const uint64_t da =
-                    tc::sdesc(hb + (kx * G::NCC + 2 * cp) * G::COPY + row0 * 256, G::COPY, 128);
+                    G::SW64 ? tc::sdesc_sw64(hb + kx * 4 * G::COPY + row0 * 1024 + 32 * cp, 16, 512)
+                            : tc::sdesc(hb + (kx * G::NCC + 2 * cp) * G::COPY + row0 * 256, G::COPY, 128);
                 uint64_t db;
                 if (!DGRAD) {  // K chunk index of (tap, channel grp*NCC + 2cp)
                   const int kc = tap * (W::C1 / 8) + grp * G::NCC + 2 * cp;
@@ -209,7 +220,7 @@ struct HaloConv1 {
   static constexpr int ROWS = 13, COPY = ROWS * 16 * 16, HBYTES = 5 * COPY;
   static constexpr int B_BYTES = 30 * N * 16;
   static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 128;
-  static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256;
+  static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256 + 1024;
   const ClientRec* recs;
   CnnDims d;
 };
@@ -219,7 +230,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv1_halo(const HaloConv1<WQ> op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
   typedef HaloConv1<WQ> Op;
   typedef CnnW<WQ> W;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sH = smem + Op::B_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * Op::HBYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);

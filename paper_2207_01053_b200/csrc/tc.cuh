@@ -41,6 +41,11 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, ui
   return sdesc(saddr, lbo, sbo) | ((uint64_t)2 << 61);
 }
 
+// 64-byte swizzle (TMA CU_TENSOR_MAP_SWIZZLE_64B): 8-row x 64 B atoms (512 B); K-major SBO = 512.
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return sdesc(saddr, lbo, sbo) | ((uint64_t)4 << 61);
+}
+
 // ---- instruction descriptor: kind::f16, A/B bf16, D fp32
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4)                      // c_format = F32
