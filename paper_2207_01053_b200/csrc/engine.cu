@@ -179,6 +179,14 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
     const uint32_t bx[2] = {64, (uint32_t)R};
     ok &= tmap_encode(&out[TM_A2], r.buf[B_A2], 2, d, st, bx, CU_TENSOR_MAP_SWIZZLE_128B);
   }
+  if (C1 == 32 && C2 == 64) {
+    const uint64_t d1[4] = {C1, 16, 16, Bk}, s1[3] = {C1 * 2, 32 * C1, 512 * C1};
+    const uint32_t b1[4] = {32, 16, 4, 1};
+    ok &= tmap_encode(&out[TM_A1WS], r.buf[B_A1], 4, d1, s1, b1, CU_TENSOR_MAP_SWIZZLE_64B);
+    const uint64_t d2[4] = {C2, 16, 16, Bk}, s2[3] = {C2 * 2, 32 * C2, 512 * C2};
+    const uint32_t b2[4] = {64, 16, 4, 1};
+    ok &= tmap_encode(&out[TM_DZ2WS], r.buf[B_DZ2], 4, d2, s2, b2, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
   if (r.buf[B_XS]) {
     const uint64_t dx[4] = {8, 36, 36, Bk}, sx[3] = {16, 36 * 16, 1296 * 16};
     const uint32_t bx[4] = {8, 16, 13, 1};
@@ -531,7 +539,10 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab);
   launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
   launch_conv_halo<WQ, true>(ctx, drecs, d, L, OP_C2D, dtab);
-  launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2Wgrad<WQ>>(drecs, d, lr), L, OP_C2W, dtab);
+  if constexpr (WQ == 4)
+    launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2WgradSW>(drecs, d, lr), L, OP_C2W, dtab);
+  else
+    launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2Wgrad<WQ>>(drecs, d, lr), L, OP_C2W, dtab);
   ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr, 1};
   ev = op_begin(ctx, OP_C2R);
   k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->stream>>>(r2, tasks, dtab + L.prefix_off[OP_C2R], L.ntask);

@@ -168,26 +168,66 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue warps 0-7
+    // ---------------- epilogue warps 0-7 (warps w, w+4 share TMEM lanes; column chunks c0 = 16 g + 32 j)
+    constexpr int NCH = (Op::N + 31) / 32;                  // chunks per warp group
+    constexpr int NV = Op::NOUT < 16 ? Op::NOUT : 16;        // valid columns per chunk
+    const int g = warp >> 2, row = (warp & 3) * 32 + lane;
+    float bias[NCH][16];
+    if (!DGRAD) {  // conv2 bias, loaded once per CTA
+#pragma unroll
+      for (int j = 0; j < NCH; ++j)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int n = g * 16 + 32 * j + q;
+          bias[j][q] = n < Op::NOUT ? t.c->params[op.d.b2 + n] : 0.f;
+        }
+    }
     for (int i = 0; i < ntile; ++i) {
-      const int acc = i & 1;
+      const int acc = i & 1, m = (tile0 + i) * 128 + row, r = m >> 8, y = (m >> 4) & 15, x = m & 15;
+      // dgrad: prefetch this pixel's pooled activation + argmax (independent of the MMA) before waiting
+      float a1v[NCH][NV];
+      int argv[NCH][NV];
+      if (DGRAD) {
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          const int c0 = g * 16 + 32 * j;
+          if (c0 < Op::N) {
+            const int64_t o = (int64_t)m * W::C1 + c0;
+            ld_bf16<NV>((const bf16*)t.c->buf[B_A1] + o, a1v[j]);
+            ld_u8<NV>((const uint8_t*)t.c->buf[B_I1] + o, argv[j]);
+          }
+        }
+      }
       tc::mbar_wait(acc_full + 8 * acc, (i >> 1) & 1);
       tc::fence_after();
-      t.m0 = (tile0 + i) * 128;
-      const int row = (warp & 3) * 32 + lane;
-      for (int c0 = (warp >> 2) * 16; c0 < Op::N; c0 += 32) {
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const int c0 = g * 16 + 32 * j;
+        if (c0 >= Op::N) continue;
         float v[16];
         tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(acc * Op::N + c0), v);
-        if (DGRAD) {
-          TcConv2Dgrad<WQ> e;
-          e.recs = op.recs;
-          e.d = op.d;
-          e.epilogue(t, row, c0, v);
-        } else {
-          TmaConv2Fwd<WQ> e;
-          e.recs = op.recs;
-          e.d = op.d;
-          e.epilogue(t, row, c0, v);
+        if (DGRAD) {  // pool-1 backward: dz1 = scatter(v * (a1 > 0)) to the argmax of each 2x2 window
+          bf16* dz1 = (bf16*)t.c->buf[B_DZC1];
+          float out[NV];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+#pragma unroll
+            for (int e = 0; e < NV; ++e) out[e] = (argv[j][e] == q && a1v[j][e] > 0.f) ? v[e] : 0.f;
+            const int Y = 2 * y + (q >> 1), X = 2 * x + (q & 1);
+            st_bf16<NV>(dz1 + ((int64_t)r * 1024 + Y * 32 + X) * W::C1 + c0, out);
+          }
+        } else {  // bias + ReLU + 2x2 max-pool (first max) over lanes (l, l+1, l+16, l+17)
+          const int base = lane & 14;
+          float val[16], best[16];
+          int arg[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) val[e] = e < NV ? fmaxf(v[e] + bias[j][e], 0.f) : 0.f;
+          pool_lanes(val, base, base + 1, base + 16, base + 17, best, arg);
+          if (lane < 16 && (lane & 1) == 0) {
+            const int64_t o = ((int64_t)r * 64 + (y >> 1) * 8 + (x >> 1)) * W::C2 + c0;
+            st_bf16<NV>((bf16*)t.c->buf[B_A2] + o, best);
+            st_u8<NV>((uint8_t*)t.c->buf[B_I2] + o, arg);
+          }
         }
       }
       tc::fence_before();

@@ -618,6 +618,8 @@ enum TmapId : int {
   TM_A1H,      // a1                box (8,16,12,1)  conv2 fwd halo (kernels_conv.cuh)
   TM_DZ2H,     // dz2               box (8,16,12,1)  conv2 dgrad halo
   TM_XSH,      // xs [B][36][36][8]  box (8,16,13,1)  conv1 halo
+  TM_A1WS,     // a1  box (32,16,4,1)  64B-swizzled    conv2 wgrad A (width 1)
+  TM_DZ2WS,    // dz2 box (64,16,4,1)  128B-swizzled   conv2 wgrad B (width 1)
   TM_W1P,      // w1p (240, C1)      box (8, N)       conv1 weights [C1][kx][ky6][8]
   TM_COUNT
 };
@@ -746,6 +748,44 @@ struct TmaConv2Wgrad : TcConv2Wgrad<WQ> {  // split-K over 2048-pixel chunks -> 
 #pragma unroll
     for (int j = 0; j < 16; ++j)
       if (c0 + j < W::C2) part[(int64_t)(c0 + j) * N] = v[j];
+  }
+};
+
+// conv2 wgrad, width 1 (C1 = 32, C2 = 64): one 64-byte-swizzled box per tap (32 ci x 64 px) for A
+// (MN-major SW64: 32-element MN blocks 4 KB apart = one tap each) and one 128-byte-swizzled box
+// (64 co x 64 px) for B, instead of 24 16-byte-row boxes per K block.
+struct TmaConv2WgradSW : TmaConv2Wgrad<4> {
+  typedef CnnW<4> W;
+  __device__ void init_stage(const TcTile& t, uint8_t* a, uint8_t* b) const {
+    for (int g = 0; g < 4; ++g) {
+      const int tap = (t.m0 >> 5) + g;
+      if (tap < 25) continue;
+      for (int i = threadIdx.x; i < 64 * 4; i += kTcProd) {  // 64 pixel rows x 4 chunks of 16 B
+        const int r = i >> 2, c = i & 3;  // physical chunk c holds logical chunk c ^ ((r >> 1) & 3)
+        const bool one = tap == 25 && c == ((r >> 1) & 3);
+        reinterpret_cast<uint4*>(a + 4096 * g)[i] = one ? make_uint4(0x3F80u, 0, 0, 0) : make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+  __device__ uint32_t tx_bytes(const TcTile& t, int kb) const {
+    const int valid = 25 - (t.m0 >> 5);
+    return 4096u * (valid < 4 ? (valid < 0 ? 0 : valid) : 4) + 8192u;
+  }
+  __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
+    const int kg = t.n0 * (kWgradChunkPx / 64) + kb, r = kg >> 2, y0 = (kg & 3) * 4;
+    for (int g = 0; g < 4; ++g) {
+      const int tap = (t.m0 >> 5) + g;
+      if (tap >= 25) break;
+      const int ky = tap / 5, kx = tap - ky * 5;
+      tc::tma_load_4d(a + 4096 * g, tmap_of(t, TM_A1WS), mbar, 0, kx - 2, y0 + ky - 2, r);
+    }
+    tc::tma_load_4d(b, tmap_of(t, TM_DZ2WS), mbar, 0, 0, y0, r);
+  }
+  __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {
+    return tc::sdesc_sw64(base + 1024 * ks, 4096, 512);
+  }
+  __device__ uint64_t b_desc(const TcTile&, uint32_t base, int ks) const {
+    return tc::sdesc_sw128(base + 2048 * ks, 16, 1024);
   }
 };
 
