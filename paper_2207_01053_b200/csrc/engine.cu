@@ -98,6 +98,10 @@ struct protea_ctx {
   DevArray<double> wts;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint64_t launches = 0;
+  // side stream: fc1 wgrad (HBM-bound weight RMW) overlaps the conv backward chain (L2 / tensor bound)
+  cudaStream_t side = nullptr;
+  cudaStream_t cur = nullptr;  // stream the launch helpers currently issue to
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   // per-op-class accounting of the current round (protea_round_stats)
   uint32_t time_ops = 0;
   std::vector<cudaEvent_t> evpool;
@@ -218,11 +222,11 @@ int op_begin(protea_ctx* ctx, int op) {
   const int i = (int)ctx->evused;
   ctx->evused += 2;
   ctx->ev_op.push_back(op);
-  cudaEventRecord(ctx->evpool[i], ctx->stream);
+  cudaEventRecord(ctx->evpool[i], ctx->cur);
   return i;
 }
 void op_end(protea_ctx* ctx, int i) {
-  if (i >= 0) cudaEventRecord(ctx->evpool[i + 1], ctx->stream);
+  if (i >= 0) cudaEventRecord(ctx->evpool[i + 1], ctx->cur);
 }
 void reset_ops(protea_ctx* ctx, uint32_t time_ops) {
   ctx->time_ops = time_ops;
@@ -447,7 +451,7 @@ void launch_gemm(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, cons
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int* prefix = dtab + L.prefix_off[opid];
   const int ev = op_begin(ctx, op_class(opid));
-  k_gemm_simt<BM, BN, OpT><<<L.grid[opid], (BM / 4) * (BN / 4), 0, ctx->stream>>>(op, tasks, prefix, L.ntask);
+  k_gemm_simt<BM, BN, OpT><<<L.grid[opid], (BM / 4) * (BN / 4), 0, ctx->cur>>>(op, tasks, prefix, L.ntask);
   op_end(ctx, ev);
 }
 
@@ -462,7 +466,7 @@ void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, c
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int* prefix = dtab + L.prefix_off[opid];
   const int ev = op_begin(ctx, opid);
-  k_gemm_tc<BN, STAGES, OpT><<<L.grid[opid], kTcThreads, SMEM, ctx->stream>>>(op, tasks, prefix, L.ntask);
+  k_gemm_tc<BN, STAGES, OpT><<<L.grid[opid], kTcThreads, SMEM, ctx->cur>>>(op, tasks, prefix, L.ntask);
   op_end(ctx, ev);
 }
 
@@ -480,7 +484,7 @@ void launch_conv_halo(protea_ctx* ctx, const ClientRec* drecs, const CnnDims& d,
   op.d = d;
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int ev = op_begin(ctx, opid);
-  k_conv_halo<WQ, DGRAD><<<L.grid[opid], kConvThreads, Op::SMEM, ctx->stream>>>(op, tasks, dtab + L.prefix_off[opid],
+  k_conv_halo<WQ, DGRAD><<<L.grid[opid], kConvThreads, Op::SMEM, ctx->cur>>>(op, tasks, dtab + L.prefix_off[opid],
                                                                                  L.ntask);
   op_end(ctx, ev);
 }
@@ -507,7 +511,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const CnnDims d = cnn_dims(m);
   int ev = op_begin(ctx, OP_STAGE);
-  k_stage_x<<<L.grid[OP_STAGE], kStageThreads, 0, ctx->stream>>>(drecs, tasks, dtab + L.prefix_off[OP_STAGE],
+  k_stage_x<<<L.grid[OP_STAGE], kStageThreads, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_STAGE],
                                                                   L.ntask);
   op_end(ctx, ev);
   {
@@ -521,7 +525,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
     op1.recs = drecs;
     op1.d = d;
     const int ev1 = op_begin(ctx, OP_C1F);
-    k_conv1_halo<WQ><<<L.grid[OP_C1F], kConvThreads, Op1::SMEM, ctx->stream>>>(op1, tasks,
+    k_conv1_halo<WQ><<<L.grid[OP_C1F], kConvThreads, Op1::SMEM, ctx->cur>>>(op1, tasks,
                                                                               dtab + L.prefix_off[OP_C1F], L.ntask);
     op_end(ctx, ev1);
   }
@@ -532,12 +536,19 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
   HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
   ev = op_begin(ctx, OP_HEAD);
-  k_head_a<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
-  k_head_b<T><<<L.grid[OP_HEAD], kHeadSlice, 0, ctx->stream>>>(ha, tasks, dtab + L.prefix_off[OP_HEAD], L.ntask);
+  k_head_a<T><<<L.ntask, kHeadThreads, 0, ctx->cur>>>(ha, tasks);
+  k_head_b<T><<<L.grid[OP_HEAD], kHeadSlice, 0, ctx->cur>>>(ha, tasks, dtab + L.prefix_off[OP_HEAD], L.ntask);
   ctx->launches++;
   op_end(ctx, ev);
   launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab);
+  // fork: fc1 wgrad (needs dh, a2; fc1 dgrad already read the old W3) runs on the side stream while the
+  // conv backward chain continues on the main stream; joined before the step ends.
+  cudaEventRecord(ctx->fork_ev, ctx->stream);
+  cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0);
+  ctx->cur = ctx->side;
   launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
+  ctx->cur = ctx->stream;
+  cudaEventRecord(ctx->join_ev, ctx->side);
   launch_conv_halo<WQ, true>(ctx, drecs, d, L, OP_C2D, dtab);
   if constexpr (WQ == 4)
     launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2WgradSW>(drecs, d, lr), L, OP_C2W, dtab);
@@ -545,13 +556,14 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
     launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2Wgrad<WQ>>(drecs, d, lr), L, OP_C2W, dtab);
   ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr, 1};
   ev = op_begin(ctx, OP_C2R);
-  k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->stream>>>(r2, tasks, dtab + L.prefix_off[OP_C2R], L.ntask);
+  k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->cur>>>(r2, tasks, dtab + L.prefix_off[OP_C2R], L.ntask);
   op_end(ctx, ev);
   launch_gemm_tc<TC_C1W_BN, TC_STAGES>(ctx, TcConv1Wgrad<WQ>{drecs, d}, L, OP_C1W, dtab);
   ev = op_begin(ctx, OP_C1R);
-  k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->stream>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
+  k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
                                                                        L.ntask, m.c1, d.w1, d.b1, lr);
   op_end(ctx, ev);
+  cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0);  // join the fc1 wgrad branch
 }
 
 void launch_step_tc(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const int32_t* dtab,
@@ -606,7 +618,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
   const Layer& fc = m.layers[7];
   RHeadArgs ha{drecs, m.classes, fc.off_w, fc.off_b, lr};
   int ev = op_begin(ctx, PROTEA_OPC_R_HEAD);
-  k_rhead<T><<<L.ntask, 256, 0, ctx->stream>>>(ha, tasks);
+  k_rhead<T><<<L.ntask, 256, 0, ctx->cur>>>(ha, tasks);
   op_end(ctx, ev);
   // backward, layer 6 (b3b) down to 1 (b1a): dgrad (dout, out, mask, add), then wgrad + reduce
   struct Bw { int dout, out, mask, add, add_mode, cadd; };
@@ -641,7 +653,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
     launch_gemm<Wg, R_BM, R_BN>(ctx, wg, L, RI_W0 + i, dtab);
     ReduceArgs ra{drecs, B_R_WSP, l.cout, 9 * l.cin, l.off_w, l.off_b, l.hout * l.wout, lr, 0};
     ev = op_begin(ctx, PROTEA_OPC_R_REDUCE);
-    k_reduce_update<<<L.grid[RI_R0 + i], kReduceBlock, 0, ctx->stream>>>(ra, tasks, dtab + L.prefix_off[RI_R0 + i],
+    k_reduce_update<<<L.grid[RI_R0 + i], kReduceBlock, 0, ctx->cur>>>(ra, tasks, dtab + L.prefix_off[RI_R0 + i],
                                                                          L.ntask);
     op_end(ctx, ev);
   }
@@ -662,8 +674,8 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Fc1Fwd<T, F1F_BM, F1F_BN>, F1F_BM, F1F_BN>(ctx, {drecs, d}, L, OP_F1F, dtab);
     HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
     int ev = op_begin(ctx, OP_HEAD);
-    k_head_a<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
-    k_head_b<T><<<L.grid[OP_HEAD], kHeadSlice, 0, ctx->stream>>>(ha, tasks, dtab + L.prefix_off[OP_HEAD], L.ntask);
+    k_head_a<T><<<L.ntask, kHeadThreads, 0, ctx->cur>>>(ha, tasks);
+    k_head_b<T><<<L.grid[OP_HEAD], kHeadSlice, 0, ctx->cur>>>(ha, tasks, dtab + L.prefix_off[OP_HEAD], L.ntask);
     ctx->launches++;
     op_end(ctx, ev);
     launch_gemm<Fc1Dgrad<T, F1D_BM, F1D_BN>, F1D_BM, F1D_BN>(ctx, {drecs, d}, L, OP_F1D, dtab);
@@ -672,13 +684,13 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Conv2Wgrad<T, C2W_BM, C2W_BN>, C2W_BM, C2W_BN>(ctx, {drecs, d}, L, OP_C2W, dtab);
     ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr, 0};
     ev = op_begin(ctx, OP_C2R);
-    k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->stream>>>(r2, tasks, dtab + L.prefix_off[OP_C2R],
+    k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->cur>>>(r2, tasks, dtab + L.prefix_off[OP_C2R],
                                                                        L.ntask);
     op_end(ctx, ev);
     launch_gemm<Conv1Wgrad<T, C1W_BM, C1W_BN>, C1W_BM, C1W_BN>(ctx, {drecs, d}, L, OP_C1W, dtab);
     ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr, 0};
     ev = op_begin(ctx, OP_C1R);
-    k_reduce_update<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->stream>>>(r1, tasks, dtab + L.prefix_off[OP_C1R],
+    k_reduce_update<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(r1, tasks, dtab + L.prefix_off[OP_C1R],
                                                                        L.ntask);
     op_end(ctx, ev);
   } else if (m.arch == PROTEA_MODEL_MLP) {
@@ -686,7 +698,7 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<MlpFc1Fwd<T, MF_BM, MF_BN>, MF_BM, MF_BN>(ctx, {drecs, d}, L, OP_MF, dtab);
     HeadArgs ha{drecs, B_H1, B_DZ1, 64, m.classes, d.w2, d.b2, d.b1, lr};
     const int ev = op_begin(ctx, OP_MHEAD);
-    k_head<T><<<L.ntask, kHeadThreads, 0, ctx->stream>>>(ha, tasks);
+    k_head<T><<<L.ntask, kHeadThreads, 0, ctx->cur>>>(ha, tasks);
     op_end(ctx, ev);
     launch_gemm<MlpFc1Wgrad<T, MW_BM, MW_BN>, MW_BM, MW_BN>(ctx, {drecs, d, lr}, L, OP_MW, dtab);
   }
@@ -743,6 +755,13 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
     set_global_error(std::string("protea_init: cudaSetDevice: ") + cudaGetErrorString(e));
     return PROTEA_ERR_CUDA;
   }
+  ctx->cur = ctx->stream;
+  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming) != cudaSuccess) {
+    set_global_error("protea_init: stream/event creation failed");
+    return PROTEA_ERR_CUDA;
+  }
   if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
     set_global_error("protea_init: cudaEventCreate failed");
     return PROTEA_ERR_CUDA;
@@ -776,6 +795,12 @@ void protea_finalize(protea_ctx* ctx) {
   ctx->ptrs.release();
   ctx->wts.release();
   for (auto e : ctx->evpool) cudaEventDestroy(e);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+  }
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
