@@ -283,6 +283,7 @@ int rsplits(const Layer& l, int rows) { return cdiv(rows * l.hout * l.wout, kWgr
 // tensor-core tile shapes (bf16 mode): M tile = 128, BN per op, STAGES-deep ring
 constexpr int TC_C1F_BN = 32, TC_C1W_BN = 32, TC_C2F_BN = 64, TC_C2D_BN = 32, TC_C2W_BN = 64, TC_F1F_BN = 64, TC_F1D_BN = 64, TC_F1W_BN = 128;
 constexpr int TC_STAGES = 4, TC_F1W_STAGES = 1;
+constexpr bool kOverlapFc1Wgrad = false;
 
 int tiles(const ModelDims& m, int op, int rows, bool tc) {
   if (op >= RI_F0) {
@@ -541,14 +542,18 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   ctx->launches++;
   op_end(ctx, ev);
   launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab);
-  // fork: fc1 wgrad (needs dh, a2; fc1 dgrad already read the old W3) runs on the side stream while the
-  // conv backward chain continues on the main stream; joined before the step ends.
-  cudaEventRecord(ctx->fork_ev, ctx->stream);
-  cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0);
-  ctx->cur = ctx->side;
+  // Optional fork (kOverlapFc1Wgrad): fc1 wgrad (needs dh, a2; fc1 dgrad already read the old W3) on the side
+  // stream while the conv backward chain continues on the main stream.  Measured on B200: the concurrent
+  // kernels contend (the 225 KB-smem halo convs cannot co-reside with the RMW CTAs), 101 -> 105 ms/round,
+  // so it is off by default.
+  if (kOverlapFc1Wgrad) {
+    cudaEventRecord(ctx->fork_ev, ctx->stream);
+    cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0);
+    ctx->cur = ctx->side;
+  }
   launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
   ctx->cur = ctx->stream;
-  cudaEventRecord(ctx->join_ev, ctx->side);
+  if (kOverlapFc1Wgrad) cudaEventRecord(ctx->join_ev, ctx->side);
   launch_conv_halo<WQ, true>(ctx, drecs, d, L, OP_C2D, dtab);
   if constexpr (WQ == 4)
     launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2WgradSW>(drecs, d, lr), L, OP_C2W, dtab);
@@ -563,7 +568,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
                                                                        L.ntask, m.c1, d.w1, d.b1, lr);
   op_end(ctx, ev);
-  cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0);  // join the fc1 wgrad branch
+  if (kOverlapFc1Wgrad) cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0);  // join the fc1 wgrad branch
 }
 
 void launch_step_tc(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const int32_t* dtab,
