@@ -305,14 +305,14 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
   }
   if (tc) switch (op) {
       case OP_STAGE: return cdiv(rows * 1296, kStageThreads);
-      case OP_C1F: return cdiv(rows * 8, kConv1TPC);
+      case OP_C1F: return rows * 8;  // persistent halo kernel: prefix over 128-pixel tiles
       case OP_C1W: return 2 * cdiv(rows * 1024, kWgradChunkPx);
       case OP_C1R: return cdiv(76 * m.c1, kReduceBlock);
-      case OP_C2F: return m.c1 >= 16 ? cdiv(rows * 2, kConvTPC) : rows * 2;  // halo kernel unless width 1/4
+      case OP_C2F: return rows * 2;  // halo kernel (width >= 1/2) or TmaConv2Fwd: both 128-pixel tiles
       case OP_F1F: return m.f / 128;
       case OP_F1D: return 64 * m.c2 / 128;
       case OP_F1W: return (64 * m.c2 / 128) * cdiv(m.f, 128);
-      case OP_C2D: return cdiv(rows * 2, kConvTPC);
+      case OP_C2D: return rows * 2;
       case OP_C2W: return cdiv(rows * 256, kWgradChunkPx) * cdiv(25 * m.c1 + 1, 128);
       default: break;
     }
@@ -471,22 +471,23 @@ void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, c
   op_end(ctx, ev);
 }
 
-template <int WQ, bool DGRAD>
-void launch_conv_halo(protea_ctx* ctx, const ClientRec* drecs, const CnnDims& d, const Launch& L, int opid,
-                      const int32_t* dtab) {
-  typedef HaloConv2<WQ, DGRAD> Op;
+int g_num_sms = 148;
+
+template <class Op>
+void launch_conv_persistent(protea_ctx* ctx, const ClientRec* drecs, const CnnDims& d, const Launch& L, int opid,
+                            const int32_t* dtab) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_conv_halo<WQ, DGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
+    cudaFuncSetAttribute(k_conv_persistent<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
     attr = true;
   }
   Op op;
   op.recs = drecs;
   op.d = d;
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const int grid = std::min(L.grid[opid], g_num_sms);  // one CTA per SM, each a contiguous tile range
   const int ev = op_begin(ctx, opid);
-  k_conv_halo<WQ, DGRAD><<<L.grid[opid], kConvThreads, Op::SMEM, ctx->cur>>>(op, tasks, dtab + L.prefix_off[opid],
-                                                                                 L.ntask);
+  k_conv_persistent<Op><<<grid, kConvThreads, Op::SMEM, ctx->cur>>>(op, tasks, dtab + L.prefix_off[opid], L.ntask);
   op_end(ctx, ev);
 }
 
@@ -515,23 +516,9 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   k_stage_x<<<L.grid[OP_STAGE], kStageThreads, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_STAGE],
                                                                   L.ntask);
   op_end(ctx, ev);
-  {
-    typedef HaloConv1<WQ> Op1;
-    static bool attr1 = false;
-    if (!attr1) {
-      cudaFuncSetAttribute(k_conv1_halo<WQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op1::SMEM);
-      attr1 = true;
-    }
-    Op1 op1;
-    op1.recs = drecs;
-    op1.d = d;
-    const int ev1 = op_begin(ctx, OP_C1F);
-    k_conv1_halo<WQ><<<L.grid[OP_C1F], kConvThreads, Op1::SMEM, ctx->cur>>>(op1, tasks,
-                                                                              dtab + L.prefix_off[OP_C1F], L.ntask);
-    op_end(ctx, ev1);
-  }
+  launch_conv_persistent<HaloConv1<WQ>>(ctx, drecs, d, L, OP_C1F, dtab);
   if constexpr (WQ >= 2)
-    launch_conv_halo<WQ, false>(ctx, drecs, d, L, OP_C2F, dtab);
+    launch_conv_persistent<HaloConv2<WQ, false>>(ctx, drecs, d, L, OP_C2F, dtab);
   else
     launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TmaConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
   launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
@@ -554,7 +541,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
   ctx->cur = ctx->stream;
   if (kOverlapFc1Wgrad) cudaEventRecord(ctx->join_ev, ctx->side);
-  launch_conv_halo<WQ, true>(ctx, drecs, d, L, OP_C2D, dtab);
+  launch_conv_persistent<HaloConv2<WQ, true>>(ctx, drecs, d, L, OP_C2D, dtab);
   if constexpr (WQ == 4)
     launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2WgradSW>(drecs, d, lr), L, OP_C2W, dtab);
   else
@@ -761,6 +748,11 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
     return PROTEA_ERR_CUDA;
   }
   ctx->cur = ctx->stream;
+  {
+    int nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, opts->device) == cudaSuccess && nsm > 0)
+      g_num_sms = nsm;
+  }
   if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming) != cudaSuccess) {

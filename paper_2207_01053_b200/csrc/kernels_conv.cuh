@@ -1,17 +1,18 @@
-// kernels_conv.cuh — "halo" implicit-GEMM 5x5 convolution on tcgen05 (bf16 mode).
+// kernels_conv.cuh — persistent "halo" implicit-GEMM 5x5 convolutions on tcgen05 (bf16 mode).
 //
-// conv2 fwd (M = output pixels, N = C2, K = 25 taps x C1) and conv2 dgrad
-// (M = a1 pixels, N = C1, K = 25 taps x C2) re-read every input element once
-// per tap when the im2col operand is gathered per K block.  Here a CTA owns
-// TPC consecutive 128-pixel tiles (8 image rows x 16 columns) of ONE client:
-//  * its whole weight operand (all 25 taps) is loaded once by TMA and stays
-//    resident in shared memory;
+// conv1 fwd (M = output pixels, N = C1, K = 25 taps x 3 (padded 8) ch), conv2 fwd
+// (N = C2, K = 25 x C1) and conv2 dgrad (M = a1 pixels, N = C1, K = 25 x C2)
+// re-read every input element once per tap when the im2col operand is gathered
+// per K block.  Here:
+//  * a PERSISTENT CTA (one per SM) walks a contiguous range of the iteration's
+//    128-pixel tiles (8 image rows x 16 columns), client after client;
+//  * the weight operand of the current client (all 25 taps) is loaded once by
+//    TMA and stays resident in shared memory until the range moves to the
+//    next client (b_full / b_empty barriers);
 //  * per tile (and per 32-channel group of the input) the TMA loads the input
-//    halo ONCE as 5 x-shifted copies [kx][channel chunk][12 rows][16 px][8 ch]
-//    (out-of-bounds rows / columns are the TMA's zero fill = the conv padding);
-//  * the A operand of tap (ky, kx) is then just a UMMA descriptor into copy kx
-//    starting at row ky: 128 consecutive 16-byte pixel rows (SBO = 128 B), the
-//    second 8-channel chunk of the K=16 MMA one copy further (LBO = 12*256 B);
+//    halo ONCE as 5 x-shifted copies (out-of-bounds rows / columns are the
+//    TMA's zero fill = the conv padding); the A operand of tap (ky, kx) is then
+//    only a UMMA descriptor into copy kx starting at row ky;
 //  * the halo is double-buffered and the fp32 accumulator double-buffered in
 //    TMEM, so TMA, tcgen05.mma and the epilogue of the previous tile overlap.
 // Warp roles: warps 0-7 epilogue (tcgen05.ld + fused layer epilogue), warp 8
@@ -21,9 +22,11 @@
 
 namespace protea {
 
-constexpr int kConvTPC = 4;  // 128-pixel tiles per CTA (2 images of 16x16)
 constexpr int kConvThreads = 320;
 
+// ---------------------------------------------------------------------------
+// conv2 fwd / dgrad
+// ---------------------------------------------------------------------------
 template <int CIN>  // channels of the gathered input (per 32-channel halo group)
 struct HaloGeom {
   // CIN >= 32: one TMA box (32 ch, 16 px, 12 rows) per x-shift, 64-byte swizzled (64 B pixel rows);
@@ -32,261 +35,237 @@ struct HaloGeom {
   static constexpr int NCC = CIN < 32 ? CIN / 8 : 4;  // 8-channel chunks per halo group
   static constexpr int GROUPS = CIN / (8 * NCC);       // halo groups per tile
   static constexpr int ROWS = 12;                      // 8 output rows + 4 halo rows
-  static constexpr int COPY = ROWS * 16 * 16;          // bytes of one (kx, chunk) copy
+  static constexpr int COPY = ROWS * 16 * 16;          // bytes of one (kx, 8-channel chunk) copy
   static constexpr int BYTES = 5 * NCC * COPY;         // one halo buffer
 };
 
-// Fwd: input a1 (C1 channels), weights K-major [kchunk][C2][8]; epilogue = TmaConv2Fwd's.
-// Dgrad: input dz2 (C2 channels, flipped taps), weights MN-major [tap][C1/8][C2][8]; epilogue = TcConv2Dgrad's.
+// Fwd: input a1 (C1 channels), weights K-major [kchunk][C2][8]; epilogue bias + ReLU + 2x2 pool -> a2, i2.
+// Dgrad: input dz2 (C2 channels, flipped taps), weights MN-major [tap][C1/8][C2][8]; epilogue ReLU mask
+// + pool-1 backward scatter -> dz1.
 template <int WQ, bool DGRAD>
 struct HaloConv2 {
   typedef CnnW<WQ> W;
   static constexpr int CIN = DGRAD ? W::C2 : W::C1;   // gathered input channels
-  static constexpr int NOUT = DGRAD ? W::C1 : W::C2;  // MMA N (valid)
+  static constexpr int NOUT = DGRAD ? W::C1 : W::C2;  // valid output channels
   static constexpr int N = NOUT < 16 ? 16 : NOUT;     // MMA N
+  static constexpr bool B_MN = DGRAD;
   typedef HaloGeom<CIN> G;
+  static constexpr int GROUPS = G::GROUPS;
+  static constexpr int HBYTES = G::BYTES;
   static constexpr int B_BYTES = 25 * CIN * N * 2;    // resident weights (K x N bf16)
   static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
-  static constexpr int SMEM = B_BYTES + 2 * G::BYTES + 256 + 1024;  // + realignment slack
+  static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256 + 1024;  // + realignment slack
+  static constexpr int TILES_PER_IMAGE = 2;
   const ClientRec* recs;
   CnnDims d;
+
+  __device__ void load_b(const TcTile& t, uint32_t sb, uint32_t bar) const {
+    if (!DGRAD) {  // [kchunk][C2][8]: box (8, C2) per 8-wide K chunk
+      for (int kc = 0; kc < 25 * W::C1 / 8; ++kc) tc::tma_load_2d(sb + kc * N * 16, tmap_of(t, TM_W2F), bar, 8 * kc, 0);
+    } else {  // [tap][C1/8 (padded to N/8)][C2][8]: box (8 ci, 1 tap, C2 co)
+      for (int tap = 0; tap < 25; ++tap)
+        for (int nc = 0; nc < N / 8; ++nc)
+          tc::tma_load_3d(sb + (tap * (N / 8) + nc) * W::C2 * 16, tmap_of(t, TM_W2D), bar, 8 * nc, tap, 0);
+    }
+  }
+  __device__ void load_halo(const TcTile& t, int tile, int grp, uint32_t base, uint32_t bar) const {
+    const void* tin = tmap_of(t, DGRAD ? TM_DZ2H : TM_A1H);
+    const int r = tile >> 1, y0 = (tile & 1) * 8;
+    if constexpr (G::SW64) {
+      for (int kx = 0; kx < 5; ++kx)  // copy kx = [12 rows][16 px][32 ch], 64 B swizzled
+        tc::tma_load_4d(base + kx * 4 * G::COPY, tin, bar, 32 * grp, DGRAD ? 2 - kx : kx - 2, y0 - 2, r);
+    } else {
+      for (int kx = 0; kx < 5; ++kx)
+        for (int cc = 0; cc < G::NCC; ++cc)
+          tc::tma_load_4d(base + (kx * G::NCC + cc) * G::COPY, tin, bar, 8 * (grp * G::NCC + cc),
+                          DGRAD ? 2 - kx : kx - 2, y0 - 2, r);
+    }
+  }
+  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc) const {
+    for (int ky = 0; ky < 5; ++ky)
+      for (int kx = 0; kx < 5; ++kx) {
+        const int tap = ky * 5 + kx, row0 = DGRAD ? 4 - ky : ky;
+        for (int cp = 0; cp < G::NCC / 2; ++cp) {
+          const uint64_t da = G::SW64 ? tc::sdesc_sw64(hb + kx * 4 * G::COPY + row0 * 1024 + 32 * cp, 16, 512)
+                                      : tc::sdesc(hb + (kx * G::NCC + 2 * cp) * G::COPY + row0 * 256, G::COPY, 128);
+          uint64_t db;
+          if (!DGRAD) {  // K chunk index of (tap, channel grp*NCC + 2cp)
+            const int kc = tap * (W::C1 / 8) + grp * G::NCC + 2 * cp;
+            db = tc::sdesc(sb + kc * N * 16, N * 16, 128);
+          } else {  // k rows = co (16 of them) of tap; n groups at C2*16
+            const int co0 = (grp * G::NCC + 2 * cp) * 8;
+            db = tc::sdesc(sb + tap * (N / 8) * W::C2 * 16 + co0 * 16, 128, W::C2 * 16);
+          }
+          tc::mma_bf16(dt, da, db, idesc, (grp | tap | cp) != 0);
+        }
+      }
+  }
+  // Epilogue of one tile: warps w, w+4 share TMEM lanes; column chunks c0 = 16 g + 32 j.
+  __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
+                           int lane) const {
+    constexpr int NCH = (N + 31) / 32;
+    constexpr int NV = NOUT < 16 ? NOUT : 16;
+    const int g = warp >> 2, row = (warp & 3) * 32 + lane;
+    const int m = tile * 128 + row, r = m >> 8, y = (m >> 4) & 15, x = m & 15;
+    float a1v[NCH][NV];
+    int argv[NCH][NV];
+    float bias[NCH][16];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {  // operands independent of the MMA: fetch before waiting
+      const int c0 = g * 16 + 32 * j;
+      if (c0 >= N) continue;
+      if (DGRAD) {
+        const int64_t o = (int64_t)m * W::C1 + c0;
+        ld_bf16<NV>((const bf16*)t.c->buf[B_A1] + o, a1v[j]);
+        ld_u8<NV>((const uint8_t*)t.c->buf[B_I1] + o, argv[j]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) bias[j][q] = q < NV ? t.c->params[d.b2 + c0 + q] : 0.f;
+      }
+    }
+    tc::mbar_wait(full_bar, parity);
+    tc::fence_after();
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c0 = g * 16 + 32 * j;
+      if (c0 >= N) continue;
+      float v[16];
+      tc::tmem_ld16(tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
+      if (DGRAD) {  // pool-1 backward: dz1 = scatter(v * (a1 > 0)) to the argmax of each 2x2 window
+        bf16* dz1 = (bf16*)t.c->buf[B_DZC1];
+        float out[NV];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+          for (int e = 0; e < NV; ++e) out[e] = (argv[j][e] == q && a1v[j][e] > 0.f) ? v[e] : 0.f;
+          const int Y = 2 * y + (q >> 1), X = 2 * x + (q & 1);
+          st_bf16<NV>(dz1 + ((int64_t)r * 1024 + Y * 32 + X) * W::C1 + c0, out);
+        }
+      } else {  // bias + ReLU + 2x2 max-pool (first max) over lanes (l, l+1, l+16, l+17)
+        const int base = lane & 14;
+        float val[16], best[16];
+        int arg[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) val[e] = e < NV ? fmaxf(v[e] + bias[j][e], 0.f) : 0.f;
+        pool_lanes(val, base, base + 1, base + 16, base + 17, best, arg);
+        if (lane < 16 && (lane & 1) == 0) {
+          const int64_t o = ((int64_t)r * 64 + (y >> 1) * 8 + (x >> 1)) * W::C2 + c0;
+          st_bf16<NV>((bf16*)t.c->buf[B_A2] + o, best);
+          st_u8<NV>((uint8_t*)t.c->buf[B_I2] + o, arg);
+        }
+      }
+    }
+  }
 };
 
-template <int WQ, bool DGRAD>
-__global__ void __launch_bounds__(kConvThreads, 1)
-    k_conv_halo(const HaloConv2<WQ, DGRAD> op, const Task* __restrict__ tasks, const int* __restrict__ prefix,
-                int ntask) {
-  typedef HaloConv2<WQ, DGRAD> Op;
-  typedef typename Op::G G;
-  typedef CnnW<WQ> W;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* sB = smem;
-  uint8_t* sH = smem + Op::B_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * G::BYTES);
-  // barriers: 0 b_full, 1-2 h_full, 3-4 h_empty, 5-6 acc_full, 7-8 acc_empty
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  const int ti = find_task(prefix, ntask, blockIdx.x);
-  TcTile t;
-  t.tk = tasks[ti];
-  t.c = op.recs + t.tk.rec;
-  const int tile0 = (blockIdx.x - __ldg(prefix + ti)) * kConvTPC;
-  const int ntile = min(kConvTPC, t.tk.rows * 2 - tile0);
-  t.n_mma = Op::N;
-
-  const uint32_t bar0 = tc::smem_u32(bars);
-  const uint32_t b_full = bar0, h_full = bar0 + 8, h_empty = bar0 + 24, acc_full = bar0 + 40, acc_empty = bar0 + 56;
-  if (threadIdx.x == 0) {
-    tc::mbar_init(b_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(h_full + 8 * i, 1);
-      tc::mbar_init(h_empty + 8 * i, 1);
-      tc::mbar_init(acc_full + 8 * i, 1);
-      tc::mbar_init(acc_empty + 8 * i, 8);
-    }
-    tc::mbar_fence_init();
-  }
-  if (warp == 9) tc::tmem_alloc(tc::smem_u32(tmem_slot), Op::TMEM_COLS);
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t sb = tc::smem_u32(sB), sh = tc::smem_u32(sH);
-  const int nstage = ntile * G::GROUPS;
-
-  if (warp == 8) {
-    if (lane == 0) {
-      // ---------------- TMA producer
-      const void* tin = tmap_of(t, DGRAD ? TM_DZ2H : TM_A1H);
-      tc::mbar_expect_tx(b_full, Op::B_BYTES);
-      if (!DGRAD) {  // [kchunk][C2][8]: box (8, C2) per 8-wide K chunk
-        for (int kc = 0; kc < 25 * W::C1 / 8; ++kc)
-          tc::tma_load_2d(sb + kc * Op::N * 16, tmap_of(t, TM_W2F), b_full, 8 * kc, 0);
-      } else {  // [tap][C1/8 (padded to N/8)][C2][8]: box (8 ci, 1 tap, C2 co)
-        for (int tap = 0; tap < 25; ++tap)
-          for (int nc = 0; nc < Op::N / 8; ++nc)
-            tc::tma_load_3d(sb + (tap * (Op::N / 8) + nc) * W::C2 * 16, tmap_of(t, TM_W2D), b_full, 8 * nc, tap, 0);
-      }
-      for (int s = 0; s < nstage; ++s) {
-        const int buf = s & 1, tile = tile0 + s / G::GROUPS, grp = s % G::GROUPS;
-        if (s >= 2) tc::mbar_wait(h_empty + 8 * buf, ((s >> 1) - 1) & 1);
-        tc::mbar_expect_tx(h_full + 8 * buf, G::BYTES);
-        const int r = tile >> 1, y0 = (tile & 1) * 8;
-        const uint32_t base = sh + buf * G::BYTES;
-        if constexpr (G::SW64) {
-          for (int kx = 0; kx < 5; ++kx)  // copy kx = [12 rows][16 px][32 ch], 64 B swizzled
-            tc::tma_load_4d(base + kx * 4 * G::COPY, tin, h_full + 8 * buf, 32 * grp, DGRAD ? 2 - kx : kx - 2,
-                            y0 - 2, r);
-        } else {
-          for (int kx = 0; kx < 5; ++kx)
-            for (int cc = 0; cc < G::NCC; ++cc)
-              tc::tma_load_4d(base + (kx * G::NCC + cc) * G::COPY, tin, h_full + 8 * buf, 8 * (grp * G::NCC + cc),
-                              DGRAD ? 2 - kx : kx - 2, y0 - 2, r);
-        }
-      }
-    }
-  } else if (warp == 9) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
-      const uint32_t idesc = tc::idesc_bf16(128, Op::N, false, DGRAD);
-      tc::mbar_wait(b_full, 0);
-      tc::fence_after();
-      for (int i = 0; i < ntile; ++i) {
-        const int acc = i & 1;
-        if (i >= 2) tc::mbar_wait(acc_empty + 8 * acc, ((i >> 1) - 1) & 1);
-        tc::fence_after();
-        const uint32_t dt = tmem + acc * Op::N;
-        for (int grp = 0; grp < G::GROUPS; ++grp) {
-          const int s = i * G::GROUPS + grp, buf = s & 1;
-          tc::mbar_wait(h_full + 8 * buf, (s >> 1) & 1);
-          tc::fence_after();
-          const uint32_t hb = sh + buf * G::BYTES;
-          for (int ky = 0; ky < 5; ++ky)
-            for (int kx = 0; kx < 5; ++kx) {
-              const int tap = ky * 5 + kx, row0 = DGRAD ? 4 - ky : ky;
-              for (int cp = 0; cp < G::NCC / 2; ++cp) {
-                const uint64_t da =
-                    G::SW64 ? tc::sdesc_sw64(hb + kx * 4 * G::COPY + row0 * 1024 + 32 * cp, 16, 512)
-                            : tc::sdesc(hb + (kx * G::NCC + 2 * cp) * G::COPY + row0 * 256, G::COPY, 128);
-                uint64_t db;
-                if (!DGRAD) {  // K chunk index of (tap, channel grp*NCC + 2cp)
-                  const int kc = tap * (W::C1 / 8) + grp * G::NCC + 2 * cp;
-                  db = tc::sdesc(sb + kc * Op::N * 16, Op::N * 16, 128);
-                } else {  // k rows = co (16 of them) of tap; n groups at C2*16
-                  const int co0 = (grp * G::NCC + 2 * cp) * 8;
-                  db = tc::sdesc(sb + tap * (Op::N / 8) * W::C2 * 16 + co0 * 16, 128, W::C2 * 16);
-                }
-                tc::mma_bf16(dt, da, db, idesc, (grp | tap | cp) != 0);
-              }
-            }
-          tc::commit(h_empty + 8 * buf);
-        }
-        tc::commit(acc_full + 8 * acc);
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---------------- epilogue warps 0-7 (warps w, w+4 share TMEM lanes; column chunks c0 = 16 g + 32 j)
-    constexpr int NCH = (Op::N + 31) / 32;                  // chunks per warp group
-    constexpr int NV = Op::NOUT < 16 ? Op::NOUT : 16;        // valid columns per chunk
-    const int g = warp >> 2, row = (warp & 3) * 32 + lane;
-    float bias[NCH][16];
-    if (!DGRAD) {  // conv2 bias, loaded once per CTA
-#pragma unroll
-      for (int j = 0; j < NCH; ++j)
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int n = g * 16 + 32 * j + q;
-          bias[j][q] = n < Op::NOUT ? t.c->params[op.d.b2 + n] : 0.f;
-        }
-    }
-    for (int i = 0; i < ntile; ++i) {
-      const int acc = i & 1, m = (tile0 + i) * 128 + row, r = m >> 8, y = (m >> 4) & 15, x = m & 15;
-      // dgrad: prefetch this pixel's pooled activation + argmax (independent of the MMA) before waiting
-      float a1v[NCH][NV];
-      int argv[NCH][NV];
-      if (DGRAD) {
-#pragma unroll
-        for (int j = 0; j < NCH; ++j) {
-          const int c0 = g * 16 + 32 * j;
-          if (c0 < Op::N) {
-            const int64_t o = (int64_t)m * W::C1 + c0;
-            ld_bf16<NV>((const bf16*)t.c->buf[B_A1] + o, a1v[j]);
-            ld_u8<NV>((const uint8_t*)t.c->buf[B_I1] + o, argv[j]);
-          }
-        }
-      }
-      tc::mbar_wait(acc_full + 8 * acc, (i >> 1) & 1);
-      tc::fence_after();
-#pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        const int c0 = g * 16 + 32 * j;
-        if (c0 >= Op::N) continue;
-        float v[16];
-        tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(acc * Op::N + c0), v);
-        if (DGRAD) {  // pool-1 backward: dz1 = scatter(v * (a1 > 0)) to the argmax of each 2x2 window
-          bf16* dz1 = (bf16*)t.c->buf[B_DZC1];
-          float out[NV];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-#pragma unroll
-            for (int e = 0; e < NV; ++e) out[e] = (argv[j][e] == q && a1v[j][e] > 0.f) ? v[e] : 0.f;
-            const int Y = 2 * y + (q >> 1), X = 2 * x + (q & 1);
-            st_bf16<NV>(dz1 + ((int64_t)r * 1024 + Y * 32 + X) * W::C1 + c0, out);
-          }
-        } else {  // bias + ReLU + 2x2 max-pool (first max) over lanes (l, l+1, l+16, l+17)
-          const int base = lane & 14;
-          float val[16], best[16];
-          int arg[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) val[e] = e < NV ? fmaxf(v[e] + bias[j][e], 0.f) : 0.f;
-          pool_lanes(val, base, base + 1, base + 16, base + 17, best, arg);
-          if (lane < 16 && (lane & 1) == 0) {
-            const int64_t o = ((int64_t)r * 64 + (y >> 1) * 8 + (x >> 1)) * W::C2 + c0;
-            st_bf16<NV>((bf16*)t.c->buf[B_A2] + o, best);
-            st_u8<NV>((uint8_t*)t.c->buf[B_I2] + o, arg);
-          }
-        }
-      }
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(acc_empty + 8 * acc);
-    }
-  }
-  tc::fence_before();
-  __syncthreads();
-  if (warp == 9) {
-    tc::fence_after();
-    tc::tmem_dealloc(tmem, Op::TMEM_COLS);
-  }
-}
-
-// --------------------------------------------------------------------------
-// conv1 (3 -> C1, 5x5, 32x32 input) on the halo scheme.  Input: the staged bf16
-// batch xs[r][36][36][8] (2-pixel border and channel padding built in, one
-// 16-byte chunk per pixel).  K order = (kx, ky in 0..5, ci 8): one K=16 MMA
-// covers the tap pair (ky, ky+1) of one x-shifted halo copy, so its second
-// 8-element K chunk is simply the next halo row (LBO = 256 B); ky = 5 carries
-// zero weights.  The padded weight shadow w1p is [C1][kx 5][ky 6][8] (B_W1P).
-// Tile = 8 output rows x 16 columns (8 tiles per image); a CTA does one image.
-// --------------------------------------------------------------------------
-constexpr int kConv1TPC = 8;
+// ---------------------------------------------------------------------------
+// conv1 fwd (3 -> C1, 32x32 input).  Input: the staged bf16 batch xs[r][36][36][8]
+// (2-pixel border and channel padding built in, one 16-byte chunk per pixel).
+// K order = (kx, ky in 0..5, ci 8): one K=16 MMA covers the tap pair (ky, ky+1)
+// of one x-shifted halo copy, so its second 8-element K chunk is simply the next
+// halo row (LBO = 256 B); ky = 5 carries zero weights.  Weights: w1p
+// [C1][kx 5][ky 6][8].  Tile = 8 output rows x 16 columns (8 tiles per image).
+// ---------------------------------------------------------------------------
 template <int WQ>
 struct HaloConv1 {
   typedef CnnW<WQ> W;
   static constexpr int N = W::C1 < 16 ? 16 : W::C1;
+  static constexpr int NOUT = W::C1;
+  static constexpr bool B_MN = false;
+  static constexpr int GROUPS = 1;
   static constexpr int ROWS = 13, COPY = ROWS * 16 * 16, HBYTES = 5 * COPY;
   static constexpr int B_BYTES = 30 * N * 16;
   static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 128;
   static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256 + 1024;
+  static constexpr int TILES_PER_IMAGE = 8;
   const ClientRec* recs;
   CnnDims d;
+
+  __device__ void load_b(const TcTile& t, uint32_t sb, uint32_t bar) const {
+    for (int kc = 0; kc < 30; ++kc) tc::tma_load_2d(sb + kc * N * 16, tmap_of(t, TM_W1P), bar, 8 * kc, 0);
+  }
+  __device__ void load_halo(const TcTile& t, int tile, int grp, uint32_t base, uint32_t bar) const {
+    const int r = tile >> 3, y0 = ((tile >> 1) & 3) * 8, x0 = (tile & 1) * 16;
+    for (int kx = 0; kx < 5; ++kx)  // staged coordinates: output (y, x) reads xs[y + ky][x + kx]
+      tc::tma_load_4d(base + kx * COPY, tmap_of(t, TM_XSH), bar, 0, x0 + kx, y0, r);
+  }
+  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc) const {
+    for (int kx = 0; kx < 5; ++kx)
+      for (int p = 0; p < 3; ++p) {
+        const uint64_t da = tc::sdesc(hb + kx * COPY + 2 * p * 256, 256, 128);
+        const uint64_t db = tc::sdesc(sb + (kx * 6 + 2 * p) * N * 16, N * 16, 128);
+        tc::mma_bf16(dt, da, db, idesc, (kx | p) != 0);
+      }
+  }
+  __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
+                           int lane) const {
+    constexpr int NV = W::C1 < 16 ? W::C1 : 16;
+    constexpr int NCH = (N + 31) / 32;
+    const int g = warp >> 2;
+    const int r = tile >> 3, y0 = ((tile >> 1) & 3) * 8, x0 = (tile & 1) * 16;
+    const int row = (warp & 3) * 32 + lane, y = y0 + (row >> 4), x = x0 + (row & 15), base = lane & 14;
+    float bias[NCH][16];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j)
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int n = g * 16 + 32 * j + q;
+        bias[j][q] = (q < NV && n < W::C1) ? t.c->params[d.b1 + n] : 0.f;
+      }
+    tc::mbar_wait(full_bar, parity);
+    tc::fence_after();
+    bf16* a1 = (bf16*)t.c->buf[B_A1];
+    uint8_t* i1 = (uint8_t*)t.c->buf[B_I1];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c0 = g * 16 + 32 * j;
+      if (c0 >= N) continue;
+      float v[16], val[16], best[16];
+      int arg[16];
+      tc::tmem_ld16(tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) val[e] = e < NV ? fmaxf(v[e] + bias[j][e], 0.f) : 0.f;
+      pool_lanes(val, base, base + 1, base + 16, base + 17, best, arg);
+      if (lane < 16 && (lane & 1) == 0) {
+        const int64_t o = ((int64_t)r * 256 + (y >> 1) * 16 + (x >> 1)) * W::C1 + c0;
+        st_bf16<NV>(a1 + o, best);
+        st_u8<NV>(i1 + o, arg);
+      }
+    }
+  }
 };
 
-template <int WQ>
+// ---------------------------------------------------------------------------
+// Persistent kernel.  prefix[] counts TILES per task (rows * TILES_PER_IMAGE);
+// CTA b owns global tiles [b*T/grid, (b+1)*T/grid).
+// Barriers: b_full / b_empty (client weights), h_full[2] / h_empty[2] (halo
+// stages), acc_full[2] / acc_empty[2] (TMEM accumulators).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int next_task(const int* __restrict__ prefix, int ntask, int ti, int g) {
+  while (ti + 1 < ntask && __ldg(prefix + ti + 1) <= g) ++ti;
+  return ti;
+}
+
+template <class Op>
 __global__ void __launch_bounds__(kConvThreads, 1)
-    k_conv1_halo(const HaloConv1<WQ> op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
-  typedef HaloConv1<WQ> Op;
-  typedef CnnW<WQ> W;
+    k_conv_persistent(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sH = smem + Op::B_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * Op::HBYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ti = find_task(prefix, ntask, blockIdx.x);
-  TcTile t;
-  t.tk = tasks[ti];
-  t.c = op.recs + t.tk.rec;
-  const int tile0 = (blockIdx.x - __ldg(prefix + ti)) * kConv1TPC;
-  const int ntile = min(kConv1TPC, t.tk.rows * 8 - tile0);
-  t.n_mma = Op::N;
+  const int total = __ldg(prefix + ntask);
+  const int g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
+  const int g1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  const int ti0 = find_task(prefix, ntask, g0 < total ? g0 : total - 1);
+
   const uint32_t bar0 = tc::smem_u32(bars);
-  const uint32_t b_full = bar0, h_full = bar0 + 8, h_empty = bar0 + 24, acc_full = bar0 + 40, acc_empty = bar0 + 56;
+  const uint32_t b_full = bar0, b_empty = bar0 + 8, h_full = bar0 + 16, h_empty = bar0 + 32, acc_full = bar0 + 48,
+                 acc_empty = bar0 + 64;
   if (threadIdx.x == 0) {
     tc::mbar_init(b_full, 1);
+    tc::mbar_init(b_empty, 1);
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(h_full + 8 * i, 1);
       tc::mbar_init(h_empty + 8 * i, 1);
@@ -301,63 +280,67 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t sb = tc::smem_u32(smem), sh = tc::smem_u32(sH);
+  TcTile t;
+  t.n_mma = Op::N;
+
   if (warp == 8) {
-    if (lane == 0) {
-      tc::mbar_expect_tx(b_full, Op::B_BYTES);
-      for (int kc = 0; kc < 30; ++kc) tc::tma_load_2d(sb + kc * Op::N * 16, tmap_of(t, TM_W1P), b_full, 8 * kc, 0);
-      for (int i = 0; i < ntile; ++i) {
-        const int buf = i & 1, tile = tile0 + i, r = tile >> 3, y0 = ((tile >> 1) & 3) * 8, x0 = (tile & 1) * 16;
-        if (i >= 2) tc::mbar_wait(h_empty + 8 * buf, ((i >> 1) - 1) & 1);
-        tc::mbar_expect_tx(h_full + 8 * buf, Op::HBYTES);
-        for (int kx = 0; kx < 5; ++kx)  // staged coordinates: output (y, x) reads xs[y + ky][x + kx]
-          tc::tma_load_4d(sh + buf * Op::HBYTES + kx * Op::COPY, tmap_of(t, TM_XSH), h_full + 8 * buf, 0, x0 + kx, y0,
-                          r);
+    if (lane == 0) {  // ---------------- TMA producer
+      int ti = ti0, cur = -1, nb = 0, s = 0;
+      for (int g = g0; g < g1; ++g) {
+        ti = next_task(prefix, ntask, ti, g);
+        t.tk = tasks[ti];
+        t.c = op.recs + t.tk.rec;
+        if (ti != cur) {  // new client: wait until the MMAs released the previous weights, reload
+          if (nb > 0) tc::mbar_wait(b_empty, (nb - 1) & 1);
+          tc::mbar_expect_tx(b_full, Op::B_BYTES);
+          op.load_b(t, sb, b_full);
+          cur = ti;
+          ++nb;
+        }
+        const int tile = g - __ldg(prefix + ti);
+        for (int grp = 0; grp < Op::GROUPS; ++grp, ++s) {
+          const int buf = s & 1;
+          if (s >= 2) tc::mbar_wait(h_empty + 8 * buf, ((s >> 1) - 1) & 1);
+          tc::mbar_expect_tx(h_full + 8 * buf, Op::HBYTES);
+          op.load_halo(t, tile, grp, sh + buf * Op::HBYTES, h_full + 8 * buf);
+        }
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
-      const uint32_t idesc = tc::idesc_bf16(128, Op::N, false, false);
-      tc::mbar_wait(b_full, 0);
-      tc::fence_after();
-      for (int i = 0; i < ntile; ++i) {
-        const int acc = i & 1, buf = i & 1;
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t idesc = tc::idesc_bf16(128, Op::N, false, Op::B_MN);
+      int ti = ti0, cur = -1, nb = 0, s = 0, i = 0;
+      for (int g = g0; g < g1; ++g, ++i) {
+        ti = next_task(prefix, ntask, ti, g);
+        if (ti != cur) {
+          if (nb > 0) tc::commit(b_empty);  // completes when every MMA issued so far (old weights) is done
+          tc::mbar_wait(b_full, nb & 1);
+          tc::fence_after();
+          cur = ti;
+          ++nb;
+        }
+        const int acc = i & 1;
         if (i >= 2) tc::mbar_wait(acc_empty + 8 * acc, ((i >> 1) - 1) & 1);
-        tc::mbar_wait(h_full + 8 * buf, (i >> 1) & 1);
         tc::fence_after();
-        const uint32_t hb = sh + buf * Op::HBYTES, dt = tmem + acc * Op::N;
-        for (int kx = 0; kx < 5; ++kx)
-          for (int p = 0; p < 3; ++p) {
-            const uint64_t da = tc::sdesc(hb + kx * Op::COPY + 2 * p * 256, 256, 128);
-            const uint64_t db = tc::sdesc(sb + (kx * 6 + 2 * p) * Op::N * 16, Op::N * 16, 128);
-            tc::mma_bf16(dt, da, db, idesc, (kx | p) != 0);
-          }
-        tc::commit(h_empty + 8 * buf);
+        for (int grp = 0; grp < Op::GROUPS; ++grp, ++s) {
+          const int buf = s & 1;
+          tc::mbar_wait(h_full + 8 * buf, (s >> 1) & 1);
+          tc::fence_after();
+          op.mma_stage(sh + buf * Op::HBYTES, sb, tmem + acc * Op::N, grp, idesc);
+          tc::commit(h_empty + 8 * buf);
+        }
         tc::commit(acc_full + 8 * acc);
       }
     }
     __syncwarp();
-  } else {
-    constexpr int NV = W::C1 < 16 ? W::C1 : 16;
-    bf16* a1 = (bf16*)t.c->buf[B_A1];
-    uint8_t* i1 = (uint8_t*)t.c->buf[B_I1];
-    for (int i = 0; i < ntile; ++i) {
-      const int acc = i & 1, tile = tile0 + i, r = tile >> 3, y0 = ((tile >> 1) & 3) * 8, x0 = (tile & 1) * 16;
-      tc::mbar_wait(acc_full + 8 * acc, (i >> 1) & 1);
-      tc::fence_after();
-      const int row = (warp & 3) * 32 + lane, y = y0 + (row >> 4), x = x0 + (row & 15), base = lane & 14;
-      for (int c0 = (warp >> 2) * 16; c0 < Op::N; c0 += 32) {
-        float v[16], val[16], best[16];
-        int arg[16];
-        tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(acc * Op::N + c0), v);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) val[j] = j < NV ? fmaxf(v[j] + t.c->params[op.d.b1 + c0 + j], 0.f) : 0.f;
-        pool_lanes(val, base, base + 1, base + 16, base + 17, best, arg);
-        if (lane < 16 && (lane & 1) == 0) {
-          const int64_t o = ((int64_t)r * 256 + (y >> 1) * 16 + (x >> 1)) * W::C1 + c0;
-          st_bf16<NV>(a1 + o, best);
-          st_u8<NV>(i1 + o, arg);
-        }
-      }
+  } else {  // ---------------- epilogue warps 0-7
+    int ti = ti0, i = 0;
+    for (int g = g0; g < g1; ++g, ++i) {
+      ti = next_task(prefix, ntask, ti, g);
+      t.tk = tasks[ti];
+      t.c = op.recs + t.tk.rec;
+      const int acc = i & 1;
+      op.epilogue(t, g - __ldg(prefix + ti), tmem + acc * Op::N, acc_full + 8 * acc, (i >> 1) & 1, warp, lane);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(acc_empty + 8 * acc);
