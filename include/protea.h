@@ -104,9 +104,12 @@ typedef struct {
   uint64_t peak_bytes;  /* exact arena high-water mark of the client's slot (Table 1 VRAM) */
   uint64_t steps;       /* S_k = E * ceil(n_k / B_k) */
   uint64_t flops;       /* E * n_k * f(model, width) */
-  uint64_t step_ns;     /* device time of one local step (CUDA events, probe; Table 1 CUDA_time / S_k) */
-  uint64_t train_ns;    /* step_ns * steps (estimate) or measured in-run attribution */
-  uint64_t sm_ns;       /* in-run SM time attributed to the client (0 if not measured) */
+  uint64_t step_ns;     /* device time of one local step: probe (CUDA events) in protea_profile_clients;
+                           train_ns / steps in the in-run profiles of protea_run_round */
+  uint64_t train_ns;    /* probe: step_ns * steps; in-run: sm_ns / #SMs (the client's SM-time share as
+                           whole-GPU time) — Table 1 CUDA_time */
+  uint64_t sm_ns;       /* in-run: sum of the durations of the CTAs that worked for the client (globaltimer;
+                           persistent kernels split a CTA's time by tile count); 0 in probe profiles */
   uint32_t uses_gpu;    /* 1 */
   uint32_t reserved;
 } protea_profile;

@@ -115,6 +115,7 @@ struct protea_ctx {
   // TMA tensor maps per (client, slot offset, batch, group), reused across rounds
   std::map<std::tuple<uint64_t, int, int, int64_t, int>, std::array<CUtensorMap, TM_COUNT>> tmap_cache;  // (offset, B, E, n, group): everything the slot layout depends on
   DevArray<CUtensorMap> tmaps;
+  DevArray<uint64_t> smns;  // K9 per-client SM-time counters of the current round
 };
 
 namespace {
@@ -930,6 +931,10 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     r.P = gr.m.P;
     r.c1 = gr.m.c1;
   }
+  // ---- K9 per-client SM-time counters
+  CK(ctx->smns.reserve(std::max<size_t>(rc.size(), 1)));
+  CK(cudaMemsetAsync(ctx->smns.p, 0, std::max<size_t>(rc.size(), 1) * 8, ctx->stream));
+  for (size_t i = 0; i < rc.size(); ++i) recs[i].sm_ns = ctx->smns.p + i;
   // ---- TMA tensor maps (bf16 CNN clients)
   if (tc_mode) {
     std::vector<CUtensorMap> maps;
@@ -1246,6 +1251,10 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
       stats->flops += (uint64_t)c.E * c.n * flops_per_sample(ctx->groups[c.group].m);
     }
   }
+  std::vector<uint64_t> smns(all.size(), 0);
+  if (!all.empty()) CK(cudaMemcpy(smns.data(), ctx->smns.p, all.size() * 8, cudaMemcpyDeviceToHost));
+  std::map<int64_t, uint64_t> sm_of;
+  for (size_t i = 0; i < all.size(); ++i) sm_of[all[i].id] = smns[i];
   if (measured) {
     size_t k = 0;
     for (size_t i = 0; i < n; ++i) {
@@ -1258,6 +1267,12 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
       p.steps = (uint64_t)c.epochs * ceil_div((uint64_t)nn, (uint64_t)c.batch);
       p.flops = (uint64_t)c.epochs * nn * flops_per_sample(ctx->groups[c.model_id].m);
       p.uses_gpu = 1;
+      auto it = sm_of.find(c.client_id);  // clients of other ranks keep 0
+      if (it != sm_of.end()) {
+        p.sm_ns = it->second;
+        p.train_ns = it->second / (uint64_t)g_num_sms;  // SM-time share expressed as whole-GPU time
+        p.step_ns = p.steps ? p.train_ns / p.steps : 0;
+      }
     }
   }
   return PROTEA_OK;

@@ -101,26 +101,36 @@ struct HaloConv2 {
       }
   }
   // Epilogue of one tile: warps w, w+4 share TMEM lanes; column chunks c0 = 16 g + 32 j.
+  struct EpiState {  // per-client values cached across the tiles of a client (the bias)
+    const ClientRec* c = nullptr;
+    float bias[(N + 31) / 32][16];
+  };
   __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
-                           int lane) const {
+                           int lane, EpiState& st) const {
     constexpr int NCH = (N + 31) / 32;
     constexpr int NV = NOUT < 16 ? NOUT : 16;
     const int g = warp >> 2, row = (warp & 3) * 32 + lane;
     const int m = tile * 128 + row, r = m >> 8, y = (m >> 4) & 15, x = m & 15;
     float a1v[NCH][NV];
     int argv[NCH][NV];
-    float bias[NCH][16];
+    if (!DGRAD && st.c != t.c) {
+      st.c = t.c;
 #pragma unroll
-    for (int j = 0; j < NCH; ++j) {  // operands independent of the MMA: fetch before waiting
-      const int c0 = g * 16 + 32 * j;
-      if (c0 >= N) continue;
-      if (DGRAD) {
+      for (int j = 0; j < NCH; ++j)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int n = g * 16 + 32 * j + q;
+          st.bias[j][q] = (q < NV && n < NOUT) ? t.c->params[d.b2 + n] : 0.f;
+        }
+    }
+    if (DGRAD) {
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {  // operands independent of the MMA: fetch before waiting
+        const int c0 = g * 16 + 32 * j;
+        if (c0 >= N) continue;
         const int64_t o = (int64_t)m * W::C1 + c0;
         ld_bf16<NV>((const bf16*)t.c->buf[B_A1] + o, a1v[j]);
         ld_u8<NV>((const uint8_t*)t.c->buf[B_I1] + o, argv[j]);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 16; ++q) bias[j][q] = q < NV ? t.c->params[d.b2 + c0 + q] : 0.f;
       }
     }
     tc::mbar_wait(full_bar, parity);
@@ -146,7 +156,7 @@ struct HaloConv2 {
         float val[16], best[16];
         int arg[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) val[e] = e < NV ? fmaxf(v[e] + bias[j][e], 0.f) : 0.f;
+        for (int e = 0; e < 16; ++e) val[e] = e < NV ? fmaxf(v[e] + st.bias[j][e], 0.f) : 0.f;
         pool_lanes(val, base, base + 1, base + 16, base + 17, best, arg);
         if (lane < 16 && (lane & 1) == 0) {
           const int64_t o = ((int64_t)r * 64 + (y >> 1) * 8 + (x >> 1)) * W::C2 + c0;
@@ -197,21 +207,27 @@ struct HaloConv1 {
         tc::mma_bf16(dt, da, db, idesc, (kx | p) != 0);
       }
   }
+  struct EpiState {
+    const ClientRec* c = nullptr;
+    float bias[(N + 31) / 32][16];
+  };
   __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
-                           int lane) const {
+                           int lane, EpiState& st) const {
     constexpr int NV = W::C1 < 16 ? W::C1 : 16;
     constexpr int NCH = (N + 31) / 32;
     const int g = warp >> 2;
     const int r = tile >> 3, y0 = ((tile >> 1) & 3) * 8, x0 = (tile & 1) * 16;
     const int row = (warp & 3) * 32 + lane, y = y0 + (row >> 4), x = x0 + (row & 15), base = lane & 14;
-    float bias[NCH][16];
+    if (st.c != t.c) {
+      st.c = t.c;
 #pragma unroll
-    for (int j = 0; j < NCH; ++j)
+      for (int j = 0; j < NCH; ++j)
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int n = g * 16 + 32 * j + q;
-        bias[j][q] = (q < NV && n < W::C1) ? t.c->params[d.b1 + n] : 0.f;
-      }
+        for (int q = 0; q < 16; ++q) {
+          const int n = g * 16 + 32 * j + q;
+          st.bias[j][q] = (q < NV && n < W::C1) ? t.c->params[d.b1 + n] : 0.f;
+        }
+    }
     tc::mbar_wait(full_bar, parity);
     tc::fence_after();
     bf16* a1 = (bf16*)t.c->buf[B_A1];
@@ -224,7 +240,7 @@ struct HaloConv1 {
       int arg[16];
       tc::tmem_ld16(tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) val[e] = e < NV ? fmaxf(v[e] + bias[j][e], 0.f) : 0.f;
+      for (int e = 0; e < 16; ++e) val[e] = e < NV ? fmaxf(v[e] + st.bias[j][e], 0.f) : 0.f;
       pool_lanes(val, base, base + 1, base + 16, base + 17, best, arg);
       if (lane < 16 && (lane & 1) == 0) {
         const int64_t o = ((int64_t)r * 256 + (y >> 1) * 16 + (x >> 1)) * W::C1 + c0;
@@ -259,6 +275,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
   const int g1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
   const int ti0 = find_task(prefix, ntask, g0 < total ? g0 : total - 1);
+  const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
 
   const uint32_t bar0 = tc::smem_u32(bars);
   const uint32_t b_full = bar0, b_empty = bar0 + 8, h_full = bar0 + 16, h_empty = bar0 + 32, acc_full = bar0 + 48,
@@ -334,13 +351,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
     __syncwarp();
   } else {  // ---------------- epilogue warps 0-7
+    typename Op::EpiState st;
     int ti = ti0, i = 0;
     for (int g = g0; g < g1; ++g, ++i) {
       ti = next_task(prefix, ntask, ti, g);
       t.tk = tasks[ti];
       t.c = op.recs + t.tk.rec;
       const int acc = i & 1;
-      op.epilogue(t, g - __ldg(prefix + ti), tmem + acc * Op::N, acc_full + 8 * acc, (i >> 1) & 1, warp, lane);
+      op.epilogue(t, g - __ldg(prefix + ti), tmem + acc * Op::N, acc_full + 8 * acc, (i >> 1) & 1, warp, lane, st);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(acc_empty + 8 * acc);
@@ -351,6 +369,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   if (warp == 9) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, Op::TMEM_COLS);
+  }
+  if (threadIdx.x == 0 && g1 > g0) {  // K9: split this CTA's duration over its clients by tile count
+    const uint64_t dt = globaltimer() - t_start;
+    int ti = ti0, lo = g0;
+    while (lo < g1) {
+      const int hi = min(g1, __ldg(prefix + ti + 1));
+      const ClientRec* c = op.recs + tasks[ti].rec;
+      if (c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(dt * (hi - lo) / (g1 - g0)));
+      lo = hi;
+      ++ti;
+    }
   }
 }
 

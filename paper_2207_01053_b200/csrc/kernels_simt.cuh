@@ -42,6 +42,7 @@ __global__ void __launch_bounds__((BM / 4) * (BN / 4))
   t.tk = tasks[ti];
   t.c = op.recs + t.tk.rec;
   op.setup(t, blockIdx.x - __ldg(prefix + ti));
+  const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   float acc[4][4];
 #pragma unroll
@@ -87,6 +88,8 @@ __global__ void __launch_bounds__((BM / 4) * (BN / 4))
     __syncthreads();
   }
   op.epilogue(t, t.m0 + ty * 4, t.n0 + tx * 4, acc);
+  if (threadIdx.x == 0 && t.c->sm_ns)  // K9: per-client SM-time attribution
+    atomicAdd((unsigned long long*)t.c->sm_ns, (unsigned long long)(globaltimer() - t_start));
 }
 
 // tile decode helpers (host mirrors these in engine.cu: tiles_*())

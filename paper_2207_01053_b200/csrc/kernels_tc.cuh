@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   t.tk = tasks[ti];
   t.c = op.recs + t.tk.rec;
   op.setup(t, blockIdx.x - __ldg(prefix + ti));
+  const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
 
   const uint32_t bar0 = tc::smem_u32(bars);
   const uint32_t done = bar0 + 16 * STAGES;
@@ -216,6 +217,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc::fence_after();
     tc::tmem_dealloc(tmem, TMEM_COLS);
   }
+  if (threadIdx.x == 0 && t.c->sm_ns)  // K9: per-client SM-time attribution (CTA duration)
+    atomicAdd((unsigned long long*)t.c->sm_ns, (unsigned long long)(globaltimer() - t_start));
 }
 
 __device__ __forceinline__ int round16(int x) { return (x + 15) & ~15; }

@@ -212,3 +212,35 @@ def test_config5_resnet8_bf16(torch):
     got, _ = gpu_run(wl, precision=1)
     ref = oracle_run(wl)
     assert rel_l2(got[4], ref[4]) <= BF16_TOL
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_inrun_profiles_sm_time(torch, precision):
+    """A3 in-run profiles: exact HWM / S_k / FLOPs, and the per-client SM-time
+    attribution (K9): positive for every client, bounded by resident-CTA slots x
+    SMs x round time (parity unpinned: a measurement)."""
+    import paper_2207_01053_b200 as pb
+    wl = synth.build_workload(3, k=10, samples=15)
+    _, ex = gpu_run(wl, precision=precision, return_sim=True)
+    sim = ex["sim"]
+    clients = sim.clients([(c.id, 0, c.batch, c.epochs) for c in wl.clients])
+    g = torch.tensor(synth.init_weights(synth.MODEL_CNN), device="cuda")
+    _, (st, meas) = sim.run_round(clients, ex["plan"], g, lr=0.05, seed=wl.seed, measured=True)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    eb = 4 if precision == 0 else 2
+    cl = {c.id: c for c in wl.clients}
+    for p in meas:
+        c = cl[int(p["client_id"])]
+        assert int(p["peak_bytes"]) == opf.hwm_bytes(c.model, 4, 10, c.batch, c.n, c.epochs, eb)
+        assert int(p["steps"]) == opf.local_steps(c.n, c.batch, c.epochs)
+        assert int(p["sm_ns"]) > 0 and int(p["train_ns"]) * nsm <= int(p["sm_ns"]) + nsm
+    assert sum(int(p["sm_ns"]) for p in meas) <= 32 * nsm * st["round_ns"]
+    sim.close()
+
+
+def test_config3_dirichlet_fp32(torch):
+    # config 3 shape: Dirichlet(0.5) shard sizes over a 1000-client pool (many tiny, ragged shards)
+    wl = synth.build_workload(3, k=8, samples=8)
+    got, _ = gpu_run(wl)
+    ref = oracle_run(wl)
+    assert rel_l2(got[4], ref[4]) <= FP32_TOL
