@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc::fence_after();
     tc::tmem_dealloc(tmem, TMEM_COLS);
   }
-  if (threadIdx.x == 0 && t.c->sm_ns)  // K9: per-client SM-time attribution (CTA duration)
+  if (threadIdx.x == 0 && op.recs && t.c->sm_ns)  // K9: per-client SM-time attribution (CTA duration)
     atomicAdd((unsigned long long*)t.c->sm_ns, (unsigned long long)(globaltimer() - t_start));
 }
 
