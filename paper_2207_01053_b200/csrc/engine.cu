@@ -272,7 +272,7 @@ constexpr int MW_BM = 64, MW_BN = 64;
 
 enum Op : int {
   OP_C1F = 0, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R,
-  OP_MF, OP_MHEAD, OP_MW, OP_ADMIT_, OP_FEDAVG_, OP_STAGE,
+  OP_MF, OP_MHEAD, OP_MW, OP_ADMIT_, OP_FEDAVG_, OP_STAGE, OP_HEADA = 31 /* CNN head part a (stats: OP_HEAD) */,
   // ResNet-8 launch instances (each needs its own prefix table); stats use PROTEA_OPC_R_* classes
   RI_F0 = 32, RI_HEAD = RI_F0 + 7, RI_D1 = RI_HEAD + 1, RI_W0 = RI_D1 + 6, RI_R0 = RI_W0 + 7, OP_COUNT = RI_R0 + 7
 };
@@ -322,6 +322,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
     case OP_C2F: return cdiv(rows * 256, C2F_BM) * cdiv(m.c2, C2F_BN);
     case OP_F1F: return cdiv(rows, F1F_BM) * cdiv(m.f, F1F_BN);
     case OP_HEAD: return cdiv(m.f, kHeadSlice);
+    case OP_HEADA: return cdiv(rows, kHeadRows);
     case OP_F1D: return cdiv(rows, F1D_BM) * cdiv(64 * m.c2, F1D_BN);
     case OP_F1W: return cdiv(m.f, F1W_BM) * cdiv(64 * m.c2, F1W_BN);
     case OP_C2D: return cdiv(rows * 256, C2D_BM) * cdiv(m.c1, C2D_BN);
@@ -338,9 +339,9 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
 
 std::vector<int> ops_of(const ModelDims& m, bool tc) {
   if (m.arch == PROTEA_MODEL_CNN && tc)
-    return {OP_STAGE, OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
+    return {OP_STAGE, OP_C1F, OP_C2F, OP_F1F, OP_HEADA, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_CNN)
-    return {OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
+    return {OP_C1F, OP_C2F, OP_F1F, OP_HEADA, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_MLP) return {OP_MF, OP_MHEAD, OP_MW};
   std::vector<int> v;
   for (int i = 0; i < 7; ++i) v.push_back(RI_F0 + i);
@@ -356,6 +357,7 @@ std::vector<int> ops_of(const ModelDims& m, bool tc) {
 // written once; weights fp32, activations e bytes).  DESIGN.md "Roofline".
 void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, uint64_t* by);
 int op_class(int op) {
+  if (op == OP_HEADA) return OP_HEAD;
   if (op < RI_F0) return op;
   if (op < RI_HEAD) return PROTEA_OPC_R_FWD;
   if (op == RI_HEAD) return PROTEA_OPC_R_HEAD;
@@ -525,7 +527,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
   HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
   ev = op_begin(ctx, OP_HEAD);
-  k_head_a<T><<<L.ntask, kHeadThreads, 0, ctx->cur>>>(ha, tasks);
+  k_head_a<T><<<L.grid[OP_HEADA], kHeadThreads, 0, ctx->cur>>>(ha, tasks, dtab + L.prefix_off[OP_HEADA], L.ntask);
   k_head_b<T><<<L.grid[OP_HEAD], kHeadSlice, 0, ctx->cur>>>(ha, tasks, dtab + L.prefix_off[OP_HEAD], L.ntask);
   ctx->launches++;
   op_end(ctx, ev);
@@ -547,10 +549,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
     launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2WgradSW>(drecs, d, lr), L, OP_C2W, dtab);
   else
     launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2Wgrad<WQ>>(drecs, d, lr), L, OP_C2W, dtab);
-  ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr, 1};
-  ev = op_begin(ctx, OP_C2R);
-  k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->cur>>>(r2, tasks, dtab + L.prefix_off[OP_C2R], L.ntask);
-  op_end(ctx, ev);
+
   launch_gemm_tc<TC_C1W_BN, TC_STAGES>(ctx, TcConv1Wgrad<WQ>{drecs, d}, L, OP_C1W, dtab);
   ev = op_begin(ctx, OP_C1R);
   k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
@@ -667,7 +666,7 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Fc1Fwd<T, F1F_BM, F1F_BN>, F1F_BM, F1F_BN>(ctx, {drecs, d}, L, OP_F1F, dtab);
     HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
     int ev = op_begin(ctx, OP_HEAD);
-    k_head_a<T><<<L.ntask, kHeadThreads, 0, ctx->cur>>>(ha, tasks);
+    k_head_a<T><<<L.grid[OP_HEADA], kHeadThreads, 0, ctx->cur>>>(ha, tasks, dtab + L.prefix_off[OP_HEADA], L.ntask);
     k_head_b<T><<<L.grid[OP_HEAD], kHeadSlice, 0, ctx->cur>>>(ha, tasks, dtab + L.prefix_off[OP_HEAD], L.ntask);
     ctx->launches++;
     op_end(ctx, ev);

@@ -651,30 +651,35 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a, const Task* _
 //           column f, ReLU mask), fc1 bias SGD, W2[:, f] SGD; slice 0 also b2.
 // Every W2 column is read and written by exactly one CTA -> race free.
 // --------------------------------------------------------------------------
+constexpr int kHeadRows = 8;  // rows of the batch per k_head_a CTA
 template <typename T>
-__global__ void __launch_bounds__(kHeadThreads) k_head_a(HeadArgs a, const Task* __restrict__ tasks) {
-  __shared__ float dlog[64 * 64];
-  __shared__ float lossr[64];
-  const Task tk = tasks[blockIdx.x];
+__global__ void __launch_bounds__(kHeadThreads)
+    k_head_a(HeadArgs a, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
+  __shared__ float dlog[kHeadRows * 64];
+  __shared__ float lossr[kHeadRows];
+  const int ti = find_task(prefix, ntask, blockIdx.x);
+  const Task tk = tasks[ti];
   const ClientRec* c = a.recs + tk.rec;
-  const int rows = tk.rows, F = a.F, C = a.classes;
+  const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
+  const int r0 = (blockIdx.x - __ldg(prefix + ti)) * kHeadRows;
+  const int nr = min(kHeadRows, tk.rows - r0), rows = tk.rows, F = a.F, C = a.classes;
   const T* h = (const T*)c->buf[a.hbuf];
   const float* W = c->params + a.w;
   const float* bias = c->params + a.b;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int idx = warp; idx < rows * C; idx += kHeadThreads / 32) {
+  for (int idx = warp; idx < nr * C; idx += kHeadThreads / 32) {
     const int r = idx / C, cc = idx - r * C;
     float s = 0.f;
-    for (int f = lane; f < F; f += 32) s = fmaf(ldv(h + (int64_t)r * F + f), W[(int64_t)cc * F + f], s);
+    for (int f = lane; f < F; f += 32) s = fmaf(ldv(h + (int64_t)(r0 + r) * F + f), W[(int64_t)cc * F + f], s);
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) dlog[r * C + cc] = s + bias[cc];
   }
   __syncthreads();
   float* out = (float*)c->buf[B_WSP];
-  if (threadIdx.x < rows) {
+  if (threadIdx.x < nr) {
     const int r = threadIdx.x;
-    const int label = c->y[c->perm[tk.base + r]];
+    const int label = c->y[c->perm[tk.base + r0 + r]];
     float mx = -INFINITY;
     for (int cc = 0; cc < C; ++cc) mx = fmaxf(mx, dlog[r * C + cc]);
     float s = 0.f;
@@ -683,14 +688,15 @@ __global__ void __launch_bounds__(kHeadThreads) k_head_a(HeadArgs a, const Task*
     const float inv = 1.f / (s * (float)rows);
     for (int cc = 0; cc < C; ++cc) {
       const float p = expf(dlog[r * C + cc] - mx);
-      out[r * C + cc] = p * inv - (cc == label ? 1.f / (float)rows : 0.f);
+      out[(r0 + r) * C + cc] = p * inv - (cc == label ? 1.f / (float)rows : 0.f);
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     float s = 0.f;
-    for (int r = 0; r < rows; ++r) s += lossr[r];
-    c->stats[0] += s / (float)rows;
+    for (int r = 0; r < nr; ++r) s += lossr[r];
+    atomicAdd(&c->stats[0], s / (float)rows);  // loss statistic only (summation order not fixed)
+    if (c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(globaltimer() - t_start));
   }
 }
 

@@ -78,6 +78,15 @@ struct has_tma {
   static constexpr bool value = f<Op>(nullptr);
 };
 
+template <class Op>
+struct has_finish {
+  template <class U>
+  static constexpr bool f(decltype(U::FINISH)*) { return U::FINISH; }
+  template <class U>
+  static constexpr bool f(...) { return false; }
+  static constexpr bool value = f<Op>(nullptr);
+};
+
 template <int BN, int STAGES, class Op>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_gemm_tc(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
@@ -217,6 +226,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc::fence_after();
     tc::tmem_dealloc(tmem, TMEM_COLS);
   }
+  if constexpr (has_finish<Op>::value) op.finish(t);  // e.g. last split-K CTA reduces and updates
   if (threadIdx.x == 0 && op.recs && t.c->sm_ns)  // K9: per-client SM-time attribution (CTA duration)
     atomicAdd((unsigned long long*)t.c->sm_ns, (unsigned long long)(globaltimer() - t_start));
 }
@@ -751,6 +761,39 @@ struct TmaConv2Wgrad : TcConv2Wgrad<WQ> {  // split-K over 2048-pixel chunks -> 
 #pragma unroll
     for (int j = 0; j < 16; ++j)
       if (c0 + j < W::C2) part[(int64_t)(c0 + j) * N] = v[j];
+  }
+  // The last split of each (client, M tile) to finish sums the partials in split order (deterministic) and
+  // applies the SGD update to the fp32 master and the bf16 shadow (fused reduce).  Counters: stats[8 + mtile].
+  static constexpr bool FINISH = true;
+  __device__ void finish(const TcTile& t) const {
+    __shared__ int last;
+    int* cnt = reinterpret_cast<int*>(t.c->stats) + 8 + t.m0 / 128;
+    const int splits = (t.tk.rows * 256 + kWgradChunkPx - 1) / kWgradChunkPx;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(cnt, 1) == splits - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int N = 25 * W::C1 + 1, Kw = 25 * W::C1;
+    const float* part = (const float*)t.c->buf[B_WSP];
+    float* P = t.c->params;
+    bf16* S = (bf16*)t.c->buf[B_WSH];
+    for (int e = threadIdx.x; e < 128 * W::C2; e += blockDim.x) {
+      const int m = t.m0 + (e & 127), co = e >> 7;
+      if (m >= N) continue;
+      float g = 0.f;
+      for (int sp = 0; sp < splits; ++sp) g += __ldcg(part + ((int64_t)sp * W::C2 + co) * N + m);
+      if (m < Kw) {
+        const int64_t idx = d.w2 + (int64_t)co * Kw + m;
+        const float nw = P[idx] - this->lr * g;
+        P[idx] = nw;
+        S[idx] = __float2bfloat16_rn(nw);
+      } else {
+        P[d.b2 + co] -= this->lr * g;
+      }
+    }
+    if (threadIdx.x == 0) *cnt = 0;
   }
 };
 
