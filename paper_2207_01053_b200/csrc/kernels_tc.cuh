@@ -785,12 +785,12 @@ struct TmaConv2Wgrad : TcConv2Wgrad<WQ> {  // split-K over 2048-pixel chunks -> 
       float g = 0.f;
       for (int sp = 0; sp < splits; ++sp) g += __ldcg(part + ((int64_t)sp * W::C2 + co) * N + m);
       if (m < Kw) {
-        const int64_t idx = d.w2 + (int64_t)co * Kw + m;
+        const int64_t idx = this->d.w2 + (int64_t)co * Kw + m;
         const float nw = P[idx] - this->lr * g;
         P[idx] = nw;
         S[idx] = __float2bfloat16_rn(nw);
       } else {
-        P[d.b2 + co] -= this->lr * g;
+        P[this->d.b2 + co] -= this->lr * g;
       }
     }
     if (threadIdx.x == 0) *cnt = 0;
