@@ -102,8 +102,9 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
                 ("a2", b * 64 * c2 * e), ("i2", b * 64 * c2),
                 ("h", b * f * e), ("dh", b * f * e),
                 ("dz2", b * 256 * c2 * e), ("dz1", b * 1024 * c1 * e)]
-        if e == 2:  # bf16 mode: input staged for the tensor cores + padded conv1 weight shadow
-            out += [("xs", b * 36 * 36 * 8 * 2), ("w1p", c1 * 30 * 8 * 2)]
+        if e == 2:  # bf16 mode: input staged for the tensor cores + conv1 weight shadow
+            # (6x6 window taps x 4 pool positions x C1 x 8 padded channels, bf16)
+            out += [("xs", b * 36 * 36 * 8 * 2), ("w1q", 36 * 4 * c1 * 8 * 2)]
     elif model == RESNET8:
         out += [("a0", b * 1024 * 16 * e),
                 ("r1", b * 1024 * 16 * e), ("o1", b * 1024 * 16 * e),

@@ -69,6 +69,19 @@ int cnn_conv2_splits(int rows);
 
 SlotLayout slot_layout(const ModelDims& m, int batch, int64_t n, int epochs, int elem_bytes);
 
+// bf16-mode conv1 "pool-quad" weight shadow w1q (buffer B_W1P), DESIGN.md §6:
+// [dy 6][dx>>1 3][dx&1 2][n = q*C1 + co][ci 8] bf16, q = 2qy+qx a position of
+// the 2x2 pool window and (dy, dx) = (qy+ky, qx+kx) the tap's offset inside the
+// 6x6 input window of one pooled output; entry = W1[co][ky][kx][ci] (zero when
+// ky or kx is outside 0..4 or ci >= 3).
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int64_t w1q_index(int C1, int dy, int dx, int q, int co, int ci) {
+  return ((int64_t)((dy * 3 + (dx >> 1)) * 2 + (dx & 1)) * (4 * C1) + q * C1 + co) * 8 + ci;
+}
+inline uint64_t w1q_bytes(int C1) { return 36ull * 4 * C1 * 8 * 2; }
+
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 }  // namespace protea

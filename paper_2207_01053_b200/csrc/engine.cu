@@ -192,13 +192,16 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
     const uint32_t b2[4] = {64, 16, 4, 1};
     ok &= tmap_encode(&out[TM_DZ2WS], r.buf[B_DZ2], 4, d2, s2, b2, CU_TENSOR_MAP_SWIZZLE_128B);
   }
-  if (r.buf[B_XS]) {
-    const uint64_t dx[4] = {8, 36, 36, Bk}, sx[3] = {16, 36 * 16, 1296 * 16};
-    const uint32_t bx[4] = {8, 16, 13, 1};
-    ok &= tmap_encode(&out[TM_XSH], r.buf[B_XS], 4, dx, sx, bx);
-    const uint64_t dw[2] = {240, C1}, sw[1] = {480};
-    const uint32_t bw[2] = {8, (uint32_t)(C1 < 16 ? 16 : C1)};
-    ok &= tmap_encode(&out[TM_W1P], r.buf[B_W1P], 2, dw, sw, bw);
+  if (r.buf[B_XS]) {  // staged input xs[B][36 Y][2 par][18 X'][8] (k_stage_x)
+    const uint64_t dx[5] = {8, 18, 2, 36, Bk}, sx[4] = {16, 288, 576, 36 * 576};
+    const uint32_t bh[5] = {8, 10, 2, 36, 1}, bw[5] = {8, 8, 1, 36, 1};
+    ok &= tmap_encode(&out[TM_XSH], r.buf[B_XS], 5, dx, sx, bh);
+    ok &= tmap_encode(&out[TM_XSW], r.buf[B_XS], 5, dx, sx, bw);
+  }
+  if (r.buf[B_XS] && C1 == 32) {  // pool-quad conv1 gradient g1[B][16][16][4 q][C1] (k_conv1_wgrad_q)
+    const uint64_t d[4] = {4 * C1, 16, 16, Bk}, st[3] = {8 * C1, 128 * C1, 2048 * C1};
+    const uint32_t bx[4] = {64, 8, 16, 1};
+    ok &= tmap_encode(&out[TM_G], r.buf[B_DZC1], 4, d, st, bx, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   {
     const uint64_t d[2] = {F, Bk}, st[1] = {2 * F};
@@ -306,8 +309,9 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
   }
   if (tc) switch (op) {
       case OP_STAGE: return cdiv(rows * 1296, kStageThreads);
-      case OP_C1F: return rows * 8;  // persistent halo kernel: prefix over 128-pixel tiles
-      case OP_C1W: return 2 * cdiv(rows * 1024, kWgradChunkPx);
+      case OP_C1F: return rows * 2;  // persistent pool-quad kernel: 2 tiles of 128 pooled pixels per image
+      case OP_C1W:  // width 1: persistent pool-quad kernel, one item per split; else 2 M tiles per split
+        return (m.width_q == 4 ? 1 : 2) * cdiv(rows * 1024, kWgradChunkPx);
       case OP_C1R: return cdiv(76 * m.c1, kReduceBlock);
       case OP_C2F: return rows * 2;  // halo kernel (width >= 1/2) or TmaConv2Fwd: both 128-pixel tiles
       case OP_F1F: return m.f / 128;
@@ -494,6 +498,19 @@ void launch_conv_persistent(protea_ctx* ctx, const ClientRec* drecs, const CnnDi
   op_end(ctx, ev);
 }
 
+void launch_conv1_wgrad_q(protea_ctx* ctx, const ClientRec* drecs, const Launch& L, const int32_t* dtab) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_conv1_wgrad_q, cudaFuncAttributeMaxDynamicSharedMemorySize, kW1Smem);
+    attr = true;
+  }
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const int grid = std::min(L.grid[OP_C1W], g_num_sms);
+  const int ev = op_begin(ctx, OP_C1W);
+  k_conv1_wgrad_q<<<grid, kConvThreads, kW1Smem, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1W], L.ntask);
+  op_end(ctx, ev);
+}
+
 template <class OpT>
 OpT tma_op(const ClientRec* recs, const CnnDims& d) {
   OpT op;
@@ -519,7 +536,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   k_stage_x<<<L.grid[OP_STAGE], kStageThreads, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_STAGE],
                                                                   L.ntask);
   op_end(ctx, ev);
-  launch_conv_persistent<HaloConv1<WQ>>(ctx, drecs, d, L, OP_C1F, dtab);
+  launch_conv_persistent<QuadConv1<WQ>>(ctx, drecs, d, L, OP_C1F, dtab);
   if constexpr (WQ >= 2)
     launch_conv_persistent<HaloConv2<WQ, false>>(ctx, drecs, d, L, OP_C2F, dtab);
   else
@@ -550,7 +567,10 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   else
     launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2Wgrad<WQ>>(drecs, d, lr), L, OP_C2W, dtab);
 
-  launch_gemm_tc<TC_C1W_BN, TC_STAGES>(ctx, TcConv1Wgrad<WQ>{drecs, d}, L, OP_C1W, dtab);
+  if constexpr (WQ == 4)
+    launch_conv1_wgrad_q(ctx, drecs, L, dtab);
+  else
+    launch_gemm_tc<TC_C1W_BN, TC_STAGES>(ctx, TcConv1Wgrad<WQ>{drecs, d}, L, OP_C1W, dtab);
   ev = op_begin(ctx, OP_C1R);
   k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
                                                                        L.ntask, m.c1, d.w1, d.b1, lr);

@@ -41,7 +41,7 @@ struct HaloGeom {
 
 // Fwd: input a1 (C1 channels), weights K-major [kchunk][C2][8]; epilogue bias + ReLU + 2x2 pool -> a2, i2.
 // Dgrad: input dz2 (C2 channels, flipped taps), weights MN-major [tap][C1/8][C2][8]; epilogue ReLU mask
-// + pool-1 backward scatter -> dz1.
+// + pool-1 backward scatter -> dz1 (width 1: in the pool-quad layout of k_conv1_wgrad_q).
 template <int WQ, bool DGRAD>
 struct HaloConv2 {
   typedef CnnW<WQ> W;
@@ -148,8 +148,12 @@ struct HaloConv2 {
         for (int q = 0; q < 4; ++q) {
 #pragma unroll
           for (int e = 0; e < NV; ++e) out[e] = (argv[j][e] == q && a1v[j][e] > 0.f) ? v[e] : 0.f;
-          const int Y = 2 * y + (q >> 1), X = 2 * x + (q & 1);
-          st_bf16<NV>(dz1 + ((int64_t)r * 1024 + Y * 32 + X) * W::C1 + c0, out);
+          if constexpr (WQ == 4) {  // pool-quad layout g1[r][py][px][q][C1] (k_conv1_wgrad_q)
+            st_bf16<NV>(dz1 + (((int64_t)r * 256 + y * 16 + x) * 4 + q) * W::C1 + c0, out);
+          } else {  // full-resolution dz1[r][Y][X][C1] (TcConv1Wgrad)
+            const int Y = 2 * y + (q >> 1), X = 2 * x + (q & 1);
+            st_bf16<NV>(dz1 + ((int64_t)r * 1024 + Y * 32 + X) * W::C1 + c0, out);
+          }
         }
       } else {  // bias + ReLU + 2x2 max-pool (first max) over lanes (l, l+1, l+16, l+17)
         const int base = lane & 14;
@@ -169,85 +173,98 @@ struct HaloConv2 {
 };
 
 // ---------------------------------------------------------------------------
-// conv1 fwd (3 -> C1, 32x32 input).  Input: the staged bf16 batch xs[r][36][36][8]
-// (2-pixel border and channel padding built in, one 16-byte chunk per pixel).
-// K order = (kx, ky in 0..5, ci 8): one K=16 MMA covers the tap pair (ky, ky+1)
-// of one x-shifted halo copy, so its second 8-element K chunk is simply the next
-// halo row (LBO = 256 B); ky = 5 carries zero weights.  Weights: w1p
-// [C1][kx 5][ky 6][8].  Tile = 8 output rows x 16 columns (8 tiles per image).
+// conv1 fwd (3 -> C1, 32x32 input) + bias + ReLU + 2x2 max-pool, "pool-quad" form.
+// One GEMM row per POOLED output (py, px); its 4 pool positions q = (qy, qx)
+// become 4 groups of output columns: D[(py,px)][q*C1 + co] = sum over the 6x6
+// input window (dy, dx) and ci of xs[2py+dy][2px+dx][ci] * w1q[(dy,dx)][q][co][ci]
+// (w1q: common.h, zero outside each q's 5x5 taps).  With the staged input split
+// by column parity, the 8 pooled columns of a core matrix read 8 CONSECUTIVE
+// 16-byte chunks, so the A operand of the MMA for (dy, dx pair) is a plain
+// descriptor into ONE halo buffer (no im2col, no shifted copies): K = 16 =
+// (even dx, 8 ci) + (odd dx, 8 ci) at LBO = 160 B, M groups = pooled rows at
+// SBO = 640 B.  18 MMAs (M = 128, N = 4 C1, K = 16) per tile; the epilogue pools
+// inside a thread (the 4 q columns of a channel), no cross-lane shuffles.
+// Tile = 16 pooled rows x 8 pooled columns (2 tiles per image); halo
+// [36 rows][2 parities][10 columns][8] = 11.5 KB.
 // ---------------------------------------------------------------------------
 template <int WQ>
-struct HaloConv1 {
+struct QuadConv1 {
   typedef CnnW<WQ> W;
-  static constexpr int N = W::C1 < 16 ? 16 : W::C1;
+  static constexpr int N = 4 * W::C1;
   static constexpr int NOUT = W::C1;
   static constexpr bool B_MN = false;
   static constexpr int GROUPS = 1;
-  static constexpr int ROWS = 13, COPY = ROWS * 16 * 16, HBYTES = 5 * COPY;
-  static constexpr int B_BYTES = 30 * N * 16;
-  static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 128;
+  static constexpr int HBYTES = 36 * 2 * 10 * 16;
+  static constexpr int B_BYTES = 36 * N * 16;  // w1q, [36 K chunks][N][8]
+  static constexpr int TMEM_COLS = 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
   static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256 + 1024;
-  static constexpr int TILES_PER_IMAGE = 8;
+  static constexpr int TILES_PER_IMAGE = 2;
+  static constexpr int NCO = W::C1 >= 32 ? 16 : W::C1;  // channels per epilogue thread
   const ClientRec* recs;
   CnnDims d;
 
   __device__ void load_b(const TcTile& t, uint32_t sb, uint32_t bar) const {
-    for (int kc = 0; kc < 30; ++kc) tc::tma_load_2d(sb + kc * N * 16, tmap_of(t, TM_W1P), bar, 8 * kc, 0);
+    const uint8_t* w1q = (const uint8_t*)t.c->buf[B_W1P];
+    for (int kc = 0; kc < 36; ++kc) tc::bulk_load(sb + kc * N * 16, w1q + kc * N * 16, N * 16, bar);
   }
   __device__ void load_halo(const TcTile& t, int tile, int grp, uint32_t base, uint32_t bar) const {
-    const int r = tile >> 3, y0 = ((tile >> 1) & 3) * 8, x0 = (tile & 1) * 16;
-    for (int kx = 0; kx < 5; ++kx)  // staged coordinates: output (y, x) reads xs[y + ky][x + kx]
-      tc::tma_load_4d(base + kx * COPY, tmap_of(t, TM_XSH), bar, 0, x0 + kx, y0, r);
+    tc::tma_load_5d(base, tmap_of(t, TM_XSH), bar, 0, (tile & 1) * 8, 0, 0, tile >> 1);
   }
   __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc) const {
-    for (int kx = 0; kx < 5; ++kx)
-      for (int p = 0; p < 3; ++p) {
-        const uint64_t da = tc::sdesc(hb + kx * COPY + 2 * p * 256, 256, 128);
-        const uint64_t db = tc::sdesc(sb + (kx * 6 + 2 * p) * N * 16, N * 16, 128);
-        tc::mma_bf16(dt, da, db, idesc, (kx | p) != 0);
+    for (int dy = 0; dy < 6; ++dy)
+      for (int dp = 0; dp < 3; ++dp) {
+        const uint64_t da = tc::sdesc(hb + dy * 320 + dp * 16, 160, 640);
+        const uint64_t db = tc::sdesc(sb + (dy * 3 + dp) * 2 * N * 16, N * 16, 128);
+        tc::mma_bf16(dt, da, db, idesc, (dy | dp) != 0);
       }
   }
   struct EpiState {
     const ClientRec* c = nullptr;
-    float bias[(N + 31) / 32][16];
+    float bias[NCO];
   };
   __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
                            int lane, EpiState& st) const {
-    constexpr int NV = W::C1 < 16 ? W::C1 : 16;
-    constexpr int NCH = (N + 31) / 32;
     const int g = warp >> 2;
-    const int r = tile >> 3, y0 = ((tile >> 1) & 3) * 8, x0 = (tile & 1) * 16;
-    const int row = (warp & 3) * 32 + lane, y = y0 + (row >> 4), x = x0 + (row & 15), base = lane & 14;
-    if (st.c != t.c) {
+    const bool active = g * NCO < W::C1;  // widths < 1: warps 4-7 idle
+    const int r = tile >> 1, row = (warp & 3) * 32 + lane, py = row >> 3, px = (tile & 1) * 8 + (row & 7);
+    if (active && st.c != t.c) {
       st.c = t.c;
 #pragma unroll
-      for (int j = 0; j < NCH; ++j)
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int n = g * 16 + 32 * j + q;
-          st.bias[j][q] = (q < NV && n < W::C1) ? t.c->params[d.b1 + n] : 0.f;
-        }
+      for (int c = 0; c < NCO; ++c) st.bias[c] = t.c->params[d.b1 + g * NCO + c];
     }
     tc::mbar_wait(full_bar, parity);
     tc::fence_after();
-    bf16* a1 = (bf16*)t.c->buf[B_A1];
-    uint8_t* i1 = (uint8_t*)t.c->buf[B_I1];
+    if (!active) return;
+    float v[4 * NCO];
+    const uint32_t ta = tacc + ((uint32_t)((warp & 3) * 32) << 16);
+    if (NCO == W::C1) {  // the 4 q groups are contiguous columns
 #pragma unroll
-    for (int j = 0; j < NCH; ++j) {
-      const int c0 = g * 16 + 32 * j;
-      if (c0 >= N) continue;
-      float v[16], val[16], best[16];
-      int arg[16];
-      tc::tmem_ld16(tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
+      for (int k = 0; k < 4 * NCO / 16; ++k) tc::tmem_ld16(ta + 16 * k, *reinterpret_cast<float(*)[16]>(v + 16 * k));
+    } else {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) val[e] = e < NV ? fmaxf(v[e] + st.bias[j][e], 0.f) : 0.f;
-      pool_lanes(val, base, base + 1, base + 16, base + 17, best, arg);
-      if (lane < 16 && (lane & 1) == 0) {
-        const int64_t o = ((int64_t)r * 256 + (y >> 1) * 16 + (x >> 1)) * W::C1 + c0;
-        st_bf16<NV>(a1 + o, best);
-        st_u8<NV>(i1 + o, arg);
-      }
+      for (int q = 0; q < 4; ++q)
+        tc::tmem_ld16(ta + q * W::C1 + g * NCO, *reinterpret_cast<float(*)[16]>(v + 16 * q));
     }
+    float best[NCO];
+    int arg[NCO];
+#pragma unroll
+    for (int c = 0; c < NCO; ++c) {  // bias + ReLU, then the first maximum in q order (strict >)
+      float b = fmaxf(v[c] + st.bias[c], 0.f);
+      int a = 0;
+#pragma unroll
+      for (int q = 1; q < 4; ++q) {
+        const float x = fmaxf(v[q * NCO + c] + st.bias[c], 0.f);
+        if (x > b) {
+          b = x;
+          a = q;
+        }
+      }
+      best[c] = b;
+      arg[c] = a;
+    }
+    const int64_t o = ((int64_t)r * 256 + py * 16 + px) * W::C1 + g * NCO;
+    st_bf16<NCO>((bf16*)t.c->buf[B_A1] + o, best);
+    st_u8<NCO>((uint8_t*)t.c->buf[B_I1] + o, arg);
   }
 };
 
@@ -376,6 +393,163 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     while (lo < g1) {
       const int hi = min(g1, __ldg(prefix + ti + 1));
       const ClientRec* c = op.recs + tasks[ti].rec;
+      if (c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(dt * (hi - lo) / (g1 - g0)));
+      lo = hi;
+      ++ti;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// conv1 wgrad (width 1, C1 = 32) in pool-quad form.  dz1 is nonzero only at the
+// pool window's argmax, so conv2 dgrad stores it per POOLED pixel p as
+// g1[p][q][co] (q = 2qy+qx the window position).  Then
+//   D[(q,co)][(dy,dx,ci)] = sum_p g1[p][q][co] * xs[2py+dy][2px+dx][ci]     (one GEMM, K = pooled pixels)
+//   dW1[co][ky][kx][ci]   = sum_q D[(q,co)][(ky+qy, kx+qx, ci)]            (fold in the epilogue)
+//   db1[co]               = sum_q D[(q,co)][(2+qy, 2+qx, 3)]               (staged channel 3 = 1 in the image)
+// Work item = (client, split of 2 images = kWgradChunkPx full-resolution pixels);
+// sub-tile = (image, column half) = 128 pooled pixels.  Per K step (16 pooled
+// pixels = 2 pooled rows): 6 MMAs (one per dy), M = 128 (q, co), N = 48 (dx, ci).
+// A = g1 sub-tile by TMA (two 64-row boxes, 128-byte swizzle, MN-major);
+// B = 6 x-shifted copies (one per dx) of the staged rows [36 Y][8 X'][8 ci],
+// MN-major without swizzle (core matrix = 8 ci x 8 pooled columns, LBO = next
+// pooled row = 256 B, SBO = next dx copy).  TMEM: D at column dy*48 + dx*8 + ci.
+// The epilogue folds through shared memory and writes the split's partial
+// [76][C1] (k_reduce_conv1_tc sums the splits in order and applies SGD).
+// Persistent: one CTA per SM walks a contiguous range of work items.
+// ---------------------------------------------------------------------------
+constexpr int kW1GBytes = 2 * 128 * 128;                // g1 sub-tile: 128 (q,co) x 128 pooled px bf16
+constexpr int kW1XCopy = 36 * 8 * 16;                   // one dx copy [36][8][8] bf16
+constexpr int kW1Stage = kW1GBytes + 6 * kW1XCopy;      // 60416 = 59 x 1024
+constexpr int kW1Fold = 4 * 76 * 32 * 4;                // fold buffer S[q][76][32] fp32
+constexpr int kW1Smem = 2 * kW1Stage + kW1Fold + 256 + 1024;
+
+__global__ void __launch_bounds__(kConvThreads, 1)
+    k_conv1_wgrad_q(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks,
+                    const int* __restrict__ prefix, int ntask) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+  float* S = reinterpret_cast<float*>(smem + 2 * kW1Stage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kW1Stage + kW1Fold);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = __ldg(prefix + ntask);
+  const int g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
+  const int g1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  const int ti0 = find_task(prefix, ntask, g0 < total ? g0 : total - 1);
+  const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
+  const uint32_t bar0 = tc::smem_u32(bars);
+  const uint32_t full = bar0, empty = bar0 + 16, acc_full = bar0 + 32, acc_empty = bar0 + 40;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(full + 8 * i, 1);
+      tc::mbar_init(empty + 8 * i, 1);
+    }
+    tc::mbar_init(acc_full, 1);
+    tc::mbar_init(acc_empty, 8);
+    tc::mbar_fence_init();
+  }
+  if (warp == 9) tc::tmem_alloc(tc::smem_u32(tmem_slot), 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sb = tc::smem_u32(smem);
+
+  if (warp == 8) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int ti = ti0, s = 0;
+      for (int g = g0; g < g1; ++g) {
+        ti = next_task(prefix, ntask, ti, g);
+        TcTile t;
+        t.tk = tasks[ti];
+        t.c = recs + t.tk.rec;
+        const int r0 = 2 * (g - __ldg(prefix + ti)), nsub = 2 * min(2, t.tk.rows - r0);
+        for (int sub = 0; sub < nsub; ++sub, ++s) {
+          const int buf = s & 1, r = r0 + (sub >> 1), h = sub & 1;
+          const uint32_t gb = sb + buf * kW1Stage;
+          if (s >= 2) tc::mbar_wait(empty + 8 * buf, ((s >> 1) - 1) & 1);
+          tc::mbar_expect_tx(full + 8 * buf, kW1Stage);
+          tc::tma_load_4d(gb, tmap_of(t, TM_G), full + 8 * buf, 0, 8 * h, 0, r);
+          tc::tma_load_4d(gb + kW1GBytes / 2, tmap_of(t, TM_G), full + 8 * buf, 64, 8 * h, 0, r);
+          for (int dx = 0; dx < 6; ++dx)
+            tc::tma_load_5d(gb + kW1GBytes + dx * kW1XCopy, tmap_of(t, TM_XSW), full + 8 * buf, 0,
+                            8 * h + (dx >> 1), dx & 1, 0, r);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      const uint32_t idesc = tc::idesc_bf16(128, 48, true, true);
+      int ti = ti0, s = 0, i = 0;
+      for (int g = g0; g < g1; ++g, ++i) {
+        ti = next_task(prefix, ntask, ti, g);
+        const int r0 = 2 * (g - __ldg(prefix + ti)), nsub = 2 * min(2, __ldg(&tasks[ti].rows) - r0);
+        if (i >= 1) tc::mbar_wait(acc_empty, (i - 1) & 1);
+        tc::fence_after();
+        for (int sub = 0; sub < nsub; ++sub, ++s) {
+          const int buf = s & 1;
+          const uint32_t gb = sb + buf * kW1Stage;
+          tc::mbar_wait(full + 8 * buf, (s >> 1) & 1);
+          tc::fence_after();
+          for (int ks = 0; ks < 8; ++ks) {
+            const uint64_t da = tc::sdesc_sw128(gb + 2048 * ks, kW1GBytes / 2, 1024);
+            for (int dy = 0; dy < 6; ++dy) {
+              const uint64_t db = tc::sdesc(gb + kW1GBytes + (4 * ks + dy) * 128, 256, kW1XCopy);
+              tc::mma_bf16(tmem + dy * 48, da, db, idesc, (sub | ks) != 0);
+            }
+          }
+          tc::commit(empty + 8 * buf);
+        }
+        tc::commit(acc_full);
+      }
+    }
+    __syncwarp();
+  } else {  // ---------------- epilogue warps 0-7: warp w holds q = w % 4, ky in [0,3) (w < 4) or [3,5)
+    const int q = warp & 3, qy = q >> 1, qx = q & 1, ky0 = warp < 4 ? 0 : 3, ky1 = warp < 4 ? 3 : 5;
+    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16);
+    int ti = ti0, i = 0;
+    for (int g = g0; g < g1; ++g, ++i) {
+      ti = next_task(prefix, ntask, ti, g);
+      const ClientRec* c = recs + tasks[ti].rec;
+      const int split = g - __ldg(prefix + ti);
+      tc::mbar_wait(acc_full, i & 1);
+      tc::fence_after();
+      float* Sq = S + q * 76 * 32;
+      for (int ky = ky0; ky < ky1; ++ky) {
+        float v[48];
+        const uint32_t col = ta + (uint32_t)((ky + qy) * 48);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) tc::tmem_ld16(col + 16 * k, *reinterpret_cast<float(*)[16]>(v + 16 * k));
+#pragma unroll
+        for (int kx = 0; kx < 5; ++kx)
+#pragma unroll
+          for (int ci = 0; ci < 3; ++ci)
+            Sq[((ky * 5 + kx) * 3 + ci) * 32 + lane] = qx ? v[(kx + 1) * 8 + ci] : v[kx * 8 + ci];
+        if (ky == 2) Sq[75 * 32 + lane] = qx ? v[3 * 8 + 3] : v[2 * 8 + 3];
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty);  // TMEM drained: the next item's MMAs may start
+      tc::named_sync(1, 256);
+      float* part = (float*)c->buf[B_WSP] + (int64_t)split * 76 * 32;
+      for (int e = threadIdx.x; e < 76 * 32; e += 256)
+        part[e] = ((S[e] + S[2432 + e]) + S[2 * 2432 + e]) + S[3 * 2432 + e];
+      tc::named_sync(1, 256);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+  if (threadIdx.x == 0 && g1 > g0) {  // K9: split this CTA's duration over its clients by item count
+    const uint64_t dt = globaltimer() - t_start;
+    int ti = ti0, lo = g0;
+    while (lo < g1) {
+      const int hi = min(g1, __ldg(prefix + ti + 1));
+      const ClientRec* c = recs + tasks[ti].rec;
       if (c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(dt * (hi - lo) / (g1 - g0)));
       lo = hi;
       ++ti;

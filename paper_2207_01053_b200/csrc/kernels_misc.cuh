@@ -17,12 +17,17 @@ __global__ void k_admit_params(const ClientRec* __restrict__ recs, const int* __
     c->params[i] = w;
     if (sh) sh[i] = __float2bfloat16_rn(w);
   }
-  __nv_bfloat16* w1p = (__nv_bfloat16*)c->buf[B_W1P];  // conv1 shadow [c1][kx 5][ky 6][8], W1 at offset 0
-  if (w1p)
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < c->c1 * 240; e += gridDim.x * blockDim.x) {
-      const int co = e / 240, rem = e % 240, kx = rem / 48, ky = (rem % 48) >> 3, ci = e & 7;
-      w1p[e] = __float2bfloat16_rn(ky < 5 && ci < 3 ? c->wg[co * 75 + (ky * 5 + kx) * 3 + ci] : 0.f);
+  __nv_bfloat16* w1q = (__nv_bfloat16*)c->buf[B_W1P];  // conv1 pool-quad shadow (common.h w1q_index), W1 at offset 0
+  if (w1q) {
+    const int C1 = c->c1, N = 4 * C1;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 288 * N; e += gridDim.x * blockDim.x) {
+      const int ci = e & 7, n = (e >> 3) % N, mh = (e >> 3) / N;  // mh = (dy*3 + dx/2)*2 + dx%2
+      const int dy = (mh >> 1) / 3, dx = 2 * ((mh >> 1) % 3) + (mh & 1), q = n / C1, co = n - q * C1;
+      const int ky = dy - (q >> 1), kx = dx - (q & 1);
+      const bool in = (unsigned)ky < 5u && (unsigned)kx < 5u && ci < 3;
+      w1q[e] = __float2bfloat16_rn(in ? c->wg[co * 75 + (ky * 5 + kx) * 3 + ci] : 0.f);
     }
+  }
   if (blockIdx.x == 0 && threadIdx.x < 16) c->stats[threadIdx.x] = 0.f;
 }
 

@@ -630,10 +630,11 @@ enum TmapId : int {
   TM_DH,       // dh (F, B)              box (64,R)   128B-swizzled, fc1 dgrad B
   TM_A1H,      // a1                box (8,16,12,1)  conv2 fwd halo (kernels_conv.cuh)
   TM_DZ2H,     // dz2               box (8,16,12,1)  conv2 dgrad halo
-  TM_XSH,      // xs [B][36][36][8]  box (8,16,13,1)  conv1 halo
+  TM_XSH,      // xs [B][36 Y][2 par][18 X'][8] box (8,10,2,36,1)  conv1 fwd halo (kernels_conv.cuh)
   TM_A1WS,     // a1  box (32,16,4,1)  64B-swizzled    conv2 wgrad A (width 1)
   TM_DZ2WS,    // dz2 box (64,16,4,1)  128B-swizzled   conv2 wgrad B (width 1)
-  TM_W1P,      // w1p (240, C1)      box (8, N)       conv1 weights [C1][kx][ky6][8]
+  TM_XSW,      // xs                box (8,8,1,36,1)  conv1 wgrad: one x-shifted copy per dx
+  TM_G,        // g1 [B][16][16][4 q][C1] box (64,8,16,1) 128B-swizzled  conv1 wgrad A (MN-major)
   TM_COUNT
 };
 
@@ -877,9 +878,11 @@ struct TmaFc1Dgrad : TcFc1Dgrad<WQ> {
 };
 
 // --------------------------------------------------------------------------
-// conv1 on tensor cores.  K1 (gather): the batch is staged as bf16
-// xs[r][36][36][8] = x/255 with a 2-pixel zero border and the 3 channels padded
-// to 8, so that every (pixel, tap) is one aligned 16-byte chunk.
+// conv1 on tensor cores.  K1 (staging): the batch is staged as bf16 x/255 with a
+// 2-pixel zero border and the 3 channels padded to 8 (one aligned 16-byte chunk
+// per pixel), columns split by parity: xs[r][Y 36][X % 2][X / 2 (18)][8] for the
+// padded coordinates (Y, X) = (y + 2, x + 2).  Channel 3 is 1.0 inside the image
+// (0 in the border): the conv1 wgrad reads the bias gradient from it.
 // --------------------------------------------------------------------------
 constexpr int kStageThreads = 256;
 __global__ void __launch_bounds__(kStageThreads)
@@ -888,19 +891,22 @@ __global__ void __launch_bounds__(kStageThreads)
   const int ti = find_task(prefix, ntask, blockIdx.x);
   const Task tk = tasks[ti];
   const ClientRec* c = recs + tk.rec;
-  const int e = (blockIdx.x - __ldg(prefix + ti)) * kStageThreads + threadIdx.x;  // staged pixel index
+  const int e = (blockIdx.x - __ldg(prefix + ti)) * kStageThreads + threadIdx.x;  // staged pixel, storage order
   if (e >= tk.rows * 1296) return;
-  const int r = e / 1296, rem = e - r * 1296, Y = rem / 36, X = rem - Y * 36;
+  const int r = e / 1296, rem = e - r * 1296, Y = rem / 36, rx = rem - Y * 36, X = 2 * (rx % 18) + rx / 18;
   const int y = Y - 2, x = X - 2;
   uint4 out = make_uint4(0, 0, 0, 0);
   if ((unsigned)y < 32u && (unsigned)x < 32u) {
     const uint8_t* px = c->x + (int64_t)c->perm[tk.base + r] * 3072 + (y * 32 + x) * 3;
     const __nv_bfloat162 v01 = __floats2bfloat162_rn(px01(px[0]), px01(px[1]));
-    const __nv_bfloat162 v2 = __floats2bfloat162_rn(px01(px[2]), 0.f);
+    const __nv_bfloat162 v23 = __floats2bfloat162_rn(px01(px[2]), 1.f);
     out.x = *reinterpret_cast<const uint32_t*>(&v01);
-    out.y = *reinterpret_cast<const uint32_t*>(&v2);
+    out.y = *reinterpret_cast<const uint32_t*>(&v23);
   }
   reinterpret_cast<uint4*>(c->buf[B_XS])[e] = out;
+}
+__device__ __forceinline__ int64_t xs_index(int r, int Y, int X) {  // 8-element chunk index of padded (Y, X)
+  return ((int64_t)(r * 36 + Y) * 2 + (X & 1)) * 18 + (X >> 1);
 }
 
 // conv1 wgrad: D[m = tap*8 + ci (+ bias row 200), n = co] = sum_p xs(p, tap, ci) dz1[p][co],
@@ -910,7 +916,7 @@ template <int WQ>
 struct TcConv1Wgrad {
   typedef CnnW<WQ> W;
   static constexpr bool A_MN = true, B_MN = true;
-  struct PA { int i, off, kind; };  // kind 0: gather (off = staged offset of the tap), 1: ones, 2: zero
+  struct PA { int i, ky, kx, kind; };  // kind 0: gather tap (ky, kx), 1: ones, 2: zero
   struct PB { int i, n0; };
   const ClientRec* recs;
   CnnDims d;
@@ -925,15 +931,15 @@ struct TcConv1Wgrad {
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
   __device__ PA a_pre(const TcTile& t, int i, int j) const {
     const int tap = (t.m0 >> 3) + j;
-    if (tap == 25) return PA{i, 0, 1};
-    if (tap > 25) return PA{i, 0, 2};
+    if (tap == 25) return PA{i, 0, 0, 1};
+    if (tap > 25) return PA{i, 0, 0, 2};
     const int ky = tap / 5, kx = tap - ky * 5;
-    return PA{i, (ky * 36 + kx) * 8, 0};
+    return PA{i, ky, kx, 0};
   }
   __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
     if (s.kind) return s.kind == 1 ? (const void*)kOneChunk : nullptr;
     const int p = t.n0 * kWgradChunkPx + kb * 64 + s.i, r = p >> 10, y = (p >> 5) & 31, x = p & 31;
-    return (const bf16*)t.c->buf[B_XS] + ((int64_t)r * 1296 + y * 36 + x) * 8 + s.off;
+    return (const bf16*)t.c->buf[B_XS] + xs_index(r, y + s.ky, x + s.kx) * 8;
   }
   __device__ PB b_pre(const TcTile& t, int i, int j) const { return PB{i, 8 * j}; }
   __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
@@ -977,8 +983,11 @@ __global__ void __launch_bounds__(kReduceBlock)
     float* w = c->params + off_w + co * 75 + idx;
     const float nw = *w - lr * g;
     *w = nw;
-    const int tap = idx / 3, ky = tap / 5, kx = tap - ky * 5;  // w1p layout [C1][kx][ky 6][8]
-    ((bf16*)c->buf[B_W1P])[co * 240 + (kx * 6 + ky) * 8 + idx % 3] = __float2bfloat16_rn(nw);
+    const int tap = idx / 3, ky = tap / 5, kx = tap - ky * 5, ci = idx - 3 * tap;
+    const bf16 h = __float2bfloat16_rn(nw);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)  // the weight's 4 places in the pool-quad shadow (common.h w1q_index)
+      ((bf16*)c->buf[B_W1P])[w1q_index(C1, ky + (q >> 1), kx + (q & 1), q, co, ci)] = h;
   }
 }
 

@@ -133,8 +133,8 @@ SlotLayout slot_layout(const ModelDims& m, int b, int64_t n, int epochs, int e) 
     put(B_DZ2, B * 256 * m.c2 * e);
     put(B_DZC1, B * 1024 * m.c1 * e);
     if (e == 2) {
-      put(B_XS, B * 36 * 36 * 8 * 2);        // bf16 input staged for the tensor cores: 2-px zero border, ci padded to 8
-      put(B_W1P, (uint64_t)m.c1 * 30 * 8 * 2);  // conv1 weight shadow [c1][kx 5][ky 6][8 ci] bf16
+      put(B_XS, B * 36 * 36 * 8 * 2);  // bf16 input staged for the tensor cores: 2-px zero border, ci padded to 8
+      put(B_W1P, w1q_bytes(m.c1));     // conv1 pool-quad weight shadow (common.h w1q_index)
     }
   } else {
     put(B_R_A0, B * 1024 * 16 * e);
