@@ -275,7 +275,7 @@ constexpr int MW_BM = 64, MW_BN = 64;
 
 enum Op : int {
   OP_C1F = 0, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R,
-  OP_MF, OP_MHEAD, OP_MW, OP_ADMIT_, OP_FEDAVG_, OP_STAGE, OP_HEADA = 31 /* CNN head part a (stats: OP_HEAD) */,
+  OP_MF, OP_MHEAD, OP_MW, OP_ADMIT_, OP_FEDAVG_, OP_STAGE,
   // ResNet-8 launch instances (each needs its own prefix table); stats use PROTEA_OPC_R_* classes
   RI_F0 = 32, RI_HEAD = RI_F0 + 7, RI_D1 = RI_HEAD + 1, RI_W0 = RI_D1 + 6, RI_R0 = RI_W0 + 7, OP_COUNT = RI_R0 + 7
 };
@@ -325,8 +325,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
     case OP_C1F: return cdiv(rows * 1024, C1F_BM) * cdiv(m.c1, C1F_BN);
     case OP_C2F: return cdiv(rows * 256, C2F_BM) * cdiv(m.c2, C2F_BN);
     case OP_F1F: return cdiv(rows, F1F_BM) * cdiv(m.f, F1F_BN);
-    case OP_HEAD: return cdiv(m.f, kHeadSlice);
-    case OP_HEADA: return cdiv(rows, kHeadRows);
+    case OP_HEAD: return 1;  // k_head_cnn: one CTA per client
     case OP_F1D: return cdiv(rows, F1D_BM) * cdiv(64 * m.c2, F1D_BN);
     case OP_F1W: return cdiv(m.f, F1W_BM) * cdiv(64 * m.c2, F1W_BN);
     case OP_C2D: return cdiv(rows * 256, C2D_BM) * cdiv(m.c1, C2D_BN);
@@ -343,9 +342,9 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
 
 std::vector<int> ops_of(const ModelDims& m, bool tc) {
   if (m.arch == PROTEA_MODEL_CNN && tc)
-    return {OP_STAGE, OP_C1F, OP_C2F, OP_F1F, OP_HEADA, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C1W, OP_C1R};
+    return {OP_STAGE, OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_CNN)
-    return {OP_C1F, OP_C2F, OP_F1F, OP_HEADA, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
+    return {OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_MLP) return {OP_MF, OP_MHEAD, OP_MW};
   std::vector<int> v;
   for (int i = 0; i < 7; ++i) v.push_back(RI_F0 + i);
@@ -361,7 +360,6 @@ std::vector<int> ops_of(const ModelDims& m, bool tc) {
 // written once; weights fp32, activations e bytes).  DESIGN.md "Roofline".
 void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, uint64_t* by);
 int op_class(int op) {
-  if (op == OP_HEADA) return OP_HEAD;
   if (op < RI_F0) return op;
   if (op < RI_HEAD) return PROTEA_OPC_R_FWD;
   if (op == RI_HEAD) return PROTEA_OPC_R_HEAD;
@@ -511,6 +509,22 @@ void launch_conv1_wgrad_q(protea_ctx* ctx, const ClientRec* drecs, const Launch&
   op_end(ctx, ev);
 }
 
+template <typename T>
+void launch_head_cnn(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const Task* tasks,
+                     float lr) {
+  const CnnDims d = cnn_dims(m);
+  const size_t smem = head_cnn_smem(m.f, m.classes);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_head_cnn<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)head_cnn_smem(512, 64));
+    attr = true;
+  }
+  HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
+  const int ev = op_begin(ctx, OP_HEAD);
+  k_head_cnn<T><<<L.ntask, kHeadCnnThreads, smem, ctx->cur>>>(ha, tasks);
+  op_end(ctx, ev);
+}
+
 template <class OpT>
 OpT tma_op(const ClientRec* recs, const CnnDims& d) {
   OpT op;
@@ -542,12 +556,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   else
     launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TmaConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
   launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
-  HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
-  ev = op_begin(ctx, OP_HEAD);
-  k_head_a<T><<<L.grid[OP_HEADA], kHeadThreads, 0, ctx->cur>>>(ha, tasks, dtab + L.prefix_off[OP_HEADA], L.ntask);
-  k_head_b<T><<<L.grid[OP_HEAD], kHeadSlice, 0, ctx->cur>>>(ha, tasks, dtab + L.prefix_off[OP_HEAD], L.ntask);
-  ctx->launches++;
-  op_end(ctx, ev);
+  launch_head_cnn<T>(ctx, m, L, drecs, tasks, lr);
   launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab);
   // Optional fork (kOverlapFc1Wgrad): fc1 wgrad (needs dh, a2; fc1 dgrad already read the old W3) on the side
   // stream while the conv backward chain continues on the main stream.  Measured on B200: the concurrent
@@ -684,12 +693,8 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Conv1Fwd<T, C1F_BM, C1F_BN>, C1F_BM, C1F_BN>(ctx, {drecs, d}, L, OP_C1F, dtab);
     launch_gemm<Conv2Fwd<T, C2F_BM, C2F_BN>, C2F_BM, C2F_BN>(ctx, {drecs, d}, L, OP_C2F, dtab);
     launch_gemm<Fc1Fwd<T, F1F_BM, F1F_BN>, F1F_BM, F1F_BN>(ctx, {drecs, d}, L, OP_F1F, dtab);
-    HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
-    int ev = op_begin(ctx, OP_HEAD);
-    k_head_a<T><<<L.grid[OP_HEADA], kHeadThreads, 0, ctx->cur>>>(ha, tasks, dtab + L.prefix_off[OP_HEADA], L.ntask);
-    k_head_b<T><<<L.grid[OP_HEAD], kHeadSlice, 0, ctx->cur>>>(ha, tasks, dtab + L.prefix_off[OP_HEAD], L.ntask);
-    ctx->launches++;
-    op_end(ctx, ev);
+    launch_head_cnn<T>(ctx, m, L, drecs, tasks, lr);
+    int ev;
     launch_gemm<Fc1Dgrad<T, F1D_BM, F1D_BN>, F1D_BM, F1D_BN>(ctx, {drecs, d}, L, OP_F1D, dtab);
     launch_gemm<Fc1Wgrad<T, F1W_BM, F1W_BN>, F1W_BM, F1W_BN>(ctx, {drecs, d, lr}, L, OP_F1W, dtab);
     launch_gemm<Conv2Dgrad<T, C2D_BM, C2D_BN>, C2D_BM, C2D_BN>(ctx, {drecs, d}, L, OP_C2D, dtab);

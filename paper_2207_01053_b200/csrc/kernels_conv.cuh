@@ -23,6 +23,9 @@
 namespace protea {
 
 constexpr int kConvThreads = 320;
+// dgrad epilogue operands: loaded one tile ahead (true) or at the start of the tile's epilogue,
+// before its accumulator wait (false).  Measured on B200: the one-tile-ahead variant was slower.
+constexpr bool kCrossTilePrefetch = false;
 
 // ---------------------------------------------------------------------------
 // conv2 fwd / dgrad
@@ -82,33 +85,58 @@ struct HaloConv2 {
     }
   }
   __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc) const {
+    const uint64_t a0 = G::SW64 ? tc::sdesc_sw64(hb, 16, 512) : tc::sdesc(hb, G::COPY, 128);
+    const uint64_t b0 = !DGRAD ? tc::sdesc(sb + grp * G::NCC * N * 16, N * 16, 128)  // K chunk (tap, grp*NCC + 2cp)
+                               : tc::sdesc(sb + grp * G::NCC * 128, 128, W::C2 * 16);  // k rows = co of tap
+#pragma unroll
     for (int ky = 0; ky < 5; ++ky)
+#pragma unroll
       for (int kx = 0; kx < 5; ++kx) {
         const int tap = ky * 5 + kx, row0 = DGRAD ? 4 - ky : ky;
+#pragma unroll
         for (int cp = 0; cp < G::NCC / 2; ++cp) {
-          const uint64_t da = G::SW64 ? tc::sdesc_sw64(hb + kx * 4 * G::COPY + row0 * 1024 + 32 * cp, 16, 512)
-                                      : tc::sdesc(hb + (kx * G::NCC + 2 * cp) * G::COPY + row0 * 256, G::COPY, 128);
-          uint64_t db;
-          if (!DGRAD) {  // K chunk index of (tap, channel grp*NCC + 2cp)
-            const int kc = tap * (W::C1 / 8) + grp * G::NCC + 2 * cp;
-            db = tc::sdesc(sb + kc * N * 16, N * 16, 128);
-          } else {  // k rows = co (16 of them) of tap; n groups at C2*16
-            const int co0 = (grp * G::NCC + 2 * cp) * 8;
-            db = tc::sdesc(sb + tap * (N / 8) * W::C2 * 16 + co0 * 16, 128, W::C2 * 16);
-          }
-          tc::mma_bf16(dt, da, db, idesc, (grp | tap | cp) != 0);
+          const uint32_t ao = G::SW64 ? kx * 4 * G::COPY + row0 * 1024 + 32 * cp
+                                      : (kx * G::NCC + 2 * cp) * G::COPY + row0 * 256;
+          const uint32_t bo = !DGRAD ? (tap * (W::C1 / 8) + 2 * cp) * N * 16 : tap * (N / 8) * W::C2 * 16 + cp * 256;
+          tc::mma_bf16(dt, tc::dadd(a0, ao), tc::dadd(b0, bo), idesc, (grp | tap | cp) != 0);
         }
       }
   }
   // Epilogue of one tile: warps w, w+4 share TMEM lanes; column chunks c0 = 16 g + 32 j.
+  static constexpr int NCH = (N + 31) / 32;
+  static constexpr int NV = NOUT < 16 ? NOUT : 16;
   struct EpiState {  // per-client values cached across the tiles of a client (the bias)
     const ClientRec* c = nullptr;
-    float bias[(N + 31) / 32][16];
+    float bias[NCH][16];
   };
+  // dgrad: the pool-1 operands (a1 > 0 mask, argmax) of the NEXT tile are loaded into registers
+  // while the current tile is processed (the epilogue, not the MMA, is the critical path).
+  struct Pre {
+    uint4 a[NCH][2];
+    uint4 i[NCH];
+  };
+  __device__ void prefetch(const TcTile& t, int tile, int warp, int lane, Pre& p) const {
+    if constexpr (DGRAD) {
+      const int g = warp >> 2, m = tile * 128 + (warp & 3) * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const int c0 = g * 16 + 32 * j;
+        if (c0 >= N) continue;
+        const int64_t o = (int64_t)m * W::C1 + c0;
+        const uint4* a = reinterpret_cast<const uint4*>((const bf16*)t.c->buf[B_A1] + o);
+        p.a[j][0] = a[0];
+        if (NV == 16) p.a[j][1] = a[1];
+        if (NV == 16)
+          p.i[j] = *reinterpret_cast<const uint4*>((const uint8_t*)t.c->buf[B_I1] + o);
+        else {
+          const uint2 u = *reinterpret_cast<const uint2*>((const uint8_t*)t.c->buf[B_I1] + o);
+          p.i[j] = make_uint4(u.x, u.y, 0, 0);
+        }
+      }
+    }
+  }
   __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
-                           int lane, EpiState& st) const {
-    constexpr int NCH = (N + 31) / 32;
-    constexpr int NV = NOUT < 16 ? NOUT : 16;
+                           int lane, EpiState& st, const Pre& pre) const {
     const int g = warp >> 2, row = (warp & 3) * 32 + lane;
     const int m = tile * 128 + row, r = m >> 8, y = (m >> 4) & 15, x = m & 15;
     float a1v[NCH][NV];
@@ -124,13 +152,13 @@ struct HaloConv2 {
         }
     }
     if (DGRAD) {
+      Pre now;
+      if constexpr (!kCrossTilePrefetch) prefetch(t, tile, warp, lane, now);  // before waiting on the MMA
+      const Pre& p = kCrossTilePrefetch ? pre : now;
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) {  // operands independent of the MMA: fetch before waiting
-        const int c0 = g * 16 + 32 * j;
-        if (c0 >= N) continue;
-        const int64_t o = (int64_t)m * W::C1 + c0;
-        ld_bf16<NV>((const bf16*)t.c->buf[B_A1] + o, a1v[j]);
-        ld_u8<NV>((const uint8_t*)t.c->buf[B_I1] + o, argv[j]);
+      for (int j = 0; j < NCH; ++j) {
+        ld_bf16<NV>(reinterpret_cast<const bf16*>(&p.a[j][0]), a1v[j]);
+        ld_u8<NV>(reinterpret_cast<const uint8_t*>(&p.i[j]), argv[j]);
       }
     }
     tc::mbar_wait(full_bar, parity);
@@ -211,19 +239,22 @@ struct QuadConv1 {
     tc::tma_load_5d(base, tmap_of(t, TM_XSH), bar, 0, (tile & 1) * 8, 0, 0, tile >> 1);
   }
   __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc) const {
+    const uint64_t a0 = tc::sdesc(hb, 160, 640), b0 = tc::sdesc(sb, N * 16, 128);
+#pragma unroll
     for (int dy = 0; dy < 6; ++dy)
-      for (int dp = 0; dp < 3; ++dp) {
-        const uint64_t da = tc::sdesc(hb + dy * 320 + dp * 16, 160, 640);
-        const uint64_t db = tc::sdesc(sb + (dy * 3 + dp) * 2 * N * 16, N * 16, 128);
-        tc::mma_bf16(dt, da, db, idesc, (dy | dp) != 0);
-      }
+#pragma unroll
+      for (int dp = 0; dp < 3; ++dp)
+        tc::mma_bf16(dt, tc::dadd(a0, dy * 320 + dp * 16), tc::dadd(b0, (dy * 3 + dp) * 2 * N * 16), idesc,
+                     (dy | dp) != 0);
   }
   struct EpiState {
     const ClientRec* c = nullptr;
     float bias[NCO];
   };
+  struct Pre {};
+  __device__ void prefetch(const TcTile&, int, int, int, Pre&) const {}
   __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
-                           int lane, EpiState& st) const {
+                           int lane, EpiState& st, const Pre&) const {
     const int g = warp >> 2;
     const bool active = g * NCO < W::C1;  // widths < 1: warps 4-7 idle
     const int r = tile >> 1, row = (warp & 3) * 32 + lane, py = row >> 3, px = (tile & 1) * 8 + (row & 7);
@@ -279,6 +310,26 @@ __device__ __forceinline__ int next_task(const int* __restrict__ prefix, int nta
   return ti;
 }
 
+// Walks a CTA's contiguous tile range task by task; the prefix table is read only
+// when the range crosses into the next task (no dependent global load per tile).
+struct TaskCursor {
+  int ti, lo, hi;  // current task and its tile range [lo, hi)
+  __device__ void init(const int* __restrict__ prefix, int ntask, int g) {
+    ti = find_task(prefix, ntask, g);
+    lo = __ldg(prefix + ti);
+    hi = __ldg(prefix + ti + 1);
+  }
+  __device__ bool advance(const int* __restrict__ prefix, int g) {  // true if the task changed
+    if (g < hi) return false;
+    do {
+      ++ti;
+      lo = hi;
+      hi = __ldg(prefix + ti + 1);
+    } while (g >= hi);
+    return true;
+  }
+};
+
 template <class Op>
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv_persistent(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
@@ -319,19 +370,20 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
   if (warp == 8) {
     if (lane == 0) {  // ---------------- TMA producer
-      int ti = ti0, cur = -1, nb = 0, s = 0;
+      TaskCursor cur;
+      cur.init(prefix, ntask, g0);
+      int nb = 0, s = 0;
       for (int g = g0; g < g1; ++g) {
-        ti = next_task(prefix, ntask, ti, g);
-        t.tk = tasks[ti];
-        t.c = op.recs + t.tk.rec;
-        if (ti != cur) {  // new client: wait until the MMAs released the previous weights, reload
+        const bool fresh = cur.advance(prefix, g) || g == g0;
+        if (fresh) {  // new client: wait until the MMAs released the previous weights, reload
+          t.tk = tasks[cur.ti];
+          t.c = op.recs + t.tk.rec;
           if (nb > 0) tc::mbar_wait(b_empty, (nb - 1) & 1);
           tc::mbar_expect_tx(b_full, Op::B_BYTES);
           op.load_b(t, sb, b_full);
-          cur = ti;
           ++nb;
         }
-        const int tile = g - __ldg(prefix + ti);
+        const int tile = g - cur.lo;
         for (int grp = 0; grp < Op::GROUPS; ++grp, ++s) {
           const int buf = s & 1;
           if (s >= 2) tc::mbar_wait(h_empty + 8 * buf, ((s >> 1) - 1) & 1);
@@ -343,14 +395,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   } else if (warp == 9) {
     if (lane == 0) {  // ---------------- MMA issuer
       const uint32_t idesc = tc::idesc_bf16(128, Op::N, false, Op::B_MN);
-      int ti = ti0, cur = -1, nb = 0, s = 0, i = 0;
+      TaskCursor cur;
+      cur.init(prefix, ntask, g0);
+      int nb = 0, s = 0, i = 0;
       for (int g = g0; g < g1; ++g, ++i) {
-        ti = next_task(prefix, ntask, ti, g);
-        if (ti != cur) {
+        if (cur.advance(prefix, g) || g == g0) {
           if (nb > 0) tc::commit(b_empty);  // completes when every MMA issued so far (old weights) is done
           tc::mbar_wait(b_full, nb & 1);
           tc::fence_after();
-          cur = ti;
           ++nb;
         }
         const int acc = i & 1;
@@ -367,18 +419,33 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
     }
     __syncwarp();
-  } else {  // ---------------- epilogue warps 0-7
+  } else if (g0 < g1) {  // ---------------- epilogue warps 0-7 (next tile's operands prefetched)
     typename Op::EpiState st;
-    int ti = ti0, i = 0;
+    typename Op::Pre pc, pn;
+    TaskCursor cur, nxt;
+    cur.init(prefix, ntask, g0);
+    nxt = cur;
+    t.tk = tasks[cur.ti];
+    t.c = op.recs + t.tk.rec;
+    TcTile tn = t;
+    if (kCrossTilePrefetch) op.prefetch(t, g0 - cur.lo, warp, lane, pc);
+    int i = 0;
     for (int g = g0; g < g1; ++g, ++i) {
-      ti = next_task(prefix, ntask, ti, g);
-      t.tk = tasks[ti];
-      t.c = op.recs + t.tk.rec;
+      if (g + 1 < g1) {
+        if (nxt.advance(prefix, g + 1)) {
+          tn.tk = tasks[nxt.ti];
+          tn.c = op.recs + tn.tk.rec;
+        }
+        if (kCrossTilePrefetch) op.prefetch(tn, g + 1 - nxt.lo, warp, lane, pn);
+      }
       const int acc = i & 1;
-      op.epilogue(t, g - __ldg(prefix + ti), tmem + acc * Op::N, acc_full + 8 * acc, (i >> 1) & 1, warp, lane, st);
+      op.epilogue(t, g - cur.lo, tmem + acc * Op::N, acc_full + 8 * acc, (i >> 1) & 1, warp, lane, st, pc);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(acc_empty + 8 * acc);
+      t = tn;
+      cur = nxt;
+      pc = pn;
     }
   }
   tc::fence_before();
@@ -492,13 +559,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const uint32_t gb = sb + buf * kW1Stage;
           tc::mbar_wait(full + 8 * buf, (s >> 1) & 1);
           tc::fence_after();
-          for (int ks = 0; ks < 8; ++ks) {
-            const uint64_t da = tc::sdesc_sw128(gb + 2048 * ks, kW1GBytes / 2, 1024);
-            for (int dy = 0; dy < 6; ++dy) {
-              const uint64_t db = tc::sdesc(gb + kW1GBytes + (4 * ks + dy) * 128, 256, kW1XCopy);
-              tc::mma_bf16(tmem + dy * 48, da, db, idesc, (sub | ks) != 0);
-            }
-          }
+          const uint64_t a0 = tc::sdesc_sw128(gb, kW1GBytes / 2, 1024), b0 = tc::sdesc(gb + kW1GBytes, 256, kW1XCopy);
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+            for (int dy = 0; dy < 6; ++dy)
+              tc::mma_bf16(tmem + dy * 48, tc::dadd(a0, 2048 * ks), tc::dadd(b0, (4 * ks + dy) * 128), idesc,
+                           (sub | ks) != 0);
           tc::commit(empty + 8 * buf);
         }
         tc::commit(acc_full);

@@ -644,42 +644,62 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a, const Task* _
 }
 
 // --------------------------------------------------------------------------
-// CNN head split across CTAs (the single-CTA k_head is latency bound):
-//  k_head_a (1 CTA / client): fc2 fwd, softmax-CE, dlogits -> scratch (the
-//           wgrad partial buffer, free at this point of the step), loss.
-//  k_head_b (F/64 CTAs / client): for its 64 features f: dh[:, f] (old W2
-//           column f, ReLU mask), fc1 bias SGD, W2[:, f] SGD; slice 0 also b2.
-// Every W2 column is read and written by exactly one CTA -> race free.
+// CNN head, one CTA per client (F <= 512 threads, one feature each):
+//  1. logits = h W2^T + b2 (warp per row, lanes over features; W2 staged in smem)
+//  2. softmax-CE: dlogits = (softmax - onehot) / rows, loss
+//  3. thread f: dh[:, f] = (dlogits W2[:, f]) * (h[:, f] > 0) with the OLD W2,
+//     fc1 bias SGD (sum_r dh[r][f]), W2[:, f] -= lr dlogits^T h[:, f]
+//  4. b2 -= lr sum_r dlogits
+// Every global load of a phase is independent of the phase's stores, so they are
+// issued together (the former per-row global-load loops were latency bound).
 // --------------------------------------------------------------------------
-constexpr int kHeadRows = 8;  // rows of the batch per k_head_a CTA
+constexpr int kHeadCnnThreads = 512;
+inline size_t head_cnn_smem(int F, int C) { return (size_t)(C * F + 64 * C + 64) * sizeof(float); }
 template <typename T>
-__global__ void __launch_bounds__(kHeadThreads)
-    k_head_a(HeadArgs a, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
-  __shared__ float dlog[kHeadRows * 64];
-  __shared__ float lossr[kHeadRows];
-  const int ti = find_task(prefix, ntask, blockIdx.x);
-  const Task tk = tasks[ti];
+__global__ void __launch_bounds__(kHeadCnnThreads)
+    k_head_cnn(HeadArgs a, const Task* __restrict__ tasks) {
+  extern __shared__ float hsm[];
+  const Task tk = tasks[blockIdx.x];
   const ClientRec* c = a.recs + tk.rec;
   const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
-  const int r0 = (blockIdx.x - __ldg(prefix + ti)) * kHeadRows;
-  const int nr = min(kHeadRows, tk.rows - r0), rows = tk.rows, F = a.F, C = a.classes;
-  const T* h = (const T*)c->buf[a.hbuf];
-  const float* W = c->params + a.w;
-  const float* bias = c->params + a.b;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int idx = warp; idx < nr * C; idx += kHeadThreads / 32) {
-    const int r = idx / C, cc = idx - r * C;
-    float s = 0.f;
-    for (int f = lane; f < F; f += 32) s = fmaf(ldv(h + (int64_t)(r0 + r) * F + f), W[(int64_t)cc * F + f], s);
+  const int rows = tk.rows, F = a.F, C = a.classes;
+  float* Ws = hsm;              // [C][F] old W2
+  float* dlog = Ws + C * F;     // [rows][C]
+  float* lossr = dlog + 64 * C; // [rows]
+  const T* __restrict__ h = (const T*)c->buf[a.hbuf];
+  T* __restrict__ dh = (T*)c->buf[a.dhbuf];
+  float* __restrict__ W = c->params + a.w;
+  float* __restrict__ bias = c->params + a.b;
+  for (int i = threadIdx.x; i < C * F; i += kHeadCnnThreads) Ws[i] = W[i];
+  __syncthreads();
+  // 1. logits
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < rows; r += kHeadCnnThreads / 32) {
+    for (int c0 = 0; c0 < C; c0 += 16) {
+      float acc[16];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) dlog[r * C + cc] = s + bias[cc];
+      for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+#pragma unroll 4
+      for (int f = lane; f < F; f += 32) {
+        const float hv = ldv(h + (int64_t)r * F + f);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < C) acc[j] = fmaf(hv, Ws[(c0 + j) * F + f], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float v = acc[j];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && c0 + j < C) dlog[r * C + c0 + j] = v + bias[c0 + j];
+      }
+    }
   }
   __syncthreads();
-  float* out = (float*)c->buf[B_WSP];
-  if (threadIdx.x < nr) {
+  // 2. softmax cross-entropy (mean over the batch rows)
+  if (threadIdx.x < rows) {
     const int r = threadIdx.x;
-    const int label = c->y[c->perm[tk.base + r0 + r]];
+    const int label = c->y[c->perm[tk.base + r]];
     float mx = -INFINITY;
     for (int cc = 0; cc < C; ++cc) mx = fmaxf(mx, dlog[r * C + cc]);
     float s = 0.f;
@@ -688,55 +708,51 @@ __global__ void __launch_bounds__(kHeadThreads)
     const float inv = 1.f / (s * (float)rows);
     for (int cc = 0; cc < C; ++cc) {
       const float p = expf(dlog[r * C + cc] - mx);
-      out[(r0 + r) * C + cc] = p * inv - (cc == label ? 1.f / (float)rows : 0.f);
+      dlog[r * C + cc] = p * inv - (cc == label ? 1.f / (float)rows : 0.f);
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float s = 0.f;
-    for (int r = 0; r < nr; ++r) s += lossr[r];
-    atomicAdd(&c->stats[0], s / (float)rows);  // loss statistic only (summation order not fixed)
-    if (c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(globaltimer() - t_start));
-  }
-}
-
-constexpr int kHeadSlice = 64;
-template <typename T>
-__global__ void __launch_bounds__(kHeadSlice)
-    k_head_b(HeadArgs a, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
-  __shared__ float dlog[64 * 64];
-  const int ti = find_task(prefix, ntask, blockIdx.x);
-  const Task tk = tasks[ti];
-  const ClientRec* c = a.recs + tk.rec;
-  const int slice = blockIdx.x - __ldg(prefix + ti);
-  const int rows = tk.rows, F = a.F, C = a.classes;
-  const float* dl = (const float*)c->buf[B_WSP];
-  for (int i = threadIdx.x; i < rows * C; i += kHeadSlice) dlog[i] = dl[i];
-  __syncthreads();
-  const int f = slice * kHeadSlice + threadIdx.x;
+  // 3. per feature: dh, fc1 bias SGD, W2 column SGD (classes in chunks of 16 register accumulators)
+  const int f = threadIdx.x;
   if (f < F) {
-    const T* h = (const T*)c->buf[a.hbuf];
-    T* dh = (T*)c->buf[a.dhbuf];
-    float* W = c->params + a.w;
     float gb = 0.f;
+#pragma unroll 4
     for (int r = 0; r < rows; ++r) {
+      const float hv = ldv(h + (int64_t)r * F + f);
       float s = 0.f;
-      for (int cc = 0; cc < C; ++cc) s = fmaf(dlog[r * C + cc], W[(int64_t)cc * F + f], s);
-      s = ldv(h + (int64_t)r * F + f) > 0.f ? s : 0.f;
+      for (int cc = 0; cc < C; ++cc) s = fmaf(dlog[r * C + cc], Ws[cc * F + f], s);
+      s = hv > 0.f ? s : 0.f;
       stv(dh + (int64_t)r * F + f, s);
       gb += s;
     }
     c->params[a.b_prev + f] -= a.lr * gb;
-    for (int cc = 0; cc < C; ++cc) {
-      float g = 0.f;
-      for (int r = 0; r < rows; ++r) g = fmaf(dlog[r * C + cc], ldv(h + (int64_t)r * F + f), g);
-      W[(int64_t)cc * F + f] -= a.lr * g;
+    for (int c0 = 0; c0 < C; c0 += 16) {
+      float g[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) g[j] = 0.f;
+#pragma unroll 4
+      for (int r = 0; r < rows; ++r) {
+        const float hv = ldv(h + (int64_t)r * F + f);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < C) g[j] = fmaf(dlog[r * C + c0 + j], hv, g[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < C) W[(int64_t)(c0 + j) * F + f] = Ws[(c0 + j) * F + f] - a.lr * g[j];
     }
   }
-  if (slice == 0 && threadIdx.x < C) {
+  // 4. b2, loss statistic
+  if (threadIdx.x < C) {
     float g = 0.f;
     for (int r = 0; r < rows; ++r) g += dlog[r * C + threadIdx.x];
-    c->params[a.b + threadIdx.x] -= a.lr * g;
+    bias[threadIdx.x] -= a.lr * g;
+  }
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int r = 0; r < rows; ++r) s += lossr[r];
+    c->stats[0] += s / (float)rows;
+    if (c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(globaltimer() - t_start));
   }
 }
 

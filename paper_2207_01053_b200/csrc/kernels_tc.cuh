@@ -197,23 +197,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---------------- MMA issuer (one thread of warp 8)
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_bf16(128, t.n_mma, Op::A_MN, Op::B_MN);
+      // descriptors are linear in the stage base and the k step: precompute, then add constants
+      uint64_t da0, dak, db0, dbk;
+      if constexpr (TMA) {
+        da0 = op.a_desc(t, sbase, 0);
+        dak = op.a_desc(t, sbase, 1) - da0;
+        db0 = op.b_desc(t, sbase + A_BYTES, 0);
+        dbk = op.b_desc(t, sbase + A_BYTES, 1) - db0;
+      } else {
+        da0 = cp_desc<Op::A_MN, 128>(sbase, 0);
+        dak = cp_desc<Op::A_MN, 128>(sbase, 1) - da0;
+        db0 = cp_desc<Op::B_MN, BN>(sbase + A_BYTES, 0);
+        dbk = cp_desc<Op::B_MN, BN>(sbase + A_BYTES, 1) - db0;
+      }
       for (int kb = 0; kb < t.nk; ++kb) {
         const int s = kb % STAGES;
         tc::mbar_wait(bar0 + 8 * s, (kb / STAGES) & 1);
         tc::fence_after();
-        const uint32_t a_base = sbase + s * STAGE, b_base = a_base + A_BYTES;
+        const uint64_t so = (uint64_t)(s * (STAGE >> 4));
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          uint64_t da, db;
-          if constexpr (TMA) {
-            da = op.a_desc(t, a_base, ks);
-            db = op.b_desc(t, b_base, ks);
-          } else {
-            da = cp_desc<Op::A_MN, 128>(a_base, ks);
-            db = cp_desc<Op::B_MN, BN>(b_base, ks);
-          }
-          tc::mma_bf16(tmem, da, db, idesc, (kb | ks) != 0);
-        }
+        for (int ks = 0; ks < 4; ++ks)
+          tc::mma_bf16(tmem, da0 + so + ks * dak, db0 + so + ks * dbk, idesc, (kb | ks) != 0);
         tc::commit(bar0 + 8 * (STAGES + s));
       }
       tc::commit(done);

@@ -34,6 +34,12 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   return d;                // base_offset 0, lbo_mode 0, layout_type 0 (SWIZZLE_NONE)
 }
 
+// Advance a descriptor's start address by `bytes` (multiple of 16; stays inside the 256 KB window).
+// Issue cost matters: an MMA whose descriptor is rebuilt from scratch costs ~78 issue cycles,
+// more than the 128 x N x 16 MMA itself for N < 160 (tools/mma_bench.cu); constant offsets from a
+// precomputed base keep the issuer ahead of the tensor pipe.
+__host__ __device__ constexpr uint64_t dadd(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
+
 // 128-byte-swizzled operand (TMA CU_TENSOR_MAP_SWIZZLE_128B): 8-row x 128 B atoms (1024 B,
 // atom-aligned base); K-major: SBO = 1024, K steps advance the start address by 32 B
 // inside the atom; MN-major: SBO = 1024 (8 k rows), LBO = stride of 64-element MN blocks.
