@@ -99,9 +99,14 @@ struct protea_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint64_t launches = 0;
   // side stream: fc1 wgrad (HBM-bound weight RMW) overlaps the conv backward chain (L2 / tensor bound)
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr;  // lowest priority: the deferred fc1 wgrad
+  cudaStream_t hi = nullptr;    // highest priority: the lock-step chain of execute()
   cudaStream_t cur = nullptr;  // stream the launch helpers currently issue to
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  std::vector<cudaEvent_t> gjoin;  // per model group: end of its deferred fc1 wgrad
+  std::vector<char> gpending;      // per model group: a deferred fc1 wgrad not yet joined
+  bool overlap_now = false;        // current iteration defers fc1 wgrad (light iteration)
+  int64_t overlap_rows = 640;      // defer when the iteration's total rows are at most this (PROTEA_OVERLAP_ROWS)
   // per-op-class accounting of the current round (protea_round_stats)
   uint32_t time_ops = 0;
   std::vector<cudaEvent_t> evpool;
@@ -287,7 +292,14 @@ int rsplits(const Layer& l, int rows) { return cdiv(rows * l.hout * l.wout, kWgr
 // tensor-core tile shapes (bf16 mode): M tile = 128, BN per op, STAGES-deep ring
 constexpr int TC_C1F_BN = 32, TC_C1W_BN = 32, TC_C2F_BN = 64, TC_C2D_BN = 32, TC_C2W_BN = 64, TC_F1F_BN = 64, TC_F1D_BN = 64, TC_F1W_BN = 128;
 constexpr int TC_STAGES = 4, TC_F1W_STAGES = 1;
-constexpr bool kOverlapFc1Wgrad = false;
+// Join a group's deferred fc1 wgrad into the current stream (before anything that writes a2 / dh
+// or reads the fc1 weights: the next conv2 fwd, a release, the end of the round).
+void join_group(protea_ctx* ctx, int g) {
+  if (g < (int)ctx->gpending.size() && ctx->gpending[g]) {
+    cudaStreamWaitEvent(ctx->cur, ctx->gjoin[g], 0);
+    ctx->gpending[g] = 0;
+  }
+}
 
 int tiles(const ModelDims& m, int op, int rows, bool tc) {
   if (op >= RI_F0) {
@@ -551,6 +563,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
                                                                   L.ntask);
   op_end(ctx, ev);
   launch_conv_persistent<QuadConv1<WQ>>(ctx, drecs, d, L, OP_C1F, dtab);
+  join_group(ctx, L.group);  // the previous step's deferred fc1 wgrad still reads a2
   if constexpr (WQ >= 2)
     launch_conv_persistent<HaloConv2<WQ, false>>(ctx, drecs, d, L, OP_C2F, dtab);
   else
@@ -558,18 +571,22 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
   launch_head_cnn<T>(ctx, m, L, drecs, tasks, lr);
   launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab);
-  // Optional fork (kOverlapFc1Wgrad): fc1 wgrad (needs dh, a2; fc1 dgrad already read the old W3) on the side
-  // stream while the conv backward chain continues on the main stream.  Measured on B200: the concurrent
-  // kernels contend (the 225 KB-smem halo convs cannot co-reside with the RMW CTAs), 101 -> 105 ms/round,
-  // so it is off by default.
-  if (kOverlapFc1Wgrad) {
-    cudaEventRecord(ctx->fork_ev, ctx->stream);
+  // fc1 wgrad (HBM-bound RMW of the fp32 master + bf16 shadow) needs dh, a2 and the fc1 weights, which
+  // nothing in the rest of this step touches.  In light iterations (the lock-step tail, where every
+  // other op is latency bound) it runs on the low-priority side stream and is joined only before the
+  // next conv2 fwd of the group (which overwrites a2), a release, or the end of the round.
+  if (ctx->overlap_now) {
+    cudaEventRecord(ctx->fork_ev, ctx->cur);
     cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0);
+    cudaStream_t main = ctx->cur;
     ctx->cur = ctx->side;
+    launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
+    cudaEventRecord(ctx->gjoin[L.group], ctx->side);
+    ctx->gpending[L.group] = 1;
+    ctx->cur = main;
+  } else {
+    launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
   }
-  launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
-  ctx->cur = ctx->stream;
-  if (kOverlapFc1Wgrad) cudaEventRecord(ctx->join_ev, ctx->side);
   launch_conv_persistent<HaloConv2<WQ, true>>(ctx, drecs, d, L, OP_C2D, dtab);
   if constexpr (WQ == 4)
     launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2WgradSW>(drecs, d, lr), L, OP_C2W, dtab);
@@ -584,7 +601,6 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
                                                                        L.ntask, m.c1, d.w1, d.b1, lr);
   op_end(ctx, ev);
-  if (kOverlapFc1Wgrad) cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0);  // join the fc1 wgrad branch
 }
 
 void launch_step_tc(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const int32_t* dtab,
@@ -778,7 +794,11 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, opts->device) == cudaSuccess && nsm > 0)
       g_num_sms = nsm;
   }
-  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+  int prio_least = 0, prio_greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest);
+  if (const char* ov = std::getenv("PROTEA_OVERLAP_ROWS")) ctx->overlap_rows = std::atoll(ov);
+  if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_least) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, prio_greatest) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming) != cudaSuccess) {
     set_global_error("protea_init: stream/event creation failed");
@@ -821,6 +841,11 @@ void protea_finalize(protea_ctx* ctx) {
     cudaStreamSynchronize(ctx->side);
     cudaStreamDestroy(ctx->side);
   }
+  if (ctx->hi) {
+    cudaStreamSynchronize(ctx->hi);
+    cudaStreamDestroy(ctx->hi);
+  }
+  for (auto e : ctx->gjoin) cudaEventDestroy(e);
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1060,7 +1085,24 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
   const int32_t* dtab = ctx->tab.p;
   int maxE = 1;
   for (auto& c : rc) maxE = std::max(maxE, c.E);
+  // the iterations run on the high-priority stream (forked from / joined into the caller's stream)
+  while ((int)ctx->gjoin.size() < G) {
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    ctx->gjoin.push_back(ev);
+  }
+  ctx->gpending.assign(G, 0);
+  CK(cudaEventRecord(ctx->fork_ev, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->hi, ctx->fork_ev, 0));
+  ctx->cur = ctx->hi;
+  std::vector<int64_t> iter_rows(T, 0);
+  for (auto& c : rc)
+    for (uint64_t t = c.admit; t < c.release; ++t) {
+      const int64_t j = (int64_t)((t - c.admit) % c.nb);
+      iter_rows[t] += std::min<int64_t>(c.B, c.n - j * c.B);
+    }
   for (uint64_t t = 0; t < T; ++t) {
+    ctx->overlap_now = tc_mode && iter_rows[t] <= ctx->overlap_rows;
     if (admits[t].second > 0) {
       const int* ids = dtab + admits[t].first;
       int64_t maxP = 0, maxn = 0;
@@ -1072,10 +1114,10 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
       for (auto& c : rc)
         if (c.admit == t) ctx->op_bytes[PROTEA_OPC_ADMIT] += 8 * (uint64_t)ctx->groups[c.group].m.P + 4 * (uint64_t)c.E * c.n;
       int ev = op_begin(ctx, PROTEA_OPC_ADMIT);
-      k_admit_params<<<dim3(grid_for(maxP / 4 + 1, 256, 64), admits[t].second), 256, 0, ctx->stream>>>(drecs, ids);
+      k_admit_params<<<dim3(grid_for(maxP / 4 + 1, 256, 64), admits[t].second), 256, 0, ctx->cur>>>(drecs, ids);
       op_end(ctx, ev);
       ev = op_begin(ctx, PROTEA_OPC_ADMIT);
-      k_admit_perm<<<dim3(cdiv((int)maxn, kPermThreads), admits[t].second, maxE), kPermThreads, 0, ctx->stream>>>(
+      k_admit_perm<<<dim3(cdiv((int)maxn, kPermThreads), admits[t].second, maxE), kPermThreads, 0, ctx->cur>>>(
           drecs, ids, seed, round, shuffle);
       op_end(ctx, ev);
     }
@@ -1094,12 +1136,18 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
         if (rel_by_group[t][g].second > 0) {
           const int64_t P = ctx->groups[g].m.P;
           ctx->op_bytes[PROTEA_OPC_FEDAVG] += (uint64_t)P * (20 + 4 * rel_by_group[t][g].second);
+          join_group(ctx, g);  // the released clients' last fc1 wgrad
           const int ev = op_begin(ctx, PROTEA_OPC_FEDAVG);
-          k_release_acc<<<grid_for(P, 256), 256, 0, ctx->stream>>>(drecs, dtab + rel_by_group[t][g].first,
-                                                                    rel_by_group[t][g].second, P, loss_dev);
+          k_release_acc<<<grid_for(P, 256), 256, 0, ctx->cur>>>(drecs, dtab + rel_by_group[t][g].first,
+                                                                 rel_by_group[t][g].second, P, loss_dev);
           op_end(ctx, ev);
         }
   }
+  for (int g = 0; g < G; ++g) join_group(ctx, g);
+  ctx->overlap_now = false;
+  CK(cudaEventRecord(ctx->join_ev, ctx->hi));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
+  ctx->cur = ctx->stream;
   CK(cudaGetLastError());
   if (iters_out) *iters_out = T;
   return PROTEA_OK;
