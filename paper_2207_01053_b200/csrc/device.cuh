@@ -48,6 +48,26 @@ __device__ __forceinline__ int find_task(const int* __restrict__ prefix, int nta
   return lo;
 }
 
+// Walks a CTA's contiguous tile range task by task; the prefix table is read only
+// when the range crosses into the next task (no dependent global load per tile).
+struct TaskCursor {
+  int ti, lo, hi;  // current task and its tile range [lo, hi)
+  __device__ void init(const int* __restrict__ prefix, int ntask, int g) {
+    ti = find_task(prefix, ntask, g);
+    lo = __ldg(prefix + ti);
+    hi = __ldg(prefix + ti + 1);
+  }
+  __device__ bool advance(const int* __restrict__ prefix, int g) {  // true if the task changed
+    if (g < hi) return false;
+    do {
+      ++ti;
+      lo = hi;
+      hi = __ldg(prefix + ti + 1);
+    } while (g >= hi);
+    return true;
+  }
+};
+
 template <typename T>
 __device__ __forceinline__ float ldv(const T* p);
 template <>

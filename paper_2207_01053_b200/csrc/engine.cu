@@ -490,6 +490,23 @@ void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, c
 
 int g_num_sms = 148;
 
+template <int BN, int STAGES, class OpT>
+void launch_gemm_persistent(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, const int32_t* dtab,
+                            int ctas_per_sm) {
+  constexpr int SMEM = pers_smem_bytes<BN, STAGES>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_persistent<BN, STAGES, OpT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const int grid = std::min(L.grid[opid], ctas_per_sm * g_num_sms);
+  const int ev = op_begin(ctx, opid);
+  k_gemm_persistent<BN, STAGES, OpT><<<grid, kPersThreads, SMEM, ctx->cur>>>(op, tasks, dtab + L.prefix_off[opid],
+                                                                               L.ntask);
+  op_end(ctx, ev);
+}
+
 template <class Op>
 void launch_conv_persistent(protea_ctx* ctx, const ClientRec* drecs, const CnnDims& d, const Launch& L, int opid,
                             const int32_t* dtab) {
@@ -570,7 +587,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
     launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TmaConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
   launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
   launch_head_cnn<T>(ctx, m, L, drecs, tasks, lr);
-  launch_gemm_tc<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab);
+  launch_gemm_persistent<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab, 2);
   // fc1 wgrad (HBM-bound RMW of the fp32 master + bf16 shadow) needs dh, a2 and the fc1 weights, which
   // nothing in the rest of this step touches.  In light iterations (the lock-step tail, where every
   // other op is latency bound) it runs on the low-priority side stream and is joined only before the

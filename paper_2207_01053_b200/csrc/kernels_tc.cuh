@@ -235,6 +235,147 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     atomicAdd((unsigned long long*)t.c->sm_ns, (unsigned long long)(globaltimer() - t_start));
 }
 
+// --------------------------------------------------------------------------
+// Persistent variant for TMA ops without split-K finish (fc1 fwd / dgrad): a CTA
+// walks a contiguous range of the launch's tiles; warp 9 streams every tile's K
+// blocks through the STAGES ring, warp 8 issues the MMAs into one of two TMEM
+// accumulators, warps 0-7 drain the other one through the op's epilogue, so the
+// epilogue of tile i overlaps the loads and MMAs of tile i+1 (the per-CTA
+// prologue / drain / epilogue serialisation of k_gemm_tc was the bottleneck).
+// --------------------------------------------------------------------------
+constexpr int kPersThreads = 320;
+template <int BN, int STAGES>
+constexpr int pers_smem_bytes() {
+  return STAGES * (128 * 64 * 2 + BN * 64 * 2) + (2 * STAGES + 4) * 8 + 16 + 1024;
+}
+template <int BN, int STAGES, class Op>
+__global__ void __launch_bounds__(kPersThreads, 1)
+    k_gemm_persistent(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
+  static_assert(has_tma<Op>::value && !has_finish<Op>::value, "persistent GEMM: TMA ops without finish");
+  constexpr int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 256;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = __ldg(prefix + ntask);
+  const int g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
+  const int g1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
+  const uint32_t bar0 = tc::smem_u32(bars);
+  const uint32_t full = bar0, empty = bar0 + 8 * STAGES, acc_full = bar0 + 16 * STAGES, acc_empty = acc_full + 16;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(full + 8 * s, 1);
+      tc::mbar_init(empty + 8 * s, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(acc_full + 8 * i, 1);
+      tc::mbar_init(acc_empty + 8 * i, 8);
+    }
+    tc::mbar_fence_init();
+  }
+  if (warp == 8) tc::tmem_alloc(tc::smem_u32(tmem_slot), TMEM_COLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = tc::smem_u32(smem);
+  TcTile t;
+  TaskCursor cur;
+  cur.init(prefix, ntask, g0 < total ? g0 : total - 1);
+  if (warp == 9) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int it = 0;
+      for (int g = g0; g < g1; ++g) {
+        if (cur.advance(prefix, g) || g == g0) {
+          t.tk = tasks[cur.ti];
+          t.c = op.recs + t.tk.rec;
+        }
+        op.setup(t, g - cur.lo);
+        for (int kb = 0; kb < t.nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) tc::mbar_wait(empty + 8 * s, ((it / STAGES) - 1) & 1);
+          const uint32_t a_base = sbase + s * STAGE;
+          tc::mbar_expect_tx(full + 8 * s, op.tx_bytes(t, kb));
+          op.tma_issue(t, kb, a_base, a_base + A_BYTES, full + 8 * s);
+        }
+      }
+    }
+  } else if (warp == 8) {
+    if (lane == 0 && g0 < g1) {  // ---------------- MMA issuer
+      t.tk = tasks[cur.ti];
+      t.c = op.recs + t.tk.rec;
+      const uint64_t da0 = op.a_desc(t, sbase, 0), dak = op.a_desc(t, sbase, 1) - da0;
+      const uint64_t db0 = op.b_desc(t, sbase + A_BYTES, 0), dbk = op.b_desc(t, sbase + A_BYTES, 1) - db0;
+      int it = 0, i = 0;
+      for (int g = g0; g < g1; ++g, ++i) {
+        if (cur.advance(prefix, g)) {
+          t.tk = tasks[cur.ti];
+          t.c = op.recs + t.tk.rec;
+        }
+        op.setup(t, g - cur.lo);
+        const uint32_t idesc = tc::idesc_bf16(128, t.n_mma, Op::A_MN, Op::B_MN);
+        const int acc = i & 1;
+        if (i >= 2) tc::mbar_wait(acc_empty + 8 * acc, ((i >> 1) - 1) & 1);
+        tc::fence_after();
+        const uint32_t dt = tmem + acc * BN;
+        for (int kb = 0; kb < t.nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          tc::mbar_wait(full + 8 * s, (it / STAGES) & 1);
+          tc::fence_after();
+          const uint64_t so = (uint64_t)(s * (STAGE >> 4));
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            tc::mma_bf16(dt, da0 + so + ks * dak, db0 + so + ks * dbk, idesc, (kb | ks) != 0);
+          tc::commit(empty + 8 * s);
+        }
+        tc::commit(acc_full + 8 * acc);
+      }
+    }
+    __syncwarp();
+  } else {  // ---------------- epilogue warps 0-7
+    const int row = (warp & 3) * 32 + lane;
+    int i = 0;
+    for (int g = g0; g < g1; ++g, ++i) {
+      if (cur.advance(prefix, g) || g == g0) {
+        t.tk = tasks[cur.ti];
+        t.c = op.recs + t.tk.rec;
+      }
+      op.setup(t, g - cur.lo);
+      const int acc = i & 1;
+      tc::mbar_wait(acc_full + 8 * acc, (i >> 1) & 1);
+      tc::fence_after();
+      for (int c0 = (warp >> 2) * 16; c0 < t.n_mma; c0 += 32) {
+        float v[16];
+        tc::tmem_ld16(tmem + acc * BN + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
+        op.epilogue(t, row, c0, v);
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty + 8 * acc);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, TMEM_COLS);
+  }
+  if (threadIdx.x == 0 && g1 > g0) {  // K9: split the CTA's duration over its clients by tile count
+    const uint64_t dt = globaltimer() - t_start;
+    int ti = find_task(prefix, ntask, g0), lo = g0;
+    while (lo < g1) {
+      const int hi = min(g1, __ldg(prefix + ti + 1));
+      const ClientRec* c = op.recs + tasks[ti].rec;
+      if (c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(dt * (hi - lo) / (g1 - g0)));
+      lo = hi;
+      ++ti;
+    }
+  }
+}
+
 __device__ __forceinline__ int round16(int x) { return (x + 15) & ~15; }
 
 // Vectorised epilogue helpers: a thread owns 16 consecutive channels of one pixel.
@@ -549,20 +690,27 @@ struct TcFc1Dgrad {
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
     const int n1 = t.m0 + row;
     const int p = n1 >> W::L2, c = n1 & (W::C2 - 1), py = p >> 3, px = p & 7;
-    const bf16* a2 = (const bf16*)t.c->buf[B_A2];
-    const uint8_t* i2 = (const uint8_t*)t.c->buf[B_I2];
-    bf16* dz2 = (bf16*)t.c->buf[B_DZ2];
+    const bf16* __restrict__ a2 = (const bf16*)t.c->buf[B_A2];
+    const uint8_t* __restrict__ i2 = (const uint8_t*)t.c->buf[B_I2];
+    bf16* __restrict__ dz2 = (bf16*)t.c->buf[B_DZ2];
+    const int nr = t.tk.rows - c0;
+    bf16 am[16];
+    uint8_t ar[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {  // all mask / argmax loads in flight before the first store
+      const int64_t o = (int64_t)(c0 + j) * W::K1 + n1;
+      am[j] = j < nr ? __ldg(a2 + o) : __float2bfloat16_rn(0.f);
+      ar[j] = j < nr ? __ldg(i2 + o) : 0;
+    }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
+      if (j >= nr) continue;
       const int r = c0 + j;
-      if (r >= t.tk.rows) continue;
-      const int64_t o = (int64_t)r * W::K1 + n1;
-      const float val = __bfloat162float(a2[o]) > 0.f ? v[j] : 0.f;
-      const int arg = i2[o];
+      const float val = __bfloat162float(am[j]) > 0.f ? v[j] : 0.f;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int y = 2 * py + (q >> 1), x = 2 * px + (q & 1);
-        dz2[((int64_t)r * 256 + y * 16 + x) * W::C2 + c] = __float2bfloat16_rn(q == arg ? val : 0.f);
+        dz2[((int64_t)r * 256 + y * 16 + x) * W::C2 + c] = __float2bfloat16_rn(q == ar[j] ? val : 0.f);
       }
     }
   }
