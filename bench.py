@@ -302,9 +302,11 @@ def main():
         rnd += 1
         launches += st["kernel_launches"]
         dom_ns += st["op_ns"][dominant]
-        dom_fl += st["op_flops"][dominant]
-        dom_by += st["op_bytes"][dominant]
-        dom_n += st["op_launches"][dominant]
+        # the timed launches and their work (fc1 wgrad launches deferred to the side stream in light
+        # iterations run concurrently with other kernels and are not timed)
+        dom_fl += st["op_timed_flops"][dominant]
+        dom_by += st["op_timed_bytes"][dominant]
+        dom_n += st["op_timed_launches"][dominant]
         profiles = meas  # A3 -> next A4: the latest in-run profile replaces the previous one (reading R7)
     barrier()
     host_s = time.perf_counter() - host_t0

@@ -170,6 +170,11 @@ typedef struct {
   uint64_t op_launches[PROTEA_N_OPC]; /* kernel launches per op class */
   uint64_t op_flops[PROTEA_N_OPC];    /* algorithmic FLOPs per op class (2 x useful MACs) */
   uint64_t op_bytes[PROTEA_N_OPC];    /* algorithmic (compulsory) HBM bytes per op class: operands read once, results written once */
+  /* The launches behind op_ns and their algorithmic work.  Launches deferred to the low-priority side
+   * stream (fc1 wgrad in light iterations, run concurrently with other kernels) are not timed. */
+  uint64_t op_timed_launches[PROTEA_N_OPC];
+  uint64_t op_timed_flops[PROTEA_N_OPC];
+  uint64_t op_timed_bytes[PROTEA_N_OPC];
 } protea_round_stats;
 
 /* Create a context on opts->device.  world > 1 bootstraps an NCCL communicator

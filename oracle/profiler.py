@@ -87,7 +87,8 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
     bf16 mode the slot also holds a bf16 shadow copy of the weights).
     wsp = split-K partials of the conv weight gradients: each conv layer's
     reduction over b*Hout*Wout pixels is cut into ceil(b*Hout*Wout / 2048)
-    splits, each holding cout*(K+1) fp32 partials (the +1 is the bias column).
+    splits, each holding cout*(K+1) fp32 partials (the +1 is the bias column), rows
+    padded to a multiple of 4 floats (16-byte aligned rows, reading R21).
     """
     b, e = batch, elem_bytes
     P = n_params(model, width_q, classes)
@@ -116,7 +117,8 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
         raise ValueError(model)
     convs = conv_layers(model, width_q)
     if convs:
-        out.append(("wsp", 4 * max(math.ceil(b * hw / WGRAD_CHUNK_PX) * co * (K + 1) for hw, co, K in convs)))
+        out.append(("wsp", 4 * max(math.ceil(b * hw / WGRAD_CHUNK_PX) * co * (-(-(K + 1) // 4) * 4)
+                                   for hw, co, K in convs)))
     return out
 
 

@@ -82,7 +82,9 @@ class RoundStats(ctypes.Structure):
     _fields_ = [("round_ns", ctypes.c_uint64), ("iterations", ctypes.c_uint64), ("client_steps", ctypes.c_uint64),
                 ("kernel_launches", ctypes.c_uint64), ("flops", ctypes.c_uint64), ("loss_sum", ctypes.c_double),
                 ("op_ns", ctypes.c_uint64 * N_OPC), ("op_launches", ctypes.c_uint64 * N_OPC),
-                ("op_flops", ctypes.c_uint64 * N_OPC), ("op_bytes", ctypes.c_uint64 * N_OPC)]
+                ("op_flops", ctypes.c_uint64 * N_OPC), ("op_bytes", ctypes.c_uint64 * N_OPC),
+                ("op_timed_launches", ctypes.c_uint64 * N_OPC), ("op_timed_flops", ctypes.c_uint64 * N_OPC),
+                ("op_timed_bytes", ctypes.c_uint64 * N_OPC)]
 
     def as_dict(self):
         d = {}

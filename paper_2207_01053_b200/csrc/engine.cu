@@ -112,6 +112,9 @@ struct protea_ctx {
   std::vector<cudaEvent_t> evpool;
   size_t evused = 0;
   std::vector<int> ev_op;
+  std::vector<std::pair<uint64_t, uint64_t>> ev_work;  // (flops, bytes) of each timed launch
+  const uint64_t* cur_fl = nullptr;                  // per-op work of the launch being issued (Launch::fl/by)
+  const uint64_t* cur_by = nullptr;
   uint64_t op_launches[PROTEA_N_OPC] = {}, op_flops[PROTEA_N_OPC] = {}, op_bytes[PROTEA_N_OPC] = {};
   double loss_host = 0.0;
   // partial-round state (protea_round_partial / protea_round_finalize)
@@ -219,10 +222,11 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
 
 namespace {
 // Bracket one launch of op class `op` with CUDA events if requested.
-int op_begin(protea_ctx* ctx, int op) {
+int op_begin(protea_ctx* ctx, int op, int raw = -1) {  // op: stats class; raw: launch op id (work lookup)
   ctx->op_launches[op]++;
   ctx->launches++;
   if (!((ctx->time_ops >> op) & 1u)) return -1;
+  if (ctx->cur == ctx->side && ctx->side != ctx->stream) return -1;  // concurrent with other kernels: not timed
   while (ctx->evused + 2 > ctx->evpool.size()) {
     cudaEvent_t e;
     if (cudaEventCreate(&e) != cudaSuccess) return -1;
@@ -231,6 +235,7 @@ int op_begin(protea_ctx* ctx, int op) {
   const int i = (int)ctx->evused;
   ctx->evused += 2;
   ctx->ev_op.push_back(op);
+  ctx->ev_work.emplace_back(raw >= 0 && ctx->cur_fl ? ctx->cur_fl[raw] : 0, raw >= 0 && ctx->cur_by ? ctx->cur_by[raw] : 0);
   cudaEventRecord(ctx->evpool[i], ctx->cur);
   return i;
 }
@@ -241,6 +246,7 @@ void reset_ops(protea_ctx* ctx, uint32_t time_ops) {
   ctx->time_ops = time_ops;
   ctx->evused = 0;
   ctx->ev_op.clear();
+  ctx->ev_work.clear();
   for (int i = 0; i < PROTEA_N_OPC; ++i) ctx->op_launches[i] = ctx->op_flops[i] = ctx->op_bytes[i] = 0;
 }
 }  // namespace
@@ -330,7 +336,8 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
       case OP_F1D: return 64 * m.c2 / 128;
       case OP_F1W: return (64 * m.c2 / 128) * cdiv(m.f, 128);
       case OP_C2D: return rows * 2;
-      case OP_C2W: return cdiv(rows * 256, kWgradChunkPx) * cdiv(25 * m.c1 + 1, 128);
+      case OP_C2W:  // width 1: persistent halo kernel, one item per split; else one CTA per (split, M tile)
+        return cdiv(rows * 256, kWgradChunkPx) * (m.width_q == 4 ? 1 : cdiv(25 * m.c1 + 1, 128));
       default: break;
     }
   switch (op) {
@@ -462,13 +469,15 @@ struct Launch {
   int64_t task_off;            // tasks: 4 ints each
   int64_t prefix_off[OP_COUNT];
   int grid[OP_COUNT];
+  int c2w_groups;                       // width-1 conv2 wgrad: M-tile groups per split (1 or 7)
+  uint64_t fl[OP_COUNT], by[OP_COUNT];  // algorithmic work of each op of this launch (op_work)
 };
 
 template <class OpT, int BM, int BN>
 void launch_gemm(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, const int32_t* dtab) {
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int* prefix = dtab + L.prefix_off[opid];
-  const int ev = op_begin(ctx, op_class(opid));
+  const int ev = op_begin(ctx, op_class(opid), opid);
   k_gemm_simt<BM, BN, OpT><<<L.grid[opid], (BM / 4) * (BN / 4), 0, ctx->cur>>>(op, tasks, prefix, L.ntask);
   op_end(ctx, ev);
 }
@@ -483,7 +492,7 @@ void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, c
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int* prefix = dtab + L.prefix_off[opid];
-  const int ev = op_begin(ctx, opid);
+  const int ev = op_begin(ctx, opid, opid);
   k_gemm_tc<BN, STAGES, OpT><<<L.grid[opid], kTcThreads, SMEM, ctx->cur>>>(op, tasks, prefix, L.ntask);
   op_end(ctx, ev);
 }
@@ -501,7 +510,7 @@ void launch_gemm_persistent(protea_ctx* ctx, const OpT& op, const Launch& L, int
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[opid], ctas_per_sm * g_num_sms);
-  const int ev = op_begin(ctx, opid);
+  const int ev = op_begin(ctx, opid, opid);
   k_gemm_persistent<BN, STAGES, OpT><<<grid, kPersThreads, SMEM, ctx->cur>>>(op, tasks, dtab + L.prefix_off[opid],
                                                                                L.ntask);
   op_end(ctx, ev);
@@ -520,7 +529,7 @@ void launch_conv_persistent(protea_ctx* ctx, const ClientRec* drecs, const CnnDi
   op.d = d;
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[opid], g_num_sms);  // one CTA per SM, each a contiguous tile range
-  const int ev = op_begin(ctx, opid);
+  const int ev = op_begin(ctx, opid, opid);
   k_conv_persistent<Op><<<grid, kConvThreads, Op::SMEM, ctx->cur>>>(op, tasks, dtab + L.prefix_off[opid], L.ntask);
   op_end(ctx, ev);
 }
@@ -533,8 +542,23 @@ void launch_conv1_wgrad_q(protea_ctx* ctx, const ClientRec* drecs, const Launch&
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[OP_C1W], g_num_sms);
-  const int ev = op_begin(ctx, OP_C1W);
+  const int ev = op_begin(ctx, OP_C1W, OP_C1W);
   k_conv1_wgrad_q<<<grid, kConvThreads, kW1Smem, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1W], L.ntask);
+  op_end(ctx, ev);
+}
+
+void launch_conv2_wgrad_halo(protea_ctx* ctx, const ClientRec* drecs, const CnnDims& d, const Launch& L,
+                             const int32_t* dtab, float lr) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_conv2_wgrad_halo, cudaFuncAttributeMaxDynamicSharedMemorySize, kW2Smem);
+    attr = true;
+  }
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const int grid = std::min(L.grid[OP_C2W], g_num_sms);
+  const int ev = op_begin(ctx, OP_C2W, OP_C2W);
+  k_conv2_wgrad_halo<<<grid, kConvThreads, kW2Smem, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C2W], L.ntask,
+                                                                   d, lr, L.c2w_groups);
   op_end(ctx, ev);
 }
 
@@ -549,7 +573,7 @@ void launch_head_cnn(protea_ctx* ctx, const ModelDims& m, const Launch& L, const
     attr = true;
   }
   HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
-  const int ev = op_begin(ctx, OP_HEAD);
+  const int ev = op_begin(ctx, OP_HEAD, OP_HEAD);
   k_head_cnn<T><<<L.ntask, kHeadCnnThreads, smem, ctx->cur>>>(ha, tasks);
   op_end(ctx, ev);
 }
@@ -575,7 +599,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   typedef __nv_bfloat16 T;
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const CnnDims d = cnn_dims(m);
-  int ev = op_begin(ctx, OP_STAGE);
+  int ev = op_begin(ctx, OP_STAGE, OP_STAGE);
   k_stage_x<<<L.grid[OP_STAGE], kStageThreads, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_STAGE],
                                                                   L.ntask);
   op_end(ctx, ev);
@@ -606,7 +630,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   }
   launch_conv_persistent<HaloConv2<WQ, true>>(ctx, drecs, d, L, OP_C2D, dtab);
   if constexpr (WQ == 4)
-    launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2WgradSW>(drecs, d, lr), L, OP_C2W, dtab);
+    launch_conv2_wgrad_halo(ctx, drecs, d, L, dtab, lr);
   else
     launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2Wgrad<WQ>>(drecs, d, lr), L, OP_C2W, dtab);
 
@@ -614,7 +638,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
     launch_conv1_wgrad_q(ctx, drecs, L, dtab);
   else
     launch_gemm_tc<TC_C1W_BN, TC_STAGES>(ctx, TcConv1Wgrad<WQ>{drecs, d}, L, OP_C1W, dtab);
-  ev = op_begin(ctx, OP_C1R);
+  ev = op_begin(ctx, OP_C1R, OP_C1R);
   k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
                                                                        L.ntask, m.c1, d.w1, d.b1, lr);
   op_end(ctx, ev);
@@ -671,7 +695,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
   }
   const Layer& fc = m.layers[7];
   RHeadArgs ha{drecs, m.classes, fc.off_w, fc.off_b, lr};
-  int ev = op_begin(ctx, PROTEA_OPC_R_HEAD);
+  int ev = op_begin(ctx, PROTEA_OPC_R_HEAD, RI_HEAD);
   k_rhead<T><<<L.ntask, 256, 0, ctx->cur>>>(ha, tasks);
   op_end(ctx, ev);
   // backward, layer 6 (b3b) down to 1 (b1a): dgrad (dout, out, mask, add), then wgrad + reduce
@@ -706,7 +730,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
     wg.in_buf = in_of[i];
     launch_gemm<Wg, R_BM, R_BN>(ctx, wg, L, RI_W0 + i, dtab);
     ReduceArgs ra{drecs, B_R_WSP, l.cout, 9 * l.cin, l.off_w, l.off_b, l.hout * l.wout, lr, 0};
-    ev = op_begin(ctx, PROTEA_OPC_R_REDUCE);
+    ev = op_begin(ctx, PROTEA_OPC_R_REDUCE, RI_R0 + i);
     k_reduce_update<<<L.grid[RI_R0 + i], kReduceBlock, 0, ctx->cur>>>(ra, tasks, dtab + L.prefix_off[RI_R0 + i],
                                                                          L.ntask);
     op_end(ctx, ev);
@@ -733,13 +757,13 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Conv2Dgrad<T, C2D_BM, C2D_BN>, C2D_BM, C2D_BN>(ctx, {drecs, d}, L, OP_C2D, dtab);
     launch_gemm<Conv2Wgrad<T, C2W_BM, C2W_BN>, C2W_BM, C2W_BN>(ctx, {drecs, d}, L, OP_C2W, dtab);
     ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr, 0};
-    ev = op_begin(ctx, OP_C2R);
+    ev = op_begin(ctx, OP_C2R, OP_C2R);
     k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->cur>>>(r2, tasks, dtab + L.prefix_off[OP_C2R],
                                                                        L.ntask);
     op_end(ctx, ev);
     launch_gemm<Conv1Wgrad<T, C1W_BM, C1W_BN>, C1W_BM, C1W_BN>(ctx, {drecs, d}, L, OP_C1W, dtab);
     ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr, 0};
-    ev = op_begin(ctx, OP_C1R);
+    ev = op_begin(ctx, OP_C1R, OP_C1R);
     k_reduce_update<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(r1, tasks, dtab + L.prefix_off[OP_C1R],
                                                                        L.ntask);
     op_end(ctx, ev);
@@ -747,7 +771,7 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     const MlpDims d = mlp_dims(m);
     launch_gemm<MlpFc1Fwd<T, MF_BM, MF_BN>, MF_BM, MF_BN>(ctx, {drecs, d}, L, OP_MF, dtab);
     HeadArgs ha{drecs, B_H1, B_DZ1, 64, m.classes, d.w2, d.b2, d.b1, lr};
-    const int ev = op_begin(ctx, OP_MHEAD);
+    const int ev = op_begin(ctx, OP_MHEAD, OP_MHEAD);
     k_head<T><<<L.ntask, kHeadThreads, 0, ctx->cur>>>(ha, tasks);
     op_end(ctx, ev);
     launch_gemm<MlpFc1Wgrad<T, MW_BM, MW_BN>, MW_BM, MW_BN>(ctx, {drecs, d, lr}, L, OP_MW, dtab);
@@ -1066,16 +1090,26 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
           tab.push_back(rows[i]);
           tab.push_back((int32_t)((int64_t)ep * c.n + (int64_t)j * c.B));
         }
+        // width-1 conv2 wgrad: when the iteration has few splits (the tail), each split's 7 M tiles become
+        // 7 work items (no extra partials: disjoint outputs), otherwise one item covers all 7 tiles
+        L.c2w_groups = 1;
+        if (tc_mode && m.arch == PROTEA_MODEL_CNN && m.width_q == 4) {
+          int64_t nsplit = 0;
+          for (int r : rows) nsplit += cdiv(r * 256, kWgradChunkPx);
+          if (nsplit < 2 * g_num_sms) L.c2w_groups = 7;
+        }
         for (int op : ops_of(m, tc_mode)) {
           L.prefix_off[op] = (int64_t)tab.size();
           int acc_t = 0;
           for (size_t i = 0; i < act.size(); ++i) {
             tab.push_back(acc_t);
-            acc_t += tiles(m, op, rows[i], tc_mode);
+            acc_t += tiles(m, op, rows[i], tc_mode) * (op == OP_C2W ? L.c2w_groups : 1);
             uint64_t fl, by;
             op_work(m, op, (uint64_t)rows[i], (uint64_t)e, &fl, &by);
             ctx->op_flops[op_class(op)] += fl;
             ctx->op_bytes[op_class(op)] += by;
+            L.fl[op] += fl;
+            L.by[op] += by;
           }
           tab.push_back(acc_t);
           L.grid[op] = acc_t;
@@ -1141,6 +1175,8 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     for (int li : launch_idx[t]) {
       const Launch& L = launches[li];
       const ModelDims& m = ctx->groups[L.group].m;
+      ctx->cur_fl = L.fl;
+      ctx->cur_by = L.by;
       if (e == 4)
         launch_step<float>(ctx, m, L, drecs, dtab, lr);
       else if (m.arch == PROTEA_MODEL_CNN)
@@ -1162,6 +1198,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
   }
   for (int g = 0; g < G; ++g) join_group(ctx, g);
   ctx->overlap_now = false;
+  ctx->cur_fl = ctx->cur_by = nullptr;
   CK(cudaEventRecord(ctx->join_ev, ctx->hi));
   CK(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   ctx->cur = ctx->stream;
@@ -1334,6 +1371,9 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
       float ems = 0.f;
       CK(cudaEventElapsedTime(&ems, ctx->evpool[2 * k], ctx->evpool[2 * k + 1]));
       stats->op_ns[ctx->ev_op[k]] += (uint64_t)((double)ems * 1e6);
+      stats->op_timed_launches[ctx->ev_op[k]]++;
+      stats->op_timed_flops[ctx->ev_op[k]] += ctx->ev_work[k].first;
+      stats->op_timed_bytes[ctx->ev_op[k]] += ctx->ev_work[k].second;
     }
     for (auto& c : all) {
       stats->client_steps += c.S;

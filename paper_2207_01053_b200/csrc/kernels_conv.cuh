@@ -605,4 +605,249 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// conv2 wgrad (width 1: C1 = 32, C2 = 64) + SGD, halo form.  D[m = (tap, ci)][co] =
+// sum_p a1[p + tap][ci] dz2[p][co] over the client's output pixels p, with ALL 7
+// M tiles (800 weights + bias row) accumulating in TMEM at once (7 x 64 columns):
+// per half image the a1 halo is loaded ONCE as 5 x-shifted copies (the conv2
+// fwd's 64-byte-swizzled boxes) and every tap's A operand is a descriptor into
+// them (MN-major SW64, one 32-channel atom per tap), instead of re-gathering
+// each tap from L2 per M tile.  M tiles: j < 5 = taps (ky 0..3, kx = j) at
+// LBO = one halo row; 5 = taps (4, kx 0..3) at LBO = one copy; 6 = tap (4, 4) +
+// the bias "ones" block (a constant copy-shaped region after copy 4).
+// Work item = (client, split of 8 images = kWgradChunkPx pixels[, M tile]): with
+// ng = 7 (light iterations) each M tile of a split is its own item and loads
+// only the halo copies it reads.  A client whose batch is one split updates
+// the weights straight from TMEM; otherwise every item stores its rows of the
+// split's partial [C2][804] and the client's last item (counter stats[8]) sums
+// them in split order and applies SGD to the fp32 master and the bf16 shadow.
+// Persistent: one CTA per SM, contiguous item ranges.
+// ---------------------------------------------------------------------------
+constexpr int kW2Copy = 12 * 16 * 64;                    // [12 rows][16 px][32 ci] bf16, 64-byte swizzle
+constexpr int kW2Dz = 128 * 128;                         // dz2 half image [128 px][64 co] bf16, 128-byte swizzle
+constexpr int kW2Stage = 6 * kW2Copy + kW2Dz;           // 5 copies + ones block + dz2 = 88 KB
+constexpr int kW2Pad = 8192;  // M tile 6's unused atoms 2-3 read (ignored rows) up to 7.5 KB past the last stage
+constexpr int kW2Smem = 2 * kW2Stage + kW2Pad + 256 + 1024;
+constexpr int kW2N = 25 * 32 + 1;                        // weight rows + bias row
+constexpr int kW2NP = 804;                               // partial row stride (float4-aligned)
+
+__device__ __forceinline__ int w2_row(int j, int row) {  // weight row of TMEM lane `row` in M tile j (-1: none)
+  const int atom = row >> 5, ci = row & 31;
+  if (j < 5) return (atom * 5 + j) * 32 + ci;
+  if (j == 5) return (20 + atom) * 32 + ci;
+  if (atom == 0) return 24 * 32 + ci;
+  return (atom == 1 && ci == 0) ? 800 : -1;
+}
+
+__global__ void __launch_bounds__(kConvThreads, 1)
+    k_conv2_wgrad_halo(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks,
+                       const int* __restrict__ prefix, int ntask, CnnDims d, float lr, int ng) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kW2Stage + kW2Pad);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = __ldg(prefix + ntask);
+  const int g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
+  const int g1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
+  const uint32_t bar0 = tc::smem_u32(bars);
+  const uint32_t full = bar0, empty = bar0 + 16, acc_full = bar0 + 32, acc_empty = bar0 + 40;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(full + 8 * i, 1);
+      tc::mbar_init(empty + 8 * i, 1);
+    }
+    tc::mbar_init(acc_full, 1);
+    tc::mbar_init(acc_empty, 8);
+    tc::mbar_fence_init();
+  }
+  // the bias "ones" block of each stage: 1.0 at channel 0 of every pixel row (64-byte swizzle:
+  // row r of a 512-byte atom keeps logical 16-byte chunk c at physical chunk c ^ ((r >> 1) & 3))
+  for (int i = threadIdx.x; i < 2 * kW2Copy / 16; i += blockDim.x) {
+    const int st = i / (kW2Copy / 16), k = i - st * (kW2Copy / 16), r = k >> 2, c = k & 3;
+    reinterpret_cast<uint4*>(smem + st * kW2Stage + 5 * kW2Copy)[k] =
+        c == ((r >> 1) & 3) ? make_uint4(0x3F80u, 0, 0, 0) : make_uint4(0, 0, 0, 0);
+  }
+  tc::fence_proxy_async();
+  if (warp == 9) tc::tmem_alloc(tc::smem_u32(tmem_slot), 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sb = tc::smem_u32(smem);
+  TaskCursor cur;
+  cur.init(prefix, ntask, g0 < total ? g0 : total - 1);
+
+  if (warp == 8) {
+    if (lane == 0) {  // ---------------- TMA producer: per half image, 5 halo copies + 2 dz2 boxes
+      TcTile t;
+      int s = 0;
+      for (int g = g0; g < g1; ++g) {
+        if (cur.advance(prefix, g) || g == g0) {
+          t.tk = tasks[cur.ti];
+          t.c = recs + t.tk.rec;
+        }
+        const int item = g - cur.lo, grp = item % ng, r0 = 8 * (item / ng), nsub = 2 * min(8, t.tk.rows - r0);
+        // halo copies read by the item's M tiles: all (ng = 1); tile j < 5: copy j; 5: copies 0-3; 6: copy 4
+        const int need = ng == 1 ? 0x1F : grp < 5 ? 1 << grp : grp == 5 ? 0xF : 0x10;
+        const uint32_t tx = __popc(need) * kW2Copy + kW2Dz;
+        for (int sub = 0; sub < nsub; ++sub, ++s) {
+          const int buf = s & 1, r = r0 + (sub >> 1), y0 = 8 * (sub & 1);
+          const uint32_t base = sb + buf * kW2Stage;
+          if (s >= 2) tc::mbar_wait(empty + 8 * buf, ((s >> 1) - 1) & 1);
+          tc::mbar_expect_tx(full + 8 * buf, tx);
+          for (int kx = 0; kx < 5; ++kx)
+            if ((need >> kx) & 1)
+              tc::tma_load_4d(base + kx * kW2Copy, tmap_of(t, TM_A1H), full + 8 * buf, 0, kx - 2, y0 - 2, r);
+          for (int h = 0; h < 2; ++h)
+            tc::tma_load_4d(base + 6 * kW2Copy + h * (kW2Dz / 2), tmap_of(t, TM_DZ2WS), full + 8 * buf, 0, 0,
+                            y0 + 4 * h, r);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {  // ---------------- MMA issuer: 8 K steps (output rows) x 7 M tiles per half image
+      const uint32_t idesc = tc::idesc_bf16(128, 64, true, true);
+      const uint64_t a_kx = tc::sdesc_sw64(sb, 1024, 512), a_k4 = tc::sdesc_sw64(sb, kW2Copy, 512);
+      const uint64_t b0 = tc::sdesc_sw128(sb + 6 * kW2Copy, 16, 1024);
+      int s = 0, i = 0;
+      for (int g = g0; g < g1; ++g, ++i) {
+        cur.advance(prefix, g);
+        const int item = g - cur.lo, grp = item % ng, r0 = 8 * (item / ng);
+        const int nsub = 2 * min(8, __ldg(&tasks[cur.ti].rows) - r0);
+        if (i >= 1) tc::mbar_wait(acc_empty, (i - 1) & 1);
+        tc::fence_after();
+        for (int sub = 0; sub < nsub; ++sub, ++s) {
+          const int buf = s & 1;
+          const uint32_t so = buf * kW2Stage;
+          tc::mbar_wait(full + 8 * buf, (s >> 1) & 1);
+          tc::fence_after();
+          if (ng == 1) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+              const uint64_t db = tc::dadd(b0, so + 2048 * ks);
+              const uint32_t acc = (sub | ks) != 0;
+#pragma unroll
+              for (int j = 0; j < 5; ++j)
+                tc::mma_bf16(tmem + 64 * j, tc::dadd(a_kx, so + j * kW2Copy + ks * 1024), db, idesc, acc);
+              tc::mma_bf16(tmem + 64 * 5, tc::dadd(a_k4, so + (ks + 4) * 1024), db, idesc, acc);
+              tc::mma_bf16(tmem + 64 * 6, tc::dadd(a_k4, so + 4 * kW2Copy + (ks + 4) * 1024), db, idesc, acc);
+            }
+          } else {  // one M tile
+            const uint64_t a = grp < 5 ? tc::dadd(a_kx, so + grp * kW2Copy)
+                                       : tc::dadd(a_k4, so + (grp == 5 ? 0 : 4 * kW2Copy) + 4 * 1024);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              tc::mma_bf16(tmem + 64 * grp, tc::dadd(a, ks * 1024), tc::dadd(b0, so + 2048 * ks), idesc,
+                           (sub | ks) != 0);
+          }
+          tc::commit(empty + 8 * buf);
+        }
+        tc::commit(acc_full);
+      }
+    }
+    __syncwarp();
+  } else {  // ---------------- epilogue warps 0-7: lanes (warp % 4) * 32.., columns 32 (warp / 4)..
+    const int row = (warp & 3) * 32 + lane, cb = (warp >> 2) * 32;
+    const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const int Kw = 800;
+    int i = 0;
+    for (int g = g0; g < g1; ++g, ++i) {
+      cur.advance(prefix, g);
+      const Task tk = tasks[cur.ti];
+      const ClientRec* c = recs + tk.rec;
+      const int item = g - cur.lo, split = item / ng, grp = item % ng, splits = (tk.rows + 7) / 8;
+      float* P = c->params;
+      bf16* S = (bf16*)c->buf[B_WSH];
+      float* part = (float*)c->buf[B_WSP] + (int64_t)split * 64 * kW2NP;
+      tc::mbar_wait(acc_full, i & 1);
+      tc::fence_after();
+#pragma unroll 1
+      for (int j = ng == 1 ? 0 : grp; j < (ng == 1 ? 7 : grp + 1); ++j) {
+        float v[32];
+        tc::tmem_ld16(ta + 64 * j + cb, *reinterpret_cast<float(*)[16]>(v));
+        tc::tmem_ld16(ta + 64 * j + cb + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+        const int m = w2_row(j, row);
+        if (m < 0) continue;
+        if (splits == 1) {  // whole batch in this item: SGD straight from the accumulator
+          if (m == Kw) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) P[d.b2 + cb + q] -= lr * v[q];
+          } else {
+            float w[32];
+#pragma unroll
+            for (int q = 0; q < 32; ++q) w[q] = P[d.w2 + (int64_t)(cb + q) * Kw + m];
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              const int64_t idx = d.w2 + (int64_t)(cb + q) * Kw + m;
+              const float nw = w[q] - lr * v[q];
+              P[idx] = nw;
+              S[idx] = __float2bfloat16_rn(nw);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) part[(int64_t)(cb + q) * kW2NP + m] = v[q];
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty);  // TMEM drained: the next item's MMAs may start
+      if (splits > 1) {  // the last split of the client reduces in split order and applies SGD
+        int* cnt = reinterpret_cast<int*>(c->stats) + 8;
+        __threadfence();
+        tc::named_sync(1, 256);
+        if (threadIdx.x == 0) *last_flag = atomicAdd(cnt, 1) == splits * ng - 1;
+        tc::named_sync(1, 256);
+        if (*last_flag) {
+          __threadfence();
+          // float4 over m (row stride 804), all splits' loads of a chunk in flight together
+          const float4* pt = (const float4*)c->buf[B_WSP];
+          constexpr int Q = kW2NP / 4;  // float4 per co row
+          for (int e = threadIdx.x; e < 64 * Q; e += 256) {
+            const int co = e / Q, m0 = 4 * (e - co * Q);
+            float4 gs = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int sp = 0; sp < splits; ++sp) {
+              const float4 p = __ldcg(pt + (int64_t)sp * 64 * Q + e);
+              gs.x += p.x, gs.y += p.y, gs.z += p.z, gs.w += p.w;
+            }
+            if (m0 < Kw) {
+              const int64_t idx = d.w2 + (int64_t)co * Kw + m0;
+              float4 w = *reinterpret_cast<const float4*>(P + idx);
+              w.x -= lr * gs.x, w.y -= lr * gs.y, w.z -= lr * gs.z, w.w -= lr * gs.w;
+              *reinterpret_cast<float4*>(P + idx) = w;
+              const __nv_bfloat162 h0 = __floats2bfloat162_rn(w.x, w.y), h1 = __floats2bfloat162_rn(w.z, w.w);
+              *reinterpret_cast<uint2*>(S + idx) =
+                  make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+            } else if (m0 == Kw) {
+              P[d.b2 + co] -= lr * gs.x;
+            }
+          }
+          if (threadIdx.x == 0) *cnt = 0;
+        }
+        tc::named_sync(1, 256);
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+  if (threadIdx.x == 0 && g1 > g0) {  // K9: split this CTA's duration over its clients by item count
+    const uint64_t dt = globaltimer() - t_start;
+    int ti = find_task(prefix, ntask, g0), lo = g0;
+    while (lo < g1) {
+      const int hi = min(g1, __ldg(prefix + ti + 1));
+      const ClientRec* c = recs + tasks[ti].rec;
+      if (c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(dt * (hi - lo) / (g1 - g0)));
+      lo = hi;
+      ++ti;
+    }
+  }
+}
+
 }  // namespace protea

@@ -152,7 +152,8 @@ SlotLayout slot_layout(const ModelDims& m, int b, int64_t n, int epochs, int e) 
   }
   uint64_t wsp = 0;
   for (const Layer& l : m.layers)
-    if (l.kind == 0) wsp = std::max<uint64_t>(wsp, 4ull * splits_for(l, b) * l.cout * (l.K() + 1));
+    if (l.kind == 0)  // rows of K+1 partials padded to a multiple of 4 floats (16-byte aligned)
+      wsp = std::max<uint64_t>(wsp, 4ull * splits_for(l, b) * l.cout * ((l.K() + 1 + 3) / 4 * 4));
   if (wsp) put(m.arch == PROTEA_MODEL_RESNET8 ? B_R_WSP : B_WSP, wsp);
   // slot order = enum order except that the wgrad partials come last (oracle order)
   uint64_t off = 0;
