@@ -33,7 +33,8 @@ def build(force=False, verbose=False):
     if not force and up_to_date():
         return OUT
     nd = nccl_dir()
-    cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+    dbg = ["-DPROTEA_DBG=1"] if os.environ.get("PROTEA_DBG") == "1" else []  # kernel cycle counters (tools)
+    cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", *dbg,
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
            *sources(), "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",

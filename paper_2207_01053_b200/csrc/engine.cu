@@ -797,6 +797,16 @@ bool is_device_ptr(const void* p) {
 // C ABI
 // ---------------------------------------------------------------------------
 extern "C" {
+// Debug cycle counters of instrumented kernels (built with -DPROTEA_DBG=1); not part of the public ABI.
+int protea_debug_counters(uint64_t* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, protea::g_dbg, 64 * sizeof(uint64_t)) != cudaSuccess) return -1;
+  if (reset) {
+    const uint64_t z[64] = {};
+    cudaMemcpyToSymbol(protea::g_dbg, z, sizeof(z));
+  }
+  return 0;
+}
+
 
 const char* protea_last_error(const protea_ctx* ctx) {
   if (ctx) return ctx->err.c_str();

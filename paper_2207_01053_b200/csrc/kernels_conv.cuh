@@ -22,6 +22,15 @@
 
 namespace protea {
 
+#ifndef PROTEA_DBG
+#define PROTEA_DBG 0
+#endif
+__device__ unsigned long long g_dbg[64];  // PROTEA_DBG cycle counters (protea_debug_counters)
+#define DBG_T0(v) const long long v = PROTEA_DBG ? clock64() : 0
+#define DBG_ADD(i, v) \
+  if (PROTEA_DBG && (threadIdx.x & 31) == 0) atomicAdd(&g_dbg[i], (unsigned long long)(clock64() - (v)))
+
+
 constexpr int kConvThreads = 320;
 // dgrad epilogue operands: loaded one tile ahead (true) or at the start of the tile's epilogue,
 // before its accumulator wait (false).  Measured on B200: the one-tile-ahead variant was slower.
@@ -59,6 +68,7 @@ struct HaloConv2 {
   static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
   static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256 + 1024;  // + realignment slack
   static constexpr int TILES_PER_IMAGE = 2;
+  static constexpr int DBG = DGRAD ? 32 : 16;
   const ClientRec* recs;
   CnnDims d;
 
@@ -98,7 +108,7 @@ struct HaloConv2 {
           const uint32_t ao = G::SW64 ? kx * 4 * G::COPY + row0 * 1024 + 32 * cp
                                       : (kx * G::NCC + 2 * cp) * G::COPY + row0 * 256;
           const uint32_t bo = !DGRAD ? (tap * (W::C1 / 8) + 2 * cp) * N * 16 : tap * (N / 8) * W::C2 * 16 + cp * 256;
-          tc::mma_bf16(dt, tc::dadd(a0, ao), tc::dadd(b0, bo), idesc, (grp | tap | cp) != 0);
+          tc::mma_bf16_w(dt, tc::dadd(a0, ao), tc::dadd(b0, bo), idesc, (grp | tap | cp) != 0);
         }
       }
   }
@@ -228,6 +238,7 @@ struct QuadConv1 {
   static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256 + 1024;
   static constexpr int TILES_PER_IMAGE = 2;
   static constexpr int NCO = W::C1 >= 32 ? 16 : W::C1;  // channels per epilogue thread
+  static constexpr int DBG = 48;
   const ClientRec* recs;
   CnnDims d;
 
@@ -244,7 +255,7 @@ struct QuadConv1 {
     for (int dy = 0; dy < 6; ++dy)
 #pragma unroll
       for (int dp = 0; dp < 3; ++dp)
-        tc::mma_bf16(dt, tc::dadd(a0, dy * 320 + dp * 16), tc::dadd(b0, (dy * 3 + dp) * 2 * N * 16), idesc,
+        tc::mma_bf16_w(dt, tc::dadd(a0, dy * 320 + dp * 16), tc::dadd(b0, (dy * 3 + dp) * 2 * N * 16), idesc,
                      (dy | dp) != 0);
   }
   struct EpiState {
@@ -314,6 +325,7 @@ __device__ __forceinline__ int next_task(const int* __restrict__ prefix, int nta
 template <class Op>
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv_persistent(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
+  constexpr int D0 = Op::DBG;  // PROTEA_DBG counter block
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sH = smem + Op::B_BYTES;
@@ -367,36 +379,46 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int tile = g - cur.lo;
         for (int grp = 0; grp < Op::GROUPS; ++grp, ++s) {
           const int buf = s & 1;
+          DBG_T0(tw);
           if (s >= 2) tc::mbar_wait(h_empty + 8 * buf, ((s >> 1) - 1) & 1);
+          DBG_ADD(D0 + 0, tw);
+          DBG_T0(ti);
           tc::mbar_expect_tx(h_full + 8 * buf, Op::HBYTES);
           op.load_halo(t, tile, grp, sh + buf * Op::HBYTES, h_full + 8 * buf);
+          DBG_ADD(D0 + 1, ti);
         }
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    {  // ---------------- MMA issuer (whole warp, elected lane issues)
       const uint32_t idesc = tc::idesc_bf16(128, Op::N, false, Op::B_MN);
       TaskCursor cur;
       cur.init(prefix, ntask, g0);
       int nb = 0, s = 0, i = 0;
       for (int g = g0; g < g1; ++g, ++i) {
         if (cur.advance(prefix, g) || g == g0) {
-          if (nb > 0) tc::commit(b_empty);  // completes when every MMA issued so far (old weights) is done
+          if (nb > 0) tc::commit_w(b_empty);  // completes when every MMA issued so far (old weights) is done
           tc::mbar_wait(b_full, nb & 1);
           tc::fence_after();
           ++nb;
         }
         const int acc = i & 1;
+        DBG_T0(ta0);
         if (i >= 2) tc::mbar_wait(acc_empty + 8 * acc, ((i >> 1) - 1) & 1);
+        DBG_ADD(D0 + 2, ta0);
         tc::fence_after();
         for (int grp = 0; grp < Op::GROUPS; ++grp, ++s) {
           const int buf = s & 1;
+          DBG_T0(tf);
           tc::mbar_wait(h_full + 8 * buf, (s >> 1) & 1);
+          DBG_ADD(D0 + 3, tf);
+          DBG_T0(tm);
           tc::fence_after();
           op.mma_stage(sh + buf * Op::HBYTES, sb, tmem + acc * Op::N, grp, idesc);
-          tc::commit(h_empty + 8 * buf);
+          tc::commit_w(h_empty + 8 * buf);
+          DBG_ADD(D0 + 4, tm);
         }
-        tc::commit(acc_full + 8 * acc);
+        tc::commit_w(acc_full + 8 * acc);
       }
     }
     __syncwarp();
@@ -420,7 +442,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (kCrossTilePrefetch) op.prefetch(tn, g + 1 - nxt.lo, warp, lane, pn);
       }
       const int acc = i & 1;
+      DBG_T0(te);
       op.epilogue(t, g - cur.lo, tmem + acc * Op::N, acc_full + 8 * acc, (i >> 1) & 1, warp, lane, st, pc);
+      if (warp == 0) DBG_ADD(D0 + 5, te);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(acc_empty + 8 * acc);
@@ -435,6 +459,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     tc::fence_after();
     tc::tmem_dealloc(tmem, Op::TMEM_COLS);
   }
+  if (PROTEA_DBG && threadIdx.x == 0) atomicAdd(&g_dbg[D0 + 8], (unsigned long long)(globaltimer() - t_start));
   if (threadIdx.x == 0 && g1 > g0) {  // K9: split this CTA's duration over its clients by tile count
     const uint64_t dt = globaltimer() - t_start;
     int ti = ti0, lo = g0;
@@ -527,7 +552,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    {  // ---------------- MMA issuer (whole warp, elected lane issues)
       const uint32_t idesc = tc::idesc_bf16(128, 48, true, true);
       int ti = ti0, s = 0, i = 0;
       for (int g = g0; g < g1; ++g, ++i) {
@@ -545,11 +570,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
             for (int dy = 0; dy < 6; ++dy)
-              tc::mma_bf16(tmem + dy * 48, tc::dadd(a0, 2048 * ks), tc::dadd(b0, (4 * ks + dy) * 128), idesc,
+              tc::mma_bf16_w(tmem + dy * 48, tc::dadd(a0, 2048 * ks), tc::dadd(b0, (4 * ks + dy) * 128), idesc,
                            (sub | ks) != 0);
-          tc::commit(empty + 8 * buf);
+          tc::commit_w(empty + 8 * buf);
         }
-        tc::commit(acc_full);
+        tc::commit_w(acc_full);
       }
     }
     __syncwarp();
@@ -696,7 +721,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         for (int sub = 0; sub < nsub; ++sub, ++s) {
           const int buf = s & 1, r = r0 + (sub >> 1), y0 = 8 * (sub & 1);
           const uint32_t base = sb + buf * kW2Stage;
+          DBG_T0(tw);
           if (s >= 2) tc::mbar_wait(empty + 8 * buf, ((s >> 1) - 1) & 1);
+          DBG_ADD(0, tw);
+          DBG_T0(ti);
           tc::mbar_expect_tx(full + 8 * buf, tx);
           for (int kx = 0; kx < 5; ++kx)
             if ((need >> kx) & 1)
@@ -704,11 +732,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           for (int h = 0; h < 2; ++h)
             tc::tma_load_4d(base + 6 * kW2Copy + h * (kW2Dz / 2), tmap_of(t, TM_DZ2WS), full + 8 * buf, 0, 0,
                             y0 + 4 * h, r);
+          DBG_ADD(1, ti);
         }
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {  // ---------------- MMA issuer: 8 K steps (output rows) x 7 M tiles per half image
+    {  // ---------------- MMA issuer (whole warp, elected lane issues): 8 K steps x 7 M tiles per half image
       const uint32_t idesc = tc::idesc_bf16(128, 64, true, true);
       const uint64_t a_kx = tc::sdesc_sw64(sb, 1024, 512), a_k4 = tc::sdesc_sw64(sb, kW2Copy, 512);
       const uint64_t b0 = tc::sdesc_sw128(sb + 6 * kW2Copy, 16, 1024);
@@ -717,12 +746,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         cur.advance(prefix, g);
         const int item = g - cur.lo, grp = item % ng, r0 = 8 * (item / ng);
         const int nsub = 2 * min(8, __ldg(&tasks[cur.ti].rows) - r0);
+        DBG_T0(ta0);
         if (i >= 1) tc::mbar_wait(acc_empty, (i - 1) & 1);
+        DBG_ADD(2, ta0);
         tc::fence_after();
         for (int sub = 0; sub < nsub; ++sub, ++s) {
           const int buf = s & 1;
           const uint32_t so = buf * kW2Stage;
+          DBG_T0(tf);
           tc::mbar_wait(full + 8 * buf, (s >> 1) & 1);
+          DBG_ADD(3, tf);
+          DBG_T0(tm);
           tc::fence_after();
           if (ng == 1) {
 #pragma unroll
@@ -731,21 +765,22 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               const uint32_t acc = (sub | ks) != 0;
 #pragma unroll
               for (int j = 0; j < 5; ++j)
-                tc::mma_bf16(tmem + 64 * j, tc::dadd(a_kx, so + j * kW2Copy + ks * 1024), db, idesc, acc);
-              tc::mma_bf16(tmem + 64 * 5, tc::dadd(a_k4, so + (ks + 4) * 1024), db, idesc, acc);
-              tc::mma_bf16(tmem + 64 * 6, tc::dadd(a_k4, so + 4 * kW2Copy + (ks + 4) * 1024), db, idesc, acc);
+                tc::mma_bf16_w(tmem + 64 * j, tc::dadd(a_kx, so + j * kW2Copy + ks * 1024), db, idesc, acc);
+              tc::mma_bf16_w(tmem + 64 * 5, tc::dadd(a_k4, so + (ks + 4) * 1024), db, idesc, acc);
+              tc::mma_bf16_w(tmem + 64 * 6, tc::dadd(a_k4, so + 4 * kW2Copy + (ks + 4) * 1024), db, idesc, acc);
             }
           } else {  // one M tile
             const uint64_t a = grp < 5 ? tc::dadd(a_kx, so + grp * kW2Copy)
                                        : tc::dadd(a_k4, so + (grp == 5 ? 0 : 4 * kW2Copy) + 4 * 1024);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
-              tc::mma_bf16(tmem + 64 * grp, tc::dadd(a, ks * 1024), tc::dadd(b0, so + 2048 * ks), idesc,
+              tc::mma_bf16_w(tmem + 64 * grp, tc::dadd(a, ks * 1024), tc::dadd(b0, so + 2048 * ks), idesc,
                            (sub | ks) != 0);
           }
-          tc::commit(empty + 8 * buf);
+          tc::commit_w(empty + 8 * buf);
+          DBG_ADD(4, tm);
         }
-        tc::commit(acc_full);
+        tc::commit_w(acc_full);
       }
     }
     __syncwarp();
@@ -762,8 +797,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       float* P = c->params;
       bf16* S = (bf16*)c->buf[B_WSH];
       float* part = (float*)c->buf[B_WSP] + (int64_t)split * 64 * kW2NP;
+      DBG_T0(te);
       tc::mbar_wait(acc_full, i & 1);
-      tc::fence_after();
+      if (warp == 0) DBG_ADD(5, te);
+      DBG_T0(td);
 #pragma unroll 1
       for (int j = ng == 1 ? 0 : grp; j < (ng == 1 ? 7 : grp + 1); ++j) {
         float v[32];
@@ -795,6 +832,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(acc_empty);  // TMEM drained: the next item's MMAs may start
+      if (warp == 0) DBG_ADD(6, td);
+      DBG_T0(tr);
       if (splits > 1) {  // the last split of the client reduces in split order and applies SGD
         int* cnt = reinterpret_cast<int*>(c->stats) + 8;
         __threadfence();
@@ -829,6 +868,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
         tc::named_sync(1, 256);
       }
+      if (warp == 0) DBG_ADD(7, tr);
     }
   }
   tc::fence_before();
@@ -837,6 +877,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     tc::fence_after();
     tc::tmem_dealloc(tmem, 512);
   }
+  if (PROTEA_DBG && threadIdx.x == 0) atomicAdd(&g_dbg[8], (unsigned long long)(globaltimer() - t_start));
   if (threadIdx.x == 0 && g1 > g0) {  // K9: split this CTA's duration over its clients by item count
     const uint64_t dt = globaltimer() - t_start;
     int ti = find_task(prefix, ntask, g0), lo = g0;

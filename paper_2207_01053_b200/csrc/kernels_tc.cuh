@@ -194,8 +194,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       op.epilogue(t, row, c0, v);
     }
   } else {
-    // ---------------- MMA issuer (one thread of warp 8)
-    if (lane == 0) {
+    // ---------------- MMA issuer (warp 8, elected lane issues)
+    {
       const uint32_t idesc = tc::idesc_bf16(128, t.n_mma, Op::A_MN, Op::B_MN);
       // descriptors are linear in the stage base and the k step: precompute, then add constants
       uint64_t da0, dak, db0, dbk;
@@ -217,10 +217,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint64_t so = (uint64_t)(s * (STAGE >> 4));
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)
-          tc::mma_bf16(tmem, da0 + so + ks * dak, db0 + so + ks * dbk, idesc, (kb | ks) != 0);
-        tc::commit(bar0 + 8 * (STAGES + s));
+          tc::mma_bf16_w(tmem, da0 + so + ks * dak, db0 + so + ks * dbk, idesc, (kb | ks) != 0);
+        tc::commit_w(bar0 + 8 * (STAGES + s));
       }
-      tc::commit(done);
+      tc::commit_w(done);
     }
     __syncwarp();
   }
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kPersThreads, 1)
       }
     }
   } else if (warp == 8) {
-    if (lane == 0 && g0 < g1) {  // ---------------- MMA issuer
+    if (g0 < g1) {  // ---------------- MMA issuer (whole warp, elected lane issues)
       t.tk = tasks[cur.ti];
       t.c = op.recs + t.tk.rec;
       const uint64_t da0 = op.a_desc(t, sbase, 0), dak = op.a_desc(t, sbase, 1) - da0;
@@ -328,10 +328,10 @@ __global__ void __launch_bounds__(kPersThreads, 1)
           const uint64_t so = (uint64_t)(s * (STAGE >> 4));
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks)
-            tc::mma_bf16(dt, da0 + so + ks * dak, db0 + so + ks * dbk, idesc, (kb | ks) != 0);
-          tc::commit(empty + 8 * s);
+            tc::mma_bf16_w(dt, da0 + so + ks * dak, db0 + so + ks * dbk, idesc, (kb | ks) != 0);
+          tc::commit_w(empty + 8 * s);
         }
-        tc::commit(acc_full + 8 * acc);
+        tc::commit_w(acc_full + 8 * acc);
       }
     }
     __syncwarp();

@@ -151,6 +151,12 @@ int main() {
       {"MN SW128 A / MN SW128 B N=64 ", 64, true, true, 2, 2, 16384, 1024, 8192, 1024, 2048, 2048},
       {"MN SW128 A / MN SW128 B N=128", 128, true, true, 2, 2, 16384, 1024, 8192, 1024, 2048, 2048},
       {"MN none A / MN none B N=64", 64, true, true, 0, 0, 2048, 128, 1024, 128, 4096, 2048},
+      {"MN SW64 A(LBO1024) / MN SW128 B N=64 (c2 wgrad)", 64, true, true, 4, 2, 1024, 512, 16, 1024, 1024, 2048},
+      {"MN SW64 A(LBO12288) / MN SW128 B N=64", 64, true, true, 4, 2, 12288, 512, 16, 1024, 1024, 2048},
+      {"MN SW64 A(LBO4096) / MN SW128 B N=64", 64, true, true, 4, 2, 4096, 512, 16, 1024, 1024, 2048},
+      {"Kmaj SW64 A(SBO512) / MN none B N=32 (c2 dgrad-ish)", 32, false, true, 4, 0, 16, 512, 128, 512, 32, 256},
+      {"Kmaj SW128 A / Kmaj SW128 B N=32", 32, false, false, 2, 2, 16, 1024, 16, 1024, 32, 32},
+      {"Kmaj SW128 A / Kmaj SW128 B N=16", 16, false, false, 2, 2, 16, 1024, 16, 1024, 32, 32},
   };
   cudaFuncSetAttribute(k_mma_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 161 * 1024);
   cudaFuncSetAttribute(k_mma_bench2, cudaFuncAttributeMaxDynamicSharedMemorySize, 161 * 1024);
