@@ -199,6 +199,9 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
     const uint64_t d2[4] = {C2, 16, 16, Bk}, s2[3] = {C2 * 2, 32 * C2, 512 * C2};
     const uint32_t b2[4] = {64, 16, 4, 1};
     ok &= tmap_encode(&out[TM_DZ2WS], r.buf[B_DZ2], 4, d2, s2, b2, CU_TENSOR_MAP_SWIZZLE_128B);
+    const uint32_t bq1[4] = {32, 12, 20, 1}, bq2[4] = {64, 8, 16, 1};
+    ok &= tmap_encode(&out[TM_A1Q], r.buf[B_A1], 4, d1, s1, bq1, CU_TENSOR_MAP_SWIZZLE_64B);
+    ok &= tmap_encode(&out[TM_DZ2Q], r.buf[B_DZ2], 4, d2, s2, bq2, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   if (r.buf[B_XS]) {  // staged input xs[B][36 Y][2 par][18 X'][8] (k_stage_x)
     const uint64_t dx[5] = {8, 18, 2, 36, Bk}, sx[4] = {16, 288, 576, 36 * 576};

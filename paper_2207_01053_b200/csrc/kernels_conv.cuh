@@ -631,28 +631,31 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
-// conv2 wgrad (width 1: C1 = 32, C2 = 64) + SGD, halo form.  D[m = (tap, ci)][co] =
-// sum_p a1[p + tap][ci] dz2[p][co] over the client's output pixels p, with ALL 7
-// M tiles (800 weights + bias row) accumulating in TMEM at once (7 x 64 columns):
-// per half image the a1 halo is loaded ONCE as 5 x-shifted copies (the conv2
-// fwd's 64-byte-swizzled boxes) and every tap's A operand is a descriptor into
-// them (MN-major SW64, one 32-channel atom per tap), instead of re-gathering
-// each tap from L2 per M tile.  M tiles: j < 5 = taps (ky 0..3, kx = j) at
-// LBO = one halo row; 5 = taps (4, kx 0..3) at LBO = one copy; 6 = tap (4, 4) +
-// the bias "ones" block (a constant copy-shaped region after copy 4).
-// Work item = (client, split of 8 images = kWgradChunkPx pixels[, M tile]): with
-// ng = 7 (light iterations) each M tile of a split is its own item and loads
-// only the halo copies it reads.  A client whose batch is one split updates
-// the weights straight from TMEM; otherwise every item stores its rows of the
-// split's partial [C2][804] and the client's last item (counter stats[8]) sums
-// them in split order and applies SGD to the fp32 master and the bf16 shadow.
-// Persistent: one CTA per SM, contiguous item ranges.
+// conv2 wgrad (width 1: C1 = 32, C2 = 64) + SGD, single-halo form.  D[m = (tap, ci)][co] =
+// sum_p a1[p + tap][ci] dz2[p][co] over the client's output pixels p; ALL 7 M tiles (800
+// weights + bias row) accumulate side by side in TMEM (7 x 64 columns).
+// Sub-step = 16 output rows x 8 columns (one image half): ONE TMA box brings the a1 halo
+// [20 rows][12 px][32 ci] (64-byte swizzle, 15 KB) and one the dz2 tile [16][8][64 co]
+// (128-byte swizzle).  Every tap's A operand is a descriptor INTO the halo: the swizzle
+// is a function of the absolute shared-memory address, so a start shifted by whole
+// 64-byte pixel rows needs no base offset (verified on B200: tools/swz_test.cu).
+// MN-major SW64: an atom = 32 channels x 8 consecutive pixels of a halo row; K groups
+// (output rows) at SBO = 768 B (one halo row); M tiles j < 5 = taps (ky 0..3, kx = j) at
+// LBO = 768, tile 5 = taps (4, kx 0..3) at LBO = 64 (one pixel), tile 6 = tap (4, 4) +
+// the bias "ones" block (a constant halo-shaped region after the halo, LBO = 15 KB).
+// Work item = (client, split of 8 images = kWgradChunkPx pixels[, M tile]): with ng = 7
+// (light iterations) each M tile of a split is its own item.  A client whose batch is
+// one split updates the weights straight from TMEM; otherwise every item stores its
+// rows of the split's partial [C2][804] and the client's last item (counter stats[8])
+// sums them in split order and applies SGD to the fp32 master and the bf16 shadow.
+// Persistent: one CTA per SM, contiguous item ranges, 3-stage TMA ring.
 // ---------------------------------------------------------------------------
-constexpr int kW2Copy = 12 * 16 * 64;                    // [12 rows][16 px][32 ci] bf16, 64-byte swizzle
-constexpr int kW2Dz = 128 * 128;                         // dz2 half image [128 px][64 co] bf16, 128-byte swizzle
-constexpr int kW2Stage = 6 * kW2Copy + kW2Dz;           // 5 copies + ones block + dz2 = 88 KB
-constexpr int kW2Pad = 8192;  // M tile 6's unused atoms 2-3 read (ignored rows) up to 7.5 KB past the last stage
-constexpr int kW2Smem = 2 * kW2Stage + kW2Pad + 256 + 1024;
+constexpr int kW2Halo = 20 * 12 * 64;                   // a1 halo [20][12][32] bf16
+constexpr int kW2Dz = 16 * 8 * 128;                     // dz2 [16][8][64] bf16
+constexpr int kW2Stage = 2 * kW2Halo + kW2Dz;           // halo + ones block + dz2 = 46 KB
+constexpr int kW2Stages = 4;
+constexpr int kW2Pad = 16384;  // M tile 6's unused atoms 2-3 read (ignored rows) past the last stage
+constexpr int kW2Smem = kW2Stages * kW2Stage + kW2Pad + 256 + 1024;
 constexpr int kW2N = 25 * 32 + 1;                        // weight rows + bias row
 constexpr int kW2NP = 804;                               // partial row stride (float4-aligned)
 
@@ -669,8 +672,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                        const int* __restrict__ prefix, int ntask, CnnDims d, float lr, int ng) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kW2Stage + kW2Pad);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kW2Stages * kW2Stage + kW2Pad);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kW2Stages + 2);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = __ldg(prefix + ntask);
@@ -678,9 +681,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int g1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
   const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
   const uint32_t bar0 = tc::smem_u32(bars);
-  const uint32_t full = bar0, empty = bar0 + 16, acc_full = bar0 + 32, acc_empty = bar0 + 40;
+  const uint32_t full = bar0, empty = bar0 + 8 * kW2Stages, acc_full = bar0 + 16 * kW2Stages, acc_empty = acc_full + 8;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kW2Stages; ++i) {
       tc::mbar_init(full + 8 * i, 1);
       tc::mbar_init(empty + 8 * i, 1);
     }
@@ -688,12 +691,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     tc::mbar_init(acc_empty, 8);
     tc::mbar_fence_init();
   }
-  // the bias "ones" block of each stage: 1.0 at channel 0 of every pixel row (64-byte swizzle:
-  // row r of a 512-byte atom keeps logical 16-byte chunk c at physical chunk c ^ ((r >> 1) & 3))
-  for (int i = threadIdx.x; i < 2 * kW2Copy / 16; i += blockDim.x) {
-    const int st = i / (kW2Copy / 16), k = i - st * (kW2Copy / 16), r = k >> 2, c = k & 3;
-    reinterpret_cast<uint4*>(smem + st * kW2Stage + 5 * kW2Copy)[k] =
-        c == ((r >> 1) & 3) ? make_uint4(0x3F80u, 0, 0, 0) : make_uint4(0, 0, 0, 0);
+  // the bias "ones" block of each stage: 1.0 at channel 0 of every 64-byte pixel row; 64-byte
+  // swizzle on absolute addresses: logical chunk 0 of the row at byte a sits in chunk (a >> 7) & 3
+  for (int i = threadIdx.x; i < kW2Stages * (kW2Halo / 16); i += blockDim.x) {
+    const int st = i / (kW2Halo / 16), k = i - st * (kW2Halo / 16);
+    const uint32_t off = st * kW2Stage + kW2Halo + 16 * k;
+    reinterpret_cast<uint4*>(smem + off)[0] =
+        ((off >> 4) & 3) == ((off >> 7) & 3) ? make_uint4(0x3F80u, 0, 0, 0) : make_uint4(0, 0, 0, 0);
   }
   tc::fence_proxy_async();
   if (warp == 9) tc::tmem_alloc(tc::smem_u32(tmem_slot), 512);
@@ -706,7 +710,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   cur.init(prefix, ntask, g0 < total ? g0 : total - 1);
 
   if (warp == 8) {
-    if (lane == 0) {  // ---------------- TMA producer: per half image, 5 halo copies + 2 dz2 boxes
+    if (lane == 0) {  // ---------------- TMA producer: per image half, the a1 halo + the dz2 tile
       TcTile t;
       int s = 0;
       for (int g = g0; g < g1; ++g) {
@@ -714,33 +718,27 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           t.tk = tasks[cur.ti];
           t.c = recs + t.tk.rec;
         }
-        const int item = g - cur.lo, grp = item % ng, r0 = 8 * (item / ng), nsub = 2 * min(8, t.tk.rows - r0);
-        // halo copies read by the item's M tiles: all (ng = 1); tile j < 5: copy j; 5: copies 0-3; 6: copy 4
-        const int need = ng == 1 ? 0x1F : grp < 5 ? 1 << grp : grp == 5 ? 0xF : 0x10;
-        const uint32_t tx = __popc(need) * kW2Copy + kW2Dz;
+        const int item = g - cur.lo, r0 = 8 * (item / ng), nsub = 2 * min(8, t.tk.rows - r0);
         for (int sub = 0; sub < nsub; ++sub, ++s) {
-          const int buf = s & 1, r = r0 + (sub >> 1), y0 = 8 * (sub & 1);
+          const int buf = s % kW2Stages, r = r0 + (sub >> 1), x0 = 8 * (sub & 1);
           const uint32_t base = sb + buf * kW2Stage;
           DBG_T0(tw);
-          if (s >= 2) tc::mbar_wait(empty + 8 * buf, ((s >> 1) - 1) & 1);
+          if (s >= kW2Stages) tc::mbar_wait(empty + 8 * buf, ((s / kW2Stages) - 1) & 1);
           DBG_ADD(0, tw);
           DBG_T0(ti);
-          tc::mbar_expect_tx(full + 8 * buf, tx);
-          for (int kx = 0; kx < 5; ++kx)
-            if ((need >> kx) & 1)
-              tc::tma_load_4d(base + kx * kW2Copy, tmap_of(t, TM_A1H), full + 8 * buf, 0, kx - 2, y0 - 2, r);
-          for (int h = 0; h < 2; ++h)
-            tc::tma_load_4d(base + 6 * kW2Copy + h * (kW2Dz / 2), tmap_of(t, TM_DZ2WS), full + 8 * buf, 0, 0,
-                            y0 + 4 * h, r);
+          tc::mbar_expect_tx(full + 8 * buf, kW2Halo + kW2Dz);
+          tc::tma_load_4d(base, tmap_of(t, TM_A1Q), full + 8 * buf, 0, x0 - 2, -2, r);
+          tc::tma_load_4d(base + 2 * kW2Halo, tmap_of(t, TM_DZ2Q), full + 8 * buf, 0, x0, 0, r);
           DBG_ADD(1, ti);
         }
       }
     }
   } else if (warp == 9) {
-    {  // ---------------- MMA issuer (whole warp, elected lane issues): 8 K steps x 7 M tiles per half image
+    {  // ---------------- MMA issuer (whole warp, elected lane issues): 8 K steps x 7 M tiles per half
       const uint32_t idesc = tc::idesc_bf16(128, 64, true, true);
-      const uint64_t a_kx = tc::sdesc_sw64(sb, 1024, 512), a_k4 = tc::sdesc_sw64(sb, kW2Copy, 512);
-      const uint64_t b0 = tc::sdesc_sw128(sb + 6 * kW2Copy, 16, 1024);
+      const uint64_t a_ky = tc::sdesc_sw64(sb, 768, 768), a_kx = tc::sdesc_sw64(sb, 64, 768),
+                     a_1 = tc::sdesc_sw64(sb, kW2Halo, 768);
+      const uint64_t b0 = tc::sdesc_sw128(sb + 2 * kW2Halo, 16, 1024);
       int s = 0, i = 0;
       for (int g = g0; g < g1; ++g, ++i) {
         cur.advance(prefix, g);
@@ -751,10 +749,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         DBG_ADD(2, ta0);
         tc::fence_after();
         for (int sub = 0; sub < nsub; ++sub, ++s) {
-          const int buf = s & 1;
+          const int buf = s % kW2Stages;
           const uint32_t so = buf * kW2Stage;
           DBG_T0(tf);
-          tc::mbar_wait(full + 8 * buf, (s >> 1) & 1);
+          tc::mbar_wait(full + 8 * buf, (s / kW2Stages) & 1);
           DBG_ADD(3, tf);
           DBG_T0(tm);
           tc::fence_after();
@@ -762,20 +760,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
               const uint64_t db = tc::dadd(b0, so + 2048 * ks);
-              const uint32_t acc = (sub | ks) != 0;
+              const uint32_t acc = (sub | ks) != 0, row = so + 2 * ks * 768;
 #pragma unroll
-              for (int j = 0; j < 5; ++j)
-                tc::mma_bf16_w(tmem + 64 * j, tc::dadd(a_kx, so + j * kW2Copy + ks * 1024), db, idesc, acc);
-              tc::mma_bf16_w(tmem + 64 * 5, tc::dadd(a_k4, so + (ks + 4) * 1024), db, idesc, acc);
-              tc::mma_bf16_w(tmem + 64 * 6, tc::dadd(a_k4, so + 4 * kW2Copy + (ks + 4) * 1024), db, idesc, acc);
+              for (int j = 0; j < 5; ++j) tc::mma_bf16_w(tmem + 64 * j, tc::dadd(a_ky, row + 64 * j), db, idesc, acc);
+              tc::mma_bf16_w(tmem + 64 * 5, tc::dadd(a_kx, row + 4 * 768), db, idesc, acc);
+              tc::mma_bf16_w(tmem + 64 * 6, tc::dadd(a_1, row + 4 * 768 + 4 * 64), db, idesc, acc);
             }
           } else {  // one M tile
-            const uint64_t a = grp < 5 ? tc::dadd(a_kx, so + grp * kW2Copy)
-                                       : tc::dadd(a_k4, so + (grp == 5 ? 0 : 4 * kW2Copy) + 4 * 1024);
+            const uint64_t a = grp < 5 ? tc::dadd(a_ky, so + 64 * grp)
+                                       : grp == 5 ? tc::dadd(a_kx, so + 4 * 768) : tc::dadd(a_1, so + 4 * 768 + 256);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
-              tc::mma_bf16_w(tmem + 64 * grp, tc::dadd(a, ks * 1024), tc::dadd(b0, so + 2048 * ks), idesc,
-                           (sub | ks) != 0);
+              tc::mma_bf16_w(tmem + 64 * grp, tc::dadd(a, 2 * ks * 768), tc::dadd(b0, so + 2048 * ks), idesc,
+                             (sub | ks) != 0);
           }
           tc::commit_w(empty + 8 * buf);
           DBG_ADD(4, tm);
@@ -801,6 +798,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       tc::mbar_wait(acc_full, i & 1);
       if (warp == 0) DBG_ADD(5, te);
       DBG_T0(td);
+      tc::fence_after();
 #pragma unroll 1
       for (int j = ng == 1 ? 0 : grp; j < (ng == 1 ? 7 : grp + 1); ++j) {
         float v[32];
@@ -834,7 +832,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if (lane == 0) tc::mbar_arrive(acc_empty);  // TMEM drained: the next item's MMAs may start
       if (warp == 0) DBG_ADD(6, td);
       DBG_T0(tr);
-      if (splits > 1) {  // the last split of the client reduces in split order and applies SGD
+      if (splits > 1) {  // the last item of the client reduces in split order and applies SGD
         int* cnt = reinterpret_cast<int*>(c->stats) + 8;
         __threadfence();
         tc::named_sync(1, 256);
@@ -845,23 +843,35 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           // float4 over m (row stride 804), all splits' loads of a chunk in flight together
           const float4* pt = (const float4*)c->buf[B_WSP];
           constexpr int Q = kW2NP / 4;  // float4 per co row
-          for (int e = threadIdx.x; e < 64 * Q; e += 256) {
-            const int co = e / Q, m0 = 4 * (e - co * Q);
-            float4 gs = make_float4(0.f, 0.f, 0.f, 0.f);
+          constexpr int U = 4;  // independent float4 chunks per thread per pass (memory-level parallelism)
+          for (int e0 = threadIdx.x; e0 < 64 * Q; e0 += 256 * U) {
+            float4 gs[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) gs[u] = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int sp = 0; sp < splits; ++sp) {
-              const float4 p = __ldcg(pt + (int64_t)sp * 64 * Q + e);
-              gs.x += p.x, gs.y += p.y, gs.z += p.z, gs.w += p.w;
+              float4 p[U];
+#pragma unroll
+              for (int u = 0; u < U; ++u)
+                p[u] = e0 + 256 * u < 64 * Q ? __ldcg(pt + (int64_t)sp * 64 * Q + e0 + 256 * u) : make_float4(0, 0, 0, 0);
+#pragma unroll
+              for (int u = 0; u < U; ++u) gs[u].x += p[u].x, gs[u].y += p[u].y, gs[u].z += p[u].z, gs[u].w += p[u].w;
             }
-            if (m0 < Kw) {
-              const int64_t idx = d.w2 + (int64_t)co * Kw + m0;
-              float4 w = *reinterpret_cast<const float4*>(P + idx);
-              w.x -= lr * gs.x, w.y -= lr * gs.y, w.z -= lr * gs.z, w.w -= lr * gs.w;
-              *reinterpret_cast<float4*>(P + idx) = w;
-              const __nv_bfloat162 h0 = __floats2bfloat162_rn(w.x, w.y), h1 = __floats2bfloat162_rn(w.z, w.w);
-              *reinterpret_cast<uint2*>(S + idx) =
-                  make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
-            } else if (m0 == Kw) {
-              P[d.b2 + co] -= lr * gs.x;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int e = e0 + 256 * u;
+              if (e >= 64 * Q) continue;
+              const int co = e / Q, m0 = 4 * (e - co * Q);
+              if (m0 < Kw) {
+                const int64_t idx = d.w2 + (int64_t)co * Kw + m0;
+                float4 w = *reinterpret_cast<const float4*>(P + idx);
+                w.x -= lr * gs[u].x, w.y -= lr * gs[u].y, w.z -= lr * gs[u].z, w.w -= lr * gs[u].w;
+                *reinterpret_cast<float4*>(P + idx) = w;
+                const __nv_bfloat162 h0 = __floats2bfloat162_rn(w.x, w.y), h1 = __floats2bfloat162_rn(w.z, w.w);
+                *reinterpret_cast<uint2*>(S + idx) =
+                    make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+              } else if (m0 == Kw) {
+                P[d.b2 + co] -= lr * gs[u].x;
+              }
             }
           }
           if (threadIdx.x == 0) *cnt = 0;

@@ -787,6 +787,8 @@ enum TmapId : int {
   TM_DZ2WS,    // dz2 box (64,16,4,1)  128B-swizzled   conv2 wgrad B (width 1)
   TM_XSW,      // xs                box (8,8,1,36,1)  conv1 wgrad: one x-shifted copy per dx
   TM_G,        // g1 [B][16][16][4 q][C1] box (64,8,16,1) 128B-swizzled  conv1 wgrad A (MN-major)
+  TM_A1Q,      // a1  box (32,12,20,1) 64B-swizzled   conv2 wgrad single halo (width 1)
+  TM_DZ2Q,     // dz2 box (64,8,16,1)  128B-swizzled  conv2 wgrad B, one image half (width 1)
   TM_COUNT
 };
 

@@ -8,6 +8,8 @@ def main(path, top=25):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr = rows[0]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    mi = hdr.index("Metric Name")
+    rows = [rows[0]] + [r for r in rows[1:] if r[mi] == "gpu__time_duration.sum"]
     scale = {"ns": 1, "nsecond": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6}
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows[1:]:
