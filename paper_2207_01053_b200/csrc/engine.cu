@@ -202,6 +202,13 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
     const uint32_t bq1[4] = {32, 12, 20, 1}, bq2[4] = {64, 8, 16, 1};
     ok &= tmap_encode(&out[TM_A1Q], r.buf[B_A1], 4, d1, s1, bq1, CU_TENSOR_MAP_SWIZZLE_64B);
     ok &= tmap_encode(&out[TM_DZ2Q], r.buf[B_DZ2], 4, d2, s2, bq2, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= tmap_encode(&out[TM_DZ2Q1], r.buf[B_DZ2], 4, d2, s2, bq1, CU_TENSOR_MAP_SWIZZLE_64B);
+    const uint64_t dwf[2] = {25 * C1, C2}, swf[1] = {50 * C1};
+    const uint32_t bwf[2] = {64, 64};
+    ok &= tmap_encode(&out[TM_W2FS], w2, 2, dwf, swf, bwf, CU_TENSOR_MAP_SWIZZLE_128B);
+    const uint64_t dwd[3] = {C1, 25, C2}, swd[2] = {2 * C1, 50 * C1};
+    const uint32_t bwd[3] = {32, 1, 64};
+    ok &= tmap_encode(&out[TM_W2DS], w2, 3, dwd, swd, bwd, CU_TENSOR_MAP_SWIZZLE_64B);
   }
   if (r.buf[B_XS]) {  // staged input xs[B][36 Y][2 par][18 X'][8] (k_stage_x)
     const uint64_t dx[5] = {8, 18, 2, 36, Bk}, sx[4] = {16, 288, 576, 36 * 576};
@@ -608,7 +615,9 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   op_end(ctx, ev);
   launch_conv_persistent<QuadConv1<WQ>>(ctx, drecs, d, L, OP_C1F, dtab);
   join_group(ctx, L.group);  // the previous step's deferred fc1 wgrad still reads a2
-  if constexpr (WQ >= 2)
+  if constexpr (WQ == 4)
+    launch_conv_persistent<HaloConv2Q<false>>(ctx, drecs, d, L, OP_C2F, dtab);
+  else if constexpr (WQ == 2)
     launch_conv_persistent<HaloConv2<WQ, false>>(ctx, drecs, d, L, OP_C2F, dtab);
   else
     launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TmaConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
@@ -631,7 +640,10 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   } else {
     launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
   }
-  launch_conv_persistent<HaloConv2<WQ, true>>(ctx, drecs, d, L, OP_C2D, dtab);
+  if constexpr (WQ == 4)
+    launch_conv_persistent<HaloConv2Q<true>>(ctx, drecs, d, L, OP_C2D, dtab);
+  else
+    launch_conv_persistent<HaloConv2<WQ, true>>(ctx, drecs, d, L, OP_C2D, dtab);
   if constexpr (WQ == 4)
     launch_conv2_wgrad_halo(ctx, drecs, d, L, dtab, lr);
   else

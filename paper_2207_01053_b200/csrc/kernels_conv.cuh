@@ -211,6 +211,146 @@ struct HaloConv2 {
 };
 
 // ---------------------------------------------------------------------------
+// conv2 fwd / dgrad, width 1 (C1 = 32, C2 = 64), single-halo form.  Tile = 16 output
+// rows x 8 columns (one image half), M row m = y * 8 + x.  Per 32-channel group ONE TMA
+// box brings the input halo [20 rows][12 px][32 ch] (64-byte swizzle) and every tap's A
+// operand is a descriptor into it, shifted by whole 64-byte pixel rows (the swizzle
+// follows absolute addresses: tools/swz_test.cu): K-major, 8-row core groups = 8 pixels
+// of one halo row (SBO = 768 B = one halo row), K step 16 channels = +32 B.  The
+// weights are loaded by a few wide boxes: fwd K-major 128-byte swizzle [13][64 co][64 k]
+// (8 KB per 64-wide K block), dgrad MN-major 64-byte swizzle [25 taps][64 co][32 ci].
+// Pool partners (y,x),(y,x+1),(y+1,x),(y+1,x+1) are lanes l, l+1, l+8, l+9.
+// ---------------------------------------------------------------------------
+template <bool DGRAD>
+struct HaloConv2Q {
+  typedef CnnW<4> W;
+  static constexpr int CIN = DGRAD ? 64 : 32;
+  static constexpr int NOUT = DGRAD ? 32 : 64, N = NOUT;
+  static constexpr bool B_MN = DGRAD;
+  static constexpr int GROUPS = CIN / 32;
+  static constexpr int HALO = 20 * 12 * 64;           // one 32-channel group
+  static constexpr int HBYTES = HALO;                 // one pipeline stage = one group's halo
+  static constexpr int B_BYTES = DGRAD ? 25 * 4096 : 13 * 8192;
+  static constexpr int TMEM_COLS = 2 * N <= 64 ? 64 : 128;
+  static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256 + 1024;
+  static constexpr int TILES_PER_IMAGE = 2;
+  static constexpr int DBG = DGRAD ? 32 : 16;
+  const ClientRec* recs;
+  CnnDims d;
+
+  __device__ void load_b(const TcTile& t, uint32_t sb, uint32_t bar) const {
+    if (!DGRAD) {  // W2 shadow [64 co][800 k]: box (64 k, 64 co) per 64-wide K block (the last one zero-filled)
+      for (int kb = 0; kb < 13; ++kb) tc::tma_load_2d(sb + kb * 8192, tmap_of(t, TM_W2FS), bar, 64 * kb, 0);
+    } else {  // view [64 co][25 tap][32 ci]: box (32 ci, 1 tap, 64 co) per tap
+      for (int tap = 0; tap < 25; ++tap) tc::tma_load_3d(sb + tap * 4096, tmap_of(t, TM_W2DS), bar, 0, tap, 0);
+    }
+  }
+  __device__ void load_halo(const TcTile& t, int tile, int grp, uint32_t base, uint32_t bar) const {
+    const int r = tile >> 1, x0 = (tile & 1) * 8;
+    tc::tma_load_4d(base, tmap_of(t, DGRAD ? TM_DZ2Q1 : TM_A1Q), bar, 32 * grp, x0 - 2, -2, r);
+  }
+  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc) const {
+    const uint64_t a0 = tc::sdesc_sw64(hb, 16, 768);
+    const uint64_t b0 = !DGRAD ? tc::sdesc_sw128(sb, 16, 1024) : tc::sdesc_sw64(sb, 16, 512);
+#pragma unroll
+    for (int ky = 0; ky < 5; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < 5; ++kx) {
+        const int tap = ky * 5 + kx;
+        const uint32_t ao = (DGRAD ? (4 - ky) * 768 + (4 - kx) * 64 : ky * 768 + kx * 64);
+#pragma unroll
+        for (int cp = 0; cp < 2; ++cp) {
+          uint32_t bo;
+          if (!DGRAD) {  // K index = tap*32 + 16 cp: 64-wide block, 32-byte step inside the 128-byte row
+            const int kk = 2 * tap + cp;
+            bo = (kk >> 2) * 8192 + (kk & 3) * 32;
+          } else {  // k rows = co 32 grp + 16 cp .. of tap: 2 atoms of 8 rows per K step
+            bo = tap * 4096 + (32 * grp + 16 * cp) * 64;
+          }
+          tc::mma_bf16_w(dt, tc::dadd(a0, ao + 32 * cp), tc::dadd(b0, bo), idesc, (grp | tap | cp) != 0);
+        }
+      }
+  }
+  static constexpr int NCH = (N + 31) / 32;
+  struct EpiState {
+    const ClientRec* c = nullptr;
+    float bias[NCH][16];
+  };
+  struct Pre {
+    uint4 a[NCH][2];
+    uint4 i[NCH];
+  };
+  __device__ void prefetch(const TcTile& t, int tile, int warp, int lane, Pre& p) const {
+    if constexpr (DGRAD) {
+      const int g = warp >> 2, row = (warp & 3) * 32 + lane;
+      const int r = tile >> 1, y = row >> 3, x = (tile & 1) * 8 + (row & 7);
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const int c0 = g * 16 + 32 * j;
+        const int64_t o = ((int64_t)r * 256 + y * 16 + x) * W::C1 + c0;
+        const uint4* a = reinterpret_cast<const uint4*>((const bf16*)t.c->buf[B_A1] + o);
+        p.a[j][0] = a[0];
+        p.a[j][1] = a[1];
+        p.i[j] = *reinterpret_cast<const uint4*>((const uint8_t*)t.c->buf[B_I1] + o);
+      }
+    }
+  }
+  __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
+                           int lane, EpiState& st, const Pre&) const {
+    const int g = warp >> 2, row = (warp & 3) * 32 + lane;
+    const int r = tile >> 1, y = row >> 3, x = (tile & 1) * 8 + (row & 7);
+    float a1v[NCH][16];
+    int argv[NCH][16];
+    if (!DGRAD && st.c != t.c) {
+      st.c = t.c;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) st.bias[j][q] = t.c->params[d.b2 + g * 16 + 32 * j + q];
+    }
+    if (DGRAD) {
+      Pre p;
+      prefetch(t, tile, warp, lane, p);  // operands independent of the MMA: fetch before waiting
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        ld_bf16<16>(reinterpret_cast<const bf16*>(&p.a[j][0]), a1v[j]);
+        ld_u8<16>(reinterpret_cast<const uint8_t*>(&p.i[j]), argv[j]);
+      }
+    }
+    tc::mbar_wait(full_bar, parity);
+    tc::fence_after();
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c0 = g * 16 + 32 * j;
+      float v[16];
+      tc::tmem_ld16(tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
+      if (DGRAD) {  // pool-1 backward in the pool-quad layout g1[r][py][px][q][C1] (k_conv1_wgrad_q)
+        bf16* g1 = (bf16*)t.c->buf[B_DZC1];
+        float out[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) out[e] = (argv[j][e] == q && a1v[j][e] > 0.f) ? v[e] : 0.f;
+          st_bf16<16>(g1 + (((int64_t)r * 256 + y * 16 + x) * 4 + q) * W::C1 + c0, out);
+        }
+      } else {  // bias + ReLU + 2x2 max-pool (first max) over lanes (l, l+1, l+8, l+9)
+        const int base = lane & ~9;
+        float val[16], best[16];
+        int arg[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) val[e] = fmaxf(v[e] + st.bias[j][e], 0.f);
+        pool_lanes(val, base, base + 1, base + 8, base + 9, best, arg);
+        if ((lane & 9) == 0) {
+          const int64_t o = ((int64_t)r * 64 + (y >> 1) * 8 + (x >> 1)) * W::C2 + c0;
+          st_bf16<16>((bf16*)t.c->buf[B_A2] + o, best);
+          st_u8<16>((uint8_t*)t.c->buf[B_I2] + o, arg);
+        }
+      }
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
 // conv1 fwd (3 -> C1, 32x32 input) + bias + ReLU + 2x2 max-pool, "pool-quad" form.
 // One GEMM row per POOLED output (py, px); its 4 pool positions q = (qy, qx)
 // become 4 groups of output columns: D[(py,px)][q*C1 + co] = sum over the 6x6
@@ -398,7 +538,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       for (int g = g0; g < g1; ++g, ++i) {
         if (cur.advance(prefix, g) || g == g0) {
           if (nb > 0) tc::commit_w(b_empty);  // completes when every MMA issued so far (old weights) is done
+          DBG_T0(tb);
           tc::mbar_wait(b_full, nb & 1);
+          DBG_ADD(D0 + 6, tb);
           tc::fence_after();
           ++nb;
         }
@@ -445,6 +587,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       DBG_T0(te);
       op.epilogue(t, g - cur.lo, tmem + acc * Op::N, acc_full + 8 * acc, (i >> 1) & 1, warp, lane, st, pc);
       if (warp == 0) DBG_ADD(D0 + 5, te);
+      if (PROTEA_DBG && i == 0 && warp == 0 && lane == 0)  // kernel start -> first tile's epilogue done
+        atomicAdd(&g_dbg[D0 + 7], (unsigned long long)(globaltimer() - t_start));
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(acc_empty + 8 * acc);

@@ -789,6 +789,9 @@ enum TmapId : int {
   TM_G,        // g1 [B][16][16][4 q][C1] box (64,8,16,1) 128B-swizzled  conv1 wgrad A (MN-major)
   TM_A1Q,      // a1  box (32,12,20,1) 64B-swizzled   conv2 wgrad single halo (width 1)
   TM_DZ2Q,     // dz2 box (64,8,16,1)  128B-swizzled  conv2 wgrad B, one image half (width 1)
+  TM_DZ2Q1,    // dz2 box (32,12,20,1) 64B-swizzled   conv2 dgrad single halo, one 32-channel group (width 1)
+  TM_W2FS,     // W2 shadow (800, 64)    box (64,64) 128B-swizzled  conv2 fwd weights (width 1)
+  TM_W2DS,     // W2 shadow (32, 25, 64) box (32,1,64) 64B-swizzled conv2 dgrad weights (width 1)
   TM_COUNT
 };
 

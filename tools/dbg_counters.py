@@ -38,8 +38,10 @@ names = ["prod_wait_empty", "prod_issue", "mma_wait_acc_empty", "mma_wait_full",
 for base, label in ((0, "conv2 wgrad halo"), (16, "conv2 fwd halo"), (32, "conv2 dgrad halo"), (48, "conv1 fwd quad")):
     print("==", label)
     for i, n in enumerate(names):
-        if base and i in (6, 7):
-            continue
         nm = n if not (base and i == 5) else "epi_total(wait+work)"
+        if base and i == 6:
+            nm = "mma_wait_weights"
+        if base and i == 7:
+            nm = "first_tile_done_ns"
         v = buf[base + i] / 148 / 1e6
-        print(f"  {nm:22s} {v:10.3f} " + ("Mcyc per CTA" if i < 8 else "ms per CTA"))
+        print(f"  {nm:22s} {v:10.3f} " + ("Mcyc per CTA" if (i < 8 and not (base and i == 7)) else "ms per CTA"))

@@ -1,4 +1,4 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/gpu_t.log
+timeout 600 python -m pytest tests -m gpu -x -q --timeout 120 2>&1 | tail -5 > gpurun_out/gpu_t.log
 timeout 240 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_t.json 2> gpurun_out/bench_t.err
 cat gpurun_out/gpu_t.log
 python - <<'PY'
