@@ -210,11 +210,11 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
     const uint32_t bwd[3] = {32, 1, 64};
     ok &= tmap_encode(&out[TM_W2DS], w2, 3, dwd, swd, bwd, CU_TENSOR_MAP_SWIZZLE_64B);
   }
-  if (r.buf[B_XS]) {  // staged input xs[B][36 Y][2 par][18 X'][8] (k_stage_x)
-    const uint64_t dx[5] = {8, 18, 2, 36, Bk}, sx[4] = {16, 288, 576, 36 * 576};
-    const uint32_t bh[5] = {8, 10, 2, 36, 1}, bw[5] = {8, 8, 1, 36, 1};
-    ok &= tmap_encode(&out[TM_XSH], r.buf[B_XS], 5, dx, sx, bh);
-    ok &= tmap_encode(&out[TM_XSW], r.buf[B_XS], 5, dx, sx, bw);
+  if (r.buf[B_XS]) {  // staged input xs[B][36 Y][2 par][18 X' x 8 ch] (k_stage_x): pixel runs as the inner dim
+    const uint64_t dx[4] = {144, 2, 36, Bk}, sx[3] = {288, 576, 36 * 576};
+    const uint32_t bh[4] = {80, 2, 36, 1}, bw[4] = {64, 1, 36, 1};
+    ok &= tmap_encode(&out[TM_XSH], r.buf[B_XS], 4, dx, sx, bh);
+    ok &= tmap_encode(&out[TM_XSW], r.buf[B_XS], 4, dx, sx, bw);
   }
   if (r.buf[B_XS] && C1 == 32) {  // pool-quad conv1 gradient g1[B][16][16][4 q][C1] (k_conv1_wgrad_q)
     const uint64_t d[4] = {4 * C1, 16, 16, Bk}, st[3] = {8 * C1, 128 * C1, 2048 * C1};

@@ -387,7 +387,7 @@ struct QuadConv1 {
     for (int kc = 0; kc < 36; ++kc) tc::bulk_load(sb + kc * N * 16, w1q + kc * N * 16, N * 16, bar);
   }
   __device__ void load_halo(const TcTile& t, int tile, int grp, uint32_t base, uint32_t bar) const {
-    tc::tma_load_5d(base, tmap_of(t, TM_XSH), bar, 0, (tile & 1) * 8, 0, 0, tile >> 1);
+    tc::tma_load_4d(base, tmap_of(t, TM_XSH), bar, 64 * (tile & 1), 0, 0, tile >> 1);  // 10-pixel runs (160 B)
   }
   __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc) const {
     const uint64_t a0 = tc::sdesc(hb, 160, 640), b0 = tc::sdesc(sb, N * 16, 128);
@@ -690,8 +690,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           tc::tma_load_4d(gb, tmap_of(t, TM_G), full + 8 * buf, 0, 8 * h, 0, r);
           tc::tma_load_4d(gb + kW1GBytes / 2, tmap_of(t, TM_G), full + 8 * buf, 64, 8 * h, 0, r);
           for (int dx = 0; dx < 6; ++dx)
-            tc::tma_load_5d(gb + kW1GBytes + dx * kW1XCopy, tmap_of(t, TM_XSW), full + 8 * buf, 0,
-                            8 * h + (dx >> 1), dx & 1, 0, r);
+            tc::tma_load_4d(gb + kW1GBytes + dx * kW1XCopy, tmap_of(t, TM_XSW), full + 8 * buf,
+                            8 * (8 * h + (dx >> 1)), dx & 1, 0, r);
         }
       }
     }

@@ -782,10 +782,10 @@ enum TmapId : int {
   TM_DH,       // dh (F, B)              box (64,R)   128B-swizzled, fc1 dgrad B
   TM_A1H,      // a1                box (8,16,12,1)  conv2 fwd halo (kernels_conv.cuh)
   TM_DZ2H,     // dz2               box (8,16,12,1)  conv2 dgrad halo
-  TM_XSH,      // xs [B][36 Y][2 par][18 X'][8] box (8,10,2,36,1)  conv1 fwd halo (kernels_conv.cuh)
+  TM_XSH,      // xs [B][36 Y][2 par][18 X' x 8] box (80,2,36,1)  conv1 fwd halo (kernels_conv.cuh)
   TM_A1WS,     // a1  box (32,16,4,1)  64B-swizzled    conv2 wgrad A (width 1)
   TM_DZ2WS,    // dz2 box (64,16,4,1)  128B-swizzled   conv2 wgrad B (width 1)
-  TM_XSW,      // xs                box (8,8,1,36,1)  conv1 wgrad: one x-shifted copy per dx
+  TM_XSW,      // xs                box (64,1,36,1)  conv1 wgrad: one x-shifted copy per dx
   TM_G,        // g1 [B][16][16][4 q][C1] box (64,8,16,1) 128B-swizzled  conv1 wgrad A (MN-major)
   TM_A1Q,      // a1  box (32,12,20,1) 64B-swizzled   conv2 wgrad single halo (width 1)
   TM_DZ2Q,     // dz2 box (64,8,16,1)  128B-swizzled  conv2 wgrad B, one image half (width 1)
