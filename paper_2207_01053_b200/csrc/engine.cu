@@ -370,6 +370,8 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
 }
 
 std::vector<int> ops_of(const ModelDims& m, bool tc) {
+  if (m.arch == PROTEA_MODEL_CNN && tc && m.width_q == 4)  // conv1 reduce fused into k_conv1_wgrad_q
+    return {OP_STAGE, OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C1W};
   if (m.arch == PROTEA_MODEL_CNN && tc)
     return {OP_STAGE, OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_CNN)
@@ -480,6 +482,7 @@ struct Launch {
   int64_t prefix_off[OP_COUNT];
   int grid[OP_COUNT];
   int c2w_groups;                       // width-1 conv2 wgrad: M-tile groups per split (1 or 7)
+  int f1f_splits;                       // width-1 fc1 fwd: K splits per M tile (1 or 4)
   uint64_t fl[OP_COUNT], by[OP_COUNT];  // algorithmic work of each op of this launch (op_work)
 };
 
@@ -544,7 +547,8 @@ void launch_conv_persistent(protea_ctx* ctx, const ClientRec* drecs, const CnnDi
   op_end(ctx, ev);
 }
 
-void launch_conv1_wgrad_q(protea_ctx* ctx, const ClientRec* drecs, const Launch& L, const int32_t* dtab) {
+void launch_conv1_wgrad_q(protea_ctx* ctx, const ClientRec* drecs, const Launch& L, const int32_t* dtab,
+                          const CnnDims& d, float lr) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_conv1_wgrad_q, cudaFuncAttributeMaxDynamicSharedMemorySize, kW1Smem);
@@ -553,7 +557,8 @@ void launch_conv1_wgrad_q(protea_ctx* ctx, const ClientRec* drecs, const Launch&
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[OP_C1W], g_num_sms);
   const int ev = op_begin(ctx, OP_C1W, OP_C1W);
-  k_conv1_wgrad_q<<<grid, kConvThreads, kW1Smem, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1W], L.ntask);
+  k_conv1_wgrad_q<<<grid, kConvThreads, kW1Smem, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1W], L.ntask,
+                                                                d.w1, d.b1, lr);
   op_end(ctx, ev);
 }
 
@@ -621,6 +626,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
     launch_conv_persistent<HaloConv2<WQ, false>>(ctx, drecs, d, L, OP_C2F, dtab);
   else
     launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TmaConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
+  // (a split-K persistent variant, TmaFc1FwdS, measured slower here: 7.2 -> 8.0 ms/round)
   launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
   launch_head_cnn<T>(ctx, m, L, drecs, tasks, lr);
   launch_gemm_persistent<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab, 2);
@@ -649,14 +655,15 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   else
     launch_gemm_tc<TC_C2W_BN, TC_STAGES>(ctx, tma_op_lr<TmaConv2Wgrad<WQ>>(drecs, d, lr), L, OP_C2W, dtab);
 
-  if constexpr (WQ == 4)
-    launch_conv1_wgrad_q(ctx, drecs, L, dtab);
-  else
+  if constexpr (WQ == 4) {
+    launch_conv1_wgrad_q(ctx, drecs, L, dtab, d, lr);  // the split reduce + SGD is fused (last split)
+  } else {
     launch_gemm_tc<TC_C1W_BN, TC_STAGES>(ctx, TcConv1Wgrad<WQ>{drecs, d}, L, OP_C1W, dtab);
-  ev = op_begin(ctx, OP_C1R, OP_C1R);
-  k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
-                                                                       L.ntask, m.c1, d.w1, d.b1, lr);
-  op_end(ctx, ev);
+    ev = op_begin(ctx, OP_C1R, OP_C1R);
+    k_reduce_conv1_tc<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1R],
+                                                                         L.ntask, m.c1, d.w1, d.b1, lr);
+    op_end(ctx, ev);
+  }
 }
 
 void launch_step_tc(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const int32_t* dtab,
@@ -1118,6 +1125,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
         // width-1 conv2 wgrad: when the iteration has few splits (the tail), each split's 7 M tiles become
         // 7 work items (no extra partials: disjoint outputs), otherwise one item covers all 7 tiles
         L.c2w_groups = 1;
+        L.f1f_splits = 1;
         if (tc_mode && m.arch == PROTEA_MODEL_CNN && m.width_q == 4) {
           int64_t nsplit = 0;
           for (int r : rows) nsplit += cdiv(r * 256, kWgradChunkPx);
@@ -1128,7 +1136,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
           int acc_t = 0;
           for (size_t i = 0; i < act.size(); ++i) {
             tab.push_back(acc_t);
-            acc_t += tiles(m, op, rows[i], tc_mode) * (op == OP_C2W ? L.c2w_groups : 1);
+            acc_t += tiles(m, op, rows[i], tc_mode) * (op == OP_C2W ? L.c2w_groups : op == OP_F1F ? L.f1f_splits : 1);
             uint64_t fl, by;
             op_work(m, op, (uint64_t)rows[i], (uint64_t)e, &fl, &by);
             ctx->op_flops[op_class(op)] += fl;

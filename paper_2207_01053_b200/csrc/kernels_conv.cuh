@@ -632,7 +632,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 // MN-major without swizzle (core matrix = 8 ci x 8 pooled columns, LBO = next
 // pooled row = 256 B, SBO = next dx copy).  TMEM: D at column dy*48 + dx*8 + ci.
 // The epilogue folds through shared memory and writes the split's partial
-// [76][C1] (k_reduce_conv1_tc sums the splits in order and applies SGD).
+// [76][C1]; the client's last split sums the partials in split order and
+// applies SGD to the master and the pool-quad shadow (conv1_reduce_update).
 // Persistent: one CTA per SM walks a contiguous range of work items.
 // ---------------------------------------------------------------------------
 constexpr int kW1GBytes = 2 * 128 * 128;                // g1 sub-tile: 128 (q,co) x 128 pooled px bf16
@@ -643,7 +644,8 @@ constexpr int kW1Smem = 2 * kW1Stage + kW1Fold + 256 + 1024;
 
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv1_wgrad_q(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks,
-                    const int* __restrict__ prefix, int ntask) {
+                    const int* __restrict__ prefix, int ntask, int64_t off_w, int64_t off_b, float lr) {
+  __shared__ int last_flag;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   float* S = reinterpret_cast<float*>(smem + 2 * kW1Stage);
@@ -752,6 +754,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       float* part = (float*)c->buf[B_WSP] + (int64_t)split * 76 * 32;
       for (int e = threadIdx.x; e < 76 * 32; e += 256)
         part[e] = ((S[e] + S[2432 + e]) + S[2 * 2432 + e]) + S[3 * 2432 + e];
+      // the client's last split sums the partials in split order and applies SGD (counter stats[9])
+      const int splits = cdiv(tasks[ti].rows * 1024, kWgradChunkPx);
+      int* cnt = reinterpret_cast<int*>(c->stats) + 9;
+      __threadfence();
+      tc::named_sync(1, 256);
+      if (threadIdx.x == 0) last_flag = atomicAdd(cnt, 1) == splits - 1;
+      tc::named_sync(1, 256);
+      if (last_flag) {
+        __threadfence();
+        for (int e = threadIdx.x; e < 76 * 32; e += 256) conv1_reduce_update(c, splits, 32, off_w, off_b, lr, e);
+        if (threadIdx.x == 0) *cnt = 0;
+      }
       tc::named_sync(1, 256);
     }
   }

@@ -87,6 +87,15 @@ struct has_finish {
   static constexpr bool value = f<Op>(nullptr);
 };
 
+template <class Op>
+struct has_pfinish {
+  template <class U>
+  static constexpr bool f(decltype(U::PFINISH)*) { return U::PFINISH; }
+  template <class U>
+  static constexpr bool f(...) { return false; }
+  static constexpr bool value = f<Op>(nullptr);
+};
+
 template <int BN, int STAGES, class Op>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_gemm_tc(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
@@ -355,6 +364,7 @@ __global__ void __launch_bounds__(kPersThreads, 1)
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(acc_empty + 8 * acc);
+      if constexpr (has_pfinish<Op>::value) op.pfinish(t);  // split-K: the last split reduces (epilogue warps)
     }
   }
   tc::fence_before();
@@ -1015,6 +1025,62 @@ struct TmaFc1Fwd : TcFc1Fwd<WQ> {
   }
 };
 
+// fc1 fwd for the persistent GEMM with optional split-K (light iterations: few clients, so the
+// 4 M tiles per client cannot keep the HBM busy).  splits > 1: item = (client, M tile, K split);
+// each split stores fp32 partials [split][F][rows] in the client's wgrad scratch (free at this
+// point of the step) and the last split of a (client, M tile) (counter stats[10 + tile]) sums
+// them in split order and applies bias + ReLU.
+struct TmaFc1FwdS : TmaFc1Fwd<4> {
+  typedef CnnW<4> W;
+  int splits;
+  __device__ void setup(TcTile& t, int local) const {
+    t.m0 = (local / splits) * 128;
+    t.n0 = local % splits;
+    t.nk = W::K1 / 64 / splits;
+    t.n_mma = round16(t.tk.rows);
+  }
+  __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
+    const int kg = t.n0 * t.nk + kb;
+    tc::tma_load_2d(a, tmap_of(t, TM_W3K), mbar, kg * 64, t.m0);
+    tc::tma_load_2d(b, tmap_of(t, TM_A2), mbar, kg * 64, 0);
+  }
+  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
+    if (splits == 1) {
+      TmaFc1Fwd<4>::epilogue(t, row, c0, v);
+      return;
+    }
+    const int rows = t.tk.rows, f = t.m0 + row;
+    float* part = (float*)t.c->buf[B_WSP] + ((int64_t)t.n0 * W::F + f) * rows;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (c0 + j < rows) part[c0 + j] = v[j];
+  }
+  static constexpr bool PFINISH = true;
+  __device__ void pfinish(const TcTile& t) const {
+    if (splits == 1) return;
+    __shared__ int last;
+    int* cnt = reinterpret_cast<int*>(t.c->stats) + 10 + t.m0 / 128;
+    __threadfence();
+    tc::named_sync(1, 256);
+    if (threadIdx.x == 0) last = atomicAdd(cnt, 1) == splits - 1;
+    tc::named_sync(1, 256);
+    if (last) {
+      __threadfence();
+      const int rows = t.tk.rows;
+      const float* part = (const float*)t.c->buf[B_WSP];
+      bf16* h = (bf16*)t.c->buf[B_H];
+      for (int e = threadIdx.x; e < 128 * rows; e += 256) {
+        const int f = t.m0 + e / rows, r = e - (e / rows) * rows;
+        float g = 0.f;
+        for (int sp = 0; sp < splits; ++sp) g += __ldcg(part + ((int64_t)sp * W::F + f) * rows + r);
+        h[(int64_t)r * W::F + f] = __float2bfloat16_rn(fmaxf(g + t.c->params[this->d.b3 + f], 0.f));
+      }
+      if (threadIdx.x == 0) *cnt = 0;
+    }
+    tc::named_sync(1, 256);
+  }
+};
+
 template <int WQ>
 struct TmaFc1Dgrad : TcFc1Dgrad<WQ> {
   typedef CnnW<WQ> W;
@@ -1120,19 +1186,14 @@ struct TcConv1Wgrad {
   }
 };
 
-__global__ void __launch_bounds__(kReduceBlock)
-    k_reduce_conv1_tc(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, const int* __restrict__ prefix,
-                      int ntask, int C1, int64_t off_w, int64_t off_b, float lr) {
-  const int ti = find_task(prefix, ntask, blockIdx.x);
-  const Task tk = tasks[ti];
-  const ClientRec* c = recs + tk.rec;
+// Sum the split partials of element e = idx * C1 + co (idx 0..74 = weight (tap, ci), 75 = bias) in split
+// order and apply SGD to the fp32 master and the pool-quad bf16 shadow (common.h w1q_index).
+__device__ __forceinline__ void conv1_reduce_update(const ClientRec* c, int splits, int C1, int64_t off_w,
+                                                    int64_t off_b, float lr, int e) {
   const int total = 76 * C1;
-  const int e = (blockIdx.x - __ldg(prefix + ti)) * kReduceBlock + threadIdx.x;
-  if (e >= total) return;
-  const int splits = cdiv(tk.rows * 1024, kWgradChunkPx);
   const float* part = (const float*)c->buf[B_WSP];
   float g = 0.f;
-  for (int s = 0; s < splits; ++s) g += part[(int64_t)s * total + e];
+  for (int s = 0; s < splits; ++s) g += __ldcg(part + (int64_t)s * total + e);
   const int idx = e / C1, co = e - idx * C1;
   if (idx == 75) {
     c->params[off_b + co] -= lr * g;
@@ -1143,9 +1204,20 @@ __global__ void __launch_bounds__(kReduceBlock)
     const int tap = idx / 3, ky = tap / 5, kx = tap - ky * 5, ci = idx - 3 * tap;
     const bf16 h = __float2bfloat16_rn(nw);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)  // the weight's 4 places in the pool-quad shadow (common.h w1q_index)
+    for (int q = 0; q < 4; ++q)  // the weight's 4 places in the pool-quad shadow
       ((bf16*)c->buf[B_W1P])[w1q_index(C1, ky + (q >> 1), kx + (q & 1), q, co, ci)] = h;
   }
+}
+
+__global__ void __launch_bounds__(kReduceBlock)
+    k_reduce_conv1_tc(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, const int* __restrict__ prefix,
+                      int ntask, int C1, int64_t off_w, int64_t off_b, float lr) {
+  const int ti = find_task(prefix, ntask, blockIdx.x);
+  const Task tk = tasks[ti];
+  const ClientRec* c = recs + tk.rec;
+  const int e = (blockIdx.x - __ldg(prefix + ti)) * kReduceBlock + threadIdx.x;
+  if (e >= 76 * C1) return;
+  conv1_reduce_update(c, cdiv(tk.rows * 1024, kWgradChunkPx), C1, off_w, off_b, lr, e);
 }
 
 // --------------------------------------------------------------------------
