@@ -482,7 +482,6 @@ struct Launch {
   int64_t prefix_off[OP_COUNT];
   int grid[OP_COUNT];
   int c2w_groups;                       // width-1 conv2 wgrad: M-tile groups per split (1 or 7)
-  int f1f_splits;                       // width-1 fc1 fwd: K splits per M tile (1 or 4)
   uint64_t fl[OP_COUNT], by[OP_COUNT];  // algorithmic work of each op of this launch (op_work)
 };
 
@@ -626,7 +625,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
     launch_conv_persistent<HaloConv2<WQ, false>>(ctx, drecs, d, L, OP_C2F, dtab);
   else
     launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TmaConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
-  // (a split-K persistent variant, TmaFc1FwdS, measured slower here: 7.2 -> 8.0 ms/round)
+  // (a split-K persistent variant for light iterations measured slower: 7.2 -> 8.0 ms/round)
   launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
   launch_head_cnn<T>(ctx, m, L, drecs, tasks, lr);
   launch_gemm_persistent<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab, 2);
@@ -1125,7 +1124,6 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
         // width-1 conv2 wgrad: when the iteration has few splits (the tail), each split's 7 M tiles become
         // 7 work items (no extra partials: disjoint outputs), otherwise one item covers all 7 tiles
         L.c2w_groups = 1;
-        L.f1f_splits = 1;
         if (tc_mode && m.arch == PROTEA_MODEL_CNN && m.width_q == 4) {
           int64_t nsplit = 0;
           for (int r : rows) nsplit += cdiv(r * 256, kWgradChunkPx);
@@ -1136,7 +1134,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
           int acc_t = 0;
           for (size_t i = 0; i < act.size(); ++i) {
             tab.push_back(acc_t);
-            acc_t += tiles(m, op, rows[i], tc_mode) * (op == OP_C2W ? L.c2w_groups : op == OP_F1F ? L.f1f_splits : 1);
+            acc_t += tiles(m, op, rows[i], tc_mode) * (op == OP_C2W ? L.c2w_groups : 1);
             uint64_t fl, by;
             op_work(m, op, (uint64_t)rows[i], (uint64_t)e, &fl, &by);
             ctx->op_flops[op_class(op)] += fl;

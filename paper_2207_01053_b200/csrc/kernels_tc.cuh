@@ -1025,62 +1025,6 @@ struct TmaFc1Fwd : TcFc1Fwd<WQ> {
   }
 };
 
-// fc1 fwd for the persistent GEMM with optional split-K (light iterations: few clients, so the
-// 4 M tiles per client cannot keep the HBM busy).  splits > 1: item = (client, M tile, K split);
-// each split stores fp32 partials [split][F][rows] in the client's wgrad scratch (free at this
-// point of the step) and the last split of a (client, M tile) (counter stats[10 + tile]) sums
-// them in split order and applies bias + ReLU.
-struct TmaFc1FwdS : TmaFc1Fwd<4> {
-  typedef CnnW<4> W;
-  int splits;
-  __device__ void setup(TcTile& t, int local) const {
-    t.m0 = (local / splits) * 128;
-    t.n0 = local % splits;
-    t.nk = W::K1 / 64 / splits;
-    t.n_mma = round16(t.tk.rows);
-  }
-  __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
-    const int kg = t.n0 * t.nk + kb;
-    tc::tma_load_2d(a, tmap_of(t, TM_W3K), mbar, kg * 64, t.m0);
-    tc::tma_load_2d(b, tmap_of(t, TM_A2), mbar, kg * 64, 0);
-  }
-  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
-    if (splits == 1) {
-      TmaFc1Fwd<4>::epilogue(t, row, c0, v);
-      return;
-    }
-    const int rows = t.tk.rows, f = t.m0 + row;
-    float* part = (float*)t.c->buf[B_WSP] + ((int64_t)t.n0 * W::F + f) * rows;
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (c0 + j < rows) part[c0 + j] = v[j];
-  }
-  static constexpr bool PFINISH = true;
-  __device__ void pfinish(const TcTile& t) const {
-    if (splits == 1) return;
-    __shared__ int last;
-    int* cnt = reinterpret_cast<int*>(t.c->stats) + 10 + t.m0 / 128;
-    __threadfence();
-    tc::named_sync(1, 256);
-    if (threadIdx.x == 0) last = atomicAdd(cnt, 1) == splits - 1;
-    tc::named_sync(1, 256);
-    if (last) {
-      __threadfence();
-      const int rows = t.tk.rows;
-      const float* part = (const float*)t.c->buf[B_WSP];
-      bf16* h = (bf16*)t.c->buf[B_H];
-      for (int e = threadIdx.x; e < 128 * rows; e += 256) {
-        const int f = t.m0 + e / rows, r = e - (e / rows) * rows;
-        float g = 0.f;
-        for (int sp = 0; sp < splits; ++sp) g += __ldcg(part + ((int64_t)sp * W::F + f) * rows + r);
-        h[(int64_t)r * W::F + f] = __float2bfloat16_rn(fmaxf(g + t.c->params[this->d.b3 + f], 0.f));
-      }
-      if (threadIdx.x == 0) *cnt = 0;
-    }
-    tc::named_sync(1, 256);
-  }
-};
-
 template <int WQ>
 struct TmaFc1Dgrad : TcFc1Dgrad<WQ> {
   typedef CnnW<WQ> W;
