@@ -103,6 +103,15 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z;
 }
 
+// Programmatic dependent launch (kernels launched with cudaLaunchAttributeProgrammaticStreamSerialization):
+// pdl_wait() blocks until the preceding kernel of the stream has completed and its writes are visible
+// (a no-op without the attribute); pdl_trigger() lets the next kernel's CTAs start their prologue.
+// Rule used by every kernel of the lock-step chain: all threads call pdl_wait() before touching data the
+// preceding kernel may write; only data written two or more kernels earlier (e.g. weights updated in the
+// previous step) is read before it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

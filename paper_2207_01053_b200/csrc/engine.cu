@@ -106,6 +106,9 @@ struct protea_ctx {
   std::vector<cudaEvent_t> gjoin;  // per model group: end of its deferred fc1 wgrad
   std::vector<char> gpending;      // per model group: a deferred fc1 wgrad not yet joined
   bool overlap_now = false;        // current iteration defers fc1 wgrad (light iteration)
+  // programmatic dependent launch on the lock-step stream (PROTEA_PDL=1).  Off by default: measured on
+  // B200, config 2: 70.2 ms/round without, 71.5 ms with (early CTAs of the next kernel hold SM resources).
+  bool pdl = false;
   int64_t overlap_rows = 640;      // defer when the iteration's total rows are at most this (PROTEA_OVERLAP_ROWS)
   // per-op-class accounting of the current round (protea_round_stats)
   uint32_t time_ops = 0;
@@ -251,6 +254,22 @@ int op_begin(protea_ctx* ctx, int op, int raw = -1) {  // op: stats class; raw: 
 }
 void op_end(protea_ctx* ctx, int i) {
   if (i >= 0) cudaEventRecord(ctx->evpool[i + 1], ctx->cur);
+}
+// Launch on ctx->cur; on the lock-step stream with programmatic stream serialization (PDL) so the kernel's
+// CTAs can run their prologue while the preceding kernel drains (kernels call pdl_wait(), device.cuh).
+template <typename... KArgs, typename... Args>
+void launch_k(protea_ctx* ctx, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->cur;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (ctx->pdl && ctx->cur == ctx->hi) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, args...);
 }
 void reset_ops(protea_ctx* ctx, uint32_t time_ops) {
   ctx->time_ops = time_ops;
@@ -505,7 +524,7 @@ void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, c
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int* prefix = dtab + L.prefix_off[opid];
   const int ev = op_begin(ctx, opid, opid);
-  k_gemm_tc<BN, STAGES, OpT><<<L.grid[opid], kTcThreads, SMEM, ctx->cur>>>(op, tasks, prefix, L.ntask);
+  launch_k(ctx, k_gemm_tc<BN, STAGES, OpT>, L.grid[opid], kTcThreads, SMEM, op, tasks, prefix, L.ntask);
   op_end(ctx, ev);
 }
 
@@ -523,8 +542,8 @@ void launch_gemm_persistent(protea_ctx* ctx, const OpT& op, const Launch& L, int
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[opid], ctas_per_sm * g_num_sms);
   const int ev = op_begin(ctx, opid, opid);
-  k_gemm_persistent<BN, STAGES, OpT><<<grid, kPersThreads, SMEM, ctx->cur>>>(op, tasks, dtab + L.prefix_off[opid],
-                                                                               L.ntask);
+  launch_k(ctx, k_gemm_persistent<BN, STAGES, OpT>, grid, kPersThreads, SMEM, op, tasks,
+           (const int*)(dtab + L.prefix_off[opid]), L.ntask);
   op_end(ctx, ev);
 }
 
@@ -542,7 +561,8 @@ void launch_conv_persistent(protea_ctx* ctx, const ClientRec* drecs, const CnnDi
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[opid], g_num_sms);  // one CTA per SM, each a contiguous tile range
   const int ev = op_begin(ctx, opid, opid);
-  k_conv_persistent<Op><<<grid, kConvThreads, Op::SMEM, ctx->cur>>>(op, tasks, dtab + L.prefix_off[opid], L.ntask);
+  launch_k(ctx, k_conv_persistent<Op>, grid, kConvThreads, Op::SMEM, op, tasks, (const int*)(dtab + L.prefix_off[opid]),
+           L.ntask);
   op_end(ctx, ev);
 }
 
@@ -556,8 +576,8 @@ void launch_conv1_wgrad_q(protea_ctx* ctx, const ClientRec* drecs, const Launch&
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[OP_C1W], g_num_sms);
   const int ev = op_begin(ctx, OP_C1W, OP_C1W);
-  k_conv1_wgrad_q<<<grid, kConvThreads, kW1Smem, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C1W], L.ntask,
-                                                                d.w1, d.b1, lr);
+  launch_k(ctx, k_conv1_wgrad_q, grid, kConvThreads, kW1Smem, drecs, tasks, (const int*)(dtab + L.prefix_off[OP_C1W]),
+           L.ntask, d.w1, d.b1, lr);
   op_end(ctx, ev);
 }
 
@@ -571,8 +591,8 @@ void launch_conv2_wgrad_halo(protea_ctx* ctx, const ClientRec* drecs, const CnnD
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[OP_C2W], g_num_sms);
   const int ev = op_begin(ctx, OP_C2W, OP_C2W);
-  k_conv2_wgrad_halo<<<grid, kConvThreads, kW2Smem, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_C2W], L.ntask,
-                                                                   d, lr, L.c2w_groups);
+  launch_k(ctx, k_conv2_wgrad_halo, grid, kConvThreads, kW2Smem, drecs, tasks, (const int*)(dtab + L.prefix_off[OP_C2W]),
+           L.ntask, d, lr, L.c2w_groups);
   op_end(ctx, ev);
 }
 
@@ -588,7 +608,7 @@ void launch_head_cnn(protea_ctx* ctx, const ModelDims& m, const Launch& L, const
   }
   HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
   const int ev = op_begin(ctx, OP_HEAD, OP_HEAD);
-  k_head_cnn<T><<<L.ntask, kHeadCnnThreads, smem, ctx->cur>>>(ha, tasks);
+  launch_k(ctx, k_head_cnn<T>, L.ntask, kHeadCnnThreads, smem, ha, tasks);
   op_end(ctx, ev);
 }
 
@@ -614,8 +634,8 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const CnnDims d = cnn_dims(m);
   int ev = op_begin(ctx, OP_STAGE, OP_STAGE);
-  k_stage_x<<<L.grid[OP_STAGE], kStageThreads, 0, ctx->cur>>>(drecs, tasks, dtab + L.prefix_off[OP_STAGE],
-                                                                  L.ntask);
+  launch_k(ctx, k_stage_x, L.grid[OP_STAGE], kStageThreads, 0, drecs, tasks, (const int*)(dtab + L.prefix_off[OP_STAGE]),
+           L.ntask);
   op_end(ctx, ev);
   launch_conv_persistent<QuadConv1<WQ>>(ctx, drecs, d, L, OP_C1F, dtab);
   join_group(ctx, L.group);  // the previous step's deferred fc1 wgrad still reads a2
@@ -869,6 +889,7 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
   int prio_least = 0, prio_greatest = 0;
   cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest);
   if (const char* ov = std::getenv("PROTEA_OVERLAP_ROWS")) ctx->overlap_rows = std::atoll(ov);
+  if (const char* pd = std::getenv("PROTEA_PDL")) ctx->pdl = std::atoi(pd) != 0;
   if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_least) != cudaSuccess ||
       cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, prio_greatest) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess ||

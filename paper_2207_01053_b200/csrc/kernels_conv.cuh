@@ -500,6 +500,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const uint32_t sb = tc::smem_u32(smem), sh = tc::smem_u32(sH);
   TcTile t;
   t.n_mma = Op::N;
+  // the first client's weights were written at least two kernels earlier: load them before the PDL wait
+  if (warp == 8 && lane == 0 && g0 < g1) {
+    TaskCursor c0;
+    c0.init(prefix, ntask, g0);
+    t.tk = tasks[c0.ti];
+    t.c = op.recs + t.tk.rec;
+    tc::mbar_expect_tx(b_full, Op::B_BYTES);
+    op.load_b(t, sb, b_full);
+  }
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 8) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -511,9 +522,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (fresh) {  // new client: wait until the MMAs released the previous weights, reload
           t.tk = tasks[cur.ti];
           t.c = op.recs + t.tk.rec;
-          if (nb > 0) tc::mbar_wait(b_empty, (nb - 1) & 1);
-          tc::mbar_expect_tx(b_full, Op::B_BYTES);
-          op.load_b(t, sb, b_full);
+          if (nb > 0) {  // (the first client's weights were issued before the PDL wait)
+            tc::mbar_wait(b_empty, (nb - 1) & 1);
+            tc::mbar_expect_tx(b_full, Op::B_BYTES);
+            op.load_b(t, sb, b_full);
+          }
           ++nb;
         }
         const int tile = g - cur.lo;
@@ -674,6 +687,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t sb = tc::smem_u32(smem);
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 8) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -866,6 +881,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const uint32_t sb = tc::smem_u32(smem);
   TaskCursor cur;
   cur.init(prefix, ntask, g0 < total ? g0 : total - 1);
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 8) {
     if (lane == 0) {  // ---------------- TMA producer: per image half, the a1 halo + the dz2 tile

@@ -659,6 +659,8 @@ template <typename T>
 __global__ void __launch_bounds__(kHeadCnnThreads)
     k_head_cnn(HeadArgs a, const Task* __restrict__ tasks) {
   extern __shared__ float hsm[];
+  pdl_wait();
+  pdl_trigger();
   const Task tk = tasks[blockIdx.x];
   const ClientRec* c = a.recs + tk.rec;
   const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;

@@ -140,6 +140,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   if constexpr (TMA) {
     if (warp == 0 && lane == 0) {
@@ -294,6 +296,8 @@ __global__ void __launch_bounds__(kPersThreads, 1)
   TcTile t;
   TaskCursor cur;
   cur.init(prefix, ntask, g0 < total ? g0 : total - 1);
+  pdl_wait();
+  pdl_trigger();
   if (warp == 9) {
     if (lane == 0) {  // ---------------- TMA producer
       int it = 0;
@@ -1055,6 +1059,8 @@ constexpr int kStageThreads = 256;
 __global__ void __launch_bounds__(kStageThreads)
     k_stage_x(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, const int* __restrict__ prefix,
               int ntask) {
+  pdl_wait();  // xs is still read by the preceding conv1 wgrad
+  pdl_trigger();
   const int ti = find_task(prefix, ntask, blockIdx.x);
   const Task tk = tasks[ti];
   const ClientRec* c = recs + tk.rec;
