@@ -212,6 +212,12 @@ protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clien
 protea_status protea_plan(const protea_profile* profiles, size_t n, const protea_cluster* cluster,
                           const protea_plan_opts* opts, protea_assignment* out, uint64_t* makespan_steps);
 
+/* 64-bit FNV-1a hash of a round's client list and plan (every field of both arrays, in the given
+ * order).  Pure host function.  protea_run_round with world > 1 compares it across ranks before
+ * any device work (NCCL max of h and ~h, SURVEY §8(e) "plan agreement"); ranks that were given
+ * different plans or client lists fail with PROTEA_ERR_PLAN. */
+uint64_t protea_plan_hash(const protea_client* clients, size_t n, const protea_assignment* plan);
+
 /* Run one round.  Every rank passes the same clients and plan; this rank runs
  * the clients whose gpu == rank in lock-step iterations at their planned arena
  * offsets, then all ranks sum the per-GPU FedAvg partials (NCCL when world > 1)
@@ -219,6 +225,7 @@ protea_status protea_plan(const protea_profile* profiles, size_t n, const protea
  * global_in / global_out: n_params floats (all registered groups concatenated),
  * host or device; a group without sampled clients is copied unchanged.
  * measured (nullable): n records of in-run profiles; stats (nullable).
+ * world > 1: the ranks' protea_plan_hash values must agree (else PLAN, nothing run).
  * Errors: INVALID, PLAN, OOM, CUDA, NCCL. */
 protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, const protea_client* clients,
                                size_t n, const protea_assignment* plan, const float* global_in, float* global_out,

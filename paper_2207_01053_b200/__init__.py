@@ -3,7 +3,7 @@
 Every step of the hot path runs in the library's CUDA kernels; this module only
 converts numpy / torch objects to the C structs and pointers the ABI takes.
 There is no CPU fallback: importing the package fails loudly if the shared
-library is missing (build it with `python -m paper_2207_01053_b200.build` or
+library is missing (build it with `python paper_2207_01053_b200/build.py` or
 `__graft_entry__.build()`).
 """
 from __future__ import annotations
@@ -30,7 +30,7 @@ ORDER_ASC_ID, ORDER_DESC_STEPS = 0, 1
 
 EXPORTS = ["protea_init", "protea_finalize", "protea_last_error", "protea_register_model", "protea_register_shards",
            "protea_profile_clients", "protea_plan", "protea_run_round", "protea_fedavg", "protea_client_footprint",
-           "protea_selftest_gemm", "protea_round_partial", "protea_round_finalize"]
+           "protea_selftest_gemm", "protea_round_partial", "protea_round_finalize", "protea_plan_hash"]
 
 
 class ProteaError(RuntimeError):
@@ -125,8 +125,10 @@ _lib.protea_round_partial.argtypes = [_vp, _vp, _sz]
 _lib.protea_round_finalize.argtypes = [_vp, _vp, _vp, _vp, _sz]
 _lib.protea_selftest_gemm.argtypes = [_vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
 for _f in EXPORTS:
-    if _f not in ("protea_finalize", "protea_last_error"):
+    if _f not in ("protea_finalize", "protea_last_error", "protea_plan_hash"):
         getattr(_lib, _f).restype = ctypes.c_int
+_lib.protea_plan_hash.argtypes = [_vp, _sz, _vp]
+_lib.protea_plan_hash.restype = ctypes.c_uint64
 
 
 def _check(code, ctx=None):
@@ -219,6 +221,14 @@ def protea_plan(profiles, caps, policy=POLICY_PROFILED, order=ORDER_ASC_ID, marg
     _check(_lib.protea_plan(profiles.ctypes.data, len(profiles), ctypes.byref(cl), ctypes.byref(po),
                             out.ctypes.data, mk.ctypes.data))
     return out, mk
+
+
+def protea_plan_hash(clients, plan):
+    """64-bit hash of a round's client list and plan (run_round compares it across ranks when world > 1)."""
+    clients = np.ascontiguousarray(clients, dtype=CLIENT_DT)
+    plan = np.ascontiguousarray(plan, dtype=ASSIGN_DT)
+    assert len(clients) == len(plan)
+    return int(_lib.protea_plan_hash(clients.ctypes.data, len(clients), plan.ctypes.data))
 
 
 def protea_run_round(ctx, clients, plan, global_in, global_out, lr=0.05, seed=0, rnd=0, shuffle=True,

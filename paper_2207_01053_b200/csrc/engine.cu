@@ -838,6 +838,34 @@ bool is_device_ptr(const void* p) {
 // C ABI
 // ---------------------------------------------------------------------------
 extern "C" {
+uint64_t protea_plan_hash(const protea_client* clients, size_t n, const protea_assignment* plan) {
+  uint64_t h = 1469598103934665603ull;  // FNV-1a 64
+  auto mix = [&h](const void* p, size_t bytes) {
+    const uint8_t* b = static_cast<const uint8_t*>(p);
+    for (size_t i = 0; i < bytes; ++i) {
+      h ^= b[i];
+      h *= 1099511628211ull;
+    }
+  };
+  mix(&n, sizeof(n));
+  for (size_t i = 0; clients && i < n; ++i) {
+    mix(&clients[i].client_id, 8);
+    mix(&clients[i].model_id, 4);
+    mix(&clients[i].batch, 4);
+    mix(&clients[i].epochs, 4);
+  }
+  for (size_t i = 0; plan && i < n; ++i) {
+    mix(&plan[i].client_id, 8);
+    mix(&plan[i].gpu, 4);
+    mix(&plan[i].q1024, 4);
+    mix(&plan[i].offset, 8);
+    mix(&plan[i].slot, 8);
+    mix(&plan[i].admit, 8);
+    mix(&plan[i].release, 8);
+  }
+  return h;
+}
+
 // Debug cycle counters of instrumented kernels (built with -DPROTEA_DBG=1); not part of the public ABI.
 int protea_debug_counters(uint64_t* out, int reset) {
   if (cudaMemcpyFromSymbol(out, protea::g_dbg, 64 * sizeof(uint64_t)) != cudaSuccess) return -1;
@@ -1320,6 +1348,20 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
     if (a.gpu == ctx->rank) all.push_back(r);
   }
   if (pa.size() != n) return fail(ctx, PROTEA_ERR_PLAN, "run_round: plan and client list differ");
+  // plan agreement across ranks: max over ranks of (h, ~h) equals (h, ~h) iff all agree
+  if (ctx->comm && ctx->world > 1) {
+    const uint64_t h = protea_plan_hash(clients, n, plan);
+    uint64_t hv[2] = {h, ~h};
+    CK(cudaSetDevice(ctx->device));
+    CK(ctx->acc.reserve(2));
+    CK(cudaMemcpyAsync(ctx->acc.p, hv, 16, cudaMemcpyHostToDevice, ctx->stream));
+    ncclResult_t r = ncclAllReduce(ctx->acc.p, ctx->acc.p, 2, ncclUint64, ncclMax, ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return fail(ctx, PROTEA_ERR_NCCL, std::string("run_round: plan hash allreduce: ") + ncclGetErrorString(r));
+    CK(cudaMemcpyAsync(hv, ctx->acc.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (hv[0] != h || hv[1] != ~h)
+      return fail(ctx, PROTEA_ERR_PLAN, "run_round: ranks disagree on the plan / client list (plan hash)");
+  }
   // live slots pairwise disjoint on this GPU
   {
     std::vector<std::pair<uint64_t, int>> ev;  // (time*2 + kind, idx)

@@ -44,6 +44,20 @@ def _worker(rank, world, port, q):
         hs = [torch.zeros_like(h) for _ in range(world)]
         dist.all_gather(hs, h)
         same = all(torch.equal(hs[0], x) for x in hs)
+        # the library's agreement check (protea_run_round, world > 1): max over ranks of (h, ~h) == (h, ~h)
+        cl = pb.clients_array([(c.id, 0, c.batch, c.epochs) for c in wl.clients])
+        ph = pb.protea_plan_hash(cl, plan)
+        hv = torch.tensor([ph >> 1, (~ph & (2**64 - 1)) >> 1], dtype=torch.int64)  # int64-safe halves
+        dist.all_reduce(hv, op=dist.ReduceOp.MAX)
+        agree = int(hv[0]) == ph >> 1 and int(hv[1]) == (~ph & (2**64 - 1)) >> 1
+        bad = plan.copy()
+        if rank == 1:
+            bad[0]["admit"] += 1  # a rank with a different plan
+        bh = pb.protea_plan_hash(cl, bad)
+        bv = torch.tensor([bh >> 1, (~bh & (2**64 - 1)) >> 1], dtype=torch.int64)
+        dist.all_reduce(bv, op=dist.ReduceOp.MAX)
+        disagree = not (int(bv[0]) == bh >> 1 and int(bv[1]) == (~bh & (2**64 - 1)) >> 1)
+        same = same and agree and disagree
         mine = [c for c, a in zip(wl.clients, plan) if int(a["gpu"]) == rank]
         w0 = synth.init_weights(wl.model).astype(np.float64)
         acc = np.zeros_like(w0)
