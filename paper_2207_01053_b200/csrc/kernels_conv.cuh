@@ -819,8 +819,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 // Work item = (client, split of 8 images = kWgradChunkPx pixels[, M tile]): with ng = 7
 // (light iterations) each M tile of a split is its own item.  A client whose batch is
 // one split updates the weights straight from TMEM; otherwise every item stores its
-// rows of the split's partial [C2][804] and the client's last item (counter stats[8])
-// sums them in split order and applies SGD to the fp32 master and the bf16 shadow.
+// rows of the split's partial [C2][804], and after its CTA's last item each item sums
+// one slice of the elements over the splits in split order and applies SGD to the fp32
+// master and the bf16 shadow (distributed, balanced reduce; counters stats[8], stats[10]).
 // Persistent: one CTA per SM, contiguous item ranges, 3-stage TMA ring.
 // ---------------------------------------------------------------------------
 constexpr int kW2Halo = 20 * 12 * 64;                   // a1 halo [20][12][32] bf16
@@ -847,7 +848,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kW2Stages * kW2Stage + kW2Pad);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kW2Stages + 2);
-  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = __ldg(prefix + ntask);
   const int g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
@@ -1007,54 +1007,63 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if (lane == 0) tc::mbar_arrive(acc_empty);  // TMEM drained: the next item's MMAs may start
       if (warp == 0) DBG_ADD(6, td);
       DBG_T0(tr);
-      if (splits > 1) {  // the last item of the client reduces in split order and applies SGD
-        int* cnt = reinterpret_cast<int*>(c->stats) + 8;
+      if (splits > 1) {  // publish this item's partial (arrival counter stats[8])
         __threadfence();
         tc::named_sync(1, 256);
-        if (threadIdx.x == 0) *last_flag = atomicAdd(cnt, 1) == splits * ng - 1;
-        tc::named_sync(1, 256);
-        if (*last_flag) {
-          __threadfence();
-          // float4 over m (row stride 804), all splits' loads of a chunk in flight together
-          const float4* pt = (const float4*)c->buf[B_WSP];
-          constexpr int Q = kW2NP / 4;  // float4 per co row
-          constexpr int U = 4;  // independent float4 chunks per thread per pass (memory-level parallelism)
-          for (int e0 = threadIdx.x; e0 < 64 * Q; e0 += 256 * U) {
-            float4 gs[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) gs[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int sp = 0; sp < splits; ++sp) {
-              float4 p[U];
-#pragma unroll
-              for (int u = 0; u < U; ++u)
-                p[u] = e0 + 256 * u < 64 * Q ? __ldcg(pt + (int64_t)sp * 64 * Q + e0 + 256 * u) : make_float4(0, 0, 0, 0);
-#pragma unroll
-              for (int u = 0; u < U; ++u) gs[u].x += p[u].x, gs[u].y += p[u].y, gs[u].z += p[u].z, gs[u].w += p[u].w;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const int e = e0 + 256 * u;
-              if (e >= 64 * Q) continue;
-              const int co = e / Q, m0 = 4 * (e - co * Q);
-              if (m0 < Kw) {
-                const int64_t idx = d.w2 + (int64_t)co * Kw + m0;
-                float4 w = *reinterpret_cast<const float4*>(P + idx);
-                w.x -= lr * gs[u].x, w.y -= lr * gs[u].y, w.z -= lr * gs[u].z, w.w -= lr * gs[u].w;
-                *reinterpret_cast<float4*>(P + idx) = w;
-                const __nv_bfloat162 h0 = __floats2bfloat162_rn(w.x, w.y), h1 = __floats2bfloat162_rn(w.z, w.w);
-                *reinterpret_cast<uint2*>(S + idx) =
-                    make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
-              } else if (m0 == Kw) {
-                P[d.b2 + co] -= lr * gs[u].x;
-              }
-            }
-          }
-          if (threadIdx.x == 0) *cnt = 0;
-        }
-        tc::named_sync(1, 256);
+        if (threadIdx.x == 0) atomicAdd(reinterpret_cast<int*>(c->stats) + 8, 1);
       }
       if (warp == 0) DBG_ADD(7, tr);
     }
+    // Split reduce, distributed: item i of a client (of n = splits * ng) sums slice i of the client's
+    // 64 x 804 partial elements in split order and applies SGD to it.  It runs after ALL of this CTA's
+    // items, so waiting for the client's other items (other CTAs, all co-resident: grid <= #SMs) cannot
+    // deadlock; the last slice to finish resets the counters (stats[8] arrivals, stats[10] slices done).
+    DBG_T0(tsr);
+    TaskCursor rc;
+    rc.init(prefix, ntask, g0 < total ? g0 : total - 1);
+    for (int g = g0; g < g1; ++g) {
+      rc.advance(prefix, g);
+      const Task tk = tasks[rc.ti];
+      const int splits = (tk.rows + 7) / 8, nitem = splits * ng, item = g - rc.lo;
+      if (splits == 1) continue;
+      const ClientRec* c = recs + tk.rec;
+      int* arrive = reinterpret_cast<int*>(c->stats) + 8;
+      int* done = reinterpret_cast<int*>(c->stats) + 10;
+      if (threadIdx.x == 0)
+        while (atomicAdd(arrive, 0) < nitem) __nanosleep(256);
+      tc::named_sync(1, 256);
+      __threadfence();
+      float* P = c->params;
+      bf16* S = (bf16*)c->buf[B_WSH];
+      const float4* pt = (const float4*)c->buf[B_WSP];
+      constexpr int Q = kW2NP / 4, NE = 64 * Q;  // float4 chunks per split
+      const int e_lo = (int)((int64_t)item * NE / nitem), e_hi = (int)((int64_t)(item + 1) * NE / nitem);
+      for (int e = e_lo + threadIdx.x; e < e_hi; e += 256) {
+        float4 gs = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int sp = 0; sp < splits; ++sp) {
+          const float4 q = __ldcg(pt + (int64_t)sp * NE + e);
+          gs.x += q.x, gs.y += q.y, gs.z += q.z, gs.w += q.w;
+        }
+        const int co = e / Q, m0 = 4 * (e - co * Q);
+        if (m0 < 800) {
+          const int64_t idx = d.w2 + (int64_t)co * 800 + m0;
+          float4 w = *reinterpret_cast<const float4*>(P + idx);
+          w.x -= lr * gs.x, w.y -= lr * gs.y, w.z -= lr * gs.z, w.w -= lr * gs.w;
+          *reinterpret_cast<float4*>(P + idx) = w;
+          const __nv_bfloat162 h0 = __floats2bfloat162_rn(w.x, w.y), h1 = __floats2bfloat162_rn(w.z, w.w);
+          *reinterpret_cast<uint2*>(S + idx) =
+              make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+        } else if (m0 == 800) {
+          P[d.b2 + co] -= lr * gs.x;
+        }
+      }
+      tc::named_sync(1, 256);
+      if (threadIdx.x == 0 && atomicAdd(done, 1) == nitem - 1) {  // last slice: reset for the next step
+        *arrive = 0;
+        *done = 0;
+      }
+    }
+    if (warp == 0) DBG_ADD(9, tsr);
   }
   tc::fence_before();
   __syncthreads();
