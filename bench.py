@@ -285,9 +285,13 @@ def main():
 
     # ---- timed region (device time, CUDA events on the library's stream)
     clocks = ClockSampler(local) if rank == 0 else None
+    from paper_2207_01053_b200.monitor import UtilMonitor  # paper's UtilMonitor analogue (host side)
+    umon = UtilMonitor(device=local, interval=0.1) if rank == 0 else None
     barrier()
     if clocks:
         clocks.start()
+    if umon:
+        umon.start()
     launches = 0
     dom_ns = dom_fl = dom_by = dom_n = 0
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -311,6 +315,7 @@ def main():
     barrier()
     host_s = time.perf_counter() - host_t0
     clk = clocks.stop() if clocks else None
+    host_mon = umon.stop() if umon else None
     dev_ms = sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([dev_ms], dtype=torch.float64, device=sim.device)
     if world > 1:
@@ -388,7 +393,7 @@ def main():
                 "clocks": clk,
                 "detail": {"round_tflops": sum(int(f["flops"]) for f in foot) / (ms_per_step / 1e3) / 1e12,
                            "iterations_per_round": int(st["iterations"]), "host_wall_s": host_s,
-                           "probe_s": probe_s, "probe_step_ns": sorted({int(p["step_ns"]) for p in probe}),
+                           "probe_s": probe_s, "util_monitor": host_mon, "probe_step_ns": sorted({int(p["step_ns"]) for p in probe}),
                            "op_ms_warmup": {pb.OPC_NAMES[i]: op_stats["op_ns"][i] / 1e6 for i in range(pb.N_OPC)
                                             if op_stats and op_stats["op_ns"][i]},
                            "loss_mean_last_round": st["loss_sum"] / max(1, st["client_steps"])}}

@@ -57,6 +57,26 @@ class Simulation:
                              time_ops, partial_only)
         return global_out, r
 
+    def run_round_guarded(self, clients, profiles, global_in, global_out=None, caps=None, policy=POLICY_PROFILED,
+                          max_retries=8, backoff=2.0, **kw):
+        """Plan from ``profiles`` and run; if the library rejects the plan because a client's slot is smaller
+        than its high-water mark (stale or hand-made profile), apply the SPEC out-of-memory backoff to that
+        client (peak x ``backoff``, clamped to the capacity) and re-plan.  Returns (out, stats, profiles)."""
+        from . import ERR_OOM, ERR_PLAN, ProteaError
+        from .monitor import failed_client, oom_backoff
+        caps = [self.arena.numel()] if caps is None else caps
+        for _ in range(max_retries + 1):
+            plan, _mk = self.plan(profiles, caps=caps, policy=policy)
+            try:
+                out, st = self.run_round(clients, plan, global_in, global_out, **kw)
+                return out, st, profiles
+            except ProteaError as e:
+                cid = failed_client(str(e))
+                if e.code not in (ERR_OOM, ERR_PLAN) or cid is None or "HWM" not in str(e):
+                    raise
+                profiles = oom_backoff(profiles, cid, backoff, max(caps))
+        raise RuntimeError("run_round_guarded: out-of-memory backoff did not converge")
+
     def close(self):
         if self.ctx is not None:
             protea_finalize(self.ctx)

@@ -244,3 +244,30 @@ def test_config3_dirichlet_fp32(torch):
     got, _ = gpu_run(wl)
     ref = oracle_run(wl)
     assert rel_l2(got[4], ref[4]) <= FP32_TOL
+
+
+@pytest.mark.gpu
+def test_oom_backoff_guarded(torch):
+    """SPEC on_failure: a plan built from a profile that underestimates one client's
+    high-water mark is rejected before any device work (PLAN: slot < HWM); run_round_guarded doubles that
+    client's estimate until the plan fits and the round then equals the round run from exact profiles."""
+    from paper_2207_01053_b200.sim import Simulation, concat_globals
+    wl = synth.build_workload(2, n_clients=4, samples=24)
+    sim = Simulation(precision=1, arena_bytes=1 << 30)
+    mid = sim.register_model(wl.model, 4, wl.classes, 32, 32, 3)
+    sim.register_shards([(c.id, *wl.shards[c.id]) for c in wl.clients])
+    clients = sim.clients([(c.id, mid, c.batch, c.epochs) for c in wl.clients])
+    prof = sim.profile(clients)
+    g = torch.tensor(concat_globals([synth.init_weights(wl.model, 4, wl.classes)]), device="cuda")
+    plan, _ = sim.plan(prof)
+    ref, _ = sim.run_round(clients, plan, g.clone(), lr=0.05, seed=wl.seed, rnd=0)
+    bad = prof.copy()
+    victim = int(bad[1]["client_id"])
+    bad[1]["peak_bytes"] = int(bad[1]["peak_bytes"]) // 5  # stale estimate: needs three doublings
+    out, st, fixed = sim.run_round_guarded(clients, bad, g.clone(), lr=0.05, seed=wl.seed, rnd=0)
+    assert int(fixed[1]["peak_bytes"]) >= int(prof[1]["peak_bytes"])
+    assert int(fixed[1]["peak_bytes"]) == (int(prof[1]["peak_bytes"]) // 5) * 8
+    assert int(fixed[0]["peak_bytes"]) == int(prof[0]["peak_bytes"])  # other clients unaffected
+    assert victim == int(fixed[1]["client_id"])
+    assert torch.equal(out, ref)
+    sim.close()
