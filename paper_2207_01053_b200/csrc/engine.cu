@@ -109,7 +109,7 @@ struct protea_ctx {
   // programmatic dependent launch on the lock-step stream (PROTEA_PDL=1).  Off by default: measured on
   // B200, config 2: 70.2 ms/round without, 71.5 ms with (early CTAs of the next kernel hold SM resources).
   bool pdl = false;
-  int64_t overlap_rows = 640;      // defer when the iteration's total rows are at most this (PROTEA_OVERLAP_ROWS)
+  int64_t overlap_rows = int64_t(1) << 40;  // defer when the iteration has at most this many rows (PROTEA_OVERLAP_ROWS); measured best: always
   // per-op-class accounting of the current round (protea_round_stats)
   uint32_t time_ops = 0;
   std::vector<cudaEvent_t> evpool;
