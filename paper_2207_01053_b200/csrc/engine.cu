@@ -167,7 +167,6 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
   {
     const uint64_t d[4] = {C2, 16, 16, Bk}, st[3] = {C2 * 2, 32 * C2, 512 * C2};
     const uint32_t b8[4] = {8, 16, 8, 1}, b4[4] = {8, 16, 4, 1}, b12[4] = {8, 16, 12, 1}, w12[4] = {32, 16, 12, 1};
-    ok &= tmap_encode(&out[TM_DZ2], r.buf[B_DZ2], 4, d, st, b8);
     ok &= tmap_encode(&out[TM_DZ2W], r.buf[B_DZ2], 4, d, st, b4);
     if (C2 >= 32)
       ok &= tmap_encode(&out[TM_DZ2H], r.buf[B_DZ2], 4, d, st, w12, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -195,13 +194,9 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
     const uint32_t bx[2] = {64, (uint32_t)R};
     ok &= tmap_encode(&out[TM_A2], r.buf[B_A2], 2, d, st, bx, CU_TENSOR_MAP_SWIZZLE_128B);
   }
-  if (C1 == 32 && C2 == 64) {
+  if (C1 == 32 && C2 == 64) {  // width 1: single-halo conv2 kernels (kernels_conv.cuh)
     const uint64_t d1[4] = {C1, 16, 16, Bk}, s1[3] = {C1 * 2, 32 * C1, 512 * C1};
-    const uint32_t b1[4] = {32, 16, 4, 1};
-    ok &= tmap_encode(&out[TM_A1WS], r.buf[B_A1], 4, d1, s1, b1, CU_TENSOR_MAP_SWIZZLE_64B);
     const uint64_t d2[4] = {C2, 16, 16, Bk}, s2[3] = {C2 * 2, 32 * C2, 512 * C2};
-    const uint32_t b2[4] = {64, 16, 4, 1};
-    ok &= tmap_encode(&out[TM_DZ2WS], r.buf[B_DZ2], 4, d2, s2, b2, CU_TENSOR_MAP_SWIZZLE_128B);
     const uint32_t bq1[4] = {32, 12, 20, 1}, bq2[4] = {64, 8, 16, 1};
     ok &= tmap_encode(&out[TM_A1Q], r.buf[B_A1], 4, d1, s1, bq1, CU_TENSOR_MAP_SWIZZLE_64B);
     ok &= tmap_encode(&out[TM_DZ2Q], r.buf[B_DZ2], 4, d2, s2, bq2, CU_TENSOR_MAP_SWIZZLE_128B);

@@ -471,120 +471,6 @@ struct CnnW {
 // CNN ops on tensor cores (bf16 activations, bf16 shadow weights B_WSH)
 // --------------------------------------------------------------------------
 template <int WQ>
-struct TcConv2Fwd {
-  typedef CnnW<WQ> W;
-  static constexpr bool A_MN = false, B_MN = false;
-  struct PA { const bf16* base; int y, x, j; };
-  struct PB { const bf16* row; int j; };
-  const ClientRec* recs;
-  CnnDims d;
-  __device__ void setup(TcTile& t, int local) const {
-    t.m0 = local * 128;
-    t.n0 = 0;
-    t.nk = (25 * W::C1 + 63) / 64;
-    t.n_mma = W::C2 < 16 ? 16 : W::C2;
-  }
-  __device__ const void* any(const TcTile& t) const { return t.c->params; }
-  __device__ PA a_pre(const TcTile& t, int i, int j) const {
-    const int m = t.m0 + i, r = m >> 8, p = (m >> 2) & 63, q = m & 3;
-    return PA{(const bf16*)t.c->buf[B_A1] + (int64_t)r * 256 * W::C1, ((p >> 3) << 1) + (q >> 1),
-              ((p & 7) << 1) + (q & 1), j};
-  }
-  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
-    const int k = kb * 64 + 8 * s.j;
-    if (k >= 25 * W::C1) return nullptr;
-    const int tap = k >> W::L1, ci = k & (W::C1 - 1), ky = tap / 5, kx = tap - ky * 5;
-    const int sy = s.y + ky - 2, sx = s.x + kx - 2;
-    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return nullptr;
-    return s.base + (sy * 16 + sx) * W::C1 + ci;
-  }
-  __device__ PB b_pre(const TcTile& t, int i, int j) const {
-    return PB{i < W::C2 ? (const bf16*)t.c->buf[B_WSH] + d.w2 + (int64_t)i * 25 * W::C1 : nullptr, j};
-  }
-  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
-    const int k = kb * 64 + 8 * s.j;
-    if (!s.row || k >= 25 * W::C1) return nullptr;
-    return s.row + k;
-  }
-  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
-    const int m = t.m0 + row, r = m >> 8, p = (m & 255) >> 2, q = m & 3;
-    const int base = (threadIdx.x & 31) & ~3;
-    bf16* a2 = (bf16*)t.c->buf[B_A2];
-    uint8_t* i2 = (uint8_t*)t.c->buf[B_I2];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int n = c0 + j;
-      const float val = n < W::C2 ? fmaxf(v[j] + t.c->params[d.b2 + n], 0.f) : 0.f;
-      const float v0 = __shfl_sync(0xffffffffu, val, base), v1 = __shfl_sync(0xffffffffu, val, base + 1);
-      const float v2 = __shfl_sync(0xffffffffu, val, base + 2), v3 = __shfl_sync(0xffffffffu, val, base + 3);
-      if (q == 0 && n < W::C2) {
-        float best = v0;
-        int arg = 0;
-        if (v1 > best) { best = v1; arg = 1; }
-        if (v2 > best) { best = v2; arg = 2; }
-        if (v3 > best) { best = v3; arg = 3; }
-        const int64_t o = ((int64_t)r * 64 + p) * W::C2 + n;
-        a2[o] = __float2bfloat16_rn(best);
-        i2[o] = (uint8_t)arg;
-      }
-    }
-  }
-};
-
-template <int WQ>
-struct TcConv2Dgrad {
-  typedef CnnW<WQ> W;
-  static constexpr bool A_MN = false, B_MN = true;
-  struct PA { const bf16* base; int y, x, j; };
-  struct PB { int i, n0; };
-  const ClientRec* recs;
-  CnnDims d;
-  __device__ void setup(TcTile& t, int local) const {
-    t.m0 = local * 128;
-    t.n0 = 0;
-    t.nk = (25 * W::C2 + 63) / 64;
-    t.n_mma = W::C1 < 16 ? 16 : W::C1;
-  }
-  __device__ const void* any(const TcTile& t) const { return t.c->params; }
-  __device__ PA a_pre(const TcTile& t, int i, int j) const {
-    const int m = t.m0 + i, r = m >> 8;
-    return PA{(const bf16*)t.c->buf[B_DZ2] + (int64_t)r * 256 * W::C2, (m >> 4) & 15, m & 15, j};
-  }
-  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
-    const int k = kb * 64 + 8 * s.j;
-    if (k >= 25 * W::C2) return nullptr;
-    const int tap = k >> W::L2, co = k & (W::C2 - 1), ky = tap / 5, kx = tap - ky * 5;
-    const int sy = s.y - ky + 2, sx = s.x - kx + 2;
-    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return nullptr;
-    return s.base + (sy * 16 + sx) * W::C2 + co;
-  }
-  __device__ PB b_pre(const TcTile& t, int i, int j) const { return PB{i, 8 * j}; }
-  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
-    const int k = kb * 64 + s.i;
-    if (k >= 25 * W::C2 || s.n0 >= W::C1) return nullptr;
-    const int tap = k >> W::L2, co = k & (W::C2 - 1);
-    return (const bf16*)t.c->buf[B_WSH] + d.w2 + (co * 25 + tap) * W::C1 + s.n0;
-  }
-  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
-    constexpr int N = W::C1 < 16 ? W::C1 : 16;  // valid channels in this 16-column chunk
-    const int m = t.m0 + row, r = m >> 8, y = (m >> 4) & 15, x = m & 15;
-    const int64_t o = (int64_t)m * W::C1 + c0;
-    float a[N], out[N];
-    int arg[N];
-    ld_bf16<N>((const bf16*)t.c->buf[B_A1] + o, a);
-    ld_u8<N>((const uint8_t*)t.c->buf[B_I1] + o, arg);
-    bf16* dz1 = (bf16*)t.c->buf[B_DZC1];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-#pragma unroll
-      for (int j = 0; j < N; ++j) out[j] = (arg[j] == q && a[j] > 0.f) ? v[j] : 0.f;
-      const int Y = 2 * y + (q >> 1), X = 2 * x + (q & 1);
-      st_bf16<N>(dz1 + ((int64_t)r * 1024 + Y * 32 + X) * W::C1 + c0, out);
-    }
-  }
-};
-
-template <int WQ>
 struct TcConv2Wgrad {  // full reduction in one CTA -> SGD update in the epilogue (no split-K partials)
   typedef CnnW<WQ> W;
   static constexpr bool A_MN = true, B_MN = true;
@@ -786,7 +672,6 @@ struct TcFc1Wgrad {  // M = K1 (input features), N = F (outputs), K = rows; W <-
 enum TmapId : int {
   TM_A1 = 0,   // a1  [B][16][16][C1] box (8,16,8,1)   conv2 fwd A
   TM_A1W,      // a1                box (8,16,4,1)   conv2 wgrad A
-  TM_DZ2,      // dz2 [B][16][16][C2] box (8,16,8,1) conv2 dgrad A
   TM_DZ2W,     // dz2               box (8,16,4,1)   conv2 wgrad B
   TM_W2F,      // W2 shadow (25C1, C2)   box (8, C2) conv2 fwd B
   TM_W2D,      // W2 shadow (C1, 25, C2) box (8,1,C2) conv2 dgrad B
@@ -797,8 +682,6 @@ enum TmapId : int {
   TM_A1H,      // a1                box (8,16,12,1)  conv2 fwd halo (kernels_conv.cuh)
   TM_DZ2H,     // dz2               box (8,16,12,1)  conv2 dgrad halo
   TM_XSH,      // xs [B][36 Y][2 par][18 X' x 8] box (80,2,36,1)  conv1 fwd halo (kernels_conv.cuh)
-  TM_A1WS,     // a1  box (32,16,4,1)  64B-swizzled    conv2 wgrad A (width 1)
-  TM_DZ2WS,    // dz2 box (64,16,4,1)  128B-swizzled   conv2 wgrad B (width 1)
   TM_XSW,      // xs                box (64,1,36,1)  conv1 wgrad: one x-shifted copy per dx
   TM_G,        // g1 [B][16][16][4 q][C1] box (64,8,16,1) 128B-swizzled  conv1 wgrad A (MN-major)
   TM_A1Q,      // a1  box (32,12,20,1) 64B-swizzled   conv2 wgrad single halo (width 1)
@@ -857,33 +740,6 @@ struct TmaConv2Fwd {  // M = rows*256 (natural order, tile = 8 image rows), N = 
       st_bf16<N>((bf16*)t.c->buf[B_A2] + o, best);
       st_u8<N>((uint8_t*)t.c->buf[B_I2] + o, arg);
     }
-  }
-};
-
-template <int WQ>
-struct TmaConv2Dgrad : TcConv2Dgrad<WQ> {  // same GEMM and epilogue, operands by TMA
-  typedef CnnW<WQ> W;
-  static constexpr bool TMA = true;
-  __device__ void init_stage(const TcTile&, uint8_t*, uint8_t*) const {}
-  __device__ uint32_t tx_bytes(const TcTile& t, int kb) const { return 16384 + (uint32_t)t.n_mma * 128; }
-  __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
-    const int r = t.m0 >> 8, y0 = (t.m0 >> 4) & 15;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int k = kb * 64 + 8 * j, tap = k >> W::L2, cc = k & (W::C2 - 1), ky = tap / 5, kx = tap - ky * 5;
-      tc::tma_load_4d(a + 2048 * j, tmap_of(t, TM_DZ2), mbar, cc, 2 - kx, tap < 25 ? y0 + 2 - ky : -64, r);
-    }
-    constexpr int NTB = 64 / W::C2;  // taps per K block
-#pragma unroll
-    for (int tb = 0; tb < NTB; ++tb)
-      for (int nc = 0; nc < t.n_mma / 8; ++nc)
-        tc::tma_load_3d(b + 1024 * nc + 16 * W::C2 * tb, tmap_of(t, TM_W2D), mbar, 8 * nc, kb * NTB + tb, 0);
-  }
-  __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {
-    return tc::sdesc(base + 4096 * ks, 2048, 128);
-  }
-  __device__ uint64_t b_desc(const TcTile&, uint32_t base, int ks) const {
-    return tc::sdesc(base + 256 * ks, 128, 1024);  // MN-major: k rows at 16 B, n chunks at 1 KB
   }
 };
 
@@ -966,44 +822,6 @@ struct TmaConv2Wgrad : TcConv2Wgrad<WQ> {  // split-K over 2048-pixel chunks -> 
       }
     }
     if (threadIdx.x == 0) *cnt = 0;
-  }
-};
-
-// conv2 wgrad, width 1 (C1 = 32, C2 = 64): one 64-byte-swizzled box per tap (32 ci x 64 px) for A
-// (MN-major SW64: 32-element MN blocks 4 KB apart = one tap each) and one 128-byte-swizzled box
-// (64 co x 64 px) for B, instead of 24 16-byte-row boxes per K block.
-struct TmaConv2WgradSW : TmaConv2Wgrad<4> {
-  typedef CnnW<4> W;
-  __device__ void init_stage(const TcTile& t, uint8_t* a, uint8_t* b) const {
-    for (int g = 0; g < 4; ++g) {
-      const int tap = (t.m0 >> 5) + g;
-      if (tap < 25) continue;
-      for (int i = threadIdx.x; i < 64 * 4; i += kTcProd) {  // 64 pixel rows x 4 chunks of 16 B
-        const int r = i >> 2, c = i & 3;  // physical chunk c holds logical chunk c ^ ((r >> 1) & 3)
-        const bool one = tap == 25 && c == ((r >> 1) & 3);
-        reinterpret_cast<uint4*>(a + 4096 * g)[i] = one ? make_uint4(0x3F80u, 0, 0, 0) : make_uint4(0, 0, 0, 0);
-      }
-    }
-  }
-  __device__ uint32_t tx_bytes(const TcTile& t, int kb) const {
-    const int valid = 25 - (t.m0 >> 5);
-    return 4096u * (valid < 4 ? (valid < 0 ? 0 : valid) : 4) + 8192u;
-  }
-  __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
-    const int kg = t.n0 * (kWgradChunkPx / 64) + kb, r = kg >> 2, y0 = (kg & 3) * 4;
-    for (int g = 0; g < 4; ++g) {
-      const int tap = (t.m0 >> 5) + g;
-      if (tap >= 25) break;
-      const int ky = tap / 5, kx = tap - ky * 5;
-      tc::tma_load_4d(a + 4096 * g, tmap_of(t, TM_A1WS), mbar, 0, kx - 2, y0 + ky - 2, r);
-    }
-    tc::tma_load_4d(b, tmap_of(t, TM_DZ2WS), mbar, 0, 0, y0, r);
-  }
-  __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {
-    return tc::sdesc_sw64(base + 1024 * ks, 4096, 512);
-  }
-  __device__ uint64_t b_desc(const TcTile&, uint32_t base, int ks) const {
-    return tc::sdesc_sw128(base + 2048 * ks, 16, 1024);
   }
 };
 
