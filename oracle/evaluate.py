@@ -1,0 +1,44 @@
+"""Client evaluation (forward only), float64 — oracle, test infrastructure only.
+
+SURVEY §8(f).3: each client evaluates the global model on its held-out
+validation split (§4.1: the clients' data is split into training
+and validation sets; the evaluate round follows aggregation, §3.3).
+For a model w and samples (x, y):
+
+    loss_sum = sum_i [ logsumexp(z_i) - z_i[y_i] ]      (z_i = the model's logits)
+    correct  = #{ i : argmax_c z_i[c] == y_i }           (first maximum on ties)
+
+The forward pass is the one of oracle/sgd.py (readings R10/R11).
+"""
+import numpy as np
+
+from . import sgd
+
+
+def logits(w, model, width_q, classes, x_u8):
+    """x_u8 [n, H, W, C] u8 -> logits [n, classes] (float64)."""
+    p = sgd.unpack(np.asarray(w, dtype=np.float64), model, width_q, classes)
+    xb = np.asarray(x_u8, dtype=np.float64) / 255.0
+    nb = xb.shape[0]
+    if model == sgd.MLP:
+        h1 = sgd.relu(xb.reshape(nb, -1) @ p["fc1.W"].T + p["fc1.b"])
+        return h1 @ p["fc2.W"].T + p["fc2.b"]
+    if model == sgd.CNN:
+        z1, _ = sgd.conv_fwd(xb, p["conv1.W"], p["conv1.b"], 1, 2)
+        a1, _ = sgd.pool2_fwd(sgd.relu(z1))
+        z2, _ = sgd.conv_fwd(a1, p["conv2.W"], p["conv2.b"], 1, 2)
+        a2, _ = sgd.pool2_fwd(sgd.relu(z2))
+        h = sgd.relu(a2.reshape(nb, -1) @ p["fc1.W"].T + p["fc1.b"])
+        return h @ p["fc2.W"].T + p["fc2.b"]
+    raise ValueError("evaluate: MLP and CNN models only")
+
+
+def evaluate(w, model, width_q, classes, x_u8, y):
+    """-> (loss_sum, correct, n) of the model w on (x, y)."""
+    z = logits(w, model, width_q, classes, x_u8)
+    y = np.asarray(y, dtype=np.int64)
+    m = z.max(axis=1)
+    lse = np.log(np.exp(z - m[:, None]).sum(axis=1)) + m
+    loss_sum = float(np.sum(lse - z[np.arange(len(y)), y]))
+    correct = int(np.sum(np.argmax(z, axis=1) == y))  # numpy argmax = first maximum
+    return loss_sum, correct, len(y)
