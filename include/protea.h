@@ -212,6 +212,22 @@ protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clien
 protea_status protea_plan(const protea_profile* profiles, size_t n, const protea_cluster* cluster,
                           const protea_plan_opts* opts, protea_assignment* out, uint64_t* makespan_steps);
 
+/* Result of evaluating a model on a set of samples (§4.1: every client
+ * keeps a validation split; the evaluate round follows aggregation). */
+typedef struct {
+  double loss_sum;   /* sum over samples of the cross-entropy of the model's logits (fp32 forward, fp64 sum) */
+  uint64_t correct;  /* samples whose first-maximum logit is the label */
+  uint64_t n;        /* samples evaluated */
+} protea_eval_result;
+
+/* Evaluate registered model `model_id` (MLP or CNN-w) with `weights` (its n_params floats, host or device)
+ * on n samples: x u8 [n][H][W][C] NHWC and y int32 [n], both host, copied by the library.  The forward
+ * pass runs in fp32 on the verify-mode kernels over groups of 64 samples (one grouped launch per layer).
+ * loss_sum / n is the mean validation loss, correct / n the accuracy.  Errors: INVALID (unknown or
+ * ResNet model, n <= 0, null pointer, label outside [0, classes)), CUDA. */
+protea_status protea_evaluate(protea_ctx* ctx, int32_t model_id, const float* weights, const uint8_t* x,
+                              const int32_t* y, int64_t n, protea_eval_result* out);
+
 /* 64-bit FNV-1a hash of a round's client list and plan (every field of both arrays, in the given
  * order).  Pure host function.  protea_run_round with world > 1 compares it across ranks before
  * any device work (NCCL max of h and ~h, SURVEY §8(e) "plan agreement"); ranks that were given

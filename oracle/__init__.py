@@ -18,6 +18,8 @@ What it computes (PAPER.md = /root/reference/PAPER.md, line numbers "P:n"):
                as the available system resources can hold" (§3.2 (3)-(4)).
 * `round`    — one federated round: local SGD for every sampled client, then
                FedAvg per shape group (§3.3 configure_fit / aggregate_fit).
+* `evaluate` — forward-only evaluation of a model on a client's validation
+               split: loss sum and first-max accuracy (§4.1).
 
 Everything is float64 numpy (floating point) or Python ints (integers).
 Pins (tests/test_oracle_*.py) tie each function to something other than

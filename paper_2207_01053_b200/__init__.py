@@ -30,7 +30,8 @@ ORDER_ASC_ID, ORDER_DESC_STEPS = 0, 1
 
 EXPORTS = ["protea_init", "protea_finalize", "protea_last_error", "protea_register_model", "protea_register_shards",
            "protea_profile_clients", "protea_plan", "protea_run_round", "protea_fedavg", "protea_client_footprint",
-           "protea_selftest_gemm", "protea_round_partial", "protea_round_finalize", "protea_plan_hash"]
+           "protea_selftest_gemm", "protea_round_partial", "protea_round_finalize", "protea_plan_hash",
+           "protea_evaluate"]
 
 
 class ProteaError(RuntimeError):
@@ -128,6 +129,7 @@ for _f in EXPORTS:
     if _f not in ("protea_finalize", "protea_last_error", "protea_plan_hash"):
         getattr(_lib, _f).restype = ctypes.c_int
 _lib.protea_plan_hash.argtypes = [_vp, _sz, _vp]
+_lib.protea_evaluate.argtypes = [_vp, ctypes.c_int32, _vp, _vp, _vp, ctypes.c_int64, _vp]
 _lib.protea_plan_hash.restype = ctypes.c_uint64
 
 
@@ -221,6 +223,21 @@ def protea_plan(profiles, caps, policy=POLICY_PROFILED, order=ORDER_ASC_ID, marg
     _check(_lib.protea_plan(profiles.ctypes.data, len(profiles), ctypes.byref(cl), ctypes.byref(po),
                             out.ctypes.data, mk.ctypes.data))
     return out, mk
+
+
+class EvalResult(ctypes.Structure):
+    _fields_ = [("loss_sum", ctypes.c_double), ("correct", ctypes.c_uint64), ("n", ctypes.c_uint64)]
+
+
+def protea_evaluate(ctx, model_id, weights, x, y):
+    """Evaluate model `model_id` with `weights` (float32 tensor/array, host or device) on u8 samples x
+    [n, H, W, C] and int32 labels y (host).  Returns (loss_sum, correct, n)."""
+    x = np.ascontiguousarray(x, dtype=np.uint8)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    r = EvalResult()
+    _check(_lib.protea_evaluate(ctx, model_id, _ptr(weights), x.ctypes.data, y.ctypes.data, len(y),
+                                ctypes.byref(r)), ctx)
+    return r.loss_sum, int(r.correct), int(r.n)
 
 
 def protea_plan_hash(clients, plan):

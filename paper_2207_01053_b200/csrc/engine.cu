@@ -94,6 +94,12 @@ struct protea_ctx {
   DevArray<double> acc;
   DevArray<ClientRec> recs;
   DevArray<int32_t> tab;
+  // protea_evaluate workspace (kept apart from the round's tables)
+  DevArray<ClientRec> ev_recs;
+  DevArray<int32_t> ev_tab;
+  DevArray<uint8_t> ev_ws;
+  DevArray<double> ev_loss;
+  DevArray<uint32_t> ev_ok;
   DevArray<const float*> ptrs;
   DevArray<double> wts;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -950,6 +956,11 @@ void protea_finalize(protea_ctx* ctx) {
   ctx->acc.release();
   ctx->recs.release();
   ctx->tab.release();
+  ctx->ev_recs.release();
+  ctx->ev_tab.release();
+  ctx->ev_ws.release();
+  ctx->ev_loss.release();
+  ctx->ev_ok.release();
   ctx->ptrs.release();
   ctx->wts.release();
   for (auto e : ctx->evpool) cudaEventDestroy(e);
@@ -1608,6 +1619,126 @@ protea_status protea_round_finalize(protea_ctx* ctx, const double* acc_sum, cons
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->have_partial = false;
+  return PROTEA_OK;
+}
+
+protea_status protea_evaluate(protea_ctx* ctx, int32_t model_id, const float* weights, const uint8_t* x,
+                              const int32_t* y, int64_t n, protea_eval_result* out) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  if (!weights || !x || !y || !out) return fail(ctx, PROTEA_ERR_INVALID, "evaluate: null pointer");
+  if (n <= 0) return fail(ctx, PROTEA_ERR_INVALID, "evaluate: n must be > 0");
+  if (model_id < 0 || model_id >= (int)ctx->groups.size()) return fail(ctx, PROTEA_ERR_INVALID, "evaluate: unknown model_id");
+  const ModelDims& m = ctx->groups[model_id].m;
+  if (m.arch != PROTEA_MODEL_CNN && m.arch != PROTEA_MODEL_MLP)
+    return fail(ctx, PROTEA_ERR_INVALID, "evaluate: MLP and CNN models only");
+  for (int64_t i = 0; i < n; ++i)
+    if (y[i] < 0 || y[i] >= m.classes)
+      return fail(ctx, PROTEA_ERR_INVALID, "evaluate: label of sample " + std::to_string(i) + " outside [0, classes)");
+  CK(cudaSetDevice(ctx->device));
+  constexpr int RB = 64;  // samples per group (one task of the grouped forward launches)
+  const int T = (int)cdiv(n, RB);
+  const int64_t D = m.in_dim(), P = m.P;
+  // per-group activation buffers (fp32 verify-mode layout, slot_layout sizes at batch RB)
+  const SlotLayout sl = slot_layout(m, RB, RB, 1, 4);
+  std::vector<int> used;
+  for (int b : {B_A1, B_I1, B_A2, B_I2, B_H, B_H1})
+    if (sl.used[b]) used.push_back(b);
+  uint64_t per = 0;
+  for (int b : used) per += align256(sl.size[b]);
+  const uint64_t off_w = 0, off_x = align256(4 * (uint64_t)P), off_y = off_x + align256((uint64_t)n * D),
+                 off_p = off_y + align256(4 * (uint64_t)n), off_a = off_p + align256(4 * (uint64_t)n);
+  CK(ctx->ev_ws.reserve(off_a + per * T));
+  uint8_t* ws = ctx->ev_ws.p;
+  cudaStream_t st = ctx->stream;
+  CK(cudaMemcpyAsync(ws + off_w, weights, 4 * (size_t)P, is_device_ptr(weights) ? cudaMemcpyDeviceToDevice
+                                                                                  : cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ws + off_x, x, (size_t)n * D, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ws + off_y, y, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+  std::vector<int32_t> ident(n);
+  for (int64_t i = 0; i < n; ++i) ident[i] = (int32_t)i;
+  CK(cudaMemcpyAsync(ws + off_p, ident.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+  std::vector<ClientRec> recs(T);
+  for (int t = 0; t < T; ++t) {
+    ClientRec& r = recs[t];
+    std::memset(&r, 0, sizeof(r));
+    r.params = (float*)(ws + off_w);
+    r.perm = (int32_t*)(ws + off_p);
+    r.x = ws + off_x;
+    r.y = (const int32_t*)(ws + off_y);
+    r.n = (int32_t)n;
+    r.B = RB;
+    r.E = 1;
+    r.nb = T;
+    r.P = P;
+    r.c1 = m.c1;
+    uint64_t o = off_a + per * t;
+    for (int b : used) {
+      r.buf[b] = ws + o;
+      o += align256(sl.size[b]);
+    }
+  }
+  // schedule table: T tasks (rec t, step 0, rows, base 64 t) and the forward ops' prefix arrays
+  const std::vector<int> ops = m.arch == PROTEA_MODEL_CNN ? std::vector<int>{OP_C1F, OP_C2F, OP_F1F}
+                                                          : std::vector<int>{OP_MF};
+  std::vector<int32_t> tab;
+  Launch L;
+  std::memset(&L, 0, sizeof(L));
+  L.ntask = T;
+  L.task_off = 0;
+  std::vector<int> rows(T);
+  for (int t = 0; t < T; ++t) {
+    rows[t] = (int)std::min<int64_t>(RB, n - (int64_t)t * RB);
+    tab.insert(tab.end(), {t, 0, rows[t], t * RB});
+  }
+  for (int op : ops) {
+    L.prefix_off[op] = (int64_t)tab.size();
+    int acc_t = 0;
+    for (int t = 0; t < T; ++t) {
+      tab.push_back(acc_t);
+      acc_t += tiles(m, op, rows[t], false);
+    }
+    tab.push_back(acc_t);
+    L.grid[op] = acc_t;
+  }
+  CK(ctx->ev_recs.reserve(T));
+  CK(ctx->ev_tab.reserve(tab.size()));
+  CK(ctx->ev_loss.reserve(T));
+  CK(ctx->ev_ok.reserve(T));
+  CK(cudaMemcpyAsync(ctx->ev_recs.p, recs.data(), T * sizeof(ClientRec), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->ev_tab.p, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, st));
+  const ClientRec* drecs = ctx->ev_recs.p;
+  const int32_t* dtab = ctx->ev_tab.p;
+  const Task* tasks = reinterpret_cast<const Task*>(dtab);
+  ctx->cur = st;
+  const uint32_t keep_time = ctx->time_ops;
+  ctx->time_ops = 0;
+  if (m.arch == PROTEA_MODEL_CNN) {
+    const CnnDims d = cnn_dims(m);
+    launch_gemm<Conv1Fwd<float, C1F_BM, C1F_BN>, C1F_BM, C1F_BN>(ctx, {drecs, d}, L, OP_C1F, dtab);
+    launch_gemm<Conv2Fwd<float, C2F_BM, C2F_BN>, C2F_BM, C2F_BN>(ctx, {drecs, d}, L, OP_C2F, dtab);
+    launch_gemm<Fc1Fwd<float, F1F_BM, F1F_BN>, F1F_BM, F1F_BN>(ctx, {drecs, d}, L, OP_F1F, dtab);
+    k_eval_head<float><<<T, 256, 0, st>>>(drecs, tasks, B_H, m.f, m.classes, d.w4, d.b4, ctx->ev_loss.p,
+                                          ctx->ev_ok.p);
+  } else {
+    const MlpDims d = mlp_dims(m);
+    launch_gemm<MlpFc1Fwd<float, MF_BM, MF_BN>, MF_BM, MF_BN>(ctx, {drecs, d}, L, OP_MF, dtab);
+    k_eval_head<float><<<T, 256, 0, st>>>(drecs, tasks, B_H1, 64, m.classes, d.w2, d.b2, ctx->ev_loss.p,
+                                          ctx->ev_ok.p);
+  }
+  ctx->time_ops = keep_time;
+  CK(cudaGetLastError());
+  std::vector<double> lo(T);
+  std::vector<uint32_t> ok(T);
+  CK(cudaMemcpyAsync(lo.data(), ctx->ev_loss.p, T * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ok.data(), ctx->ev_ok.p, T * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  out->loss_sum = 0.0;
+  out->correct = 0;
+  for (int t = 0; t < T; ++t) {  // fixed group order: deterministic
+    out->loss_sum += lo[t];
+    out->correct += ok[t];
+  }
+  out->n = (uint64_t)n;
   return PROTEA_OK;
 }
 

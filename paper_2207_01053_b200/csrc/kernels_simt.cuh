@@ -653,6 +653,61 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a, const Task* _
 // Every global load of a phase is independent of the phase's stores, so they are
 // issued together (the former per-row global-load loops were latency bound).
 // --------------------------------------------------------------------------
+// --------------------------------------------------------------------------
+// Evaluation head (protea_evaluate): one CTA per group of <= 64 samples: logits
+// z = h W^T + b (warp per (row, class), lanes over features), per-row CE loss and
+// first-maximum prediction, summed in row order (fp64 loss) into the group's slot.
+// --------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_eval_head(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, int hbuf, int F, int C,
+                int64_t w, int64_t b, double* __restrict__ loss_out, uint32_t* __restrict__ correct_out) {
+  __shared__ float z[64 * 64];
+  __shared__ float lossr[64];
+  __shared__ int okr[64];
+  const Task tk = tasks[blockIdx.x];
+  const ClientRec* c = recs + tk.rec;
+  const int rows = tk.rows;
+  const T* h = (const T*)c->buf[hbuf];
+  const float* W = c->params + w;
+  const float* bias = c->params + b;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int idx = warp; idx < rows * C; idx += 8) {
+    const int r = idx / C, cc = idx - r * C;
+    float s = 0.f;
+    for (int f = lane; f < F; f += 32) s = fmaf(ldv(h + (int64_t)r * F + f), W[(int64_t)cc * F + f], s);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) z[r * C + cc] = s + bias[cc];
+  }
+  __syncthreads();
+  if (threadIdx.x < rows) {
+    const int r = threadIdx.x, label = c->y[c->perm[tk.base + r]];
+    float mx = z[r * C];
+    int arg = 0;
+    for (int cc = 1; cc < C; ++cc)
+      if (z[r * C + cc] > mx) {
+        mx = z[r * C + cc];
+        arg = cc;
+      }
+    float s = 0.f;
+    for (int cc = 0; cc < C; ++cc) s += expf(z[r * C + cc] - mx);
+    lossr[r] = logf(s) + mx - z[r * C + label];
+    okr[r] = arg == label;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    uint32_t k = 0;
+    for (int r = 0; r < rows; ++r) {
+      s += (double)lossr[r];
+      k += okr[r];
+    }
+    loss_out[blockIdx.x] = s;
+    correct_out[blockIdx.x] = k;
+  }
+}
+
 constexpr int kHeadCnnThreads = 512;
 inline size_t head_cnn_smem(int F, int C) { return (size_t)(C * F + 64 * C + 64) * sizeof(float); }
 template <typename T>

@@ -7,8 +7,8 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import (PREC_FP32, POLICY_PROFILED, ORDER_ASC_ID, clients_array, protea_finalize, protea_init,
-               protea_plan, protea_profile_clients, protea_register_model, protea_register_shards,
+from . import (PREC_FP32, POLICY_PROFILED, ORDER_ASC_ID, clients_array, protea_evaluate, protea_finalize,
+               protea_init, protea_plan, protea_profile_clients, protea_register_model, protea_register_shards,
                protea_run_round)
 
 
@@ -56,6 +56,10 @@ class Simulation:
         r = protea_run_round(self.ctx, clients, plan, global_in, global_out, lr, seed, rnd, shuffle, measured,
                              time_ops, partial_only)
         return global_out, r
+
+    def evaluate(self, model_id, weights, x, y):
+        """Forward-only evaluation (loss_sum, correct, n) of `weights` of model `model_id` on (x, y)."""
+        return protea_evaluate(self.ctx, model_id, weights, x, y)
 
     def run_round_guarded(self, clients, profiles, global_in, global_out=None, caps=None, policy=POLICY_PROFILED,
                           max_retries=8, backoff=2.0, **kw):
