@@ -510,7 +510,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     op.load_b(t, sb, b_full);
   }
   pdl_wait();
-  pdl_trigger();
 
   if (warp == 8) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -610,6 +609,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       pc = pn;
     }
   }
+  pdl_trigger();  // main work done: let the next kernel's CTAs start on the SMs this grid frees
   tc::fence_before();
   __syncthreads();
   if (warp == 9) {
@@ -688,7 +688,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sb = tc::smem_u32(smem);
   pdl_wait();
-  pdl_trigger();
 
   if (warp == 8) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -784,6 +783,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       tc::named_sync(1, 256);
     }
   }
+  pdl_trigger();  // main work done: let the next kernel's CTAs start on the SMs this grid frees
   tc::fence_before();
   __syncthreads();
   if (warp == 9) {
@@ -882,7 +882,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   TaskCursor cur;
   cur.init(prefix, ntask, g0 < total ? g0 : total - 1);
   pdl_wait();
-  pdl_trigger();
 
   if (warp == 8) {
     if (lane == 0) {  // ---------------- TMA producer: per image half, the a1 halo + the dz2 tile
@@ -1065,6 +1064,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
     if (warp == 0) DBG_ADD(9, tsr);
   }
+  pdl_trigger();  // main work done: let the next kernel's CTAs start on the SMs this grid frees
   tc::fence_before();
   __syncthreads();
   if (warp == 9) {

@@ -141,7 +141,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
-  pdl_trigger();
 
   if constexpr (TMA) {
     if (warp == 0 && lane == 0) {
@@ -235,6 +234,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     __syncwarp();
   }
+  pdl_trigger();  // main work done: let the next kernel's CTAs start on the SMs this grid frees
   tc::fence_before();
   __syncthreads();
   if (warp == 8) {
@@ -297,7 +297,6 @@ __global__ void __launch_bounds__(kPersThreads, 1)
   TaskCursor cur;
   cur.init(prefix, ntask, g0 < total ? g0 : total - 1);
   pdl_wait();
-  pdl_trigger();
   if (warp == 9) {
     if (lane == 0) {  // ---------------- TMA producer
       int it = 0;
@@ -371,6 +370,7 @@ __global__ void __launch_bounds__(kPersThreads, 1)
       if constexpr (has_pfinish<Op>::value) op.pfinish(t);  // split-K: the last split reduces (epilogue warps)
     }
   }
+  pdl_trigger();  // main work done: let the next kernel's CTAs start on the SMs this grid frees
   tc::fence_before();
   __syncthreads();
   if (warp == 8) {
