@@ -273,8 +273,10 @@ def main():
     dominant, op_stats = None, None
     for w in range(args.warmup):
         plan, _ = pb.protea_plan(profiles, caps)
+        # the first warm-up round runs serialised (no side-stream overlap) with every op class timed: the
+        # per-op shares of that round are the ones a serialised ncu launch list of this command shows
         _, st = sim.run_round(all_clients, plan, g, g2, lr=wl.lr, seed=wl.seed, rnd=rnd,
-                              time_ops=(0xFFFFFFFF if w == 0 else 0))
+                              time_ops=(0xFFFFFFFF if w == 0 else 0), serialize=(w == 0))
         g, g2 = g2, g
         rnd += 1
         if w == 0:
@@ -351,7 +353,8 @@ def main():
             "frac": achieved / peak, "traffic": traffic,
             "peak_src": pk["src"] if bound != "alu" else f"derived: 148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
             "per_launch": {"flops": fl_per, "bytes": by_per, "avg_ns": avg_ns, "launches": dom_n},
-            "share_of_step": dom_ns / (dev_ms * 1e6 / 1.0) if world == 1 else None}
+            "share_of_step": dom_ns / (dev_ms * 1e6 / 1.0) if world == 1 else None,
+            "share_of_step_serialized": (op_stats["op_ns"][dominant] / max(1, op_stats["round_ns"])) if op_stats else None}
 
     # ---- e2e: through the public API with HOST buffers (H2D of shards + global weights, D2H of the result)
     e2e = None

@@ -157,6 +157,9 @@ typedef struct {
   uint32_t partial_only; /* 1: skip the cross-rank sum and the finalisation; keep this rank's fp64 FedAvg
                             partial (protea_round_partial) for a caller-side reduction (protea_round_finalize);
                             global_out is not written */
+  uint32_t serialize;    /* 1: every launch on the lock-step stream (no fc1-wgrad deferral to the side
+                            stream), so per-op CUDA-event times are the kernels' own, as in a serialised
+                            ncu launch list; 0: default overlap */
 } protea_round_opts;
 
 typedef struct {

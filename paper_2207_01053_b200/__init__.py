@@ -76,7 +76,8 @@ OPC_NAMES = ["conv1_fwd", "conv2_fwd", "fc1_fwd", "head", "fc1_dgrad", "fc1_wgra
 
 class RoundOpts(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_float), ("seed", ctypes.c_uint32), ("round", ctypes.c_uint32),
-                ("shuffle", ctypes.c_int32), ("time_ops", ctypes.c_uint32), ("partial_only", ctypes.c_uint32)]
+                ("shuffle", ctypes.c_int32), ("time_ops", ctypes.c_uint32), ("partial_only", ctypes.c_uint32),
+                ("serialize", ctypes.c_uint32)]
 
 
 class RoundStats(ctypes.Structure):
@@ -249,9 +250,9 @@ def protea_plan_hash(clients, plan):
 
 
 def protea_run_round(ctx, clients, plan, global_in, global_out, lr=0.05, seed=0, rnd=0, shuffle=True,
-                     measured=False, time_ops=0, partial_only=False):
+                     measured=False, time_ops=0, partial_only=False, serialize=False):
     """global_in / global_out: float32 torch tensors (cuda or cpu) or numpy arrays."""
-    o = RoundOpts(lr, seed, rnd, 1 if shuffle else 0, time_ops, 1 if partial_only else 0)
+    o = RoundOpts(lr, seed, rnd, 1 if shuffle else 0, time_ops, 1 if partial_only else 0, 1 if serialize else 0)
     st = RoundStats()
     n_params = global_in.numel() if hasattr(global_in, "numel") else global_in.size
     meas = np.zeros(len(clients), dtype=PROFILE_DT) if measured else None

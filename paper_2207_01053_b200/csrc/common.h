@@ -64,6 +64,7 @@ struct SlotLayout {
 
 // Split-K partition of the conv wgrad reductions (pixels per split).
 constexpr int kWgradChunkPx = 2048;
+constexpr int kW1QImages = 2;  // width-1 pool-quad conv1 wgrad: images per split (k_conv1_wgrad_q)
 int cnn_conv1_splits(int rows);
 int cnn_conv2_splits(int rows);
 

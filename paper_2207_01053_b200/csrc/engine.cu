@@ -115,9 +115,10 @@ struct protea_ctx {
   // programmatic dependent launch on the lock-step stream (PROTEA_PDL=1).  Off by default: measured on
   // B200, config 2: 70.2 ms/round without, 71.5 ms with (early CTAs of the next kernel hold SM resources).
   bool pdl = false;
-  int64_t overlap_rows = int64_t(1) << 40;  // defer when the iteration has at most this many rows (PROTEA_OVERLAP_ROWS); measured best: always
+  int64_t overlap_rows = 640;  // defer when the iteration has at most this many rows (PROTEA_OVERLAP_ROWS); measured best: 640
   // per-op-class accounting of the current round (protea_round_stats)
   uint32_t time_ops = 0;
+  bool serialize = false;  // this round: no side-stream deferral (protea_round_opts.serialize)
   std::vector<cudaEvent_t> evpool;
   size_t evused = 0;
   std::vector<int> ev_op;
@@ -359,7 +360,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
       case OP_STAGE: return cdiv(rows * 1296, kStageThreads);
       case OP_C1F: return rows * 2;  // persistent pool-quad kernel: 2 tiles of 128 pooled pixels per image
       case OP_C1W:  // width 1: persistent pool-quad kernel, one item per split; else 2 M tiles per split
-        return (m.width_q == 4 ? 1 : 2) * cdiv(rows * 1024, kWgradChunkPx);
+        return m.width_q == 4 ? cdiv(rows, kW1QImages) : 2 * cdiv(rows * 1024, kWgradChunkPx);
       case OP_C1R: return cdiv(76 * m.c1, kReduceBlock);
       case OP_C2F: return rows * 2;  // halo kernel (width >= 1/2) or TmaConv2Fwd: both 128-pixel tiles
       case OP_F1F: return m.f / 128;
@@ -444,7 +445,7 @@ void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, u
     return;
   }
   const uint64_t c1 = m.c1, c2 = m.c2, f = m.f, C = m.classes;
-  const uint64_t s1 = cdiv((int)(r * 1024), kWgradChunkPx), s2 = cdiv((int)(r * 256), kWgradChunkPx);
+  const uint64_t s1 = m.width_q == 4 && e == 2 ? cdiv((int)r, kW1QImages) : cdiv((int)(r * 1024), kWgradChunkPx), s2 = cdiv((int)(r * 256), kWgradChunkPx);
   uint64_t F = 0, B = 0;
   switch (op) {
     case OP_C1F: F = 2 * r * 1024 * c1 * 75; B = r * 3072 + 4 * c1 * 76 + r * 256 * c1 * (e + 1); break;
@@ -1239,7 +1240,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
       iter_rows[t] += std::min<int64_t>(c.B, c.n - j * c.B);
     }
   for (uint64_t t = 0; t < T; ++t) {
-    ctx->overlap_now = tc_mode && iter_rows[t] <= ctx->overlap_rows;
+    ctx->overlap_now = tc_mode && !ctx->serialize && iter_rows[t] <= ctx->overlap_rows;
     if (admits[t].second > 0) {
       const int* ids = dtab + admits[t].first;
       int64_t maxP = 0, maxn = 0;
@@ -1404,6 +1405,7 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
   CK(ctx->acc.reserve(Ptot + 1));
   CK(cudaMemsetAsync(ctx->acc.p, 0, (Ptot + 1) * 8, ctx->stream));
   reset_ops(ctx, opts->time_ops);
+  ctx->serialize = opts->serialize != 0;
   const uint64_t l0 = ctx->launches;
   uint64_t iters = 0;
   double* loss_dev = ctx->acc.p + Ptot;  // one extra fp64 after the accumulators: sum of step losses

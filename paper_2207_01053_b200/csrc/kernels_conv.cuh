@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 //   D[(q,co)][(dy,dx,ci)] = sum_p g1[p][q][co] * xs[2py+dy][2px+dx][ci]     (one GEMM, K = pooled pixels)
 //   dW1[co][ky][kx][ci]   = sum_q D[(q,co)][(ky+qy, kx+qx, ci)]            (fold in the epilogue)
 //   db1[co]               = sum_q D[(q,co)][(2+qy, 2+qx, 3)]               (staged channel 3 = 1 in the image)
-// Work item = (client, split of 2 images = kWgradChunkPx full-resolution pixels);
+// Work item = (client, split of kW1QImages images);
 // sub-tile = (image, column half) = 128 pooled pixels.  Per K step (16 pooled
 // pixels = 2 pooled rows): 6 MMAs (one per dy), M = 128 (q, co), N = 48 (dx, ci).
 // A = g1 sub-tile by TMA (two 64-row boxes, 128-byte swizzle, MN-major);
@@ -658,7 +658,6 @@ constexpr int kW1Smem = 2 * kW1Stage + kW1Fold + 256 + 1024;
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv1_wgrad_q(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks,
                     const int* __restrict__ prefix, int ntask, int64_t off_w, int64_t off_b, float lr) {
-  __shared__ int last_flag;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   float* S = reinterpret_cast<float*>(smem + 2 * kW1Stage);
@@ -697,7 +696,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         TcTile t;
         t.tk = tasks[ti];
         t.c = recs + t.tk.rec;
-        const int r0 = 2 * (g - __ldg(prefix + ti)), nsub = 2 * min(2, t.tk.rows - r0);
+        const int r0 = kW1QImages * (g - __ldg(prefix + ti)), nsub = 2 * min(kW1QImages, t.tk.rows - r0);
         for (int sub = 0; sub < nsub; ++sub, ++s) {
           const int buf = s & 1, r = r0 + (sub >> 1), h = sub & 1;
           const uint32_t gb = sb + buf * kW1Stage;
@@ -717,7 +716,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       int ti = ti0, s = 0, i = 0;
       for (int g = g0; g < g1; ++g, ++i) {
         ti = next_task(prefix, ntask, ti, g);
-        const int r0 = 2 * (g - __ldg(prefix + ti)), nsub = 2 * min(2, __ldg(&tasks[ti].rows) - r0);
+        const int r0 = kW1QImages * (g - __ldg(prefix + ti)), nsub = 2 * min(kW1QImages, __ldg(&tasks[ti].rows) - r0);
         if (i >= 1) tc::mbar_wait(acc_empty, (i - 1) & 1);
         tc::fence_after();
         for (int sub = 0; sub < nsub; ++sub, ++s) {
@@ -768,19 +767,34 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       float* part = (float*)c->buf[B_WSP] + (int64_t)split * 76 * 32;
       for (int e = threadIdx.x; e < 76 * 32; e += 256)
         part[e] = ((S[e] + S[2432 + e]) + S[2 * 2432 + e]) + S[3 * 2432 + e];
-      // the client's last split sums the partials in split order and applies SGD (counter stats[9])
-      const int splits = cdiv(tasks[ti].rows * 1024, kWgradChunkPx);
-      int* cnt = reinterpret_cast<int*>(c->stats) + 9;
+      // publish this split's partial (arrival counter stats[9])
       __threadfence();
       tc::named_sync(1, 256);
-      if (threadIdx.x == 0) last_flag = atomicAdd(cnt, 1) == splits - 1;
+      if (threadIdx.x == 0) atomicAdd(reinterpret_cast<int*>(c->stats) + 9, 1);
+    }
+    // Split reduce, distributed (as in k_conv2_wgrad_halo): split i of a client (of n) sums slice i of
+    // the 76 x C1 partial elements over all splits in split order and applies SGD to it.  It runs after
+    // ALL of this CTA's items (the client's other splits live on co-resident CTAs: no deadlock); the
+    // last slice to finish resets the counters (stats[9] arrivals, stats[11] slices done).
+    TaskCursor rc;
+    rc.init(prefix, ntask, g0 < total ? g0 : total - 1);
+    for (int g = g0; g < g1; ++g) {
+      rc.advance(prefix, g);
+      const ClientRec* c = recs + tasks[rc.ti].rec;
+      const int splits = cdiv(tasks[rc.ti].rows, kW1QImages), item = g - rc.lo;
+      int* arrive = reinterpret_cast<int*>(c->stats) + 9;
+      int* done = reinterpret_cast<int*>(c->stats) + 11;
+      if (threadIdx.x == 0)
+        while (atomicAdd(arrive, 0) < splits) __nanosleep(128);
       tc::named_sync(1, 256);
-      if (last_flag) {
-        __threadfence();
-        for (int e = threadIdx.x; e < 76 * 32; e += 256) conv1_reduce_update(c, splits, 32, off_w, off_b, lr, e);
-        if (threadIdx.x == 0) *cnt = 0;
+      __threadfence();
+      const int e_lo = item * 2432 / splits, e_hi = (item + 1) * 2432 / splits;
+      for (int e = e_lo + threadIdx.x; e < e_hi; e += 256) conv1_reduce_update(c, splits, 32, off_w, off_b, lr, e);
+      tc::named_sync(1, 256);
+      if (threadIdx.x == 0 && atomicAdd(done, 1) == splits - 1) {  // last slice: reset for the next step
+        *arrive = 0;
+        *done = 0;
       }
-      tc::named_sync(1, 256);
     }
   }
   pdl_trigger();  // main work done: let the next kernel's CTAs start on the SMs this grid frees
@@ -1038,11 +1052,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       constexpr int Q = kW2NP / 4, NE = 64 * Q;  // float4 chunks per split
       const int e_lo = (int)((int64_t)item * NE / nitem), e_hi = (int)((int64_t)(item + 1) * NE / nitem);
       for (int e = e_lo + threadIdx.x; e < e_hi; e += 256) {
+        float4 q[8];  // splits <= 8 (B <= 64): every load in flight at once, summed in split order
+#pragma unroll
+        for (int sp = 0; sp < 8; ++sp)
+          if (sp < splits) q[sp] = __ldcg(pt + (int64_t)sp * NE + e);
         float4 gs = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int sp = 0; sp < splits; ++sp) {
-          const float4 q = __ldcg(pt + (int64_t)sp * NE + e);
-          gs.x += q.x, gs.y += q.y, gs.z += q.z, gs.w += q.w;
-        }
+#pragma unroll
+        for (int sp = 0; sp < 8; ++sp)
+          if (sp < splits) gs.x += q[sp].x, gs.y += q[sp].y, gs.z += q[sp].z, gs.w += q[sp].w;
         const int co = e / Q, m0 = 4 * (e - co * Q);
         if (m0 < 800) {
           const int64_t idx = d.w2 + (int64_t)co * 800 + m0;

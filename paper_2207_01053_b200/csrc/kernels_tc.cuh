@@ -961,7 +961,14 @@ __device__ __forceinline__ void conv1_reduce_update(const ClientRec* c, int spli
   const int total = 76 * C1;
   const float* part = (const float*)c->buf[B_WSP];
   float g = 0.f;
-  for (int s = 0; s < splits; ++s) g += __ldcg(part + (int64_t)s * total + e);
+  for (int s0 = 0; s0 < splits; s0 += 8) {  // 8 independent loads in flight, summed in split order
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = s0 + j < splits ? __ldcg(part + (int64_t)(s0 + j) * total + e) : 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (s0 + j < splits) g += v[j];
+  }
   const int idx = e / C1, co = e - idx * C1;
   if (idx == 75) {
     c->params[off_b + co] -= lr * g;

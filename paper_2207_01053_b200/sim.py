@@ -50,11 +50,11 @@ class Simulation:
         return protea_plan(profiles, caps, policy, order, margin_permille, max_active)
 
     def run_round(self, clients, plan, global_in, global_out=None, lr=0.05, seed=0, rnd=0, shuffle=True,
-                  measured=False, time_ops=0, partial_only=False):
+                  measured=False, time_ops=0, partial_only=False, serialize=False):
         if global_out is None:
             global_out = self.torch.empty_like(global_in)
         r = protea_run_round(self.ctx, clients, plan, global_in, global_out, lr, seed, rnd, shuffle, measured,
-                             time_ops, partial_only)
+                             time_ops, partial_only, serialize)
         return global_out, r
 
     def evaluate(self, model_id, weights, x, y):

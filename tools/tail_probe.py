@@ -3,8 +3,9 @@
 Runs three rounds and prints per-op device time per lock-step iteration:
   full   — all 100 clients (the bench round),
   tail   — only the 25 B=8 clients (126 iterations of 200 rows: the tail's shape),
-  heavy  — 100 clients but E=1 and 128 samples each, B=(8,16,32,64) (front-loaded).
+  heavy  — 100 clients, E=1, n = 7 B each: 7 iterations of all 3000 rows.
 """
+import dataclasses
 import json
 import os
 import sys
@@ -47,6 +48,11 @@ def main():
     wl = synth.build_workload(2)
     res = [run(wl, {c.id for c in wl.clients}, "full"),
            run(wl, {c.id for c in wl.clients if c.batch == 8}, "tail (B=8 only)")]
+    # heavy: every client does 7 full batches (E=1, n = 7 B): 7 iterations of all 3000 rows
+    hv = synth.build_workload(2)
+    hv.clients = [dataclasses.replace(c, n=7 * c.batch, epochs=1) for c in hv.clients]
+    hv.shards = {c.id: (hv.shards[c.id][0][:c.n], hv.shards[c.id][1][:c.n]) for c in hv.clients}
+    res.append(run(hv, {c.id for c in hv.clients}, "heavy (100 clients x 7 full batches)"))
     for r in res:
         print(json.dumps(r))
 
