@@ -328,7 +328,7 @@ int rsplits(const Layer& l, int rows) { return cdiv(rows * l.hout * l.wout, kWgr
 
 // tensor-core tile shapes (bf16 mode): M tile = 128, BN per op, STAGES-deep ring
 constexpr int TC_C1F_BN = 32, TC_C1W_BN = 32, TC_C2F_BN = 64, TC_C2D_BN = 32, TC_C2W_BN = 64, TC_F1F_BN = 64, TC_F1D_BN = 64, TC_F1W_BN = 128;
-constexpr int TC_STAGES = 4, TC_F1W_STAGES = 1;
+constexpr int TC_STAGES = 4, TC_F1W_STAGES = 1, TC_F1F_STAGES = 8;
 // Join a group's deferred fc1 wgrad into the current stream (before anything that writes a2 / dh
 // or reads the fc1 weights: the next conv2 fwd, a release, the end of the round).
 void join_group(protea_ctx* ctx, int g) {
@@ -602,15 +602,17 @@ template <typename T>
 void launch_head_cnn(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const Task* tasks,
                      float lr) {
   const CnnDims d = cnn_dims(m);
-  const size_t smem = head_cnn_smem(m.f, m.classes);
+  const size_t staged = head_cnn_smem_staged(m.f, m.classes, sizeof(T));
+  const int stage_h = staged <= kHeadStageMax;
+  const size_t smem = stage_h ? staged : head_cnn_smem(m.f, m.classes);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_head_cnn<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)head_cnn_smem(512, 64));
+    cudaFuncSetAttribute(k_head_cnn<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHeadStageMax);
     attr = true;
   }
   HeadArgs ha{drecs, B_H, B_DH, m.f, m.classes, d.w4, d.b4, d.b3, lr};
   const int ev = op_begin(ctx, OP_HEAD, OP_HEAD);
-  launch_k(ctx, k_head_cnn<T>, L.ntask, kHeadCnnThreads, smem, ha, tasks);
+  launch_k(ctx, k_head_cnn<T>, L.ntask, kHeadCnnThreads, smem, ha, tasks, stage_h);
   op_end(ctx, ev);
 }
 
@@ -648,7 +650,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   else
     launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TmaConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
   // (a split-K persistent variant for light iterations measured slower: 7.2 -> 8.0 ms/round)
-  launch_gemm_tc<TC_F1F_BN, TC_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
+  launch_gemm_tc<TC_F1F_BN, TC_F1F_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
   launch_head_cnn<T>(ctx, m, L, drecs, tasks, lr);
   launch_gemm_persistent<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab, 2);
   // fc1 wgrad (HBM-bound RMW of the fp32 master + bf16 shadow) needs dh, a2 and the fc1 weights, which

@@ -710,9 +710,12 @@ __global__ void __launch_bounds__(256)
 
 constexpr int kHeadCnnThreads = 512;
 inline size_t head_cnn_smem(int F, int C) { return (size_t)(C * F + 64 * C + 64) * sizeof(float); }
+// + the client's activations h [64][F] staged in shared memory when that still fits (kHeadStageMax)
+constexpr size_t kHeadStageMax = 220 * 1024;
+inline size_t head_cnn_smem_staged(int F, int C, size_t esz) { return head_cnn_smem(F, C) + 64 * (size_t)F * esz; }
 template <typename T>
 __global__ void __launch_bounds__(kHeadCnnThreads)
-    k_head_cnn(HeadArgs a, const Task* __restrict__ tasks) {
+    k_head_cnn(HeadArgs a, const Task* __restrict__ tasks, int stage_h) {
   extern __shared__ float hsm[];
   pdl_wait();
   pdl_trigger();
@@ -727,6 +730,13 @@ __global__ void __launch_bounds__(kHeadCnnThreads)
   T* __restrict__ dh = (T*)c->buf[a.dhbuf];
   float* __restrict__ W = c->params + a.w;
   float* __restrict__ bias = c->params + a.b;
+  if (stage_h) {  // h read once with 16-byte loads (every row is re-read C + 2 times below)
+    T* hs = reinterpret_cast<T*>(lossr + 64);
+    const int n16 = rows * F * (int)sizeof(T) / 16;
+    for (int i = threadIdx.x; i < n16; i += kHeadCnnThreads)
+      reinterpret_cast<uint4*>(hs)[i] = __ldg(reinterpret_cast<const uint4*>(h) + i);
+    h = hs;
+  }
   for (int i = threadIdx.x; i < C * F; i += kHeadCnnThreads) Ws[i] = W[i];
   __syncthreads();
   // 1. logits

@@ -15,6 +15,10 @@ from paper_2207_01053_b200.sim import Simulation  # noqa: E402
 lib = ctypes.CDLL(os.path.join(ROOT, "paper_2207_01053_b200", "libprotea.so"))
 lib.protea_debug_counters.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
 wl = synth.build_workload(2)
+if "heavy" in sys.argv:  # every client 7 full batches, E=1: 7 iterations of all 3000 rows
+    import dataclasses
+    wl.clients = [dataclasses.replace(c, n=7 * c.batch, epochs=1) for c in wl.clients]
+    wl.shards = {c.id: (wl.shards[c.id][0][:c.n], wl.shards[c.id][1][:c.n]) for c in wl.clients}
 sim = Simulation(precision=pb.PREC_BF16, arena_bytes=4 << 30)
 mid = sim.register_model(pb.MODEL_CNN, 4, 10, 32, 32, 3)
 sim.register_shards([(c.id, *wl.shards[c.id]) for c in wl.clients])
@@ -34,7 +38,7 @@ sim.run_round(clients, plan, out, g, lr=wl.lr, seed=wl.seed, rnd=1)
 torch.cuda.synchronize()
 lib.protea_debug_counters(buf, 0)
 names = ["prod_wait_empty", "prod_issue", "mma_wait_acc_empty", "mma_wait_full", "mma_issue", "epi_wait_acc_full",
-         "epi_drain", "epi_finish", "cta_ns_total"]
+         "epi_drain", "epi_finish", "cta_ns_total", "split_reduce(c2w)"]
 for base, label in ((0, "conv2 wgrad halo"), (16, "conv2 fwd halo"), (32, "conv2 dgrad halo"), (48, "conv1 fwd quad")):
     print("==", label)
     for i, n in enumerate(names):
