@@ -246,8 +246,11 @@ def main():
     sim = Simulation(device=local, precision=prec, arena_bytes=arena_bytes, rank=rank, world=world, nccl_id=nccl_id)
     mid = sim.register_model(pb.MODEL_CNN, 4, 10, 32, 32, 3)
     tmpl = synth.class_templates(wl.shape, wl.classes, wl.seed)
-    shards = {c.id: synth.make_shard(tmpl, c.n, c.id, wl.seed) for c in mine}
-    sim.register_shards([(c.id, *shards[c.id]) for c in mine])
+    # every rank holds every sampled client's shard (HBM is ample; run_round takes n_k of all
+    # clients from the registry for the FedAvg denominator); the e2e timing re-sends only this rank's shards
+    all_shards = {c.id: synth.make_shard(tmpl, c.n, c.id, wl.seed) for c in wl.clients}
+    shards = {c.id: all_shards[c.id] for c in mine}
+    sim.register_shards([(c.id, *all_shards[c.id]) for c in wl.clients])
     all_clients = sim.clients([(c.id, mid, c.batch, c.epochs) for c in wl.clients])
     my_clients = sim.clients([(c.id, mid, c.batch, c.epochs) for c in mine])
 

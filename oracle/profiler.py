@@ -113,6 +113,8 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
                 ("r3", b * 64 * 64 * e), ("o3", b * 64 * 64 * e),
                 ("gap", b * 64 * e), ("dgap", b * 64 * 4),
                 ("g0", b * 1024 * 16 * e), ("g1", b * 1024 * 16 * e), ("g2", b * 1024 * 16 * e)]
+        if e == 2:  # bf16 mode: conv0 weight shadow padded to 8 input channels [16][9][8] (tensor cores)
+            out.append(("w0p", 16 * 9 * 8 * 2))
     else:
         raise ValueError(model)
     convs = conv_layers(model, width_q)

@@ -202,7 +202,9 @@ def loss_and_grad(p, model, xb, yb, emulate_bf16=False):
 
     emulate_bf16: round to bf16 exactly where the CUDA bf16 mode stores bf16
     (pooled / hidden activations, dh, the pre-activation gradients dz, and the
-    conv2 / fc1 weights read by the tensor cores); everything else float64."""
+    conv2 / fc1 weights read by the tensor cores; ResNet-8: every stored
+    activation and gradient, the staged input and every conv's weights); everything else
+    float64."""
     q = bf16 if emulate_bf16 else (lambda v: v)
     g = {}
     nb = xb.shape[0]
@@ -243,14 +245,17 @@ def loss_and_grad(p, model, xb, yb, emulate_bf16=False):
         g["conv1.W"], g["conv1.b"], _ = conv_bwd(dz1, xb.shape, cols1, q(p["conv1.W"]), 1, 2, False)
         return loss, g
     if model == RESNET8:
-        z0, cols0 = conv_fwd(xb, p["conv0.W"], p["conv0.b"], 1, 1)
-        a0 = relu(z0)
+        # emulate_bf16: the staged input, the stored activations (a0, each block's ra and output), the
+        # stored gradients (each block's ds and dza, dz0) and every conv's weights (tensor-core shadow)
+        z0, cols0 = conv_fwd(q(xb), q(p["conv0.W"]), p["conv0.b"], 1, 1)
+        a0 = q(relu(z0))
         caches = []
         a = a0
         for blk, stride in (("b1", 1), ("b2", 2), ("b3", 2)):
-            za, colsa = conv_fwd(a, p[blk + "a.W"], p[blk + "a.b"], stride, 1)
-            ra = relu(za)
-            zb, colsb = conv_fwd(ra, p[blk + "b.W"], p[blk + "b.b"], 1, 1)
+            Wa, Wb = q(p[blk + "a.W"]), q(p[blk + "b.W"])
+            za, colsa = conv_fwd(a, Wa, p[blk + "a.b"], stride, 1)
+            ra = q(relu(za))
+            zb, colsb = conv_fwd(ra, Wb, p[blk + "b.b"], 1, 1)
             cout = zb.shape[3]
             if stride == 1 and a.shape[3] == cout:
                 sc = a
@@ -259,8 +264,8 @@ def loss_and_grad(p, model, xb, yb, emulate_bf16=False):
                 sc = np.zeros(sub.shape[:3] + (cout,))
                 sc[..., :sub.shape[3]] = sub
             s = zb + sc
-            out = relu(s)
-            caches.append((blk, stride, a, za, colsa, ra, colsb, s))
+            out = q(relu(s))
+            caches.append((blk, stride, a, za, colsa, ra, colsb, s, Wa, Wb))
             a = out
         gap = a.mean(axis=(1, 2))
         z = gap @ p["fc.W"].T + p["fc.b"]
@@ -269,17 +274,17 @@ def loss_and_grad(p, model, xb, yb, emulate_bf16=False):
         dgap = dz @ p["fc.W"]
         HW = a.shape[1] * a.shape[2]
         dout = np.broadcast_to(dgap[:, None, None, :] / HW, a.shape).copy()
-        for blk, stride, a_in, za, colsa, ra, colsb, s in reversed(caches):
-            ds = dout * (s > 0)
-            g[blk + "b.W"], g[blk + "b.b"], dra = conv_bwd(ds, ra.shape, colsb, p[blk + "b.W"], 1, 1, True)
-            dza = dra * (za > 0)
-            g[blk + "a.W"], g[blk + "a.b"], da_in = conv_bwd(dza, a_in.shape, colsa, p[blk + "a.W"], stride, 1, True)
+        for blk, stride, a_in, za, colsa, ra, colsb, s, Wa, Wb in reversed(caches):
+            ds = q(dout * (s > 0))
+            g[blk + "b.W"], g[blk + "b.b"], dra = conv_bwd(ds, ra.shape, colsb, Wb, 1, 1, True)
+            dza = q(dra * (za > 0))
+            g[blk + "a.W"], g[blk + "a.b"], da_in = conv_bwd(dza, a_in.shape, colsa, Wa, stride, 1, True)
             if stride == 1 and a_in.shape[3] == ds.shape[3]:
                 da_in = da_in + ds
             else:
                 da_in[:, ::2, ::2, :] += ds[..., :a_in.shape[3]]
             dout = da_in
-        dz0 = dout * (z0 > 0)
+        dz0 = q(dout * (z0 > 0))
         g["conv0.W"], g["conv0.b"], _ = conv_bwd(dz0, xb.shape, cols0, p["conv0.W"], 1, 1, False)
         return loss, g
     raise ValueError(model)

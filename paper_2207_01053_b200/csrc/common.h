@@ -51,7 +51,9 @@ enum Buf : int {
   // CNN
   B_A1, B_I1, B_A2, B_I2, B_H, B_DH, B_DZ2, B_DZC1, B_XS, B_W1P, B_WSP,
   // ResNet-8
-  B_R_A0, B_R_R1, B_R_O1, B_R_R2, B_R_O2, B_R_R3, B_R_O3, B_R_GAP, B_R_DGAP, B_R_G0, B_R_G1, B_R_G2, B_R_WSP,
+  B_R_A0, B_R_R1, B_R_O1, B_R_R2, B_R_O2, B_R_R3, B_R_O3, B_R_GAP, B_R_DGAP, B_R_G0, B_R_G1, B_R_G2,
+  B_R_W0P,  // bf16 mode: conv0 weights padded to 8 input channels [16][9][8] (tensor-core operand)
+  B_R_WSP,
   B_COUNT
 };
 

@@ -18,6 +18,7 @@
 
 #include <array>
 #include <tuple>
+#include <type_traits>
 
 #include <algorithm>
 #include <cstdio>
@@ -36,6 +37,7 @@
 #include "kernels_tc.cuh"
 #include "kernels_conv.cuh"
 #include "kernels_resnet.cuh"
+#include "kernels_resnet_tc.cuh"
 
 namespace protea {
 
@@ -238,6 +240,7 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
 namespace {
 // Bracket one launch of op class `op` with CUDA events if requested.
 int op_begin(protea_ctx* ctx, int op, int raw = -1) {  // op: stats class; raw: launch op id (work lookup)
+  if (op < 0 || op >= PROTEA_N_OPC) op = PROTEA_N_OPC - 1;  // (defensive: never index past the stats arrays)
   ctx->op_launches[op]++;
   ctx->launches++;
   if (!((ctx->time_ops >> op) & 1u)) return -1;
@@ -341,16 +344,20 @@ void join_group(protea_ctx* ctx, int g) {
 int tiles(const ModelDims& m, int op, int rows, bool tc) {
   if (op >= RI_F0) {
     if (op == RI_HEAD) return 1;
+    // bf16 mode: every conv on tcgen05 (kernels_resnet_tc.cuh), 128-row tiles (conv0 on the staged input)
     if (op < RI_HEAD) {
       const Layer& l = m.layers[op - RI_F0];
+      if (tc) return cdiv(rows * l.hout * l.wout, 128);
       return cdiv(rows * l.hout * l.wout, R_BM) * cdiv(l.cout, R_BN);
     }
     if (op < RI_W0) {
       const Layer& l = m.layers[1 + op - RI_D1];
+      if (tc) return cdiv(rows * l.hin * l.win, 128);
       return cdiv(rows * l.hin * l.win, R_BM) * cdiv(l.cin, R_BN);
     }
     if (op < RI_R0) {
       const Layer& l = m.layers[op - RI_W0];
+      if (tc) return rsplits(l, rows) * cdiv(9 * (l.cin < 8 ? 8 : l.cin) + 1, 128);
       return rsplits(l, rows) * cdiv(l.cout, R_BM) * cdiv(9 * l.cin + 1, R_BN);
     }
     const Layer& l = m.layers[op - RI_R0];
@@ -525,7 +532,7 @@ void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, c
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int* prefix = dtab + L.prefix_off[opid];
-  const int ev = op_begin(ctx, opid, opid);
+  const int ev = op_begin(ctx, op_class(opid), opid);
   launch_k(ctx, k_gemm_tc<BN, STAGES, OpT>, L.grid[opid], kTcThreads, SMEM, op, tasks, prefix, L.ntask);
   op_end(ctx, ev);
 }
@@ -543,7 +550,7 @@ void launch_gemm_persistent(protea_ctx* ctx, const OpT& op, const Launch& L, int
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[opid], ctas_per_sm * g_num_sms);
-  const int ev = op_begin(ctx, opid, opid);
+  const int ev = op_begin(ctx, op_class(opid), opid);
   launch_k(ctx, k_gemm_persistent<BN, STAGES, OpT>, grid, kPersThreads, SMEM, op, tasks,
            (const int*)(dtab + L.prefix_off[opid]), L.ntask);
   op_end(ctx, ev);
@@ -562,7 +569,7 @@ void launch_conv_persistent(protea_ctx* ctx, const ClientRec* drecs, const CnnDi
   op.d = d;
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[opid], g_num_sms);  // one CTA per SM, each a contiguous tile range
-  const int ev = op_begin(ctx, opid, opid);
+  const int ev = op_begin(ctx, op_class(opid), opid);
   launch_k(ctx, k_conv_persistent<Op>, grid, kConvThreads, Op::SMEM, op, tasks, (const int*)(dtab + L.prefix_off[opid]),
            L.ntask);
   op_end(ctx, ev);
@@ -699,6 +706,27 @@ void launch_step_tc(protea_ctx* ctx, const ModelDims& m, const Launch& L, const 
     launch_step_tc_w<4>(ctx, m, L, drecs, dtab, lr);
 }
 
+int ilog2(int v) {
+  int r = 0;
+  while ((1 << (r + 1)) <= v) ++r;
+  return r;
+}
+RTcConv rtc(const Layer& l) {
+  RTcConv c;
+  c.H = l.hin;
+  c.W = l.win;
+  c.Cin = l.cin;
+  c.Cout = l.cout;
+  c.s = l.stride;
+  c.Ho = l.hout;
+  c.Wo = l.wout;
+  c.lci = ilog2(l.cin);
+  c.lco = ilog2(l.cout);
+  c.w = l.off_w;
+  c.b = l.off_b;
+  return c;
+}
+
 RConv rconv(const Layer& l) {
   RConv c;
   c.H = l.hin;
@@ -713,7 +741,13 @@ RConv rconv(const Layer& l) {
   return c;
 }
 
-// ResNet-8 step (SIMT; bf16 mode stores activations in bf16).  Buffers: a0 r1 o1 r2 o2 r3 o3, gradients
+void stage_r(protea_ctx* ctx, const ClientRec* drecs, const Task* tasks, const Launch& L, int out_buf) {
+  const int ev = op_begin(ctx, PROTEA_OPC_R_FWD);
+  k_stage_r<<<dim3(L.ntask, 16), 256, 0, ctx->cur>>>(drecs, tasks, out_buf);
+  op_end(ctx, ev);
+}
+
+// ResNet-8 step (fp32 verify: SIMT; bf16 mode: tcgen05 convs, kernels_resnet_tc.cuh, activations in bf16).  Buffers: a0 r1 o1 r2 o2 r3 o3, gradients
 // ping-pong g0 g1 g2; each layer's dgrad runs before its SGD update (old weights).
 template <typename T>
 void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs,
@@ -724,6 +758,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
   typedef RFwd<T, R_BM, R_BN> F;
   typedef RDgrad<T, R_BM, R_BN> D;
   typedef RWgrad<T, R_BM, R_BN> Wg;
+  constexpr bool TC = std::is_same<T, __nv_bfloat16>::value;  // bf16 mode: layers 1-6 on tcgen05
   for (int i = 0; i < 7; ++i) {
     F f;
     f.recs = drecs;
@@ -736,6 +771,18 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
     if (i == 2) { f.res_buf = B_R_A0; f.res_mode = 1; }                      // block 1: identity shortcut
     if (i == 4) { f.res_buf = B_R_O1; f.res_mode = 2; f.Cres = 16; }         // block 2: option A from o1
     if (i == 6) { f.res_buf = B_R_O2; f.res_mode = 2; f.Cres = 32; }         // block 3: option A from o2
+    if (TC) {
+      RTcFwd tf{drecs, rtc(m.layers[i]), f.in_buf, f.out_buf, f.res_buf, f.res_mode, f.Cres, B_WSH};
+      if (i == 0) {  // conv0: the u8 input staged as [r][32][32][8] bf16 into g2 (free until the backward)
+        stage_r(ctx, drecs, tasks, L, B_R_G2);
+        tf.L.Cin = 8;
+        tf.L.lci = 3;
+        tf.in_buf = B_R_G2;
+        tf.wbuf = B_R_W0P;
+      }
+      launch_gemm_tc<64, TC_STAGES>(ctx, tf, L, RI_F0 + i, dtab);
+      continue;
+    }
     launch_gemm<F, R_BM, R_BN>(ctx, f, L, RI_F0 + i, dtab);
   }
   const Layer& fc = m.layers[7];
@@ -766,15 +813,32 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
       dg.add_buf = bw[i].add;
       dg.add_mode = bw[i].add_mode;
       dg.Cadd = bw[i].cadd;
-      launch_gemm<D, R_BM, R_BN>(ctx, dg, L, RI_D1 + i - 1, dtab);
+      if (TC) {
+        RTcDgrad td{drecs, rtc(l), dg.dout_buf, dg.out_buf, dg.mask_buf, dg.add_buf, dg.add_mode, dg.Cadd};
+        launch_gemm_tc<64, TC_STAGES>(ctx, td, L, RI_D1 + i - 1, dtab);
+      } else {
+        launch_gemm<D, R_BM, R_BN>(ctx, dg, L, RI_D1 + i - 1, dtab);
+      }
     }
-    Wg wg;
-    wg.recs = drecs;
-    wg.L = rconv(l);
-    wg.dout_buf = wg_dout[i];
-    wg.in_buf = in_of[i];
-    launch_gemm<Wg, R_BM, R_BN>(ctx, wg, L, RI_W0 + i, dtab);
-    ReduceArgs ra{drecs, B_R_WSP, l.cout, 9 * l.cin, l.off_w, l.off_b, l.hout * l.wout, lr, 0};
+    if (TC) {
+      RTcWgrad tw{drecs, rtc(l), wg_dout[i], in_of[i], l.cin};
+      if (i == 0) {  // conv0: re-stage the input into g1 (free once b1a's dgrad has read it)
+        stage_r(ctx, drecs, tasks, L, B_R_G1);
+        tw.L.Cin = 8;
+        tw.L.lci = 3;
+        tw.in_buf = B_R_G1;
+      }
+      launch_gemm_tc<64, TC_STAGES>(ctx, tw, L, RI_W0 + i, dtab);
+    } else {
+      Wg wg;
+      wg.recs = drecs;
+      wg.L = rconv(l);
+      wg.dout_buf = wg_dout[i];
+      wg.in_buf = in_of[i];
+      launch_gemm<Wg, R_BM, R_BN>(ctx, wg, L, RI_W0 + i, dtab);
+    }
+    // the fp32 master and (bf16 mode) the tensor-core shadow
+    ReduceArgs ra{drecs, B_R_WSP, l.cout, 9 * l.cin, l.off_w, l.off_b, l.hout * l.wout, lr, TC ? (i == 0 ? 2 : 1) : 0};
     ev = op_begin(ctx, PROTEA_OPC_R_REDUCE, RI_R0 + i);
     k_reduce_update<<<L.grid[RI_R0 + i], kReduceBlock, 0, ctx->cur>>>(ra, tasks, dtab + L.prefix_off[RI_R0 + i],
                                                                          L.ntask);

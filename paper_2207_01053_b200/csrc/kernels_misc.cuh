@@ -28,6 +28,12 @@ __global__ void k_admit_params(const ClientRec* __restrict__ recs, const int* __
       w1q[e] = __float2bfloat16_rn(in ? c->wg[co * 75 + (ky * 5 + kx) * 3 + ci] : 0.f);
     }
   }
+  __nv_bfloat16* w0p = (__nv_bfloat16*)c->buf[B_R_W0P];  // ResNet conv0 [16][9][3] -> [16][9][8], W0 at offset 0
+  if (w0p)
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 16 * 72; e += gridDim.x * blockDim.x) {
+      const int ci = e & 7, tap = (e >> 3) % 9, co = e / 72;
+      w0p[e] = __float2bfloat16_rn(ci < 3 ? c->wg[co * 27 + tap * 3 + ci] : 0.f);
+    }
   if (blockIdx.x == 0 && threadIdx.x < 16) c->stats[threadIdx.x] = 0.f;
 }
 

@@ -1,0 +1,218 @@
+// kernels_resnet_tc.cuh — ResNet-8 (BASELINE.json configs[4]) 3x3 convolutions on tcgen05 (bf16 mode).
+//
+// Same model and data layout as kernels_resnet.cuh (reading R11: NHWC bf16 activations,
+// weights [cout][ky][kx][cin], pad 1, stride 1 or 2, option-A shortcut), run as implicit GEMMs on
+// the generic cp.async-fed tcgen05 GEMM (k_gemm_tc, kernels_tc.cuh): every 16-byte operand chunk is
+// 8 consecutive channels of one pixel (or 8 consecutive output channels of one weight row), gathered
+// straight from the client's slot; out-of-image taps and K padding are zero-filled by cp.async.
+// Weights come from the bf16 shadow (B_WSH), kept in step with the fp32 master by k_reduce_update.
+// Layers 1-6 (cin in {16, 32, 64}); conv0 (cin = 3 from the u8 image) stays on the SIMT kernels.
+//   fwd   M = rows*Ho*Wo out pixels, N = cout,  K = 9 cin        (A K-major, B K-major)
+//         epilogue: + bias (+ identity / option-A residual), ReLU -> bf16
+//   dgrad M = rows*H*W in pixels,   N = cin,   K = 9 cout       (A K-major, B MN-major)
+//         epilogue: (+ shortcut gradient) x ReLU mask of the stored activation -> bf16
+//   wgrad M = 9 cin + 1 (bias row), N = cout, K = 2048-pixel split (A, B MN-major)
+//         epilogue: partial[split][cout][9 cin + 1] (summed in split order + SGD by k_reduce_update)
+#pragma once
+#include "kernels_resnet.cuh"
+#include "kernels_tc.cuh"
+
+namespace protea {
+
+struct RTcConv {  // RConv + log2 of the channel counts
+  int H, W, Cin, Cout, s, Ho, Wo, lci, lco;
+  int64_t w, b;
+};
+
+struct RTcFwd {
+  static constexpr bool A_MN = false, B_MN = false;
+  struct PA { int r, y0, x0, j; };  // r < 0: row beyond M
+  struct PB { const bf16* p; int j; };
+  const ClientRec* recs;
+  RTcConv L;
+  int in_buf, out_buf, res_buf, res_mode, Cres;  // res_mode 1: identity, 2: option-A (2Ho x 2Wo x Cres)
+  int wbuf;                                      // weights [cout][9][cin] bf16: B_WSH at L.w, or B_R_W0P (conv0)
+  __device__ void setup(TcTile& t, int local) const {
+    t.m0 = local * 128;
+    t.n0 = 0;
+    t.nk = (9 * L.Cin + 63) / 64;
+    t.n_mma = L.Cout;
+  }
+  __device__ const void* any(const TcTile& t) const { return t.c->params; }
+  __device__ PA a_pre(const TcTile& t, int i, int j) const {
+    const int m = t.m0 + i, hw = L.Ho * L.Wo;
+    if (m >= t.tk.rows * hw) return PA{-1, 0, 0, j};
+    const int r = m / hw, rem = m - r * hw, yo = rem / L.Wo, xo = rem - yo * L.Wo;
+    return PA{r, yo * L.s - 1, xo * L.s - 1, j};
+  }
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
+    const int k = kb * 64 + 8 * s.j;
+    if (s.r < 0 || k >= 9 * L.Cin) return nullptr;
+    const int tap = k >> L.lci, ci = k & (L.Cin - 1), ky = tap / 3, kx = tap - 3 * ky;
+    const int y = s.y0 + ky, x = s.x0 + kx;
+    if ((unsigned)y >= (unsigned)L.H || (unsigned)x >= (unsigned)L.W) return nullptr;
+    return (const bf16*)t.c->buf[in_buf] + (((int64_t)s.r * L.H + y) * L.W + x) * L.Cin + ci;
+  }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const {
+    const bf16* w = (const bf16*)t.c->buf[wbuf] + (wbuf == B_WSH ? L.w : 0);
+    return PB{i < L.Cout ? w + (int64_t)i * 9 * L.Cin + 8 * j : nullptr, j};
+  }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
+    return s.p && kb * 64 + 8 * s.j < 9 * L.Cin ? s.p + kb * 64 : nullptr;
+  }
+  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
+    const int m = t.m0 + row, hw = L.Ho * L.Wo;
+    if (m >= t.tk.rows * hw) return;
+    const float* bias = t.c->params + L.b + c0;
+    float o[16], q[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) o[j] = v[j] + bias[j];
+    if (res_mode == 1) {
+      ld_bf16<16>((const bf16*)t.c->buf[res_buf] + (int64_t)m * L.Cout + c0, q);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) o[j] += q[j];
+    } else if (res_mode == 2 && c0 < Cres) {
+      const int r = m / hw, rem = m - r * hw, yo = rem / L.Wo, xo = rem - yo * L.Wo;
+      ld_bf16<16>((const bf16*)t.c->buf[res_buf] + (((int64_t)r * 2 * L.Ho + 2 * yo) * 2 * L.Wo + 2 * xo) * Cres + c0, q);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) o[j] += q[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) o[j] = fmaxf(o[j], 0.f);
+    st_bf16<16>((bf16*)t.c->buf[out_buf] + (int64_t)m * L.Cout + c0, o);
+  }
+};
+
+struct RTcDgrad {
+  static constexpr bool A_MN = false, B_MN = true;
+  struct PA { int r, y, x, j; };  // the input pixel of row i (r < 0: beyond M)
+  struct PB { int i, n0; };       // k row i of the block, 8 input channels from n0
+  const ClientRec* recs;
+  RTcConv L;
+  int dout_buf, out_buf, mask_buf, add_buf, add_mode, Cadd;
+  __device__ void setup(TcTile& t, int local) const {
+    t.m0 = local * 128;
+    t.n0 = 0;
+    t.nk = (9 * L.Cout + 63) / 64;
+    t.n_mma = L.Cin;
+  }
+  __device__ const void* any(const TcTile& t) const { return t.c->params; }
+  __device__ PA a_pre(const TcTile& t, int i, int j) const {
+    const int m = t.m0 + i, hw = L.H * L.W;
+    if (m >= t.tk.rows * hw) return PA{-1, 0, 0, j};
+    const int r = m / hw, rem = m - r * hw, y = rem / L.W;
+    return PA{r, y, rem - y * L.W, j};
+  }
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
+    const int k = kb * 64 + 8 * s.j;
+    if (s.r < 0 || k >= 9 * L.Cout) return nullptr;
+    const int tap = k >> L.lco, co = k & (L.Cout - 1), ky = tap / 3, kx = tap - 3 * ky;
+    int ty = s.y - ky + 1, tx = s.x - kx + 1;
+    if (L.s == 2) {
+      if ((ty | tx) & 1) return nullptr;
+      ty >>= 1;
+      tx >>= 1;
+    }
+    if ((unsigned)ty >= (unsigned)L.Ho || (unsigned)tx >= (unsigned)L.Wo) return nullptr;
+    return (const bf16*)t.c->buf[dout_buf] + (((int64_t)s.r * L.Ho + ty) * L.Wo + tx) * L.Cout + co;
+  }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const { return PB{i, 8 * j}; }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
+    const int k = kb * 64 + s.i;
+    if (k >= 9 * L.Cout || s.n0 >= L.Cin) return nullptr;
+    const int tap = k >> L.lco, co = k & (L.Cout - 1);
+    return (const bf16*)t.c->buf[B_WSH] + L.w + ((int64_t)co * 9 + tap) * L.Cin + s.n0;
+  }
+  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
+    const int m = t.m0 + row, hw = L.H * L.W;
+    if (m >= t.tk.rows * hw) return;
+    const int64_t o = (int64_t)m * L.Cin + c0;
+    float a[16], q[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = v[j];
+    if (add_mode == 1) {
+      ld_bf16<16>((const bf16*)t.c->buf[add_buf] + o, q);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) a[j] += q[j];
+    } else if (add_mode == 2) {
+      const int r = m / hw, rem = m - r * hw, y = rem / L.W, x = rem - y * L.W;
+      if (((y | x) & 1) == 0) {
+        ld_bf16<16>((const bf16*)t.c->buf[add_buf] + (((int64_t)r * (L.H / 2) + y / 2) * (L.W / 2) + x / 2) * Cadd + c0, q);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] += q[j];
+      }
+    }
+    ld_bf16<16>((const bf16*)t.c->buf[mask_buf] + o, q);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = q[j] > 0.f ? a[j] : 0.f;
+    st_bf16<16>((bf16*)t.c->buf[out_buf] + o, a);
+  }
+};
+
+struct RTcWgrad {
+  static constexpr bool A_MN = true, B_MN = true;
+  struct PA { int i, dy, dx, ci, kind; };  // kind 0: gather, 1: bias ones row, 2: zero
+  struct PB { int i, n0; };
+  const ClientRec* recs;
+  RTcConv L;
+  int dout_buf, in_buf;
+  int cin_real;  // channels of the weight layout (conv0: 3 real of the 8 staged; else Cin)
+  __device__ int mtiles() const { return (9 * L.Cin + 1 + 127) / 128; }
+  __device__ void setup(TcTile& t, int local) const {
+    const int mt = mtiles(), split = local / mt, px = t.tk.rows * L.Ho * L.Wo - split * kWgradChunkPx;
+    t.m0 = (local - split * mt) * 128;
+    t.n0 = split;  // the split index (K = this split's pixels)
+    t.nk = ((px < kWgradChunkPx ? px : kWgradChunkPx) + 63) / 64;
+    t.n_mma = L.Cout;
+  }
+  __device__ const void* any(const TcTile& t) const { return t.c->params; }
+  __device__ PA a_pre(const TcTile& t, int i, int j) const {
+    const int mg = t.m0 + 8 * j, Kw = 9 * L.Cin;
+    if (mg == Kw) return PA{i, 0, 0, 0, 1};
+    if (mg > Kw) return PA{i, 0, 0, 0, 2};
+    const int tap = mg >> L.lci, ky = tap / 3, kx = tap - 3 * ky;
+    return PA{i, ky - 1, kx - 1, mg & (L.Cin - 1), 0};
+  }
+  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
+    if (s.kind) return s.kind == 1 ? (const void*)kOneChunk : nullptr;
+    const int hw = L.Ho * L.Wo, p = t.n0 * kWgradChunkPx + kb * 64 + s.i;
+    if (p >= t.tk.rows * hw) return nullptr;
+    const int r = p / hw, rem = p - r * hw, yo = rem / L.Wo, xo = rem - yo * L.Wo;
+    const int y = yo * L.s + s.dy, x = xo * L.s + s.dx;
+    if ((unsigned)y >= (unsigned)L.H || (unsigned)x >= (unsigned)L.W) return nullptr;
+    return (const bf16*)t.c->buf[in_buf] + (((int64_t)r * L.H + y) * L.W + x) * L.Cin + s.ci;
+  }
+  __device__ PB b_pre(const TcTile& t, int i, int j) const { return PB{i, 8 * j}; }
+  __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
+    const int p = t.n0 * kWgradChunkPx + kb * 64 + s.i;
+    if (p >= t.tk.rows * L.Ho * L.Wo || s.n0 >= L.Cout) return nullptr;
+    return (const bf16*)t.c->buf[dout_buf] + (int64_t)p * L.Cout + s.n0;
+  }
+  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
+    const int m = t.m0 + row, N = 9 * cin_real + 1;  // partial row = the weight layout's K + bias
+    if (m > 9 * L.Cin) return;
+    const int ci = m & (L.Cin - 1), n = m == 9 * L.Cin ? 9 * cin_real : (m >> L.lci) * cin_real + ci;
+    if (m < 9 * L.Cin && ci >= cin_real) return;  // padded input channels
+    float* part = (float*)t.c->buf[B_R_WSP] + ((int64_t)t.n0 * L.Cout + c0) * N + n;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) part[(int64_t)j * N] = v[j];
+  }
+};
+
+// conv0 input staged for the tensor cores: xs[r][32][32][8] bf16 = px01(x) in channels 0-2, 0 in 3-7
+// (written into a gradient buffer that is free at that point of the step).  blockIdx.x = task.
+__global__ void __launch_bounds__(256) k_stage_r(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks,
+                                                 int out_buf) {
+  const Task tk = tasks[blockIdx.x];
+  const ClientRec* c = recs + tk.rec;
+  uint4* out = (uint4*)c->buf[out_buf];
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < tk.rows * 1024; e += gridDim.y * blockDim.x) {
+    const int r = e >> 10, p = e & 1023;
+    const uint8_t* px = c->x + (int64_t)c->perm[tk.base + r] * 3072 + p * 3;
+    const __nv_bfloat162 a = __floats2bfloat162_rn(px01(px[0]), px01(px[1]));
+    const __nv_bfloat162 b = __floats2bfloat162_rn(px01(px[2]), 0.f);
+    out[e] = make_uint4(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b), 0u, 0u);
+  }
+}
+
+}  // namespace protea

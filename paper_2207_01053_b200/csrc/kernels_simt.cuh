@@ -458,7 +458,7 @@ struct ReduceArgs {
   int64_t off_w, off_b;
   int px_per_row;  // pixels per sample of the layer output (split count = ceil(rows*px/2048))
   float lr;
-  int shadow;      // 1: also write the bf16 weight shadow (bf16 mode)
+  int shadow;      // 1: also write the bf16 weight shadow (bf16 mode); 2: and the padded ResNet conv0 copy
 };
 constexpr int kReduceBlock = 256;
 __global__ void __launch_bounds__(kReduceBlock)
@@ -479,6 +479,8 @@ __global__ void __launch_bounds__(kReduceBlock)
     const float nw = c->params[idx] - a.lr * g;
     c->params[idx] = nw;
     if (a.shadow) ((__nv_bfloat16*)c->buf[B_WSH])[idx] = __float2bfloat16_rn(nw);  // tensor-core operand copy
+    if (a.shadow == 2)  // ResNet conv0 (W0 at offset 0, [16][9][3]): the padded [16][9][8] operand copy
+      ((__nv_bfloat16*)c->buf[B_R_W0P])[m * 72 + (n / 3) * 8 + n % 3] = __float2bfloat16_rn(nw);
   } else {
     c->params[a.off_b + m] -= a.lr * g;
   }

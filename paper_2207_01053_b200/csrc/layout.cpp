@@ -149,6 +149,7 @@ SlotLayout slot_layout(const ModelDims& m, int b, int64_t n, int epochs, int e) 
     put(B_R_G0, B * 1024 * 16 * e);
     put(B_R_G1, B * 1024 * 16 * e);
     put(B_R_G2, B * 1024 * 16 * e);
+    if (e == 2) put(B_R_W0P, 16 * 9 * 8 * 2);  // conv0 weight shadow padded to 8 input channels
   }
   uint64_t wsp = 0;
   for (const Layer& l : m.layers)

@@ -74,3 +74,40 @@ def test_bf16_deterministic(torch):
     a, _ = gpu_run(wl, precision=1)
     b, _ = gpu_run(wl, precision=1)
     assert np.array_equal(a[4], b[4])
+
+
+def _resnet_one_step(B, k=3, epochs=1):
+    import dataclasses
+    wl = synth.build_workload(5, n_clients=200, k=k, samples=6)
+    tmpl = synth.class_templates(wl.shape, wl.classes, wl.seed)
+    wl.clients = [dataclasses.replace(c, n=B, batch=B, epochs=epochs) for c in wl.clients]
+    wl.shards = {c.id: synth.make_shard(tmpl, c.n, c.id, wl.seed) for c in wl.clients}
+    return wl
+
+
+@pytest.mark.parametrize("B", [8, 64])
+def test_resnet8_bf16_one_step_vs_bf16_emulated_oracle(torch, B):
+    """ResNet-8 convs 1-6 on tcgen05 (kernels_resnet_tc.cuh): one local step against the oracle
+    rounding to bf16 where the CUDA bf16 path stores bf16 (activations, gradients, the weight
+    shadow of convs 1-6; reading R17).  B = 64 spans several 128-row tiles, 2048-pixel
+    wgrad splits and the stride-2 / option-A blocks."""
+    wl = _resnet_one_step(B)
+    got, ex = gpu_run(wl, precision=1)
+    emu = oracle_run(wl, emulate_bf16=True)
+    d = rel_l2(got[4] - ex["g0"][4], emu[4] - ex["g0"][4])
+    assert d <= 5e-3, d
+
+
+def test_resnet8_bf16_two_epochs_vs_oracle(torch):
+    """Several steps (ragged last batch: n = 45, B = 16, E = 2) against the float64 oracle: the
+    update itself (not only the weights) within the bf16 bar."""
+    import dataclasses
+    wl = _resnet_one_step(16, k=2, epochs=2)
+    tmpl = synth.class_templates(wl.shape, wl.classes, wl.seed)
+    wl.clients = [dataclasses.replace(c, n=45) for c in wl.clients]
+    wl.shards = {c.id: synth.make_shard(tmpl, c.n, c.id, wl.seed) for c in wl.clients}
+    got, ex = gpu_run(wl, precision=1)
+    ref = oracle_run(wl)
+    assert rel_l2(got[4], ref[4]) <= 1e-2
+    d = rel_l2(got[4] - ex["g0"][4], ref[4] - ex["g0"][4])
+    assert d <= 5e-2, d

@@ -63,7 +63,7 @@ def run_case(label, cfg, kw, gpus, prec, reps):
                 continue
             sim = Simulation(precision=prec, arena_bytes=cap, rank=r, world=G)
             mids = {w: sim.register_model(wl.model, w, wl.classes, H, W, C) for w in widths}
-            sim.register_shards([(c.id, *wl.shards[c.id]) for c in mine])
+            sim.register_shards([(c.id, *wl.shards[c.id]) for c in wl.clients])  # n_k of every client (FedAvg N)
             clients = sim.clients([(c.id, mids[c.width_q], c.batch, c.epochs) for c in wl.clients])
             g = torch.tensor(concat_globals([g0[w] for w in widths]), device=sim.device)
             o = torch.empty_like(g)
