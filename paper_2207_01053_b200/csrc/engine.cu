@@ -741,6 +741,33 @@ RConv rconv(const Layer& l) {
   return c;
 }
 
+// ResNet tcgen05 ops: persistent cp.async GEMM, contiguous tile ranges; the B tile (BN) sized to the
+// layer's N (16 / 32 -> 32, 64 -> 64) so no gather slots are spent on zero-filled columns
+template <int BN, class Op>
+void launch_rtc_bn(protea_ctx* ctx, const Op& op, const Launch& L, int opid, const int32_t* dtab) {
+  constexpr int RS = 8;  // ring stages (1 CTA per SM: 8 K blocks in flight)
+  constexpr int SMEM = rp_smem_bytes<BN, RS>();
+  static int per_sm = 0;  // resident CTAs per SM (registers / shared memory): the persistent grid
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_gemm_tc_pers<BN, RS, Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm_tc_pers<BN, RS, Op>, kRpThreads, SMEM);
+    per_sm = std::max(1, std::min(per_sm, 2));
+  }
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const int grid = std::min(L.grid[opid], per_sm * g_num_sms);
+  const int ev = op_begin(ctx, op_class(opid), opid);
+  launch_k(ctx, k_gemm_tc_pers<BN, RS, Op>, grid, kRpThreads, SMEM, op, tasks, (const int*)(dtab + L.prefix_off[opid]),
+           L.ntask);
+  op_end(ctx, ev);
+}
+template <class Op>
+void launch_rtc(protea_ctx* ctx, const Op& op, const Launch& L, int opid, const int32_t* dtab, int N) {
+  if (N <= 32)
+    launch_rtc_bn<32>(ctx, op, L, opid, dtab);
+  else
+    launch_rtc_bn<64>(ctx, op, L, opid, dtab);
+}
+
 void stage_r(protea_ctx* ctx, const ClientRec* drecs, const Task* tasks, const Launch& L, int out_buf) {
   const int ev = op_begin(ctx, PROTEA_OPC_R_FWD);
   k_stage_r<<<dim3(L.ntask, 16), 256, 0, ctx->cur>>>(drecs, tasks, out_buf);
@@ -780,7 +807,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
         tf.in_buf = B_R_G2;
         tf.wbuf = B_R_W0P;
       }
-      launch_gemm_tc<64, TC_STAGES>(ctx, tf, L, RI_F0 + i, dtab);
+      launch_rtc(ctx, tf, L, RI_F0 + i, dtab, tf.L.Cout);
       continue;
     }
     launch_gemm<F, R_BM, R_BN>(ctx, f, L, RI_F0 + i, dtab);
@@ -815,7 +842,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
       dg.Cadd = bw[i].cadd;
       if (TC) {
         RTcDgrad td{drecs, rtc(l), dg.dout_buf, dg.out_buf, dg.mask_buf, dg.add_buf, dg.add_mode, dg.Cadd};
-        launch_gemm_tc<64, TC_STAGES>(ctx, td, L, RI_D1 + i - 1, dtab);
+        launch_rtc(ctx, td, L, RI_D1 + i - 1, dtab, td.L.Cin);
       } else {
         launch_gemm<D, R_BM, R_BN>(ctx, dg, L, RI_D1 + i - 1, dtab);
       }
@@ -828,7 +855,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
         tw.L.lci = 3;
         tw.in_buf = B_R_G1;
       }
-      launch_gemm_tc<64, TC_STAGES>(ctx, tw, L, RI_W0 + i, dtab);
+      launch_rtc(ctx, tw, L, RI_W0 + i, dtab, tw.L.Cout);
     } else {
       Wg wg;
       wg.recs = drecs;

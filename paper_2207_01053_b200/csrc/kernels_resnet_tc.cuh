@@ -19,6 +19,176 @@
 
 namespace protea {
 
+// ---------------------------------------------------------------------------
+// Persistent cp.async-fed tcgen05 GEMM for the gathered ResNet ops: one CTA walks a
+// contiguous range of the launch's 128-row tiles (the per-CTA prologue, TMEM
+// allocation and launch cost of k_gemm_tc are paid once instead of per tile — a
+// 32x32x16 layer has ~70k tiles per heavy iteration).  Warps 0-7 gather every
+// tile's K blocks through the STAGES ring (one 16-byte cp.async per chunk),
+// warp 12 issues the MMAs into one of two TMEM accumulators, warps 8-11 drain the
+// other through the op's epilogue (TMEM lane quadrant = warp % 4), so gathers,
+// MMAs and epilogues of consecutive tiles overlap.
+// ---------------------------------------------------------------------------
+constexpr int kRpProd = 256, kRpThreads = 416;  // 8 producer + 4 epilogue + 1 MMA warps
+template <int BN, int STAGES>
+constexpr int rp_smem_bytes() {
+  return STAGES * (128 * 64 * 2 + BN * 64 * 2) + (2 * STAGES + 4) * 8 + 16 + 1024;
+}
+template <int BN, int STAGES, class Op>
+__global__ void __launch_bounds__(kRpThreads, 1)
+    k_gemm_tc_pers(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
+  constexpr int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr int ACC_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : 128, TMEM_COLS = 2 * ACC_COLS;
+  constexpr int LAG = (STAGES - 1) < 2 ? (STAGES - 1) : 2;
+  constexpr int NA = 1024 / kRpProd;                         // A chunks per producer thread per K block
+  constexpr int NB = (BN * 8 + kRpProd - 1) / kRpProd;       // B chunks
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = __ldg(prefix + ntask);
+  const int g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
+  const int g1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
+  const uint32_t bar0 = tc::smem_u32(bars);
+  const uint32_t full = bar0, empty = bar0 + 8 * STAGES, acc_full = bar0 + 16 * STAGES, acc_empty = acc_full + 16;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(full + 8 * s, kRpProd);
+      tc::mbar_init(empty + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(acc_full + 8 * a, 1);
+      tc::mbar_init(acc_empty + 8 * a, 4);
+    }
+    tc::mbar_fence_init();
+  }
+  if (warp == 12) tc::tmem_alloc(tc::smem_u32(tmem_slot), TMEM_COLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = tc::smem_u32(smem);
+  TaskCursor cur;
+  cur.init(prefix, ntask, g0 < total ? g0 : total - 1);
+  pdl_wait();
+
+  if (warp < 8) {  // ---------------- cp.async producers
+    const int tid = threadIdx.x;
+    int kbg = 0;
+    for (int g = g0; g < g1; ++g) {
+      cur.advance(prefix, g);
+      TcTile t;
+      t.tk = tasks[cur.ti];
+      t.c = op.recs + t.tk.rec;
+      op.setup(t, g - cur.lo);
+      const void* any = op.any(t);
+      typename Op::PA pa[NA];
+      typename Op::PB pb[NB];
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        int i, j;
+        chunk_coords<Op::A_MN, 128>(tid + kRpProd * u, i, j);
+        pa[u] = op.a_pre(t, i, j);
+      }
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        int i = 0, j = 0;
+        if (tid + kRpProd * u < BN * 8) chunk_coords<Op::B_MN, BN>(tid + kRpProd * u, i, j);
+        pb[u] = op.b_pre(t, i, j);
+      }
+      for (int kb = 0; kb < t.nk; ++kb, ++kbg) {
+        const int s = kbg % STAGES;
+        if (kbg >= STAGES) tc::mbar_wait(empty + 8 * s, ((kbg / STAGES) - 1) & 1);
+        const uint32_t a_base = sbase + s * STAGE, b_base = a_base + A_BYTES;
+#pragma unroll
+        for (int u = 0; u < NA; ++u) tc::cp16(a_base + 16 * (tid + kRpProd * u), op.a_src(t, pa[u], kb), any);
+#pragma unroll
+        for (int u = 0; u < NB; ++u)
+          if (tid + kRpProd * u < BN * 8) tc::cp16(b_base + 16 * (tid + kRpProd * u), op.b_src(t, pb[u], kb), any);
+        tc::cp_commit();
+        if (kbg >= LAG) {
+          tc::cp_wait<LAG>();
+          tc::fence_proxy_async();
+          tc::mbar_arrive(full + 8 * ((kbg - LAG) % STAGES));
+        }
+      }
+    }
+    tc::cp_wait<0>();
+    tc::fence_proxy_async();
+    for (int k = (kbg - LAG > 0 ? kbg - LAG : 0); k < kbg; ++k) tc::mbar_arrive(full + 8 * (k % STAGES));
+  } else if (warp < 12) {  // ---------------- epilogue: TMEM quadrant warp % 4
+    const int row = (warp & 3) * 32 + lane;
+    int it = 0;
+    for (int g = g0; g < g1; ++g, ++it) {
+      cur.advance(prefix, g);
+      TcTile t;
+      t.tk = tasks[cur.ti];
+      t.c = op.recs + t.tk.rec;
+      op.setup(t, g - cur.lo);
+      const int a = it & 1;
+      tc::mbar_wait(acc_full + 8 * a, (it >> 1) & 1);
+      tc::fence_after();
+      for (int c0 = 0; c0 < t.n_mma; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(a * ACC_COLS + c0), v);
+        op.epilogue(t, row, c0, v);
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty + 8 * a);
+    }
+  } else {  // ---------------- MMA issuer (warp 12, elected lane issues)
+    const uint64_t da0 = cp_desc<Op::A_MN, 128>(sbase, 0), dak = cp_desc<Op::A_MN, 128>(sbase, 1) - da0;
+    const uint64_t db0 = cp_desc<Op::B_MN, BN>(sbase + A_BYTES, 0),
+                   dbk = cp_desc<Op::B_MN, BN>(sbase + A_BYTES, 1) - db0;
+    int kbg = 0, it = 0;
+    for (int g = g0; g < g1; ++g, ++it) {
+      cur.advance(prefix, g);
+      TcTile t;
+      t.tk = tasks[cur.ti];
+      t.c = op.recs + t.tk.rec;
+      op.setup(t, g - cur.lo);
+      const uint32_t idesc = tc::idesc_bf16(128, t.n_mma, Op::A_MN, Op::B_MN);
+      const int a = it & 1;
+      if (it >= 2) tc::mbar_wait(acc_empty + 8 * a, ((it >> 1) - 1) & 1);
+      tc::fence_after();
+      for (int kb = 0; kb < t.nk; ++kb, ++kbg) {
+        const int s = kbg % STAGES;
+        tc::mbar_wait(full + 8 * s, (kbg / STAGES) & 1);
+        tc::fence_after();
+        const uint64_t so = (uint64_t)(s * (STAGE >> 4));
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          tc::mma_bf16_w(tmem + (uint32_t)(a * ACC_COLS), da0 + so + ks * dak, db0 + so + ks * dbk, idesc,
+                         (kb | ks) != 0);
+        tc::commit_w(empty + 8 * s);
+      }
+      tc::commit_w(acc_full + 8 * a);
+    }
+    __syncwarp();
+  }
+  pdl_trigger();
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, TMEM_COLS);
+  }
+  if (threadIdx.x == 0 && g1 > g0) {  // K9: split this CTA's duration over its clients by tile count
+    const uint64_t dt = globaltimer() - t_start;
+    int ti = find_task(prefix, ntask, g0), lo = g0;
+    while (lo < g1) {
+      const int hi = min(g1, __ldg(prefix + ti + 1));
+      const ClientRec* c = op.recs + tasks[ti].rec;
+      if (c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(dt * (hi - lo) / (g1 - g0)));
+      lo = hi;
+      ++ti;
+    }
+  }
+}
+
 struct RTcConv {  // RConv + log2 of the channel counts
   int H, W, Cin, Cout, s, Ho, Wo, lci, lco;
   int64_t w, b;
