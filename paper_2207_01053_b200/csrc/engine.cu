@@ -722,6 +722,10 @@ RTcConv rtc(const Layer& l) {
   c.Wo = l.wout;
   c.lci = ilog2(l.cin);
   c.lco = ilog2(l.cout);
+  c.lw = ilog2(l.win);
+  c.lhw = ilog2(l.hin * l.win);
+  c.lwo = ilog2(l.wout);
+  c.lhwo = ilog2(l.hout * l.wout);
   c.w = l.off_w;
   c.b = l.off_b;
   return c;

@@ -189,8 +189,9 @@ __global__ void __launch_bounds__(kRpThreads, 1)
   }
 }
 
-struct RTcConv {  // RConv + log2 of the channel counts
+struct RTcConv {  // RConv + log2 of the channel counts and of the (power-of-two) spatial sizes
   int H, W, Cin, Cout, s, Ho, Wo, lci, lco;
+  int lw, lhw, lwo, lhwo;  // log2 W, log2 H*W, log2 Wo, log2 Ho*Wo
   int64_t w, b;
 };
 
@@ -212,7 +213,7 @@ struct RTcFwd {
   __device__ PA a_pre(const TcTile& t, int i, int j) const {
     const int m = t.m0 + i, hw = L.Ho * L.Wo;
     if (m >= t.tk.rows * hw) return PA{-1, 0, 0, j};
-    const int r = m / hw, rem = m - r * hw, yo = rem / L.Wo, xo = rem - yo * L.Wo;
+    const int r = m >> L.lhwo, rem = m & (hw - 1), yo = rem >> L.lwo, xo = rem & (L.Wo - 1);
     return PA{r, yo * L.s - 1, xo * L.s - 1, j};
   }
   __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
@@ -242,7 +243,7 @@ struct RTcFwd {
 #pragma unroll
       for (int j = 0; j < 16; ++j) o[j] += q[j];
     } else if (res_mode == 2 && c0 < Cres) {
-      const int r = m / hw, rem = m - r * hw, yo = rem / L.Wo, xo = rem - yo * L.Wo;
+      const int r = m >> L.lhwo, rem = m & (hw - 1), yo = rem >> L.lwo, xo = rem & (L.Wo - 1);
       ld_bf16<16>((const bf16*)t.c->buf[res_buf] + (((int64_t)r * 2 * L.Ho + 2 * yo) * 2 * L.Wo + 2 * xo) * Cres + c0, q);
 #pragma unroll
       for (int j = 0; j < 16; ++j) o[j] += q[j];
@@ -270,8 +271,8 @@ struct RTcDgrad {
   __device__ PA a_pre(const TcTile& t, int i, int j) const {
     const int m = t.m0 + i, hw = L.H * L.W;
     if (m >= t.tk.rows * hw) return PA{-1, 0, 0, j};
-    const int r = m / hw, rem = m - r * hw, y = rem / L.W;
-    return PA{r, y, rem - y * L.W, j};
+    const int r = m >> L.lhw, rem = m & (hw - 1), y = rem >> L.lw;
+    return PA{r, y, rem & (L.W - 1), j};
   }
   __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
     const int k = kb * 64 + 8 * s.j;
@@ -305,7 +306,7 @@ struct RTcDgrad {
 #pragma unroll
       for (int j = 0; j < 16; ++j) a[j] += q[j];
     } else if (add_mode == 2) {
-      const int r = m / hw, rem = m - r * hw, y = rem / L.W, x = rem - y * L.W;
+      const int r = m >> L.lhw, rem = m & (hw - 1), y = rem >> L.lw, x = rem & (L.W - 1);
       if (((y | x) & 1) == 0) {
         ld_bf16<16>((const bf16*)t.c->buf[add_buf] + (((int64_t)r * (L.H / 2) + y / 2) * (L.W / 2) + x / 2) * Cadd + c0, q);
 #pragma unroll
@@ -347,7 +348,7 @@ struct RTcWgrad {
     if (s.kind) return s.kind == 1 ? (const void*)kOneChunk : nullptr;
     const int hw = L.Ho * L.Wo, p = t.n0 * kWgradChunkPx + kb * 64 + s.i;
     if (p >= t.tk.rows * hw) return nullptr;
-    const int r = p / hw, rem = p - r * hw, yo = rem / L.Wo, xo = rem - yo * L.Wo;
+    const int r = p >> L.lhwo, rem = p & (hw - 1), yo = rem >> L.lwo, xo = rem & (L.Wo - 1);
     const int y = yo * L.s + s.dy, x = xo * L.s + s.dx;
     if ((unsigned)y >= (unsigned)L.H || (unsigned)x >= (unsigned)L.W) return nullptr;
     return (const bf16*)t.c->buf[in_buf] + (((int64_t)r * L.H + y) * L.W + x) * L.Cin + s.ci;
