@@ -86,11 +86,13 @@ __global__ void __launch_bounds__(kRpThreads, 1)
       const void* any = op.any(t);
       typename Op::PA pa[NA];
       typename Op::PB pb[NB];
+      int jA;  // every A chunk of this thread has the same chunk column (q = tid + 256 u)
 #pragma unroll
       for (int u = 0; u < NA; ++u) {
         int i, j;
         chunk_coords<Op::A_MN, 128>(tid + kRpProd * u, i, j);
         pa[u] = op.a_pre(t, i, j);
+        jA = j;
       }
 #pragma unroll
       for (int u = 0; u < NB; ++u) {
@@ -102,8 +104,9 @@ __global__ void __launch_bounds__(kRpThreads, 1)
         const int s = kbg % STAGES;
         if (kbg >= STAGES) tc::mbar_wait(empty + 8 * s, ((kbg / STAGES) - 1) & 1);
         const uint32_t a_base = sbase + s * STAGE, b_base = a_base + A_BYTES;
+        const typename Op::KS ks = op.a_ks(t, jA, kb);  // the K block's tap / channel state, once per thread
 #pragma unroll
-        for (int u = 0; u < NA; ++u) tc::cp16(a_base + 16 * (tid + kRpProd * u), op.a_src(t, pa[u], kb), any);
+        for (int u = 0; u < NA; ++u) tc::cp16(a_base + 16 * (tid + kRpProd * u), op.a_src(t, pa[u], ks), any);
 #pragma unroll
         for (int u = 0; u < NB; ++u)
           if (tid + kRpProd * u < BN * 8) tc::cp16(b_base + 16 * (tid + kRpProd * u), op.b_src(t, pb[u], kb), any);
@@ -197,7 +200,8 @@ struct RTcConv {  // RConv + log2 of the channel counts and of the (power-of-two
 
 struct RTcFwd {
   static constexpr bool A_MN = false, B_MN = false;
-  struct PA { int r, y0, x0, j; };  // r < 0: row beyond M
+  struct PA { const bf16* p; int y0, x0; };  // input pixel (r, y0, x0) of the row (y0 = -4096: beyond M)
+  struct KS { int off, ky, kx, ok; };          // tap (ky, kx) / channel of the K block's chunk column
   struct PB { const bf16* p; int j; };
   const ClientRec* recs;
   RTcConv L;
@@ -212,17 +216,17 @@ struct RTcFwd {
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
   __device__ PA a_pre(const TcTile& t, int i, int j) const {
     const int m = t.m0 + i, hw = L.Ho * L.Wo;
-    if (m >= t.tk.rows * hw) return PA{-1, 0, 0, j};
-    const int r = m >> L.lhwo, rem = m & (hw - 1), yo = rem >> L.lwo, xo = rem & (L.Wo - 1);
-    return PA{r, yo * L.s - 1, xo * L.s - 1, j};
+    if (m >= t.tk.rows * hw) return PA{nullptr, -4096, -4096};
+    const int r = m >> L.lhwo, rem = m & (hw - 1), y0 = (rem >> L.lwo) * L.s - 1, x0 = (rem & (L.Wo - 1)) * L.s - 1;
+    return PA{(const bf16*)t.c->buf[in_buf] + (((int64_t)r * L.H + y0) * L.W + x0) * L.Cin, y0, x0};
   }
-  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
-    const int k = kb * 64 + 8 * s.j;
-    if (s.r < 0 || k >= 9 * L.Cin) return nullptr;
-    const int tap = k >> L.lci, ci = k & (L.Cin - 1), ky = tap / 3, kx = tap - 3 * ky;
-    const int y = s.y0 + ky, x = s.x0 + kx;
-    if ((unsigned)y >= (unsigned)L.H || (unsigned)x >= (unsigned)L.W) return nullptr;
-    return (const bf16*)t.c->buf[in_buf] + (((int64_t)s.r * L.H + y) * L.W + x) * L.Cin + ci;
+  __device__ KS a_ks(const TcTile& t, int j, int kb) const {
+    const int k = kb * 64 + 8 * j, tap = k >> L.lci, ky = tap / 3, kx = tap - 3 * ky;
+    return KS{(ky * L.W + kx) * L.Cin + (k & (L.Cin - 1)), ky, kx, k < 9 * L.Cin};
+  }
+  __device__ const void* a_src(const TcTile& t, const PA& s, const KS& k) const {
+    if (!k.ok || (unsigned)(s.y0 + k.ky) >= (unsigned)L.H || (unsigned)(s.x0 + k.kx) >= (unsigned)L.W) return nullptr;
+    return s.p + k.off;
   }
   __device__ PB b_pre(const TcTile& t, int i, int j) const {
     const bf16* w = (const bf16*)t.c->buf[wbuf] + (wbuf == B_WSH ? L.w : 0);
@@ -256,8 +260,9 @@ struct RTcFwd {
 
 struct RTcDgrad {
   static constexpr bool A_MN = false, B_MN = true;
-  struct PA { int r, y, x, j; };  // the input pixel of row i (r < 0: beyond M)
-  struct PB { int i, n0; };       // k row i of the block, 8 input channels from n0
+  struct PA { const bf16* p; int y, x; };  // dout of image r, and the input pixel (y, x) of the row
+  struct KS { int ky, kx, co, ok; };
+  struct PB { int i, n0; };               // k row i of the block, 8 input channels from n0
   const ClientRec* recs;
   RTcConv L;
   int dout_buf, out_buf, mask_buf, add_buf, add_mode, Cadd;
@@ -270,22 +275,24 @@ struct RTcDgrad {
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
   __device__ PA a_pre(const TcTile& t, int i, int j) const {
     const int m = t.m0 + i, hw = L.H * L.W;
-    if (m >= t.tk.rows * hw) return PA{-1, 0, 0, j};
-    const int r = m >> L.lhw, rem = m & (hw - 1), y = rem >> L.lw;
-    return PA{r, y, rem & (L.W - 1), j};
+    if (m >= t.tk.rows * hw) return PA{nullptr, -4096, -4096};
+    const int r = m >> L.lhw, rem = m & (hw - 1);
+    return PA{(const bf16*)t.c->buf[dout_buf] + (int64_t)r * L.Ho * L.Wo * L.Cout, rem >> L.lw, rem & (L.W - 1)};
   }
-  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
-    const int k = kb * 64 + 8 * s.j;
-    if (s.r < 0 || k >= 9 * L.Cout) return nullptr;
-    const int tap = k >> L.lco, co = k & (L.Cout - 1), ky = tap / 3, kx = tap - 3 * ky;
-    int ty = s.y - ky + 1, tx = s.x - kx + 1;
+  __device__ KS a_ks(const TcTile& t, int j, int kb) const {
+    const int k = kb * 64 + 8 * j, tap = k >> L.lco, ky = tap / 3;
+    return KS{ky, tap - 3 * ky, k & (L.Cout - 1), k < 9 * L.Cout};
+  }
+  __device__ const void* a_src(const TcTile& t, const PA& s, const KS& k) const {
+    int ty = s.y - k.ky + 1, tx = s.x - k.kx + 1;
+    if (!k.ok) return nullptr;
     if (L.s == 2) {
       if ((ty | tx) & 1) return nullptr;
       ty >>= 1;
       tx >>= 1;
     }
     if ((unsigned)ty >= (unsigned)L.Ho || (unsigned)tx >= (unsigned)L.Wo) return nullptr;
-    return (const bf16*)t.c->buf[dout_buf] + (((int64_t)s.r * L.Ho + ty) * L.Wo + tx) * L.Cout + co;
+    return s.p + (ty * L.Wo + tx) * L.Cout + k.co;
   }
   __device__ PB b_pre(const TcTile& t, int i, int j) const { return PB{i, 8 * j}; }
   __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
@@ -323,6 +330,7 @@ struct RTcDgrad {
 struct RTcWgrad {
   static constexpr bool A_MN = true, B_MN = true;
   struct PA { int i, dy, dx, ci, kind; };  // kind 0: gather, 1: bias ones row, 2: zero
+  struct KS { int p0; };                   // first pixel of the K block
   struct PB { int i, n0; };
   const ClientRec* recs;
   RTcConv L;
@@ -344,9 +352,10 @@ struct RTcWgrad {
     const int tap = mg >> L.lci, ky = tap / 3, kx = tap - 3 * ky;
     return PA{i, ky - 1, kx - 1, mg & (L.Cin - 1), 0};
   }
-  __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const {
+  __device__ KS a_ks(const TcTile& t, int j, int kb) const { return KS{t.n0 * kWgradChunkPx + kb * 64}; }
+  __device__ const void* a_src(const TcTile& t, const PA& s, const KS& k) const {
     if (s.kind) return s.kind == 1 ? (const void*)kOneChunk : nullptr;
-    const int hw = L.Ho * L.Wo, p = t.n0 * kWgradChunkPx + kb * 64 + s.i;
+    const int hw = L.Ho * L.Wo, p = k.p0 + s.i;
     if (p >= t.tk.rows * hw) return nullptr;
     const int r = p >> L.lhwo, rem = p & (hw - 1), yo = rem >> L.lwo, xo = rem & (L.Wo - 1);
     const int y = yo * L.s + s.dy, x = xo * L.s + s.dx;
