@@ -347,9 +347,14 @@ def main():
         bound, achieved, peak, unit = "hbm", by_per / avg_ns, pk["hbm"], "GB/s"
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tf):  # DRAM bytes per launch of this op from the committed ncu capture of the same command
+    if os.path.exists(tf):  # DRAM bytes of this op from the committed ncu launch list of the same command
         try:
-            traffic = json.load(open(tf)).get(pb.OPC_NAMES[dominant], {}).get(dtype, {}).get("dram_bytes_per_launch")
+            rec = json.load(open(tf)).get(pb.OPC_NAMES[dominant], {}).get(dtype, {})
+            # the ncu list covers every launch of the op in the round, `achieved` only the timed ones: scale
+            # the timed launches' algorithmic bytes by the round's measured DRAM / algorithmic byte ratio
+            algo_round = float(st["op_bytes"][dominant])
+            if rec and algo_round > 0:
+                traffic = by_per * rec["dram_bytes_per_launch"] * rec["launches"] / algo_round
         except Exception:
             traffic = None
     roof = {"kernel": pb.OPC_NAMES[dominant], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
