@@ -6,7 +6,8 @@
 // 8 consecutive channels of one pixel (or 8 consecutive output channels of one weight row), gathered
 // straight from the client's slot; out-of-image taps and K padding are zero-filled by cp.async.
 // Weights come from the bf16 shadow (B_WSH), kept in step with the fp32 master by k_reduce_update.
-// Layers 1-6 (cin in {16, 32, 64}); conv0 (cin = 3 from the u8 image) stays on the SIMT kernels.
+// Layers 1-6 gather cin in {16, 32, 64} channels straight from the activations; conv0 reads the u8
+// image staged as [r][32][32][8] bf16 (k_stage_r) with its weights padded to [16][9][8] (B_R_W0P).
 //   fwd   M = rows*Ho*Wo out pixels, N = cout,  K = 9 cin        (A K-major, B K-major)
 //         epilogue: + bias (+ identity / option-A residual), ReLU -> bf16
 //   dgrad M = rows*H*W in pixels,   N = cin,   K = 9 cout       (A K-major, B MN-major)
