@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(256) k_rhead(RHeadArgs a, const Task* __restri
   for (int idx = threadIdx.x; idx < rows * 64; idx += 256) {
     const int r = idx >> 6, ch = idx & 63;
     float s = 0.f;
+#pragma unroll 8
     for (int p = 0; p < 64; ++p) s += ldv(o3 + ((int64_t)r * 64 + p) * 64 + ch);
     gap[idx] = s * (1.f / 64.f);
   }
@@ -237,9 +238,16 @@ __global__ void __launch_bounds__(256) k_rhead(RHeadArgs a, const Task* __restri
   __syncthreads();
   // ds3 = dgap / 64 * (o3 > 0)  -> g0
   T* g0 = (T*)c->buf[B_R_G0];
-  for (int idx = threadIdx.x; idx < rows * 64 * 64; idx += 256) {
-    const int r = idx >> 12, ch = idx & 63;
-    stv(g0 + idx, ldv(o3 + idx) > 0.f ? dgap[r * 64 + ch] * (1.f / 64.f) : 0.f);
+  constexpr int V = 16 / sizeof(T);  // elements per 16-byte vector
+  for (int iv = threadIdx.x; iv < rows * 64 * 64 / V; iv += 256) {
+    const int idx = iv * V, r = idx >> 12, ch = idx & 63;
+    const uint4 ov = reinterpret_cast<const uint4*>(o3)[iv];
+    const T* o = reinterpret_cast<const T*>(&ov);
+    uint4 gv;
+    T* gq = reinterpret_cast<T*>(&gv);
+#pragma unroll
+    for (int j = 0; j < V; ++j) stv(gq + j, ldv(o + j) > 0.f ? dgap[r * 64 + ch + j] * (1.f / 64.f) : 0.f);
+    reinterpret_cast<uint4*>(g0)[iv] = gv;
   }
   for (int idx = threadIdx.x; idx < C * 64; idx += 256) {
     const int cc = idx >> 6, f = idx & 63;

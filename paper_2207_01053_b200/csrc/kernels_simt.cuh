@@ -472,7 +472,14 @@ __global__ void __launch_bounds__(kReduceBlock)
   const int splits = cdiv(tk.rows * a.px_per_row, kWgradChunkPx);
   const float* part = (const float*)c->buf[a.wsp_buf];
   float g = 0.f;
-  for (int s = 0; s < splits; ++s) g += part[(int64_t)s * total + e];
+  for (int s0 = 0; s0 < splits; s0 += 8) {  // 8 independent loads in flight, summed in split order
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = s0 + j < splits ? __ldcg(part + (int64_t)(s0 + j) * total + e) : 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (s0 + j < splits) g += v[j];
+  }
   const int m = e / N, n = e - m * N;
   if (n < a.Nw) {
     const int64_t idx = a.off_w + (int64_t)m * a.Nw + n;
