@@ -24,13 +24,13 @@ namespace protea {
 // Persistent cp.async-fed tcgen05 GEMM for the gathered ResNet ops: one CTA walks a
 // contiguous range of the launch's 128-row tiles (the per-CTA prologue, TMEM
 // allocation and launch cost of k_gemm_tc are paid once instead of per tile — a
-// 32x32x16 layer has ~70k tiles per heavy iteration).  Warps 0-7 gather every
+// 32x32x16 layer has ~70k tiles per heavy iteration).  Warps 0-15 gather every
 // tile's K blocks through the STAGES ring (one 16-byte cp.async per chunk),
-// warp 12 issues the MMAs into one of two TMEM accumulators, warps 8-11 drain the
+// warp 20 issues the MMAs into one of two TMEM accumulators, warps 16-19 drain the
 // other through the op's epilogue (TMEM lane quadrant = warp % 4), so gathers,
 // MMAs and epilogues of consecutive tiles overlap.
 // ---------------------------------------------------------------------------
-constexpr int kRpProd = 256, kRpThreads = 416;  // 8 producer + 4 epilogue + 1 MMA warps
+constexpr int kRpProd = 512, kRpThreads = 672;  // 16 producer + 4 epilogue + 1 MMA warps
 template <int BN, int STAGES>
 constexpr int rp_smem_bytes() {
   return STAGES * (128 * 64 * 2 + BN * 64 * 2) + (2 * STAGES + 4) * 8 + 16 + 1024;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kRpThreads, 1)
     }
     tc::mbar_fence_init();
   }
-  if (warp == 12) tc::tmem_alloc(tc::smem_u32(tmem_slot), TMEM_COLS);
+  if (warp == kRpProd / 32 + 4) tc::tmem_alloc(tc::smem_u32(tmem_slot), TMEM_COLS);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kRpThreads, 1)
   cur.init(prefix, ntask, g0 < total ? g0 : total - 1);
   pdl_wait();
 
-  if (warp < 8) {  // ---------------- cp.async producers
+  if (warp < kRpProd / 32) {  // ---------------- cp.async producers
     const int tid = threadIdx.x;
     int kbg = 0;
     for (int g = g0; g < g1; ++g) {
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kRpThreads, 1)
     tc::cp_wait<0>();
     tc::fence_proxy_async();
     for (int k = (kbg - LAG > 0 ? kbg - LAG : 0); k < kbg; ++k) tc::mbar_arrive(full + 8 * (k % STAGES));
-  } else if (warp < 12) {  // ---------------- epilogue: TMEM quadrant warp % 4
+  } else if (warp < kRpProd / 32 + 4) {  // ---------------- epilogue: TMEM quadrant warp % 4
     const int row = (warp & 3) * 32 + lane;
     int it = 0;
     for (int g = g0; g < g1; ++g, ++it) {
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kRpThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(acc_empty + 8 * a);
     }
-  } else {  // ---------------- MMA issuer (warp 12, elected lane issues)
+  } else {  // ---------------- MMA issuer (last warp, elected lane issues)
     const uint64_t da0 = cp_desc<Op::A_MN, 128>(sbase, 0), dak = cp_desc<Op::A_MN, 128>(sbase, 1) - da0;
     const uint64_t db0 = cp_desc<Op::B_MN, BN>(sbase + A_BYTES, 0),
                    dbk = cp_desc<Op::B_MN, BN>(sbase + A_BYTES, 1) - db0;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kRpThreads, 1)
   pdl_trigger();
   tc::fence_before();
   __syncthreads();
-  if (warp == 12) {
+  if (warp == kRpProd / 32 + 4) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, TMEM_COLS);
   }
