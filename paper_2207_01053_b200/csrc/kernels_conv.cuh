@@ -1051,7 +1051,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const float4* pt = (const float4*)c->buf[B_WSP];
       constexpr int Q = kW2NP / 4, NE = 64 * Q;  // float4 chunks per split
       const int e_lo = (int)((int64_t)item * NE / nitem), e_hi = (int)((int64_t)(item + 1) * NE / nitem);
+#pragma unroll 2
       for (int e = e_lo + threadIdx.x; e < e_hi; e += 256) {
+        const int co = e / Q, m0 = 4 * (e - co * Q);
+        const int64_t idx = d.w2 + (int64_t)co * 800 + m0;
+        float4 w = m0 < 800 ? *reinterpret_cast<const float4*>(P + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
         float4 q[8];  // splits <= 8 (B <= 64): every load in flight at once, summed in split order
 #pragma unroll
         for (int sp = 0; sp < 8; ++sp)
@@ -1060,10 +1064,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
         for (int sp = 0; sp < 8; ++sp)
           if (sp < splits) gs.x += q[sp].x, gs.y += q[sp].y, gs.z += q[sp].z, gs.w += q[sp].w;
-        const int co = e / Q, m0 = 4 * (e - co * Q);
         if (m0 < 800) {
-          const int64_t idx = d.w2 + (int64_t)co * 800 + m0;
-          float4 w = *reinterpret_cast<const float4*>(P + idx);
           w.x -= lr * gs.x, w.y -= lr * gs.y, w.z -= lr * gs.z, w.w -= lr * gs.w;
           *reinterpret_cast<float4*>(P + idx) = w;
           const __nv_bfloat162 h0 = __floats2bfloat162_rn(w.x, w.y), h1 = __floats2bfloat162_rn(w.z, w.w);
