@@ -909,7 +909,17 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     op_end(ctx, ev);
   } else if (m.arch == PROTEA_MODEL_MLP) {
     const MlpDims d = mlp_dims(m);
-    launch_gemm<MlpFc1Fwd<T, MF_BM, MF_BN>, MF_BM, MF_BN>(ctx, {drecs, d}, L, OP_MF, dtab);
+    {
+      const size_t smem = (16 * 784 + 256) * 4 + 64 * 784;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_mlp_fc1_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+      }
+      const int ev = op_begin(ctx, OP_MF, OP_MF);
+      k_mlp_fc1_fwd<T><<<dim3(L.ntask, 4), kMlpFwdThreads, smem, ctx->cur>>>(drecs, tasks, d);
+      op_end(ctx, ev);
+    }
     HeadArgs ha{drecs, B_H1, B_DZ1, 64, m.classes, d.w2, d.b2, d.b1, lr};
     const int ev = op_begin(ctx, OP_MHEAD, OP_MHEAD);
     k_head<T><<<L.ntask, kHeadThreads, 0, ctx->cur>>>(ha, tasks);

@@ -532,6 +532,44 @@ struct MlpFc1Fwd {  // M = rows, N = 64, K = 784
   }
 };
 
+// MLP fc1 forward for one lock-step iteration: CTA (client, 16 of the 64 outputs).  The rows' u8
+// inputs and the CTA's 16 weight rows are staged in shared memory once (the generic tile GEMM
+// re-fetched them per 16-wide K step through the permutation: latency-bound at K = 784); every
+// thread then runs whole 784-long dot products, accumulated in k order with the same fmaf sequence
+// as k_gemm_simt (bitwise-identical h).  Dynamic smem: 16 x 784 fp32 + a 256-entry px01 table + rows x 784 u8.
+constexpr int kMlpFwdThreads = 256;
+template <typename T>
+__global__ void __launch_bounds__(kMlpFwdThreads) k_mlp_fc1_fwd(const ClientRec* __restrict__ recs,
+                                                                const Task* __restrict__ tasks, MlpDims d) {
+  extern __shared__ __align__(16) uint8_t msm[];
+  float* Ws = reinterpret_cast<float*>(msm);  // [16][784]
+  float* lut = Ws + 16 * 784;                 // px01(u) for u in [0, 256): the same fp32 values, no division
+  uint8_t* xs = msm + (16 * 784 + 256) * 4;   // [rows][784]
+  const Task tk = tasks[blockIdx.x];
+  const ClientRec* c = recs + tk.rec;
+  const int rows = tk.rows, n0 = blockIdx.y * 16;
+  const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
+  for (int i = threadIdx.x; i < 16 * 784; i += kMlpFwdThreads) Ws[i] = c->params[d.w1 + (int64_t)n0 * 784 + i];
+  if (threadIdx.x < 256) lut[threadIdx.x] = px01((uint8_t)threadIdx.x);
+  for (int i = threadIdx.x; i < rows * 49; i += kMlpFwdThreads) {  // 784 = 49 x 16 bytes per row
+    const int r = i / 49, q = i - r * 49;
+    reinterpret_cast<uint4*>(xs + r * 784)[q] =
+        __ldg(reinterpret_cast<const uint4*>(c->x + (int64_t)c->perm[tk.base + r] * 784) + q);
+  }
+  __syncthreads();
+  T* h = (T*)c->buf[B_H1];
+  for (int o = threadIdx.x; o < rows * 16; o += kMlpFwdThreads) {
+    const int r = o >> 4, n = o & 15;
+    const float* w = Ws + n * 784;
+    const uint8_t* x = xs + r * 784;
+    float acc = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < 784; ++k) acc = fmaf(lut[x[k]], w[k], acc);
+    stv(h + (int64_t)r * 64 + n0 + n, fmaxf(acc + c->params[d.b1 + n0 + n], 0.f));
+  }
+  if (threadIdx.x == 0 && c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(globaltimer() - t_start));
+}
+
 template <typename T, int BM, int BN>
 struct MlpFc1Wgrad {  // M = 64, N = 784, K = rows (fc1 bias: k_head)
   static constexpr bool A_KFAST = false, B_KFAST = false;
