@@ -112,6 +112,10 @@ struct protea_ctx {
   cudaStream_t cur = nullptr;  // stream the launch helpers currently issue to
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   std::vector<cudaEvent_t> gjoin;  // per model group: end of its deferred fc1 wgrad
+  // per model group: its own high-priority lock-step stream (the groups' chains are independent within
+  // a round: different clients, weights and FedAvg accumulators), with an event to join it
+  std::vector<cudaStream_t> gstream;
+  std::vector<cudaEvent_t> gdone;
   std::vector<char> gpending;      // per model group: a deferred fc1 wgrad not yet joined
   bool overlap_now = false;        // current iteration defers fc1 wgrad (light iteration)
   // programmatic dependent launch on the lock-step stream (PROTEA_PDL=1).  Off by default: measured on
@@ -1081,6 +1085,11 @@ void protea_finalize(protea_ctx* ctx) {
     cudaStreamDestroy(ctx->hi);
   }
   for (auto e : ctx->gjoin) cudaEventDestroy(e);
+  for (auto sgs : ctx->gstream) {
+    cudaStreamSynchronize(sgs);
+    cudaStreamDestroy(sgs);
+  }
+  for (auto e : ctx->gdone) cudaEventDestroy(e);
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -1337,9 +1346,35 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     ctx->gjoin.push_back(ev);
   }
   ctx->gpending.assign(G, 0);
+  // group g > 0 runs on its own stream (same priority as hi); admissions join every group first
+  while ((int)ctx->gstream.size() < G) {
+    int lo = 0, hi_p = 0;
+    cudaStream_t sgs;
+    cudaEvent_t ev;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi_p));
+    CK(cudaStreamCreateWithPriority(&sgs, cudaStreamNonBlocking, hi_p));
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    ctx->gstream.push_back(sgs);
+    ctx->gdone.push_back(ev);
+  }
+  std::vector<cudaStream_t> gs(G, ctx->hi);
+  for (int g = 1; g < G; ++g) gs[g] = ctx->serialize ? ctx->hi : ctx->gstream[g];  // serialize: one stream
   CK(cudaEventRecord(ctx->fork_ev, ctx->stream));
   CK(cudaStreamWaitEvent(ctx->hi, ctx->fork_ev, 0));
   ctx->cur = ctx->hi;
+  auto join_groups_into_hi = [&]() {  // hi waits for every other group stream
+    for (int g = 1; g < G; ++g) {
+      cudaEventRecord(ctx->gdone[g], gs[g]);
+      cudaStreamWaitEvent(ctx->hi, ctx->gdone[g], 0);
+    }
+  };
+  auto fork_groups_from_hi = [&]() {  // every other group stream waits for hi
+    if (G > 1) {
+      cudaEventRecord(ctx->gdone[0], ctx->hi);
+      for (int g = 1; g < G; ++g) cudaStreamWaitEvent(gs[g], ctx->gdone[0], 0);
+    }
+  };
+  fork_groups_from_hi();
   std::vector<int64_t> iter_rows(T, 0);
   for (auto& c : rc)
     for (uint64_t t = c.admit; t < c.release; ++t) {
@@ -1347,8 +1382,12 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
       iter_rows[t] += std::min<int64_t>(c.B, c.n - j * c.B);
     }
   for (uint64_t t = 0; t < T; ++t) {
-    ctx->overlap_now = tc_mode && !ctx->serialize && iter_rows[t] <= ctx->overlap_rows;
+    // (several groups already overlap each other: no side-stream deferral then)
+    ctx->overlap_now = tc_mode && !ctx->serialize && G == 1 && iter_rows[t] <= ctx->overlap_rows;
     if (admits[t].second > 0) {
+      // an admitted client may reuse a slot released by any group: every group's earlier work first
+      ctx->cur = ctx->hi;
+      if (t > 0) join_groups_into_hi();
       const int* ids = dtab + admits[t].first;
       int64_t maxP = 0, maxn = 0;
       for (auto& c : rc)
@@ -1365,10 +1404,12 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
       k_admit_perm<<<dim3(cdiv((int)maxn, kPermThreads), admits[t].second, maxE), kPermThreads, 0, ctx->cur>>>(
           drecs, ids, seed, round, shuffle);
       op_end(ctx, ev);
+      fork_groups_from_hi();
     }
     for (int li : launch_idx[t]) {
       const Launch& L = launches[li];
       const ModelDims& m = ctx->groups[L.group].m;
+      ctx->cur = gs[L.group];
       ctx->cur_fl = L.fl;
       ctx->cur_by = L.by;
       if (e == 4)
@@ -1383,14 +1424,20 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
         if (rel_by_group[t][g].second > 0) {
           const int64_t P = ctx->groups[g].m.P;
           ctx->op_bytes[PROTEA_OPC_FEDAVG] += (uint64_t)P * (20 + 4 * rel_by_group[t][g].second);
+          ctx->cur = gs[g];
           join_group(ctx, g);  // the released clients' last fc1 wgrad
           const int ev = op_begin(ctx, PROTEA_OPC_FEDAVG);
           k_release_acc<<<grid_for(P, 256), 256, 0, ctx->cur>>>(drecs, dtab + rel_by_group[t][g].first,
-                                                                 rel_by_group[t][g].second, P, loss_dev);
+                                                                 rel_by_group[t][g].second, P, loss_dev + g);
           op_end(ctx, ev);
         }
   }
-  for (int g = 0; g < G; ++g) join_group(ctx, g);
+  for (int g = 0; g < G; ++g) {
+    ctx->cur = gs[g];
+    join_group(ctx, g);
+  }
+  ctx->cur = ctx->hi;
+  join_groups_into_hi();
   ctx->overlap_now = false;
   ctx->cur_fl = ctx->cur_by = nullptr;
   CK(cudaEventRecord(ctx->join_ev, ctx->hi));
@@ -1509,13 +1556,14 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
     CK(cudaMemcpyAsync(ctx->gin.p, global_in, Ptot * 4, cudaMemcpyDeviceToDevice, ctx->stream));
     wg = ctx->gin.p;
   }
-  CK(ctx->acc.reserve(Ptot + 1));
-  CK(cudaMemsetAsync(ctx->acc.p, 0, (Ptot + 1) * 8, ctx->stream));
+  const size_t NG = ctx->groups.size();  // one fp64 loss-sum slot per group after the accumulators
+  CK(ctx->acc.reserve(Ptot + NG));
+  CK(cudaMemsetAsync(ctx->acc.p, 0, (Ptot + NG) * 8, ctx->stream));
   reset_ops(ctx, opts->time_ops);
   ctx->serialize = opts->serialize != 0;
   const uint64_t l0 = ctx->launches;
   uint64_t iters = 0;
-  double* loss_dev = ctx->acc.p + Ptot;  // one extra fp64 after the accumulators: sum of step losses
+  double* loss_dev = ctx->acc.p + Ptot;  // per-group fp64 sums of step losses after the accumulators
   protea_status st =
       execute(ctx, all, wg, ctx->acc.p, opts->lr, opts->seed, opts->round, opts->shuffle, &iters, loss_dev);
   if (st != PROTEA_OK) return st;
@@ -1559,10 +1607,12 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
     }
   }
   if (!out_dev) CK(cudaMemcpyAsync(global_out, out, Ptot * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  double loss_sum = 0.0;
-  CK(cudaMemcpyAsync(&loss_sum, loss_dev, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<double> loss_g(NG, 0.0);
+  CK(cudaMemcpyAsync(loss_g.data(), loss_dev, NG * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  double loss_sum = 0.0;
+  for (double v : loss_g) loss_sum += v;  // group order
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   if (stats) {
