@@ -121,6 +121,9 @@ struct protea_ctx {
   // programmatic dependent launch on the lock-step stream (PROTEA_PDL=1).  Off by default: measured on
   // B200, config 2: 70.2 ms/round without, 71.5 ms with (early CTAs of the next kernel hold SM resources).
   bool pdl = false;
+  int lanes = 1;     // lock-step lanes per model group (PROTEA_LANES): independent chains on own streams
+  int spin_cap = 148;  // CTAs of a kernel whose CTAs spin-wait on each other (the width-1 CNN wgrad split
+                       // reduces): g_num_sms / lanes, so concurrent lanes' instances are all co-resident
   int64_t overlap_rows = 640;  // defer when the iteration has at most this many rows (PROTEA_OVERLAP_ROWS); measured best: 640
   // per-op-class accounting of the current round (protea_round_stats)
   uint32_t time_ops = 0;
@@ -509,6 +512,7 @@ MlpDims mlp_dims(const ModelDims& m) {
 // One (iteration, group) launch descriptor, offsets into the int32 table.
 struct Launch {
   int group;
+  int vg;  // virtual group = group * lanes + lane: the stream it runs on
   int ntask;
   int64_t task_off;            // tasks: 4 ints each
   int64_t prefix_off[OP_COUNT];
@@ -553,7 +557,7 @@ void launch_gemm_persistent(protea_ctx* ctx, const OpT& op, const Launch& L, int
     attr = true;
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
-  const int grid = std::min(L.grid[opid], ctas_per_sm * g_num_sms);
+  const int grid = std::min(L.grid[opid], ctas_per_sm * ctx->spin_cap);
   const int ev = op_begin(ctx, op_class(opid), opid);
   launch_k(ctx, k_gemm_persistent<BN, STAGES, OpT>, grid, kPersThreads, SMEM, op, tasks,
            (const int*)(dtab + L.prefix_off[opid]), L.ntask);
@@ -572,7 +576,7 @@ void launch_conv_persistent(protea_ctx* ctx, const ClientRec* drecs, const CnnDi
   op.recs = drecs;
   op.d = d;
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
-  const int grid = std::min(L.grid[opid], g_num_sms);  // one CTA per SM, each a contiguous tile range
+  const int grid = std::min(L.grid[opid], ctx->spin_cap);  // one CTA per SM, each a contiguous tile range
   const int ev = op_begin(ctx, op_class(opid), opid);
   launch_k(ctx, k_conv_persistent<Op>, grid, kConvThreads, Op::SMEM, op, tasks, (const int*)(dtab + L.prefix_off[opid]),
            L.ntask);
@@ -587,7 +591,7 @@ void launch_conv1_wgrad_q(protea_ctx* ctx, const ClientRec* drecs, const Launch&
     attr = true;
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
-  const int grid = std::min(L.grid[OP_C1W], g_num_sms);
+  const int grid = std::min(L.grid[OP_C1W], ctx->spin_cap);  // spin-waiting split reduce: all CTAs co-resident
   const int ev = op_begin(ctx, OP_C1W, OP_C1W);
   launch_k(ctx, k_conv1_wgrad_q, grid, kConvThreads, kW1Smem, drecs, tasks, (const int*)(dtab + L.prefix_off[OP_C1W]),
            L.ntask, d.w1, d.b1, lr);
@@ -602,7 +606,7 @@ void launch_conv2_wgrad_halo(protea_ctx* ctx, const ClientRec* drecs, const CnnD
     attr = true;
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
-  const int grid = std::min(L.grid[OP_C2W], g_num_sms);
+  const int grid = std::min(L.grid[OP_C2W], ctx->spin_cap);  // spin-waiting split reduce: all CTAs co-resident
   const int ev = op_begin(ctx, OP_C2W, OP_C2W);
   launch_k(ctx, k_conv2_wgrad_halo, grid, kConvThreads, kW2Smem, drecs, tasks, (const int*)(dtab + L.prefix_off[OP_C2W]),
            L.ntask, d, lr, L.c2w_groups);
@@ -1031,6 +1035,7 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
   cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest);
   if (const char* ov = std::getenv("PROTEA_OVERLAP_ROWS")) ctx->overlap_rows = std::atoll(ov);
   if (const char* pd = std::getenv("PROTEA_PDL")) ctx->pdl = std::atoi(pd) != 0;
+  if (const char* ln = std::getenv("PROTEA_LANES")) ctx->lanes = std::max(1, std::min(4, std::atoi(ln)));
   if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_least) != cudaSuccess ||
       cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, prio_greatest) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
@@ -1184,6 +1189,7 @@ struct RunClient {
   uint64_t S, admit, release;
   uint64_t offset;
   int rec = -1;
+  int lane = 0;  // lock-step lane within the model group (PROTEA_LANES)
 };
 
 // Validates and executes the lock-step schedule of `rc` (this rank's clients,
@@ -1254,6 +1260,13 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
       for (size_t k = 0; k < owner.size(); ++k) recs[owner[k]].tmaps = ctx->tmaps.p + k * TM_COUNT;
     }
   }
+  // ---- lock-step lanes: within each (group, batch size) class the clients alternate between lanes, so
+  // every lane gets the same mix of step counts; each lane is an independent chain on its own stream
+  const int NL = tc_mode ? ctx->lanes : 1;
+  {
+    std::map<std::pair<int, int>, int> seen_class;
+    for (auto& c : rc) c.lane = NL > 1 ? seen_class[{c.group, c.B}]++ % NL : 0;
+  }
   // ---- schedule tables
   uint64_t T = 0;
   for (auto& c : rc) T = std::max(T, c.release);
@@ -1271,15 +1284,17 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
       admits[t] = {(int64_t)tab.size(), (int)adm.size()};
       tab.insert(tab.end(), adm.begin(), adm.end());
     }
-    for (int g = 0; g < G; ++g) {
+    for (int v = 0; v < G * NL; ++v) {
+      const int g = v / NL, lane = v % NL;
       const ModelDims& m = ctx->groups[g].m;
       std::vector<const RunClient*> act;
       for (auto& c : rc)
-        if (c.group == g && c.admit <= t && t < c.release) act.push_back(&c);
+        if (c.group == g && c.lane == lane && c.admit <= t && t < c.release) act.push_back(&c);
       if (!act.empty()) {
         Launch L;
         std::memset(&L, 0, sizeof(L));
         L.group = g;
+        L.vg = v;
         L.ntask = (int)act.size();
         while (tab.size() % 4) tab.push_back(0);
         L.task_off = (int64_t)tab.size();
@@ -1320,7 +1335,9 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
         launch_idx[t].push_back((int)launches.size());
         launches.push_back(L);
       }
-      // releases after iteration t (client finished its last step)
+    }
+    for (int g = 0; g < G; ++g) {
+      // releases after iteration t (client finished its last step), all lanes, ascending id
       std::vector<int> rel;
       for (auto& c : rc)
         if (c.group == g && c.release == t + 1) rel.push_back(c.rec);
@@ -1347,7 +1364,8 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
   }
   ctx->gpending.assign(G, 0);
   // group g > 0 runs on its own stream (same priority as hi); admissions join every group first
-  while ((int)ctx->gstream.size() < G) {
+  const int V = G * NL;
+  while ((int)ctx->gstream.size() < V) {
     int lo = 0, hi_p = 0;
     cudaStream_t sgs;
     cudaEvent_t ev;
@@ -1357,21 +1375,22 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     ctx->gstream.push_back(sgs);
     ctx->gdone.push_back(ev);
   }
-  std::vector<cudaStream_t> gs(G, ctx->hi);
-  for (int g = 1; g < G; ++g) gs[g] = ctx->serialize ? ctx->hi : ctx->gstream[g];  // serialize: one stream
+  std::vector<cudaStream_t> gs(V, ctx->hi);
+  for (int v = 1; v < V; ++v) gs[v] = ctx->serialize ? ctx->hi : ctx->gstream[v];  // serialize: one stream
+  ctx->spin_cap = std::max(1, g_num_sms / (ctx->serialize ? 1 : NL));  // one spin-waiting wgrad per lane at a time
   CK(cudaEventRecord(ctx->fork_ev, ctx->stream));
   CK(cudaStreamWaitEvent(ctx->hi, ctx->fork_ev, 0));
   ctx->cur = ctx->hi;
-  auto join_groups_into_hi = [&]() {  // hi waits for every other group stream
-    for (int g = 1; g < G; ++g) {
-      cudaEventRecord(ctx->gdone[g], gs[g]);
-      cudaStreamWaitEvent(ctx->hi, ctx->gdone[g], 0);
+  auto join_groups_into_hi = [&]() {  // hi waits for every other lane stream
+    for (int v = 1; v < V; ++v) {
+      cudaEventRecord(ctx->gdone[v], gs[v]);
+      cudaStreamWaitEvent(ctx->hi, ctx->gdone[v], 0);
     }
   };
-  auto fork_groups_from_hi = [&]() {  // every other group stream waits for hi
-    if (G > 1) {
+  auto fork_groups_from_hi = [&]() {  // every other lane stream waits for hi
+    if (V > 1) {
       cudaEventRecord(ctx->gdone[0], ctx->hi);
-      for (int g = 1; g < G; ++g) cudaStreamWaitEvent(gs[g], ctx->gdone[0], 0);
+      for (int v = 1; v < V; ++v) cudaStreamWaitEvent(gs[v], ctx->gdone[0], 0);
     }
   };
   fork_groups_from_hi();
@@ -1383,7 +1402,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     }
   for (uint64_t t = 0; t < T; ++t) {
     // (several groups already overlap each other: no side-stream deferral then)
-    ctx->overlap_now = tc_mode && !ctx->serialize && G == 1 && iter_rows[t] <= ctx->overlap_rows;
+    ctx->overlap_now = tc_mode && !ctx->serialize && V == 1 && iter_rows[t] <= ctx->overlap_rows;
     if (admits[t].second > 0) {
       // an admitted client may reuse a slot released by any group: every group's earlier work first
       ctx->cur = ctx->hi;
@@ -1409,7 +1428,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     for (int li : launch_idx[t]) {
       const Launch& L = launches[li];
       const ModelDims& m = ctx->groups[L.group].m;
-      ctx->cur = gs[L.group];
+      ctx->cur = gs[L.vg];
       ctx->cur_fl = L.fl;
       ctx->cur_by = L.by;
       if (e == 4)
@@ -1424,7 +1443,11 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
         if (rel_by_group[t][g].second > 0) {
           const int64_t P = ctx->groups[g].m.P;
           ctx->op_bytes[PROTEA_OPC_FEDAVG] += (uint64_t)P * (20 + 4 * rel_by_group[t][g].second);
-          ctx->cur = gs[g];
+          ctx->cur = gs[g * NL];
+          for (int l = 1; l < NL; ++l) {  // the group's other lanes finished iteration t first
+            cudaEventRecord(ctx->gdone[g * NL + l], gs[g * NL + l]);
+            cudaStreamWaitEvent(ctx->cur, ctx->gdone[g * NL + l], 0);
+          }
           join_group(ctx, g);  // the released clients' last fc1 wgrad
           const int ev = op_begin(ctx, PROTEA_OPC_FEDAVG);
           k_release_acc<<<grid_for(P, 256), 256, 0, ctx->cur>>>(drecs, dtab + rel_by_group[t][g].first,
@@ -1433,7 +1456,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
         }
   }
   for (int g = 0; g < G; ++g) {
-    ctx->cur = gs[g];
+    ctx->cur = gs[g * NL];
     join_group(ctx, g);
   }
   ctx->cur = ctx->hi;
