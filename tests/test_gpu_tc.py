@@ -111,3 +111,46 @@ def test_resnet8_bf16_two_epochs_vs_oracle(torch):
     assert rel_l2(got[4], ref[4]) <= 1e-2
     d = rel_l2(got[4] - ex["g0"][4], ref[4] - ex["g0"][4])
     assert d <= 5e-2, d
+
+
+def _bf16_round(wl, env=None, serialize=False):
+    """One bf16 round through the C ABI; env: PROTEA_* variables read by protea_init."""
+    import os
+    import torch
+    from paper_2207_01053_b200.sim import Simulation, concat_globals
+    old = {k: os.environ.get(k) for k in (env or {})}
+    os.environ.update(env or {})
+    try:
+        sim = Simulation(precision=1, arena_bytes=1 << 30)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    widths = sorted({c.width_q for c in wl.clients})
+    mids = {w: sim.register_model(wl.model, w, wl.classes, 32, 32, 3) for w in widths}
+    sim.register_shards([(c.id, *wl.shards[c.id]) for c in wl.clients])
+    clients = sim.clients([(c.id, mids[c.width_q], c.batch, c.epochs) for c in wl.clients])
+    plan, _ = sim.plan(sim.profile(clients))
+    g = torch.tensor(concat_globals([synth.init_weights(wl.model, w, wl.classes, seed=0) for w in widths]),
+                     device="cuda")
+    out, _ = sim.run_round(clients, plan, g, lr=wl.lr, seed=wl.seed, rnd=0, serialize=serialize)
+    res = out.cpu().numpy()
+    sim.close()
+    return res
+
+
+def test_group_streams_equal_serialized(torch):
+    """Config 4's width groups run their lock-step chains on separate streams; the result must be
+    bitwise the one of the serialised round (every launch on one stream)."""
+    wl = synth.build_workload(4, k=9, samples=24, epochs=1)
+    assert np.array_equal(_bf16_round(wl), _bf16_round(wl, serialize=True))
+
+
+def test_lanes_equal_single_lane(torch):
+    """PROTEA_LANES=2 splits a group's clients into two independent chains (own streams, persistent
+    kernels capped to their SM share); a client's arithmetic does not depend on its co-scheduled
+    clients, so the federated result is bitwise the single-lane one."""
+    wl = synth.build_workload(2, n_clients=8, samples=40, epochs=1)
+    assert np.array_equal(_bf16_round(wl), _bf16_round(wl, env={"PROTEA_LANES": "2"}))
