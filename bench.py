@@ -407,6 +407,15 @@ def main():
                            "probe_s": probe_s, "util_monitor": host_mon, "probe_step_ns": sorted({int(p["step_ns"]) for p in probe}),
                            "op_ms_warmup": {pb.OPC_NAMES[i]: op_stats["op_ns"][i] / 1e6 for i in range(pb.N_OPC)
                                             if op_stats and op_stats["op_ns"][i]},
+                           # every op class of the serialised warm-up round against both roofs (tensor-pipe and
+                           # HBM utilisation = achieved algorithmic FLOP/s, bytes/s over the measured peaks)
+                           "op_util_warmup": {pb.OPC_NAMES[i]: {
+                               "ms": op_stats["op_ns"][i] / 1e6,
+                               "tflops": op_stats["op_flops"][i] / op_stats["op_ns"][i] / 1e3,
+                               "gbs": op_stats["op_bytes"][i] / op_stats["op_ns"][i],
+                               "tensor_frac": op_stats["op_flops"][i] / op_stats["op_ns"][i] / 1e3 / pk["bf16_sus"],
+                               "hbm_frac": op_stats["op_bytes"][i] / op_stats["op_ns"][i] / pk["hbm"]}
+                               for i in range(pb.N_OPC) if op_stats and op_stats["op_ns"][i]},
                            "loss_mean_last_round": st["loss_sum"] / max(1, st["client_steps"])}}
         print(json.dumps(line), flush=True)
     sim.close()

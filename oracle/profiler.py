@@ -88,7 +88,8 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
     wsp = split-K partials of the conv weight gradients: each conv layer's
     reduction over b*Hout*Wout pixels is cut into ceil(b*Hout*Wout / 2048)
     splits, each holding cout*(K+1) fp32 partials (the +1 is the bias column), rows
-    padded to a multiple of 4 floats (16-byte aligned rows, reading R21).
+    padded to a multiple of 4 floats (16-byte aligned rows, reading R21); the CNN
+    reuses one region (max over layers), ResNet-8 keeps one per layer (sum).
     """
     b, e = batch, elem_bytes
     P = n_params(model, width_q, classes)
@@ -115,12 +116,15 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
                 ("g0", b * 1024 * 16 * e), ("g1", b * 1024 * 16 * e), ("g2", b * 1024 * 16 * e)]
         if e == 2:  # bf16 mode: conv0 weight shadow padded to 8 input channels [16][9][8] (tensor cores)
             out.append(("w0p", 16 * 9 * 8 * 2))
+            out.append(("xs", b * 1024 * 8 * 2))  # conv0 input staged as [b][32][32][8] bf16
     else:
         raise ValueError(model)
     convs = conv_layers(model, width_q)
     if convs:
-        out.append(("wsp", 4 * max(math.ceil(b * hw / WGRAD_CHUNK_PX) * co * (-(-(K + 1) // 4) * 4)
-                                   for hw, co, K in convs)))
+        per_layer = [4 * math.ceil(b * hw / WGRAD_CHUNK_PX) * co * (-(-(K + 1) // 4) * 4) for hw, co, K in convs]
+        # CNN: one region reused layer by layer (max); ResNet-8: a region per layer, all seven kept until
+        # the step's single merged SGD reduce (sum)
+        out.append(("wsp", sum(per_layer) if model == RESNET8 else max(per_layer)))
     return out
 
 

@@ -53,6 +53,7 @@ enum Buf : int {
   // ResNet-8
   B_R_A0, B_R_R1, B_R_O1, B_R_R2, B_R_O2, B_R_R3, B_R_O3, B_R_GAP, B_R_DGAP, B_R_G0, B_R_G1, B_R_G2,
   B_R_W0P,  // bf16 mode: conv0 weights padded to 8 input channels [16][9][8] (tensor-core operand)
+  B_R_XS,   // bf16 mode: conv0 input staged as [r][32][32][8] bf16 (read by conv0 fwd and wgrad)
   B_R_WSP,
   B_COUNT
 };
@@ -86,5 +87,21 @@ inline int64_t w1q_index(int C1, int dy, int dx, int q, int co, int ci) {
 inline uint64_t w1q_bytes(int C1) { return 36ull * 4 * C1 * 8 * 2; }
 
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// ResNet-8 weight-gradient partials: one region per conv layer (all seven layers' partials are kept
+// until the step's single merged SGD reduce), region l = [splits_l(B)][cout_l][9 cin_l + 1] fp32 rows
+// padded to 4 floats, splits_l(B) = ceil(B * Ho_l * Wo_l / kWgradChunkPx).  Float offset of region l
+// (l = 7: the total) for a slot of batch B.
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int64_t r8_wsp_off(int layer, int B) {
+  const int hw[7] = {1024, 1024, 1024, 256, 256, 64, 64}, co[7] = {16, 16, 16, 32, 32, 64, 64},
+            ci[7] = {3, 16, 16, 16, 32, 32, 64};
+  int64_t off = 0;
+  for (int j = 0; j < layer; ++j)
+    off += (int64_t)((B * hw[j] + kWgradChunkPx - 1) / kWgradChunkPx) * co[j] * ((9 * ci[j] + 1 + 3) / 4 * 4);
+  return off;
+}
 
 }  // namespace protea

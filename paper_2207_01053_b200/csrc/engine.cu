@@ -812,11 +812,11 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
     if (i == 6) { f.res_buf = B_R_O2; f.res_mode = 2; f.Cres = 32; }         // block 3: option A from o2
     if (TC) {
       RTcFwd tf{drecs, rtc(m.layers[i]), f.in_buf, f.out_buf, f.res_buf, f.res_mode, f.Cres, B_WSH};
-      if (i == 0) {  // conv0: the u8 input staged as [r][32][32][8] bf16 into g2 (free until the backward)
-        stage_r(ctx, drecs, tasks, L, B_R_G2);
+      if (i == 0) {  // conv0: the u8 input staged once per step as [r][32][32][8] bf16 (xs)
+        stage_r(ctx, drecs, tasks, L, B_R_XS);
         tf.L.Cin = 8;
         tf.L.lci = 3;
-        tf.in_buf = B_R_G2;
+        tf.in_buf = B_R_XS;
         tf.wbuf = B_R_W0P;
       }
       launch_rtc(ctx, tf, L, RI_F0 + i, dtab, tf.L.Cout);
@@ -840,6 +840,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
       {B_R_G1, B_R_G2, B_R_O2, B_R_G0, 2, 64},         // b3a: ds2 = (convT_s2(dr3) + sc(ds3)) * (o2 > 0)
       {B_R_G0, B_R_G1, B_R_R3, -1, 0, 0}};             // b3b: dr3 = convT(ds3) * (r3 > 0)
   const int wg_dout[7] = {B_R_G0, B_R_G2, B_R_G1, B_R_G0, B_R_G2, B_R_G1, B_R_G0};
+  ReduceMulti rm;
   for (int i = 6; i >= 0; --i) {
     const Layer& l = m.layers[i];
     if (i >= 1) {
@@ -860,12 +861,11 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
       }
     }
     if (TC) {
-      RTcWgrad tw{drecs, rtc(l), wg_dout[i], in_of[i], l.cin};
-      if (i == 0) {  // conv0: re-stage the input into g1 (free once b1a's dgrad has read it)
-        stage_r(ctx, drecs, tasks, L, B_R_G1);
+      RTcWgrad tw{drecs, rtc(l), wg_dout[i], in_of[i], l.cin, i};
+      if (i == 0) {  // conv0: the staged input of the forward
         tw.L.Cin = 8;
         tw.L.lci = 3;
-        tw.in_buf = B_R_G1;
+        tw.in_buf = B_R_XS;
       }
       launch_rtc(ctx, tw, L, RI_W0 + i, dtab, tw.L.Cout);
     } else {
@@ -874,15 +874,20 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
       wg.L = rconv(l);
       wg.dout_buf = wg_dout[i];
       wg.in_buf = in_of[i];
+      wg.layer = i;
       launch_gemm<Wg, R_BM, R_BN>(ctx, wg, L, RI_W0 + i, dtab);
     }
-    // the fp32 master and (bf16 mode) the tensor-core shadow
-    ReduceArgs ra{drecs, B_R_WSP, l.cout, 9 * l.cin, l.off_w, l.off_b, l.hout * l.wout, lr, TC ? (i == 0 ? 2 : 1) : 0};
-    ev = op_begin(ctx, PROTEA_OPC_R_REDUCE, RI_R0 + i);
-    k_reduce_update<<<L.grid[RI_R0 + i], kReduceBlock, 0, ctx->cur>>>(ra, tasks, dtab + L.prefix_off[RI_R0 + i],
-                                                                         L.ntask);
-    op_end(ctx, ev);
+    // SGD of the fp32 master and (bf16 mode) the tensor-core shadow: deferred to one launch after the
+    // backward (each layer's dgrad above has read its old weights; the next writer is the next step)
+    rm.a[i] = ReduceArgs{drecs, B_R_WSP, l.cout, 9 * l.cin, l.off_w, l.off_b, l.hout * l.wout, lr,
+                         TC ? (i == 0 ? 2 : 1) : 0, i};
+    rm.prefix[i] = dtab + L.prefix_off[RI_R0 + i];
   }
+  rm.base[0] = 0;
+  for (int i = 0; i < 7; ++i) rm.base[i + 1] = rm.base[i] + L.grid[RI_R0 + i];
+  ev = op_begin(ctx, PROTEA_OPC_R_REDUCE, -1);
+  k_reduce_multi<<<rm.base[7], kReduceBlock, 0, ctx->cur>>>(rm, tasks, L.ntask);
+  op_end(ctx, ev);
 }
 
 template <typename T>
@@ -904,13 +909,13 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Fc1Wgrad<T, F1W_BM, F1W_BN>, F1W_BM, F1W_BN>(ctx, {drecs, d, lr}, L, OP_F1W, dtab);
     launch_gemm<Conv2Dgrad<T, C2D_BM, C2D_BN>, C2D_BM, C2D_BN>(ctx, {drecs, d}, L, OP_C2D, dtab);
     launch_gemm<Conv2Wgrad<T, C2W_BM, C2W_BN>, C2W_BM, C2W_BN>(ctx, {drecs, d}, L, OP_C2W, dtab);
-    ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr, 0};
+    ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr, 0, -1};
     ev = op_begin(ctx, OP_C2R, OP_C2R);
     k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->cur>>>(r2, tasks, dtab + L.prefix_off[OP_C2R],
                                                                        L.ntask);
     op_end(ctx, ev);
     launch_gemm<Conv1Wgrad<T, C1W_BM, C1W_BN>, C1W_BM, C1W_BN>(ctx, {drecs, d}, L, OP_C1W, dtab);
-    ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr, 0};
+    ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr, 0, -1};
     ev = op_begin(ctx, OP_C1R, OP_C1R);
     k_reduce_update<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(r1, tasks, dtab + L.prefix_off[OP_C1R],
                                                                        L.ntask);

@@ -10,7 +10,7 @@
 //   dgrad M = in pixels,  N = cin,  K = 9 cout (stride-2 taps must divide);
 //         epilogue (+ shortcut gradient) x ReLU mask of the stored activation
 //   wgrad M = cout, N = 9 cin + 1 (bias), K = out pixels, split-K (2048 px) ->
-//         partials summed in split order by k_reduce_update.
+//         partials (a region per layer) summed in split order by the step's one k_reduce_multi.
 #pragma once
 #include "kernels_simt.cuh"
 
@@ -141,6 +141,7 @@ struct RWgrad {
   const ClientRec* recs;
   RConv L;
   int dout_buf, in_buf;  // in_buf -1: the u8 input image
+  int layer;             // partial region of this layer (r8_wsp_off)
   __device__ void setup(GemmTile& t, int local) const {
     const int N = 9 * L.Cin + 1, nt = cdiv(N, BN), mt = cdiv(L.Cout, BM);
     t.split = local / (mt * nt);
@@ -168,7 +169,7 @@ struct RWgrad {
     return ldv((const T*)t.c->buf[in_buf] + (((int64_t)r * L.H + y) * L.W + x) * L.Cin + ci);
   }
   __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
-    float* part = (float*)t.c->buf[B_R_WSP] + (int64_t)t.split * t.M * t.N;
+    float* part = (float*)t.c->buf[B_R_WSP] + r8_wsp_off(layer, t.c->B) + (int64_t)t.split * t.M * t.N;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll

@@ -13,7 +13,8 @@
 //   dgrad M = rows*H*W in pixels,   N = cin,   K = 9 cout       (A K-major, B MN-major)
 //         epilogue: (+ shortcut gradient) x ReLU mask of the stored activation -> bf16
 //   wgrad M = 9 cin + 1 (bias row), N = cout, K = 2048-pixel split (A, B MN-major)
-//         epilogue: partial[split][cout][9 cin + 1] (summed in split order + SGD by k_reduce_update)
+//         epilogue: partial[split][cout][9 cin + 1] in the layer's region (summed in split order + SGD
+//         by the step's one k_reduce_multi)
 #pragma once
 #include "kernels_resnet.cuh"
 #include "kernels_tc.cuh"
@@ -337,6 +338,7 @@ struct RTcWgrad {
   RTcConv L;
   int dout_buf, in_buf;
   int cin_real;  // channels of the weight layout (conv0: 3 real of the 8 staged; else Cin)
+  int layer;     // partial region of this layer (r8_wsp_off)
   __device__ int mtiles() const { return (9 * L.Cin + 1 + 127) / 128; }
   __device__ void setup(TcTile& t, int local) const {
     const int mt = mtiles(), split = local / mt, px = t.tk.rows * L.Ho * L.Wo - split * kWgradChunkPx;
@@ -374,7 +376,7 @@ struct RTcWgrad {
     if (m > 9 * L.Cin) return;
     const int ci = m & (L.Cin - 1), n = m == 9 * L.Cin ? 9 * cin_real : (m >> L.lci) * cin_real + ci;
     if (m < 9 * L.Cin && ci >= cin_real) return;  // padded input channels
-    float* part = (float*)t.c->buf[B_R_WSP] + ((int64_t)t.n0 * L.Cout + c0) * N + n;
+    float* part = (float*)t.c->buf[B_R_WSP] + r8_wsp_off(layer, t.c->B) + ((int64_t)t.n0 * L.Cout + c0) * N + n;
 #pragma unroll
     for (int j = 0; j < 16; ++j) part[(int64_t)j * N] = v[j];
   }

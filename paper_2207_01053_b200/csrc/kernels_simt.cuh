@@ -459,18 +459,19 @@ struct ReduceArgs {
   int px_per_row;  // pixels per sample of the layer output (split count = ceil(rows*px/2048))
   float lr;
   int shadow;      // 1: also write the bf16 weight shadow (bf16 mode); 2: and the padded ResNet conv0 copy
+  int layer;       // ResNet-8: the layer's partial region (r8_wsp_off); -1: the buffer start
 };
 constexpr int kReduceBlock = 256;
-__global__ void __launch_bounds__(kReduceBlock)
-    k_reduce_update(ReduceArgs a, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
-  const int ti = find_task(prefix, ntask, blockIdx.x);
+__device__ __forceinline__ void reduce_update_block(const ReduceArgs& a, const Task* __restrict__ tasks,
+                                                    const int* __restrict__ prefix, int ntask, int block) {
+  const int ti = find_task(prefix, ntask, block);
   const Task tk = tasks[ti];
   const ClientRec* c = a.recs + tk.rec;
   const int N = a.Nw + 1, total = a.M * N;
-  const int e = (blockIdx.x - prefix[ti]) * kReduceBlock + threadIdx.x;
+  const int e = (block - prefix[ti]) * kReduceBlock + threadIdx.x;
   if (e >= total) return;
   const int splits = cdiv(tk.rows * a.px_per_row, kWgradChunkPx);
-  const float* part = (const float*)c->buf[a.wsp_buf];
+  const float* part = (const float*)c->buf[a.wsp_buf] + (a.layer >= 0 ? r8_wsp_off(a.layer, c->B) : 0);
   float g = 0.f;
   for (int s0 = 0; s0 < splits; s0 += 8) {  // 8 independent loads in flight, summed in split order
     float v[8];
@@ -491,6 +492,25 @@ __global__ void __launch_bounds__(kReduceBlock)
   } else {
     c->params[a.off_b + m] -= a.lr * g;
   }
+}
+
+__global__ void __launch_bounds__(kReduceBlock)
+    k_reduce_update(ReduceArgs a, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
+  reduce_update_block(a, tasks, prefix, ntask, blockIdx.x);
+}
+
+// ResNet-8: the SGD reduces of all seven conv layers of a step in ONE launch (the layers' partials sit
+// in separate regions, r8_wsp_off); block b belongs to layer l with base[l] <= b < base[l + 1].
+struct ReduceMulti {
+  ReduceArgs a[7];
+  const int* prefix[7];
+  int base[8];
+};
+__global__ void __launch_bounds__(kReduceBlock)
+    k_reduce_multi(ReduceMulti r, const Task* __restrict__ tasks, int ntask) {
+  int l = 0;
+  while (l < 6 && (int)blockIdx.x >= r.base[l + 1]) ++l;
+  reduce_update_block(r.a[l], tasks, r.prefix[l], ntask, blockIdx.x - r.base[l]);
 }
 
 // --------------------------------------------------------------------------

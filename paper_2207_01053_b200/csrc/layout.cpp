@@ -150,11 +150,13 @@ SlotLayout slot_layout(const ModelDims& m, int b, int64_t n, int epochs, int e) 
     put(B_R_G1, B * 1024 * 16 * e);
     put(B_R_G2, B * 1024 * 16 * e);
     if (e == 2) put(B_R_W0P, 16 * 9 * 8 * 2);  // conv0 weight shadow padded to 8 input channels
+    if (e == 2) put(B_R_XS, B * 1024 * 8 * 2);  // conv0 input staged for the tensor cores
   }
   uint64_t wsp = 0;
   for (const Layer& l : m.layers)
     if (l.kind == 0)  // rows of K+1 partials padded to a multiple of 4 floats (16-byte aligned)
       wsp = std::max<uint64_t>(wsp, 4ull * splits_for(l, b) * l.cout * ((l.K() + 1 + 3) / 4 * 4));
+  if (m.arch == PROTEA_MODEL_RESNET8) wsp = 4ull * r8_wsp_off(7, b);  // a region per layer (sum, not max)
   if (wsp) put(m.arch == PROTEA_MODEL_RESNET8 ? B_R_WSP : B_WSP, wsp);
   // slot order = enum order except that the wgrad partials come last (oracle order)
   uint64_t off = 0;
