@@ -667,7 +667,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   // (a split-K persistent variant for light iterations measured slower: 7.2 -> 8.0 ms/round)
   launch_gemm_tc<TC_F1F_BN, TC_F1F_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
   launch_head_cnn<T>(ctx, m, L, drecs, tasks, lr);
-  launch_gemm_persistent<TC_F1D_BN, TC_STAGES>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab, 2);
+  launch_gemm_persistent<TC_F1D_BN, 8>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab, 1);
   // fc1 wgrad (HBM-bound RMW of the fp32 master + bf16 shadow) needs dh, a2 and the fc1 weights, which
   // nothing in the rest of this step touches.  In light iterations (the lock-step tail, where every
   // other op is latency bound) it runs on the low-priority side stream and is joined only before the
