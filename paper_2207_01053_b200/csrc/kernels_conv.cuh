@@ -653,15 +653,16 @@ constexpr int kW1GBytes = 2 * 128 * 128;                // g1 sub-tile: 128 (q,c
 constexpr int kW1XCopy = 36 * 8 * 16;                   // one dx copy [36][8][8] bf16
 constexpr int kW1Stage = kW1GBytes + 6 * kW1XCopy;      // 60416 = 59 x 1024
 constexpr int kW1Fold = 4 * 76 * 32 * 4;                // fold buffer S[q][76][32] fp32
-constexpr int kW1Smem = 2 * kW1Stage + kW1Fold + 256 + 1024;
+constexpr int kW1Stages = 3;                            // TMA ring depth (3 x 59 KB + fold: 216 KB)
+constexpr int kW1Smem = kW1Stages * kW1Stage + kW1Fold + 256 + 1024;
 
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv1_wgrad_q(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks,
                     const int* __restrict__ prefix, int ntask, int64_t off_w, int64_t off_b, float lr) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
-  float* S = reinterpret_cast<float*>(smem + 2 * kW1Stage);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kW1Stage + kW1Fold);
+  float* S = reinterpret_cast<float*>(smem + kW1Stages * kW1Stage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kW1Stages * kW1Stage + kW1Fold);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = __ldg(prefix + ntask);
@@ -670,9 +671,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int ti0 = find_task(prefix, ntask, g0 < total ? g0 : total - 1);
   const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
   const uint32_t bar0 = tc::smem_u32(bars);
-  const uint32_t full = bar0, empty = bar0 + 16, acc_full = bar0 + 32, acc_empty = bar0 + 40;
+  const uint32_t full = bar0, empty = bar0 + 8 * kW1Stages, acc_full = bar0 + 16 * kW1Stages, acc_empty = acc_full + 8;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kW1Stages; ++i) {
       tc::mbar_init(full + 8 * i, 1);
       tc::mbar_init(empty + 8 * i, 1);
     }
@@ -698,9 +699,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         t.c = recs + t.tk.rec;
         const int r0 = kW1QImages * (g - __ldg(prefix + ti)), nsub = 2 * min(kW1QImages, t.tk.rows - r0);
         for (int sub = 0; sub < nsub; ++sub, ++s) {
-          const int buf = s & 1, r = r0 + (sub >> 1), h = sub & 1;
+          const int buf = s % kW1Stages, r = r0 + (sub >> 1), h = sub & 1;
           const uint32_t gb = sb + buf * kW1Stage;
-          if (s >= 2) tc::mbar_wait(empty + 8 * buf, ((s >> 1) - 1) & 1);
+          if (s >= kW1Stages) tc::mbar_wait(empty + 8 * buf, ((s / kW1Stages) - 1) & 1);
           tc::mbar_expect_tx(full + 8 * buf, kW1Stage);
           tc::tma_load_4d(gb, tmap_of(t, TM_G), full + 8 * buf, 0, 8 * h, 0, r);
           tc::tma_load_4d(gb + kW1GBytes / 2, tmap_of(t, TM_G), full + 8 * buf, 64, 8 * h, 0, r);
@@ -720,9 +721,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (i >= 1) tc::mbar_wait(acc_empty, (i - 1) & 1);
         tc::fence_after();
         for (int sub = 0; sub < nsub; ++sub, ++s) {
-          const int buf = s & 1;
+          const int buf = s % kW1Stages;
           const uint32_t gb = sb + buf * kW1Stage;
-          tc::mbar_wait(full + 8 * buf, (s >> 1) & 1);
+          tc::mbar_wait(full + 8 * buf, (s / kW1Stages) & 1);
           tc::fence_after();
           const uint64_t a0 = tc::sdesc_sw128(gb, kW1GBytes / 2, 1024), b0 = tc::sdesc(gb + kW1GBytes, 256, kW1XCopy);
 #pragma unroll
