@@ -264,6 +264,25 @@ protea_status protea_round_partial(protea_ctx* ctx, double* dst, size_t n_params
 protea_status protea_round_finalize(protea_ctx* ctx, const double* acc_sum, const float* global_in, float* global_out,
                                     size_t n_params);
 
+/* HeteroFL-style overlapping-width aggregation for the CNN-w family (DESIGN.md
+ * reading R23; the paper's FedAvg P:234 generalised to nested sub-models).  The global model is the
+ * full-width CNN (width_q 4, `classes` outputs); a width-q client holds the sub-model of the first
+ * C1 = 8q / C2 = 16q / F = 128q channels of every hidden dimension (fc1 inputs: the first C2 channels
+ * of each of the 8x8 pooled positions; fc2: every class).
+ * protea_heterofl_extract: sub_out (device, n_params(CNN, width_q) floats) = that sub-model of
+ *   global_full (device, n_params(CNN, 4) floats).
+ * protea_heterofl_aggregate: out[i] (device, full width) = the num_examples-weighted mean of element i
+ *   over the clients whose sub-model holds it (fp64, in the given client order, one rounding), or
+ *   global_full[i] when none does.  params: host array of n device pointers (client k: its width_q[k]
+ *   sub-model); width_q, num_examples: host arrays of n.
+ * Errors: INVALID (null, classes not in [2, 64], width not in {1, 2, 4}, n_k <= 0), EMPTY (n == 0),
+ * CUDA.  Validation precedes device work. */
+protea_status protea_heterofl_extract(protea_ctx* ctx, int32_t classes, const float* global_full, int32_t width_q,
+                                      float* sub_out);
+protea_status protea_heterofl_aggregate(protea_ctx* ctx, int32_t classes, const float* global_full,
+                                        const float* const* params, const int32_t* width_q,
+                                        const int64_t* num_examples, size_t n, float* out);
+
 /* out[d] = sum_k n_k params[k][d] / sum_k n_k, fp64 accumulation in the given
  * order, one rounding to fp32.  params: host array of n device pointers, each
  * dim floats; out: device, dim floats.

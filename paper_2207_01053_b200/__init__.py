@@ -31,7 +31,7 @@ ORDER_ASC_ID, ORDER_DESC_STEPS = 0, 1
 EXPORTS = ["protea_init", "protea_finalize", "protea_last_error", "protea_register_model", "protea_register_shards",
            "protea_profile_clients", "protea_plan", "protea_run_round", "protea_fedavg", "protea_client_footprint",
            "protea_selftest_gemm", "protea_round_partial", "protea_round_finalize", "protea_plan_hash",
-           "protea_evaluate"]
+           "protea_evaluate", "protea_heterofl_extract", "protea_heterofl_aggregate"]
 
 
 class ProteaError(RuntimeError):
@@ -132,6 +132,8 @@ for _f in EXPORTS:
 _lib.protea_plan_hash.argtypes = [_vp, _sz, _vp]
 _lib.protea_evaluate.argtypes = [_vp, ctypes.c_int32, _vp, _vp, _vp, ctypes.c_int64, _vp]
 _lib.protea_plan_hash.restype = ctypes.c_uint64
+_lib.protea_heterofl_extract.argtypes = [_vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp]
+_lib.protea_heterofl_aggregate.argtypes = [_vp, ctypes.c_int32, _vp, _vp, _vp, _vp, _sz, _vp]
 
 
 def _check(code, ctx=None):
@@ -293,3 +295,28 @@ def protea_client_footprint(arch, width_q, classes, H, W, C, n, batch, epochs, p
 def protea_selftest_gemm(A, B, D, M, N, K, mn_major=False):
     """include/protea_selftest.h: D = A B^T on the library's tcgen05 core (device tensors)."""
     _check(_lib.protea_selftest_gemm(A.data_ptr(), B.data_ptr(), D.data_ptr(), M, N, K, 1 if mn_major else 0))
+
+
+def protea_heterofl_extract(ctx, global_full, width_q, classes=10):
+    """Width-q sub-model (new device tensor) of the full-width CNN weights (HeteroFL, R23)."""
+    import torch
+    q = int(width_q)
+    c1, c2, f = 8 * q, 16 * q, 128 * q
+    out = torch.empty(c1 * 75 + c1 + c2 * 25 * c1 + c2 + f * 64 * c2 + f + classes * f + classes,
+                      dtype=torch.float32, device=global_full.device)
+    _check(_lib.protea_heterofl_extract(ctx, int(classes), global_full.data_ptr(), q, out.data_ptr()), ctx)
+    return out
+
+
+def protea_heterofl_aggregate(ctx, global_full, params, widths, num_examples, out=None, classes=10):
+    """n_k-weighted per-element mean over the clients whose width-q sub-model holds the element; the
+    rest keeps global_full (device tensors; HeteroFL, R23)."""
+    import torch
+    out = torch.empty_like(global_full) if out is None else out
+    n = len(params)
+    ptrs = (ctypes.c_void_p * max(n, 1))(*[p.data_ptr() for p in params])
+    wq = np.asarray(widths, dtype=np.int32)
+    ne = np.asarray(num_examples, dtype=np.int64)
+    _check(_lib.protea_heterofl_aggregate(ctx, int(classes), global_full.data_ptr(), ptrs, wq.ctypes.data,
+                                          ne.ctypes.data, n, out.data_ptr()), ctx)
+    return out

@@ -104,6 +104,7 @@ struct protea_ctx {
   DevArray<uint32_t> ev_ok;
   DevArray<const float*> ptrs;
   DevArray<double> wts;
+  DevArray<int32_t> wq;  // protea_heterofl_aggregate: client widths
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint64_t launches = 0;
   // side stream: fc1 wgrad (HBM-bound weight RMW) overlaps the conv backward chain (L2 / tensor bound)
@@ -1085,6 +1086,7 @@ void protea_finalize(protea_ctx* ctx) {
   ctx->ev_ok.release();
   ctx->ptrs.release();
   ctx->wts.release();
+  ctx->wq.release();
   for (auto e : ctx->evpool) cudaEventDestroy(e);
   if (ctx->side) {
     cudaStreamSynchronize(ctx->side);
@@ -1926,6 +1928,60 @@ protea_status protea_evaluate(protea_ctx* ctx, int32_t model_id, const float* we
     out->correct += ok[t];
   }
   out->n = (uint64_t)n;
+  return PROTEA_OK;
+}
+
+static int64_t cnn_params(int q, int classes) {
+  const int64_t C1 = 8 * q, C2 = 16 * q, F = 128 * q;
+  return C1 * 75 + C1 + C2 * 25 * C1 + C2 + F * 64 * C2 + F + (int64_t)classes * F + classes;
+}
+
+protea_status protea_heterofl_extract(protea_ctx* ctx, int32_t classes, const float* global_full, int32_t width_q,
+                                      float* sub_out) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  if (!global_full || !sub_out) return fail(ctx, PROTEA_ERR_INVALID, "heterofl_extract: null argument");
+  if (classes < 2 || classes > 64) return fail(ctx, PROTEA_ERR_INVALID, "heterofl_extract: classes not in [2, 64]");
+  if (width_q != 1 && width_q != 2 && width_q != 4)
+    return fail(ctx, PROTEA_ERR_INVALID, "heterofl_extract: width_q not in {1, 2, 4}");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t P = cnn_params(4, classes);
+  k_heterofl_extract<<<grid_for(P, 256), 256, 0, ctx->stream>>>(global_full, width_q, classes, sub_out, P);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PROTEA_OK;
+}
+
+protea_status protea_heterofl_aggregate(protea_ctx* ctx, int32_t classes, const float* global_full,
+                                        const float* const* params, const int32_t* width_q,
+                                        const int64_t* num_examples, size_t n, float* out) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  if (n == 0) return fail(ctx, PROTEA_ERR_EMPTY, "heterofl_aggregate: no results to aggregate");
+  if (!global_full || !params || !width_q || !num_examples || !out)
+    return fail(ctx, PROTEA_ERR_INVALID, "heterofl_aggregate: null argument");
+  if (classes < 2 || classes > 64) return fail(ctx, PROTEA_ERR_INVALID, "heterofl_aggregate: classes not in [2, 64]");
+  std::vector<double> w(n);
+  for (size_t k = 0; k < n; ++k) {
+    const std::string who = "heterofl_aggregate: client " + std::to_string(k);
+    if (!params[k]) return fail(ctx, PROTEA_ERR_INVALID, who + ": params is null");
+    if (width_q[k] != 1 && width_q[k] != 2 && width_q[k] != 4)
+      return fail(ctx, PROTEA_ERR_INVALID, who + ": width_q not in {1, 2, 4}");
+    if (num_examples[k] <= 0) return fail(ctx, PROTEA_ERR_INVALID, who + ": num_examples <= 0");
+    w[k] = (double)num_examples[k];
+  }
+  CK(cudaSetDevice(ctx->device));
+  CK(ctx->ptrs.reserve(n));
+  CK(ctx->wts.reserve(n));
+  CK(ctx->wq.reserve(n));
+  CK(cudaMemcpyAsync(ctx->ptrs.p, params, n * sizeof(float*), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->wts.p, w.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->wq.p, width_q, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  const int64_t P = cnn_params(4, classes);
+  k_heterofl<<<grid_for(P, 256), 256, 0, ctx->stream>>>(ctx->ptrs.p, ctx->wq.p, ctx->wts.p, (int)n, global_full, out,
+                                                         P, classes);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
   return PROTEA_OK;
 }
 

@@ -111,3 +111,74 @@ __global__ void k_fedavg(const float* const* __restrict__ ptrs, const double* __
 }
 
 }  // namespace protea
+
+namespace protea {
+
+// HeteroFL-style overlapping-width aggregation for the CNN-w family (DESIGN.md reading
+// R23).  Full-width (q = 4) flat index i -> flat index in the width-q sub-model (the first C1/C2/F
+// channels of every hidden dimension, fc1 inputs as the first C2 channels of each of the 64 pooled
+// positions), or -1 when the sub-model does not hold the element.
+__device__ __forceinline__ int64_t hfl_sub_index(int64_t i, int q, int classes) {
+  const int C1f = 32, C2f = 64, Ff = 512, C1 = 8 * q, C2 = 16 * q, F = 128 * q;
+  int64_t so = 0;
+  if (i < (int64_t)C1f * 75) return i / 75 < C1 ? i : -1;  // conv1 W [C1][5][5][3]: the first C1 rows
+  i -= (int64_t)C1f * 75;
+  so += (int64_t)C1 * 75;
+  if (i < C1f) return i < C1 ? so + i : -1;
+  i -= C1f;
+  so += C1;
+  if (i < (int64_t)C2f * 25 * C1f) {  // conv2 W [C2][5][5][C1]
+    const int64_t co = i / (25 * C1f), r = i % (25 * C1f), tap = r / C1f, ci = r % C1f;
+    return co < C2 && ci < C1 ? so + (co * 25 + tap) * C1 + ci : -1;
+  }
+  i -= (int64_t)C2f * 25 * C1f;
+  so += (int64_t)C2 * 25 * C1;
+  if (i < C2f) return i < C2 ? so + i : -1;
+  i -= C2f;
+  so += C2;
+  if (i < (int64_t)Ff * 64 * C2f) {  // fc1 W [F][64 pooled positions][C2]
+    const int64_t o = i / (64 * C2f), r = i % (64 * C2f), p = r / C2f, c = r % C2f;
+    return o < F && c < C2 ? so + (o * 64 + p) * C2 + c : -1;
+  }
+  i -= (int64_t)Ff * 64 * C2f;
+  so += (int64_t)F * 64 * C2;
+  if (i < Ff) return i < F ? so + i : -1;
+  i -= Ff;
+  so += F;
+  if (i < (int64_t)classes * Ff) {  // fc2 W [classes][F]
+    const int64_t cls = i / Ff, f = i % Ff;
+    return f < F ? so + cls * F + f : -1;
+  }
+  i -= (int64_t)classes * Ff;
+  so += (int64_t)classes * F;
+  return so + i;  // fc2 bias: every class
+}
+
+// out[i] = g[i] + sum_{k holds i} n_k (w_k[j_k(i)] - g[i]) / sum_{k holds i} n_k  (fp64, client order),
+// or g[i] when no client holds it
+__global__ void k_heterofl(const float* const* __restrict__ ptrs, const int32_t* __restrict__ wq,
+                           const double* __restrict__ n, int K, const float* __restrict__ g, float* __restrict__ out,
+                           int64_t P, int classes) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    const double gi = (double)g[i];
+    double acc = 0.0, den = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const int64_t j = hfl_sub_index(i, wq[k], classes);
+      if (j >= 0) {
+        acc += n[k] * ((double)ptrs[k][j] - gi);
+        den += n[k];
+      }
+    }
+    out[i] = den > 0.0 ? (float)(gi + acc / den) : g[i];
+  }
+}
+
+// the width-q sub-model of the full-width weights (what a width-q client starts from)
+__global__ void k_heterofl_extract(const float* __restrict__ g, int q, int classes, float* __restrict__ sub, int64_t P) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = hfl_sub_index(i, q, classes);
+    if (j >= 0) sub[j] = g[i];
+  }
+}
+
+}  // namespace protea
