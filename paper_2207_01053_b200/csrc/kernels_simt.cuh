@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(256)
 }
 
 constexpr int kHeadCnnThreads = 512;
-inline size_t head_cnn_smem(int F, int C) { return (size_t)(C * F + 64 * C + 64) * sizeof(float); }
+inline size_t head_cnn_smem(int F, int C) { return (size_t)(C * F + 64 * C + 64 + 128) * sizeof(float); }
 // + the client's activations h [64][F] staged in shared memory when that still fits (kHeadStageMax)
 constexpr size_t kHeadStageMax = 220 * 1024;
 inline size_t head_cnn_smem_staged(int F, int C, size_t esz) { return head_cnn_smem(F, C) + 64 * (size_t)F * esz; }
@@ -793,18 +793,24 @@ __global__ void __launch_bounds__(kHeadCnnThreads)
   float* Ws = hsm;              // [C][F] old W2
   float* dlog = Ws + C * F;     // [rows][C]
   float* lossr = dlog + 64 * C; // [rows]
+  int* lbl = reinterpret_cast<int*>(lossr + 64);  // [rows] labels (prefetched: perm -> y is a dependent pair)
+  float* b2s = lossr + 128;     // [C] fc2 bias
   const T* __restrict__ h = (const T*)c->buf[a.hbuf];
   T* __restrict__ dh = (T*)c->buf[a.dhbuf];
   float* __restrict__ W = c->params + a.w;
   float* __restrict__ bias = c->params + a.b;
+  if (threadIdx.x < rows) lbl[threadIdx.x] = c->y[c->perm[tk.base + threadIdx.x]];
+  if (threadIdx.x >= 256 && threadIdx.x - 256 < C) b2s[threadIdx.x - 256] = bias[threadIdx.x - 256];
   if (stage_h) {  // h read once with 16-byte loads (every row is re-read C + 2 times below)
-    T* hs = reinterpret_cast<T*>(lossr + 64);
+    T* hs = reinterpret_cast<T*>(lossr + 192);
     const int n16 = rows * F * (int)sizeof(T) / 16;
     for (int i = threadIdx.x; i < n16; i += kHeadCnnThreads)
       reinterpret_cast<uint4*>(hs)[i] = __ldg(reinterpret_cast<const uint4*>(h) + i);
     h = hs;
   }
-  for (int i = threadIdx.x; i < C * F; i += kHeadCnnThreads) Ws[i] = W[i];
+#pragma unroll 4
+  for (int i = threadIdx.x; i < C * F / 4; i += kHeadCnnThreads)  // F % 128 == 0, fc2 W 16-byte aligned
+    reinterpret_cast<float4*>(Ws)[i] = reinterpret_cast<const float4*>(W)[i];
   __syncthreads();
   // 1. logits
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -825,7 +831,7 @@ __global__ void __launch_bounds__(kHeadCnnThreads)
         float v = acc[j];
 #pragma unroll
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0 && c0 + j < C) dlog[r * C + c0 + j] = v + bias[c0 + j];
+        if (lane == 0 && c0 + j < C) dlog[r * C + c0 + j] = v + b2s[c0 + j];
       }
     }
   }
@@ -833,7 +839,7 @@ __global__ void __launch_bounds__(kHeadCnnThreads)
   // 2. softmax cross-entropy (mean over the batch rows)
   if (threadIdx.x < rows) {
     const int r = threadIdx.x;
-    const int label = c->y[c->perm[tk.base + r]];
+    const int label = lbl[r];
     float mx = -INFINITY;
     for (int cc = 0; cc < C; ++cc) mx = fmaxf(mx, dlog[r * C + cc]);
     float s = 0.f;
@@ -880,7 +886,7 @@ __global__ void __launch_bounds__(kHeadCnnThreads)
   if (threadIdx.x < C) {
     float g = 0.f;
     for (int r = 0; r < rows; ++r) g += dlog[r * C + threadIdx.x];
-    bias[threadIdx.x] -= a.lr * g;
+    bias[threadIdx.x] = b2s[threadIdx.x] - a.lr * g;
   }
   if (threadIdx.x == 0) {
     float s = 0.f;
