@@ -877,20 +877,26 @@ constexpr int kStageThreads = 256;
 __global__ void __launch_bounds__(kStageThreads)
     k_stage_x(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, const int* __restrict__ prefix,
               int ntask) {
+  __shared__ float lut[256];  // px01(u): the same fp32 values as the division, without one per channel
+  lut[threadIdx.x] = px01((uint8_t)threadIdx.x);
   pdl_wait();  // xs is still read by the preceding conv1 wgrad
   pdl_trigger();
   const int ti = find_task(prefix, ntask, blockIdx.x);
   const Task tk = tasks[ti];
   const ClientRec* c = recs + tk.rec;
   const int e = (blockIdx.x - __ldg(prefix + ti)) * kStageThreads + threadIdx.x;  // staged pixel, storage order
-  if (e >= tk.rows * 1296) return;
   const int r = e / 1296, rem = e - r * 1296, Y = rem / 36, rx = rem - Y * 36, X = 2 * (rx % 18) + rx / 18;
   const int y = Y - 2, x = X - 2;
+  const bool in = e < tk.rows * 1296 && (unsigned)y < 32u && (unsigned)x < 32u;
+  const uint8_t* px = in ? c->x + (int64_t)__ldg(c->perm + tk.base + r) * 3072 + (y * 32 + x) * 3 : nullptr;
+  uint32_t u0 = 0, u1 = 0, u2 = 0;
+  if (in) u0 = __ldg(px), u1 = __ldg(px + 1), u2 = __ldg(px + 2);
+  __syncthreads();  // lut
+  if (e >= tk.rows * 1296) return;
   uint4 out = make_uint4(0, 0, 0, 0);
-  if ((unsigned)y < 32u && (unsigned)x < 32u) {
-    const uint8_t* px = c->x + (int64_t)c->perm[tk.base + r] * 3072 + (y * 32 + x) * 3;
-    const __nv_bfloat162 v01 = __floats2bfloat162_rn(px01(px[0]), px01(px[1]));
-    const __nv_bfloat162 v23 = __floats2bfloat162_rn(px01(px[2]), 1.f);
+  if (in) {
+    const __nv_bfloat162 v01 = __floats2bfloat162_rn(lut[u0], lut[u1]);
+    const __nv_bfloat162 v23 = __floats2bfloat162_rn(lut[u2], 1.f);
     out.x = *reinterpret_cast<const uint32_t*>(&v01);
     out.y = *reinterpret_cast<const uint32_t*>(&v23);
   }
