@@ -331,7 +331,14 @@ def main():
 
     # ---- roofline of the dominant kernel (achieved per launch from the live events)
     pk = peaks()
-    avg_ns = dom_ns / max(1, dom_n)
+    timing_src = "timed rounds (CUDA events on the launching stream)"
+    if dom_n == 0 and op_stats is not None and op_stats["op_launches"][dominant]:
+        # every launch of the op ran deferred on the side stream in the timed rounds (PROTEA_OVERLAP_ROWS):
+        # take the serialised warm-up round's launches of it instead
+        dom_n = int(op_stats["op_launches"][dominant])
+        dom_ns, dom_fl, dom_by = op_stats["op_ns"][dominant], op_stats["op_flops"][dominant], op_stats["op_bytes"][dominant]
+        timing_src = "serialised warm-up round (every timed-round launch was deferred to the side stream)"
+    avg_ns = max(dom_ns / max(1, dom_n), 1.0)
     fl_per = dom_fl / max(1, dom_n)
     by_per = dom_by / max(1, dom_n)
     alu_peak = fp32_alu_peak_tflops(pk["sm_max_mhz"])
@@ -360,7 +367,7 @@ def main():
     roof = {"kernel": pb.OPC_NAMES[dominant], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": traffic,
             "peak_src": pk["src"] if bound != "alu" else f"derived: 148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
-            "per_launch": {"flops": fl_per, "bytes": by_per, "avg_ns": avg_ns, "launches": dom_n},
+            "per_launch": {"flops": fl_per, "bytes": by_per, "avg_ns": avg_ns, "launches": dom_n, "source": timing_src},
             "share_of_step": dom_ns / (dev_ms * 1e6 / 1.0) if world == 1 else None,
             "share_of_step_serialized": (op_stats["op_ns"][dominant] / max(1, op_stats["round_ns"])) if op_stats else None}
 
