@@ -122,6 +122,7 @@ struct protea_ctx {
   // programmatic dependent launch on the lock-step stream (PROTEA_PDL=1).  Off by default: measured on
   // B200, config 2: 70.2 ms/round without, 71.5 ms with (early CTAs of the next kernel hold SM resources).
   bool pdl = false;
+  int f1w_side_smem = 0;  // deferred fc1 wgrad: dynamic smem floor (PROTEA_F1W_SIDE_SMEM), limits its CTAs per SM
   int lanes = 1;     // lock-step lanes per model group (PROTEA_LANES): independent chains on own streams
   int spin_cap = 148;  // CTAs of a kernel whose CTAs spin-wait on each other (the width-1 CNN wgrad split
                        // reduces): g_num_sms / lanes, so concurrent lanes' instances are all co-resident
@@ -532,17 +533,19 @@ void launch_gemm(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, cons
 }
 
 template <int BN, int STAGES, class OpT>
-void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, const int32_t* dtab) {
+void launch_gemm_tc(protea_ctx* ctx, const OpT& op, const Launch& L, int opid, const int32_t* dtab,
+                    int smem_floor = 0) {  // smem_floor: reserve at least this much (fewer resident CTAs)
   constexpr int SMEM = tc_smem_bytes<BN, STAGES>();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, OpT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(k_gemm_tc<BN, STAGES, OpT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int* prefix = dtab + L.prefix_off[opid];
   const int ev = op_begin(ctx, op_class(opid), opid);
-  launch_k(ctx, k_gemm_tc<BN, STAGES, OpT>, L.grid[opid], kTcThreads, SMEM, op, tasks, prefix, L.ntask);
+  launch_k(ctx, k_gemm_tc<BN, STAGES, OpT>, L.grid[opid], kTcThreads, (size_t)std::max(SMEM, smem_floor), op, tasks,
+           prefix, L.ntask);
   op_end(ctx, ev);
 }
 
@@ -678,7 +681,8 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
     cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0);
     cudaStream_t main = ctx->cur;
     ctx->cur = ctx->side;
-    launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
+    // deferred: fewer resident CTAs (PROTEA_F1W_SIDE_SMEM) spread its HBM stream over the chain it overlaps
+    launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab, ctx->f1w_side_smem);
     cudaEventRecord(ctx->gjoin[L.group], ctx->side);
     ctx->gpending[L.group] = 1;
     ctx->cur = main;
@@ -1041,6 +1045,7 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
   cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest);
   if (const char* ov = std::getenv("PROTEA_OVERLAP_ROWS")) ctx->overlap_rows = std::atoll(ov);
   if (const char* pd = std::getenv("PROTEA_PDL")) ctx->pdl = std::atoi(pd) != 0;
+  if (const char* fs = std::getenv("PROTEA_F1W_SIDE_SMEM")) ctx->f1w_side_smem = std::max(0, std::min(220 * 1024, std::atoi(fs)));
   if (const char* ln = std::getenv("PROTEA_LANES")) ctx->lanes = std::max(1, std::min(4, std::atoi(ln)));
   if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_least) != cudaSuccess ||
       cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, prio_greatest) != cudaSuccess ||
