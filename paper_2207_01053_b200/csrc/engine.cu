@@ -122,7 +122,9 @@ struct protea_ctx {
   // programmatic dependent launch on the lock-step stream (PROTEA_PDL=1).  Off by default: measured on
   // B200, config 2: 70.2 ms/round without, 71.5 ms with (early CTAs of the next kernel hold SM resources).
   bool pdl = false;
-  int f1w_side_smem = 0;  // deferred fc1 wgrad: dynamic smem floor (PROTEA_F1W_SIDE_SMEM), limits its CTAs per SM
+  int f1w_side_smem = 0;
+  bool defer_c2r = true;
+  bool single_chain = true;  // this round's lock-step chain is one stream (one group, one lane)  // width-1 conv2 wgrad split reduce on the side stream (PROTEA_DEFER_C2R=0: in-kernel)  // deferred fc1 wgrad: dynamic smem floor (PROTEA_F1W_SIDE_SMEM), limits its CTAs per SM
   int lanes = 1;     // lock-step lanes per model group (PROTEA_LANES): independent chains on own streams
   int spin_cap = 148;  // CTAs of a kernel whose CTAs spin-wait on each other (the width-1 CNN wgrad split
                        // reduces): g_num_sms / lanes, so concurrent lanes' instances are all co-resident
@@ -611,10 +613,21 @@ void launch_conv2_wgrad_halo(protea_ctx* ctx, const ClientRec* drecs, const CnnD
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[OP_C2W], ctx->spin_cap);  // spin-waiting split reduce: all CTAs co-resident
+  // deferred split reduce: the weights are next read by the group's next conv2 fwd, so the reduce runs on
+  // the low-priority side stream and overlaps conv1 wgrad (single-stream rounds only)
+  const int defer = ctx->defer_c2r && ctx->single_chain && ctx->cur == ctx->hi && !ctx->serialize;
   const int ev = op_begin(ctx, OP_C2W, OP_C2W);
   launch_k(ctx, k_conv2_wgrad_halo, grid, kConvThreads, kW2Smem, drecs, tasks, (const int*)(dtab + L.prefix_off[OP_C2W]),
-           L.ntask, d, lr, L.c2w_groups);
+           L.ntask, d, lr, L.c2w_groups, defer);
   op_end(ctx, ev);
+  if (defer) {
+    cudaEventRecord(ctx->fork_ev, ctx->cur);
+    cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0);
+    k_conv2_wgrad_reduce<<<dim3(cdiv(64 * (kW2NP / 4), 256), L.ntask), 256, 0, ctx->side>>>(drecs, tasks, d, lr);
+    ctx->launches++;
+    cudaEventRecord(ctx->gjoin[L.group], ctx->side);
+    ctx->gpending[L.group] = 1;
+  }
 }
 
 template <typename T>
@@ -1046,6 +1059,7 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
   if (const char* ov = std::getenv("PROTEA_OVERLAP_ROWS")) ctx->overlap_rows = std::atoll(ov);
   if (const char* pd = std::getenv("PROTEA_PDL")) ctx->pdl = std::atoi(pd) != 0;
   if (const char* fs = std::getenv("PROTEA_F1W_SIDE_SMEM")) ctx->f1w_side_smem = std::max(0, std::min(220 * 1024, std::atoi(fs)));
+  if (const char* dc = std::getenv("PROTEA_DEFER_C2R")) ctx->defer_c2r = std::atoi(dc) != 0;
   if (const char* ln = std::getenv("PROTEA_LANES")) ctx->lanes = std::max(1, std::min(4, std::atoi(ln)));
   if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_least) != cudaSuccess ||
       cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, prio_greatest) != cudaSuccess ||
@@ -1390,6 +1404,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
   std::vector<cudaStream_t> gs(V, ctx->hi);
   for (int v = 1; v < V; ++v) gs[v] = ctx->serialize ? ctx->hi : ctx->gstream[v];  // serialize: one stream
   ctx->spin_cap = std::max(1, g_num_sms / (ctx->serialize ? 1 : NL));  // one spin-waiting wgrad per lane at a time
+  ctx->single_chain = V == 1;
   CK(cudaEventRecord(ctx->fork_ev, ctx->stream));
   CK(cudaStreamWaitEvent(ctx->hi, ctx->fork_ev, 0));
   ctx->cur = ctx->hi;

@@ -765,7 +765,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(acc_empty);  // TMEM drained: the next item's MMAs may start
       tc::named_sync(1, 256);
-      float* part = (float*)c->buf[B_WSP] + (int64_t)split * 76 * 32;
+      // partials in dz2 (free from conv2 wgrad's end to the next fc1 dgrad): B_WSP may still hold conv2's
+      // partials for their deferred reduce (k_conv2_wgrad_reduce on the side stream)
+      float* part = (float*)c->buf[B_DZ2] + (int64_t)split * 76 * 32;
       for (int e = threadIdx.x; e < 76 * 32; e += 256)
         part[e] = ((S[e] + S[2432 + e]) + S[2 * 2432 + e]) + S[3 * 2432 + e];
       // publish this split's partial (arrival counter stats[9])
@@ -790,7 +792,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       tc::named_sync(1, 256);
       __threadfence();
       const int e_lo = item * 2432 / splits, e_hi = (item + 1) * 2432 / splits;
-      for (int e = e_lo + threadIdx.x; e < e_hi; e += 256) conv1_reduce_update(c, splits, 32, off_w, off_b, lr, e);
+      for (int e = e_lo + threadIdx.x; e < e_hi; e += 256)
+        conv1_reduce_update(c, splits, 32, off_w, off_b, lr, e, B_DZ2);
       tc::named_sync(1, 256);
       if (threadIdx.x == 0 && atomicAdd(done, 1) == splits - 1) {  // last slice: reset for the next step
         *arrive = 0;
@@ -858,7 +861,7 @@ __device__ __forceinline__ int w2_row(int j, int row) {  // weight row of TMEM l
 
 __global__ void __launch_bounds__(kConvThreads, 1)
     k_conv2_wgrad_halo(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks,
-                       const int* __restrict__ prefix, int ntask, CnnDims d, float lr, int ng) {
+                       const int* __restrict__ prefix, int ntask, CnnDims d, float lr, int ng, int defer_reduce) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kW2Stages * kW2Stage + kW2Pad);
@@ -1021,7 +1024,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       if (lane == 0) tc::mbar_arrive(acc_empty);  // TMEM drained: the next item's MMAs may start
       if (warp == 0) DBG_ADD(6, td);
       DBG_T0(tr);
-      if (splits > 1) {  // publish this item's partial (arrival counter stats[8])
+      if (splits > 1 && !defer_reduce) {  // publish this item's partial (arrival counter stats[8])
         __threadfence();
         tc::named_sync(1, 256);
         if (threadIdx.x == 0) atomicAdd(reinterpret_cast<int*>(c->stats) + 8, 1);
@@ -1035,7 +1038,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     DBG_T0(tsr);
     TaskCursor rc;
     rc.init(prefix, ntask, g0 < total ? g0 : total - 1);
-    for (int g = g0; g < g1; ++g) {
+    for (int g = g0; g < (defer_reduce ? g0 : g1); ++g) {  // deferred: k_conv2_wgrad_reduce
       rc.advance(prefix, g);
       const Task tk = tasks[rc.ti];
       const int splits = (tk.rows + 7) / 8, nitem = splits * ng, item = g - rc.lo;
@@ -1101,6 +1104,44 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       lo = hi;
       ++ti;
     }
+  }
+}
+
+// conv2 wgrad split reduce as its own launch (the deferred form of k_conv2_wgrad_halo's in-kernel
+// reduce): block (x, task) sums float4 chunk x of the client's [C2][804] partials over its splits in
+// split order and applies SGD to the fp32 master and the bf16 shadow.  Launched on the side stream
+// after the wgrad, joined before the group's next conv2 fwd (the next reader of the weights).
+__global__ void __launch_bounds__(256) k_conv2_wgrad_reduce(const ClientRec* __restrict__ recs,
+                                                            const Task* __restrict__ tasks, CnnDims d, float lr) {
+  const Task tk = tasks[blockIdx.y];
+  const int splits = (tk.rows + 7) / 8;
+  if (splits == 1) return;  // updated from TMEM by the wgrad kernel
+  const ClientRec* c = recs + tk.rec;
+  constexpr int Q = kW2NP / 4, NE = 64 * Q;
+  const int e = blockIdx.x * 256 + threadIdx.x;
+  if (e >= NE) return;
+  float* P = c->params;
+  bf16* S = (bf16*)c->buf[B_WSH];
+  const float4* pt = (const float4*)c->buf[B_WSP];
+  const int co = e / Q, m0 = 4 * (e - co * Q);
+  const int64_t idx = d.w2 + (int64_t)co * 800 + m0;
+  float4 w = m0 < 800 ? *reinterpret_cast<const float4*>(P + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 q[8];
+#pragma unroll
+  for (int sp = 0; sp < 8; ++sp)
+    if (sp < splits) q[sp] = __ldcg(pt + (int64_t)sp * NE + e);
+  float4 gs = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int sp = 0; sp < 8; ++sp)
+    if (sp < splits) gs.x += q[sp].x, gs.y += q[sp].y, gs.z += q[sp].z, gs.w += q[sp].w;
+  if (m0 < 800) {
+    w.x -= lr * gs.x, w.y -= lr * gs.y, w.z -= lr * gs.z, w.w -= lr * gs.w;
+    *reinterpret_cast<float4*>(P + idx) = w;
+    const __nv_bfloat162 h0 = __floats2bfloat162_rn(w.x, w.y), h1 = __floats2bfloat162_rn(w.z, w.w);
+    *reinterpret_cast<uint2*>(S + idx) =
+        make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+  } else if (m0 == 800) {
+    P[d.b2 + co] -= lr * gs.x;
   }
 }
 

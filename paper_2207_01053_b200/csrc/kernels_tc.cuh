@@ -963,9 +963,9 @@ struct TcConv1Wgrad {
 // Sum the split partials of element e = idx * C1 + co (idx 0..74 = weight (tap, ci), 75 = bias) in split
 // order and apply SGD to the fp32 master and the pool-quad bf16 shadow (common.h w1q_index).
 __device__ __forceinline__ void conv1_reduce_update(const ClientRec* c, int splits, int C1, int64_t off_w,
-                                                    int64_t off_b, float lr, int e) {
+                                                    int64_t off_b, float lr, int e, int pbuf = B_WSP) {
   const int total = 76 * C1;
-  const float* part = (const float*)c->buf[B_WSP];
+  const float* part = (const float*)c->buf[pbuf];  // split partials [splits][76 C1]
   float g = 0.f;
   for (int s0 = 0; s0 < splits; s0 += 8) {  // 8 independent loads in flight, summed in split order
     float v[8];
