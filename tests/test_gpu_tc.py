@@ -201,3 +201,10 @@ def test_config2_full_size(torch):
     ref = orr.run_round([c for c in wl.clients if c.id in sample], wl.shards, {4: w0}, wl.lr, wl.seed, 0,
                         workers=2)[4]
     assert rel_l2(got, ref) <= 5e-2
+
+
+def test_deferred_conv2_reduce_bitwise(torch):
+    """The width-1 conv2 wgrad split reduce on the side stream (default) sums the same partials in the
+    same split order as the in-kernel distributed reduce (PROTEA_DEFER_C2R=0): bitwise equal rounds."""
+    wl = synth.build_workload(2, n_clients=8, samples=70, epochs=1)  # B = 16 .. 64: several splits
+    assert np.array_equal(_bf16_round(wl), _bf16_round(wl, env={"PROTEA_DEFER_C2R": "0"}))
