@@ -124,7 +124,13 @@ struct protea_ctx {
   bool pdl = false;
   int f1w_side_smem = 0;
   bool defer_c2r = true;
-  bool single_chain = true;  // this round's lock-step chain is one stream (one group, one lane)  // width-1 conv2 wgrad split reduce on the side stream (PROTEA_DEFER_C2R=0: in-kernel)  // deferred fc1 wgrad: dynamic smem floor (PROTEA_F1W_SIDE_SMEM), limits its CTAs per SM
+  bool single_chain = true;
+  // ResNet-8 bf16 backward: layer i's wgrad on its own stream beside layer i's dgrad (PROTEA_R8_OVERLAP)
+  bool r8_overlap = true;
+  int64_t r8_overlap_rows = 1024;  // ... in iterations of at most this many rows (PROTEA_R8_OVERLAP_ROWS)
+  int64_t rows_now = 0;            // rows of the current lock-step iteration (all groups)
+  cudaStream_t wstream = nullptr;
+  cudaEvent_t r8ev[16] = {};  // this round's lock-step chain is one stream (one group, one lane)  // width-1 conv2 wgrad split reduce on the side stream (PROTEA_DEFER_C2R=0: in-kernel)  // deferred fc1 wgrad: dynamic smem floor (PROTEA_F1W_SIDE_SMEM), limits its CTAs per SM
   int lanes = 1;     // lock-step lanes per model group (PROTEA_LANES): independent chains on own streams
   int spin_cap = 148;  // CTAs of a kernel whose CTAs spin-wait on each other (the width-1 CNN wgrad split
                        // reduces): g_num_sms / lanes, so concurrent lanes' instances are all co-resident
@@ -774,7 +780,7 @@ RConv rconv(const Layer& l) {
 // ResNet tcgen05 ops: persistent cp.async GEMM, contiguous tile ranges; the B tile (BN) sized to the
 // layer's N (16 / 32 -> 32, 64 -> 64) so no gather slots are spent on zero-filled columns
 template <int BN, class Op>
-void launch_rtc_bn(protea_ctx* ctx, const Op& op, const Launch& L, int opid, const int32_t* dtab) {
+void launch_rtc_bn(protea_ctx* ctx, const Op& op, const Launch& L, int opid, const int32_t* dtab, int sm_cap) {
   constexpr int RS = 8;  // ring stages (1 CTA per SM: 8 K blocks in flight)
   constexpr int SMEM = rp_smem_bytes<BN, RS>();
   static int per_sm = 0;  // resident CTAs per SM (registers / shared memory): the persistent grid
@@ -784,18 +790,20 @@ void launch_rtc_bn(protea_ctx* ctx, const Op& op, const Launch& L, int opid, con
     per_sm = std::max(1, std::min(per_sm, 2));
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
-  const int grid = std::min(L.grid[opid], per_sm * g_num_sms);
+  const int grid = std::min(L.grid[opid], per_sm * sm_cap);
   const int ev = op_begin(ctx, op_class(opid), opid);
   launch_k(ctx, k_gemm_tc_pers<BN, RS, Op>, grid, kRpThreads, SMEM, op, tasks, (const int*)(dtab + L.prefix_off[opid]),
            L.ntask);
   op_end(ctx, ev);
 }
 template <class Op>
-void launch_rtc(protea_ctx* ctx, const Op& op, const Launch& L, int opid, const int32_t* dtab, int N) {
+void launch_rtc(protea_ctx* ctx, const Op& op, const Launch& L, int opid, const int32_t* dtab, int N,
+                int sm_cap = 0) {
+  if (sm_cap <= 0) sm_cap = g_num_sms;
   if (N <= 32)
-    launch_rtc_bn<32>(ctx, op, L, opid, dtab);
+    launch_rtc_bn<32>(ctx, op, L, opid, dtab, sm_cap);
   else
-    launch_rtc_bn<64>(ctx, op, L, opid, dtab);
+    launch_rtc_bn<64>(ctx, op, L, opid, dtab, sm_cap);
 }
 
 void stage_r(protea_ctx* ctx, const ClientRec* drecs, const Task* tasks, const Launch& L, int out_buf) {
@@ -859,8 +867,22 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
       {B_R_G0, B_R_G1, B_R_R3, -1, 0, 0}};             // b3b: dr3 = convT(ds3) * (r3 > 0)
   const int wg_dout[7] = {B_R_G0, B_R_G2, B_R_G1, B_R_G0, B_R_G2, B_R_G1, B_R_G0};
   ReduceMulti rm;
+  // bf16, one chain: wgrad(i) runs on ctx->wstream beside dgrad(i) (both only read dout(i)), each on half
+  // the SMs; the gradient buffers rotate over three, so dgrad(i - 2) (which overwrites wgrad(i)'s dout)
+  // waits for wgrad(i), and the merged reduce waits for all of them
+  const bool ovl = TC && ctx->r8_overlap && ctx->single_chain && !ctx->serialize && ctx->cur == ctx->hi &&
+                   ctx->rows_now <= ctx->r8_overlap_rows;  // light iterations: latency-bound kernels
+  const int half = ovl ? std::max(1, g_num_sms / 2) : 0;
+  if (ovl)
+    for (auto& e : ctx->r8ev)
+      if (!e) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  cudaStream_t main_s = ctx->cur;
   for (int i = 6; i >= 0; --i) {
     const Layer& l = m.layers[i];
+    if (ovl) {
+      cudaEventRecord(ctx->r8ev[8 + i], main_s);  // dout(i) is ready (written before this point)
+      if (i + 2 <= 6) cudaStreamWaitEvent(main_s, ctx->r8ev[i + 2], 0);  // wgrad(i + 2) read what dgrad(i) overwrites
+    }
     if (i >= 1) {
       D dg;
       dg.recs = drecs;
@@ -873,7 +895,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
       dg.Cadd = bw[i].cadd;
       if (TC) {
         RTcDgrad td{drecs, rtc(l), dg.dout_buf, dg.out_buf, dg.mask_buf, dg.add_buf, dg.add_mode, dg.Cadd};
-        launch_rtc(ctx, td, L, RI_D1 + i - 1, dtab, td.L.Cin);
+        launch_rtc(ctx, td, L, RI_D1 + i - 1, dtab, td.L.Cin, half);
       } else {
         launch_gemm<D, R_BM, R_BN>(ctx, dg, L, RI_D1 + i - 1, dtab);
       }
@@ -885,7 +907,15 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
         tw.L.lci = 3;
         tw.in_buf = B_R_XS;
       }
-      launch_rtc(ctx, tw, L, RI_W0 + i, dtab, tw.L.Cout);
+      if (ovl) {
+        ctx->cur = ctx->wstream;
+        cudaStreamWaitEvent(ctx->cur, ctx->r8ev[8 + i], 0);
+        launch_rtc(ctx, tw, L, RI_W0 + i, dtab, tw.L.Cout, g_num_sms - half);
+        cudaEventRecord(ctx->r8ev[i], ctx->cur);
+        ctx->cur = main_s;
+      } else {
+        launch_rtc(ctx, tw, L, RI_W0 + i, dtab, tw.L.Cout);
+      }
     } else {
       Wg wg;
       wg.recs = drecs;
@@ -901,6 +931,8 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
                          TC ? (i == 0 ? 2 : 1) : 0, i};
     rm.prefix[i] = dtab + L.prefix_off[RI_R0 + i];
   }
+  if (ovl)
+    for (int i = 0; i < 2; ++i) cudaStreamWaitEvent(main_s, ctx->r8ev[i], 0);  // wgrads 2..6 joined above
   rm.base[0] = 0;
   for (int i = 0; i < 7; ++i) rm.base[i + 1] = rm.base[i] + L.grid[RI_R0 + i];
   ev = op_begin(ctx, PROTEA_OPC_R_REDUCE, -1);
@@ -1060,9 +1092,12 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
   if (const char* pd = std::getenv("PROTEA_PDL")) ctx->pdl = std::atoi(pd) != 0;
   if (const char* fs = std::getenv("PROTEA_F1W_SIDE_SMEM")) ctx->f1w_side_smem = std::max(0, std::min(220 * 1024, std::atoi(fs)));
   if (const char* dc = std::getenv("PROTEA_DEFER_C2R")) ctx->defer_c2r = std::atoi(dc) != 0;
+  if (const char* ro = std::getenv("PROTEA_R8_OVERLAP")) ctx->r8_overlap = std::atoi(ro) != 0;
+  if (const char* rr = std::getenv("PROTEA_R8_OVERLAP_ROWS")) ctx->r8_overlap_rows = std::atoll(rr);
   if (const char* ln = std::getenv("PROTEA_LANES")) ctx->lanes = std::max(1, std::min(4, std::atoi(ln)));
   if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_least) != cudaSuccess ||
       cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, prio_greatest) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&ctx->wstream, cudaStreamNonBlocking, prio_greatest) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming) != cudaSuccess) {
     set_global_error("protea_init: stream/event creation failed");
@@ -1115,6 +1150,12 @@ void protea_finalize(protea_ctx* ctx) {
     cudaStreamSynchronize(ctx->hi);
     cudaStreamDestroy(ctx->hi);
   }
+  if (ctx->wstream) {
+    cudaStreamSynchronize(ctx->wstream);
+    cudaStreamDestroy(ctx->wstream);
+  }
+  for (auto e : ctx->r8ev)
+    if (e) cudaEventDestroy(e);
   for (auto e : ctx->gjoin) cudaEventDestroy(e);
   for (auto sgs : ctx->gstream) {
     cudaStreamSynchronize(sgs);
@@ -1430,6 +1471,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
   for (uint64_t t = 0; t < T; ++t) {
     // (several groups already overlap each other: no side-stream deferral then)
     ctx->overlap_now = tc_mode && !ctx->serialize && V == 1 && iter_rows[t] <= ctx->overlap_rows;
+    ctx->rows_now = iter_rows[t];
     if (admits[t].second > 0) {
       // an admitted client may reuse a slot released by any group: every group's earlier work first
       ctx->cur = ctx->hi;
