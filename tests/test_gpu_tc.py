@@ -208,3 +208,10 @@ def test_deferred_conv2_reduce_bitwise(torch):
     same split order as the in-kernel distributed reduce (PROTEA_DEFER_C2R=0): bitwise equal rounds."""
     wl = synth.build_workload(2, n_clients=8, samples=70, epochs=1)  # B = 16 .. 64: several splits
     assert np.array_equal(_bf16_round(wl), _bf16_round(wl, env={"PROTEA_DEFER_C2R": "0"}))
+
+
+def test_resnet8_dgrad_wgrad_overlap_bitwise(torch):
+    """ResNet-8 light iterations run layer i's wgrad beside its dgrad on a second stream; the arithmetic
+    is unchanged, so the round is bitwise the serial one (PROTEA_R8_OVERLAP=0)."""
+    wl = _resnet_one_step(16, k=3, epochs=2)
+    assert np.array_equal(_bf16_round(wl), _bf16_round(wl, env={"PROTEA_R8_OVERLAP": "0"}))
