@@ -77,19 +77,36 @@ __global__ void __launch_bounds__(kPermThreads)
 // Release (P:209 stage (4) "resources get freed") + FedAvg partial:
 // acc[d] += n_k * (w_k[d] - w_g[d]) in fp64, clients in the given (ascending
 // id) order, so the per-element summation order is fixed.
-__global__ void k_release_acc(const ClientRec* __restrict__ recs, const int* __restrict__ ids, int nrel, int64_t P,
-                              double* __restrict__ loss) {
+__global__ void __launch_bounds__(256) k_release_acc(const ClientRec* __restrict__ recs, const int* __restrict__ ids,
+                                                     int nrel, int64_t P, double* __restrict__ loss) {
+  __shared__ const float* prm[256];  // the released clients' parameter pointers and weights, staged per chunk
+  __shared__ double wn[256];
   if (loss && blockIdx.x == 0 && threadIdx.x == 0)
     for (int i = 0; i < nrel; ++i) *loss += (double)recs[ids[i]].stats[0];
-  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < P; d += (int64_t)gridDim.x * blockDim.x) {
-    const ClientRec* c0 = recs + ids[0];
-    double a = c0->acc[d];
-    const double g = (double)c0->wg[d];
-    for (int i = 0; i < nrel; ++i) {
-      const ClientRec* c = recs + ids[i];
-      a += (double)c->n * ((double)c->params[d] - g);
+  const ClientRec* c0 = recs + ids[0];
+  for (int i0 = 0; i0 < nrel; i0 += 256) {  // client chunks: the per-element sum keeps the given client order
+    const int nc = min(256, nrel - i0);
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      const ClientRec* c = recs + ids[i0 + threadIdx.x];
+      prm[threadIdx.x] = c->params;
+      wn[threadIdx.x] = (double)c->n;
     }
-    c0->acc[d] = a;
+    __syncthreads();
+    for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < P; d += (int64_t)gridDim.x * blockDim.x) {
+      double a = c0->acc[d];
+      const double g = (double)c0->wg[d];
+      int i = 0;
+      for (; i + 4 <= nc; i += 4) {  // four independent loads in flight, accumulated in order
+        const float p0 = prm[i][d], p1 = prm[i + 1][d], p2 = prm[i + 2][d], p3 = prm[i + 3][d];
+        a += wn[i] * ((double)p0 - g);
+        a += wn[i + 1] * ((double)p1 - g);
+        a += wn[i + 2] * ((double)p2 - g);
+        a += wn[i + 3] * ((double)p3 - g);
+      }
+      for (; i < nc; ++i) a += wn[i] * ((double)prm[i][d] - g);
+      c0->acc[d] = a;
+    }
   }
 }
 
