@@ -364,8 +364,21 @@ def main():
                 traffic = by_per * rec["dram_bytes_per_launch"] * rec["launches"] / algo_round
         except Exception:
             traffic = None
+    # implementation bytes beyond SURVEY §8(d)'s algorithmic ones: the bf16 mode's fc1 weight shadow write
+    # (2 B per weight per client-step; fc1 dgrad / fwd read it next step).  Client-steps of the timed launches
+    # from their algorithmic work: FLOPs = 2 W rows, bytes = rows (F + K) e + 8 W clients (engine op_work)
+    impl = None
+    if pb.OPC_NAMES[dominant] == "fc1_wgrad" and prec == pb.PREC_BF16:
+        Wf, Ff, Kf = 512 * 4096, 512, 4096
+        rows = fl_per / (2 * Wf)
+        clients_per = (by_per - rows * (Ff + Kf) * eb) / (8 * Wf)
+        shadow = 2 * Wf * clients_per
+        impl = {"shadow_write_bytes_per_launch": shadow, "clients_per_launch": clients_per,
+                "achieved_with_shadow": (by_per + shadow) / avg_ns,
+                "frac_with_shadow": (by_per + shadow) / avg_ns / pk["hbm"]}
     roof = {"kernel": pb.OPC_NAMES[dominant], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak, "traffic": traffic,
+            "frac": achieved / peak, "traffic": traffic, "algorithmic": "SURVEY §8(d): 8 B per fc1 weight per "
+            "client-step (fp32 master read + write) + dh / a2 reads", "implementation_extra": impl,
             "peak_src": pk["src"] if bound != "alu" else f"derived: 148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
             "per_launch": {"flops": fl_per, "bytes": by_per, "avg_ns": avg_ns, "launches": dom_n, "source": timing_src},
             "share_of_step": dom_ns / (dev_ms * 1e6 / 1.0) if world == 1 else None,

@@ -65,7 +65,10 @@ typedef struct {
   int32_t world;           /* number of ranks (GPUs); 1 = no NCCL */
   int32_t precision;       /* PROTEA_PREC_*: activation storage + GEMM operand type */
   const uint8_t* nccl_id;  /* host, 128 bytes (ncclUniqueId from rank 0, broadcast by the caller); NULL: no NCCL
-                              communicator (world == 1, or caller-side reduction via partial_only rounds) */
+                              communicator (world == 1, or caller-side reduction via partial_only rounds).
+                              Given (also with world == 1), protea_run_round agrees on the plan and on every
+                              rank's validation verdict through the communicator before any device work, and
+                              exchanges the FedAvg partials with ncclAllGather + a rank-ordered sum (K7) */
   void* arena;             /* device, caller-owned block holding the client slots (e.g. a torch uint8 tensor) */
   uint64_t arena_bytes;    /* capacity C_g of this GPU's arena */
   void* stream;            /* cudaStream_t to order all work on (NULL = the legacy default stream) */
@@ -244,7 +247,9 @@ uint64_t protea_plan_hash(const protea_client* clients, size_t n, const protea_a
  * global_in / global_out: n_params floats (all registered groups concatenated),
  * host or device; a group without sampled clients is copied unchanged.
  * measured (nullable): n records of in-run profiles; stats (nullable).
- * world > 1: the ranks' protea_plan_hash values must agree (else PLAN, nothing run).
+ * With a communicator: the ranks' protea_plan_hash values must agree and every rank must pass its own
+ * validation (else PLAN on the ranks that passed, nothing run anywhere); a rank failing during the round
+ * is reported to all ranks before the exchange (CUDA).
  * Errors: INVALID, PLAN, OOM, CUDA, NCCL. */
 protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, const protea_client* clients,
                                size_t n, const protea_assignment* plan, const float* global_in, float* global_out,
@@ -256,13 +261,23 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
  * Errors: INVALID (no partial round recorded, size mismatch), CUDA. */
 protea_status protea_round_partial(protea_ctx* ctx, double* dst, size_t n_params);
 
-/* Finish a partial round: global_out = global_in + acc_sum / N_group per shape
- * group (N_group = sum n_k over ALL ranks' clients of that group, recorded by
+/* Finish a partial round (= protea_round_finalize_ordered with one part): global_out = global_in +
+ * acc_sum / N_group per shape group (N_group = sum n_k over ALL ranks' clients of that group, recorded by
  * the last protea_run_round; groups without clients are copied unchanged).
  * acc_sum: the element-wise sum of every rank's partial (device or host).
  * Errors: INVALID, DIM, CUDA. */
 protea_status protea_round_finalize(protea_ctx* ctx, const double* acc_sum, const float* global_in, float* global_out,
                                     size_t n_params);
+
+/* Deterministic cross-rank finalise (K7, SURVEY §8(e) "gather the partials, reduce in rank order"):
+ * global_out = global_in + (((p_0 + p_1) + p_2) + ... + p_{nparts-1}) / N_group per shape group, the sum
+ * in fp64 in rank order, one rounding to fp32 (reading R20).  partials: nparts consecutive
+ * rank partials of n_params doubles each (protea_round_partial of ranks 0..nparts-1; device or host).
+ * This is the kernel protea_run_round runs after its ncclAllGather when it holds a communicator, so the
+ * multi-rank result equals this call on the same partials bit for bit.  N_group as in
+ * protea_round_finalize.  Errors: INVALID (null, nparts < 1, no round recorded), DIM, CUDA. */
+protea_status protea_round_finalize_ordered(protea_ctx* ctx, const double* partials, int32_t nparts,
+                                            const float* global_in, float* global_out, size_t n_params);
 
 /* HeteroFL-style overlapping-width aggregation for the CNN-w family (DESIGN.md
  * reading R23; the paper's FedAvg P:234 generalised to nested sub-models).  The global model is the

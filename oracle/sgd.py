@@ -193,8 +193,9 @@ def bf16(x):
     weight shadow in bf16 and accumulates in fp32."""
     f = np.asarray(x, dtype=np.float32)
     u = f.view(np.uint32).astype(np.uint64)
-    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
-    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+    r = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000  # RNE on the upper 16 bits (finite, inf: exact)
+    r = np.where(np.isnan(f), 0x7FC00000, r)          # NaN -> the canonical quiet NaN (IEEE: stays NaN)
+    return r.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
 def loss_and_grad(p, model, xb, yb, emulate_bf16=False):

@@ -31,6 +31,7 @@ ORDER_ASC_ID, ORDER_DESC_STEPS = 0, 1
 EXPORTS = ["protea_init", "protea_finalize", "protea_last_error", "protea_register_model", "protea_register_shards",
            "protea_profile_clients", "protea_plan", "protea_run_round", "protea_fedavg", "protea_client_footprint",
            "protea_selftest_gemm", "protea_round_partial", "protea_round_finalize", "protea_plan_hash",
+           "protea_round_finalize_ordered",
            "protea_evaluate", "protea_heterofl_extract", "protea_heterofl_aggregate"]
 
 
@@ -125,6 +126,7 @@ _lib.protea_client_footprint.argtypes = [ctypes.POINTER(ModelDesc), ctypes.c_int
                                          ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
 _lib.protea_round_partial.argtypes = [_vp, _vp, _sz]
 _lib.protea_round_finalize.argtypes = [_vp, _vp, _vp, _vp, _sz]
+_lib.protea_round_finalize_ordered.argtypes = [_vp, _vp, ctypes.c_int32, _vp, _vp, _sz]
 _lib.protea_selftest_gemm.argtypes = [_vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
 for _f in EXPORTS:
     if _f not in ("protea_finalize", "protea_last_error", "protea_plan_hash"):
@@ -274,6 +276,15 @@ def protea_round_partial(ctx, dst):
 def protea_round_finalize(ctx, acc_sum, global_in, global_out):
     n = global_in.numel() if hasattr(global_in, "numel") else global_in.size
     _check(_lib.protea_round_finalize(ctx, _ptr(acc_sum), _ptr(global_in), _ptr(global_out), n), ctx)
+
+
+def protea_round_finalize_ordered(ctx, partials, global_in, global_out):
+    """partials: float64 [nparts, n_params] tensor / array (device or host), ranks in order."""
+    n = global_in.numel() if hasattr(global_in, "numel") else global_in.size
+    nparts = partials.shape[0]
+    assert tuple(partials.shape) == (nparts, n)
+    _check(_lib.protea_round_finalize_ordered(ctx, _ptr(partials), int(nparts), _ptr(global_in), _ptr(global_out), n),
+           ctx)
 
 
 def protea_fedavg(ctx, params, num_examples, out):

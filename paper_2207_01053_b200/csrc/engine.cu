@@ -57,6 +57,7 @@ struct ShardDev {
   int64_t n = 0;
   uint8_t* x = nullptr;
   int32_t* y = nullptr;
+  int32_t ymin = 0, ymax = 0;  // label range (scanned at registration; run_round checks it against the model)
 };
 
 template <typename T>
@@ -94,6 +95,8 @@ struct protea_ctx {
   std::string err;
   DevArray<float> gin, gout;
   DevArray<double> acc;
+  DevArray<double> gath;     // K7: all-gathered per-rank partials [world][P + groups]
+  DevArray<uint64_t> flag;   // plan hash / error flags exchanged before and after a round
   DevArray<ClientRec> recs;
   DevArray<int32_t> tab;
   // protea_evaluate workspace (kept apart from the round's tables)
@@ -477,7 +480,9 @@ void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, u
     case OP_F1F: F = 2 * r * f * 64 * c2; B = r * 64 * c2 * e + e * f * 64 * c2 + 4 * f + r * f * e; break;
     case OP_HEAD: F = 3 * 2 * r * C * f; B = r * f * e + 8 * C * (f + 1) + r * f * e + 8 * f + r * 4; break;
     case OP_F1D: F = 2 * r * 64 * c2 * f; B = r * f * e + e * f * 64 * c2 + r * 64 * c2 * (e + 1) + r * 256 * c2 * e; break;
-    case OP_F1W: F = 2 * r * f * 64 * c2; B = r * f * e + r * 64 * c2 * e + (8 + (e == 2 ? 2 : 0)) * f * 64 * c2; break;
+    // fp32 master read + write (8 B per weight per client-step) + the dh / a2 reads; the bf16
+    // shadow write of the bf16 mode (2 B per weight) is implementation traffic, not counted here
+    case OP_F1W: F = 2 * r * f * 64 * c2; B = r * f * e + r * 64 * c2 * e + 8 * f * 64 * c2; break;
     case OP_C2D: F = 2 * r * 256 * c1 * 25 * c2; B = r * 256 * c2 * e + e * c2 * 25 * c1 + r * 256 * c1 * (e + 1) + r * 1024 * c1 * e; break;
     case OP_C2W: F = 2 * r * 256 * c2 * 25 * c1; B = r * 256 * c2 * e + r * 256 * c1 * e + 4 * s2 * c2 * (25 * c1 + 1); break;
     case OP_C2R: F = 0; B = 4 * s2 * c2 * (25 * c1 + 1) + (8 + (e == 2 ? 2 : 0)) * c2 * (25 * c1 + 1); break;
@@ -1107,7 +1112,7 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
     set_global_error("protea_init: cudaEventCreate failed");
     return PROTEA_ERR_CUDA;
   }
-  if (opts->world > 1 && opts->nccl_id) {
+  if (opts->nccl_id) {  // also world == 1: a one-rank communicator runs the same exchange path
     ncclUniqueId id;
     std::memcpy(&id, opts->nccl_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&ctx->comm, opts->world, id, opts->rank);
@@ -1131,6 +1136,8 @@ void protea_finalize(protea_ctx* ctx) {
   ctx->gin.release();
   ctx->gout.release();
   ctx->acc.release();
+  ctx->gath.release();
+  ctx->flag.release();
   ctx->recs.release();
   ctx->tab.release();
   ctx->ev_recs.release();
@@ -1177,6 +1184,11 @@ protea_status protea_register_model(protea_ctx* ctx, const protea_model_desc* de
   Group g;
   std::string err;
   if (!make_model(*desc, &g.m, &err)) return fail(ctx, PROTEA_ERR_INVALID, "register_model: " + err);
+  // every shard of a context is read with one input size D (register_shards copies n * D bytes)
+  if (!ctx->groups.empty() && g.m.in_dim() != ctx->groups[0].m.in_dim())
+    return fail(ctx, PROTEA_ERR_INVALID, "register_model: input size " + std::to_string(g.m.in_dim()) +
+                                             " differs from the registered models' " +
+                                             std::to_string(ctx->groups[0].m.in_dim()) + " (one input size per context)");
   g.offset = 0;
   for (auto& x : ctx->groups) g.offset += x.m.P;
   ctx->groups.push_back(g);
@@ -1210,9 +1222,13 @@ protea_status protea_register_shards(protea_ctx* ctx, const protea_shard* shards
         ctx->shards.erase(it);
       }
       d.n = s.n;
+      d.x = nullptr;
+      d.y = nullptr;
       CK(cudaMalloc(&d.x, (size_t)s.n * D));
       CK(cudaMalloc(&d.y, (size_t)s.n * 4));
     }
+    d.ymin = *std::min_element(s.y, s.y + s.n);
+    d.ymax = *std::max_element(s.y, s.y + s.n);
     CK(cudaMemcpyAsync(d.x, s.x, (size_t)s.n * D, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(d.y, s.y, (size_t)s.n * 4, cudaMemcpyHostToDevice, ctx->stream));
     ctx->shards[s.client_id] = d;
@@ -1548,76 +1564,67 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
                                const protea_assignment* plan, const float* global_in, float* global_out,
                                size_t n_params, protea_profile* measured, protea_round_stats* stats) {
   if (!ctx) return PROTEA_ERR_INVALID;
-  if (!opts || !clients || !plan || !global_in || !global_out || n == 0)
-    return fail(ctx, PROTEA_ERR_INVALID, "run_round: null argument or n == 0");
   int64_t Ptot = 0;
   for (auto& g : ctx->groups) Ptot += g.m.P;
-  if ((int64_t)n_params != Ptot)
-    return fail(ctx, PROTEA_ERR_DIM, "run_round: n_params " + std::to_string(n_params) + " != registered total " +
-                                         std::to_string(Ptot));
   const int e = ctx->precision == PROTEA_PREC_FP32 ? 4 : 2;
-  // ---- validate clients and plan
-  std::map<int64_t, const protea_assignment*> pa;
-  for (size_t i = 0; i < n; ++i)
-    if (!pa.emplace(plan[i].client_id, &plan[i]).second)
-      return fail(ctx, PROTEA_ERR_PLAN, "run_round: plan lists client " + std::to_string(plan[i].client_id) + " twice");
   std::vector<RunClient> all;
-  std::map<int64_t, int> seen;
   std::vector<int64_t> Ngroup(ctx->groups.size(), 0);
-  for (size_t i = 0; i < n; ++i) {
-    const protea_client& c = clients[i];
-    const std::string who = "run_round: client " + std::to_string(c.client_id);
-    if (!seen.emplace(c.client_id, 1).second) return fail(ctx, PROTEA_ERR_INVALID, who + " listed twice");
-    if (c.model_id < 0 || c.model_id >= (int)ctx->groups.size())
-      return fail(ctx, PROTEA_ERR_INVALID, who + ": unknown model_id");
-    if (c.batch <= 0 || c.batch > kMaxBatch || c.epochs <= 0)
-      return fail(ctx, PROTEA_ERR_INVALID, who + ": batch must be in [1, 64] and epochs > 0");
-    auto sh = ctx->shards.find(c.client_id);
-    if (sh == ctx->shards.end()) return fail(ctx, PROTEA_ERR_INVALID, who + ": no registered shard");
-    auto it = pa.find(c.client_id);
-    if (it == pa.end()) return fail(ctx, PROTEA_ERR_PLAN, who + " missing from the plan");
-    const protea_assignment& a = *it->second;
-    RunClient r;
-    r.id = c.client_id;
-    r.group = c.model_id;
-    r.n = sh->second.n;
-    r.B = c.batch;
-    r.E = c.epochs;
-    r.nb = (int)ceil_div((uint64_t)r.n, (uint64_t)r.B);
-    r.S = (uint64_t)r.E * r.nb;
-    r.admit = a.admit;
-    r.release = a.release;
-    r.offset = a.offset;
-    if (a.gpu < 0 || a.gpu >= ctx->world) return fail(ctx, PROTEA_ERR_PLAN, who + ": gpu out of range");
-    if (a.release != a.admit + r.S)
-      return fail(ctx, PROTEA_ERR_PLAN, who + ": release - admit != S_k = " + std::to_string(r.S));
-    const uint64_t need = slot_layout(ctx->groups[c.model_id].m, r.B, r.n, r.E, e).total;
-    if (a.slot < need)
-      return fail(ctx, PROTEA_ERR_PLAN, who + ": slot " + std::to_string(a.slot) + " < HWM " + std::to_string(need));
-    if (a.gpu == ctx->rank && (a.offset % kAlign != 0 || a.offset + a.slot > ctx->arena_bytes))
-      return fail(ctx, PROTEA_ERR_OOM, who + ": slot [" + std::to_string(a.offset) + ", +" + std::to_string(a.slot) +
-                                           ") outside the arena of " + std::to_string(ctx->arena_bytes) + " B");
-    Ngroup[c.model_id] += r.n;
-    if (a.gpu == ctx->rank) all.push_back(r);
-  }
-  if (pa.size() != n) return fail(ctx, PROTEA_ERR_PLAN, "run_round: plan and client list differ");
-  // plan agreement across ranks: max over ranks of (h, ~h) equals (h, ~h) iff all agree
-  if (ctx->comm && ctx->world > 1) {
-    const uint64_t h = protea_plan_hash(clients, n, plan);
-    uint64_t hv[2] = {h, ~h};
-    CK(cudaSetDevice(ctx->device));
-    CK(ctx->acc.reserve(2));
-    CK(cudaMemcpyAsync(ctx->acc.p, hv, 16, cudaMemcpyHostToDevice, ctx->stream));
-    ncclResult_t r = ncclAllReduce(ctx->acc.p, ctx->acc.p, 2, ncclUint64, ncclMax, ctx->comm, ctx->stream);
-    if (r != ncclSuccess) return fail(ctx, PROTEA_ERR_NCCL, std::string("run_round: plan hash allreduce: ") + ncclGetErrorString(r));
-    CK(cudaMemcpyAsync(hv, ctx->acc.p, 16, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    if (hv[0] != h || hv[1] != ~h)
-      return fail(ctx, PROTEA_ERR_PLAN, "run_round: ranks disagree on the plan / client list (plan hash)");
-  }
-  // live slots pairwise disjoint on this GPU
-  {
-    std::vector<std::pair<uint64_t, int>> ev;  // (time*2 + kind, idx)
+  // ---- validate clients and plan (every check of this rank; with a communicator the verdict is agreed
+  // on by all ranks below before any of them starts device work, so one rank's failure cannot leave
+  // the others waiting in a collective)
+  auto validate = [&]() -> protea_status {
+    if (!opts || !clients || !plan || !global_in || !global_out || n == 0)
+      return fail(ctx, PROTEA_ERR_INVALID, "run_round: null argument or n == 0");
+    if ((int64_t)n_params != Ptot)
+      return fail(ctx, PROTEA_ERR_DIM, "run_round: n_params " + std::to_string(n_params) + " != registered total " +
+                                           std::to_string(Ptot));
+    std::map<int64_t, const protea_assignment*> pa;
+    for (size_t i = 0; i < n; ++i)
+      if (!pa.emplace(plan[i].client_id, &plan[i]).second)
+        return fail(ctx, PROTEA_ERR_PLAN, "run_round: plan lists client " + std::to_string(plan[i].client_id) + " twice");
+    std::map<int64_t, int> seen;
+    for (size_t i = 0; i < n; ++i) {
+      const protea_client& c = clients[i];
+      const std::string who = "run_round: client " + std::to_string(c.client_id);
+      if (!seen.emplace(c.client_id, 1).second) return fail(ctx, PROTEA_ERR_INVALID, who + " listed twice");
+      if (c.model_id < 0 || c.model_id >= (int)ctx->groups.size())
+        return fail(ctx, PROTEA_ERR_INVALID, who + ": unknown model_id");
+      if (c.batch <= 0 || c.batch > kMaxBatch || c.epochs <= 0)
+        return fail(ctx, PROTEA_ERR_INVALID, who + ": batch must be in [1, " + std::to_string(kMaxBatch) +
+                                                 "] and epochs > 0");
+      auto sh = ctx->shards.find(c.client_id);
+      if (sh == ctx->shards.end()) return fail(ctx, PROTEA_ERR_INVALID, who + ": no registered shard");
+      if (sh->second.ymin < 0 || sh->second.ymax >= ctx->groups[c.model_id].m.classes)
+        return fail(ctx, PROTEA_ERR_INVALID, who + ": label outside [0, " +
+                                                 std::to_string(ctx->groups[c.model_id].m.classes) + ")");
+      auto it = pa.find(c.client_id);
+      if (it == pa.end()) return fail(ctx, PROTEA_ERR_PLAN, who + " missing from the plan");
+      const protea_assignment& a = *it->second;
+      RunClient r;
+      r.id = c.client_id;
+      r.group = c.model_id;
+      r.n = sh->second.n;
+      r.B = c.batch;
+      r.E = c.epochs;
+      r.nb = (int)ceil_div((uint64_t)r.n, (uint64_t)r.B);
+      r.S = (uint64_t)r.E * r.nb;
+      r.admit = a.admit;
+      r.release = a.release;
+      r.offset = a.offset;
+      if (a.gpu < 0 || a.gpu >= ctx->world) return fail(ctx, PROTEA_ERR_PLAN, who + ": gpu out of range");
+      if (a.release != a.admit + r.S)
+        return fail(ctx, PROTEA_ERR_PLAN, who + ": release - admit != S_k = " + std::to_string(r.S));
+      const uint64_t need = slot_layout(ctx->groups[c.model_id].m, r.B, r.n, r.E, e).total;
+      if (a.slot < need)
+        return fail(ctx, PROTEA_ERR_PLAN, who + ": slot " + std::to_string(a.slot) + " < HWM " + std::to_string(need));
+      if (a.gpu == ctx->rank && (a.offset % kAlign != 0 || a.offset + a.slot > ctx->arena_bytes))
+        return fail(ctx, PROTEA_ERR_OOM, who + ": slot [" + std::to_string(a.offset) + ", +" + std::to_string(a.slot) +
+                                             ") outside the arena of " + std::to_string(ctx->arena_bytes) + " B");
+      Ngroup[c.model_id] += r.n;
+      if (a.gpu == ctx->rank) all.push_back(r);
+    }
+    if (pa.size() != n) return fail(ctx, PROTEA_ERR_PLAN, "run_round: plan and client list differ");
+    // live slots pairwise disjoint on this GPU
     std::vector<RunClient*> byoff;
     for (auto& c : all) byoff.push_back(&c);
     std::sort(byoff.begin(), byoff.end(), [](RunClient* a, RunClient* b) { return a->offset < b->offset; });
@@ -1631,6 +1638,30 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
           return fail(ctx, PROTEA_ERR_PLAN, "run_round: clients " + std::to_string(a->id) + " and " +
                                                 std::to_string(b->id) + " overlap in the arena while both live");
       }
+    return PROTEA_OK;
+  };
+  const protea_status vst = validate();
+  if (ctx->comm) {
+    // plan agreement + validation verdict: NCCL max over ranks of (h, ~h, failed) equals
+    // (h, ~h, 0) iff every rank validated and all ranks hold the same client list and plan
+    const uint64_t h = vst == PROTEA_OK ? protea_plan_hash(clients, n, plan) : 0;
+    const uint64_t flag = vst == PROTEA_OK ? 0 : 1;
+    const uint64_t hv0[3] = {h, ~h, flag};
+    uint64_t hv[3];
+    std::memcpy(hv, hv0, sizeof(hv));
+    CK(cudaSetDevice(ctx->device));
+    CK(ctx->flag.reserve(4));
+    CK(cudaMemcpyAsync(ctx->flag.p, hv, 24, cudaMemcpyHostToDevice, ctx->stream));
+    ncclResult_t r = ncclAllReduce(ctx->flag.p, ctx->flag.p, 3, ncclUint64, ncclMax, ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return fail(ctx, PROTEA_ERR_NCCL, std::string("run_round: plan hash allreduce: ") + ncclGetErrorString(r));
+    CK(cudaMemcpyAsync(hv, ctx->flag.p, 24, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (vst != PROTEA_OK) return vst;
+    if (hv[2]) return fail(ctx, PROTEA_ERR_PLAN, "run_round: another rank rejected the round (validation)");
+    if (hv[0] != hv0[0] || hv[1] != hv0[1])
+      return fail(ctx, PROTEA_ERR_PLAN, "run_round: ranks disagree on the plan / client list (plan hash)");
+  } else if (vst != PROTEA_OK) {
+    return vst;
   }
   std::sort(all.begin(), all.end(), [](const RunClient& a, const RunClient& b) { return a.id < b.id; });
   CK(cudaSetDevice(ctx->device));
@@ -1658,6 +1689,19 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
   double* loss_dev = ctx->acc.p + Ptot;  // per-group fp64 sums of step losses after the accumulators
   protea_status st =
       execute(ctx, all, wg, ctx->acc.p, opts->lr, opts->seed, opts->round, opts->shuffle, &iters, loss_dev);
+  if (ctx->comm && !opts->partial_only) {
+    // every rank reaches the exchange; one that failed inside execute() says so first (NCCL max of a flag)
+    const uint64_t f0 = st == PROTEA_OK ? 0 : 1;
+    uint64_t f = f0;
+    CK(ctx->flag.reserve(4));
+    CK(cudaMemcpyAsync(ctx->flag.p, &f, 8, cudaMemcpyHostToDevice, ctx->stream));
+    ncclResult_t r = ncclAllReduce(ctx->flag.p, ctx->flag.p, 1, ncclUint64, ncclMax, ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return fail(ctx, PROTEA_ERR_NCCL, std::string("run_round: error-flag allreduce: ") + ncclGetErrorString(r));
+    CK(cudaMemcpyAsync(&f, ctx->flag.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (st != PROTEA_OK) return st;
+    if (f) return fail(ctx, PROTEA_ERR_CUDA, "run_round: another rank failed during the round");
+  }
   if (st != PROTEA_OK) return st;
   ctx->last_Ngroup = Ngroup;
   ctx->have_partial = opts->partial_only != 0;
@@ -1675,11 +1719,20 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
     }
     return PROTEA_OK;
   }
-  if (ctx->world > 1) {
-    if (!ctx->comm)
-      return fail(ctx, PROTEA_ERR_INVALID, "run_round: world > 1 without an NCCL communicator needs partial_only = 1");
-    ncclResult_t r = ncclAllReduce(ctx->acc.p, ctx->acc.p, Ptot, ncclDouble, ncclSum, ctx->comm, ctx->stream);
-    if (r != ncclSuccess) return fail(ctx, PROTEA_ERR_NCCL, std::string("run_round: ncclAllReduce: ") + ncclGetErrorString(r));
+  if (ctx->world > 1 && !ctx->comm)
+    return fail(ctx, PROTEA_ERR_INVALID, "run_round: world > 1 without an NCCL communicator needs partial_only = 1");
+  // K7: the ranks' fp64 partials (and per-group loss sums) are all-gathered and every rank
+  // sums them in RANK ORDER inside the finalise kernel, so the result is bitwise defined for a given
+  // world size (an ncclAllReduce sum would leave the order to NCCL's algorithm choice)
+  const int64_t stride = Ptot + (int64_t)NG;
+  const double* parts = ctx->acc.p;
+  int nparts = 1;
+  if (ctx->comm) {
+    CK(ctx->gath.reserve((size_t)stride * ctx->world));
+    ncclResult_t r = ncclAllGather(ctx->acc.p, ctx->gath.p, stride, ncclDouble, ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return fail(ctx, PROTEA_ERR_NCCL, std::string("run_round: ncclAllGather: ") + ncclGetErrorString(r));
+    parts = ctx->gath.p;
+    nparts = ctx->world;
   }
   float* out = global_out;
   if (!out_dev) {
@@ -1689,22 +1742,23 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
   for (size_t g = 0; g < ctx->groups.size(); ++g) {
     const Group& gr = ctx->groups[g];
     if (Ngroup[g] > 0) {
-      ctx->op_bytes[PROTEA_OPC_FEDAVG] += 16 * (uint64_t)gr.m.P;
+      ctx->op_bytes[PROTEA_OPC_FEDAVG] += (8 * (uint64_t)nparts + 8) * (uint64_t)gr.m.P;
       const int ev = op_begin(ctx, PROTEA_OPC_FEDAVG);
-      k_finalize<<<grid_for(gr.m.P, 256), 256, 0, ctx->stream>>>(wg + gr.offset, ctx->acc.p + gr.offset,
-                                                                 (double)Ngroup[g], out + gr.offset, gr.m.P);
+      k_finalize_ordered<<<grid_for(gr.m.P, 256), 256, 0, ctx->stream>>>(
+          wg + gr.offset, parts + gr.offset, stride, nparts, (double)Ngroup[g], out + gr.offset, gr.m.P);
       op_end(ctx, ev);
     } else if (out + gr.offset != wg + gr.offset) {
       CK(cudaMemcpyAsync(out + gr.offset, wg + gr.offset, gr.m.P * 4, cudaMemcpyDeviceToDevice, ctx->stream));
     }
   }
   if (!out_dev) CK(cudaMemcpyAsync(global_out, out, Ptot * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  std::vector<double> loss_g(NG, 0.0);
-  CK(cudaMemcpyAsync(loss_g.data(), loss_dev, NG * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<double> loss_g((size_t)nparts * NG, 0.0);
+  CK(cudaMemcpy2DAsync(loss_g.data(), NG * 8, parts + Ptot, (size_t)stride * 8, NG * 8, nparts,
+                       cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   double loss_sum = 0.0;
-  for (double v : loss_g) loss_sum += v;  // group order
+  for (double v : loss_g) loss_sum += v;  // rank order, group order
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   if (stats) {
@@ -1770,7 +1824,11 @@ protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clien
       return fail(ctx, PROTEA_ERR_INVALID, who + ": unknown model_id");
     if (c.batch <= 0 || c.batch > kMaxBatch || c.epochs <= 0)
       return fail(ctx, PROTEA_ERR_INVALID, who + ": batch must be in [1, 64] and epochs > 0");
-    if (!ctx->shards.count(c.client_id)) return fail(ctx, PROTEA_ERR_INVALID, who + ": no registered shard");
+    auto sh = ctx->shards.find(c.client_id);
+    if (sh == ctx->shards.end()) return fail(ctx, PROTEA_ERR_INVALID, who + ": no registered shard");
+    if (sh->second.ymin < 0 || sh->second.ymax >= ctx->groups[c.model_id].m.classes)
+      return fail(ctx, PROTEA_ERR_INVALID, who + ": label outside [0, " +
+                                               std::to_string(ctx->groups[c.model_id].m.classes) + ")");
   }
   CK(cudaSetDevice(ctx->device));
   for (size_t i = 0; i < n; ++i) {
@@ -1842,26 +1900,26 @@ protea_status protea_round_partial(protea_ctx* ctx, double* dst, size_t n_params
   return PROTEA_OK;
 }
 
-protea_status protea_round_finalize(protea_ctx* ctx, const double* acc_sum, const float* global_in, float* global_out,
-                                    size_t n_params) {
+protea_status protea_round_finalize_ordered(protea_ctx* ctx, const double* partials, int32_t nparts,
+                                            const float* global_in, float* global_out, size_t n_params) {
   if (!ctx) return PROTEA_ERR_INVALID;
-  if (!acc_sum || !global_in || !global_out || ctx->last_Ngroup.size() != ctx->groups.size())
-    return fail(ctx, PROTEA_ERR_INVALID, "round_finalize: null argument or no round recorded");
+  if (!partials || !global_in || !global_out || nparts < 1 || ctx->last_Ngroup.size() != ctx->groups.size())
+    return fail(ctx, PROTEA_ERR_INVALID, "round_finalize: null argument, nparts < 1 or no round recorded");
   int64_t Ptot = 0;
   for (auto& g : ctx->groups) Ptot += g.m.P;
   if ((int64_t)n_params != Ptot) return fail(ctx, PROTEA_ERR_DIM, "round_finalize: n_params mismatch");
   CK(cudaSetDevice(ctx->device));
   CK(ctx->gin.reserve(Ptot));
   CK(ctx->gout.reserve(Ptot));
-  CK(ctx->acc.reserve(Ptot + 1));
+  CK(ctx->gath.reserve((size_t)Ptot * nparts));
   CK(cudaMemcpyAsync(ctx->gin.p, global_in, Ptot * 4, cudaMemcpyDefault, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->acc.p, acc_sum, Ptot * 8, cudaMemcpyDefault, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->gath.p, partials, (size_t)Ptot * nparts * 8, cudaMemcpyDefault, ctx->stream));
   for (size_t g = 0; g < ctx->groups.size(); ++g) {
     const Group& gr = ctx->groups[g];
     if (ctx->last_Ngroup[g] > 0)
-      k_finalize<<<grid_for(gr.m.P, 256), 256, 0, ctx->stream>>>(ctx->gin.p + gr.offset, ctx->acc.p + gr.offset,
-                                                                 (double)ctx->last_Ngroup[g], ctx->gout.p + gr.offset,
-                                                                 gr.m.P);
+      k_finalize_ordered<<<grid_for(gr.m.P, 256), 256, 0, ctx->stream>>>(
+          ctx->gin.p + gr.offset, ctx->gath.p + gr.offset, Ptot, nparts, (double)ctx->last_Ngroup[g],
+          ctx->gout.p + gr.offset, gr.m.P);
     else
       CK(cudaMemcpyAsync(ctx->gout.p + gr.offset, ctx->gin.p + gr.offset, gr.m.P * 4, cudaMemcpyDeviceToDevice,
                          ctx->stream));
@@ -1871,6 +1929,11 @@ protea_status protea_round_finalize(protea_ctx* ctx, const double* acc_sum, cons
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->have_partial = false;
   return PROTEA_OK;
+}
+
+protea_status protea_round_finalize(protea_ctx* ctx, const double* acc_sum, const float* global_in, float* global_out,
+                                    size_t n_params) {
+  return protea_round_finalize_ordered(ctx, acc_sum, 1, global_in, global_out, n_params);
 }
 
 protea_status protea_evaluate(protea_ctx* ctx, int32_t model_id, const float* weights, const uint8_t* x,

@@ -117,6 +117,18 @@ __global__ void k_finalize(const float* __restrict__ wg, const double* __restric
     out[d] = (float)((double)wg[d] + acc[d] / N);
 }
 
+// K7, deterministic cross-rank finalise: parts = the ranks' fp64 partials, rank r's at
+// parts + r * stride; acc = ((p_0 + p_1) + p_2) + ... in rank order, then w' = w_g + acc / N (R20).
+// With one part this is bitwise k_finalize (0 is not added first).
+__global__ void k_finalize_ordered(const float* __restrict__ wg, const double* __restrict__ parts, int64_t stride,
+                                   int nparts, double N, float* __restrict__ out, int64_t P) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < P; d += (int64_t)gridDim.x * blockDim.x) {
+    double a = parts[d];
+    for (int r = 1; r < nparts; ++r) a += parts[(int64_t)r * stride + d];
+    out[d] = (float)((double)wg[d] + a / N);
+  }
+}
+
 // protea_fedavg: out[d] = sum_k n_k p_k[d] / N, fp64 accumulation in order k.
 __global__ void k_fedavg(const float* const* __restrict__ ptrs, const double* __restrict__ w, int n, double N,
                          float* __restrict__ out, int64_t dim) {
