@@ -8,10 +8,17 @@ A5 FedAvg (+ the NCCL sum when N > 1).  The N=1 workload is BASELINE.json
 configs[1] ("config2"): 100 clients, CNN-1x on CIFAR-shaped synthetic data,
 500 samples each, B in {8,16,32,64} (id mod 4), 2 local epochs -> 5,950
 client-steps per round.  For N > 1 every GPU gets another 100 such clients
-(weak scaling, LPT partition by FLOPs, one fp64 NCCL allreduce per round).
+(weak scaling, LPT partition by FLOPs, one NCCL all-gather of the fp64 FedAvg
+partials + a rank-ordered sum per round).
 
-Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-        (N > 1 under torchrun; rank 0 prints one JSON line)
+--config 3|5 --scaling strong runs the north-star target instead: ONE round of
+the config's cohort (config 3: K = 100 of a 1000-client Dirichlet(0.5) pool,
+CNN-1x; config 5: K = 500 of a 10,000-client Dirichlet pool, ResNet-8) split
+over the N GPUs by the profile-driven LPT packing (strong scaling: total work
+fixed).  --config 2 --scaling strong splits config 2's 100 clients.
+
+Launch: python bench.py [--gpus N --steps K --warmup W] [--config 2|3|5] [--scaling weak|strong]
+        [--impl reference]   (N > 1 under torchrun; rank 0 prints one JSON line)
 """
 from __future__ import annotations
 
@@ -52,9 +59,21 @@ def fp32_alu_peak_tflops(mhz):
     return 148 * 128 * 2 * mhz * 1e6 / 1e12
 
 
-def workload(world, seed=2):
-    wl = synth.build_workload(2, n_clients=CLIENTS_PER_GPU * world, shards=False, seed=seed)
-    return wl
+def workload(world, config=2, scaling="weak"):
+    if config == 2:
+        return synth.build_workload(2, n_clients=CLIENTS_PER_GPU * (world if scaling == "weak" else 1), shards=False)
+    if config == 3:
+        return synth.build_workload(3, k=100 * (world if scaling == "weak" else 1), shards=False)
+    if config == 5:
+        return synth.build_workload(5, k=500 * (world if scaling == "weak" else 1), shards=False)
+    raise ValueError(f"bench: config {config} not supported (2, 3, 5)")
+
+
+ALGO_NOTE = {"fc1_wgrad": "SURVEY §8(d): 8 B per fc1 weight per client-step (fp32 master read + write) + dh / a2 reads",
+             "resnet_fwd": "2 x useful MACs of the 3x3 convs of the launch's rows (implicit GEMM)",
+             "resnet_dgrad": "2 x useful MACs of the 3x3 input-gradient convs", "resnet_wgrad": "2 x useful MACs "
+             "of the 3x3 weight-gradient GEMMs"}
+ARCH_NAME = {synth.MODEL_CNN: "CNN-1x (P=2,156,490)", synth.MODEL_RESNET8: "ResNet-8 (P=75,050)"}
 
 
 # ---------------------------------------------------------------------------
@@ -159,8 +178,8 @@ def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    wl = workload(1)
-    frac = 0.02
+    wl = workload(1, args.config, args.scaling)
+    frac = 0.02 if args.config == 2 else 0.01
     oracle_sample(wl, frac=0.005)  # warm the pool / imports (not timed)
     for _ in range(max(0, args.warmup - 1)):
         oracle_sample(wl, frac=0.005)
@@ -172,26 +191,36 @@ def reference_arm(args):
         steps += s
         wall += w
     value = steps / wall
-    sample = (f"first ceil({frac}*S_k) local steps of each of the 100 config2 clients per bench step "
-              f"({steps // args.steps} client-steps/step), float64 numpy oracle, {cores} processes")
+    sample = (f"first ceil({frac}*S_k) local steps of each of the {len(wl.clients)} config{args.config} clients per "
+              f"bench step ({steps // args.steps} client-steps/step), float64 numpy oracle, {cores} processes")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(1, "f64"),
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_block(wl, 1, "f64", args.config, args.scaling),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_block(world, dtype):
-    return {"workload": "config2 (BASELINE.json configs[1]): 100 clients/GPU, CNN-1x (P=2,156,490) on synthetic "
-                        "CIFAR-shaped u8 data, 500 samples/client, B=(8,16,32,64)[id%4], E=2, lr=0.05",
-            "clients_per_gpu": CLIENTS_PER_GPU, "clients_total": CLIENTS_PER_GPU * world,
-            "client_steps_per_round": 5950 * world, "max_local_steps": 126, "precision": dtype,
-            "l2": "no flush: per-GPU resident inputs (153.6 MB u8 shards + 862 MB client weights) exceed the 126 MB L2",
-            "parallelism": f"clients partitioned over {world} GPU(s) by LPT on FLOPs; NCCL fp64 FedAvg allreduce"
-                           if world > 1 else "1 GPU, all clients co-resident (lock-step grouped kernels)"}
+def config_block(wl, world, dtype, config=2, scaling="weak"):
+    steps = [c.epochs * -(-c.n // c.batch) for c in wl.clients]  # S_k = E ceil(n_k / B_k)
+    what = {2: "config2 (BASELINE.json configs[1]): CNN-1x (P=2,156,490) on synthetic CIFAR-shaped u8 data, "
+               "500 samples/client, B=(8,16,32,64)[id%4], E=2, lr=0.05",
+            3: "config3 (BASELINE.json configs[2]): K=100 of a 1000-client Dirichlet(0.5) pool (50,000 samples), "
+               "CNN-1x, B=(8,16,32,64)[id%4], E=2, lr=0.05",
+            5: "config5 (BASELINE.json configs[4]): K=500 of a 10,000-client Dirichlet(0.5) pool (500,000 samples), "
+               "ResNet-8 (P=75,050), B=(8,16,32,64)[id%4], E=2, lr=0.05"}[config]
+    per = f"{len(wl.clients) // world} clients/GPU" if scaling == "weak" else f"{len(wl.clients)} clients over {world} GPU(s)"
+    return {"workload": f"{what}; {per}",
+            "clients_total": len(wl.clients), "client_steps_per_round": int(sum(steps)),
+            "max_local_steps": int(max(steps)), "precision": dtype,
+            "l2": "no flush: per-GPU resident inputs (u8 shards + per-client fp32 weights and activations) exceed "
+                  "the 126 MB L2" if config != 5 else "no flush: per-GPU resident shards (1.5 MB..) + client "
+                  "slots (500 x 3-19 MB) exceed the 126 MB L2",
+            "parallelism": f"clients partitioned over {world} GPU(s) by LPT on FLOPs; NCCL all-gather of the fp64 "
+                           "FedAvg partials + rank-ordered sum" if world > 1
+                           else "1 GPU, all clients co-resident (lock-step grouped kernels)"}
 
 
 # ---------------------------------------------------------------------------
@@ -206,6 +235,10 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--observe-hwm", type=int, default=1,
+                    help="timed rounds observe each client's arena high-water mark (A3 profile -> next plan)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -227,11 +260,12 @@ def main():
     dtype = "f32" if prec == pb.PREC_FP32 else "bf16"
     eb = 4 if prec == pb.PREC_FP32 else 2
 
-    wl = workload(world)
+    wl = workload(world, args.config, args.scaling)
+    arch = wl.model
     # A4 inputs on every rank from the pure host footprint (identical on all ranks)
     foot = np.zeros(len(wl.clients), dtype=pb.PROFILE_DT)
     for i, c in enumerate(wl.clients):
-        pk, st, fl = pb.protea_client_footprint(pb.MODEL_CNN, 4, 10, 32, 32, 3, c.n, c.batch, c.epochs, prec)
+        pk, st, fl = pb.protea_client_footprint(arch, 4, 10, 32, 32, 3, c.n, c.batch, c.epochs, prec)
         foot[i] = (c.id, pk, st, fl, 0, 0, 0, 1, 0)
     arena_bytes = int(sum(int(f["peak_bytes"]) for f in foot) // world * 1.25) + (256 << 20)
     caps = [arena_bytes] * world
@@ -244,7 +278,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     sim = Simulation(device=local, precision=prec, arena_bytes=arena_bytes, rank=rank, world=world, nccl_id=nccl_id)
-    mid = sim.register_model(pb.MODEL_CNN, 4, 10, 32, 32, 3)
+    mid = sim.register_model(arch, 4, 10, 32, 32, 3)
     tmpl = synth.class_templates(wl.shape, wl.classes, wl.seed)
     # every rank holds every sampled client's shard (HBM is ample; run_round takes n_k of all
     # clients from the registry for the FedAvg denominator); the e2e timing re-sends only this rank's shards
@@ -305,7 +339,8 @@ def main():
         ev[k][0].record(stream)
         plan, _ = pb.protea_plan(profiles, caps)                     # A4
         _, (st, meas) = sim.run_round(all_clients, plan, g, g2, lr=wl.lr, seed=wl.seed, rnd=rnd,
-                                      measured=True, time_ops=1 << dominant)  # A2 + A3 + A5
+                                      measured=True, time_ops=1 << dominant,
+                                      observe_hwm=bool(args.observe_hwm))  # A2 + A3 + A5
         ev[k][1].record(stream)
         g, g2 = g2, g
         rnd += 1
@@ -316,7 +351,8 @@ def main():
         dom_fl += st["op_timed_flops"][dominant]
         dom_by += st["op_timed_bytes"][dominant]
         dom_n += st["op_timed_launches"][dominant]
-        profiles = meas  # A3 -> next A4: the latest in-run profile replaces the previous one (reading R7)
+        if world == 1:  # A3 -> next A4: the latest in-run profile replaces the previous one (reading R7)
+            profiles = meas  # (N > 1: each rank observes only its own clients; the plan keeps the footprints)
     barrier()
     host_s = time.perf_counter() - host_t0
     clk = clocks.stop() if clocks else None
@@ -345,7 +381,7 @@ def main():
     ridge = alu_peak * 1e12 / (pk["hbm"] * 1e9)
     # which op classes run on tcgen05 in bf16 mode (the rest are SIMT fp32 math)
     tc_ops = {"conv1_fwd", "conv2_fwd", "fc1_fwd", "fc1_dgrad", "fc1_wgrad", "conv2_dgrad", "conv2_wgrad",
-              "conv1_wgrad"} if prec == pb.PREC_BF16 else set()
+              "conv1_wgrad", "resnet_fwd", "resnet_dgrad", "resnet_wgrad"} if prec == pb.PREC_BF16 else set()
     on_tc = pb.OPC_NAMES[dominant] in tc_ops and pb.TC_OPS_BUILT.get(pb.OPC_NAMES[dominant], False)
     if fl_per / max(by_per, 1) >= ridge:
         bound, achieved, peak, unit = ("tensor", fl_per / avg_ns / 1e3, pk["bf16_sus"], "TFLOP/s") if on_tc \
@@ -377,8 +413,8 @@ def main():
                 "achieved_with_shadow": (by_per + shadow) / avg_ns,
                 "frac_with_shadow": (by_per + shadow) / avg_ns / pk["hbm"]}
     roof = {"kernel": pb.OPC_NAMES[dominant], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak, "traffic": traffic, "algorithmic": "SURVEY §8(d): 8 B per fc1 weight per "
-            "client-step (fp32 master read + write) + dh / a2 reads", "implementation_extra": impl,
+            "frac": achieved / peak, "traffic": traffic, "algorithmic": ALGO_NOTE.get(pb.OPC_NAMES[dominant], "engine op_work: "
+            "operands read once, results written once"), "implementation_extra": impl,
             "peak_src": pk["src"] if bound != "alu" else f"derived: 148 SM x 128 FP32 lanes x 2 x {pk['sm_max_mhz']:.0f} MHz",
             "per_launch": {"flops": fl_per, "bytes": by_per, "avg_ns": avg_ns, "launches": dom_n, "source": timing_src},
             "share_of_step": dom_ns / (dev_ms * 1e6 / 1.0) if world == 1 else None,
@@ -411,15 +447,17 @@ def main():
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        s, w, cores = oracle_sample(workload(1), frac=0.05)
+        frac = 0.05 if args.config == 2 else 0.02
+        s, w, cores = oracle_sample(wl, frac=frac)
         cpu = {"value": s / w, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"first ceil(0.05*S_k) local steps of each of the 100 config2 clients ({s} client-steps, "
-                         f"{w:.1f} s wall), float64 numpy oracle, one client per process"}
+               "sample": f"first ceil({frac}*S_k) local steps of each of the {len(wl.clients)} config{args.config} "
+                         f"clients ({s} client-steps, {w:.1f} s wall), float64 numpy oracle, one client per process"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": dtype, "data": "synthetic", "config": config_block(world, dtype),
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": args.scaling, "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+                "config": config_block(wl, world, dtype, args.config, args.scaling),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk,
                 "detail": {"round_tflops": sum(int(f["flops"]) for f in foot) / (ms_per_step / 1e3) / 1e12,

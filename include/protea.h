@@ -104,7 +104,9 @@ typedef struct {
 /* get_properties() record; integer SI units. */
 typedef struct {
   int64_t client_id;
-  uint64_t peak_bytes;  /* exact arena high-water mark of the client's slot (Table 1 VRAM) */
+  uint64_t peak_bytes;  /* arena high-water mark of the client's slot (Table 1 VRAM): protea_profile_clients and
+                           observe_hwm rounds report the OBSERVED mark (poisoned slot, highest touched byte,
+                           aligned to 256 B); otherwise the slot layout's bound */
   uint64_t steps;       /* S_k = E * ceil(n_k / B_k) */
   uint64_t flops;       /* E * n_k * f(model, width) */
   uint64_t step_ns;     /* device time of one local step: probe (CUDA events) in protea_profile_clients;
@@ -148,6 +150,7 @@ enum {
   PROTEA_OPC_CONV1_WGRAD, PROTEA_OPC_CONV1_REDUCE, PROTEA_OPC_MLP_FC1_FWD, PROTEA_OPC_MLP_HEAD,
   PROTEA_OPC_MLP_FC1_WGRAD, PROTEA_OPC_ADMIT, PROTEA_OPC_FEDAVG, PROTEA_OPC_STAGE_X,
   PROTEA_OPC_R_FWD, PROTEA_OPC_R_HEAD, PROTEA_OPC_R_DGRAD, PROTEA_OPC_R_WGRAD, PROTEA_OPC_R_REDUCE, /* ResNet-8 */
+  PROTEA_OPC_EVAL_HEAD, /* evaluate round: classifier head after the forward kernels */
   PROTEA_N_OPC = 32 /* room for further op classes */
 };
 
@@ -163,7 +166,19 @@ typedef struct {
   uint32_t serialize;    /* 1: every launch on the lock-step stream (no fc1-wgrad deferral to the side
                             stream), so per-op CUDA-event times are the kernels' own, as in a serialised
                             ncu launch list; 0: default overlap */
+  uint32_t observe_hwm;  /* 1: OBSERVE each client's arena high-water mark (Table 1 VRAM): its slot
+                            is filled with the poison byte PROTEA_POISON at admission and scanned at release;
+                            measured[k].peak_bytes = align256(1 + offset of the highest byte of the slot that
+                            differs from the poison).  0: measured[k].peak_bytes = the slot layout's bound */
+  uint32_t n_trace;      /* verification: number of traced clients (0 = none) */
+  const int64_t* trace_ids;   /* host, n_trace client ids (this rank's) */
+  void* const* trace_bufs;    /* host array of n_trace DEVICE pointers, each (S_k + 1) * H_k bytes with H_k =
+                                 protea_client_footprint's peak_bytes (the slot layout): snapshot s
+                                 = the client's whole slot after s local steps (s = 0: at admission) — fp32
+                                 weights first, then the step's stored activations / decisions (pool argmaxes) */
 } protea_round_opts;
+
+#define PROTEA_POISON 0xA5 /* byte value of an untouched slot byte under observe_hwm */
 
 typedef struct {
   uint64_t round_ns;        /* device time of the whole round on this rank (CUDA events) */
@@ -203,10 +218,13 @@ protea_status protea_register_model(protea_ctx* ctx, const protea_model_desc* de
  * Errors: INVALID (null, n_k <= 0, label out of range is not checked), CUDA. */
 protea_status protea_register_shards(protea_ctx* ctx, const protea_shard* shards, size_t n);
 
-/* Profile n clients (shards must be registered): exact peak bytes, S_k, FLOPs,
- * and the device time of one probe step per shape class (model, batch) run in
- * the arena (which must not be in use).  out: caller-allocated, n records.
- * Errors: INVALID, OOM (arena smaller than a probe slot), CUDA. */
+/* Profile n clients (shards must be registered): peak bytes, S_k, FLOPs, and the device time of one probe
+ * step per shape class (model, batch) run in the arena (which must not be in use).  peak_bytes is OBSERVED:
+ * every client runs one local step (its epoch permutations for all E epochs, one batch) in a poisoned slot
+ * of the layout's size followed by a 4 KiB poisoned guard; the highest touched byte of the slot, aligned to
+ * 256 B, is the client's high-water mark, and a touched guard byte (a slot overrun) is an error.
+ * out: caller-allocated, n records.
+ * Errors: INVALID, OOM (arena smaller than a probe slot, or a guard byte touched), CUDA. */
 protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clients, size_t n,
                                      protea_profile* out);
 
@@ -233,6 +251,25 @@ typedef struct {
  * ResNet model, n <= 0, null pointer, label outside [0, classes)), CUDA. */
 protea_status protea_evaluate(protea_ctx* ctx, int32_t model_id, const float* weights, const uint8_t* x,
                               const int32_t* y, int64_t n, protea_eval_result* out);
+
+/* Register clients' VALIDATION splits (§4.1: each client's data is split into training and
+ * validation sets), same record and ownership as protea_register_shards, kept apart from the training
+ * shards (re-registering an id replaces it).  Errors: INVALID (null, n_k <= 0, no model registered), CUDA. */
+protea_status protea_register_val_shards(protea_ctx* ctx, const protea_shard* shards, size_t n);
+
+/* Evaluate round (the server's configure_evaluate / aggregate_evaluate after aggregation; P:302 the
+ * validation split): every listed client evaluates its group's global weights (n_params floats, all
+ * groups concatenated, host or device) on its registered validation split.  The forward pass is the
+ * training path's (bf16 mode: the tcgen05 kernels of every model; fp32 mode: the SIMT verify kernels), in
+ * lock-step over all clients (batches above 64 rows as micro-clients), followed by a classifier head
+ * (fp32 logits, logsumexp - z[y], first-maximum argmax).  per_client (caller-allocated, n records, in the
+ * given order): loss_sum (sum of the per-sample cross-entropies), correct, n; total (nullable): their sums
+ * (aggregate_evaluate: loss_sum / n is the example-weighted mean loss, correct / n the accuracy).  The
+ * arena is used as scratch (must not be in use).  Errors: INVALID (null, unknown model, duplicate id, no
+ * validation split, label outside [0, classes)), DIM, OOM (a client's evaluation slot exceeds the arena),
+ * CUDA. */
+protea_status protea_evaluate_round(protea_ctx* ctx, const protea_client* clients, size_t n, const float* global,
+                                    size_t n_params, protea_eval_result* per_client, protea_eval_result* total);
 
 /* 64-bit FNV-1a hash of a round's client list and plan (every field of both arrays, in the given
  * order).  Pure host function.  protea_run_round with world > 1 compares it across ranks before

@@ -8,7 +8,9 @@ For a model w and samples (x, y):
     loss_sum = sum_i [ logsumexp(z_i) - z_i[y_i] ]      (z_i = the model's logits)
     correct  = #{ i : argmax_c z_i[c] == y_i }           (first maximum on ties)
 
-The forward pass is the one of oracle/sgd.py (readings R10/R11).
+The forward pass is the one of oracle/sgd.py (readings R10/R11); evaluate_round applies it
+per client to its validation split (the aggregate is the sum over clients: the example-weighted mean
+loss and the accuracy follow by dividing by the total n).
 """
 import numpy as np
 
@@ -30,7 +32,21 @@ def logits(w, model, width_q, classes, x_u8):
         a2, _ = sgd.pool2_fwd(sgd.relu(z2))
         h = sgd.relu(a2.reshape(nb, -1) @ p["fc1.W"].T + p["fc1.b"])
         return h @ p["fc2.W"].T + p["fc2.b"]
-    raise ValueError("evaluate: MLP and CNN models only")
+    if model == sgd.RESNET8:  # conv0, three basic blocks (option-A shortcut), global average pool, fc
+        z0, _ = sgd.conv_fwd(xb, p["conv0.W"], p["conv0.b"], 1, 1)
+        a = sgd.relu(z0)
+        for blk, stride in (("b1", 1), ("b2", 2), ("b3", 2)):
+            za, _ = sgd.conv_fwd(a, p[blk + "a.W"], p[blk + "a.b"], stride, 1)
+            zb, _ = sgd.conv_fwd(sgd.relu(za), p[blk + "b.W"], p[blk + "b.b"], 1, 1)
+            if stride == 1:
+                sc = a
+            else:
+                sub = a[:, ::2, ::2, :]
+                sc = np.zeros(sub.shape[:3] + (zb.shape[3],))
+                sc[..., :sub.shape[3]] = sub
+            a = sgd.relu(zb + sc)
+        return a.mean(axis=(1, 2)) @ p["fc.W"].T + p["fc.b"]
+    raise ValueError(model)
 
 
 def evaluate(w, model, width_q, classes, x_u8, y):
@@ -42,3 +58,17 @@ def evaluate(w, model, width_q, classes, x_u8, y):
     loss_sum = float(np.sum(lse - z[np.arange(len(y)), y]))
     correct = int(np.sum(np.argmax(z, axis=1) == y))  # numpy argmax = first maximum
     return loss_sum, correct, len(y)
+
+
+def evaluate_round(clients, val_shards, global_w):
+    """PAPER.md P:238 (configure_evaluate / aggregate_evaluate) with P:302's validation split: every client
+    evaluates its shape group's global weights on its own validation data.  clients: objects with id,
+    model, width_q, classes; val_shards: id -> (x u8 [n, D], y); global_w: width_q -> weights.
+    Returns ({id: (loss_sum, correct, n)}, (sum loss_sum, sum correct, sum n))."""
+    per = {}
+    for c in clients:
+        x, y = val_shards[c.id]
+        H, W, C = sgd.input_shape(c.model)
+        per[c.id] = evaluate(global_w[c.width_q], c.model, c.width_q, c.classes, x.reshape(-1, H, W, C), y)
+    tot = (sum(v[0] for v in per.values()), sum(v[1] for v in per.values()), sum(v[2] for v in per.values()))
+    return per, tot

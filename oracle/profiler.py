@@ -85,13 +85,14 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
 
     elem_bytes = 4 in fp32-verify mode, 2 in bf16 mode (activation storage; in
     bf16 mode the slot also holds a bf16 shadow copy of the weights).
+    b = min(batch, n): a batch holds at most that many rows,
+    and per-row buffers are sized for it.
     wsp = split-K partials of the conv weight gradients: each conv layer's
     reduction over b*Hout*Wout pixels is cut into ceil(b*Hout*Wout / 2048)
-    splits, each holding cout*(K+1) fp32 partials (the +1 is the bias column), rows
-    padded to a multiple of 4 floats (16-byte aligned rows, reading R21); the CNN
-    reuses one region (max over layers), ResNet-8 keeps one per layer (sum).
+    splits, each holding cout rows of K+1 fp32 partials (the +1 is the bias
+    column); see the branches below for which layers keep partials where.
     """
-    b, e = batch, elem_bytes
+    b, e = min(batch, n), elem_bytes  # a batch holds min(B, n) rows (SURVEY §8(c).2 step 3)
     P = n_params(model, width_q, classes)
     out = [("params", 4 * P), ("perm", 4 * epochs * n), ("stats", 64)]
     if e == 2:
@@ -112,7 +113,7 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
                 ("r1", b * 1024 * 16 * e), ("o1", b * 1024 * 16 * e),
                 ("r2", b * 256 * 32 * e), ("o2", b * 256 * 32 * e),
                 ("r3", b * 64 * 64 * e), ("o3", b * 64 * 64 * e),
-                ("gap", b * 64 * e), ("dgap", b * 64 * 4),
+                ("dgap", b * 64 * 4),
                 ("g0", b * 1024 * 16 * e), ("g1", b * 1024 * 16 * e), ("g2", b * 1024 * 16 * e)]
         if e == 2:  # bf16 mode: conv0 weight shadow padded to 8 input channels [16][9][8] (tensor cores)
             out.append(("w0p", 16 * 9 * 8 * 2))
@@ -120,16 +121,38 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
     else:
         raise ValueError(model)
     convs = conv_layers(model, width_q)
-    if convs:
-        per_layer = [4 * math.ceil(b * hw / WGRAD_CHUNK_PX) * co * (-(-(K + 1) // 4) * 4) for hw, co, K in convs]
-        # CNN: one region reused layer by layer (max); ResNet-8: a region per layer, all seven kept until
-        # the step's single merged SGD reduce (sum)
-        out.append(("wsp", sum(per_layer) if model == RESNET8 else max(per_layer)))
+    splits = [math.ceil(b * hw / WGRAD_CHUNK_PX) for hw, _, _ in convs]
+    ceil4 = lambda k: -(-k // 4) * 4  # noqa: E731
+    if model == RESNET8:
+        # a region per layer, all seven kept until the step's single merged SGD reduce; regions placed at
+        # row pitch ceil4(K+1), the last layer's rows written at pitch K+1 (its last row ends the slot)
+        wsp = sum(s * co * ceil4(K + 1) for s, (_, co, K) in zip(splits[:-1], convs[:-1]))
+        wsp += splits[-1] * convs[-1][1] * (convs[-1][2] + 1)
+        out.append(("wsp", 4 * wsp))
+    elif model == CNN and e == 2 and width_q == 4:
+        # width 1, bf16: conv1's partials reuse dz2; conv2's partials (pitch ceil4(K+1)) exist only when
+        # a client's rows need more than one split
+        _, co, K = convs[1]
+        if splits[1] > 1:
+            out.append(("wsp", 4 * splits[1] * co * ceil4(K + 1)))
+    elif convs:
+        # one region reused layer by layer (max), rows at pitch K+1
+        out.append(("wsp", max(4 * s * co * (K + 1) for s, (_, co, K) in zip(splits, convs))))
     return out
 
 
+MICRO_ROWS = 64  # a batch of more rows runs as micro-clients of <= 64 rows (DESIGN.md §5 "batches > 64")
+
+
 def hwm_bytes(model, width_q, classes, batch, n, epochs, elem_bytes) -> int:
-    return sum(align256(sz) for _, sz in slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes))
+    """Sum of align256(buffer) over the slot; a batch of b = min(B, n) > 64 rows holds ceil(b / 64) slots of
+    min(64, rest) rows back to back plus the fp32 merge weights (4P bytes)."""
+    b = min(batch, n)
+    if b <= MICRO_ROWS:
+        return sum(align256(sz) for _, sz in slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes))
+    tot = sum(hwm_bytes(model, width_q, classes, min(MICRO_ROWS, b - r0), n, epochs, elem_bytes)
+              for r0 in range(0, b, MICRO_ROWS))
+    return tot + align256(4 * n_params(model, width_q, classes))
 
 
 def eq1_q1024(slot_bytes: int, total_capacity: int) -> int:

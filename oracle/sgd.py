@@ -169,6 +169,50 @@ def pool2_bwd(dp, arg, shape):
     return dr
 
 
+# ---------------------------------------------------------------------------
+# forced decisions (teacher-forced parity; tests/teacher_forced.py)
+# ---------------------------------------------------------------------------
+# A ReLU mask or a 2x2 max-pool argmax is a discrete decision taken from floating-point values.  Where
+# the candidates lie within rounding of each other both choices are correct results of the method, and
+# the one the GPU took depends on its summation order ("Full-size parity").  With
+# `decisions` the oracle takes the GPU's choice, but only after checking that it is VALID: the forced
+# choice must be within `tol` x (the layer's max |value|) of the oracle's own.  Anything else raises.
+class ForcedDecisionError(AssertionError):
+    pass
+
+
+def _tol_check(name, bad, slack, scale, tol):
+    if np.any(bad & (slack > tol * scale)):
+        worst = float(np.max(np.where(bad, slack, 0.0)) / scale)
+        raise ForcedDecisionError(f"{name}: GPU decision off by {worst:.3e} of the layer scale (tol {tol:.1e})")
+
+
+def forced_relu_mask(name, z, gpu_pos, tol, rep):
+    """mask = gpu_pos (the GPU's stored activation > 0), valid where it differs from z > 0 only if |z| is
+    within tol of zero."""
+    own = z > 0
+    diff = own != gpu_pos
+    _tol_check(name, diff, np.abs(z), max(float(np.max(np.abs(z))), 1e-300), tol)
+    rep[name] = rep.get(name, 0) + int(diff.sum())
+    return gpu_pos
+
+
+def forced_pool(name, z, gpu_arg, gpu_pos, tol, rep):
+    """2x2/2 max pool of relu(z) with the GPU's argmax where its pooled value is positive: the forced
+    element must be within tol of the window max, and the ReLU decision of the pooled value (the GPU's
+    pooled value > 0) within tol of zero.  Returns (pooled value, argmax, mask = pooled > 0)."""
+    best, arg = pool2_fwd(relu(z))
+    win = np.stack([z[:, dy::2, dx::2, :] for dy in (0, 1) for dx in (0, 1)])  # pre-activation windows
+    ga = np.where(gpu_pos, gpu_arg, arg)
+    pre = np.take_along_axis(win, ga[None], axis=0)[0]
+    diff = ga != arg
+    _tol_check(name + ".argmax", diff, best - relu(pre), max(float(np.max(np.abs(z))), 1e-300), tol)
+    rep[name + ".argmax"] = rep.get(name + ".argmax", 0) + int(diff.sum())
+    # ReLU of the pooled value: the forced element's pre-activation where the GPU kept it, else the window max
+    mask = forced_relu_mask(name + ".relu", np.where(gpu_pos, pre, win.max(axis=0)), gpu_pos, tol, rep)
+    return np.where(mask, relu(pre), 0.0), ga, mask
+
+
 def softmax_ce(z, y):
     """Mean CE over the batch and dz = (softmax - onehot)/|beta|."""
     nb = z.shape[0]
@@ -198,64 +242,89 @@ def bf16(x):
     return r.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
-def loss_and_grad(p, model, xb, yb, emulate_bf16=False):
+def loss_and_grad(p, model, xb, yb, emulate_bf16=False, decisions=None, tol=0.0):
     """xb float64 [nb, H, W, C] in [0,1]; returns (loss, grads dict).
 
     emulate_bf16: round to bf16 exactly where the CUDA bf16 mode stores bf16
     (pooled / hidden activations, dh, the pre-activation gradients dz, and the
     conv2 / fc1 weights read by the tensor cores; ResNet-8: every stored
     activation and gradient, the staged input and every conv's weights); everything else
-    float64."""
+    float64.
+
+    decisions (teacher-forced parity only; None = the oracle's own decisions): the GPU's ReLU masks and
+    pool argmaxes of this step, taken where valid within `tol` (forced_relu_mask / forced_pool); keys
+    MLP "h1"; CNN "a1", "i1", "a2", "i2", "h"; ResNet-8 "a0", "r1", "o1", "r2", "o2", "r3", "o3" (the
+    GPU's stored activations, > 0 = the mask; i1 / i2 its argmaxes).  The number of decisions that
+    differed from the oracle's own is added to decisions["_forced"]."""
     q = bf16 if emulate_bf16 else (lambda v: v)
+    dec = decisions
+    rep = dec.setdefault("_forced", {}) if dec is not None else None
     g = {}
     nb = xb.shape[0]
     if model == MLP:
         x = xb.reshape(nb, -1)
         z1 = x @ p["fc1.W"].T + p["fc1.b"]
         h1 = q(relu(z1))
+        m1 = h1 > 0 if dec is None else forced_relu_mask("h1", z1, dec["h1"] > 0, tol, rep)
+        h1 = np.where(m1, h1, 0.0)
         z2 = h1 @ p["fc2.W"].T + p["fc2.b"]
         loss, dz2 = softmax_ce(z2, yb)
         g["fc2.W"], g["fc2.b"] = dz2.T @ h1, dz2.sum(0)
         dh1 = dz2 @ p["fc2.W"]
-        dz1 = dh1 * (h1 > 0)
+        dz1 = dh1 * m1
         g["fc1.b"] = dz1.sum(0)
         g["fc1.W"] = q(dz1).T @ x
         return loss, g
     if model == CNN:
         W2q, W3q = q(p["conv2.W"]), q(p["fc1.W"])
         z1, cols1 = conv_fwd(q(xb), q(p["conv1.W"]), p["conv1.b"], 1, 2)
-        a1, arg1 = pool2_fwd(relu(z1))
+        if dec is None:
+            a1, arg1 = pool2_fwd(relu(z1))
+            m1 = a1 > 0
+        else:
+            a1, arg1, m1 = forced_pool("pool1", z1, dec["i1"], dec["a1"] > 0, tol, rep)
         a1 = q(a1)
         z2, cols2 = conv_fwd(a1, W2q, p["conv2.b"], 1, 2)
-        a2, arg2 = pool2_fwd(relu(z2))
+        if dec is None:
+            a2, arg2 = pool2_fwd(relu(z2))
+            m2 = a2 > 0
+        else:
+            a2, arg2, m2 = forced_pool("pool2", z2, dec["i2"], dec["a2"] > 0, tol, rep)
         a2 = q(a2)
         f = a2.reshape(nb, -1)
         z3 = f @ W3q.T + p["fc1.b"]
         h = q(relu(z3))
+        m3 = h > 0 if dec is None else forced_relu_mask("h", z3, dec["h"] > 0, tol, rep)
+        h = np.where(m3, h, 0.0)
         z4 = h @ p["fc2.W"].T + p["fc2.b"]
         loss, dz4 = softmax_ce(z4, yb)
         g["fc2.W"], g["fc2.b"] = dz4.T @ h, dz4.sum(0)
-        dz3 = (dz4 @ p["fc2.W"]) * (h > 0)
+        dz3 = (dz4 @ p["fc2.W"]) * m3
         g["fc1.b"] = dz3.sum(0)
         dz3 = q(dz3)
         g["fc1.W"] = dz3.T @ f
         da2 = (dz3 @ W3q).reshape(a2.shape)
-        dz2 = q(pool2_bwd(da2 * (a2 > 0), arg2, z2.shape))
+        dz2 = q(pool2_bwd(da2 * m2, arg2, z2.shape))
         g["conv2.W"], g["conv2.b"], da1 = conv_bwd(dz2, a1.shape, cols2, W2q, 1, 2, True)
-        dz1 = q(pool2_bwd(da1 * (a1 > 0), arg1, z1.shape))
+        dz1 = q(pool2_bwd(da1 * m1, arg1, z1.shape))
         g["conv1.W"], g["conv1.b"], _ = conv_bwd(dz1, xb.shape, cols1, q(p["conv1.W"]), 1, 2, False)
         return loss, g
     if model == RESNET8:
         # emulate_bf16: the staged input, the stored activations (a0, each block's ra and output), the
         # stored gradients (each block's ds and dza, dz0) and every conv's weights (tensor-core shadow)
+        def rmask(name, z):  # the ReLU decision of a stored activation (own, or the GPU's where valid)
+            return z > 0 if dec is None else forced_relu_mask(name, z, dec[name] > 0, tol, rep)
+
         z0, cols0 = conv_fwd(q(xb), q(p["conv0.W"]), p["conv0.b"], 1, 1)
-        a0 = q(relu(z0))
+        m0 = rmask("a0", z0)
+        a0 = q(np.where(m0, relu(z0), 0.0))
         caches = []
         a = a0
-        for blk, stride in (("b1", 1), ("b2", 2), ("b3", 2)):
+        for bi, (blk, stride) in enumerate((("b1", 1), ("b2", 2), ("b3", 2))):
             Wa, Wb = q(p[blk + "a.W"]), q(p[blk + "b.W"])
             za, colsa = conv_fwd(a, Wa, p[blk + "a.b"], stride, 1)
-            ra = q(relu(za))
+            ma = rmask(f"r{bi + 1}", za)
+            ra = q(np.where(ma, relu(za), 0.0))
             zb, colsb = conv_fwd(ra, Wb, p[blk + "b.b"], 1, 1)
             cout = zb.shape[3]
             if stride == 1 and a.shape[3] == cout:
@@ -265,8 +334,9 @@ def loss_and_grad(p, model, xb, yb, emulate_bf16=False):
                 sc = np.zeros(sub.shape[:3] + (cout,))
                 sc[..., :sub.shape[3]] = sub
             s = zb + sc
-            out = q(relu(s))
-            caches.append((blk, stride, a, za, colsa, ra, colsb, s, Wa, Wb))
+            ms = rmask(f"o{bi + 1}", s)
+            out = q(np.where(ms, relu(s), 0.0))
+            caches.append((blk, stride, a, ma, colsa, ra, colsb, ms, Wa, Wb))
             a = out
         gap = a.mean(axis=(1, 2))
         z = gap @ p["fc.W"].T + p["fc.b"]
@@ -275,25 +345,25 @@ def loss_and_grad(p, model, xb, yb, emulate_bf16=False):
         dgap = dz @ p["fc.W"]
         HW = a.shape[1] * a.shape[2]
         dout = np.broadcast_to(dgap[:, None, None, :] / HW, a.shape).copy()
-        for blk, stride, a_in, za, colsa, ra, colsb, s, Wa, Wb in reversed(caches):
-            ds = q(dout * (s > 0))
+        for blk, stride, a_in, ma, colsa, ra, colsb, ms, Wa, Wb in reversed(caches):
+            ds = q(dout * ms)
             g[blk + "b.W"], g[blk + "b.b"], dra = conv_bwd(ds, ra.shape, colsb, Wb, 1, 1, True)
-            dza = q(dra * (za > 0))
+            dza = q(dra * ma)
             g[blk + "a.W"], g[blk + "a.b"], da_in = conv_bwd(dza, a_in.shape, colsa, Wa, stride, 1, True)
             if stride == 1 and a_in.shape[3] == ds.shape[3]:
                 da_in = da_in + ds
             else:
                 da_in[:, ::2, ::2, :] += ds[..., :a_in.shape[3]]
             dout = da_in
-        dz0 = q(dout * (z0 > 0))
+        dz0 = q(dout * m0)
         g["conv0.W"], g["conv0.b"], _ = conv_bwd(dz0, xb.shape, cols0, p["conv0.W"], 1, 1, False)
         return loss, g
     raise ValueError(model)
 
 
-def flat_loss_and_grad(w, model, width_q, classes, xb, yb, emulate_bf16=False):
+def flat_loss_and_grad(w, model, width_q, classes, xb, yb, emulate_bf16=False, decisions=None, tol=0.0):
     p = unpack(np.asarray(w, dtype=np.float64), model, width_q, classes)
-    loss, g = loss_and_grad(p, model, xb, yb, emulate_bf16)
+    loss, g = loss_and_grad(p, model, xb, yb, emulate_bf16, decisions, tol)
     return loss, pack(g, model, width_q, classes)
 
 

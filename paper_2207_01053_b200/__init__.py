@@ -31,7 +31,7 @@ ORDER_ASC_ID, ORDER_DESC_STEPS = 0, 1
 EXPORTS = ["protea_init", "protea_finalize", "protea_last_error", "protea_register_model", "protea_register_shards",
            "protea_profile_clients", "protea_plan", "protea_run_round", "protea_fedavg", "protea_client_footprint",
            "protea_selftest_gemm", "protea_round_partial", "protea_round_finalize", "protea_plan_hash",
-           "protea_round_finalize_ordered",
+           "protea_round_finalize_ordered", "protea_register_val_shards", "protea_evaluate_round",
            "protea_evaluate", "protea_heterofl_extract", "protea_heterofl_aggregate"]
 
 
@@ -68,17 +68,19 @@ class PlanOpts(ctypes.Structure):
 N_OPC = 32
 # op classes that run on tcgen05 tensor cores in bf16 mode (CNN); the others use SIMT fp32 math
 TC_OPS_BUILT = {"conv1_fwd": True, "conv2_fwd": True, "fc1_fwd": True, "fc1_dgrad": True, "fc1_wgrad": True,
-                "conv2_dgrad": True, "conv2_wgrad": True, "conv1_wgrad": True}
+                "conv2_dgrad": True, "conv2_wgrad": True, "conv1_wgrad": True, "resnet_fwd": True,
+                "resnet_dgrad": True, "resnet_wgrad": True}
 OPC_NAMES = ["conv1_fwd", "conv2_fwd", "fc1_fwd", "head", "fc1_dgrad", "fc1_wgrad", "conv2_dgrad", "conv2_wgrad",
              "conv2_reduce", "conv1_wgrad", "conv1_reduce", "mlp_fc1_fwd", "mlp_head", "mlp_fc1_wgrad", "admit",
              "fedavg", "stage_x", "resnet_fwd", "resnet_head", "resnet_dgrad", "resnet_wgrad",
-             "resnet_reduce"] + [f"op{i}" for i in range(22, 32)]
+             "resnet_reduce", "eval_head"] + [f"op{i}" for i in range(23, 32)]
 
 
 class RoundOpts(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_float), ("seed", ctypes.c_uint32), ("round", ctypes.c_uint32),
                 ("shuffle", ctypes.c_int32), ("time_ops", ctypes.c_uint32), ("partial_only", ctypes.c_uint32),
-                ("serialize", ctypes.c_uint32)]
+                ("serialize", ctypes.c_uint32), ("observe_hwm", ctypes.c_uint32), ("n_trace", ctypes.c_uint32),
+                ("trace_ids", ctypes.c_void_p), ("trace_bufs", ctypes.c_void_p)]
 
 
 class RoundStats(ctypes.Structure):
@@ -127,6 +129,8 @@ _lib.protea_client_footprint.argtypes = [ctypes.POINTER(ModelDesc), ctypes.c_int
 _lib.protea_round_partial.argtypes = [_vp, _vp, _sz]
 _lib.protea_round_finalize.argtypes = [_vp, _vp, _vp, _vp, _sz]
 _lib.protea_round_finalize_ordered.argtypes = [_vp, _vp, ctypes.c_int32, _vp, _vp, _sz]
+_lib.protea_register_val_shards.argtypes = [_vp, _vp, _sz]
+_lib.protea_evaluate_round.argtypes = [_vp, _vp, _sz, _vp, _sz, _vp, _vp]
 _lib.protea_selftest_gemm.argtypes = [_vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
 for _f in EXPORTS:
     if _f not in ("protea_finalize", "protea_last_error", "protea_plan_hash"):
@@ -191,8 +195,7 @@ def protea_register_model(ctx, arch, width_q=4, classes=10, H=32, W=32, C=3):
     return mid.value, npar.value
 
 
-def protea_register_shards(ctx, shards):
-    """shards: iterable of (client_id, x u8 [n, D], y int32 [n]) host arrays."""
+def _shard_records(shards):
     keep = []
     rec = np.zeros(len(shards), dtype=SHARD_DT)
     for i, (cid, x, y) in enumerate(shards):
@@ -200,7 +203,30 @@ def protea_register_shards(ctx, shards):
         y = np.ascontiguousarray(y, dtype=np.int32)
         keep += [x, y]
         rec[i] = (cid, y.shape[0], x.ctypes.data, y.ctypes.data)
+    return rec, keep
+
+
+def protea_register_shards(ctx, shards):
+    """shards: iterable of (client_id, x u8 [n, D], y int32 [n]) host arrays."""
+    rec, keep = _shard_records(shards)
     _check(_lib.protea_register_shards(ctx, rec.ctypes.data, len(rec)), ctx)
+
+
+def protea_register_val_shards(ctx, shards):
+    """Validation splits, same records as protea_register_shards."""
+    rec, keep = _shard_records(shards)
+    _check(_lib.protea_register_val_shards(ctx, rec.ctypes.data, len(rec)), ctx)
+
+
+def protea_evaluate_round(ctx, clients, global_w):
+    """Every client evaluates its group's global weights (float32 tensor/array, host or device, all groups
+    concatenated) on its validation split.  Returns (per-client EVAL_DT records, (loss_sum, correct, n))."""
+    n_params = global_w.numel() if hasattr(global_w, "numel") else global_w.size
+    per = np.zeros(len(clients), dtype=EVAL_DT)
+    tot = EvalResult()
+    _check(_lib.protea_evaluate_round(ctx, clients.ctypes.data, len(clients), _ptr(global_w), n_params,
+                                      per.ctypes.data, ctypes.byref(tot)), ctx)
+    return per, (tot.loss_sum, int(tot.correct), int(tot.n))
 
 
 def clients_array(rows):
@@ -230,6 +256,9 @@ def protea_plan(profiles, caps, policy=POLICY_PROFILED, order=ORDER_ASC_ID, marg
     return out, mk
 
 
+EVAL_DT = np.dtype([("loss_sum", np.float64), ("correct", np.uint64), ("n", np.uint64)])
+
+
 class EvalResult(ctypes.Structure):
     _fields_ = [("loss_sum", ctypes.c_double), ("correct", ctypes.c_uint64), ("n", ctypes.c_uint64)]
 
@@ -254,9 +283,16 @@ def protea_plan_hash(clients, plan):
 
 
 def protea_run_round(ctx, clients, plan, global_in, global_out, lr=0.05, seed=0, rnd=0, shuffle=True,
-                     measured=False, time_ops=0, partial_only=False, serialize=False):
-    """global_in / global_out: float32 torch tensors (cuda or cpu) or numpy arrays."""
-    o = RoundOpts(lr, seed, rnd, 1 if shuffle else 0, time_ops, 1 if partial_only else 0, 1 if serialize else 0)
+                     measured=False, time_ops=0, partial_only=False, serialize=False, observe_hwm=False,
+                     trace=None):
+    """global_in / global_out: float32 torch tensors (cuda or cpu) or numpy arrays.
+    trace: {client_id: device uint8 tensor of (S_k + 1) * footprint peak_bytes} slot snapshots per local step."""
+    trace = trace or {}
+    tids = np.array(list(trace.keys()), dtype=np.int64)
+    tbufs = np.array([_ptr(t) for t in trace.values()], dtype=np.uint64)
+    o = RoundOpts(lr, seed, rnd, 1 if shuffle else 0, time_ops, 1 if partial_only else 0, 1 if serialize else 0,
+                  1 if observe_hwm else 0, len(tids), tids.ctypes.data if len(tids) else None,
+                  tbufs.ctypes.data if len(tids) else None)
     st = RoundStats()
     n_params = global_in.numel() if hasattr(global_in, "numel") else global_in.size
     meas = np.zeros(len(clients), dtype=PROFILE_DT) if measured else None

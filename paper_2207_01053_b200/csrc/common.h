@@ -73,6 +73,20 @@ int cnn_conv2_splits(int rows);
 
 SlotLayout slot_layout(const ModelDims& m, int batch, int64_t n, int epochs, int elem_bytes);
 
+// Batches larger than kMicroRows rows (§4.3: batch sizes 1024 / 2048) run as micro-clients:
+// the batch's rows are cut into ceil(min(B, n) / kMicroRows) chunks, each a full client slot of
+// min(kMicroRows, rest) rows that takes its SGD step from the same weights; after the step a merge kernel
+// forms w + sum_m (b_m / |beta|) (w_m - w) = w - lr grad(mean over |beta|) (engine.cu).
+// The client's slot is the micro slots back to back followed by the merge weights (fp32, P floats).
+constexpr int kMicroRows = 64;
+constexpr float kMicroLrScale = 1048576.0f;  // micro SGD steps use lr * 2^20 (exact scaling, see engine.cu)
+// Exact arena high-water mark of a client (= slot_layout(...).total when min(B, n) <= kMicroRows).
+uint64_t client_hwm(const ModelDims& m, int batch, int64_t n, int epochs, int elem_bytes);
+inline int micro_count(int batch, int64_t n) {
+  const int64_t b = batch < n ? batch : n;
+  return b <= kMicroRows ? 1 : (int)((b + kMicroRows - 1) / kMicroRows);
+}
+
 // bf16-mode conv1 "pool-quad" weight shadow w1q (buffer B_W1P), DESIGN.md §6:
 // [dy 6][dx>>1 3][dx&1 2][n = q*C1 + co][ci 8] bf16, q = 2qy+qx a position of
 // the 2x2 pool window and (dy, dx) = (qy+ky, qx+kx) the tap's offset inside the

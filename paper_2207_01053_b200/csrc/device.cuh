@@ -18,13 +18,14 @@ struct ClientRec {
   const int32_t* y;        // labels
   const float* wg;         // global weights of the client's group (device)
   double* acc;             // group FedAvg accumulator (fp64)
-  int32_t n, B, E, nb;     // nb = ceil(n/B)
+  int32_t n, B, E, nb;     // B = min(B_k, n): rows one batch can hold (per-row buffer capacity); nb = ceil(n/B_k)
   int64_t P;               // parameters of the client's model
   int32_t c1;              // CNN conv1 channels (padded conv1 shadow in bf16 mode), else 0
   int32_t pad_;
   int64_t id;
   uint64_t* sm_ns;         // per-client device-time attribution (nullable)
   const void* tmaps;       // bf16 CNN: TM_COUNT CUtensorMaps (128 B each, global memory), else nullptr
+  float* mw;               // micro-client 0 of a batch > kMicroRows: the merge weights (P fp32), else nullptr
 };
 
 // One active client in one lock-step iteration.

@@ -91,12 +91,16 @@ struct protea_ctx {
   uint64_t arena_bytes = 0;
   std::vector<Group> groups;
   std::map<int64_t, ShardDev> shards;
+  std::map<int64_t, ShardDev> val_shards;  // validation splits, protea_register_val_shards
+  bool eval_mode = false;                  // execute(): forward + k_eval_head only (evaluate round)
   ncclComm_t comm = nullptr;
   std::string err;
   DevArray<float> gin, gout;
   DevArray<double> acc;
   DevArray<double> gath;     // K7: all-gathered per-rank partials [world][P + groups]
   DevArray<uint64_t> flag;   // plan hash / error flags exchanged before and after a round
+  DevArray<uint64_t> regions;          // observed HWMs: (offset, bytes) per slot / guard region
+  DevArray<unsigned long long> hwm;    // observed HWMs: 1 + highest touched byte per region
   DevArray<ClientRec> recs;
   DevArray<int32_t> tab;
   // protea_evaluate workspace (kept apart from the round's tables)
@@ -324,7 +328,7 @@ static protea_status fail(protea_ctx* ctx, protea_status s, const std::string& m
 // ---------------------------------------------------------------------------
 namespace {
 
-constexpr int kMaxBatch = 64;
+constexpr int kMaxBatch = 4096;  // batches above kMicroRows rows run as micro-clients (common.h)
 
 // tile shapes
 constexpr int C1F_BM = 64, C1F_BN = 32;
@@ -641,6 +645,15 @@ void launch_conv2_wgrad_halo(protea_ctx* ctx, const ClientRec* drecs, const CnnD
   }
 }
 
+// Evaluate round: the classifier head after the forward kernels (kernels_misc.cuh k_eval_head)
+template <typename T>
+void launch_eval(protea_ctx* ctx, const Launch& L, const ClientRec* drecs, const Task* tasks, int feat_buf, int F,
+                 int hw, const Layer& fc, int C) {
+  const int ev = op_begin(ctx, PROTEA_OPC_EVAL_HEAD);
+  k_eval_head<T><<<L.ntask, kEvalThreads, 0, ctx->cur>>>(drecs, tasks, feat_buf, F, hw, fc.off_w, fc.off_b, C);
+  op_end(ctx, ev);
+}
+
 template <typename T>
 void launch_head_cnn(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const Task* tasks,
                      float lr) {
@@ -694,6 +707,10 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
     launch_gemm_tc<TC_C2F_BN, TC_STAGES>(ctx, TmaConv2Fwd<WQ>{drecs, d}, L, OP_C2F, dtab);
   // (a split-K persistent variant for light iterations measured slower: 7.2 -> 8.0 ms/round)
   launch_gemm_tc<TC_F1F_BN, TC_F1F_STAGES>(ctx, tma_op<TmaFc1Fwd<WQ>>(drecs, d), L, OP_F1F, dtab);
+  if (ctx->eval_mode) {
+    launch_eval<T>(ctx, L, drecs, tasks, B_H, m.f, 1, m.layers[3], m.classes);
+    return;
+  }
   launch_head_cnn<T>(ctx, m, L, drecs, tasks, lr);
   launch_gemm_persistent<TC_F1D_BN, 8>(ctx, tma_op<TmaFc1Dgrad<WQ>>(drecs, d), L, OP_F1D, dtab, 1);
   // fc1 wgrad (HBM-bound RMW of the fp32 master + bf16 shadow) needs dh, a2 and the fc1 weights, which
@@ -856,6 +873,10 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
     launch_gemm<F, R_BM, R_BN>(ctx, f, L, RI_F0 + i, dtab);
   }
   const Layer& fc = m.layers[7];
+  if (ctx->eval_mode) {
+    launch_eval<T>(ctx, L, drecs, tasks, B_R_O3, 64, 64, fc, m.classes);
+    return;
+  }
   RHeadArgs ha{drecs, m.classes, fc.off_w, fc.off_b, lr};
   int ev = op_begin(ctx, PROTEA_OPC_R_HEAD, RI_HEAD);
   k_rhead<T><<<L.ntask, 256, 0, ctx->cur>>>(ha, tasks);
@@ -958,6 +979,10 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Conv1Fwd<T, C1F_BM, C1F_BN>, C1F_BM, C1F_BN>(ctx, {drecs, d}, L, OP_C1F, dtab);
     launch_gemm<Conv2Fwd<T, C2F_BM, C2F_BN>, C2F_BM, C2F_BN>(ctx, {drecs, d}, L, OP_C2F, dtab);
     launch_gemm<Fc1Fwd<T, F1F_BM, F1F_BN>, F1F_BM, F1F_BN>(ctx, {drecs, d}, L, OP_F1F, dtab);
+    if (ctx->eval_mode) {
+      launch_eval<T>(ctx, L, drecs, tasks, B_H, m.f, 1, m.layers[3], m.classes);
+      return;
+    }
     launch_head_cnn<T>(ctx, m, L, drecs, tasks, lr);
     int ev;
     launch_gemm<Fc1Dgrad<T, F1D_BM, F1D_BN>, F1D_BM, F1D_BN>(ctx, {drecs, d}, L, OP_F1D, dtab);
@@ -987,6 +1012,10 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
       const int ev = op_begin(ctx, OP_MF, OP_MF);
       k_mlp_fc1_fwd<T><<<dim3(L.ntask, 4), kMlpFwdThreads, smem, ctx->cur>>>(drecs, tasks, d);
       op_end(ctx, ev);
+    }
+    if (ctx->eval_mode) {
+      launch_eval<T>(ctx, L, drecs, tasks, B_H1, 64, 1, m.layers[1], m.classes);
+      return;
     }
     HeadArgs ha{drecs, B_H1, B_DZ1, 64, m.classes, d.w2, d.b2, d.b1, lr};
     const int ev = op_begin(ctx, OP_MHEAD, OP_MHEAD);
@@ -1129,15 +1158,18 @@ void protea_finalize(protea_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  for (auto& kv : ctx->shards) {
-    cudaFree(kv.second.x);
-    cudaFree(kv.second.y);
-  }
+  for (auto* mp : {&ctx->shards, &ctx->val_shards})
+    for (auto& kv : *mp) {
+      cudaFree(kv.second.x);
+      cudaFree(kv.second.y);
+    }
   ctx->gin.release();
   ctx->gout.release();
   ctx->acc.release();
   ctx->gath.release();
   ctx->flag.release();
+  ctx->regions.release();
+  ctx->hwm.release();
   ctx->recs.release();
   ctx->tab.release();
   ctx->ev_recs.release();
@@ -1197,7 +1229,8 @@ protea_status protea_register_model(protea_ctx* ctx, const protea_model_desc* de
   return PROTEA_OK;
 }
 
-protea_status protea_register_shards(protea_ctx* ctx, const protea_shard* shards, size_t n) {
+static protea_status register_into(protea_ctx* ctx, std::map<int64_t, ShardDev>& dst, const protea_shard* shards,
+                                   size_t n) {
   if (!ctx) return PROTEA_ERR_INVALID;
   if (!shards || n == 0) return fail(ctx, PROTEA_ERR_INVALID, "register_shards: null or empty");
   for (size_t i = 0; i < n; ++i)
@@ -1211,15 +1244,15 @@ protea_status protea_register_shards(protea_ctx* ctx, const protea_shard* shards
   CK(cudaSetDevice(ctx->device));
   for (size_t i = 0; i < n; ++i) {
     const protea_shard& s = shards[i];
-    auto it = ctx->shards.find(s.client_id);
+    auto it = dst.find(s.client_id);
     ShardDev d;
-    if (it != ctx->shards.end() && it->second.n == s.n) {
+    if (it != dst.end() && it->second.n == s.n) {
       d = it->second;  // same size: refresh the device copy in place
     } else {
-      if (it != ctx->shards.end()) {
+      if (it != dst.end()) {
         cudaFree(it->second.x);
         cudaFree(it->second.y);
-        ctx->shards.erase(it);
+        dst.erase(it);
       }
       d.n = s.n;
       d.x = nullptr;
@@ -1231,10 +1264,20 @@ protea_status protea_register_shards(protea_ctx* ctx, const protea_shard* shards
     d.ymax = *std::max_element(s.y, s.y + s.n);
     CK(cudaMemcpyAsync(d.x, s.x, (size_t)s.n * D, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(d.y, s.y, (size_t)s.n * 4, cudaMemcpyHostToDevice, ctx->stream));
-    ctx->shards[s.client_id] = d;
+    dst[s.client_id] = d;
   }
   CK(cudaStreamSynchronize(ctx->stream));
   return PROTEA_OK;
+}
+
+protea_status protea_register_shards(protea_ctx* ctx, const protea_shard* shards, size_t n) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  return register_into(ctx, ctx->shards, shards, n);
+}
+
+protea_status protea_register_val_shards(protea_ctx* ctx, const protea_shard* shards, size_t n) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  return register_into(ctx, ctx->val_shards, shards, n);
 }
 
 protea_status protea_client_footprint(const protea_model_desc* desc, int64_t n, int32_t batch, int32_t epochs,
@@ -1250,8 +1293,7 @@ protea_status protea_client_footprint(const protea_model_desc* desc, int64_t n, 
     set_global_error("client_footprint: " + err);
     return PROTEA_ERR_INVALID;
   }
-  const SlotLayout s = slot_layout(m, batch, n, epochs, precision == PROTEA_PREC_FP32 ? 4 : 2);
-  *peak_bytes = s.total;
+  *peak_bytes = client_hwm(m, batch, n, epochs, precision == PROTEA_PREC_FP32 ? 4 : 2);
   *steps = (uint64_t)epochs * ceil_div((uint64_t)n, (uint64_t)batch);
   *flops = (uint64_t)epochs * (uint64_t)n * flops_per_sample(m);
   return PROTEA_OK;
@@ -1271,19 +1313,74 @@ struct RunClient {
   int B, E, nb;
   uint64_t S, admit, release;
   uint64_t offset;
+  uint64_t slot = 0;  // planned slot bytes (observe_hwm poisons / scans [offset, offset + slot))
+  // micro-clients (batches above kMicroRows rows, common.h): execute() expands such a client into
+  // micro-clients micro = 0..nmicro-1, each holding rows [micro * kMicroRows, +cap) of every batch
+  int orig = -1;      // index of the client in execute()'s input
+  int micro = 0, nmicro = 1;
+  int cap = 0;        // rows this (micro-)client's slot holds: min(B, n) or its share of it
+  uint64_t mw_off = 0;  // micro 0: arena offset of the merge weights
   int rec = -1;
   int lane = 0;  // lock-step lane within the model group (PROTEA_LANES)
+};
+
+// Rows of (micro-)client c's batch in lock-step iteration t (0: the micro has no rows in this batch).
+int micro_rows(const RunClient& c, uint64_t t) {
+  const int64_t j = (int64_t)((t - c.admit) % c.nb);
+  const int64_t rb = std::min<int64_t>(c.B, c.n - j * c.B);
+  return (int)std::max<int64_t>(0, std::min<int64_t>(c.cap, rb - (int64_t)c.micro * kMicroRows));
+}
+
+// Verification / observation extras of one execute() call.
+struct ExecExtras {
+  bool observe = false;             // poison each slot at admission, scan it at release -> ctx->hwm[rec]
+  std::map<int64_t, uint8_t*> trace;  // client id -> device buffer of (S_k + 1) slot snapshots
+  bool eval = false;                  // evaluate round: forward + classifier head, no update, no merge
+  const std::map<int64_t, ShardDev>* shards = nullptr;  // data to read (default: the training shards)
+  std::vector<double>* stats_out = nullptr;  // eval: per input client (loss sum, correct) from stats[0], [2]
 };
 
 // Validates and executes the lock-step schedule of `rc` (this rank's clients,
 // ascending id) inside the arena.  wg: device concatenated global weights;
 // acc: device fp64 accumulator (zeroed by caller) or nullptr (probe mode:
 // no FedAvg terms).  Returns iterations run.
-protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* wg, double* acc, float lr,
-                      uint32_t seed, uint32_t round, int shuffle, uint64_t* iters_out, double* loss_dev) {
+protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const float* wg, double* acc, float lr,
+                      uint32_t seed, uint32_t round, int shuffle, uint64_t* iters_out, double* loss_dev,
+                      const ExecExtras* xx = nullptr) {
   const int e = ctx->precision == PROTEA_PREC_FP32 ? 4 : 2;
   const bool tc_mode = e == 2;  // bf16 mode: tensor-core GEMMs for the CNN
   const int G = (int)ctx->groups.size();
+  struct EvalFlag {  // ctx->eval_mode for the duration of this call (every return path)
+    protea_ctx* c;
+    EvalFlag(protea_ctx* c_, bool on) : c(c_) { c->eval_mode = on; }
+    ~EvalFlag() { c->eval_mode = false; }
+  } eval_flag(ctx, xx && xx->eval);
+  // ---- micro-clients: a client whose batch holds more than kMicroRows rows becomes nmicro micro-clients
+  // (slots back to back inside its slot, then the merge weights); results are reported per input client
+  std::vector<RunClient> rc;
+  bool have_micro = false;
+  for (size_t i = 0; i < rc_in.size(); ++i) {
+    const RunClient& c = rc_in[i];
+    const ModelDims& m = ctx->groups[c.group].m;
+    const int64_t beff = std::min<int64_t>(c.B, c.n);
+    const int M = micro_count(c.B, c.n);
+    uint64_t off = c.offset;
+    for (int k = 0; k < M; ++k) {
+      RunClient x = c;
+      x.orig = (int)i;
+      x.micro = k;
+      x.nmicro = M;
+      x.cap = (int)std::min<int64_t>(M == 1 ? beff : kMicroRows, beff - (int64_t)k * kMicroRows);
+      x.offset = off;
+      x.slot = k == 0 ? c.slot : 0;  // observe_hwm: micro 0's region is the whole client slot
+      off += slot_layout(m, x.cap, c.n, c.E, e).total;
+      rc.push_back(x);
+    }
+    if (M > 1) {
+      rc[rc.size() - M].mw_off = off;
+      have_micro = true;
+    }
+  }
   // ---- device records
   std::vector<ClientRec> recs(rc.size());
   std::vector<int64_t> gacc_off(G, 0);
@@ -1292,7 +1389,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     RunClient& c = rc[i];
     c.rec = (int)i;
     const Group& gr = ctx->groups[c.group];
-    const SlotLayout L = slot_layout(gr.m, c.B, c.n, c.E, e);
+    const SlotLayout L = slot_layout(gr.m, c.cap, c.n, c.E, e);
     ClientRec& r = recs[i];
     std::memset(&r, 0, sizeof(r));
     uint8_t* base = ctx->arena + c.offset;
@@ -1300,23 +1397,50 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     r.params = (float*)r.buf[B_PARAMS];
     r.perm = (int32_t*)r.buf[B_PERM];
     r.stats = (float*)r.buf[B_STATS];
-    const ShardDev& sd = ctx->shards[c.id];
+    const ShardDev& sd = (xx && xx->shards ? *const_cast<std::map<int64_t, ShardDev>*>(xx->shards) : ctx->shards)[c.id];
     r.x = sd.x;
     r.y = sd.y;
     r.wg = wg + gr.offset;
     r.acc = acc ? acc + gacc_off[c.group] : nullptr;
     r.n = (int32_t)c.n;
-    r.B = c.B;
+    r.B = c.cap;  // rows a batch can hold here: the slot's per-row buffer capacity
+    r.mw = c.mw_off ? (float*)(ctx->arena + c.mw_off) : nullptr;
     r.E = c.E;
     r.nb = c.nb;
     r.id = c.id;
     r.P = gr.m.P;
     r.c1 = gr.m.c1;
   }
+  // ---- observed high-water marks (poisoned slots) and traced clients
+  const bool observe = xx && xx->observe;
+  std::vector<uint8_t*> trace_of(rc.size(), nullptr);
+  std::vector<uint64_t> trace_bytes(rc.size(), 0);  // a snapshot = the whole slot layout (params first)
+  if (xx)
+    for (size_t i = 0; i < rc.size(); ++i) {
+      auto it = xx->trace.find(rc[i].id);
+      if (it != xx->trace.end() && rc[i].micro == 0) {  // the whole client slot (all micro slots)
+        trace_of[i] = it->second;
+        trace_bytes[i] = client_hwm(ctx->groups[rc[i].group].m, rc[i].B, rc[i].n, rc[i].E, e);
+      }
+    }
+  uint64_t max_slot = 0;
+  if (observe) {
+    std::vector<uint64_t> reg(3 * rc.size());
+    for (size_t i = 0; i < rc.size(); ++i) {
+      reg[3 * i] = rc[i].offset;
+      reg[3 * i + 1] = rc[i].slot;
+      reg[3 * i + 2] = (uint64_t)rc[i].orig;  // observed mark reported per input client
+      max_slot = std::max(max_slot, rc[i].slot);
+    }
+    CK(ctx->regions.reserve(reg.size()));
+    CK(ctx->hwm.reserve(rc_in.size()));
+    CK(cudaMemcpyAsync(ctx->regions.p, reg.data(), reg.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->hwm.p, 0, rc_in.size() * 8, ctx->stream));
+  }
   // ---- K9 per-client SM-time counters
-  CK(ctx->smns.reserve(std::max<size_t>(rc.size(), 1)));
-  CK(cudaMemsetAsync(ctx->smns.p, 0, std::max<size_t>(rc.size(), 1) * 8, ctx->stream));
-  for (size_t i = 0; i < rc.size(); ++i) recs[i].sm_ns = ctx->smns.p + i;
+  CK(ctx->smns.reserve(std::max<size_t>(rc_in.size(), 1)));
+  CK(cudaMemsetAsync(ctx->smns.p, 0, std::max<size_t>(rc_in.size(), 1) * 8, ctx->stream));
+  for (size_t i = 0; i < rc.size(); ++i) recs[i].sm_ns = ctx->smns.p + rc[i].orig;  // micros add up
   // ---- TMA tensor maps (bf16 CNN clients)
   if (tc_mode) {
     std::vector<CUtensorMap> maps;
@@ -1324,11 +1448,11 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     for (size_t i = 0; i < rc.size(); ++i) {
       const ModelDims& m = ctx->groups[rc[i].group].m;
       if (m.arch != PROTEA_MODEL_CNN) continue;
-      auto key = std::make_tuple(rc[i].offset, rc[i].B, rc[i].E, rc[i].n, rc[i].group);
+      auto key = std::make_tuple(rc[i].offset, rc[i].cap, rc[i].E, rc[i].n, rc[i].group);
       auto it = ctx->tmap_cache.find(key);
       if (it == ctx->tmap_cache.end()) {
         std::array<CUtensorMap, TM_COUNT> a;
-        if (!build_cnn_tmaps(m, recs[i], rc[i].B, a.data()))
+        if (!build_cnn_tmaps(m, recs[i], recs[i].B, a.data()))
           return fail(ctx, PROTEA_ERR_CUDA, "run_round: cuTensorMapEncodeTiled failed for client " +
                                                std::to_string(rc[i].id));
         it = ctx->tmap_cache.emplace(key, a).first;
@@ -1344,11 +1468,13 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
     }
   }
   // ---- lock-step lanes: within each (group, batch size) class the clients alternate between lanes, so
-  // every lane gets the same mix of step counts; each lane is an independent chain on its own stream
-  const int NL = tc_mode ? ctx->lanes : 1;
+  // every lane gets the same mix of step counts; each lane is an independent chain on its own stream.
+  // Micro-clients run in one extra lane per group (their SGD steps use lr * kMicroLrScale)
+  const int NL0 = tc_mode ? ctx->lanes : 1;
+  const int NL = NL0 + (have_micro ? 1 : 0);
   {
     std::map<std::pair<int, int>, int> seen_class;
-    for (auto& c : rc) c.lane = NL > 1 ? seen_class[{c.group, c.B}]++ % NL : 0;
+    for (auto& c : rc) c.lane = c.nmicro > 1 ? NL0 : (NL0 > 1 ? seen_class[{c.group, c.B}]++ % NL0 : 0);
   }
   // ---- schedule tables
   uint64_t T = 0;
@@ -1358,6 +1484,11 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
   std::vector<std::pair<int64_t, int>> admits(T + 1, {-1, 0}), rels;  // per-iteration (offset, count)
   std::vector<std::vector<std::pair<int64_t, int>>> rel_by_group(T + 1, std::vector<std::pair<int64_t, int>>(G, {-1, 0}));
   std::vector<std::vector<int>> launch_idx(T);
+  struct Merge {
+    int64_t off;
+    int rec0, R;
+  };
+  std::vector<std::vector<Merge>> merges(T);
   for (uint64_t t = 0; t < T; ++t) {
     // admissions at t (ascending id)
     std::vector<int> adm;
@@ -1372,7 +1503,8 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
       const ModelDims& m = ctx->groups[g].m;
       std::vector<const RunClient*> act;
       for (auto& c : rc)
-        if (c.group == g && c.lane == lane && c.admit <= t && t < c.release) act.push_back(&c);
+        if (c.group == g && c.lane == lane && c.admit <= t && t < c.release && micro_rows(c, t) > 0)
+          act.push_back(&c);
       if (!act.empty()) {
         Launch L;
         std::memset(&L, 0, sizeof(L));
@@ -1385,11 +1517,11 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
         for (size_t i = 0; i < act.size(); ++i) {
           const RunClient& c = *act[i];
           const int s = (int)(t - c.admit), ep = s / c.nb, j = s % c.nb;
-          rows[i] = (int)std::min<int64_t>(c.B, c.n - (int64_t)j * c.B);
+          rows[i] = micro_rows(c, t);
           tab.push_back(c.rec);
           tab.push_back(s);
           tab.push_back(rows[i]);
-          tab.push_back((int32_t)((int64_t)ep * c.n + (int64_t)j * c.B));
+          tab.push_back((int32_t)((int64_t)ep * c.n + (int64_t)j * c.B + (int64_t)c.micro * kMicroRows));
         }
         // width-1 conv2 wgrad: when the iteration has few splits (the tail), each split's 7 M tiles become
         // 7 work items (no extra partials: disjoint outputs), otherwise one item covers all 7 tiles
@@ -1419,11 +1551,24 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
         launches.push_back(L);
       }
     }
+    // micro-client merges after iteration t: [M recs][M rows] per client whose batch is split
+    for (auto& c : rc)
+      if (c.nmicro > 1 && c.micro == 0 && c.admit <= t && t < c.release) {
+        int R = 0;
+        const int64_t off = (int64_t)tab.size();
+        for (int k = 0; k < c.nmicro; ++k) tab.push_back(c.rec + k);
+        for (int k = 0; k < c.nmicro; ++k) {
+          const int r = micro_rows(rc[c.rec + k], t);
+          tab.push_back(r);
+          R += r;
+        }
+        merges[t].push_back({off, c.rec, R});
+      }
     for (int g = 0; g < G; ++g) {
       // releases after iteration t (client finished its last step), all lanes, ascending id
       std::vector<int> rel;
       for (auto& c : rc)
-        if (c.group == g && c.release == t + 1) rel.push_back(c.rec);
+        if (c.group == g && c.release == t + 1 && c.micro == 0) rel.push_back(c.rec);
       if (!rel.empty()) {
         rel_by_group[t][g] = {(int64_t)tab.size(), (int)rel.size()};
         tab.insert(tab.end(), rel.begin(), rel.end());
@@ -1481,8 +1626,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
   std::vector<int64_t> iter_rows(T, 0);
   for (auto& c : rc)
     for (uint64_t t = c.admit; t < c.release; ++t) {
-      const int64_t j = (int64_t)((t - c.admit) % c.nb);
-      iter_rows[t] += std::min<int64_t>(c.B, c.n - j * c.B);
+      iter_rows[t] += micro_rows(c, t);
     }
   for (uint64_t t = 0; t < T; ++t) {
     // (several groups already overlap each other: no side-stream deferral then)
@@ -1501,6 +1645,11 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
         }
       for (auto& c : rc)
         if (c.admit == t) ctx->op_bytes[PROTEA_OPC_ADMIT] += 8 * (uint64_t)ctx->groups[c.group].m.P + 4 * (uint64_t)c.E * c.n;
+      if (observe) {
+        k_fill_poison<<<dim3(grid_for((int64_t)(max_slot / 16), 256, 4 * g_num_sms), admits[t].second), 256, 0,
+                        ctx->cur>>>(ctx->arena, ctx->regions.p, ids);
+        ctx->launches++;
+      }
       int ev = op_begin(ctx, PROTEA_OPC_ADMIT);
       k_admit_params<<<dim3(grid_for(maxP / 4 + 1, 256, 64), admits[t].second), 256, 0, ctx->cur>>>(drecs, ids);
       op_end(ctx, ev);
@@ -1508,6 +1657,10 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
       k_admit_perm<<<dim3(cdiv((int)maxn, kPermThreads), admits[t].second, maxE), kPermThreads, 0, ctx->cur>>>(
           drecs, ids, seed, round, shuffle);
       op_end(ctx, ev);
+      for (auto& c : rc)  // snapshot 0 of a traced client: the weights it starts from
+        if (c.admit == t && trace_of[c.rec])
+          CK(cudaMemcpyAsync(trace_of[c.rec], recs[c.rec].params, trace_bytes[c.rec], cudaMemcpyDeviceToDevice,
+                             ctx->cur));
       fork_groups_from_hi();
     }
     for (int li : launch_idx[t]) {
@@ -1516,28 +1669,54 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
       ctx->cur = gs[L.vg];
       ctx->cur_fl = L.fl;
       ctx->cur_by = L.by;
+      // micro-client lane: SGD steps scaled by the exact power of two kMicroLrScale (k_micro_merge)
+      const float lr_l = have_micro && L.vg % NL == NL0 ? lr * kMicroLrScale : lr;
       if (e == 4)
-        launch_step<float>(ctx, m, L, drecs, dtab, lr);
+        launch_step<float>(ctx, m, L, drecs, dtab, lr_l);
       else if (m.arch == PROTEA_MODEL_CNN)
-        launch_step_tc(ctx, m, L, drecs, dtab, lr);
+        launch_step_tc(ctx, m, L, drecs, dtab, lr_l);
       else
-        launch_step<__nv_bfloat16>(ctx, m, L, drecs, dtab, lr);
+        launch_step<__nv_bfloat16>(ctx, m, L, drecs, dtab, lr_l);
     }
-    if (acc)
+    for (const Merge& mg : (ctx->eval_mode ? std::vector<Merge>() : merges[t])) {  // w' = w + sum_m (b_m / R)(w_m - w) / scale; reload every micro
+      const RunClient& c0 = rc[mg.rec0];
+      ctx->cur = gs[c0.group * NL + c0.lane];
+      join_group(ctx, c0.group);
+      const int64_t P = ctx->groups[c0.group].m.P;
+      k_micro_merge<<<grid_for(P, 256), 256, 0, ctx->cur>>>(drecs, dtab + mg.off, c0.nmicro, mg.R);
+      k_micro_bcast<<<dim3(grid_for(P, 256, 64), c0.nmicro), 256, 0, ctx->cur>>>(drecs, dtab + mg.off);
+      ctx->launches += 2;
+    }
+    for (auto& c : rc)  // snapshot s = t - admit + 1 of a traced client (after its deferred work)
+      if (trace_of[c.rec] && c.admit <= t && t < c.release) {
+        ctx->cur = gs[c.group * NL + c.lane];
+        join_group(ctx, c.group);
+        CK(cudaMemcpyAsync(trace_of[c.rec] + (t - c.admit + 1) * trace_bytes[c.rec], recs[c.rec].params,
+                           trace_bytes[c.rec], cudaMemcpyDeviceToDevice, ctx->cur));
+      }
+    if (acc || observe)
       for (int g = 0; g < G; ++g)
         if (rel_by_group[t][g].second > 0) {
           const int64_t P = ctx->groups[g].m.P;
-          ctx->op_bytes[PROTEA_OPC_FEDAVG] += (uint64_t)P * (20 + 4 * rel_by_group[t][g].second);
           ctx->cur = gs[g * NL];
           for (int l = 1; l < NL; ++l) {  // the group's other lanes finished iteration t first
             cudaEventRecord(ctx->gdone[g * NL + l], gs[g * NL + l]);
             cudaStreamWaitEvent(ctx->cur, ctx->gdone[g * NL + l], 0);
           }
           join_group(ctx, g);  // the released clients' last fc1 wgrad
-          const int ev = op_begin(ctx, PROTEA_OPC_FEDAVG);
-          k_release_acc<<<grid_for(P, 256), 256, 0, ctx->cur>>>(drecs, dtab + rel_by_group[t][g].first,
-                                                                 rel_by_group[t][g].second, P, loss_dev + g);
-          op_end(ctx, ev);
+          if (acc) {
+            ctx->op_bytes[PROTEA_OPC_FEDAVG] += (uint64_t)P * (20 + 4 * rel_by_group[t][g].second);
+            const int ev = op_begin(ctx, PROTEA_OPC_FEDAVG);
+            k_release_acc<<<grid_for(P, 256), 256, 0, ctx->cur>>>(drecs, dtab + rel_by_group[t][g].first,
+                                                                   rel_by_group[t][g].second, P, loss_dev + g);
+            op_end(ctx, ev);
+          }
+          if (observe) {  // the released clients' slots: highest byte touched during their whole lifetime
+            k_scan_poison<<<dim3(grid_for((int64_t)(max_slot / 16), 256, 2 * g_num_sms), rel_by_group[t][g].second),
+                            256, 0, ctx->cur>>>(ctx->arena, ctx->regions.p, dtab + rel_by_group[t][g].first,
+                                                ctx->hwm.p);
+            ctx->launches++;
+          }
         }
   }
   for (int g = 0; g < G; ++g) {
@@ -1553,6 +1732,17 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc, const float* 
   ctx->cur = ctx->stream;
   CK(cudaGetLastError());
   if (iters_out) *iters_out = T;
+  if (xx && xx->stats_out) {  // evaluate round: per input client (loss sum, correct), micro-clients summed
+    std::vector<float> st(3 * rc.size());
+    for (size_t i = 0; i < rc.size(); ++i)
+      CK(cudaMemcpyAsync(&st[3 * i], recs[i].stats, 12, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    xx->stats_out->assign(2 * rc_in.size(), 0.0);
+    for (size_t i = 0; i < rc.size(); ++i) {
+      (*xx->stats_out)[2 * rc[i].orig] += (double)st[3 * i];
+      (*xx->stats_out)[2 * rc[i].orig + 1] += (double)st[3 * i + 2];
+    }
+  }
   return PROTEA_OK;
 }
 
@@ -1611,10 +1801,11 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
       r.admit = a.admit;
       r.release = a.release;
       r.offset = a.offset;
+      r.slot = a.slot;
       if (a.gpu < 0 || a.gpu >= ctx->world) return fail(ctx, PROTEA_ERR_PLAN, who + ": gpu out of range");
       if (a.release != a.admit + r.S)
         return fail(ctx, PROTEA_ERR_PLAN, who + ": release - admit != S_k = " + std::to_string(r.S));
-      const uint64_t need = slot_layout(ctx->groups[c.model_id].m, r.B, r.n, r.E, e).total;
+      const uint64_t need = client_hwm(ctx->groups[c.model_id].m, r.B, r.n, r.E, e);
       if (a.slot < need)
         return fail(ctx, PROTEA_ERR_PLAN, who + ": slot " + std::to_string(a.slot) + " < HWM " + std::to_string(need));
       if (a.gpu == ctx->rank && (a.offset % kAlign != 0 || a.offset + a.slot > ctx->arena_bytes))
@@ -1624,6 +1815,14 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
       if (a.gpu == ctx->rank) all.push_back(r);
     }
     if (pa.size() != n) return fail(ctx, PROTEA_ERR_PLAN, "run_round: plan and client list differ");
+    if (opts->n_trace && (!opts->trace_ids || !opts->trace_bufs))
+      return fail(ctx, PROTEA_ERR_INVALID, "run_round: n_trace > 0 with null trace_ids / trace_bufs");
+    for (uint32_t i = 0; i < opts->n_trace; ++i) {
+      auto it = std::find_if(all.begin(), all.end(), [&](const RunClient& c) { return c.id == opts->trace_ids[i]; });
+      if (it == all.end() || !opts->trace_bufs[i] || !is_device_ptr(opts->trace_bufs[i]))
+        return fail(ctx, PROTEA_ERR_INVALID, "run_round: traced client " + std::to_string(opts->trace_ids[i]) +
+                                                 " is not one of this rank's clients or has no device buffer");
+    }
     // live slots pairwise disjoint on this GPU
     std::vector<RunClient*> byoff;
     for (auto& c : all) byoff.push_back(&c);
@@ -1632,7 +1831,7 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
       for (size_t j = i + 1; j < byoff.size(); ++j) {
         RunClient* a = byoff[i];
         RunClient* b = byoff[j];
-        const uint64_t aend = a->offset + slot_layout(ctx->groups[a->group].m, a->B, a->n, a->E, e).total;
+        const uint64_t aend = a->offset + client_hwm(ctx->groups[a->group].m, a->B, a->n, a->E, e);
         if (b->offset >= aend) break;
         if (a->admit < b->release && b->admit < a->release)
           return fail(ctx, PROTEA_ERR_PLAN, "run_round: clients " + std::to_string(a->id) + " and " +
@@ -1687,8 +1886,11 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
   const uint64_t l0 = ctx->launches;
   uint64_t iters = 0;
   double* loss_dev = ctx->acc.p + Ptot;  // per-group fp64 sums of step losses after the accumulators
+  ExecExtras xx;
+  xx.observe = opts->observe_hwm != 0;
+  for (uint32_t i = 0; i < opts->n_trace; ++i) xx.trace[opts->trace_ids[i]] = (uint8_t*)opts->trace_bufs[i];
   protea_status st =
-      execute(ctx, all, wg, ctx->acc.p, opts->lr, opts->seed, opts->round, opts->shuffle, &iters, loss_dev);
+      execute(ctx, all, wg, ctx->acc.p, opts->lr, opts->seed, opts->round, opts->shuffle, &iters, loss_dev, &xx);
   if (ctx->comm && !opts->partial_only) {
     // every rank reaches the exchange; one that failed inside execute() says so first (NCCL max of a flag)
     const uint64_t f0 = st == PROTEA_OK ? 0 : 1;
@@ -1787,8 +1989,13 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
   }
   std::vector<uint64_t> smns(all.size(), 0);
   if (!all.empty()) CK(cudaMemcpy(smns.data(), ctx->smns.p, all.size() * 8, cudaMemcpyDeviceToHost));
-  std::map<int64_t, uint64_t> sm_of;
+  std::map<int64_t, uint64_t> sm_of, hwm_of;
   for (size_t i = 0; i < all.size(); ++i) sm_of[all[i].id] = smns[i];
+  if (xx.observe && !all.empty()) {
+    std::vector<uint64_t> h(all.size(), 0);
+    CK(cudaMemcpy(h.data(), ctx->hwm.p, all.size() * 8, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < all.size(); ++i) hwm_of[all[i].id] = align256(h[i]);
+  }
   if (measured) {
     size_t k = 0;
     for (size_t i = 0; i < n; ++i) {
@@ -1797,7 +2004,9 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
       protea_profile& p = measured[k++];
       std::memset(&p, 0, sizeof(p));
       p.client_id = c.client_id;
-      p.peak_bytes = slot_layout(ctx->groups[c.model_id].m, c.batch, nn, c.epochs, e).total;
+      p.peak_bytes = client_hwm(ctx->groups[c.model_id].m, c.batch, nn, c.epochs, e);
+      auto ho = hwm_of.find(c.client_id);  // observe_hwm: this rank's clients report the observed mark
+      if (ho != hwm_of.end()) p.peak_bytes = ho->second;
       p.steps = (uint64_t)c.epochs * ceil_div((uint64_t)nn, (uint64_t)c.batch);
       p.flops = (uint64_t)c.epochs * nn * flops_per_sample(ctx->groups[c.model_id].m);
       p.uses_gpu = 1;
@@ -1848,7 +2057,7 @@ protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clien
     r.admit = 0;
     r.release = 1;
     r.offset = 0;
-    const uint64_t need = slot_layout(gr.m, r.B, r.n, r.E, e).total;
+    const uint64_t need = client_hwm(gr.m, r.B, r.n, r.E, e);
     if (need > ctx->arena_bytes)
       return fail(ctx, PROTEA_ERR_OOM, "profile_clients: probe slot of " + std::to_string(need) +
                                            " B exceeds the arena");
@@ -1872,13 +2081,97 @@ protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clien
     std::sort(times.begin(), times.end());
     class_ns[key] = (uint64_t)(times[times.size() / 2] * 1e6);
   }
+  // ---- observed high-water marks: every client runs ONE local step (admission with its E epoch
+  // permutations, one batch of min(B, n_k) rows) in a poisoned slot of the layout's size followed by a
+  // poisoned guard; clients are packed back to back, as many per lock-step probe as the arena holds
+  std::vector<uint64_t> observed(n, 0);
+  {
+    constexpr uint64_t kGuard = 4096;
+    std::vector<uint64_t> need(n);
+    for (size_t i = 0; i < n; ++i)
+      need[i] = client_hwm(ctx->groups[clients[i].model_id].m, clients[i].batch, ctx->shards[clients[i].client_id].n,
+                           clients[i].epochs, e);
+    int64_t Pmax = 0;
+    for (auto& g : ctx->groups) Pmax = std::max<int64_t>(Pmax, g.m.P);
+    size_t i0 = 0;
+    while (i0 < n) {
+      std::vector<RunClient> batch;
+      std::vector<size_t> idx;
+      std::vector<uint64_t> reg;
+      std::map<int64_t, int> ids_in;
+      uint64_t off = 0;
+      size_t i1 = i0;
+      while (i1 < n && off + need[i1] + kGuard <= ctx->arena_bytes) {
+        const protea_client& c = clients[i1];
+        if (ids_in.count(c.client_id)) break;  // one record per client id per probe
+        ids_in[c.client_id] = 1;
+        RunClient r;
+        r.id = c.client_id;
+        r.group = c.model_id;
+        r.n = ctx->shards[c.client_id].n;
+        r.B = c.batch;
+        r.E = c.epochs;
+        r.nb = (int)ceil_div((uint64_t)r.n, (uint64_t)r.B);
+        r.S = 1;
+        r.admit = 0;
+        r.release = 1;
+        r.offset = off;
+        r.slot = need[i1];
+        const uint64_t k2 = 2 * batch.size();  // (offset, bytes, output index): the slot, then its guard
+        reg.insert(reg.end(), {off, need[i1], k2, off + need[i1], kGuard, k2 + 1});
+        off += need[i1] + kGuard;
+        batch.push_back(r);
+        idx.push_back(i1);
+        ++i1;
+      }
+      if (batch.empty())
+        return fail(ctx, PROTEA_ERR_OOM, "profile_clients: client " + std::to_string(clients[i0].client_id) +
+                                             ": slot of " + std::to_string(need[i0]) + " B + guard exceeds the arena");
+      CK(cudaMemsetAsync(ctx->arena, PROTEA_POISON, off, ctx->stream));
+      CK(ctx->gin.reserve(Pmax));
+      CK(cudaMemsetAsync(ctx->gin.p, 0, Pmax * 4, ctx->stream));
+      // every group reads its global weights at gin + group offset - offset: zero weights for all
+      std::vector<RunClient> order(batch);
+      std::sort(order.begin(), order.end(), [](const RunClient& a, const RunClient& b) { return a.id < b.id; });
+      std::vector<std::vector<RunClient>> by_group(ctx->groups.size());
+      for (auto& r : order) by_group[r.group].push_back(r);
+      for (size_t g = 0; g < ctx->groups.size(); ++g) {
+        if (by_group[g].empty()) continue;
+        const float* wg = ctx->gin.p - ctx->groups[g].offset;
+        reset_ops(ctx, 0);
+        protea_status st = execute(ctx, by_group[g], wg, nullptr, 0.0f, 0, 0, 1, nullptr, nullptr);
+        if (st != PROTEA_OK) return st;
+      }
+      const size_t nreg = reg.size() / 3;
+      CK(ctx->regions.reserve(reg.size()));
+      CK(ctx->hwm.reserve(nreg));
+      CK(cudaMemcpyAsync(ctx->regions.p, reg.data(), reg.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaMemsetAsync(ctx->hwm.p, 0, nreg * 8, ctx->stream));
+      uint64_t max_reg = 0;
+      for (size_t k = 1; k < reg.size(); k += 3) max_reg = std::max(max_reg, reg[k]);
+      k_scan_poison<<<dim3(grid_for((int64_t)(max_reg / 16), 256, 2 * g_num_sms), (unsigned)nreg), 256, 0,
+                      ctx->stream>>>(ctx->arena, ctx->regions.p, nullptr, ctx->hwm.p);
+      CK(cudaGetLastError());
+      std::vector<uint64_t> h(nreg);
+      CK(cudaMemcpyAsync(h.data(), ctx->hwm.p, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      for (size_t k = 0; k < batch.size(); ++k) {
+        if (h[2 * k + 1])
+          return fail(ctx, PROTEA_ERR_OOM, "profile_clients: client " + std::to_string(batch[k].id) +
+                                               " wrote " + std::to_string(h[2 * k + 1]) +
+                                               " B past its slot (guard canary touched)");
+        observed[idx[k]] = align256(h[2 * k]);
+      }
+      i0 = i1;
+    }
+  }
   for (size_t i = 0; i < n; ++i) {
     const protea_client& c = clients[i];
     const int64_t nn = ctx->shards[c.client_id].n;
     protea_profile& p = out[i];
     std::memset(&p, 0, sizeof(p));
     p.client_id = c.client_id;
-    p.peak_bytes = slot_layout(ctx->groups[c.model_id].m, c.batch, nn, c.epochs, e).total;
+    p.peak_bytes = observed[i];
     p.steps = (uint64_t)c.epochs * ceil_div((uint64_t)nn, (uint64_t)c.batch);
     p.flops = (uint64_t)c.epochs * nn * flops_per_sample(ctx->groups[c.model_id].m);
     p.step_ns = class_ns[std::make_pair((int)c.model_id, (int)c.batch)];
@@ -2053,6 +2346,94 @@ protea_status protea_evaluate(protea_ctx* ctx, int32_t model_id, const float* we
     out->correct += ok[t];
   }
   out->n = (uint64_t)n;
+  return PROTEA_OK;
+}
+
+protea_status protea_evaluate_round(protea_ctx* ctx, const protea_client* clients, size_t n, const float* global,
+                                    size_t n_params, protea_eval_result* per_client, protea_eval_result* total) {
+  if (!ctx) return PROTEA_ERR_INVALID;
+  if (!clients || !global || !per_client || n == 0)
+    return fail(ctx, PROTEA_ERR_INVALID, "evaluate_round: null argument or n == 0");
+  int64_t Ptot = 0;
+  for (auto& g : ctx->groups) Ptot += g.m.P;
+  if ((int64_t)n_params != Ptot) return fail(ctx, PROTEA_ERR_DIM, "evaluate_round: n_params mismatch");
+  const int e = ctx->precision == PROTEA_PREC_FP32 ? 4 : 2;
+  std::map<int64_t, int> seen;
+  for (size_t i = 0; i < n; ++i) {
+    const protea_client& c = clients[i];
+    const std::string who = "evaluate_round: client " + std::to_string(c.client_id);
+    if (!seen.emplace(c.client_id, 1).second) return fail(ctx, PROTEA_ERR_INVALID, who + " listed twice");
+    if (c.model_id < 0 || c.model_id >= (int)ctx->groups.size())
+      return fail(ctx, PROTEA_ERR_INVALID, who + ": unknown model_id");
+    auto sh = ctx->val_shards.find(c.client_id);
+    if (sh == ctx->val_shards.end()) return fail(ctx, PROTEA_ERR_INVALID, who + ": no registered validation split");
+    if (sh->second.ymin < 0 || sh->second.ymax >= ctx->groups[c.model_id].m.classes)
+      return fail(ctx, PROTEA_ERR_INVALID, who + ": label outside [0, classes)");
+  }
+  CK(cudaSetDevice(ctx->device));
+  const float* wg = global;
+  if (!is_device_ptr(global)) {
+    CK(ctx->gin.reserve(Ptot));
+    CK(cudaMemcpyAsync(ctx->gin.p, global, Ptot * 4, cudaMemcpyHostToDevice, ctx->stream));
+    wg = ctx->gin.p;
+  }
+  // every client evaluates its group's global weights on its whole validation split: one lock-step
+  // "step" per batch of up to kMaxBatch rows (micro-clients above kMicroRows), slots packed back to back
+  // in the arena, as many clients per pass as it holds
+  size_t i0 = 0;
+  while (i0 < n) {
+    std::vector<RunClient> batch;
+    std::vector<size_t> idx;
+    uint64_t off = 0;
+    size_t i1 = i0;
+    while (i1 < n) {
+      const protea_client& c = clients[i1];
+      RunClient r;
+      r.id = c.client_id;
+      r.group = c.model_id;
+      r.n = ctx->val_shards[c.client_id].n;
+      r.B = (int)std::min<int64_t>(r.n, kMaxBatch);
+      r.E = 1;
+      r.nb = (int)ceil_div((uint64_t)r.n, (uint64_t)r.B);
+      r.S = r.nb;
+      r.admit = 0;
+      r.release = r.S;
+      const uint64_t need = client_hwm(ctx->groups[c.model_id].m, r.B, r.n, 1, e);
+      if (off + need > ctx->arena_bytes) break;
+      r.offset = off;
+      r.slot = need;
+      off += need;
+      batch.push_back(r);
+      idx.push_back(i1);
+      ++i1;
+    }
+    if (batch.empty())
+      return fail(ctx, PROTEA_ERR_OOM, "evaluate_round: client " + std::to_string(clients[i0].client_id) +
+                                           ": evaluation slot exceeds the arena");
+    ExecExtras xx;
+    xx.eval = true;
+    xx.shards = &ctx->val_shards;
+    std::vector<double> st;
+    xx.stats_out = &st;
+    reset_ops(ctx, 0);
+    protea_status s2 = execute(ctx, batch, wg, nullptr, 0.0f, 0, 0, 0, nullptr, nullptr, &xx);
+    if (s2 != PROTEA_OK) return s2;
+    for (size_t k = 0; k < batch.size(); ++k) {
+      protea_eval_result& r = per_client[idx[k]];
+      r.loss_sum = st[2 * k];
+      r.correct = (uint64_t)llround(st[2 * k + 1]);
+      r.n = (uint64_t)batch[k].n;
+    }
+    i0 = i1;
+  }
+  if (total) {
+    std::memset(total, 0, sizeof(*total));
+    for (size_t i = 0; i < n; ++i) {  // client order
+      total->loss_sum += per_client[i].loss_sum;
+      total->correct += per_client[i].correct;
+      total->n += per_client[i].n;
+    }
+  }
   return PROTEA_OK;
 }
 

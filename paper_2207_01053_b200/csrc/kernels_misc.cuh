@@ -7,15 +7,17 @@ namespace protea {
 // Admission (VCE stage (4): "another client in the round will be
 // spawned"): copy the group's global weights into the client's slot and zero
 // its stats.  blockIdx.y = admitted client, grid-stride over P.
-__global__ void k_admit_params(const ClientRec* __restrict__ recs, const int* __restrict__ ids) {
-  const ClientRec* c = recs + ids[blockIdx.y];
+// (also the micro-client broadcast after a merge: src = the merged weights, stats untouched)
+__device__ __forceinline__ void load_weights(const ClientRec* c, const float* __restrict__ src, bool admit) {
   const int64_t P = c->P;
   // group offsets in the global vector need not be 16-byte aligned: scalar, coalesced
   __nv_bfloat16* sh = (__nv_bfloat16*)c->buf[B_WSH];  // bf16 mode: tensor-core shadow
+  float* mw = admit ? c->mw : nullptr;                  // micro-client 0: the merge weights start as w_g
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    const float w = c->wg[i];
+    const float w = src[i];
     c->params[i] = w;
     if (sh) sh[i] = __float2bfloat16_rn(w);
+    if (mw) mw[i] = w;
   }
   __nv_bfloat16* w1q = (__nv_bfloat16*)c->buf[B_W1P];  // conv1 pool-quad shadow (common.h w1q_index), W1 at offset 0
   if (w1q) {
@@ -25,16 +27,161 @@ __global__ void k_admit_params(const ClientRec* __restrict__ recs, const int* __
       const int dy = (mh >> 1) / 3, dx = 2 * ((mh >> 1) % 3) + (mh & 1), q = n / C1, co = n - q * C1;
       const int ky = dy - (q >> 1), kx = dx - (q & 1);
       const bool in = (unsigned)ky < 5u && (unsigned)kx < 5u && ci < 3;
-      w1q[e] = __float2bfloat16_rn(in ? c->wg[co * 75 + (ky * 5 + kx) * 3 + ci] : 0.f);
+      w1q[e] = __float2bfloat16_rn(in ? src[co * 75 + (ky * 5 + kx) * 3 + ci] : 0.f);
     }
   }
   __nv_bfloat16* w0p = (__nv_bfloat16*)c->buf[B_R_W0P];  // ResNet conv0 [16][9][3] -> [16][9][8], W0 at offset 0
   if (w0p)
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 16 * 72; e += gridDim.x * blockDim.x) {
       const int ci = e & 7, tap = (e >> 3) % 9, co = e / 72;
-      w0p[e] = __float2bfloat16_rn(ci < 3 ? c->wg[co * 27 + tap * 3 + ci] : 0.f);
+      w0p[e] = __float2bfloat16_rn(ci < 3 ? src[co * 27 + tap * 3 + ci] : 0.f);
     }
-  if (blockIdx.x == 0 && threadIdx.x < 16) c->stats[threadIdx.x] = 0.f;
+  if (admit && blockIdx.x == 0 && threadIdx.x < 16) c->stats[threadIdx.x] = 0.f;
+}
+__global__ void k_admit_params(const ClientRec* __restrict__ recs, const int* __restrict__ ids) {
+  const ClientRec* c = recs + ids[blockIdx.y];
+  load_weights(c, c->wg, true);
+}
+
+// Micro-clients of one batch (common.h kMicroRows): list = [M recs][M rows], micro 0 first.  Every micro
+// took its SGD step from the same weights w (= mw of micro 0) with lr * kMicroLrScale (a power of two:
+// exact), so (w_m - w) / kMicroLrScale = -lr * (mean gradient over micro m's b_m rows) to fp32 rounding of
+// the SCALED step (relative eps, not ulp(w)); the merge forms, in fp64 and in micro order,
+//   w' = w + sum_m (b_m / R) (w_m - w) / kMicroLrScale,   R = sum_m b_m = |beta|,
+// = w - lr * (mean gradient over the whole batch), rounded once to fp32.
+// Block 0 also folds the micro-batch losses into micro 0's stats[0] (the batch-mean loss of the step).
+__global__ void k_micro_merge(const ClientRec* __restrict__ recs, const int* __restrict__ list, int M, int R) {
+  const ClientRec* c0 = recs + list[0];
+  float* mw = c0->mw;
+  const int64_t P = c0->P;
+  const double inv = 1.0 / ((double)kMicroLrScale * (double)R);
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < P; d += (int64_t)gridDim.x * blockDim.x) {
+    const double w = (double)mw[d];
+    double a = 0.0;
+    for (int m = 0; m < M; ++m) {
+      const int b = list[M + m];
+      if (b) a += (double)b * ((double)recs[list[m]].params[d] - w);
+    }
+    mw[d] = (float)(w + a * inv);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // stats[0] of micro 0 holds the client's running total (stats[1]) plus this step's micro-0 loss
+    float* s0 = c0->stats;
+    double step = (double)list[M] * ((double)s0[0] - (double)s0[1]);
+    for (int m = 1; m < M; ++m) {
+      float* sm = recs[list[m]].stats;
+      step += (double)list[M + m] * (double)sm[0];
+      sm[0] = 0.f;
+    }
+    s0[1] = (float)((double)s0[1] + step / (double)R);
+    s0[0] = s0[1];
+  }
+}
+// ... then every micro (blockIdx.y) reloads the merged weights (params, bf16 shadows)
+__global__ void k_micro_bcast(const ClientRec* __restrict__ recs, const int* __restrict__ list) {
+  const ClientRec* c = recs + list[blockIdx.y];
+  load_weights(c, recs[list[0]].mw, false);
+}
+
+// Observed arena high-water marks (Table 1 "VRAM" P:140-156, get_properties P:217: "how much
+// VRAM is the training making use of"; reading R2 = the peak).  A slot is filled with the poison
+// byte before the client is admitted; after it is released the highest byte of the slot that differs from
+// the poison bounds everything the client's kernels wrote.  regions: (byte offset in the arena, bytes,
+// output index) triples, 16-byte aligned; blockIdx.y = entry of `ids` (a region index; nullptr: identity).
+constexpr uint32_t kPoison4 = 0x01010101u * PROTEA_POISON;
+__global__ void k_fill_poison(uint8_t* __restrict__ arena, const uint64_t* __restrict__ regions,
+                              const int* __restrict__ ids) {
+  const int r = ids ? ids[blockIdx.y] : (int)blockIdx.y;
+  uint4* p = reinterpret_cast<uint4*>(arena + regions[3 * r]);
+  const uint64_t n16 = regions[3 * r + 1] / 16;
+  const uint4 v = make_uint4(kPoison4, kPoison4, kPoison4, kPoison4);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+// out[idx] = max(out[idx], 1 + offset of the highest non-poison byte of the region) (0: untouched)
+__global__ void __launch_bounds__(256) k_scan_poison(const uint8_t* __restrict__ arena,
+                                                     const uint64_t* __restrict__ regions, const int* __restrict__ ids,
+                                                     unsigned long long* __restrict__ out) {
+  const int r = ids ? ids[blockIdx.y] : (int)blockIdx.y;
+  const uint4* p = reinterpret_cast<const uint4*>(arena + regions[3 * r]);
+  const uint64_t n16 = regions[3 * r + 1] / 16;
+  unsigned long long best = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 v = p[i];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 3; k >= 0; --k)
+      if (w[k] != kPoison4) {  // little endian: the highest differing byte of word k
+        const int hb = (31 - __clz(w[k] ^ kPoison4)) >> 3;
+        best = max(best, (unsigned long long)(i * 16 + 4 * k + hb + 1));
+        break;
+      }
+  }
+  for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best) atomicMax(out + regions[3 * r + 2], best);
+}
+
+// Evaluate round (PAPER.md P:302 validation split, P:238 configure_evaluate / aggregate_evaluate): the
+// classifier head after the training path's forward kernels.  Per row r of the task: features g (the
+// stored activation row [F], or for ResNet-8 the global average over hw positions of [hw][F]), logits
+// z = W g + b (fp32), loss = logsumexp(z) - z[y], correct = (first maximum of z == y).  One CTA per task,
+// a warp per row; thread 0 adds the rows' losses and hits in row order to stats[0] / stats[2].
+constexpr int kEvalThreads = 256;
+template <typename T>
+__global__ void __launch_bounds__(kEvalThreads)
+    k_eval_head(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, int feat_buf, int F, int hw,
+                int64_t off_w, int64_t off_b, int C) {
+  __shared__ float g[kEvalThreads / 32][512];
+  __shared__ float z[kEvalThreads / 32][64];
+  __shared__ float loss_r[kMicroRows];
+  __shared__ int ok_r[kMicroRows];
+  const Task tk = tasks[blockIdx.x];
+  const ClientRec* c = recs + tk.rec;
+  const T* feat = (const T*)c->buf[feat_buf];
+  const float* W = c->params + off_w;
+  const float* bias = c->params + off_b;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < tk.rows; r += kEvalThreads / 32) {
+    for (int f = lane; f < F; f += 32) {
+      float a = 0.f;
+      for (int p = 0; p < hw; ++p) a += ldv(feat + ((int64_t)r * hw + p) * F + f);
+      g[warp][f] = hw > 1 ? a / (float)hw : a;
+    }
+    __syncwarp();
+    for (int k = 0; k < C; ++k) {
+      float a = 0.f;
+      for (int f = lane; f < F; f += 32) a = fmaf(W[(int64_t)k * F + f], g[warp][f], a);
+      for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0) z[warp][k] = a + bias[k];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int y = c->y[c->perm[tk.base + r]];
+      float m = z[warp][0];
+      int arg = 0;
+      for (int k = 1; k < C; ++k)
+        if (z[warp][k] > m) {
+          m = z[warp][k];
+          arg = k;
+        }
+      float se = 0.f;
+      for (int k = 0; k < C; ++k) se += expf(z[warp][k] - m);
+      loss_r[r] = logf(se) + m - z[warp][y];
+      ok_r[r] = arg == y;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float ls = 0.f;
+    int ok = 0;
+    for (int r = 0; r < tk.rows; ++r) {
+      ls += loss_r[r];
+      ok += ok_r[r];
+    }
+    c->stats[0] += ls;
+    c->stats[2] += (float)ok;
+  }
 }
 
 // Epoch permutation pi_{k,e} (reading R10): key_i = mix64(s + i*phi),

@@ -119,7 +119,9 @@ SlotLayout slot_layout(const ModelDims& m, int b, int64_t n, int epochs, int e) 
   put(B_PERM, 4 * (uint64_t)epochs * n);
   put(B_STATS, 64);
   if (e == 2) put(B_WSH, 2 * (uint64_t)m.P);  // bf16 shadow of the weights (tensor-core operands)
-  const uint64_t B = b;
+  // a batch holds min(B, n) rows (the last partial batch is kept): per-row buffers
+  // are sized for that many rows (a client with n < B never touches more; observed, tools/hwm_probe.py)
+  const uint64_t B = (uint64_t)std::min<int64_t>(b, n);
   if (m.arch == PROTEA_MODEL_MLP) {
     put(B_H1, B * 64 * e);
     put(B_DZ1, B * 64 * e);
@@ -144,19 +146,29 @@ SlotLayout slot_layout(const ModelDims& m, int b, int64_t n, int epochs, int e) 
     put(B_R_O2, B * 256 * 32 * e);
     put(B_R_R3, B * 64 * 64 * e);
     put(B_R_O3, B * 64 * 64 * e);
-    put(B_R_GAP, B * 64 * e);
-    put(B_R_DGAP, B * 64 * 4);
+    put(B_R_DGAP, B * 64 * 4);  // (the pooled features stay in the head kernel: no gap buffer)
     put(B_R_G0, B * 1024 * 16 * e);
     put(B_R_G1, B * 1024 * 16 * e);
     put(B_R_G2, B * 1024 * 16 * e);
     if (e == 2) put(B_R_W0P, 16 * 9 * 8 * 2);  // conv0 weight shadow padded to 8 input channels
     if (e == 2) put(B_R_XS, B * 1024 * 8 * 2);  // conv0 input staged for the tensor cores
   }
+  // conv weight-gradient split partials: cout rows of K+1 fp32 (K weights + the bias column) per split
   uint64_t wsp = 0;
-  for (const Layer& l : m.layers)
-    if (l.kind == 0)  // rows of K+1 partials padded to a multiple of 4 floats (16-byte aligned)
-      wsp = std::max<uint64_t>(wsp, 4ull * splits_for(l, b) * l.cout * ((l.K() + 1 + 3) / 4 * 4));
-  if (m.arch == PROTEA_MODEL_RESNET8) wsp = 4ull * r8_wsp_off(7, b);  // a region per layer (sum, not max)
+  const int rows = (int)B;
+  if (m.arch == PROTEA_MODEL_RESNET8) {
+    // a region per layer (all kept until the step's merged SGD reduce), regions placed at row pitch
+    // ceil4(K+1) (r8_wsp_off); the last layer's rows are written at pitch K+1, so its last row ends the slot
+    wsp = 4ull * ((uint64_t)r8_wsp_off(6, rows) + (uint64_t)splits_for(m.layers[6], rows) * 64 * (9 * 64 + 1));
+  } else if (m.arch == PROTEA_MODEL_CNN && e == 2 && m.width_q == 4) {
+    // width 1, bf16: conv1's partials live in dz2 (k_conv1_wgrad_q); conv2 writes partials (row pitch
+    // ceil4(K+1) = 804) only when a client's rows need more than one split, else it updates from TMEM
+    const int s2 = splits_for(m.layers[1], rows);
+    if (s2 > 1) wsp = 4ull * s2 * m.c2 * ((m.layers[1].K() + 1 + 3) / 4 * 4);
+  } else {
+    for (const Layer& l : m.layers)  // one region reused layer by layer (max), rows at pitch K+1
+      if (l.kind == 0) wsp = std::max<uint64_t>(wsp, 4ull * splits_for(l, rows) * l.cout * (l.K() + 1));
+  }
   if (wsp) put(m.arch == PROTEA_MODEL_RESNET8 ? B_R_WSP : B_WSP, wsp);
   // slot order = enum order except that the wgrad partials come last (oracle order)
   uint64_t off = 0;
@@ -172,6 +184,15 @@ SlotLayout slot_layout(const ModelDims& m, int b, int64_t n, int epochs, int e) 
     }
   s.total = off;
   return s;
+}
+
+uint64_t client_hwm(const ModelDims& m, int batch, int64_t n, int epochs, int e) {
+  const int64_t b = std::min<int64_t>(batch, n);
+  if (b <= kMicroRows) return slot_layout(m, batch, n, epochs, e).total;
+  uint64_t tot = 0;
+  for (int64_t r0 = 0; r0 < b; r0 += kMicroRows)
+    tot += slot_layout(m, (int)std::min<int64_t>(kMicroRows, b - r0), n, epochs, e).total;
+  return tot + align256(4 * (uint64_t)m.P);  // merge weights
 }
 
 }  // namespace protea

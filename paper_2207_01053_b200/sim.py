@@ -7,9 +7,9 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import (PREC_FP32, POLICY_PROFILED, ORDER_ASC_ID, clients_array, protea_evaluate, protea_finalize,
-               protea_init, protea_plan, protea_profile_clients, protea_register_model, protea_register_shards,
-               protea_run_round)
+from . import (PREC_FP32, POLICY_PROFILED, ORDER_ASC_ID, clients_array, protea_evaluate, protea_evaluate_round,
+               protea_finalize, protea_init, protea_plan, protea_profile_clients, protea_register_model,
+               protea_register_shards, protea_register_val_shards, protea_run_round)
 
 
 class Simulation:
@@ -37,6 +37,13 @@ class Simulation:
     def register_shards(self, shards):
         protea_register_shards(self.ctx, shards)
 
+    def register_val_shards(self, shards):
+        protea_register_val_shards(self.ctx, shards)
+
+    def evaluate_round(self, clients, global_w):
+        """Evaluate round: per-client (loss_sum, correct, n) records and their totals."""
+        return protea_evaluate_round(self.ctx, clients, global_w)
+
     @staticmethod
     def clients(rows):
         return clients_array(rows)
@@ -50,11 +57,11 @@ class Simulation:
         return protea_plan(profiles, caps, policy, order, margin_permille, max_active)
 
     def run_round(self, clients, plan, global_in, global_out=None, lr=0.05, seed=0, rnd=0, shuffle=True,
-                  measured=False, time_ops=0, partial_only=False, serialize=False):
+                  measured=False, time_ops=0, partial_only=False, serialize=False, observe_hwm=False, trace=None):
         if global_out is None:
             global_out = self.torch.empty_like(global_in)
         r = protea_run_round(self.ctx, clients, plan, global_in, global_out, lr, seed, rnd, shuffle, measured,
-                             time_ops, partial_only, serialize)
+                             time_ops, partial_only, serialize, observe_hwm, trace)
         return global_out, r
 
     def evaluate(self, model_id, weights, x, y):

@@ -125,6 +125,23 @@ def make_shard(templates: np.ndarray, n: int, client_id: int, seed: int = 0):
     return x, y
 
 
+def val_size(n_train: int) -> int:
+    """Validation split of a client with n_train training examples: 10 % of its data, the
+    configs' shard sizes being the training part (SURVEY §8(c).1 ambiguities): round(n_train / 9), >= 1."""
+    return max(1, int(round(n_train / 9)))
+
+
+def make_val_shard(templates: np.ndarray, n_train: int, client_id: int, seed: int = 0):
+    """The client's validation split: same class templates and noise model as its training shard, its own
+    PCG64 stream."""
+    n = val_size(n_train)
+    classes, D = templates.shape
+    rng = np.random.Generator(np.random.PCG64([0x5A56, seed, client_id]))
+    y = rng.integers(0, classes, size=n).astype(np.int32)
+    x = np.clip(np.rint(templates[y] + 32.0 * rng.standard_normal((n, D))), 0, 255).astype(np.uint8)
+    return x, y
+
+
 def sample_clients(pool: int, k: int, seed: int, rnd: int) -> np.ndarray:
     """Uniform sample without replacement, sorted ascending (SPEC D-14)."""
     if k > pool:

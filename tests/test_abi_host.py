@@ -111,7 +111,8 @@ MODELS = [(pb.MODEL_MLP, 4, 28, 28, 1), (pb.MODEL_CNN, 1, 32, 32, 3), (pb.MODEL_
 def test_footprint_matches_oracle(arch, wq, H, W, C):
     rng = random.Random(arch * 10 + wq)
     for _ in range(60):
-        n, b, e = rng.randint(1, 2000), rng.randint(1, 64), rng.randint(1, 3)
+        n, e = rng.randint(1, 2500), rng.randint(1, 3)
+        b = rng.randint(1, 64) if rng.random() < 0.6 else rng.choice([65, 100, 128, 500, 1024, 2048])
         for prec, eb in ((pb.PREC_FP32, 4), (pb.PREC_BF16, 2)):
             peak, steps, flops = pb.protea_client_footprint(arch, wq, 10, H, W, C, n, b, e, prec)
             assert peak == pf.hwm_bytes(arch, wq, 10, b, n, e, eb)

@@ -45,20 +45,23 @@ def test_bf16_round_config2_reduced(torch):
 
 @pytest.mark.parametrize("B", [8, 16, 64])
 def test_bf16_one_step_vs_bf16_emulated_oracle(torch, B):
-    """Kernel-correctness diagnostic: one local step (n = B, E = 1)
-    against the oracle rounding to bf16 at exactly the points the CUDA path
-    stores bf16 (reading R17).  The update agrees to ~1e-4 while a
-    dropped term or a wrong operand is off by >5%.  Over many steps the bf16
-    gradient's sensitivity to rounding (the f64 vs bf16 gap is already 4-7% per
-    step, cancellation over all-positive inputs) makes the comparison chaotic,
-    so only the single step is gated tightly."""
+    """Kernel-correctness diagnostic: one local step (n = B, E = 1) of three clients
+    against the oracle rounding to bf16 at exactly the points the CUDA path stores bf16 (DESIGN.md
+    reading R17), teacher forced (tests/teacher_forced.py): the step starts from the GPU's weights, takes
+    the GPU's ReLU / pool decisions where they are within rounding of the oracle's, and both sides hold
+    the result as fp32 master weights.  Bar 1e-3 on the update (a dropped term or a wrong operand is off
+    by > 5 %).  The earlier un-forced comparison of the FedAvg'd round update (2.7e-3) mixed in pool
+    argmax flips and the fp32 rounding of the new weights."""
+    from tests.teacher_forced import bench_round_with_trace, gpu_weights, oracle_updates, per_step_rel
     wl = synth.build_workload(2, n_clients=3, samples=B, epochs=1)
     for c in wl.clients:
         c.batch = B
-    got, ex = gpu_run(wl, precision=1)
-    emu = oracle_run(wl, emulate_bf16=True)
-    d = rel_l2(got[4] - ex["g0"][4], emu[4] - ex["g0"][4])
-    assert d <= 5e-3, d
+    ids = [c.id for c in wl.clients]
+    snaps, _, _ = bench_round_with_trace(wl, 1, ids)
+    for cid in ids:
+        upd, _ = oracle_updates(wl, cid, snaps[cid], 2, emulate_bf16=True, tol=1e-3)
+        tot, _ = per_step_rel(wl, cid, gpu_weights(wl, cid, snaps[cid], 2), upd)
+        assert tot.max() <= 1e-3, (cid, float(tot.max()))
 
 
 def test_bf16_mixed_widths(torch):
@@ -87,15 +90,18 @@ def _resnet_one_step(B, k=3, epochs=1):
 
 @pytest.mark.parametrize("B", [8, 64])
 def test_resnet8_bf16_one_step_vs_bf16_emulated_oracle(torch, B):
-    """ResNet-8 convs 1-6 on tcgen05 (kernels_resnet_tc.cuh): one local step against the oracle
-    rounding to bf16 where the CUDA bf16 path stores bf16 (activations, gradients, the weight
-    shadow of convs 1-6; reading R17).  B = 64 spans several 128-row tiles, 2048-pixel
-    wgrad splits and the stride-2 / option-A blocks."""
+    """ResNet-8 convs on tcgen05 (kernels_resnet_tc.cuh): one local step against the oracle rounding to
+    bf16 where the CUDA bf16 path stores bf16 (activations, gradients, the weight shadow; DESIGN.md
+    reading R17), teacher forced like the CNN test above, bar 1e-3.  B = 64 spans several 128-row
+    tiles, 2048-pixel wgrad splits and the stride-2 / option-A blocks."""
+    from tests.teacher_forced import bench_round_with_trace, gpu_weights, oracle_updates, per_step_rel
     wl = _resnet_one_step(B)
-    got, ex = gpu_run(wl, precision=1)
-    emu = oracle_run(wl, emulate_bf16=True)
-    d = rel_l2(got[4] - ex["g0"][4], emu[4] - ex["g0"][4])
-    assert d <= 5e-3, d
+    ids = [c.id for c in wl.clients]
+    snaps, _, _ = bench_round_with_trace(wl, 1, ids)
+    for cid in ids:
+        upd, _ = oracle_updates(wl, cid, snaps[cid], 2, emulate_bf16=True, tol=1e-3)
+        tot, _ = per_step_rel(wl, cid, gpu_weights(wl, cid, snaps[cid], 2), upd)
+        assert tot.max() <= 1e-3, (cid, float(tot.max()))
 
 
 def test_resnet8_bf16_two_epochs_vs_oracle(torch):
@@ -176,17 +182,14 @@ def _partial(wl, ids, w0):
     return out, sum(c.n for c in cl)
 
 
-def test_config2_full_size(torch):
+def test_config2_full_size_client_independence(torch):
     """BASELINE configs[1] at full size (100 clients x 500 samples, E = 2, 5,950 client-steps), in the
-    bench's bf16 launch configuration.  (1) Client independence at full size: the fp64 FedAvg partial of
-    the whole cohort equals the sum of the partials of its two halves (the same lock-step kernels run
-    over different co-scheduled clients).  (2) Sampled clients against the float64 oracle over the full
-    local horizon (a B = 8 client: 126 steps; a B = 64 client: ragged last batch of 52).  Over that many
-    steps the ReLU-mask / max-pool decisions have margins below fp32 rounding (tools/
-    decision_margin_probe.py: down to 3e-8 of the layer scale), so even the fp32 verify path separates
-    from float64 (1.6e-2 on the B = 8 client, tools/full_size_probe.py) while the oracle itself is
-    well-conditioned (tools/conditioning_probe.py); the per-step bar is held by the one-step tests.
-    Long-horizon bar here: 5e-2 (measured 2.1e-2)."""
+    bench's bf16 launch configuration: the fp64 FedAvg partial of the whole cohort equals the sum of the
+    partials of its two halves (the same lock-step kernels run over different co-scheduled clients, so a
+    client's arithmetic does not depend on its neighbours).  Full-size parity against the oracle at the
+    north-star bars is tests/test_gpu_teacher_forced.py (every step of a B = 8 and a B = 64 client of
+    this cohort); the global weights of the full cohort beside float32 / bf16-emulation controls are
+    reported by tools/global_controls.py."""
     wl = synth.build_workload(2)
     w0 = synth.init_weights(wl.model)
     ids = [c.id for c in wl.clients]
@@ -194,13 +197,6 @@ def test_config2_full_size(torch):
     a, _ = _partial(wl, set(ids[:50]), w0)
     b, _ = _partial(wl, set(ids[50:]), w0)
     assert np.linalg.norm(full - (a + b)) <= 1e-12 * np.linalg.norm(full)
-    sample = {0, 3}  # B = 8 and B = 64
-    part, N = _partial(wl, sample, w0)
-    got = w0.astype(np.float64) + part / N
-    from oracle import round as orr
-    ref = orr.run_round([c for c in wl.clients if c.id in sample], wl.shards, {4: w0}, wl.lr, wl.seed, 0,
-                        workers=2)[4]
-    assert rel_l2(got, ref) <= 5e-2
 
 
 def test_deferred_conv2_reduce_bitwise(torch):

@@ -24,7 +24,7 @@ def _data(model, n, seed, classes=10):
     return x, y
 
 
-@pytest.mark.parametrize("model,wq", [(sgd.MLP, 4), (sgd.CNN, 1), (sgd.CNN, 4)])
+@pytest.mark.parametrize("model,wq", [(sgd.MLP, 4), (sgd.CNN, 1), (sgd.CNN, 4), (sgd.RESNET8, 4)])
 def test_logits_vs_torch(model, wq):
     w = synth.init_weights(model, wq, 10, seed=3).astype(np.float64)
     x, _ = _data(model, 5, 1)
@@ -33,7 +33,7 @@ def test_logits_vs_torch(model, wq):
     assert np.max(np.abs(z - zt)) <= 1e-12 * max(1.0, np.max(np.abs(zt)))
 
 
-@pytest.mark.parametrize("model", [sgd.MLP, sgd.CNN])
+@pytest.mark.parametrize("model", [sgd.MLP, sgd.CNN, sgd.RESNET8])
 def test_loss_equals_training_loss(model):
     w = synth.init_weights(model, 4, 10, seed=5).astype(np.float64)
     x, y = _data(model, 7, 2)
@@ -49,3 +49,17 @@ def test_zero_weights_closed_form():
     loss_sum, correct, n = oev.evaluate(w, sgd.CNN, 1, 10, x, y)
     assert abs(loss_sum - 6 * math.log(10)) <= 1e-12
     assert correct == int(np.sum(y == 0))
+
+
+def test_evaluate_round_is_the_per_client_sum():
+    """evaluate_round = each client's evaluate() on its own split with its group's weights; totals = sums."""
+    wl = synth.build_workload(4, k=6, samples=20)
+    tmpl = synth.class_templates(wl.shape, wl.classes, wl.seed)
+    val = {c.id: synth.make_val_shard(tmpl, c.n, c.id, wl.seed) for c in wl.clients}
+    g = {q: synth.init_weights(sgd.CNN, q, 10, seed=q).astype(np.float64) for q in (1, 2, 4)}
+    per, tot = oev.evaluate_round(wl.clients, val, g)
+    for c in wl.clients:
+        x, y = val[c.id]
+        assert per[c.id] == oev.evaluate(g[c.width_q], sgd.CNN, c.width_q, 10, x.reshape(-1, 32, 32, 3), y)
+        assert per[c.id][2] == synth.val_size(c.n) == max(1, round(c.n / 9))
+    assert tot[2] == sum(v[2] for v in per.values()) and tot[1] == sum(v[1] for v in per.values())
