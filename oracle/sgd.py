@@ -242,12 +242,23 @@ def bf16(x):
     return r.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
+def bf16_rz(x):
+    """The upper 16 bits of the float32 value (round toward zero to bfloat16), as float64.
+
+    The CUDA bf16 mode keeps the CNN's fc1 weights as the fp32 master split into two 16-bit planes and
+    feeds the tensor cores the high plane (reading R17): this is that operand."""
+    f = np.asarray(x, dtype=np.float32)
+    u = f.view(np.uint32) & np.uint32(0xFFFF0000)
+    return u.view(np.float32).astype(np.float64)
+
+
 def loss_and_grad(p, model, xb, yb, emulate_bf16=False, decisions=None, tol=0.0):
     """xb float64 [nb, H, W, C] in [0,1]; returns (loss, grads dict).
 
     emulate_bf16: round to bf16 exactly where the CUDA bf16 mode stores bf16
     (pooled / hidden activations, dh, the pre-activation gradients dz, and the
-    conv2 / fc1 weights read by the tensor cores; ResNet-8: every stored
+    conv2 weights read by the tensor cores; the fc1 weights are truncated to their upper
+    16 bits, bf16_rz, the operand the split-plane master gives; ResNet-8: every stored
     activation and gradient, the staged input and every conv's weights); everything else
     float64.
 
@@ -276,7 +287,8 @@ def loss_and_grad(p, model, xb, yb, emulate_bf16=False, decisions=None, tol=0.0)
         g["fc1.W"] = q(dz1).T @ x
         return loss, g
     if model == CNN:
-        W2q, W3q = q(p["conv2.W"]), q(p["fc1.W"])
+        W2q = q(p["conv2.W"])
+        W3q = bf16_rz(p["fc1.W"]) if emulate_bf16 else p["fc1.W"]  # fc1: the hi plane of the fp32 master
         z1, cols1 = conv_fwd(q(xb), q(p["conv1.W"]), p["conv1.b"], 1, 2)
         if dec is None:
             a1, arg1 = pool2_fwd(relu(z1))

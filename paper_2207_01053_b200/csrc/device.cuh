@@ -26,7 +26,36 @@ struct ClientRec {
   uint64_t* sm_ns;         // per-client device-time attribution (nullable)
   const void* tmaps;       // bf16 CNN: TM_COUNT CUtensorMaps (128 B each, global memory), else nullptr
   float* mw;               // micro-client 0 of a batch > kMicroRows: the merge weights (P fp32), else nullptr
+  // fp32 master weights [sp_off, sp_off + sp_len) stored as two 16-bit planes (bf16-mode CNN: fc1's W, the
+  // HBM-bound weight stream): hi = the upper half of each fp32 (= the tensor-core operand, read by fc1 fwd /
+  // dgrad through TMA), lo = the lower half, hi plane at params + sp_off, lo plane right after it.  The
+  // fp32 value is exactly (hi << 16 | lo); nothing else stores those weights (DESIGN.md §5 "split planes").
+  int64_t sp_off, sp_len;
 };
+
+__device__ __forceinline__ float split_join(uint16_t hi, uint16_t lo) {
+  return __uint_as_float(((uint32_t)hi << 16) | lo);
+}
+// master weight d of client c (either representation)
+__device__ __forceinline__ float master_w(const ClientRec* c, int64_t d) {
+  const uint64_t i = (uint64_t)(d - c->sp_off);
+  if (i < (uint64_t)c->sp_len) {
+    const uint16_t* hi = reinterpret_cast<const uint16_t*>(c->params + c->sp_off);
+    return split_join(hi[i], hi[c->sp_len + i]);
+  }
+  return c->params[d];
+}
+__device__ __forceinline__ void set_master_w(const ClientRec* c, int64_t d, float w) {
+  const uint64_t i = (uint64_t)(d - c->sp_off);
+  if (i < (uint64_t)c->sp_len) {
+    uint16_t* hi = reinterpret_cast<uint16_t*>(c->params + c->sp_off);
+    const uint32_t u = __float_as_uint(w);
+    hi[i] = (uint16_t)(u >> 16);
+    hi[c->sp_len + i] = (uint16_t)(u & 0xFFFFu);
+    return;
+  }
+  c->params[d] = w;
+}
 
 // One active client in one lock-step iteration.
 struct Task {

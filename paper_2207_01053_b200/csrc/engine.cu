@@ -185,7 +185,7 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
   const uint64_t C1 = m.c1, C2 = m.c2, F = m.f, K1 = 64 * C2, Bk = B, R = (B + 15) & ~15;
   const uint8_t* wsh = (const uint8_t*)r.buf[B_WSH];
   const void* w2 = wsh + 2 * m.layers[1].off_w;
-  const void* w3 = wsh + 2 * m.layers[2].off_w;
+  const void* w3 = (const uint8_t*)r.buf[B_PARAMS] + 4 * m.layers[2].off_w;  // fc1 W: hi split plane
   bool ok = true;
   {
     const uint64_t d[4] = {C1, 16, 16, Bk}, st[3] = {C1 * 2, 32 * C1, 512 * C1};
@@ -1405,6 +1405,10 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const floa
     r.n = (int32_t)c.n;
     r.B = c.cap;  // rows a batch can hold here: the slot's per-row buffer capacity
     r.mw = c.mw_off ? (float*)(ctx->arena + c.mw_off) : nullptr;
+    if (tc_mode && gr.m.arch == PROTEA_MODEL_CNN) {  // fc1's W as split planes (device.cuh)
+      r.sp_off = gr.m.layers[2].off_w;
+      r.sp_len = (int64_t)gr.m.layers[2].cout * gr.m.layers[2].K();
+    }
     r.E = c.E;
     r.nb = c.nb;
     r.id = c.id;

@@ -15,8 +15,12 @@ __device__ __forceinline__ void load_weights(const ClientRec* c, const float* __
   float* mw = admit ? c->mw : nullptr;                  // micro-client 0: the merge weights start as w_g
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     const float w = src[i];
-    c->params[i] = w;
-    if (sh) sh[i] = __float2bfloat16_rn(w);
+    if ((uint64_t)(i - c->sp_off) < (uint64_t)c->sp_len) {
+      set_master_w(c, i, w);  // split planes: the hi plane is the tensor-core operand (no shadow)
+    } else {
+      c->params[i] = w;
+      if (sh) sh[i] = __float2bfloat16_rn(w);
+    }
     if (mw) mw[i] = w;
   }
   __nv_bfloat16* w1q = (__nv_bfloat16*)c->buf[B_W1P];  // conv1 pool-quad shadow (common.h w1q_index), W1 at offset 0
@@ -60,7 +64,7 @@ __global__ void k_micro_merge(const ClientRec* __restrict__ recs, const int* __r
     double a = 0.0;
     for (int m = 0; m < M; ++m) {
       const int b = list[M + m];
-      if (b) a += (double)b * ((double)recs[list[m]].params[d] - w);
+      if (b) a += (double)b * ((double)master_w(recs + list[m], d) - w);
     }
     mw[d] = (float)(w + a * inv);
   }
@@ -243,6 +247,15 @@ __global__ void __launch_bounds__(256) k_release_acc(const ClientRec* __restrict
     for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < P; d += (int64_t)gridDim.x * blockDim.x) {
       double a = c0->acc[d];
       const double g = (double)c0->wg[d];
+      const uint64_t si = (uint64_t)(d - c0->sp_off);  // split-plane weights (same layout for every client)
+      if (si < (uint64_t)c0->sp_len) {
+        for (int i = 0; i < nc; ++i) {
+          const uint16_t* hi = reinterpret_cast<const uint16_t*>(prm[i] + c0->sp_off);
+          a += wn[i] * ((double)split_join(hi[si], hi[c0->sp_len + si]) - g);
+        }
+        c0->acc[d] = a;
+        continue;
+      }
       int i = 0;
       for (; i + 4 <= nc; i += 4) {  // four independent loads in flight, accumulated in order
         const float p0 = prm[i][d], p1 = prm[i + 1][d], p2 = prm[i + 2][d], p3 = prm[i + 3][d];

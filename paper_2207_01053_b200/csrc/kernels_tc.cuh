@@ -545,7 +545,7 @@ struct TcFc1Fwd {
   }
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
   __device__ PA a_pre(const TcTile& t, int i, int j) const {
-    return PA{(const bf16*)t.c->buf[B_WSH] + d.w3 + (int64_t)(t.m0 + i) * W::K1 + 8 * j};
+    return PA{reinterpret_cast<const bf16*>(t.c->params + d.w3) + (int64_t)(t.m0 + i) * W::K1 + 8 * j};  // hi plane
   }
   __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const { return s.p + kb * 64; }
   __device__ PB b_pre(const TcTile& t, int i, int j) const {
@@ -580,7 +580,7 @@ struct TcFc1Dgrad {
   }
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
   __device__ PA a_pre(const TcTile& t, int i, int j) const {
-    return PA{(const bf16*)t.c->buf[B_WSH] + d.w3 + (int64_t)i * W::K1 + t.m0 + 8 * j};
+    return PA{reinterpret_cast<const bf16*>(t.c->params + d.w3) + (int64_t)i * W::K1 + t.m0 + 8 * j};  // hi plane
   }
   __device__ const void* a_src(const TcTile& t, const PA& s, int kb) const { return s.p + (int64_t)kb * 64 * W::K1; }
   __device__ PB b_pre(const TcTile& t, int i, int j) const {
@@ -643,19 +643,25 @@ struct TcFc1Wgrad {  // M = K1 (input features), N = F (outputs), K = rows; W <-
     return PB{i < t.tk.rows && n < W::F ? (const bf16*)t.c->buf[B_DH] + (int64_t)i * W::F + n : nullptr};
   }
   __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const { return s.p; }
+  // SGD on the fp32 master held as split planes (device.cuh): read hi + lo (4 B), write hi + lo (4 B) —
+  // exactly SURVEY §8(d)'s 8 B per weight per client-step; the new hi plane is next step's operand
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
     const int k1 = t.m0 + row;
-    float* P = t.c->params + d.w3 + k1;
-    bf16* S = (bf16*)t.c->buf[B_WSH] + d.w3 + k1;
+    constexpr int64_t NW = (int64_t)W::F * W::K1;
+    uint16_t* H = reinterpret_cast<uint16_t*>(t.c->params + d.w3) + k1;
+    uint16_t* L = H + NW;
     const int64_t f0 = t.n0 + c0;
-    float w[16];
+    uint16_t h[16], l[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) w[j] = P[(f0 + j) * W::K1];  // 16 independent loads in flight
+    for (int j = 0; j < 16; ++j) {  // 32 independent loads in flight
+      h[j] = H[(f0 + j) * W::K1];
+      l[j] = L[(f0 + j) * W::K1];
+    }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const float nw = w[j] - lr * v[j];
-      P[(f0 + j) * W::K1] = nw;
-      S[(f0 + j) * W::K1] = __float2bfloat16_rn(nw);
+      const uint32_t u = __float_as_uint(split_join(h[j], l[j]) - lr * v[j]);
+      H[(f0 + j) * W::K1] = (uint16_t)(u >> 16);
+      L[(f0 + j) * W::K1] = (uint16_t)(u & 0xFFFFu);
     }
   }
 };

@@ -43,6 +43,21 @@ def _act(raw, off, size, elem, shape):
     return v.astype(np.float64).reshape(shape)
 
 
+def master_weights(c, raw, elem):
+    """The fp32 master weights at the start of a slot snapshot.  bf16-mode CNN: fc1's W is stored as two
+    16-bit planes (hi = upper halves, then lo) in its fp32 region (DESIGN.md §5 "split planes")."""
+    P = sgd.n_params(c.model, c.width_q, c.classes)
+    w = raw[:4 * P].copy().view(np.float32)
+    if elem == 2 and c.model == sgd.CNN:
+        c1, c2, f = sgd.cnn_channels(c.width_q)
+        off = (c1 * 75 + c1) + (c2 * 25 * c1 + c2)
+        nw = f * 64 * c2
+        planes = raw[4 * off:4 * (off + nw)].view(np.uint16)
+        u = (planes[:nw].astype(np.uint32) << 16) | planes[nw:].astype(np.uint32)
+        w[off:off + nw] = u.view(np.float32)
+    return w
+
+
 def decode_snapshot(c, raw, elem, rows):
     """(fp32 weights, GPU decisions of the step that produced the snapshot) from one slot snapshot.  A
     batch of more than 64 rows runs as micro-clients (slots of <= 64 rows back to back):
@@ -62,8 +77,7 @@ def decode_snapshot(c, raw, elem, rows):
             off += size
         return w, {k: np.concatenate([d[k] for d in parts]) for k in parts[0]}
     lay = slot_offsets(c, elem)
-    P = sgd.n_params(c.model, c.width_q, c.classes)
-    w = raw[:4 * P].view(np.float32)
+    w = master_weights(c, raw, elem)
     B = b  # per-row buffers hold min(B, n) rows (slot layout)
     dec = {}
     if c.model == sgd.MLP:
@@ -159,8 +173,7 @@ def oracle_updates(wl, cid, snaps, elem, emulate_bf16=False, tol=None, lr=None, 
 
 def gpu_weights(wl, cid, snaps, elem):
     c = next(c for c in wl.clients if c.id == cid)
-    P = sgd.n_params(c.model, c.width_q, c.classes)
-    return snaps[:, :4 * P].copy().view(np.float32)
+    return np.stack([master_weights(c, s, elem) for s in snaps])
 
 
 def per_step_rel(wl, cid, wsnaps, upd_oracle):

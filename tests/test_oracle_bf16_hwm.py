@@ -57,6 +57,22 @@ def test_bf16_rne_matches_torch_bitwise():
     assert sgd.bf16(np.float32(1 + 3 * 2**-8)) == 1 + 2**-6
 
 
+def test_bf16_rz_is_the_upper_half():
+    """bf16_rz (the fc1 split-plane operand) = the float32's upper 16 bits: torch's int32 view masked,
+    the value's magnitude never grows, and (hi << 16 | lo) rebuilds every float32 exactly."""
+    import torch
+    rng = np.random.default_rng(3)
+    bits = rng.integers(0, 2**32, size=1_000_000, dtype=np.uint64).astype(np.uint32)
+    f = bits.view(np.float32)
+    got = sgd.bf16_rz(f).astype(np.float32).view(np.uint32)
+    ref = (torch.from_numpy(bits.view(np.int32)) & torch.tensor(-65536, dtype=torch.int32)).numpy().view(np.uint32)
+    fin = np.isfinite(f)
+    assert np.array_equal(got[fin], ref[fin])
+    assert np.all(np.abs(sgd.bf16_rz(f[fin])) <= np.abs(f[fin].astype(np.float64)))
+    hi, lo = (bits >> 16).astype(np.uint32), (bits & 0xFFFF).astype(np.uint32)
+    assert np.array_equal(((hi << 16) | lo), bits)
+
+
 def _tiny_inputs(model, nb, seed):
     rng = np.random.default_rng(seed)
     H, W, C = sgd.input_shape(model)
@@ -73,6 +89,7 @@ def test_emulate_bf16_with_identity_rounding_is_the_f64_path(monkeypatch, model,
     x, y = _tiny_inputs(model, 3, 2)
     l0, g0 = sgd.flat_loss_and_grad(w, model, width_q, 10, x, y, emulate_bf16=False)
     monkeypatch.setattr(sgd, "bf16", lambda v: v)
+    monkeypatch.setattr(sgd, "bf16_rz", lambda v: v)
     l1, g1 = sgd.flat_loss_and_grad(w, model, width_q, 10, x, y, emulate_bf16=True)
     assert l0 == l1 and np.array_equal(g0, g1)
     monkeypatch.undo()

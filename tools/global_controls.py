@@ -4,10 +4,13 @@ the float64 oracle, next to two host controls run through the SAME oracle code (
 the oracle's bf16 emulation (reading R17).  The GPU rows are the library's fp32 verify and bf16 rounds in
 the bench launch configuration.  Usage: python tools/global_controls.py [config] > profiles/...json
 (GPU box; ~6 min of host oracle time on 16 cores)."""
-import json
-import math
 import os
-import sys
+
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):  # one BLAS thread per worker process
+    os.environ.setdefault(_v, "1")
+import json  # noqa: E402
+import math  # noqa: E402
+import sys  # noqa: E402
 import time
 from concurrent.futures import ProcessPoolExecutor
 
