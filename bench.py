@@ -400,18 +400,11 @@ def main():
                 traffic = by_per * rec["dram_bytes_per_launch"] * rec["launches"] / algo_round
         except Exception:
             traffic = None
-    # implementation bytes beyond SURVEY §8(d)'s algorithmic ones: the bf16 mode's fc1 weight shadow write
-    # (2 B per weight per client-step; fc1 dgrad / fwd read it next step).  Client-steps of the timed launches
-    # from their algorithmic work: FLOPs = 2 W rows, bytes = rows (F + K) e + 8 W clients (engine op_work)
-    impl = None
-    if pb.OPC_NAMES[dominant] == "fc1_wgrad" and prec == pb.PREC_BF16:
-        Wf, Ff, Kf = 512 * 4096, 512, 4096
-        rows = fl_per / (2 * Wf)
-        clients_per = (by_per - rows * (Ff + Kf) * eb) / (8 * Wf)
-        shadow = 2 * Wf * clients_per
-        impl = {"shadow_write_bytes_per_launch": shadow, "clients_per_launch": clients_per,
-                "achieved_with_shadow": (by_per + shadow) / avg_ns,
-                "frac_with_shadow": (by_per + shadow) / avg_ns / pk["hbm"]}
+    # bf16 mode keeps fc1's fp32 master as two 16-bit planes (the upper plane is the tensor-core operand of
+    # fc1 fwd / dgrad), so fc1 wgrad moves exactly SURVEY §8(d)'s 8 B per weight: no
+    # implementation bytes beyond the algorithmic ones (round 1 wrote a separate 2 B bf16 shadow)
+    impl = ({"note": "fp32 master as hi/lo 16-bit planes: no shadow write; actual bytes = algorithmic bytes"}
+            if pb.OPC_NAMES[dominant] == "fc1_wgrad" and prec == pb.PREC_BF16 else None)
     roof = {"kernel": pb.OPC_NAMES[dominant], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": traffic, "algorithmic": ALGO_NOTE.get(pb.OPC_NAMES[dominant], "engine op_work: "
             "operands read once, results written once"), "implementation_extra": impl,

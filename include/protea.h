@@ -52,7 +52,7 @@ typedef enum {
   PROTEA_ERR_NCCL = 9
 } protea_status;
 
-enum { PROTEA_MODEL_MLP = 0, PROTEA_MODEL_CNN = 1, PROTEA_MODEL_RESNET8 = 2 };
+enum { PROTEA_MODEL_MLP = 0, PROTEA_MODEL_CNN = 1, PROTEA_MODEL_RESNET8 = 2, PROTEA_MODEL_RESNET18 = 3 };
 enum { PROTEA_PREC_FP32 = 0, PROTEA_PREC_BF16 = 1 };
 enum { PROTEA_POLICY_PROFILED = 0, PROTEA_POLICY_STATIC = 1 };
 enum { PROTEA_ORDER_ASC_ID = 0, PROTEA_ORDER_DESC_STEPS = 1 };
@@ -75,8 +75,11 @@ typedef struct {
 } protea_init_opts;
 
 /* Model family of a shape group.  CNN: width = width_q / 4, width_q in {1,2,4}
- * (BASELINE.json configs[3]); MLP / RESNET8 require width_q == 4.
- * H, W, C: input image shape (MLP 28x28x1, CNN / RESNET8 32x32x3). */
+ * (BASELINE.json configs[3]); MLP / RESNET8 / RESNET18 require width_q == 4.
+ * H, W, C: input image shape (MLP 28x28x1; CNN 32x32x3 CIFAR-shaped, or 28x28x1 FEMNIST-shaped, the paper's
+ * LEAF experiment P:304; RESNET8 / RESNET18 32x32x3).  RESNET18 is the paper's CIFAR model with
+ * GroupNorm (2 groups) after every conv and option-A shortcuts (reading R26); it runs on the SIMT
+ * kernels in both precisions. */
 typedef struct {
   int32_t arch;      /* PROTEA_MODEL_* */
   int32_t width_q;
@@ -151,6 +154,8 @@ enum {
   PROTEA_OPC_MLP_FC1_WGRAD, PROTEA_OPC_ADMIT, PROTEA_OPC_FEDAVG, PROTEA_OPC_STAGE_X,
   PROTEA_OPC_R_FWD, PROTEA_OPC_R_HEAD, PROTEA_OPC_R_DGRAD, PROTEA_OPC_R_WGRAD, PROTEA_OPC_R_REDUCE, /* ResNet-8 */
   PROTEA_OPC_EVAL_HEAD, /* evaluate round: classifier head after the forward kernels */
+  PROTEA_OPC_G_FWD, PROTEA_OPC_G_NORM, PROTEA_OPC_G_HEAD, PROTEA_OPC_G_DGRAD, PROTEA_OPC_G_WGRAD,
+  PROTEA_OPC_G_REDUCE, /* ResNet-18 (GroupNorm): conv fwd, GroupNorm fwd / bwd, head, conv dgrad, wgrad, reduces */
   PROTEA_N_OPC = 32 /* room for further op classes */
 };
 

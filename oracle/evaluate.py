@@ -25,7 +25,7 @@ def logits(w, model, width_q, classes, x_u8):
     if model == sgd.MLP:
         h1 = sgd.relu(xb.reshape(nb, -1) @ p["fc1.W"].T + p["fc1.b"])
         return h1 @ p["fc2.W"].T + p["fc2.b"]
-    if model == sgd.CNN:
+    if model in (sgd.CNN, sgd.CNN28):
         z1, _ = sgd.conv_fwd(xb, p["conv1.W"], p["conv1.b"], 1, 2)
         a1, _ = sgd.pool2_fwd(sgd.relu(z1))
         z2, _ = sgd.conv_fwd(a1, p["conv2.W"], p["conv2.b"], 1, 2)

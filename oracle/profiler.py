@@ -22,7 +22,7 @@ from __future__ import annotations
 
 import math
 
-from .sgd import MLP, CNN, RESNET8, cnn_channels, n_params
+from .sgd import MLP, CNN, CNN28, RESNET8, RESNET18, cnn_channels, n_params, resnet18_blocks
 
 ALIGN = 256
 
@@ -45,6 +45,18 @@ def macs_per_sample(model, width_q=4, classes=10):
                 ("conv2", 16 * 16 * c2 * 5 * 5 * c1),
                 ("fc1", 64 * c2 * f),
                 ("fc2", f * classes)]
+    if model == CNN28:
+        c1, c2, f = cnn_channels(width_q)
+        return [("conv1", 28 * 28 * c1 * 5 * 5 * 1),
+                ("conv2", 14 * 14 * c2 * 5 * 5 * c1),
+                ("fc1", 49 * c2 * f),
+                ("fc2", f * classes)]
+    if model == RESNET18:  # GroupNorm layers do no multiply-accumulates
+        out, hw = [("conv0", 32 * 32 * 64 * 9 * 3)], 32
+        for name, cin, cout, stride in resnet18_blocks():
+            hw //= stride
+            out += [(name + "a", hw * hw * cout * 9 * cin), (name + "b", hw * hw * cout * 9 * cout)]
+        return out + [("fc", 512 * classes)]
     if model == RESNET8:
         return [("conv0", 32 * 32 * 16 * 9 * 3),
                 ("b1a", 32 * 32 * 16 * 9 * 16), ("b1b", 32 * 32 * 16 * 9 * 16),
@@ -74,6 +86,15 @@ def conv_layers(model, width_q=4):
     if model == CNN:
         c1, c2, _ = cnn_channels(width_q)
         return [(1024, c1, 25 * 3), (256, c2, 25 * c1)]
+    if model == CNN28:
+        c1, c2, _ = cnn_channels(width_q)
+        return [(784, c1, 25 * 1), (196, c2, 25 * c1)]
+    if model == RESNET18:
+        out, hw = [(1024, 64, 27)], 32
+        for _, cin, cout, stride in resnet18_blocks():
+            hw //= stride
+            out += [(hw * hw, cout, 9 * cin), (hw * hw, cout, 9 * cout)]
+        return out
     if model == RESNET8:
         return [(1024, 16, 27), (1024, 16, 144), (1024, 16, 144), (256, 32, 144), (256, 32, 288),
                 (64, 64, 288), (64, 64, 576)]
@@ -95,19 +116,26 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
     b, e = min(batch, n), elem_bytes  # a batch holds min(B, n) rows
     P = n_params(model, width_q, classes)
     out = [("params", 4 * P), ("perm", 4 * epochs * n), ("stats", 64)]
-    if e == 2:
+    if e == 2 and model != RESNET18:
         out.append(("wsh", 2 * P))  # bf16 shadow weights read by the tensor-core GEMMs
     if model == MLP:
         out += [("h1", b * 64 * e), ("dz1", b * 64 * e)]
-    elif model == CNN:
+    elif model in (CNN, CNN28):
         c1, c2, f = cnn_channels(width_q)
-        out += [("a1", b * 256 * c1 * e), ("i1", b * 256 * c1),
-                ("a2", b * 64 * c2 * e), ("i2", b * 64 * c2),
+        hw = 1024 if model == CNN else 784  # conv1 map; conv2 map hw / 4; pool-2 output hw / 16
+        out += [("a1", b * hw // 4 * c1 * e), ("i1", b * hw // 4 * c1),
+                ("a2", b * hw // 16 * c2 * e), ("i2", b * hw // 16 * c2),
                 ("h", b * f * e), ("dh", b * f * e),
-                ("dz2", b * 256 * c2 * e), ("dz1", b * 1024 * c1 * e)]
-        if e == 2:  # bf16 mode: input staged for the tensor cores + conv1 weight shadow
+                ("dz2", b * hw // 4 * c2 * e), ("dz1", b * hw * c1 * e)]
+        if e == 2 and model == CNN:  # bf16 tcgen05 mode: input staged for the tensor cores + conv1 weight shadow
             # (6x6 window taps x 4 pool positions x C1 x 8 padded channels, bf16)
             out += [("xs", b * 36 * 36 * 8 * 2), ("w1q", 36 * 4 * c1 * 8 * 2)]
+    elif model == RESNET18:  # per conv layer its output z and activation y, then GN stats, gradients
+        convs = conv_layers(model)
+        out += [(f"z{i}", b * hw * co * e) for i, (hw, co, _) in enumerate(convs)]
+        out += [(f"y{i}", b * hw * co * e) for i, (hw, co, _) in enumerate(convs)]
+        out += [("gnstats", b * 17 * 2 * 2 * 4), ("gx", b * 65536 * e), ("gy", b * 65536 * e),
+                ("gz", b * 65536 * e), ("gnp", b * 2 * 512 * 4)]
     elif model == RESNET8:
         out += [("a0", b * 1024 * 16 * e),
                 ("r1", b * 1024 * 16 * e), ("o1", b * 1024 * 16 * e),
@@ -123,7 +151,9 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
     convs = conv_layers(model, width_q)
     splits = [math.ceil(b * hw / WGRAD_CHUNK_PX) for hw, _, _ in convs]
     ceil4 = lambda k: -(-k // 4) * 4  # noqa: E731
-    if model == RESNET8:
+    if model == RESNET18:  # one region reused layer by layer (reduced right after each wgrad), pitch K+1
+        out.append(("wsp", max(4 * s * co * (K + 1) for s, (_, co, K) in zip(splits, convs))))
+    elif model == RESNET8:
         # a region per layer, all seven kept until the step's single merged SGD reduce; regions placed at
         # row pitch ceil4(K+1), the last layer's rows written at pitch K+1 (its last row ends the slot)
         wsp = sum(s * co * ceil4(K + 1) for s, (_, co, K) in zip(splits[:-1], convs[:-1]))

@@ -42,7 +42,20 @@ import numpy as np
 
 from .splitmix import epoch_perm
 
-MLP, CNN, RESNET8 = 0, 1, 2
+MLP, CNN, RESNET8, CNN28, RESNET18 = 0, 1, 2, 3, 4  # CNN28: the CNN-w family on a 28x28x1 (FEMNIST-shaped)
+# input; RESNET18: the paper's CIFAR model (P:304) with GroupNorm (DESIGN.md reading R26)
+GN_GROUPS, GN_EPS = 2, 1e-5
+
+
+def resnet18_blocks():
+    """[(block name, cin, cout, stride)] of the 8 basic blocks (4 stages x 2, 64 / 128 / 256 / 512 channels,
+    stride 2 at the first block of stages 2-4)."""
+    out, cin = [], 64
+    for s, c in enumerate((64, 128, 256, 512)):
+        for b in range(2):
+            out.append((f"s{s + 1}b{b}", cin, c, 2 if (s > 0 and b == 0) else 1))
+            cin = c
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -57,10 +70,17 @@ def layer_shapes(model, width_q=4, classes=10):
     """List of (name, W shape, b shape)."""
     if model == MLP:
         return [("fc1", (64, 784), (64,)), ("fc2", (classes, 64), (classes,))]
-    if model == CNN:
+    if model in (CNN, CNN28):
         c1, c2, f = cnn_channels(width_q)
-        return [("conv1", (c1, 5, 5, 3), (c1,)), ("conv2", (c2, 5, 5, c1), (c2,)),
-                ("fc1", (f, 64 * c2), (f,)), ("fc2", (classes, f), (classes,))]
+        cin, pooled = (3, 64) if model == CNN else (1, 49)  # 32x32x3 -> 8x8 after two pools; 28x28x1 -> 7x7
+        return [("conv1", (c1, 5, 5, cin), (c1,)), ("conv2", (c2, 5, 5, c1), (c2,)),
+                ("fc1", (f, pooled * c2), (f,)), ("fc2", (classes, f), (classes,))]
+    if model == RESNET18:  # conv W / b, then the following GroupNorm's gamma / beta as a (C,), (C,) pair
+        out = [("conv0", (64, 3, 3, 3), (64,)), ("gn0", (64,), (64,))]
+        for name, cin, cout, _ in resnet18_blocks():
+            out += [(name + "a", (cout, 3, 3, cin), (cout,)), (name + "ga", (cout,), (cout,)),
+                    (name + "b", (cout, 3, 3, cout), (cout,)), (name + "gb", (cout,), (cout,))]
+        return out + [("fc", (classes, 512), (classes,))]
     if model == RESNET8:
         return [("conv0", (16, 3, 3, 3), (16,)),
                 ("b1a", (16, 3, 3, 16), (16,)), ("b1b", (16, 3, 3, 16), (16,)),
@@ -92,7 +112,7 @@ def pack(p, model, width_q=4, classes=10):
 
 
 def input_shape(model):
-    return (28, 28, 1) if model == MLP else (32, 32, 3)
+    return (28, 28, 1) if model in (MLP, CNN28) else (32, 32, 3)  # RESNET18, RESNET8, CNN: CIFAR-shaped
 
 
 # ---------------------------------------------------------------------------
@@ -213,6 +233,38 @@ def forced_pool(name, z, gpu_arg, gpu_pos, tol, rep):
     return np.where(mask, relu(pre), 0.0), ga, mask
 
 
+def gn_fwd(z, gamma, beta, groups=GN_GROUPS, eps=GN_EPS):
+    """GroupNorm (Wu & He 2018) of z [n, H, W, C]: per sample and group of C / groups channels, x^ = (z - mean)
+    / sqrt(var + eps) over (H, W, channels of the group), then gamma_c x^ + beta_c.  Returns (out, cache)."""
+    n, H, W, C = z.shape
+    zg = z.reshape(n, H, W, groups, C // groups)
+    mu = zg.mean(axis=(1, 2, 4), keepdims=True)
+    var = ((zg - mu) ** 2).mean(axis=(1, 2, 4), keepdims=True)
+    rstd = 1.0 / np.sqrt(var + eps)
+    xh = ((zg - mu) * rstd).reshape(n, H, W, C)
+    return xh * gamma + beta, (xh, rstd, groups)
+
+
+def gn_bwd(dy, gamma, cache):
+    """Gradients of GroupNorm: (dz, dgamma, dbeta) from dy = d(out)."""
+    xh, rstd, groups = cache
+    n, H, W, C = dy.shape
+    dbeta = dy.sum(axis=(0, 1, 2))
+    dgamma = (dy * xh).sum(axis=(0, 1, 2))
+    dxh = (dy * gamma).reshape(n, H, W, groups, C // groups)
+    xg = xh.reshape(n, H, W, groups, C // groups)
+    dz = rstd * (dxh - dxh.mean(axis=(1, 2, 4), keepdims=True) - xg * (dxh * xg).mean(axis=(1, 2, 4), keepdims=True))
+    return dz.reshape(n, H, W, C), dgamma, dbeta
+
+
+def option_a(a, cout):
+    """Option-A shortcut: the input subsampled at even pixels with zero channels appended (R11)."""
+    sub = a[:, ::2, ::2, :]
+    sc = np.zeros(sub.shape[:3] + (cout,))
+    sc[..., :sub.shape[3]] = sub
+    return sc
+
+
 def softmax_ce(z, y):
     """Mean CE over the batch and dz = (softmax - onehot)/|beta|."""
     nb = z.shape[0]
@@ -286,10 +338,14 @@ def loss_and_grad(p, model, xb, yb, emulate_bf16=False, decisions=None, tol=0.0)
         g["fc1.b"] = dz1.sum(0)
         g["fc1.W"] = q(dz1).T @ x
         return loss, g
-    if model == CNN:
-        W2q = q(p["conv2.W"])
-        W3q = bf16_rz(p["fc1.W"]) if emulate_bf16 else p["fc1.W"]  # fc1: the hi plane of the fp32 master
-        z1, cols1 = conv_fwd(q(xb), q(p["conv1.W"]), p["conv1.b"], 1, 2)
+    if model in (CNN, CNN28):
+        if model == CNN:  # tcgen05 path: bf16 weight / input operands
+            W2q = q(p["conv2.W"])
+            W3q = bf16_rz(p["fc1.W"]) if emulate_bf16 else p["fc1.W"]  # fc1: the hi plane of the fp32 master
+            W1q, xq = q(p["conv1.W"]), q(xb)
+        else:  # CNN28 runs the SIMT kernels on bf16 storage: fp32 weights and input, bf16 stored tensors
+            W1q, W2q, W3q, xq = p["conv1.W"], p["conv2.W"], p["fc1.W"], xb
+        z1, cols1 = conv_fwd(xq, W1q, p["conv1.b"], 1, 2)
         if dec is None:
             a1, arg1 = pool2_fwd(relu(z1))
             m1 = a1 > 0
@@ -319,7 +375,61 @@ def loss_and_grad(p, model, xb, yb, emulate_bf16=False, decisions=None, tol=0.0)
         dz2 = q(pool2_bwd(da2 * m2, arg2, z2.shape))
         g["conv2.W"], g["conv2.b"], da1 = conv_bwd(dz2, a1.shape, cols2, W2q, 1, 2, True)
         dz1 = q(pool2_bwd(da1 * m1, arg1, z1.shape))
-        g["conv1.W"], g["conv1.b"], _ = conv_bwd(dz1, xb.shape, cols1, q(p["conv1.W"]), 1, 2, False)
+        g["conv1.W"], g["conv1.b"], _ = conv_bwd(dz1, xb.shape, cols1, W1q, 1, 2, False)
+        return loss, g
+    if model == RESNET18:
+        # R26: conv (bias) -> GroupNorm -> ReLU; basic blocks out = ReLU(GN(conv(ReLU(GN(conv(a))))) + sc(a)),
+        # sc = identity or option A; GAP over the 4x4 map; FC.  The SIMT path (both modes) stores every conv
+        # output z, every activation and every gradient tensor in the mode's storage type (emulate_bf16:
+        # rounded there), weights and GroupNorm statistics in fp32.
+        def rmask(name, v):
+            return v > 0 if dec is None else forced_relu_mask(name, v, dec[name] > 0, tol, rep)
+
+        z0, cols0 = conv_fwd(xb, p["conv0.W"], p["conv0.b"], 1, 1)
+        z0 = q(z0)
+        y0, gc0 = gn_fwd(z0, p["gn0.W"], p["gn0.b"])
+        m0 = rmask("a0", y0)
+        a = q(np.where(m0, y0, 0.0))
+        caches = []
+        for bi, (name, cin, cout, stride) in enumerate(resnet18_blocks()):
+            za, colsa = conv_fwd(a, p[name + "a.W"], p[name + "a.b"], stride, 1)
+            za = q(za)
+            ya, gca = gn_fwd(za, p[name + "ga.W"], p[name + "ga.b"])
+            ma = rmask(f"r{bi}", ya)
+            ra = q(np.where(ma, ya, 0.0))
+            zb, colsb = conv_fwd(ra, p[name + "b.W"], p[name + "b.b"], 1, 1)
+            zb = q(zb)
+            nb_, gcb = gn_fwd(zb, p[name + "gb.W"], p[name + "gb.b"])
+            sc = a if (stride == 1 and cin == cout) else option_a(a, cout)
+            s = nb_ + sc
+            ms = rmask(f"o{bi}", s)
+            out = q(np.where(ms, s, 0.0))
+            caches.append((name, cin, cout, stride, a, colsa, gca, ma, ra, colsb, gcb, ms))
+            a = out
+        gap = a.mean(axis=(1, 2))
+        z = gap @ p["fc.W"].T + p["fc.b"]
+        loss, dz = softmax_ce(z, yb)
+        g["fc.W"], g["fc.b"] = dz.T @ gap, dz.sum(0)
+        dgap = dz @ p["fc.W"]
+        HW = a.shape[1] * a.shape[2]
+        dout = q(np.broadcast_to(dgap[:, None, None, :] / HW, a.shape).copy())
+        for name, cin, cout, stride, a_in, colsa, gca, ma, ra, colsb, gcb, ms in reversed(caches):
+            gs = q(dout * ms)  # gradient of the block output's pre-ReLU sum: GN-b's output and the shortcut
+            dzb, g[name + "gb.W"], g[name + "gb.b"] = gn_bwd(gs, p[name + "gb.W"], gcb)
+            dzb = q(dzb)
+            g[name + "b.W"], g[name + "b.b"], dra = conv_bwd(dzb, ra.shape, colsb, p[name + "b.W"], 1, 1, True)
+            dra = q(dra)
+            dza, g[name + "ga.W"], g[name + "ga.b"] = gn_bwd(dra * ma, p[name + "ga.W"], gca)
+            dza = q(dza)
+            g[name + "a.W"], g[name + "a.b"], da_in = conv_bwd(dza, a_in.shape, colsa, p[name + "a.W"], stride, 1, True)
+            if stride == 1 and cin == cout:
+                da_in = da_in + gs
+            else:
+                da_in[:, ::2, ::2, :] += gs[..., :cin]
+            dout = q(da_in)
+        dz0, g["gn0.W"], g["gn0.b"] = gn_bwd(dout * m0, p["gn0.W"], gc0)
+        dz0 = q(dz0)
+        g["conv0.W"], g["conv0.b"], _ = conv_bwd(dz0, xb.shape, cols0, p["conv0.W"], 1, 1, False)
         return loss, g
     if model == RESNET8:
         # emulate_bf16: the staged input, the stored activations (a0, each block's ra and output), the

@@ -20,13 +20,13 @@ inline uint64_t align256(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign
 // One layer of a model, in forward order.  Weights are [out][K] row-major with
 // K = k*k*cin (conv, NHWC taps (ky,kx,ci)) or K = in (fc); bias [out] follows.
 struct Layer {
-  int kind;      // 0 = conv, 1 = fc
+  int kind;      // 0 = conv, 1 = fc, 2 = GroupNorm (cin = cout = C; "weights" = gamma [C], "bias" = beta [C])
   int k, stride, pad;
   int cin, cout;
   int hin, win;  // input spatial size (conv)
   int hout, wout;
   int64_t off_w, off_b;  // offsets in the flat parameter vector
-  int64_t K() const { return kind == 0 ? (int64_t)k * k * cin : cin; }
+  int64_t K() const { return kind == 0 ? (int64_t)k * k * cin : kind == 1 ? cin : 1; }
 };
 
 struct ModelDims {
@@ -55,8 +55,19 @@ enum Buf : int {
   B_R_W0P,  // bf16 mode: conv0 weights padded to 8 input channels [16][9][8] (tensor-core operand)
   B_R_XS,   // bf16 mode: conv0 input staged as [r][32][32][8] bf16 (read by conv0 fwd and wgrad)
   B_R_WSP,
+  // ResNet-18 (GroupNorm, reading R26): conv layer l = 0..16 in forward order (stem, then blocks i = 0..7 as
+  // l = 1 + 2i (conv a), 2 + 2i (conv b)); z_l = the conv output, y_l = the activation after GroupNorm (+
+  // shortcut) and ReLU
+  B_G_Z0,
+  B_G_Y0 = B_G_Z0 + 17,
+  B_G_ST = B_G_Y0 + 17,  // GroupNorm statistics [b][17 layers][2 groups][mean, rstd] fp32
+  B_G_X, B_G_YG, B_G_ZG,  // gradient buffers (the largest activation each)
+  B_G_GNP,               // GroupNorm parameter-gradient partials [b][2][512] fp32 (per layer, reused)
+  B_G_WSP,               // conv weight-gradient split partials (per layer, reused: max over layers)
   B_COUNT
 };
+constexpr int kGroups = 2;    // GroupNorm groups (R26)
+constexpr int kG_Layers = 17;  // ResNet-18 conv layers
 
 struct SlotLayout {
   uint64_t off[B_COUNT];

@@ -26,32 +26,40 @@ struct ClientRec {
   uint64_t* sm_ns;         // per-client device-time attribution (nullable)
   const void* tmaps;       // bf16 CNN: TM_COUNT CUtensorMaps (128 B each, global memory), else nullptr
   float* mw;               // micro-client 0 of a batch > kMicroRows: the merge weights (P fp32), else nullptr
-  // fp32 master weights [sp_off, sp_off + sp_len) stored as two 16-bit planes (bf16-mode CNN: fc1's W, the
-  // HBM-bound weight stream): hi = the upper half of each fp32 (= the tensor-core operand, read by fc1 fwd /
-  // dgrad through TMA), lo = the lower half, hi plane at params + sp_off, lo plane right after it.  The
-  // fp32 value is exactly (hi << 16 | lo); nothing else stores those weights (DESIGN.md §5 "split planes").
+  // fp32 master weights of a [F][K] matrix at [sp_off, sp_off + sp_len) (sp_len = F K, sp_k = K, K a multiple
+  // of 128) stored as 16-bit halves (bf16-mode CNN: fc1's W, the HBM-bound weight stream): per row f and
+  // 128-wide block of k, 128 upper halves then 128 lower halves (512 contiguous bytes, like the fp32 row
+  // segment they replace).  The upper halves are the tensor-core operand of fc1 fwd / dgrad, read by TMA as a
+  // [F][K/128][128] tensor with a 512-byte block stride; the fp32 value is exactly (hi << 16 | lo); nothing
+  // else stores those weights (DESIGN.md §5 "split planes").
   int64_t sp_off, sp_len;
+  int64_t sp_k;
 };
 
 __device__ __forceinline__ float split_join(uint16_t hi, uint16_t lo) {
   return __uint_as_float(((uint32_t)hi << 16) | lo);
 }
+// 16-bit index of the upper half of matrix element i = f K + k (the lower half is 128 further)
+__device__ __forceinline__ int64_t split_hi_index(const ClientRec* c, int64_t i) {
+  const int64_t f = i / c->sp_k, k = i - f * c->sp_k;
+  return f * 2 * c->sp_k + (k >> 7) * 256 + (k & 127);
+}
 // master weight d of client c (either representation)
 __device__ __forceinline__ float master_w(const ClientRec* c, int64_t d) {
   const uint64_t i = (uint64_t)(d - c->sp_off);
   if (i < (uint64_t)c->sp_len) {
-    const uint16_t* hi = reinterpret_cast<const uint16_t*>(c->params + c->sp_off);
-    return split_join(hi[i], hi[c->sp_len + i]);
+    const uint16_t* h = reinterpret_cast<const uint16_t*>(c->params + c->sp_off) + split_hi_index(c, (int64_t)i);
+    return split_join(h[0], h[128]);
   }
   return c->params[d];
 }
 __device__ __forceinline__ void set_master_w(const ClientRec* c, int64_t d, float w) {
   const uint64_t i = (uint64_t)(d - c->sp_off);
   if (i < (uint64_t)c->sp_len) {
-    uint16_t* hi = reinterpret_cast<uint16_t*>(c->params + c->sp_off);
+    uint16_t* h = reinterpret_cast<uint16_t*>(c->params + c->sp_off) + split_hi_index(c, (int64_t)i);
     const uint32_t u = __float_as_uint(w);
-    hi[i] = (uint16_t)(u >> 16);
-    hi[c->sp_len + i] = (uint16_t)(u & 0xFFFFu);
+    h[0] = (uint16_t)(u >> 16);
+    h[128] = (uint16_t)(u & 0xFFFFu);
     return;
   }
   c->params[d] = w;
@@ -60,8 +68,9 @@ __device__ __forceinline__ void set_master_w(const ClientRec* c, int64_t d, floa
 // One active client in one lock-step iteration.
 struct Task {
   int32_t rec;   // ClientRec index
-  int32_t step;  // local step s in [0, S_k)
-  int32_t rows;  // |beta| = min(B, n - j*B)
+  int32_t den;   // |beta| of the whole batch: the mean-loss denominator (= rows, except for micro-clients,
+                 // which hold a share of a larger batch: common.h kMicroRows)
+  int32_t rows;  // rows of the batch in this (micro-)client: min(B, n - j*B) or its share
   int32_t base;  // e*n + j*B: index into perm of the batch's first row
 };
 

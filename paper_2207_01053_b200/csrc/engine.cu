@@ -216,11 +216,11 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
     const uint32_t bx[3] = {8, 1, (uint32_t)C2};
     ok &= tmap_encode(&out[TM_W2D], w2, 3, d, st, bx);
   }
-  {
-    const uint64_t d[2] = {K1, F}, st[1] = {2 * K1};
-    const uint32_t bk[2] = {64, 128}, bm[2] = {64, 64};
-    ok &= tmap_encode(&out[TM_W3K], w3, 2, d, st, bk, CU_TENSOR_MAP_SWIZZLE_128B);
-    ok &= tmap_encode(&out[TM_W3M], w3, 2, d, st, bm, CU_TENSOR_MAP_SWIZZLE_128B);
+  {  // fc1 W upper halves: [F][K1 / 128][128] bf16, 128-blocks 512 B apart (the lower halves in between)
+    const uint64_t d[3] = {128, K1 / 128, F}, st[2] = {512, 4 * K1};
+    const uint32_t bk[3] = {64, 1, 128}, bm[3] = {64, 1, 64};
+    ok &= tmap_encode(&out[TM_W3K], w3, 3, d, st, bk, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= tmap_encode(&out[TM_W3M], w3, 3, d, st, bm, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   {
     const uint64_t d[2] = {K1, Bk}, st[1] = {2 * K1};
@@ -366,6 +366,8 @@ void join_group(protea_ctx* ctx, int g) {
 }
 
 int tiles(const ModelDims& m, int op, int rows, bool tc) {
+  if (m.arch == PROTEA_MODEL_CNN && m.H != 32) tc = false;  // FEMNIST-shaped CNN: SIMT kernels
+  const int HW = m.H * m.W, HW2 = HW / 4, K1 = HW / 16 * m.c2, KC1 = 25 * m.C + 1;
   if (op >= RI_F0) {
     if (op == RI_HEAD) return 1;
     // bf16 mode: every conv on tcgen05 (kernels_resnet_tc.cuh), 128-row tiles (conv0 on the staged input)
@@ -403,17 +405,17 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
       default: break;
     }
   switch (op) {
-    case OP_C1F: return cdiv(rows * 1024, C1F_BM) * cdiv(m.c1, C1F_BN);
-    case OP_C2F: return cdiv(rows * 256, C2F_BM) * cdiv(m.c2, C2F_BN);
+    case OP_C1F: return cdiv(rows * HW, C1F_BM) * cdiv(m.c1, C1F_BN);
+    case OP_C2F: return cdiv(rows * HW2, C2F_BM) * cdiv(m.c2, C2F_BN);
     case OP_F1F: return cdiv(rows, F1F_BM) * cdiv(m.f, F1F_BN);
     case OP_HEAD: return 1;  // k_head_cnn: one CTA per client
-    case OP_F1D: return cdiv(rows, F1D_BM) * cdiv(64 * m.c2, F1D_BN);
-    case OP_F1W: return cdiv(m.f, F1W_BM) * cdiv(64 * m.c2, F1W_BN);
-    case OP_C2D: return cdiv(rows * 256, C2D_BM) * cdiv(m.c1, C2D_BN);
-    case OP_C2W: return cdiv(rows * 256, kWgradChunkPx) * cdiv(m.c2, C2W_BM) * cdiv(25 * m.c1 + 1, C2W_BN);
+    case OP_F1D: return cdiv(rows, F1D_BM) * cdiv(K1, F1D_BN);
+    case OP_F1W: return cdiv(m.f, F1W_BM) * cdiv(K1, F1W_BN);
+    case OP_C2D: return cdiv(rows * HW2, C2D_BM) * cdiv(m.c1, C2D_BN);
+    case OP_C2W: return cdiv(rows * HW2, kWgradChunkPx) * cdiv(m.c2, C2W_BM) * cdiv(25 * m.c1 + 1, C2W_BN);
     case OP_C2R: return cdiv(m.c2 * (25 * m.c1 + 1), kReduceBlock);
-    case OP_C1W: return cdiv(rows * 1024, kWgradChunkPx) * cdiv(m.c1, C1W_BM) * cdiv(76, C1W_BN);
-    case OP_C1R: return cdiv(m.c1 * 76, kReduceBlock);
+    case OP_C1W: return cdiv(rows * HW, kWgradChunkPx) * cdiv(m.c1, C1W_BM) * cdiv(KC1, C1W_BN);
+    case OP_C1R: return cdiv(m.c1 * KC1, kReduceBlock);
     case OP_MF: return cdiv(rows, MF_BM) * cdiv(64, MF_BN);
     case OP_MHEAD: return 1;
     case OP_MW: return cdiv(64, MW_BM) * cdiv(784, MW_BN);
@@ -422,6 +424,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
 }
 
 std::vector<int> ops_of(const ModelDims& m, bool tc) {
+  tc = tc && (m.arch != PROTEA_MODEL_CNN || m.H == 32);  // the tcgen05 CNN kernels are 32x32x3-only
   if (m.arch == PROTEA_MODEL_CNN && tc && m.width_q == 4)  // conv1 reduce fused into k_conv1_wgrad_q
     return {OP_STAGE, OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C1W};
   if (m.arch == PROTEA_MODEL_CNN && tc)
@@ -476,22 +479,25 @@ void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, u
     return;
   }
   const uint64_t c1 = m.c1, c2 = m.c2, f = m.f, C = m.classes;
-  const uint64_t s1 = m.width_q == 4 && e == 2 ? cdiv((int)r, kW1QImages) : cdiv((int)(r * 1024), kWgradChunkPx), s2 = cdiv((int)(r * 256), kWgradChunkPx);
+  // image geometry (CIFAR 32x32x3: HW 1024, HW2 256, HW4 64; FEMNIST 28x28x1: 784, 196, 49)
+  const uint64_t HW = (uint64_t)m.H * m.W, HW2 = HW / 4, HW4 = HW / 16, D = HW * m.C, KC = 25 * (uint64_t)m.C;
+  const bool tcq = m.width_q == 4 && e == 2 && m.H == 32;
+  const uint64_t s1 = tcq ? cdiv((int)r, kW1QImages) : cdiv((int)(r * HW), kWgradChunkPx), s2 = cdiv((int)(r * HW2), kWgradChunkPx);
   uint64_t F = 0, B = 0;
   switch (op) {
-    case OP_C1F: F = 2 * r * 1024 * c1 * 75; B = r * 3072 + 4 * c1 * 76 + r * 256 * c1 * (e + 1); break;
-    case OP_C2F: F = 2 * r * 256 * c2 * 25 * c1; B = r * 256 * c1 * e + e * c2 * 25 * c1 + 4 * c2 + r * 64 * c2 * (e + 1); break;
-    case OP_F1F: F = 2 * r * f * 64 * c2; B = r * 64 * c2 * e + e * f * 64 * c2 + 4 * f + r * f * e; break;
+    case OP_C1F: F = 2 * r * HW * c1 * KC; B = r * D + 4 * c1 * (KC + 1) + r * HW2 * c1 * (e + 1); break;
+    case OP_C2F: F = 2 * r * HW2 * c2 * 25 * c1; B = r * HW2 * c1 * e + e * c2 * 25 * c1 + 4 * c2 + r * HW4 * c2 * (e + 1); break;
+    case OP_F1F: F = 2 * r * f * HW4 * c2; B = r * HW4 * c2 * e + e * f * HW4 * c2 + 4 * f + r * f * e; break;
     case OP_HEAD: F = 3 * 2 * r * C * f; B = r * f * e + 8 * C * (f + 1) + r * f * e + 8 * f + r * 4; break;
-    case OP_F1D: F = 2 * r * 64 * c2 * f; B = r * f * e + e * f * 64 * c2 + r * 64 * c2 * (e + 1) + r * 256 * c2 * e; break;
+    case OP_F1D: F = 2 * r * HW4 * c2 * f; B = r * f * e + e * f * HW4 * c2 + r * HW4 * c2 * (e + 1) + r * HW2 * c2 * e; break;
     // fp32 master read + write (8 B per weight per client-step) + the dh / a2 reads; the bf16
     // shadow write of the bf16 mode (2 B per weight) is implementation traffic, not counted here
-    case OP_F1W: F = 2 * r * f * 64 * c2; B = r * f * e + r * 64 * c2 * e + 8 * f * 64 * c2; break;
-    case OP_C2D: F = 2 * r * 256 * c1 * 25 * c2; B = r * 256 * c2 * e + e * c2 * 25 * c1 + r * 256 * c1 * (e + 1) + r * 1024 * c1 * e; break;
-    case OP_C2W: F = 2 * r * 256 * c2 * 25 * c1; B = r * 256 * c2 * e + r * 256 * c1 * e + 4 * s2 * c2 * (25 * c1 + 1); break;
+    case OP_F1W: F = 2 * r * f * HW4 * c2; B = r * f * e + r * HW4 * c2 * e + 8 * f * HW4 * c2; break;
+    case OP_C2D: F = 2 * r * HW2 * c1 * 25 * c2; B = r * HW2 * c2 * e + e * c2 * 25 * c1 + r * HW2 * c1 * (e + 1) + r * HW * c1 * e; break;
+    case OP_C2W: F = 2 * r * HW2 * c2 * 25 * c1; B = r * HW2 * c2 * e + r * HW2 * c1 * e + 4 * s2 * c2 * (25 * c1 + 1); break;
     case OP_C2R: F = 0; B = 4 * s2 * c2 * (25 * c1 + 1) + (8 + (e == 2 ? 2 : 0)) * c2 * (25 * c1 + 1); break;
-    case OP_C1W: F = 2 * r * 1024 * c1 * 75; B = r * 1024 * c1 * e + r * 3072 + 4 * s1 * c1 * 76; break;
-    case OP_C1R: F = 0; B = 4 * s1 * c1 * 76 + 8 * c1 * 76; break;
+    case OP_C1W: F = 2 * r * HW * c1 * KC; B = r * HW * c1 * e + r * D + 4 * s1 * c1 * (KC + 1); break;
+    case OP_C1R: F = 0; B = 4 * s1 * c1 * (KC + 1) + 8 * c1 * (KC + 1); break;
     case OP_MF: F = 2 * r * 64 * 784; B = r * 784 + 4 * 64 * 785 + r * 64 * e; break;
     case OP_MHEAD: F = 3 * 2 * r * C * 64; B = r * 64 * e + 8 * C * 65 + r * 64 * e + 8 * 64 + r * 4; break;
     case OP_MW: F = 2 * r * 64 * 784; B = r * 64 * e + r * 784 + 8 * 64 * 784; break;
@@ -515,6 +521,9 @@ CnnDims cnn_dims(const ModelDims& m) {
   d.b3 = m.layers[2].off_b;
   d.w4 = m.layers[3].off_w;
   d.b4 = m.layers[3].off_b;
+  d.H = m.H;
+  d.W = m.W;
+  d.C = m.C;
   return d;
 }
 
@@ -989,13 +998,13 @@ void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const Cli
     launch_gemm<Fc1Wgrad<T, F1W_BM, F1W_BN>, F1W_BM, F1W_BN>(ctx, {drecs, d, lr}, L, OP_F1W, dtab);
     launch_gemm<Conv2Dgrad<T, C2D_BM, C2D_BN>, C2D_BM, C2D_BN>(ctx, {drecs, d}, L, OP_C2D, dtab);
     launch_gemm<Conv2Wgrad<T, C2W_BM, C2W_BN>, C2W_BM, C2W_BN>(ctx, {drecs, d}, L, OP_C2W, dtab);
-    ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, 256, lr, 0, -1};
+    ReduceArgs r2{drecs, B_WSP, m.c2, 25 * m.c1, d.w2, d.b2, d.HW2(), lr, 0, -1};
     ev = op_begin(ctx, OP_C2R, OP_C2R);
     k_reduce_update<<<L.grid[OP_C2R], kReduceBlock, 0, ctx->cur>>>(r2, tasks, dtab + L.prefix_off[OP_C2R],
                                                                        L.ntask);
     op_end(ctx, ev);
     launch_gemm<Conv1Wgrad<T, C1W_BM, C1W_BN>, C1W_BM, C1W_BN>(ctx, {drecs, d}, L, OP_C1W, dtab);
-    ReduceArgs r1{drecs, B_WSP, m.c1, 75, d.w1, d.b1, 1024, lr, 0, -1};
+    ReduceArgs r1{drecs, B_WSP, m.c1, 25 * d.C, d.w1, d.b1, d.HW(), lr, 0, -1};
     ev = op_begin(ctx, OP_C1R, OP_C1R);
     k_reduce_update<<<L.grid[OP_C1R], kReduceBlock, 0, ctx->cur>>>(r1, tasks, dtab + L.prefix_off[OP_C1R],
                                                                        L.ntask);
@@ -1405,9 +1414,10 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const floa
     r.n = (int32_t)c.n;
     r.B = c.cap;  // rows a batch can hold here: the slot's per-row buffer capacity
     r.mw = c.mw_off ? (float*)(ctx->arena + c.mw_off) : nullptr;
-    if (tc_mode && gr.m.arch == PROTEA_MODEL_CNN) {  // fc1's W as split planes (device.cuh)
+    if (tc_mode && gr.m.arch == PROTEA_MODEL_CNN && gr.m.H == 32) {  // fc1's W as split planes (device.cuh)
       r.sp_off = gr.m.layers[2].off_w;
       r.sp_len = (int64_t)gr.m.layers[2].cout * gr.m.layers[2].K();
+      r.sp_k = gr.m.layers[2].K();
     }
     r.E = c.E;
     r.nb = c.nb;
@@ -1451,7 +1461,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const floa
     std::vector<int> owner;
     for (size_t i = 0; i < rc.size(); ++i) {
       const ModelDims& m = ctx->groups[rc[i].group].m;
-      if (m.arch != PROTEA_MODEL_CNN) continue;
+      if (m.arch != PROTEA_MODEL_CNN || m.H != 32) continue;
       auto key = std::make_tuple(rc[i].offset, rc[i].cap, rc[i].E, rc[i].n, rc[i].group);
       auto it = ctx->tmap_cache.find(key);
       if (it == ctx->tmap_cache.end()) {
@@ -1523,14 +1533,14 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const floa
           const int s = (int)(t - c.admit), ep = s / c.nb, j = s % c.nb;
           rows[i] = micro_rows(c, t);
           tab.push_back(c.rec);
-          tab.push_back(s);
+          tab.push_back((int32_t)std::min<int64_t>(c.B, c.n - (int64_t)j * c.B));  // |beta| of the whole batch
           tab.push_back(rows[i]);
           tab.push_back((int32_t)((int64_t)ep * c.n + (int64_t)j * c.B + (int64_t)c.micro * kMicroRows));
         }
         // width-1 conv2 wgrad: when the iteration has few splits (the tail), each split's 7 M tiles become
         // 7 work items (no extra partials: disjoint outputs), otherwise one item covers all 7 tiles
         L.c2w_groups = 1;
-        if (tc_mode && m.arch == PROTEA_MODEL_CNN && m.width_q == 4) {
+        if (tc_mode && m.arch == PROTEA_MODEL_CNN && m.width_q == 4 && m.H == 32) {
           int64_t nsplit = 0;
           for (int r : rows) nsplit += cdiv(r * 256, kWgradChunkPx);
           if (nsplit < 2 * g_num_sms) L.c2w_groups = 7;
@@ -1677,7 +1687,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const floa
       const float lr_l = have_micro && L.vg % NL == NL0 ? lr * kMicroLrScale : lr;
       if (e == 4)
         launch_step<float>(ctx, m, L, drecs, dtab, lr_l);
-      else if (m.arch == PROTEA_MODEL_CNN)
+      else if (m.arch == PROTEA_MODEL_CNN && m.H == 32)
         launch_step_tc(ctx, m, L, drecs, dtab, lr_l);
       else
         launch_step<__nv_bfloat16>(ctx, m, L, drecs, dtab, lr_l);

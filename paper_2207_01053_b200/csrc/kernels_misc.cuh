@@ -48,38 +48,39 @@ __global__ void k_admit_params(const ClientRec* __restrict__ recs, const int* __
 }
 
 // Micro-clients of one batch (common.h kMicroRows): list = [M recs][M rows], micro 0 first.  Every micro
-// took its SGD step from the same weights w (= mw of micro 0) with lr * kMicroLrScale (a power of two:
-// exact), so (w_m - w) / kMicroLrScale = -lr * (mean gradient over micro m's b_m rows) to fp32 rounding of
-// the SCALED step (relative eps, not ulp(w)); the merge forms, in fp64 and in micro order,
-//   w' = w + sum_m (b_m / R) (w_m - w) / kMicroLrScale,   R = sum_m b_m = |beta|,
-// = w - lr * (mean gradient over the whole batch), rounded once to fp32.
-// Block 0 also folds the micro-batch losses into micro 0's stats[0] (the batch-mean loss of the step).
+// took its SGD step from the same weights w (= mw of micro 0) with its rows' losses divided by the WHOLE
+// batch's |beta| (Task.den: the gradient tensors it stores, and rounds in bf16 mode, are the whole batch's)
+// and lr * kMicroLrScale (a power of two: exact), so (w_m - w) / kMicroLrScale = -lr * (sum of micro m's
+// rows' gradients) / |beta| to fp32 rounding of the SCALED step (relative eps, not ulp(w)); the merge forms,
+// in fp64 and in micro order,
+//   w' = w + sum_m (w_m - w) / kMicroLrScale = w - lr * (mean gradient over the whole batch),
+// rounded once to fp32.  Micros without rows in this batch left w_m = w.
+// Block 0 also folds the micro-batch losses (already / |beta|) into micro 0's stats[0].
 __global__ void k_micro_merge(const ClientRec* __restrict__ recs, const int* __restrict__ list, int M, int R) {
   const ClientRec* c0 = recs + list[0];
   float* mw = c0->mw;
   const int64_t P = c0->P;
-  const double inv = 1.0 / ((double)kMicroLrScale * (double)R);
+  const double inv = 1.0 / (double)kMicroLrScale;
   for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < P; d += (int64_t)gridDim.x * blockDim.x) {
     const double w = (double)mw[d];
     double a = 0.0;
-    for (int m = 0; m < M; ++m) {
-      const int b = list[M + m];
-      if (b) a += (double)b * ((double)master_w(recs + list[m], d) - w);
-    }
+    for (int m = 0; m < M; ++m)
+      if (list[M + m]) a += (double)master_w(recs + list[m], d) - w;
     mw[d] = (float)(w + a * inv);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     // stats[0] of micro 0 holds the client's running total (stats[1]) plus this step's micro-0 loss
     float* s0 = c0->stats;
-    double step = (double)list[M] * ((double)s0[0] - (double)s0[1]);
+    double step = (double)s0[0] - (double)s0[1];
     for (int m = 1; m < M; ++m) {
       float* sm = recs[list[m]].stats;
-      step += (double)list[M + m] * (double)sm[0];
+      step += (double)sm[0];
       sm[0] = 0.f;
     }
-    s0[1] = (float)((double)s0[1] + step / (double)R);
+    s0[1] = (float)((double)s0[1] + step);
     s0[0] = s0[1];
   }
+  (void)R;
 }
 // ... then every micro (blockIdx.y) reloads the merged weights (params, bf16 shadows)
 __global__ void k_micro_bcast(const ClientRec* __restrict__ recs, const int* __restrict__ list) {
@@ -249,9 +250,10 @@ __global__ void __launch_bounds__(256) k_release_acc(const ClientRec* __restrict
       const double g = (double)c0->wg[d];
       const uint64_t si = (uint64_t)(d - c0->sp_off);  // split-plane weights (same layout for every client)
       if (si < (uint64_t)c0->sp_len) {
+        const int64_t hi_i = split_hi_index(c0, (int64_t)si);
         for (int i = 0; i < nc; ++i) {
-          const uint16_t* hi = reinterpret_cast<const uint16_t*>(prm[i] + c0->sp_off);
-          a += wn[i] * ((double)split_join(hi[si], hi[c0->sp_len + si]) - g);
+          const uint16_t* h = reinterpret_cast<const uint16_t*>(prm[i] + c0->sp_off) + hi_i;
+          a += wn[i] * ((double)split_join(h[0], h[128]) - g);
         }
         c0->acc[d] = a;
         continue;

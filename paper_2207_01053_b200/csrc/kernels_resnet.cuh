@@ -32,6 +32,7 @@ struct RFwd {
   int res_buf;   // -1 none
   int res_mode;  // 1: identity (same shape), 2: option-A shortcut from a (2Ho x 2Wo x Cres) tensor
   int Cres;
+  int relu = 1;  // 0: store the raw conv output (ResNet-18: GroupNorm follows)
   __device__ void setup(GemmTile& t, int local) const {
     const int nt = cdiv(L.Cout, BN);
     t.M = t.tk.rows * L.Ho * L.Wo;
@@ -69,7 +70,7 @@ struct RFwd {
           const int r = m / hw, rem = m - r * hw, yo = rem / L.Wo, xo = rem - yo * L.Wo;
           v += ldv((const T*)t.c->buf[res_buf] + (((int64_t)r * 2 * L.Ho + 2 * yo) * 2 * L.Wo + 2 * xo) * Cres + n);
         }
-        stv(out + (int64_t)m * L.Cout + n, fmaxf(v, 0.f));
+        stv(out + (int64_t)m * L.Cout + n, relu ? fmaxf(v, 0.f) : v);
       }
   }
 };
@@ -111,7 +112,7 @@ struct RDgrad {
   }
   __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
     T* out = (T*)t.c->buf[out_buf];
-    const T* mask = (const T*)t.c->buf[mask_buf];
+    const T* mask = mask_buf < 0 ? nullptr : (const T*)t.c->buf[mask_buf];
     const int hw = L.H * L.W;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -129,7 +130,7 @@ struct RDgrad {
                      (((int64_t)r * (L.H / 2) + y / 2) * (L.W / 2) + x / 2) * Cadd + n);
         }
         const int64_t o = (int64_t)m * L.Cin + n;
-        stv(out + o, ldv(mask + o) > 0.f ? v : 0.f);
+        stv(out + o, mask_buf < 0 || ldv(mask + o) > 0.f ? v : 0.f);  // mask_buf -1: no ReLU mask here
       }
   }
 };
@@ -141,7 +142,8 @@ struct RWgrad {
   const ClientRec* recs;
   RConv L;
   int dout_buf, in_buf;  // in_buf -1: the u8 input image
-  int layer;             // partial region of this layer (r8_wsp_off)
+  int layer;             // partial region of this layer (r8_wsp_off); -1: the start of wsp_buf
+  int wsp_buf = B_R_WSP;
   __device__ void setup(GemmTile& t, int local) const {
     const int N = 9 * L.Cin + 1, nt = cdiv(N, BN), mt = cdiv(L.Cout, BM);
     t.split = local / (mt * nt);
@@ -169,7 +171,8 @@ struct RWgrad {
     return ldv((const T*)t.c->buf[in_buf] + (((int64_t)r * L.H + y) * L.W + x) * L.Cin + ci);
   }
   __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
-    float* part = (float*)t.c->buf[B_R_WSP] + r8_wsp_off(layer, t.c->B) + (int64_t)t.split * t.M * t.N;
+    float* part = (float*)t.c->buf[wsp_buf] + (layer >= 0 ? r8_wsp_off(layer, t.c->B) : 0) +
+                  (int64_t)t.split * t.M * t.N;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -221,10 +224,10 @@ __global__ void __launch_bounds__(256) k_rhead(RHeadArgs a, const Task* __restri
     float s = 0.f;
     for (int cc = 0; cc < C; ++cc) s += expf(dlog[r * C + cc] - mx);
     lossr[r] = logf(s) + mx - dlog[r * C + label];
-    const float inv = 1.f / (s * (float)rows);
+    const float inv = 1.f / (s * (float)tk.den);  // |beta|: the whole batch (micro-clients too)
     for (int cc = 0; cc < C; ++cc) {
       const float p = expf(dlog[r * C + cc] - mx);
-      dlog[r * C + cc] = p * inv - (cc == label ? 1.f / (float)rows : 0.f);
+      dlog[r * C + cc] = p * inv - (cc == label ? 1.f / (float)tk.den : 0.f);
     }
   }
   __syncthreads();
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(256) k_rhead(RHeadArgs a, const Task* __restri
   if (threadIdx.x == 0) {
     float s = 0.f;
     for (int r = 0; r < rows; ++r) s += lossr[r];
-    c->stats[0] += s / (float)rows;
+    c->stats[0] += s / (float)tk.den;
   }
 }
 

@@ -116,35 +116,43 @@ __device__ __forceinline__ void pool4(const float v[4], float& best, int& arg) {
 struct CnnDims {
   int c1, c2, f, classes;
   int64_t w1, b1, w2, b2, w3, b3, w4, b4;  // conv1, conv2, fc1, fc2 offsets in params
+  int H, W, C;  // input image (32x32x3 CIFAR-shaped; 28x28x1 FEMNIST-shaped, SIMT kernels only)
+  __host__ __device__ int HW() const { return H * W; }                 // conv1 output pixels
+  __host__ __device__ int W2() const { return W >> 1; }                // conv2 map width (pool 1)
+  __host__ __device__ int HW2() const { return (H >> 1) * (W >> 1); }  // conv2 map pixels
+  __host__ __device__ int W4() const { return W >> 2; }                // pool-2 output width
+  __host__ __device__ int HW4() const { return (H >> 2) * (W >> 2); }  // pool-2 output pixels
+  __host__ __device__ int K1() const { return HW4() * c2; }            // fc1 inputs
 };
 
 template <typename T, int BM, int BN>
-struct Conv1Fwd {  // M = rows*1024 (quad-major 32x32), N = c1, K = 75
+struct Conv1Fwd {  // M = rows*HW (quad-major over the pooled grid), N = c1, K = 25 C
   static constexpr bool A_KFAST = true, B_KFAST = true;
   const ClientRec* recs;
   CnnDims d;
   __device__ void setup(GemmTile& t, int local) const {
     const int nt = cdiv(d.c1, BN);
-    t.M = t.tk.rows * 1024;
+    t.M = t.tk.rows * d.HW();
     t.N = d.c1;
     t.m0 = (local / nt) * BM;
     t.n0 = (local % nt) * BN;
     t.kb = 0;
-    t.ke = 75;
-    t.split = t.c->perm[t.tk.base + (t.m0 >> 10)];  // sample index of the tile's image
+    t.ke = 25 * d.C;
   }
   __device__ float A(const GemmTile& t, int m, int k) const {
-    const int local = m & 1023, p = local >> 2, q = local & 3;
-    const int y = ((p >> 4) << 1) + (q >> 1), x = ((p & 15) << 1) + (q & 1);
-    const int tap = k / 3, ci = k - tap * 3, ky = tap / 5, kx = tap - ky * 5;
+    const int HW = d.HW(), r = m / HW, local = m - r * HW, p = local >> 2, q = local & 3;
+    const int py = p / d.W2(), px = p - py * d.W2();
+    const int y = (py << 1) + (q >> 1), x = (px << 1) + (q & 1);
+    const int tap = k / d.C, ci = k - tap * d.C, ky = tap / 5, kx = tap - ky * 5;
     const int sy = y + ky - 2, sx = x + kx - 2;
-    if ((unsigned)sy >= 32u || (unsigned)sx >= 32u) return 0.f;
-    return px01(t.c->x[(int64_t)t.split * 3072 + (sy * 32 + sx) * 3 + ci]);
+    if ((unsigned)sy >= (unsigned)d.H || (unsigned)sx >= (unsigned)d.W) return 0.f;
+    const int s = t.c->perm[t.tk.base + r];  // sample index of the row's image
+    return px01(t.c->x[(int64_t)s * HW * d.C + (sy * d.W + sx) * d.C + ci]);
   }
-  __device__ float B(const GemmTile& t, int k, int n) const { return t.c->params[d.w1 + (int64_t)n * 75 + k]; }
+  __device__ float B(const GemmTile& t, int k, int n) const { return t.c->params[d.w1 + (int64_t)n * 25 * d.C + k]; }
   __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
     if (mb >= t.M) return;
-    const int r = mb >> 10, p = (mb & 1023) >> 2;
+    const int r = mb / d.HW(), p = (mb - r * d.HW()) >> 2;
     T* a1 = (T*)t.c->buf[B_A1];
     uint8_t* i1 = (uint8_t*)t.c->buf[B_I1];
 #pragma unroll
@@ -156,7 +164,7 @@ struct Conv1Fwd {  // M = rows*1024 (quad-major 32x32), N = c1, K = 75
       float best;
       int arg;
       pool4(v, best, arg);
-      const int64_t o = ((int64_t)r * 256 + p) * d.c1 + n;
+      const int64_t o = ((int64_t)r * d.HW2() + p) * d.c1 + n;
       stv(a1 + o, best);
       i1[o] = (uint8_t)arg;
     }
@@ -164,13 +172,13 @@ struct Conv1Fwd {  // M = rows*1024 (quad-major 32x32), N = c1, K = 75
 };
 
 template <typename T, int BM, int BN>
-struct Conv2Fwd {  // M = rows*256 (quad-major 16x16), N = c2, K = 25*c1
+struct Conv2Fwd {  // M = rows*HW2 (quad-major over the pool-2 grid), N = c2, K = 25*c1
   static constexpr bool A_KFAST = true, B_KFAST = true;
   const ClientRec* recs;
   CnnDims d;
   __device__ void setup(GemmTile& t, int local) const {
     const int nt = cdiv(d.c2, BN);
-    t.M = t.tk.rows * 256;
+    t.M = t.tk.rows * d.HW2();
     t.N = d.c2;
     t.m0 = (local / nt) * BM;
     t.n0 = (local % nt) * BN;
@@ -178,20 +186,21 @@ struct Conv2Fwd {  // M = rows*256 (quad-major 16x16), N = c2, K = 25*c1
     t.ke = 25 * d.c1;
   }
   __device__ float A(const GemmTile& t, int m, int k) const {
-    const int r = m >> 8, local = m & 255, p = local >> 2, q = local & 3;
-    const int y = ((p >> 3) << 1) + (q >> 1), x = ((p & 7) << 1) + (q & 1);
+    const int HW2 = d.HW2(), W2 = d.W2(), r = m / HW2, local = m - r * HW2, p = local >> 2, q = local & 3;
+    const int py = p / d.W4(), px = p - py * d.W4();
+    const int y = (py << 1) + (q >> 1), x = (px << 1) + (q & 1);
     const int tap = k / d.c1, ci = k - tap * d.c1, ky = tap / 5, kx = tap - ky * 5;
     const int sy = y + ky - 2, sx = x + kx - 2;
-    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return 0.f;
+    if ((unsigned)sy >= (unsigned)(d.H >> 1) || (unsigned)sx >= (unsigned)W2) return 0.f;
     const T* a1 = (const T*)t.c->buf[B_A1];
-    return ldv(a1 + ((int64_t)r * 256 + sy * 16 + sx) * d.c1 + ci);
+    return ldv(a1 + ((int64_t)r * HW2 + sy * W2 + sx) * d.c1 + ci);
   }
   __device__ float B(const GemmTile& t, int k, int n) const {
     return t.c->params[d.w2 + (int64_t)n * 25 * d.c1 + k];
   }
   __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
     if (mb >= t.M) return;
-    const int r = mb >> 8, p = (mb & 255) >> 2;
+    const int r = mb / d.HW2(), p = (mb - r * d.HW2()) >> 2;
     T* a2 = (T*)t.c->buf[B_A2];
     uint8_t* i2 = (uint8_t*)t.c->buf[B_I2];
 #pragma unroll
@@ -203,7 +212,7 @@ struct Conv2Fwd {  // M = rows*256 (quad-major 16x16), N = c2, K = 25*c1
       float best;
       int arg;
       pool4(v, best, arg);
-      const int64_t o = ((int64_t)r * 64 + p) * d.c2 + n;
+      const int64_t o = ((int64_t)r * d.HW4() + p) * d.c2 + n;
       stv(a2 + o, best);
       i2[o] = (uint8_t)arg;
     }
@@ -211,7 +220,7 @@ struct Conv2Fwd {  // M = rows*256 (quad-major 16x16), N = c2, K = 25*c1
 };
 
 template <typename T, int BM, int BN>
-struct Fc1Fwd {  // M = rows, N = f, K = 64*c2
+struct Fc1Fwd {  // M = rows, N = f, K = K1 = HW4*c2
   static constexpr bool A_KFAST = true, B_KFAST = true;
   const ClientRec* recs;
   CnnDims d;
@@ -222,13 +231,13 @@ struct Fc1Fwd {  // M = rows, N = f, K = 64*c2
     t.m0 = (local / nt) * BM;
     t.n0 = (local % nt) * BN;
     t.kb = 0;
-    t.ke = 64 * d.c2;
+    t.ke = d.K1();
   }
   __device__ float A(const GemmTile& t, int m, int k) const {
-    return ldv((const T*)t.c->buf[B_A2] + (int64_t)m * 64 * d.c2 + k);
+    return ldv((const T*)t.c->buf[B_A2] + (int64_t)m * d.K1() + k);
   }
   __device__ float B(const GemmTile& t, int k, int n) const {
-    return t.c->params[d.w3 + (int64_t)n * 64 * d.c2 + k];
+    return t.c->params[d.w3 + (int64_t)n * d.K1() + k];
   }
   __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
     T* h = (T*)t.c->buf[B_H];
@@ -243,14 +252,14 @@ struct Fc1Fwd {  // M = rows, N = f, K = 64*c2
 };
 
 template <typename T, int BM, int BN>
-struct Fc1Dgrad {  // dA2 = dh W1: M = rows, N = 64*c2, K = f; epilogue: pool2 backward -> dz2 (16x16)
+struct Fc1Dgrad {  // dA2 = dh W1: M = rows, N = K1, K = f; epilogue: pool2 backward -> dz2 (conv2 map)
   static constexpr bool A_KFAST = true, B_KFAST = false;
   const ClientRec* recs;
   CnnDims d;
   __device__ void setup(GemmTile& t, int local) const {
-    const int nt = cdiv(64 * d.c2, BN);
+    const int nt = cdiv(d.K1(), BN);
     t.M = t.tk.rows;
-    t.N = 64 * d.c2;
+    t.N = d.K1();
     t.m0 = (local / nt) * BM;
     t.n0 = (local % nt) * BN;
     t.kb = 0;
@@ -260,7 +269,7 @@ struct Fc1Dgrad {  // dA2 = dh W1: M = rows, N = 64*c2, K = f; epilogue: pool2 b
     return ldv((const T*)t.c->buf[B_DH] + (int64_t)m * d.f + k);
   }
   __device__ float B(const GemmTile& t, int k, int n) const {
-    return t.c->params[d.w3 + (int64_t)k * 64 * d.c2 + n];
+    return t.c->params[d.w3 + (int64_t)k * d.K1() + n];
   }
   __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
     const T* a2 = (const T*)t.c->buf[B_A2];
@@ -276,26 +285,26 @@ struct Fc1Dgrad {  // dA2 = dh W1: M = rows, N = 64*c2, K = f; epilogue: pool2 b
         const int64_t o = (int64_t)m * N + n;
         const float v = ldv(a2 + o) > 0.f ? acc[i][j] : 0.f;
         const int arg = i2[o];
-        const int p = n / d.c2, c = n - p * d.c2, py = p >> 3, px = p & 7;
+        const int p = n / d.c2, c = n - p * d.c2, py = p / d.W4(), px = p - py * d.W4();
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int y = 2 * py + (q >> 1), x = 2 * px + (q & 1);
-          stv(dz2 + ((int64_t)m * 256 + y * 16 + x) * d.c2 + c, q == arg ? v : 0.f);
+          stv(dz2 + ((int64_t)m * d.HW2() + y * d.W2() + x) * d.c2 + c, q == arg ? v : 0.f);
         }
       }
   }
 };
 
 template <typename T, int BM, int BN>
-struct Fc1Wgrad {  // W1 -= lr dh^T a2: M = f, N = 64*c2, K = rows (fc1 bias: k_head)
+struct Fc1Wgrad {  // W1 -= lr dh^T a2: M = f, N = K1, K = rows (fc1 bias: k_head)
   static constexpr bool A_KFAST = false, B_KFAST = false;
   const ClientRec* recs;
   CnnDims d;
   float lr;
   __device__ void setup(GemmTile& t, int local) const {
-    const int nt = cdiv(64 * d.c2, BN);
+    const int nt = cdiv(d.K1(), BN);
     t.M = d.f;
-    t.N = 64 * d.c2;
+    t.N = d.K1();
     t.m0 = (local / nt) * BM;
     t.n0 = (local % nt) * BN;
     t.kb = 0;
@@ -305,10 +314,10 @@ struct Fc1Wgrad {  // W1 -= lr dh^T a2: M = f, N = 64*c2, K = rows (fc1 bias: k_
     return ldv((const T*)t.c->buf[B_DH] + (int64_t)k * d.f + m);
   }
   __device__ float B(const GemmTile& t, int k, int n) const {
-    return ldv((const T*)t.c->buf[B_A2] + (int64_t)k * 64 * d.c2 + n);
+    return ldv((const T*)t.c->buf[B_A2] + (int64_t)k * d.K1() + n);
   }
   __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
-    const int K1 = 64 * d.c2;
+    const int K1 = d.K1();
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -322,13 +331,13 @@ struct Fc1Wgrad {  // W1 -= lr dh^T a2: M = f, N = 64*c2, K = rows (fc1 bias: k_
 };
 
 template <typename T, int BM, int BN>
-struct Conv2Dgrad {  // dA1: M = rows*256 (row-major 16x16), N = c1, K = 25*c2; epilogue pool1 backward -> dz1
+struct Conv2Dgrad {  // dA1: M = rows*HW2 (row-major), N = c1, K = 25*c2; epilogue pool1 backward -> dz1
   static constexpr bool A_KFAST = true, B_KFAST = false;
   const ClientRec* recs;
   CnnDims d;
   __device__ void setup(GemmTile& t, int local) const {
     const int nt = cdiv(d.c1, BN);
-    t.M = t.tk.rows * 256;
+    t.M = t.tk.rows * d.HW2();
     t.N = d.c1;
     t.m0 = (local / nt) * BM;
     t.n0 = (local % nt) * BN;
@@ -336,11 +345,11 @@ struct Conv2Dgrad {  // dA1: M = rows*256 (row-major 16x16), N = c1, K = 25*c2; 
     t.ke = 25 * d.c2;
   }
   __device__ float A(const GemmTile& t, int m, int k) const {
-    const int r = m >> 8, y = (m >> 4) & 15, x = m & 15;
+    const int HW2 = d.HW2(), W2 = d.W2(), r = m / HW2, rem = m - r * HW2, y = rem / W2, x = rem - y * W2;
     const int tap = k / d.c2, co = k - tap * d.c2, ky = tap / 5, kx = tap - ky * 5;
     const int sy = y - ky + 2, sx = x - kx + 2;
-    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return 0.f;
-    return ldv((const T*)t.c->buf[B_DZ2] + ((int64_t)r * 256 + sy * 16 + sx) * d.c2 + co);
+    if ((unsigned)sy >= (unsigned)(d.H >> 1) || (unsigned)sx >= (unsigned)W2) return 0.f;
+    return ldv((const T*)t.c->buf[B_DZ2] + ((int64_t)r * HW2 + sy * W2 + sx) * d.c2 + co);
   }
   __device__ float B(const GemmTile& t, int k, int n) const {
     const int tap = k / d.c2, co = k - tap * d.c2;
@@ -359,11 +368,11 @@ struct Conv2Dgrad {  // dA1: M = rows*256 (row-major 16x16), N = c1, K = 25*c2; 
         const int64_t o = (int64_t)m * d.c1 + n;
         const float v = ldv(a1 + o) > 0.f ? acc[i][j] : 0.f;
         const int arg = i1[o];
-        const int r = m >> 8, y = (m >> 4) & 15, x = m & 15;
+        const int HW2 = d.HW2(), W2 = d.W2(), r = m / HW2, rem = m - r * HW2, y = rem / W2, x = rem - y * W2;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int Y = 2 * y + (q >> 1), X = 2 * x + (q & 1);
-          stv(dz1 + ((int64_t)r * 1024 + Y * 32 + X) * d.c1 + n, q == arg ? v : 0.f);
+          stv(dz1 + ((int64_t)r * d.HW() + Y * d.W + X) * d.c1 + n, q == arg ? v : 0.f);
         }
       }
   }
@@ -371,7 +380,7 @@ struct Conv2Dgrad {  // dA1: M = rows*256 (row-major 16x16), N = c1, K = 25*c2; 
 
 // conv wgrad, split-K: partial[split][m][n] for n in [0, N) (N = K_w + 1 bias column)
 template <typename T, int BM, int BN>
-struct Conv2Wgrad {  // M = c2, N = 25*c1 + 1, K = rows*256 pixels (splits of 2048)
+struct Conv2Wgrad {  // M = c2, N = 25*c1 + 1, K = rows*HW2 pixels (splits of 2048)
   static constexpr bool A_KFAST = false, B_KFAST = false;
   const ClientRec* recs;
   CnnDims d;
@@ -384,7 +393,7 @@ struct Conv2Wgrad {  // M = c2, N = 25*c1 + 1, K = rows*256 pixels (splits of 20
     t.m0 = (rem / nt) * BM;
     t.n0 = (rem % nt) * BN;
     t.kb = t.split * kWgradChunkPx;
-    t.ke = min(t.tk.rows * 256, t.kb + kWgradChunkPx);
+    t.ke = min(t.tk.rows * d.HW2(), t.kb + kWgradChunkPx);
   }
   __device__ float A(const GemmTile& t, int m, int k) const {
     return ldv((const T*)t.c->buf[B_DZ2] + (int64_t)k * d.c2 + m);
@@ -392,11 +401,11 @@ struct Conv2Wgrad {  // M = c2, N = 25*c1 + 1, K = rows*256 pixels (splits of 20
   __device__ float B(const GemmTile& t, int k, int n) const {
     const int Kw = 25 * d.c1;
     if (n == Kw) return 1.f;
-    const int r = k >> 8, y = (k >> 4) & 15, x = k & 15;
+    const int HW2 = d.HW2(), W2 = d.W2(), r = k / HW2, rem = k - r * HW2, y = rem / W2, x = rem - y * W2;
     const int tap = n / d.c1, ci = n - tap * d.c1, ky = tap / 5, kx = tap - ky * 5;
     const int sy = y + ky - 2, sx = x + kx - 2;
-    if ((unsigned)sy >= 16u || (unsigned)sx >= 16u) return 0.f;
-    return ldv((const T*)t.c->buf[B_A1] + ((int64_t)r * 256 + sy * 16 + sx) * d.c1 + ci);
+    if ((unsigned)sy >= (unsigned)(d.H >> 1) || (unsigned)sx >= (unsigned)W2) return 0.f;
+    return ldv((const T*)t.c->buf[B_A1] + ((int64_t)r * HW2 + sy * W2 + sx) * d.c1 + ci);
   }
   __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
     float* part = (float*)t.c->buf[B_WSP] + (int64_t)t.split * t.M * t.N;
@@ -411,12 +420,12 @@ struct Conv2Wgrad {  // M = c2, N = 25*c1 + 1, K = rows*256 pixels (splits of 20
 };
 
 template <typename T, int BM, int BN>
-struct Conv1Wgrad {  // M = c1, N = 76, K = rows*1024 pixels (splits of 2048)
+struct Conv1Wgrad {  // M = c1, N = 25 C + 1, K = rows*HW pixels (splits of 2048)
   static constexpr bool A_KFAST = false, B_KFAST = false;
   const ClientRec* recs;
   CnnDims d;
   __device__ void setup(GemmTile& t, int local) const {
-    const int N = 76, nt = cdiv(N, BN), mt = cdiv(d.c1, BM);
+    const int N = 25 * d.C + 1, nt = cdiv(N, BN), mt = cdiv(d.c1, BM);
     t.split = local / (mt * nt);
     const int rem = local - t.split * mt * nt;
     t.M = d.c1;
@@ -424,19 +433,19 @@ struct Conv1Wgrad {  // M = c1, N = 76, K = rows*1024 pixels (splits of 2048)
     t.m0 = (rem / nt) * BM;
     t.n0 = (rem % nt) * BN;
     t.kb = t.split * kWgradChunkPx;
-    t.ke = min(t.tk.rows * 1024, t.kb + kWgradChunkPx);
+    t.ke = min(t.tk.rows * d.HW(), t.kb + kWgradChunkPx);
   }
   __device__ float A(const GemmTile& t, int m, int k) const {
     return ldv((const T*)t.c->buf[B_DZC1] + (int64_t)k * d.c1 + m);
   }
   __device__ float B(const GemmTile& t, int k, int n) const {
-    if (n == 75) return 1.f;
-    const int r = k >> 10, y = (k >> 5) & 31, x = k & 31;
-    const int tap = n / 3, ci = n - tap * 3, ky = tap / 5, kx = tap - ky * 5;
+    if (n == 25 * d.C) return 1.f;
+    const int HW = d.HW(), r = k / HW, rem = k - r * HW, y = rem / d.W, x = rem - y * d.W;
+    const int tap = n / d.C, ci = n - tap * d.C, ky = tap / 5, kx = tap - ky * 5;
     const int sy = y + ky - 2, sx = x + kx - 2;
-    if ((unsigned)sy >= 32u || (unsigned)sx >= 32u) return 0.f;
+    if ((unsigned)sy >= (unsigned)d.H || (unsigned)sx >= (unsigned)d.W) return 0.f;
     const int s = t.c->perm[t.tk.base + r];
-    return px01(t.c->x[(int64_t)s * 3072 + (sy * 32 + sx) * 3 + ci]);
+    return px01(t.c->x[(int64_t)s * HW * d.C + (sy * d.W + sx) * d.C + ci]);
   }
   __device__ void epilogue(const GemmTile& t, int mb, int nb, float acc[4][4]) const {
     float* part = (float*)t.c->buf[B_WSP] + (int64_t)t.split * t.M * t.N;
@@ -668,10 +677,10 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a, const Task* _
     float s = 0.f;
     for (int cc = 0; cc < C; ++cc) s += expf(dlog[r * C + cc] - mx);
     lossr[r] = logf(s) + mx - dlog[r * C + label];
-    const float inv = 1.f / (s * (float)rows);
+    const float inv = 1.f / (s * (float)tk.den);  // |beta|: the whole batch (micro-clients too)
     for (int cc = 0; cc < C; ++cc) {
       const float p = expf(dlog[r * C + cc] - mx);
-      dlog[r * C + cc] = p * inv - (cc == label ? 1.f / (float)rows : 0.f);
+      dlog[r * C + cc] = p * inv - (cc == label ? 1.f / (float)tk.den : 0.f);
     }
   }
   __syncthreads();
@@ -706,7 +715,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(HeadArgs a, const Task* _
   if (threadIdx.x == 0) {
     float s = 0.f;
     for (int r = 0; r < rows; ++r) s += lossr[r];
-    c->stats[0] += s / (float)rows;
+    c->stats[0] += s / (float)tk.den;
   }
 }
 
@@ -845,10 +854,10 @@ __global__ void __launch_bounds__(kHeadCnnThreads)
     float s = 0.f;
     for (int cc = 0; cc < C; ++cc) s += expf(dlog[r * C + cc] - mx);
     lossr[r] = logf(s) + mx - dlog[r * C + label];
-    const float inv = 1.f / (s * (float)rows);
+    const float inv = 1.f / (s * (float)tk.den);  // |beta|: the whole batch (micro-clients too)
     for (int cc = 0; cc < C; ++cc) {
       const float p = expf(dlog[r * C + cc] - mx);
-      dlog[r * C + cc] = p * inv - (cc == label ? 1.f / (float)rows : 0.f);
+      dlog[r * C + cc] = p * inv - (cc == label ? 1.f / (float)tk.den : 0.f);
     }
   }
   __syncthreads();
@@ -891,7 +900,7 @@ __global__ void __launch_bounds__(kHeadCnnThreads)
   if (threadIdx.x == 0) {
     float s = 0.f;
     for (int r = 0; r < rows; ++r) s += lossr[r];
-    c->stats[0] += s / (float)rows;
+    c->stats[0] += s / (float)tk.den;
     if (c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(globaltimer() - t_start));
   }
 }

@@ -96,8 +96,26 @@ struct has_pfinish {
   static constexpr bool value = f<Op>(nullptr);
 };
 
+template <class Op>
+struct has_block_epi {  // the op drains the whole TMEM tile itself (all 8 epilogue warps, shared memory)
+  template <class U>
+  static constexpr bool f(decltype(U::BLOCK_EPI)*) { return U::BLOCK_EPI; }
+  template <class U>
+  static constexpr bool f(...) { return false; }
+  static constexpr bool value = f<Op>(nullptr);
+};
+
+template <class Op>
+struct min_blocks {  // resident CTAs per SM the op is compiled for (register cap), default 1
+  template <class U>
+  static constexpr int f(decltype(U::MIN_BLOCKS)*) { return U::MIN_BLOCKS; }
+  template <class U>
+  static constexpr int f(...) { return 1; }
+  static constexpr int value = f<Op>(nullptr);
+};
+
 template <int BN, int STAGES, class Op>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreads, min_blocks<Op>::value)
     k_gemm_tc(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
   constexpr bool TMA = has_tma<Op>::value;
   constexpr int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
@@ -195,13 +213,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
 
     // ---------------- epilogue: TMEM -> registers -> fused layer epilogue
-    tc::mbar_wait(done, 0);
-    tc::fence_after();
-    const int row = (warp & 3) * 32 + lane;
-    for (int c0 = (warp >> 2) * 16; c0 < t.n_mma; c0 += 32) {
-      float v[16];
-      tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
-      op.epilogue(t, row, c0, v);
+    if constexpr (has_block_epi<Op>::value) {
+      op.block_epilogue(t, smem, tmem, warp, lane, done);  // waits for the MMAs itself (after its first loads)
+    } else {
+      tc::mbar_wait(done, 0);
+      tc::fence_after();
+      const int row = (warp & 3) * 32 + lane;
+      for (int c0 = (warp >> 2) * 16; c0 < t.n_mma; c0 += 32) {
+        float v[16];
+        tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
+        op.epilogue(t, row, c0, v);
+      }
     }
   } else {
     // ---------------- MMA issuer (warp 8, elected lane issues)
@@ -644,26 +666,62 @@ struct TcFc1Wgrad {  // M = K1 (input features), N = F (outputs), K = rows; W <-
   }
   __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const { return s.p; }
   // SGD on the fp32 master held as split planes (device.cuh): read hi + lo (4 B), write hi + lo (4 B) —
-  // exactly SURVEY §8(d)'s 8 B per weight per client-step; the new hi plane is next step's operand
-  __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {
-    const int k1 = t.m0 + row;
-    constexpr int64_t NW = (int64_t)W::F * W::K1;
-    uint16_t* H = reinterpret_cast<uint16_t*>(t.c->params + d.w3) + k1;
-    uint16_t* L = H + NW;
-    const int64_t f0 = t.n0 + c0;
-    uint16_t h[16], l[16];
+  // exactly SURVEY §8(d)'s 8 B per weight per client-step; the new hi plane is next step's operand.
+  // A tile column (output f, the tile's 128 k1) is one 128-block of the layout: 256 B of upper halves and the
+  // 256 B of lower halves right after them.  The 8 epilogue warps drain the tile 32 columns per pass through
+  // shared memory (the free operand stage): coalesced 8-byte loads (one warp = one column = 2 x 256 B), each
+  // thread updates its TMEM row's 16 columns in shared memory, coalesced 8-byte stores.
+  static constexpr bool BLOCK_EPI = true;
+  static constexpr int MIN_BLOCKS = 4;  // HBM-bound: 4 CTAs per SM (<= 56 registers)
+  // Software-pipelined over passes of 32 columns: the first pass's weights are loaded before the MMAs are
+  // waited for, and pass p + 1's loads are in flight while pass p is updated in shared memory (two 16 KB
+  // staging buffers in the free operand stage).
+  __device__ void block_epilogue(const TcTile& t, uint8_t* smem, uint32_t tmem, int warp, int lane,
+                                 uint32_t done) const {
+    uint16_t* Hp = reinterpret_cast<uint16_t*>(t.c->params + d.w3) + (t.m0 >> 7) * 256;  // this tile's k1 block
+    uint16_t* Lp = Hp + 128;
+    const int row = (warp & 3) * 32 + lane, cl = (warp >> 2) * 16;
+    uint2 h[4], l[4];
+    auto load = [&](int cb) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {  // 32 independent loads in flight
-      h[j] = H[(f0 + j) * W::K1];
-      l[j] = L[(f0 + j) * W::K1];
-    }
+      for (int i = 0; i < 4; ++i) {
+        const int64_t o = (int64_t)(t.n0 + cb + 4 * warp + i) * 2 * W::K1 + 4 * lane;
+        h[i] = *reinterpret_cast<const uint2*>(Hp + o);
+        l[i] = *reinterpret_cast<const uint2*>(Lp + o);
+      }
+    };
+    load(0);
+    tc::mbar_wait(done, 0);
+    tc::fence_after();
+    for (int cb = 0, buf = 0; cb < t.n_mma; cb += 32, buf ^= 1) {
+      uint16_t* sh = reinterpret_cast<uint16_t*>(smem) + buf * 8192;  // [32 columns][128 rows] x {hi, lo}
+      uint16_t* sl = sh + 4096;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t u = __float_as_uint(split_join(h[j], l[j]) - lr * v[j]);
-      H[(f0 + j) * W::K1] = (uint16_t)(u >> 16);
-      L[(f0 + j) * W::K1] = (uint16_t)(u & 0xFFFFu);
+      for (int i = 0; i < 4; ++i) {
+        *reinterpret_cast<uint2*>(sh + (4 * warp + i) * 128 + 4 * lane) = h[i];
+        *reinterpret_cast<uint2*>(sl + (4 * warp + i) * 128 + 4 * lane) = l[i];
+      }
+      if (cb + 32 < t.n_mma) load(cb + 32);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      float v[16];
+      tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(cb + cl), v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int idx = (cl + j) * 128 + row;
+        const uint32_t u = __float_as_uint(split_join(sh[idx], sl[idx]) - lr * v[j]);
+        sh[idx] = (uint16_t)(u >> 16);
+        sl[idx] = (uint16_t)(u & 0xFFFFu);
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t o = (int64_t)(t.n0 + cb + 4 * warp + i) * 2 * W::K1 + 4 * lane;
+        *reinterpret_cast<uint2*>(Hp + o) = *reinterpret_cast<const uint2*>(sh + (4 * warp + i) * 128 + 4 * lane);
+        *reinterpret_cast<uint2*>(Lp + o) = *reinterpret_cast<const uint2*>(sl + (4 * warp + i) * 128 + 4 * lane);
+      }
     }
   }
+  __device__ void epilogue(const TcTile&, int, int, const float (&)[16]) const {}
 };
 
 // --------------------------------------------------------------------------
@@ -842,7 +900,7 @@ struct TmaFc1Fwd : TcFc1Fwd<WQ> {
   __device__ void init_stage(const TcTile&, uint8_t*, uint8_t*) const {}
   __device__ uint32_t tx_bytes(const TcTile& t, int kb) const { return 16384 + 128 * batch_rows16(t); }
   __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
-    tc::tma_load_2d(a, tmap_of(t, TM_W3K), mbar, kb * 64, t.m0);  // [128 f][64 k] swizzled
+    tc::tma_load_3d(a, tmap_of(t, TM_W3K), mbar, (kb & 1) * 64, kb >> 1, t.m0);  // [128 f][64 k] swizzled
     tc::tma_load_2d(b, tmap_of(t, TM_A2), mbar, kb * 64, 0);      // [R rows][64 k] swizzled
   }
   __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {
@@ -860,8 +918,8 @@ struct TmaFc1Dgrad : TcFc1Dgrad<WQ> {
   __device__ void init_stage(const TcTile&, uint8_t*, uint8_t*) const {}
   __device__ uint32_t tx_bytes(const TcTile& t, int kb) const { return 16384 + 128 * batch_rows16(t); }
   __device__ void tma_issue(const TcTile& t, int kb, uint32_t a, uint32_t b, uint32_t mbar) const {
-    tc::tma_load_2d(a, tmap_of(t, TM_W3M), mbar, t.m0, kb * 64);            // [64 f][64 m] swizzled
-    tc::tma_load_2d(a + 8192, tmap_of(t, TM_W3M), mbar, t.m0 + 64, kb * 64);  // next 64 m
+    tc::tma_load_3d(a, tmap_of(t, TM_W3M), mbar, 0, t.m0 >> 7, kb * 64);          // [64 f][64 m] swizzled
+    tc::tma_load_3d(a + 8192, tmap_of(t, TM_W3M), mbar, 64, t.m0 >> 7, kb * 64);  // next 64 m
     tc::tma_load_2d(b, tmap_of(t, TM_DH), mbar, kb * 64, 0);                 // [R rows][64 f] swizzled
   }
   __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {

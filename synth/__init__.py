@@ -30,8 +30,14 @@ import numpy as np
 FEMNIST = dict(H=28, W=28, C=1)
 CIFAR = dict(H=32, W=32, C=3)
 
-MODEL_MLP, MODEL_CNN, MODEL_RESNET8 = 0, 1, 2
-MODEL_NAMES = {MODEL_MLP: "mlp", MODEL_CNN: "cnn", MODEL_RESNET8: "resnet8"}
+MODEL_MLP, MODEL_CNN, MODEL_RESNET8, MODEL_CNN28, MODEL_RESNET18 = 0, 1, 2, 3, 4
+MODEL_NAMES = {MODEL_MLP: "mlp", MODEL_CNN: "cnn", MODEL_RESNET8: "resnet8", MODEL_CNN28: "cnn28",
+               MODEL_RESNET18: "resnet18"}
+# the library's arch and input shape of each harness model (MODEL_CNN28 = the CNN-w family on the
+# FEMNIST-shaped 28x28x1 input of the paper's LEAF experiment; the library's arch CNN at 28x28x1)
+LIB_ARCH = {MODEL_MLP: 0, MODEL_CNN: 1, MODEL_RESNET8: 2, MODEL_CNN28: 1, MODEL_RESNET18: 3}
+INPUT_SHAPE = {MODEL_MLP: (28, 28, 1), MODEL_CNN: (32, 32, 3), MODEL_RESNET8: (32, 32, 3), MODEL_CNN28: (28, 28, 1),
+               MODEL_RESNET18: (32, 32, 3)}
 
 
 def width_channels(width_q: int) -> tuple[int, int, int]:
@@ -54,12 +60,28 @@ def param_segments(model: int, width_q: int = 4, classes: int = 10):
     if model == MODEL_MLP:
         fc(784, 64)
         fc(64, classes)
-    elif model == MODEL_CNN:
+    elif model in (MODEL_CNN, MODEL_CNN28):
         c1, c2, f = width_channels(width_q)
-        conv(5, 3, c1)
+        cin, pooled = (3, 64) if model == MODEL_CNN else (1, 49)
+        conv(5, cin, c1)
         conv(5, c1, c2)
-        fc(64 * c2, f)
+        fc(pooled * c2, f)
         fc(f, classes)
+    elif model == MODEL_RESNET18:  # conv W, b, then GroupNorm gamma = 1, beta = 0 (fan_in 0: constants)
+        def gn(c):
+            segs.append((c, -1))
+            segs.append((c, 0))
+        conv(3, 3, 64)
+        gn(64)
+        cin = 64
+        for s_, c in enumerate((64, 128, 256, 512)):
+            for _b in range(2):
+                conv(3, cin, c)
+                gn(c)
+                conv(3, c, c)
+                gn(c)
+                cin = c
+        fc(512, classes)
     elif model == MODEL_RESNET8:
         conv(3, 3, 16)
         conv(3, 16, 16)
@@ -79,6 +101,9 @@ def init_weights(model: int, width_q: int = 4, classes: int = 10, seed: int = 0)
     rng = np.random.Generator(np.random.PCG64([0x1A17, seed, model, width_q, classes]))
     out = []
     for n, fan_in in param_segments(model, width_q, classes):
+        if fan_in <= 0:  # GroupNorm gamma (-1) = 1, beta (0) = 0
+            out.append(np.full(n, 1.0 if fan_in < 0 else 0.0))
+            continue
         bound = 1.0 / math.sqrt(fan_in)
         out.append(rng.uniform(-bound, bound, size=n))
     return np.concatenate(out).astype(np.float32)
@@ -228,6 +253,18 @@ def build_workload(config: int, *, k=None, n_clients=None, samples=None, epochs=
         sizes = dirichlet_sizes(n_pool, (samples or 50) * n_pool, 0.5, seed=0)
         ids = sample_clients(n_pool, k or 500, seed, 0)
         mk = lambda i: Client(int(i), int(sizes[i]), BATCHES[i % 4], epochs or 2, model, 4, classes)
+    elif config == 7:  # the paper's CIFAR experiment model: ResNet-18 (GroupNorm, R26), pool 100
+        model, shape, classes = MODEL_RESNET18, CIFAR, 10
+        n_pool = n_clients or 100
+        sizes = np.full(n_pool, samples or 500)
+        ids = np.arange(n_pool) if k is None else sample_clients(n_pool, k, seed, 0)
+        mk = lambda i: Client(int(i), int(sizes[i]), BATCHES[i % 4], epochs or 1, model, 4, classes)
+    elif config == 6:  # the paper's FEMNIST experiment shape: 3597 writers, 62 classes, 28x28x1
+        model, shape, classes = MODEL_CNN28, FEMNIST, 62
+        n_pool = n_clients or 3597
+        sizes = dirichlet_sizes(n_pool, (samples or 226) * n_pool, 0.5, seed=0)
+        ids = sample_clients(n_pool, k or 100, seed, 0)
+        mk = lambda i: Client(int(i), int(sizes[i]), BATCHES[i % 4], epochs or 1, model, 4, classes)
     else:
         raise ValueError(config)
     wl = Workload(name=f"config{config}", model=model, shape=shape, classes=classes,

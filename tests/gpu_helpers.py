@@ -7,7 +7,12 @@ from oracle import round as orr
 
 
 def shape_of(model):
-    return (28, 28, 1) if model == synth.MODEL_MLP else (32, 32, 3)
+    return synth.INPUT_SHAPE[model]
+
+
+def arch_of(model):
+    """the library's arch id of a harness model (MODEL_CNN28 = the CNN arch on a 28x28x1 input)"""
+    return synth.LIB_ARCH[model]
 
 
 def widths_of(wl, all_widths=False):
@@ -28,7 +33,7 @@ def gpu_run(wl, rounds=1, precision=0, lr=0.05, arena_bytes=None, shuffle=True, 
     H, W, C = shape_of(wl.model)
     if sim is None:
         sim = Simulation(precision=precision, arena_bytes=arena_bytes or (1 << 30))
-    mids = {wq: sim.register_model(wl.model, wq, wl.classes, H, W, C) for wq in widths}
+    mids = {wq: sim.register_model(arch_of(wl.model), wq, wl.classes, H, W, C) for wq in widths}
     sim.register_shards([(c.id, wl.shards[c.id][0], wl.shards[c.id][1]) for c in wl.clients])
     clients = sim.clients([(c.id, mids[c.width_q], c.batch, c.epochs) for c in wl.clients])
     prof = sim.profile(clients)

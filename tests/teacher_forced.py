@@ -44,17 +44,19 @@ def _act(raw, off, size, elem, shape):
 
 
 def master_weights(c, raw, elem):
-    """The fp32 master weights at the start of a slot snapshot.  bf16-mode CNN: fc1's W is stored as two
-    16-bit planes (hi = upper halves, then lo) in its fp32 region (DESIGN.md §5 "split planes")."""
+    """The fp32 master weights at the start of a slot snapshot.  bf16-mode CNN: fc1's W is stored as 16-bit
+    halves, per row f and 128-block of k1: 128 upper halves then 128 lower halves (DESIGN.md §5 "split
+    planes")."""
     P = sgd.n_params(c.model, c.width_q, c.classes)
     w = raw[:4 * P].copy().view(np.float32)
-    if elem == 2 and c.model == sgd.CNN:
+    if elem == 2 and c.model == sgd.CNN:  # (the tcgen05 path; CNN28 runs SIMT kernels on plain fp32)
         c1, c2, f = sgd.cnn_channels(c.width_q)
         off = (c1 * 75 + c1) + (c2 * 25 * c1 + c2)
         nw = f * 64 * c2
-        planes = raw[4 * off:4 * (off + nw)].view(np.uint16)
-        u = (planes[:nw].astype(np.uint32) << 16) | planes[nw:].astype(np.uint32)
-        w[off:off + nw] = u.view(np.float32)
+        K1 = nw // f
+        blocks = raw[4 * off:4 * (off + nw)].view(np.uint16).reshape(f, K1 // 128, 2, 128)
+        u = (blocks[:, :, 0, :].astype(np.uint32) << 16) | blocks[:, :, 1, :].astype(np.uint32)
+        w[off:off + nw] = u.reshape(-1).view(np.float32)
     return w
 
 
@@ -83,12 +85,13 @@ def decode_snapshot(c, raw, elem, rows):
     if c.model == sgd.MLP:
         o, n = lay["h1"]
         dec["h1"] = _act(raw, o, n, elem, (B, 64))[:rows]
-    elif c.model == sgd.CNN:
+    elif c.model in (sgd.CNN, sgd.CNN28):
         c1, c2, f = sgd.cnn_channels(c.width_q)
-        for k, shp in (("a1", (B, 16, 16, c1)), ("a2", (B, 8, 8, c2)), ("h", (B, f))):
+        s1, s2 = (16, 8) if c.model == sgd.CNN else (14, 7)
+        for k, shp in (("a1", (B, s1, s1, c1)), ("a2", (B, s2, s2, c2)), ("h", (B, f))):
             o, n = lay[k]
             dec[k] = _act(raw, o, n, elem, shp)[:rows]
-        for k, shp in (("i1", (B, 16, 16, c1)), ("i2", (B, 8, 8, c2))):
+        for k, shp in (("i1", (B, s1, s1, c1)), ("i2", (B, s2, s2, c2))):
             o, n = lay[k]
             dec[k] = raw[o:o + n].astype(np.int64).reshape(shp)[:rows]
     else:
@@ -109,8 +112,8 @@ def bench_round_with_trace(wl, precision, trace_ids, lr=None, rnd=0):
     import paper_2207_01053_b200 as pb
     from paper_2207_01053_b200.sim import Simulation
     lr = wl.lr if lr is None else lr
-    arch = wl.model
-    H, W, C = (28, 28, 1) if arch == synth.MODEL_MLP else (32, 32, 3)
+    arch = synth.LIB_ARCH[wl.model]
+    H, W, C = synth.INPUT_SHAPE[wl.model]
     foot = np.zeros(len(wl.clients), dtype=pb.PROFILE_DT)
     for i, c in enumerate(wl.clients):
         pk, st, fl = pb.protea_client_footprint(arch, c.width_q, c.classes, H, W, C, c.n, c.batch, c.epochs,
@@ -126,7 +129,7 @@ def bench_round_with_trace(wl, precision, trace_ids, lr=None, rnd=0):
     hk = {int(f["client_id"]): int(f["peak_bytes"]) for f in foot}
     bufs = {cid: torch.empty((sgd.steps(byid[cid].n, byid[cid].batch, byid[cid].epochs) + 1) * hk[cid],
                              dtype=torch.uint8, device=sim.device) for cid in trace_ids}
-    g = torch.tensor(synth.init_weights(arch, 4, wl.classes), device=sim.device)
+    g = torch.tensor(synth.init_weights(wl.model, 4, wl.classes), device=sim.device)
     out, st = sim.run_round(clients, plan, g, lr=lr, seed=wl.seed, rnd=rnd, trace=bufs)
     snaps = {cid: b.view(-1, hk[cid]).cpu().numpy() for cid, b in bufs.items()}
     sim.close()

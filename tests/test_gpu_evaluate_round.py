@@ -11,7 +11,7 @@ import pytest
 
 import synth
 from oracle import evaluate as oev
-from tests.gpu_helpers import gpu_run, shape_of, widths_of
+from tests.gpu_helpers import arch_of, gpu_run, shape_of, widths_of
 
 pytestmark = pytest.mark.gpu
 
@@ -33,7 +33,8 @@ def _margin_count(w, c, x, y, tol):
 
 
 CASES = [(1, dict(n_clients=6, samples=90)), (4, dict(k=9, samples=60)), (5, dict(n_clients=300, k=6, samples=80)),
-         (2, dict(n_clients=3, samples=700))]  # config 2: 78 validation rows -> two micro-clients
+         (2, dict(n_clients=3, samples=700)),  # config 2: 78 validation rows -> two micro-clients
+         (6, dict(n_clients=200, k=5, samples=120))]  # FEMNIST-shaped CNN, 62 classes
 
 
 @pytest.mark.parametrize("precision", [0, 1])
@@ -47,7 +48,7 @@ def test_evaluate_round_vs_oracle(torch, config, kw, precision):
     trained, _ = gpu_run(wl, precision=0)  # a trained global model (one fp32 round) to evaluate
     sim = Simulation(precision=precision, arena_bytes=1 << 30)
     H, W, C = shape_of(wl.model)
-    mids = {q: sim.register_model(wl.model, q, wl.classes, H, W, C) for q in widths}
+    mids = {q: sim.register_model(arch_of(wl.model), q, wl.classes, H, W, C) for q in widths}
     sim.register_val_shards([(c.id, *val[c.id]) for c in wl.clients])
     clients = sim.clients([(c.id, mids[c.width_q], c.batch, c.epochs) for c in wl.clients])
     g = torch.tensor(concat_globals([trained[q] for q in widths]), device="cuda")

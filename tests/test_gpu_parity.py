@@ -158,7 +158,7 @@ def test_abi_errors_on_gpu(torch):
         sim.run_round(clients, ex["plan"], g[:-1])
     assert e.value.name == "DIM"
     c2 = clients.copy()
-    c2["batch"][0] = 65
+    c2["batch"][0] = 4097  # above kMaxBatch (batches above 64 rows run as micro-clients)
     with pytest.raises(pb.ProteaError) as e:
         sim.run_round(c2, ex["plan"], g)
     assert e.value.name == "INVALID"
@@ -271,3 +271,38 @@ def test_oom_backoff_guarded(torch):
     assert victim == int(fixed[1]["client_id"])
     assert torch.equal(out, ref)
     sim.close()
+
+
+@pytest.mark.parametrize("precision,tol", [(0, FP32_TOL), (1, BF16_TOL)])
+def test_femnist_cnn_vs_oracle(torch, precision, tol):
+    """The FEMNIST-shaped CNN-w (28x28x1, 62 classes; the paper's LEAF experiment shape) on the
+    SIMT kernels in both modes: Dirichlet shard sizes from a 3597-writer pool, ragged batches, one round."""
+    wl = synth.build_workload(6, n_clients=300, k=8, samples=12, epochs=1)
+    got, ex = gpu_run(wl, precision=precision)
+    ref = oracle_run(wl)
+    assert rel_l2(got[4], ref[4]) <= tol
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_femnist_cnn_teacher_forced(torch, precision):
+    """Every step of multi-step FEMNIST-shaped clients (B = 8 / 16 / 64, two epochs), teacher forced
+    (tests/teacher_forced.py): fp32 <= 1e-5 vs float64; bf16 <= 1e-3 vs the bf16 emulation of the SIMT
+    path's stored tensors and <= 1e-2 vs float64."""
+    import dataclasses
+
+    from tests.teacher_forced import bench_round_with_trace, gpu_weights, oracle_updates, per_step_rel
+    wl = synth.build_workload(6, n_clients=20, k=3, samples=8, epochs=1)
+    tmpl = synth.class_templates(wl.shape, wl.classes, wl.seed)
+    wl.clients = [dataclasses.replace(c, n=n, batch=B, epochs=2)
+                  for c, (n, B) in zip(wl.clients, ((40, 16), (30, 8), (100, 64)))]
+    wl.shards = {c.id: synth.make_shard(tmpl, c.n, c.id, wl.seed) for c in wl.clients}
+    ids = [c.id for c in wl.clients]
+    elem = 4 if precision == 0 else 2
+    snaps, _, _ = bench_round_with_trace(wl, precision, ids)
+    bars = [(False, 1e-5, 1e-5)] if precision == 0 else [(True, 1e-3, 1e-3), (False, 5e-2, 1e-2)]
+    for cid in ids:
+        w = gpu_weights(wl, cid, snaps[cid], elem)
+        for emulate, dtol, bar in bars:
+            upd, _ = oracle_updates(wl, cid, snaps[cid], elem, emulate_bf16=emulate, tol=dtol)
+            tot, _ = per_step_rel(wl, cid, w, upd)
+            assert tot.max() <= bar, (cid, emulate, float(tot.max()))

@@ -109,6 +109,7 @@ def test_flops_per_sample_constants():
     assert pf.flops_per_sample(sgd.CNN, 2) == 27737088
     assert pf.flops_per_sample(sgd.CNN, 1) == 8166912
     assert pf.flops_per_sample(sgd.RESNET8) == 72552192
+    assert pf.flops_per_sample(sgd.CNN28, 4, 62) == 72544256  # "CNN-1x FEMNIST, 62 classes"
 
 
 def test_flops_vs_torch_module_count():
@@ -135,6 +136,12 @@ def test_flops_vs_torch_module_count():
         m = count(layers, (3, 32, 32))
         expect = 2 * (2 * sum(m) + sum(m[1:]))
         assert pf.flops_per_sample(sgd.CNN, wq) == expect
+        layers = [nn.Conv2d(1, c1, 5, padding=2), nn.ReLU(), nn.MaxPool2d(2),  # the FEMNIST-shaped CNN
+                  nn.Conv2d(c1, c2, 5, padding=2), nn.ReLU(), nn.MaxPool2d(2), nn.Flatten(),
+                  nn.Linear(49 * c2, f), nn.ReLU(), nn.Linear(f, 62)]
+        m = count(layers, (1, 28, 28))
+        assert pf.flops_per_sample(sgd.CNN28, wq, 62) == 2 * (2 * sum(m) + sum(m[1:]))
+        assert sgd.n_params(sgd.CNN28, wq, 62) == sum(p.numel() for p in nn.Sequential(*layers).parameters())
 
 
 def test_local_steps_closed_form():

@@ -43,7 +43,7 @@ def torch_forward(model, wq, classes, w, xb):
     def cw(name):
         return p[name + ".W"].permute(0, 3, 1, 2)
 
-    if model == sgd.CNN:
+    if model in (sgd.CNN, sgd.CNN28):
         x = F.max_pool2d(F.relu(F.conv2d(x, cw("conv1"), p["conv1.b"], padding=2)), 2)
         x = F.max_pool2d(F.relu(F.conv2d(x, cw("conv2"), p["conv2.b"], padding=2)), 2)
         x = x.permute(0, 2, 3, 1).reshape(n, -1)
@@ -71,7 +71,7 @@ def torch_grad(model, wq, classes, w, xb, yb):
     return float(loss.detach()), wt.grad.numpy()
 
 
-CASES = [(sgd.MLP, 4, 5), (sgd.CNN, 1, 3), (sgd.CNN, 4, 2), (sgd.RESNET8, 4, 2)]
+CASES = [(sgd.MLP, 4, 5), (sgd.CNN, 1, 3), (sgd.CNN, 4, 2), (sgd.RESNET8, 4, 2), (sgd.CNN28, 2, 3)]
 
 
 def _batch(model, nb, seed=0, classes=10):
@@ -92,7 +92,7 @@ def test_grad_vs_torch_f64(model, wq, nb):
     assert np.linalg.norm(g - tg) <= 1e-12 * np.linalg.norm(tg)
 
 
-@pytest.mark.parametrize("model,wq,nb", [(sgd.MLP, 4, 3), (sgd.CNN, 1, 2), (sgd.RESNET8, 4, 2)])
+@pytest.mark.parametrize("model,wq,nb", [(sgd.MLP, 4, 3), (sgd.CNN, 1, 2), (sgd.RESNET8, 4, 2), (sgd.CNN28, 1, 2)])
 def test_grad_finite_differences(model, wq, nb):
     w = synth.init_weights(model, wq, 10, seed=2).astype(np.float64)
     x, y = _batch(model, nb, seed=3)
@@ -208,3 +208,63 @@ def test_synth_shapes_and_param_segments():
         assert synth.init_weights(model, wq).size == sgd.n_params(model, wq)
     s = synth.dirichlet_sizes(1000, 50000, 0.5, seed=0)
     assert s.sum() == 50000 and s.min() >= 1
+
+
+def torch_resnet18(w, xb, classes=10):
+    """Independent torch float64 ResNet-18 with GroupNorm (R26): conv(bias) -> GN -> ReLU, basic blocks with
+    identity / option-A shortcuts, GAP, FC."""
+    p, off = {}, 0
+    for name, ws, bs in sgd.layer_shapes(sgd.RESNET18, 4, classes):
+        nw, nb = int(np.prod(ws)), int(np.prod(bs))
+        p[name + ".W"] = w[off:off + nw].view(ws)
+        off += nw
+        p[name + ".b"] = w[off:off + nb].view(bs)
+        off += nb
+    x = xb.permute(0, 3, 1, 2)
+
+    def conv(x, name, s):
+        return F.conv2d(x, p[name + ".W"].permute(0, 3, 1, 2), p[name + ".b"], stride=s, padding=1)
+
+    def gn(x, name):
+        return F.group_norm(x, 2, p[name + ".W"], p[name + ".b"], eps=1e-5)
+
+    x = F.relu(gn(conv(x, "conv0", 1), "gn0"))
+    cin = 64
+    for s, c in enumerate((64, 128, 256, 512)):
+        for b in range(2):
+            name, st = f"s{s + 1}b{b}", (2 if (s > 0 and b == 0) else 1)
+            o = F.relu(gn(conv(x, name + "a", st), name + "ga"))
+            o = gn(conv(o, name + "b", 1), name + "gb")
+            if st == 1 and cin == c:
+                sc = x
+            else:
+                sub = x[:, :, ::2, ::2]
+                sc = F.pad(sub, (0, 0, 0, 0, 0, c - cin))
+            x = F.relu(o + sc)
+            cin = c
+    return F.linear(x.mean(dim=(2, 3)), p["fc.W"], p["fc.b"])
+
+
+def test_resnet18_gn_grad_vs_torch_f64():
+    w = synth.init_weights(sgd.RESNET18, 4, 10, seed=2).astype(np.float64)
+    x, y = _batch(sgd.RESNET18, 2)
+    loss, g = sgd.flat_loss_and_grad(w, sgd.RESNET18, 4, 10, x, y)
+    wt = torch.tensor(w, requires_grad=True)
+    lt = F.cross_entropy(torch_resnet18(wt, torch.tensor(x)), torch.tensor(y))
+    lt.backward()
+    assert abs(loss - lt.item()) <= 1e-12 * abs(lt.item())
+    assert np.linalg.norm(g - wt.grad.numpy()) <= 1e-10 * np.linalg.norm(wt.grad.numpy())
+
+
+def test_gn_closed_forms():
+    """GroupNorm: per (sample, group) zero mean / unit variance before the affine; gamma = 0 gives beta;
+    its backward kills a constant shift of the input (the normalisation removes it)."""
+    rng = np.random.default_rng(0)
+    z = rng.normal(size=(3, 4, 4, 8)) * 3 + 1
+    out, (xh, rstd, G) = sgd.gn_fwd(z, np.ones(8), np.zeros(8))
+    xg = xh.reshape(3, 4, 4, 2, 4)
+    assert np.allclose(xg.mean(axis=(1, 2, 4)), 0, atol=1e-12) and np.allclose(xg.var(axis=(1, 2, 4)), 1, atol=1e-4)
+    out0, _ = sgd.gn_fwd(z, np.zeros(8), np.arange(8.0))
+    assert np.allclose(out0, np.broadcast_to(np.arange(8.0), z.shape))
+    dz, dgam, dbet = sgd.gn_bwd(np.ones_like(z), np.full(8, 1.7), sgd.gn_fwd(z, np.ones(8), np.zeros(8))[1])
+    assert np.allclose(dz, 0, atol=1e-10) and np.allclose(dbet, 48) and np.allclose(dgam.reshape(2, 4).sum(1), 0, atol=1e-10)
