@@ -23,7 +23,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 OK, ERR_INVALID, ERR_EMPTY, ERR_ZERO_WEIGHT, ERR_DIM, ERR_NO_CAPACITY, ERR_PLAN, ERR_OOM, ERR_CUDA, ERR_NCCL = range(10)
 STATUS_NAMES = {0: "OK", 1: "INVALID", 2: "EMPTY", 3: "ZERO_WEIGHT", 4: "DIM", 5: "NO_CAPACITY", 6: "PLAN", 7: "OOM",
                 8: "CUDA", 9: "NCCL"}
-MODEL_MLP, MODEL_CNN, MODEL_RESNET8 = 0, 1, 2
+MODEL_MLP, MODEL_CNN, MODEL_RESNET8, MODEL_RESNET18 = 0, 1, 2, 3
 PREC_FP32, PREC_BF16 = 0, 1
 POLICY_PROFILED, POLICY_STATIC = 0, 1
 ORDER_ASC_ID, ORDER_DESC_STEPS = 0, 1

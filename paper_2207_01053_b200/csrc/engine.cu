@@ -38,6 +38,7 @@
 #include "kernels_conv.cuh"
 #include "kernels_resnet.cuh"
 #include "kernels_resnet_tc.cuh"
+#include "kernels_resnet18.cuh"
 
 namespace protea {
 
@@ -346,7 +347,11 @@ enum Op : int {
   OP_C1F = 0, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R,
   OP_MF, OP_MHEAD, OP_MW, OP_ADMIT_, OP_FEDAVG_, OP_STAGE,
   // ResNet-8 launch instances (each needs its own prefix table); stats use PROTEA_OPC_R_* classes
-  RI_F0 = 32, RI_HEAD = RI_F0 + 7, RI_D1 = RI_HEAD + 1, RI_W0 = RI_D1 + 6, RI_R0 = RI_W0 + 7, OP_COUNT = RI_R0 + 7
+  RI_F0 = 32, RI_HEAD = RI_F0 + 7, RI_D1 = RI_HEAD + 1, RI_W0 = RI_D1 + 6, RI_R0 = RI_W0 + 7,
+  // ResNet-18 (GroupNorm) launch instances, 17 conv layers each: conv fwd, GroupNorm fwd, head, GroupNorm
+  // bwd, GroupNorm reduce, conv dgrad (layer 0 unused), conv wgrad, conv reduce
+  GI_F = RI_R0 + 7, GI_N = GI_F + 17, GI_HEAD = GI_N + 17, GI_NB = GI_HEAD + 1, GI_NR = GI_NB + 17,
+  GI_D = GI_NR + 17, GI_W = GI_D + 17, GI_R = GI_W + 17, OP_COUNT = GI_R + 17
 };
 // ResNet-8 SIMT tile shape
 constexpr int R_BM = 64, R_BN = 32;
@@ -365,7 +370,29 @@ void join_group(protea_ctx* ctx, int g) {
   }
 }
 
+const Layer& gconv(const ModelDims& m, int l) { return m.layers[2 * l]; }  // ResNet-18 conv layer l (0..16)
+const Layer& gnorm_of(const ModelDims& m, int l) { return m.layers[2 * l + 1]; }
+
 int tiles(const ModelDims& m, int op, int rows, bool tc) {
+  if (op >= GI_F) {  // ResNet-18: SIMT kernels
+    if (op == GI_HEAD) return 1;
+    if (op < GI_N) {
+      const Layer& l = gconv(m, op - GI_F);
+      return cdiv(rows * l.hout * l.wout, R_BM) * cdiv(l.cout, R_BN);
+    }
+    if (op < GI_HEAD || (op >= GI_NB && op < GI_NR)) return rows * kGroups;
+    if (op < GI_D) return 1;  // GroupNorm reduce: one CTA per client
+    if (op < GI_W) {
+      const Layer& l = gconv(m, op - GI_D);
+      return cdiv(rows * l.hin * l.win, R_BM) * cdiv(l.cin, R_BN);
+    }
+    if (op < GI_R) {
+      const Layer& l = gconv(m, op - GI_W);
+      return rsplits(l, rows) * cdiv(l.cout, R_BM) * cdiv(9 * l.cin + 1, R_BN);
+    }
+    const Layer& l = gconv(m, op - GI_R);
+    return cdiv(l.cout * (9 * l.cin + 1), kReduceBlock);
+  }
   if (m.arch == PROTEA_MODEL_CNN && m.H != 32) tc = false;  // FEMNIST-shaped CNN: SIMT kernels
   const int HW = m.H * m.W, HW2 = HW / 4, K1 = HW / 16 * m.c2, KC1 = 25 * m.C + 1;
   if (op >= RI_F0) {
@@ -432,6 +459,14 @@ std::vector<int> ops_of(const ModelDims& m, bool tc) {
   if (m.arch == PROTEA_MODEL_CNN)
     return {OP_C1F, OP_C2F, OP_F1F, OP_HEAD, OP_F1D, OP_F1W, OP_C2D, OP_C2W, OP_C2R, OP_C1W, OP_C1R};
   if (m.arch == PROTEA_MODEL_MLP) return {OP_MF, OP_MHEAD, OP_MW};
+  if (m.arch == PROTEA_MODEL_RESNET18) {
+    std::vector<int> v;
+    for (int l = 0; l < kG_Layers; ++l)
+      for (int base : {GI_F, GI_N, GI_NB, GI_NR, GI_W, GI_R}) v.push_back(base + l);
+    for (int l = 1; l < kG_Layers; ++l) v.push_back(GI_D + l);
+    v.push_back(GI_HEAD);
+    return v;
+  }
   std::vector<int> v;
   for (int i = 0; i < 7; ++i) v.push_back(RI_F0 + i);
   v.push_back(RI_HEAD);
@@ -446,6 +481,14 @@ std::vector<int> ops_of(const ModelDims& m, bool tc) {
 // written once; weights fp32, activations e bytes).  DESIGN.md "Roofline".
 void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, uint64_t* by);
 int op_class(int op) {
+  if (op >= GI_F) {
+    if (op < GI_N) return PROTEA_OPC_G_FWD;
+    if (op < GI_HEAD || (op >= GI_NB && op < GI_D)) return PROTEA_OPC_G_NORM;
+    if (op == GI_HEAD) return PROTEA_OPC_G_HEAD;
+    if (op < GI_W) return PROTEA_OPC_G_DGRAD;
+    if (op < GI_R) return PROTEA_OPC_G_WGRAD;
+    return PROTEA_OPC_G_REDUCE;
+  }
   if (op < RI_F0) return op;
   if (op < RI_HEAD) return PROTEA_OPC_R_FWD;
   if (op == RI_HEAD) return PROTEA_OPC_R_HEAD;
@@ -454,6 +497,40 @@ int op_class(int op) {
   return PROTEA_OPC_R_REDUCE;
 }
 void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, uint64_t* by) {
+  if (op >= GI_F) {  // ResNet-18: conv FLOPs = 2 x useful MACs; bytes = operands once + results once
+    uint64_t F = 0, B = 0;
+    auto conv_io = [&](const Layer& l) {
+      return r * (uint64_t)l.hin * l.win * l.cin * e + r * (uint64_t)l.hout * l.wout * l.cout * e;
+    };
+    if (op == GI_HEAD) {
+      F = 3 * 2 * r * 512 * m.classes;
+      B = r * 16 * 512 * e * 2 + 8 * m.classes * 513;
+    } else if (op < GI_N) {
+      const Layer& l = gconv(m, op - GI_F);
+      F = 2 * r * l.hout * l.wout * l.cout * 9 * l.cin;
+      B = conv_io(l) + 4 * (uint64_t)l.cout * (9 * l.cin + 1);
+    } else if (op < GI_HEAD || (op >= GI_NB && op < GI_NR)) {
+      const Layer& l = gconv(m, (op < GI_HEAD ? op - GI_N : op - GI_NB));
+      B = r * (uint64_t)l.hout * l.wout * l.cout * e * (op < GI_HEAD ? 3 : 5);
+    } else if (op < GI_D) {
+      const Layer& l = gconv(m, op - GI_NR);
+      B = r * 2 * 4 * (uint64_t)l.cout + 16 * (uint64_t)l.cout;
+    } else if (op < GI_W) {
+      const Layer& l = gconv(m, op - GI_D);
+      F = 2 * r * l.hout * l.wout * l.cout * 9 * l.cin;
+      B = conv_io(l) + 4 * (uint64_t)l.cout * 9 * l.cin;
+    } else if (op < GI_R) {
+      const Layer& l = gconv(m, op - GI_W);
+      F = 2 * r * l.hout * l.wout * l.cout * 9 * l.cin;
+      B = conv_io(l) + 4 * (uint64_t)rsplits(l, (int)r) * l.cout * (9 * l.cin + 1);
+    } else {
+      const Layer& l = gconv(m, op - GI_R);
+      B = 4 * (uint64_t)rsplits(l, (int)r) * l.cout * (9 * l.cin + 1) + 8 * (uint64_t)l.cout * (9 * l.cin + 1);
+    }
+    *fl = F;
+    *by = B;
+    return;
+  }
   if (op >= RI_F0) {
     uint64_t F = 0, B = 0;
     if (op == RI_HEAD) {
@@ -975,9 +1052,153 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
   op_end(ctx, ev);
 }
 
+// ResNet-18 with GroupNorm (R26), SIMT kernels: forward (conv -> GroupNorm [+ shortcut] -> ReLU per layer),
+// head, then per block in reverse: GroupNorm bwd (b) -> conv dgrad (b, pre-update W) -> wgrad + SGD (b) ->
+// GroupNorm bwd (a) -> dgrad (a, + the shortcut gradient) -> wgrad + SGD (a); the stem last.  Gradient
+// buffers: X = d(block output / current activation), YG = d(conv output), ZG = the shortcut gradient.
+template <typename T>
+void launch_step_r18(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs,
+                     const int32_t* dtab, float lr) {
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  typedef RFwd<T, R_BM, R_BN> F;
+  typedef RDgrad<T, R_BM, R_BN> D;
+  typedef RWgrad<T, R_BM, R_BN> Wg;
+  auto prefix = [&](int op) { return (const int*)(dtab + L.prefix_off[op]); };
+  auto gn_args = [&](int l) {
+    const Layer& c = gconv(m, l);
+    const Layer& g = gnorm_of(m, l);
+    GnArgs a{};
+    a.recs = drecs;
+    a.layer = l;
+    a.HW = c.hout * c.wout;
+    a.C = c.cout;
+    a.Wo = c.wout;
+    a.z_buf = B_G_Z0 + l;
+    a.y_buf = B_G_Y0 + l;
+    a.gam = g.off_w;
+    a.bet = g.off_b;
+    a.res_mode = 0;
+    a.res_buf = -1;
+    a.gs_buf = -1;
+    return a;
+  };
+  auto conv_fwd = [&](int l, int in_buf) {
+    F f;
+    f.recs = drecs;
+    f.L = rconv(gconv(m, l));
+    f.in_buf = in_buf;
+    f.out_buf = B_G_Z0 + l;
+    f.res_buf = -1;
+    f.res_mode = 0;
+    f.Cres = 0;
+    f.relu = 0;
+    launch_gemm<F, R_BM, R_BN>(ctx, f, L, GI_F + l, dtab);
+  };
+  auto gn_fwd = [&](const GnArgs& a) {
+    const int ev = op_begin(ctx, PROTEA_OPC_G_NORM, GI_N + a.layer);
+    k_gn_fwd<T><<<L.grid[GI_N + a.layer], kGnThreads, 0, ctx->cur>>>(a, tasks, prefix(GI_N + a.layer), L.ntask);
+    op_end(ctx, ev);
+  };
+  auto gn_bwd = [&](const GnArgs& a) {
+    int ev = op_begin(ctx, PROTEA_OPC_G_NORM, GI_NB + a.layer);
+    k_gn_bwd<T><<<L.grid[GI_NB + a.layer], kGnThreads, 0, ctx->cur>>>(a, tasks, prefix(GI_NB + a.layer), L.ntask);
+    op_end(ctx, ev);
+    const Layer& g = gnorm_of(m, a.layer);
+    ev = op_begin(ctx, PROTEA_OPC_G_NORM, GI_NR + a.layer);
+    k_gn_reduce<<<L.ntask, 256, 0, ctx->cur>>>(drecs, tasks, g.cout, g.off_w, g.off_b, lr);
+    op_end(ctx, ev);
+  };
+  auto wgrad_sgd = [&](int l, int dout_buf, int in_buf) {
+    Wg wg;
+    wg.recs = drecs;
+    wg.L = rconv(gconv(m, l));
+    wg.dout_buf = dout_buf;
+    wg.in_buf = in_buf;
+    wg.layer = -1;
+    wg.wsp_buf = B_G_WSP;
+    launch_gemm<Wg, R_BM, R_BN>(ctx, wg, L, GI_W + l, dtab);
+    const Layer& c = gconv(m, l);
+    ReduceArgs ra{drecs, B_G_WSP, c.cout, 9 * c.cin, c.off_w, c.off_b, c.hout * c.wout, lr, 0, -1};
+    const int ev = op_begin(ctx, PROTEA_OPC_G_REDUCE, GI_R + l);
+    k_reduce_update<<<L.grid[GI_R + l], kReduceBlock, 0, ctx->cur>>>(ra, tasks, prefix(GI_R + l), L.ntask);
+    op_end(ctx, ev);
+  };
+  auto dgrad = [&](int l, int add_buf, int add_mode, int Cadd) {
+    D dg;
+    dg.recs = drecs;
+    dg.L = rconv(gconv(m, l));
+    dg.dout_buf = B_G_YG;
+    dg.out_buf = B_G_X;
+    dg.mask_buf = -1;
+    dg.add_buf = add_buf;
+    dg.add_mode = add_mode;
+    dg.Cadd = Cadd;
+    launch_gemm<D, R_BM, R_BN>(ctx, dg, L, GI_D + l, dtab);
+  };
+  // ---- forward
+  conv_fwd(0, -1);
+  gn_fwd(gn_args(0));
+  for (int i = 0; i < 8; ++i) {
+    const int la = 1 + 2 * i, lb = 2 + 2 * i, in_act = B_G_Y0 + 2 * i;
+    conv_fwd(la, in_act);
+    gn_fwd(gn_args(la));
+    conv_fwd(lb, B_G_Y0 + la);
+    GnArgs a = gn_args(lb);
+    const Layer& ca = gconv(m, la);
+    a.res_buf = in_act;
+    a.res_mode = (ca.stride == 1 && ca.cin == ca.cout) ? 1 : 2;
+    a.Cres = ca.cin;
+    gn_fwd(a);
+  }
+  const Layer& fc = m.layers.back();
+  if (ctx->eval_mode) {
+    launch_eval<T>(ctx, L, drecs, tasks, B_G_Y0 + 16, 512, 16, fc, m.classes);
+    return;
+  }
+  {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_g_head<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_head_smem(64));
+      attr = true;
+    }
+    GHeadArgs ha{drecs, m.classes, fc.off_w, fc.off_b, lr, B_G_Y0 + 16, B_G_X};
+    const int ev = op_begin(ctx, PROTEA_OPC_G_HEAD, GI_HEAD);
+    k_g_head<T><<<L.ntask, 256, g_head_smem(m.classes), ctx->cur>>>(ha, tasks);
+    op_end(ctx, ev);
+  }
+  // ---- backward (X holds d(block output))
+  for (int i = 7; i >= 0; --i) {
+    const int la = 1 + 2 * i, lb = 2 + 2 * i, in_act = B_G_Y0 + 2 * i;
+    const Layer& ca = gconv(m, la);
+    GnArgs b = gn_args(lb);
+    b.dout_buf = B_G_X;
+    b.dz_buf = B_G_YG;
+    b.gs_buf = B_G_ZG;
+    gn_bwd(b);
+    dgrad(lb, -1, 0, 0);                       // d(ra) -> X (pre-update W of conv b)
+    wgrad_sgd(lb, B_G_YG, B_G_Y0 + la);
+    GnArgs a = gn_args(la);
+    a.dout_buf = B_G_X;
+    a.dz_buf = B_G_YG;
+    gn_bwd(a);
+    const bool ident = ca.stride == 1 && ca.cin == ca.cout;
+    dgrad(la, B_G_ZG, ident ? 1 : 2, ca.cout);  // d(block input) = convT(dz_a) + shortcut gradient -> X
+    wgrad_sgd(la, B_G_YG, in_act);
+  }
+  GnArgs a0 = gn_args(0);
+  a0.dout_buf = B_G_X;
+  a0.dz_buf = B_G_YG;
+  gn_bwd(a0);
+  wgrad_sgd(0, B_G_YG, -1);
+}
+
 template <typename T>
 void launch_step(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs, const int32_t* dtab,
                  float lr) {
+  if (m.arch == PROTEA_MODEL_RESNET18) {
+    launch_step_r18<T>(ctx, m, L, drecs, dtab, lr);
+    return;
+  }
   if (m.arch == PROTEA_MODEL_RESNET8) {
     launch_step_resnet<T>(ctx, m, L, drecs, dtab, lr);
     return;

@@ -94,6 +94,15 @@ def decode_snapshot(c, raw, elem, rows):
         for k, shp in (("i1", (B, s1, s1, c1)), ("i2", (B, s2, s2, c2))):
             o, n = lay[k]
             dec[k] = raw[o:o + n].astype(np.int64).reshape(shp)[:rows]
+    elif c.model == sgd.RESNET18:  # y_l: the activation after GroupNorm (+ shortcut) and ReLU of conv layer l
+        from oracle.profiler import conv_layers
+        hw = [h for h, _, _ in conv_layers(sgd.RESNET18)]
+        co = [ch for _, ch, _ in conv_layers(sgd.RESNET18)]
+        for l in range(17):
+            key = "a0" if l == 0 else (f"r{(l - 1) // 2}" if l % 2 == 1 else f"o{(l - 2) // 2}")
+            side = int(round(hw[l] ** 0.5))
+            o, n = lay[f"y{l}"]
+            dec[key] = _act(raw, o, n, elem, (B, side, side, co[l]))[:rows]
     else:
         for k, shp in (("a0", (B, 32, 32, 16)), ("r1", (B, 32, 32, 16)), ("o1", (B, 32, 32, 16)),
                        ("r2", (B, 16, 16, 32)), ("o2", (B, 16, 16, 32)), ("r3", (B, 8, 8, 64)),

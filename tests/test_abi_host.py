@@ -105,7 +105,7 @@ def test_plan_float_trap_scenario_a():
 
 MODELS = [(pb.MODEL_MLP, 4, 28, 28, 1), (pb.MODEL_CNN, 1, 32, 32, 3), (pb.MODEL_CNN, 2, 32, 32, 3),
           (pb.MODEL_CNN, 4, 32, 32, 3), (pb.MODEL_RESNET8, 4, 32, 32, 3), (pb.MODEL_CNN, 4, 28, 28, 1),
-          (pb.MODEL_CNN, 1, 28, 28, 1)]
+          (pb.MODEL_CNN, 1, 28, 28, 1), (3, 4, 32, 32, 3)]  # 3 = PROTEA_MODEL_RESNET18
 
 
 @pytest.mark.parametrize("arch,wq,H,W,C", MODELS)
@@ -115,7 +115,7 @@ def test_footprint_matches_oracle(arch, wq, H, W, C):
         n, e = rng.randint(1, 2500), rng.randint(1, 3)
         b = rng.randint(1, 64) if rng.random() < 0.6 else rng.choice([65, 100, 128, 500, 1024, 2048])
         for prec, eb in ((pb.PREC_FP32, 4), (pb.PREC_BF16, 2)):
-            om = sgd.CNN28 if (arch, H) == (pb.MODEL_CNN, 28) else arch  # the oracle's FEMNIST-shaped CNN id
+            om = sgd.CNN28 if (arch, H) == (pb.MODEL_CNN, 28) else sgd.RESNET18 if arch == 3 else arch
             peak, steps, flops = pb.protea_client_footprint(arch, wq, 10, H, W, C, n, b, e, prec)
             assert peak == pf.hwm_bytes(om, wq, 10, b, n, e, eb)
             assert steps == pf.local_steps(n, b, e)

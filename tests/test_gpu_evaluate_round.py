@@ -34,7 +34,8 @@ def _margin_count(w, c, x, y, tol):
 
 CASES = [(1, dict(n_clients=6, samples=90)), (4, dict(k=9, samples=60)), (5, dict(n_clients=300, k=6, samples=80)),
          (2, dict(n_clients=3, samples=700)),  # config 2: 78 validation rows -> two micro-clients
-         (6, dict(n_clients=200, k=5, samples=120))]  # FEMNIST-shaped CNN, 62 classes
+         (6, dict(n_clients=200, k=5, samples=120)),  # FEMNIST-shaped CNN, 62 classes
+         (7, dict(n_clients=3, samples=40))]  # ResNet-18 (GroupNorm)
 
 
 @pytest.mark.parametrize("precision", [0, 1])

@@ -28,9 +28,9 @@ def torch():
 
 def _sim(wl, precision, arena=1 << 30, widths=(4,)):
     from paper_2207_01053_b200.sim import Simulation
-    H, W, C = (28, 28, 1) if wl.model == synth.MODEL_MLP else (32, 32, 3)
+    H, W, C = synth.INPUT_SHAPE[wl.model]
     sim = Simulation(precision=precision, arena_bytes=arena)
-    mids = {w: sim.register_model(wl.model, w, wl.classes, H, W, C) for w in widths}
+    mids = {w: sim.register_model(synth.LIB_ARCH[wl.model], w, wl.classes, H, W, C) for w in widths}
     sim.register_shards([(c.id, *wl.shards[c.id]) for c in wl.clients])
     clients = sim.clients([(c.id, mids[c.width_q], c.batch, c.epochs) for c in wl.clients])
     return sim, clients
@@ -44,6 +44,9 @@ CASES = [  # (config, build kwargs, precision, widths)
     (4, dict(n_clients=300, k=12, samples=70), 1, (1, 2, 4)),
     (5, dict(n_clients=300, k=8, samples=70), 1, (4,)),
     (5, dict(n_clients=300, k=8, samples=70), 0, (4,)),
+    (6, dict(n_clients=300, k=6, samples=70), 1, (4,)),
+    (7, dict(n_clients=4, samples=20), 1, (4,)),
+    (7, dict(n_clients=4, samples=20), 0, (4,)),
 ]
 
 
@@ -57,7 +60,7 @@ def test_probe_observed_hwm_equals_layout(torch, config, kw, precision, widths):
     eb = 4 if precision == 0 else 2
     bad = []
     for p, c in zip(prof, wl.clients):
-        want = opf.hwm_bytes(c.model, c.width_q, c.classes, c.batch, c.n, c.epochs, eb)
+        want = opf.hwm_bytes(c.model, c.width_q, c.classes, c.batch, c.n, c.epochs, eb)  # (CNN28 / RESNET18 ids)
         got = int(p["peak_bytes"])
         if (c.n >= c.batch and got != want) or got > want:
             bad.append((c.id, c.width_q, c.batch, c.n, got, want))
