@@ -32,6 +32,15 @@ def logits(w, model, width_q, classes, x_u8):
         a2, _ = sgd.pool2_fwd(sgd.relu(z2))
         h = sgd.relu(a2.reshape(nb, -1) @ p["fc1.W"].T + p["fc1.b"])
         return h @ p["fc2.W"].T + p["fc2.b"]
+    if model == sgd.RESNET18:  # R26: conv (bias) -> GroupNorm -> ReLU, 8 basic blocks, GAP, fc
+        a = sgd.relu(sgd.gn_fwd(sgd.conv_fwd(xb, p["conv0.W"], p["conv0.b"], 1, 1)[0], p["gn0.W"], p["gn0.b"])[0])
+        for name, cin, cout, stride in sgd.resnet18_blocks():
+            za, _ = sgd.conv_fwd(a, p[name + "a.W"], p[name + "a.b"], stride, 1)
+            ra = sgd.relu(sgd.gn_fwd(za, p[name + "ga.W"], p[name + "ga.b"])[0])
+            zb, _ = sgd.conv_fwd(ra, p[name + "b.W"], p[name + "b.b"], 1, 1)
+            sc = a if (stride == 1 and cin == cout) else sgd.option_a(a, cout)
+            a = sgd.relu(sgd.gn_fwd(zb, p[name + "gb.W"], p[name + "gb.b"])[0] + sc)
+        return a.mean(axis=(1, 2)) @ p["fc.W"].T + p["fc.b"]
     if model == sgd.RESNET8:  # conv0, three basic blocks (option-A shortcut), global average pool, fc
         z0, _ = sgd.conv_fwd(xb, p["conv0.W"], p["conv0.b"], 1, 1)
         a = sgd.relu(z0)

@@ -63,3 +63,12 @@ def test_evaluate_round_is_the_per_client_sum():
         assert per[c.id] == oev.evaluate(g[c.width_q], sgd.CNN, c.width_q, 10, x.reshape(-1, 32, 32, 3), y)
         assert per[c.id][2] == synth.val_size(c.n) == max(1, round(c.n / 9))
     assert tot[2] == sum(v[2] for v in per.values()) and tot[1] == sum(v[1] for v in per.values())
+
+
+def test_resnet18_logits_vs_torch():
+    from tests.test_oracle_sgd import torch_resnet18
+    w = synth.init_weights(sgd.RESNET18, 4, 10, seed=3).astype(np.float64)
+    x, _ = _data(sgd.RESNET18, 2, 1)
+    z = oev.logits(w, sgd.RESNET18, 4, 10, x)
+    zt = torch_resnet18(torch.tensor(w), torch.tensor(x / 255.0)).numpy()
+    assert np.max(np.abs(z - zt)) <= 1e-11 * max(1.0, np.max(np.abs(zt)))
