@@ -9,3 +9,7 @@ timeout 1500 ncu --profile-from-start off --metrics $M --clock-control none --cs
   python tools/resnet_probe.py > gpurun_out/ncu_c5.log 2>&1
 python tools/ncu_table.py gpurun_out/ncu_c5.csv > gpurun_out/ncu_table_config5.txt
 head -20 gpurun_out/ncu_table_config2.txt; head -20 gpurun_out/ncu_table_config5.txt
+timeout 900 ncu --profile-from-start off --metrics $M --clock-control none --csv --log-file gpurun_out/ncu_tail.csv \
+  python tools/prof_round.py tail > gpurun_out/ncu_tail.log 2>&1
+python tools/ncu_table.py gpurun_out/ncu_tail.csv > gpurun_out/ncu_table_config2_tail.txt
+head -20 gpurun_out/ncu_table_config2_tail.txt
