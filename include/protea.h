@@ -112,8 +112,10 @@ typedef struct {
                            aligned to 256 B); otherwise the slot layout's bound */
   uint64_t steps;       /* S_k = E * ceil(n_k / B_k) */
   uint64_t flops;       /* E * n_k * f(model, width) */
-  uint64_t step_ns;     /* device time of one local step: probe (CUDA events) in protea_profile_clients;
-                           train_ns / steps in the in-run profiles of protea_run_round */
+  uint64_t step_ns;     /* device time of one local step: in protea_profile_clients the marginal cost of a
+                           step, median two-step run - median one-step run of the client alone (CUDA events;
+                           admission and table upload cancel; >= 1000); train_ns / steps in the in-run
+                           profiles of protea_run_round */
   uint64_t train_ns;    /* probe: step_ns * steps; in-run: sm_ns / #SMs (the client's SM-time share as
                            whole-GPU time) — Table 1 CUDA_time */
   uint64_t sm_ns;       /* in-run: sum of the durations of the CTAs that worked for the client (globaltimer;

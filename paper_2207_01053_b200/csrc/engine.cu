@@ -38,6 +38,7 @@
 #include "kernels_conv.cuh"
 #include "kernels_resnet.cuh"
 #include "kernels_resnet_tc.cuh"
+#include "kernels_resnet_halo.cuh"
 #include "kernels_resnet18.cuh"
 
 namespace protea {
@@ -260,6 +261,44 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
   }
   return ok;
 }
+
+// ResNet-8 layers run by the halo kernels (kernels_resnet_halo.cuh): stride 1, C -> C, with C = 16 / 32 / 64
+// at 32x32 / 16x16 / 8x8.  PROTEA_R8_HALO = bit mask 1 fwd, 2 dgrad, 4 wgrad (default 7; a cleared bit
+// runs that pass on the gathered kernels of kernels_resnet_tc.cuh).
+int g_r8_halo = 7;
+enum { R8H_FWD = 1, R8H_DGRAD = 2, R8H_WGRAD = 4 };
+int r8_halo_c(const Layer& l, int pass) {
+  if (!(g_r8_halo & pass) || l.kind != 0 || l.k != 3 || l.stride != 1 || l.cin != l.cout) return 0;
+  const int c = l.cin;
+  return ((c == 16 && l.hin == 32) || (c == 32 && l.hin == 16) || (c == 64 && l.hin == 8)) && l.win == l.hin ? c : 0;
+}
+int r8_halo_tiles(int c) { return c == 16 ? 8 : c == 32 ? 2 : 1; }
+
+// The TMA tensor maps of one bf16-mode ResNet-8 client (RTmapId): the halo boxes (C, 10, 18, 1) of the
+// stride-1 layers' inputs (fwd) and output gradients (dgrad), and their weight taps (C, 1, C).
+bool build_r8_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap* out) {
+  static const int lay[4] = {1, 2, 4, 6};
+  static const int in_buf[4] = {B_R_A0, B_R_R1, B_R_R2, B_R_R3};
+  static const int dout_buf[4] = {B_R_G2, B_R_G1, B_R_G2, B_R_G0};  // launch_step_resnet's gradient rotation
+  bool ok = true;
+  for (int k = 0; k < 4; ++k) {
+    const Layer& l = m.layers[lay[k]];
+    const uint64_t C = l.cin, H = l.hin;
+    if (!r8_halo_c(l, 7)) continue;
+    const CUtensorMapSwizzle sw = C == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : C == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                                          : CU_TENSOR_MAP_SWIZZLE_128B;
+    const uint64_t d[4] = {C, H, H, (uint64_t)B}, st[3] = {2 * C, 2 * C * H, 2 * C * H * H};
+    const uint32_t box[4] = {(uint32_t)C, 10, 18, 1};
+    ok &= tmap_encode(&out[RTM_IN1 + k], r.buf[in_buf[k]], 4, d, st, box, sw);
+    ok &= tmap_encode(&out[RTM_DO1 + k], r.buf[dout_buf[k]], 4, d, st, box, sw);
+    const uint32_t tbox[4] = {(uint32_t)C, 8, 16, 1};
+    ok &= tmap_encode(&out[RTM_WD1 + k], r.buf[dout_buf[k]], 4, d, st, tbox, sw);
+    const uint64_t dw[3] = {C, 9, C}, sw_[2] = {2 * C, 18 * C};
+    const uint32_t bw[3] = {(uint32_t)C, 1, (uint32_t)C};
+    ok &= tmap_encode(&out[RTM_W1 + k], (const uint8_t*)r.buf[B_WSH] + 2 * l.off_w, 3, dw, sw_, bw, sw);
+  }
+  return ok;
+}
 }  // namespace
 
 namespace {
@@ -400,16 +439,19 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
     // bf16 mode: every conv on tcgen05 (kernels_resnet_tc.cuh), 128-row tiles (conv0 on the staged input)
     if (op < RI_HEAD) {
       const Layer& l = m.layers[op - RI_F0];
+      if (tc && r8_halo_c(l, R8H_FWD)) return rows * r8_halo_tiles(l.cin);  // halo kernels: 16 x 8 pixel tiles
       if (tc) return cdiv(rows * l.hout * l.wout, 128);
       return cdiv(rows * l.hout * l.wout, R_BM) * cdiv(l.cout, R_BN);
     }
     if (op < RI_W0) {
       const Layer& l = m.layers[1 + op - RI_D1];
+      if (tc && r8_halo_c(l, R8H_DGRAD)) return rows * r8_halo_tiles(l.cin);
       if (tc) return cdiv(rows * l.hin * l.win, 128);
       return cdiv(rows * l.hin * l.win, R_BM) * cdiv(l.cin, R_BN);
     }
     if (op < RI_R0) {
       const Layer& l = m.layers[op - RI_W0];
+      if (tc && r8_halo_c(l, R8H_WGRAD)) return rsplits(l, rows);  // halo wgrad: one item per split
       if (tc) return rsplits(l, rows) * cdiv(9 * (l.cin < 8 ? 8 : l.cin) + 1, 128);
       return rsplits(l, rows) * cdiv(l.cout, R_BM) * cdiv(9 * l.cin + 1, R_BN);
     }
@@ -914,6 +956,63 @@ void launch_rtc(protea_ctx* ctx, const Op& op, const Launch& L, int opid, const 
     launch_rtc_bn<64>(ctx, op, L, opid, dtab, sm_cap);
 }
 
+// ResNet-8 stride-1 layer on the halo kernel (kernels_resnet_halo.cuh); sm_cap as launch_rtc
+template <int C, bool DGRAD>
+void launch_r8_halo_c(protea_ctx* ctx, RHalo<C, DGRAD> op, const Launch& L, int opid, const int32_t* dtab,
+                      int sm_cap) {
+  typedef RHalo<C, DGRAD> Op;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_conv_persistent<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
+    attr = true;
+  }
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const int grid = std::min(L.grid[opid], std::min(sm_cap > 0 ? sm_cap : g_num_sms, ctx->spin_cap));
+  const int ev = op_begin(ctx, op_class(opid), opid);
+  launch_k(ctx, k_conv_persistent<Op>, grid, kConvThreads, Op::SMEM, op, tasks,
+           (const int*)(dtab + L.prefix_off[opid]), L.ntask);
+  op_end(ctx, ev);
+}
+template <int C>
+void launch_r8_wgrad_halo_c(protea_ctx* ctx, const ClientRec* drecs, int i, int k, const Launch& L, int opid,
+                            const int32_t* dtab, int sm_cap) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_r8_wgrad_halo<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, RWgHalo<C>::SMEM);
+    attr = true;
+  }
+  const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
+  const int grid = std::min(L.grid[opid], sm_cap > 0 ? sm_cap : g_num_sms);
+  const int ev = op_begin(ctx, op_class(opid), opid);
+  launch_k(ctx, k_r8_wgrad_halo<C>, grid, kConvThreads, RWgHalo<C>::SMEM, drecs, tasks,
+           (const int*)(dtab + L.prefix_off[opid]), L.ntask, (int)RTM_IN1 + k, (int)RTM_WD1 + k, i);
+  op_end(ctx, ev);
+}
+// layer index i in {1, 2, 4, 6}: map slot k = 0..3
+int r8_halo_slot(int i) { return i == 1 ? 0 : i == 2 ? 1 : i == 4 ? 2 : 3; }
+void launch_r8_wgrad_halo(protea_ctx* ctx, const ClientRec* drecs, const Layer& l, int i, const Launch& L, int opid,
+                          const int32_t* dtab, int sm_cap = 0) {
+  const int k = r8_halo_slot(i);
+  if (l.cin == 16) launch_r8_wgrad_halo_c<16>(ctx, drecs, i, k, L, opid, dtab, sm_cap);
+  else if (l.cin == 32) launch_r8_wgrad_halo_c<32>(ctx, drecs, i, k, L, opid, dtab, sm_cap);
+  else launch_r8_wgrad_halo_c<64>(ctx, drecs, i, k, L, opid, dtab, sm_cap);
+}
+template <bool DGRAD>
+void launch_r8_halo(protea_ctx* ctx, const ClientRec* drecs, const Layer& l, int i, int out_buf, int res_buf,
+                    int res_mode, int Cres, int mask_buf, const Launch& L, int opid, const int32_t* dtab,
+                    int sm_cap = 0) {
+  const int k = r8_halo_slot(i);
+  const int in_tm = (DGRAD ? RTM_DO1 : RTM_IN1) + k, w_tm = RTM_W1 + k;
+  switch (l.cin) {
+    case 16: launch_r8_halo_c<16, DGRAD>(ctx, {drecs, in_tm, w_tm, out_buf, res_buf, res_mode, Cres, mask_buf, l.off_b},
+                                         L, opid, dtab, sm_cap); break;
+    case 32: launch_r8_halo_c<32, DGRAD>(ctx, {drecs, in_tm, w_tm, out_buf, res_buf, res_mode, Cres, mask_buf, l.off_b},
+                                         L, opid, dtab, sm_cap); break;
+    default: launch_r8_halo_c<64, DGRAD>(ctx, {drecs, in_tm, w_tm, out_buf, res_buf, res_mode, Cres, mask_buf, l.off_b},
+                                         L, opid, dtab, sm_cap); break;
+  }
+}
+
 void stage_r(protea_ctx* ctx, const ClientRec* drecs, const Task* tasks, const Launch& L, int out_buf) {
   const int ev = op_begin(ctx, PROTEA_OPC_R_FWD);
   k_stage_r<<<dim3(L.ntask, 16), 256, 0, ctx->cur>>>(drecs, tasks, out_buf);
@@ -953,7 +1052,11 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
         tf.in_buf = B_R_XS;
         tf.wbuf = B_R_W0P;
       }
-      launch_rtc(ctx, tf, L, RI_F0 + i, dtab, tf.L.Cout);
+      if (r8_halo_c(m.layers[i], R8H_FWD))
+        launch_r8_halo<false>(ctx, drecs, m.layers[i], i, f.out_buf, f.res_buf, f.res_mode, f.Cres, -1, L, RI_F0 + i,
+                              dtab);
+      else
+        launch_rtc(ctx, tf, L, RI_F0 + i, dtab, tf.L.Cout);
       continue;
     }
     launch_gemm<F, R_BM, R_BN>(ctx, f, L, RI_F0 + i, dtab);
@@ -1007,7 +1110,11 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
       dg.Cadd = bw[i].cadd;
       if (TC) {
         RTcDgrad td{drecs, rtc(l), dg.dout_buf, dg.out_buf, dg.mask_buf, dg.add_buf, dg.add_mode, dg.Cadd};
-        launch_rtc(ctx, td, L, RI_D1 + i - 1, dtab, td.L.Cin, half);
+        if (r8_halo_c(l, R8H_DGRAD))  // (the dout halo maps follow this rotation: build_r8_tmaps)
+          launch_r8_halo<true>(ctx, drecs, l, i, dg.out_buf, dg.add_buf, dg.add_mode, dg.Cadd, dg.mask_buf, L,
+                               RI_D1 + i - 1, dtab, half);
+        else
+          launch_rtc(ctx, td, L, RI_D1 + i - 1, dtab, td.L.Cin, half);
       } else {
         launch_gemm<D, R_BM, R_BN>(ctx, dg, L, RI_D1 + i - 1, dtab);
       }
@@ -1019,14 +1126,17 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
         tw.L.lci = 3;
         tw.in_buf = B_R_XS;
       }
+      const bool hw = r8_halo_c(l, R8H_WGRAD) != 0;
       if (ovl) {
         ctx->cur = ctx->wstream;
         cudaStreamWaitEvent(ctx->cur, ctx->r8ev[8 + i], 0);
-        launch_rtc(ctx, tw, L, RI_W0 + i, dtab, tw.L.Cout, g_num_sms - half);
+        if (hw) launch_r8_wgrad_halo(ctx, drecs, l, i, L, RI_W0 + i, dtab, g_num_sms - half);
+        else launch_rtc(ctx, tw, L, RI_W0 + i, dtab, tw.L.Cout, g_num_sms - half);
         cudaEventRecord(ctx->r8ev[i], ctx->cur);
         ctx->cur = main_s;
       } else {
-        launch_rtc(ctx, tw, L, RI_W0 + i, dtab, tw.L.Cout);
+        if (hw) launch_r8_wgrad_halo(ctx, drecs, l, i, L, RI_W0 + i, dtab);
+        else launch_rtc(ctx, tw, L, RI_W0 + i, dtab, tw.L.Cout);
       }
     } else {
       Wg wg;
@@ -1357,6 +1467,7 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
   if (const char* fs = std::getenv("PROTEA_F1W_SIDE_SMEM")) ctx->f1w_side_smem = std::max(0, std::min(220 * 1024, std::atoi(fs)));
   if (const char* dc = std::getenv("PROTEA_DEFER_C2R")) ctx->defer_c2r = std::atoi(dc) != 0;
   if (const char* ro = std::getenv("PROTEA_R8_OVERLAP")) ctx->r8_overlap = std::atoi(ro) != 0;
+  if (const char* rh = std::getenv("PROTEA_R8_HALO")) g_r8_halo = std::atoi(rh) & 7;
   if (const char* rr = std::getenv("PROTEA_R8_OVERLAP_ROWS")) ctx->r8_overlap_rows = std::atoll(rr);
   if (const char* ln = std::getenv("PROTEA_LANES")) ctx->lanes = std::max(1, std::min(4, std::atoi(ln)));
   if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_least) != cudaSuccess ||
@@ -1682,12 +1793,14 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const floa
     std::vector<int> owner;
     for (size_t i = 0; i < rc.size(); ++i) {
       const ModelDims& m = ctx->groups[rc[i].group].m;
-      if (m.arch != PROTEA_MODEL_CNN || m.H != 32) continue;
+      const bool r8 = m.arch == PROTEA_MODEL_RESNET8 && g_r8_halo != 0;
+      if (!(m.arch == PROTEA_MODEL_CNN && m.H == 32) && !r8) continue;
       auto key = std::make_tuple(rc[i].offset, rc[i].cap, rc[i].E, rc[i].n, rc[i].group);
       auto it = ctx->tmap_cache.find(key);
       if (it == ctx->tmap_cache.end()) {
         std::array<CUtensorMap, TM_COUNT> a;
-        if (!build_cnn_tmaps(m, recs[i], recs[i].B, a.data()))
+        std::memset(a.data(), 0, sizeof(a));
+        if (!(r8 ? build_r8_tmaps(m, recs[i], recs[i].B, a.data()) : build_cnn_tmaps(m, recs[i], recs[i].B, a.data())))
           return fail(ctx, PROTEA_ERR_CUDA, "run_round: cuTensorMapEncodeTiled failed for client " +
                                                std::to_string(rc[i].id));
         it = ctx->tmap_cache.emplace(key, a).first;
@@ -2267,7 +2380,7 @@ protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clien
     if (c.model_id < 0 || c.model_id >= (int)ctx->groups.size())
       return fail(ctx, PROTEA_ERR_INVALID, who + ": unknown model_id");
     if (c.batch <= 0 || c.batch > kMaxBatch || c.epochs <= 0)
-      return fail(ctx, PROTEA_ERR_INVALID, who + ": batch must be in [1, 64] and epochs > 0");
+      return fail(ctx, PROTEA_ERR_INVALID, who + ": batch must be in [1, " + std::to_string(kMaxBatch) + "] and epochs > 0");
     auto sh = ctx->shards.find(c.client_id);
     if (sh == ctx->shards.end()) return fail(ctx, PROTEA_ERR_INVALID, who + ": no registered shard");
     if (sh->second.ymin < 0 || sh->second.ymax >= ctx->groups[c.model_id].m.classes)
@@ -2279,18 +2392,18 @@ protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clien
     const protea_client& c = clients[i];
     auto key = std::make_pair((int)c.model_id, (int)c.batch);
     if (class_ns.count(key)) continue;
-    // probe: this client alone, one step (a batch of B rows), at arena offset 0
+    // probe: this client alone at arena offset 0, timed (CUDA events) as a one-step and a two-step run;
+    // step_ns is the DIFFERENCE of the medians, i.e. the marginal cost of a local step without the
+    // admission, permutation and host-table upload every run pays once
     const Group& gr = ctx->groups[c.model_id];
     RunClient r;
     r.id = c.client_id;
     r.group = c.model_id;
     r.n = std::max<int64_t>(ctx->shards[c.client_id].n, 1);
     r.B = c.batch;
-    r.E = 1;
     r.nb = (int)ceil_div((uint64_t)r.n, (uint64_t)r.B);
-    r.S = 1;
+    r.E = r.nb >= 2 ? 1 : 2;  // the second step exists within this client's own schedule
     r.admit = 0;
-    r.release = 1;
     r.offset = 0;
     const uint64_t need = client_hwm(gr.m, r.B, r.n, r.E, e);
     if (need > ctx->arena_bytes)
@@ -2299,22 +2412,29 @@ protea_status protea_profile_clients(protea_ctx* ctx, const protea_client* clien
     CK(ctx->gin.reserve(gr.m.P));
     CK(cudaMemsetAsync(ctx->gin.p, 0, gr.m.P * 4, ctx->stream));
     reset_ops(ctx, 0);
-    std::vector<float> times;
-    for (int rep = 0; rep < 7; ++rep) {
-      std::vector<RunClient> one{r};
-      // gin holds zero weights at offset 0; shift so that wg + group offset == gin
-      const float* wg = ctx->gin.p - gr.offset;
-      CK(cudaEventRecord(ctx->ev0, ctx->stream));
-      protea_status st = execute(ctx, one, wg, nullptr, 0.0f, 0, 0, 0, nullptr, nullptr);
-      if (st != PROTEA_OK) return st;
-      CK(cudaEventRecord(ctx->ev1, ctx->stream));
-      CK(cudaEventSynchronize(ctx->ev1));
-      float ms;
-      CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-      if (rep >= 2) times.push_back(ms);
+    float med[2];
+    for (int steps = 1; steps <= 2; ++steps) {
+      r.S = steps;
+      r.release = steps;
+      std::vector<float> times;
+      for (int rep = 0; rep < 7; ++rep) {
+        std::vector<RunClient> one{r};
+        // gin holds zero weights at offset 0; shift so that wg + group offset == gin
+        const float* wg = ctx->gin.p - gr.offset;
+        CK(cudaEventRecord(ctx->ev0, ctx->stream));
+        protea_status st = execute(ctx, one, wg, nullptr, 0.0f, 0, 0, 0, nullptr, nullptr);
+        if (st != PROTEA_OK) return st;
+        CK(cudaEventRecord(ctx->ev1, ctx->stream));
+        CK(cudaEventSynchronize(ctx->ev1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        if (rep >= 2) times.push_back(ms);
+      }
+      std::sort(times.begin(), times.end());
+      med[steps - 1] = times[times.size() / 2];
     }
-    std::sort(times.begin(), times.end());
-    class_ns[key] = (uint64_t)(times[times.size() / 2] * 1e6);
+    // a difference of medians can be <= 0 under noise for very cheap steps: floor at 1 us
+    class_ns[key] = (uint64_t)std::max(1e3, (double)(med[1] - med[0]) * 1e6);
   }
   // ---- observed high-water marks: every client runs ONE local step (admission with its E epoch
   // permutations, one batch of min(B, n_k) rows) in a poisoned slot of the layout's size followed by a

@@ -67,6 +67,7 @@ struct HaloConv2 {
   static constexpr int B_BYTES = 25 * CIN * N * 2;    // resident weights (K x N bf16)
   static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
   static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256 + 1024;  // + realignment slack
+  static constexpr int HSTRIDE = HBYTES, BSTRIDE = B_BYTES;        // buffer strides (= the TMA bytes)
   static constexpr int TILES_PER_IMAGE = 2;
   static constexpr int DBG = DGRAD ? 32 : 16;
   const ClientRec* recs;
@@ -233,6 +234,7 @@ struct HaloConv2Q {
   static constexpr int B_BYTES = DGRAD ? 25 * 4096 : 13 * 8192;
   static constexpr int TMEM_COLS = 2 * N <= 64 ? 64 : 128;
   static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256 + 1024;
+  static constexpr int HSTRIDE = HBYTES, BSTRIDE = B_BYTES;
   static constexpr int TILES_PER_IMAGE = 2;
   static constexpr int DBG = DGRAD ? 32 : 16;
   const ClientRec* recs;
@@ -376,6 +378,7 @@ struct QuadConv1 {
   static constexpr int B_BYTES = 36 * N * 16;  // w1q, [36 K chunks][N][8]
   static constexpr int TMEM_COLS = 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
   static constexpr int SMEM = B_BYTES + 2 * HBYTES + 256 + 1024;
+  static constexpr int HSTRIDE = HBYTES, BSTRIDE = B_BYTES;
   static constexpr int TILES_PER_IMAGE = 2;
   static constexpr int NCO = W::C1 >= 32 ? 16 : W::C1;  // channels per epilogue thread
   static constexpr int DBG = 48;
@@ -468,8 +471,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   constexpr int D0 = Op::DBG;  // PROTEA_DBG counter block
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* sH = smem + Op::B_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * Op::HBYTES);
+  uint8_t* sH = smem + Op::BSTRIDE;  // (HBYTES / B_BYTES: the TMA transaction bytes; *STRIDE: the buffer pitch)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * Op::HSTRIDE);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = __ldg(prefix + ntask);
@@ -536,7 +539,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           DBG_ADD(D0 + 0, tw);
           DBG_T0(ti);
           tc::mbar_expect_tx(h_full + 8 * buf, Op::HBYTES);
-          op.load_halo(t, tile, grp, sh + buf * Op::HBYTES, h_full + 8 * buf);
+          op.load_halo(t, tile, grp, sh + buf * Op::HSTRIDE, h_full + 8 * buf);
           DBG_ADD(D0 + 1, ti);
         }
       }
@@ -568,7 +571,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           DBG_ADD(D0 + 3, tf);
           DBG_T0(tm);
           tc::fence_after();
-          op.mma_stage(sh + buf * Op::HBYTES, sb, tmem + acc * Op::N, grp, idesc);
+          op.mma_stage(sh + buf * Op::HSTRIDE, sb, tmem + acc * Op::N, grp, idesc);
           tc::commit_w(h_empty + 8 * buf);
           DBG_ADD(D0 + 4, tm);
         }

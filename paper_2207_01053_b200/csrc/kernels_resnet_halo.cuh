@@ -1,0 +1,338 @@
+// kernels_resnet_halo.cuh — ResNet-8 stride-1 3x3 convolutions (layers 1, 2, 4, 6: C -> C channels at
+// C x C... H = 32 / 16 / 8 for C = 16 / 32 / 64) as "halo" implicit GEMMs on the persistent tcgen05
+// kernel k_conv_persistent (kernels_conv.cuh), fwd and dgrad.
+//
+// The cp.async-gathered form (kernels_resnet_tc.cuh) issues one 16-byte copy per (pixel, tap, 8
+// channels): ~1,300 instructions per 128 x 64 K block, instruction-issue bound.  Here
+// a tile is 16 output rows x 8 columns of one image (M row m = y * 8 + x; 8x8 images fill rows 0-63 and
+// leave 64-127 unused) and its whole input is ONE TMA box: the halo [18 rows][10 px][C ch] with the
+// swizzle whose width is one pixel's C channels (SW32 / SW64 / SW128 for C = 16 / 32 / 64); the conv's
+// zero padding is the TMA's out-of-bounds fill.  The A operand of tap (ky, kx) is a K-major descriptor
+// into that box shifted by ky halo rows + kx pixels (8-row core groups = 8 pixels of one halo row,
+// SBO = one halo row; the swizzle follows absolute shared-memory addresses, tools/swz_test.cu), so a
+// tile costs one TMA and 9 x C/16 MMAs (M = 128, N = C, K = 16).
+//   fwd   D[p][co] = sum_{ky,kx,ci} in[p + (ky-1, kx-1)][ci] W[co][ky][kx][ci]
+//         B = the client's 9 weight taps [co][ci] (K-major), resident while the CTA stays on the client;
+//         epilogue + bias (+ identity / option-A residual), ReLU -> bf16 (as RTcFwd)
+//   dgrad D[p][ci] = sum_{ky,kx,co} dout[p - (ky-1, kx-1)][co] W[co][ky][kx][ci]
+//         same weight boxes read MN-major (K = co rows, N = ci), flipped taps into the dout halo;
+//         epilogue (+ identity add) x ReLU mask of the stored activation -> bf16 (as RTcDgrad)
+// Same arithmetic as the gathered kernels (fp32 accumulation of the same products; only the order of
+// the K accumulation differs), parity against the oracle in tests/test_gpu_tc.py / test_gpu_parity.py.
+#pragma once
+#include "kernels_conv.cuh"
+#include "kernels_resnet_tc.cuh"
+
+namespace protea {
+
+// per-client tensor maps of the ResNet-8 halo kernels (same 19-slot array as the CNN's TmapId)
+enum RTmapId : int {
+  RTM_IN1 = 0, RTM_IN2, RTM_IN4, RTM_IN6,  // fwd input halos of layers 1, 2, 4, 6: box (C, 10, 18, 1)
+  RTM_DO1, RTM_DO2, RTM_DO4, RTM_DO6,      // dgrad dout halos of layers 1, 2, 4, 6
+  RTM_W1, RTM_W2, RTM_W4, RTM_W6,          // weight shadow of layers 1, 2, 4, 6 [co][9][ci]: box (C, 1, C)
+  RTM_WD1, RTM_WD2, RTM_WD4, RTM_WD6,      // wgrad dout tiles of layers 1, 2, 4, 6: box (C, 8, 16, 1)
+  RTM_COUNT
+};
+static_assert((int)RTM_COUNT <= (int)TM_COUNT, "ResNet-8 maps share the CNN map array");
+
+__device__ __forceinline__ uint64_t sdesc_swc(uint32_t saddr, uint32_t sbo, int rb, uint32_t lbo = 16) {
+  // swizzle width = rb bytes (one pixel's channels): 32 -> SW32 (6), 64 -> SW64 (4), 128 -> SW128 (2)
+  const uint64_t lt = rb == 32 ? 6 : rb == 64 ? 4 : 2;
+  return tc::sdesc(saddr, lbo, sbo) | (lt << 61);
+}
+
+template <int C, bool DGRAD>
+struct RHalo {
+  static constexpr int H = C == 16 ? 32 : C == 32 ? 16 : 8, W = H;
+  static constexpr int N = C, NOUT = C;
+  static constexpr bool B_MN = DGRAD;
+  static constexpr int GROUPS = 1;
+  static constexpr int RB = 2 * C;       // bytes of one pixel = the swizzle width
+  static constexpr int PITCH = 10 * RB;  // one halo row
+  static constexpr int HALO = 18 * PITCH;
+  static constexpr int HBYTES = HALO, HSTRIDE = (HALO + 1023) & ~1023;  // TMA bytes / 1024-aligned buffer pitch
+  static constexpr int TAPB = C * C * 2;  // one tap's weights [co][ci]
+  static constexpr int B_BYTES = 9 * TAPB, BSTRIDE = (B_BYTES + 1023) & ~1023;
+  static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 128;
+  static constexpr int SMEM = BSTRIDE + 2 * HSTRIDE + 256 + 1024;
+  static constexpr int TX = W / 8, TY = (H + 15) / 16, TILES_PER_IMAGE = TX * TY;
+  static constexpr int NC = N / 2 < 16 ? 16 : N / 2;  // accumulator columns per epilogue warp group
+  static constexpr int NCH = NC / 16;
+  static constexpr int DBG = 0;
+  const ClientRec* recs;
+  int in_tm, w_tm;       // tensor maps: input (fwd) / dout (dgrad) halo, weight taps
+  int out_buf;           // fwd: activation out; dgrad: input gradient out
+  int res_buf, res_mode, Cres;  // fwd residual (1 identity, 2 option A); dgrad add (1 identity)
+  int mask_buf;          // dgrad: ReLU mask = the stored activation of the layer input
+  int64_t b_off;         // fwd: bias offset in params
+
+  __device__ void load_b(const TcTile& t, uint32_t sb, uint32_t bar) const {
+    for (int tap = 0; tap < 9; ++tap) tc::tma_load_3d(sb + tap * TAPB, tmap_of(t, w_tm), bar, 0, tap, 0);
+  }
+  __device__ void load_halo(const TcTile& t, int tile, int, uint32_t base, uint32_t bar) const {
+    const int r = tile / TILES_PER_IMAGE, q = tile - r * TILES_PER_IMAGE;
+    const int y0 = (q / TX) * 16, x0 = (q % TX) * 8;
+    tc::tma_load_4d(base, tmap_of(t, in_tm), bar, 0, x0 - 1, y0 - 1, r);
+  }
+  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int, uint32_t idesc) const {
+    const uint64_t a0 = sdesc_swc(hb, PITCH, RB), b0 = sdesc_swc(sb, 8 * RB, RB);
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const int tap = ky * 3 + kx;
+        const uint32_t ao = DGRAD ? (2 - ky) * PITCH + (2 - kx) * RB : ky * PITCH + kx * RB;
+#pragma unroll
+        for (int ks = 0; ks < C / 16; ++ks) {
+          // fwd: K = ci, 16 channels = +32 B inside the pixel row; dgrad: K = co rows, 16 rows = 2 core groups
+          const uint32_t bo = tap * TAPB + (DGRAD ? ks * 16 * RB : ks * 32);
+          tc::mma_bf16_w(dt, tc::dadd(a0, ao + 32 * ks), tc::dadd(b0, bo), idesc, (tap | ks) != 0);
+        }
+      }
+  }
+  struct EpiState {
+    const ClientRec* c = nullptr;
+    float bias[NCH][16];
+  };
+  struct Pre {};
+  __device__ void prefetch(const TcTile&, int, int, int, Pre&) const {}
+  __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
+                           int lane, EpiState& st, const Pre&) const {
+    const int g = warp >> 2, row = (warp & 3) * 32 + lane;
+    const bool active = g * NC < N;  // C = 16: one warp group holds all 16 columns
+    const int r = tile / TILES_PER_IMAGE, q = tile - r * TILES_PER_IMAGE;
+    const int y = (q / TX) * 16 + (row >> 3), x = (q % TX) * 8 + (row & 7);
+    const bool valid = active && y < H;
+    const int64_t pix = ((int64_t)r * H + y) * W + x;
+    if (!DGRAD && active && st.c != t.c) {
+      st.c = t.c;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) st.bias[j][e] = t.c->params[b_off + g * NC + 16 * j + e];
+    }
+    float pre[NCH][16], msk[NCH][16];  // residual / add and mask operands, fetched before the MMA wait
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c0 = g * NC + 16 * j;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) pre[j][e] = 0.f;
+      if (!valid) continue;
+      if (res_mode == 1) {
+        ld_bf16<16>((const bf16*)t.c->buf[res_buf] + pix * C + c0, pre[j]);
+      } else if (!DGRAD && res_mode == 2 && c0 < Cres) {
+        ld_bf16<16>((const bf16*)t.c->buf[res_buf] + (((int64_t)r * 2 * H + 2 * y) * 2 * W + 2 * x) * Cres + c0,
+                    pre[j]);
+      }
+      if (DGRAD) ld_bf16<16>((const bf16*)t.c->buf[mask_buf] + pix * C + c0, msk[j]);
+    }
+    tc::mbar_wait(full_bar, parity);
+    tc::fence_after();
+    if (!active) return;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c0 = g * NC + 16 * j;
+      float v[16];
+      tc::tmem_ld16(tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
+      if (!valid) continue;
+      float o[16];
+      if (!DGRAD) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) o[e] = fmaxf(v[e] + st.bias[j][e] + pre[j][e], 0.f);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) o[e] = msk[j][e] > 0.f ? v[e] + pre[j][e] : 0.f;
+      }
+      st_bf16<16>((bf16*)t.c->buf[out_buf] + pix * C + c0, o);
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Weight gradient of the same layers, one work item per 2048-pixel split of a client (the split
+// partials of kernels_resnet_tc.cuh RTcWgrad, summed in split order + SGD by k_reduce_multi):
+//   D[(kx, ci)][co] (per ky) = sum_p in[p + (ky-1, kx-1)][ci] dout[p][co],   K = the split's pixels
+// Per 16 x 8 tile the TMA brings the input halo (as the fwd) and the dout tile [16][8][C].  A is the
+// halo read MN-major: M = (kx, ci) with the three kx "atoms" ONE pixel (RB bytes) apart (LBO = RB: the
+// same bytes serve the three column shifts), K = pixels (8 per halo row, SBO = one halo row), so one
+// MMA covers a whole tap row: M = 3C (<= 128; C = 64: kx 0-1 and kx 2 as two MMAs), N = co.
+// B = the dout tile, MN-major (N = co, K = pixels).  The bias gradient sum_p dout[p][co] is one more
+// MMA per K step with A = a 128-byte block of bf16 ones (LBO = SBO = 0: every core matrix aliases it).
+// Accumulators stay in TMEM over the split's tiles (double-buffered across items where TMEM allows);
+// the 8 epilogue warps write the partial [co][9 C + 1] rows (row m of the accumulator = (kx, ci):
+// consecutive lanes store consecutive weights).
+// Warp roles as k_conv_persistent: 0-7 epilogue, 8 TMA producer (lane 0), 9 MMA issuer.
+// ---------------------------------------------------------------------------
+template <int C>
+struct RWgHalo {
+  typedef RHalo<C, false> G;
+  static constexpr int H = G::H, W = G::W, RB = G::RB, PITCH = G::PITCH, TPI = G::TILES_PER_IMAGE;
+  static constexpr int IPS = kWgradChunkPx / (H * W);                       // images per split
+  static constexpr int MH = C == 64 ? 2 : 1;                                 // M = (kx, ci) halves
+  static constexpr int DBYTES = 128 * RB;                                    // dout tile [16][8][C]
+  static constexpr int HB = G::HSTRIDE, STAGE = HB + ((DBYTES + 1023) & ~1023);
+  static constexpr int STAGES = C == 64 ? 3 : 4;
+  static constexpr int COLS = 3 * MH * C + C;                                // + the bias accumulator
+  static constexpr int NACC = 2 * COLS <= 512 ? 2 : 1;
+  static constexpr int TMEM_COLS = NACC * COLS <= 32 ? 32 : NACC * COLS <= 64 ? 64 : NACC * COLS <= 128 ? 128
+                                   : NACC * COLS <= 256 ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE + 256 + 128 + 1024;
+  static constexpr int N_PART = 9 * C + 1;                                   // partial row: 9 C weights + bias
+};
+
+template <int C>
+__global__ void __launch_bounds__(kConvThreads, 1)
+    k_r8_wgrad_halo(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, const int* __restrict__ prefix,
+                    int ntask, int in_tm, int dout_tm, int layer) {
+  typedef RWgHalo<C> P;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::STAGES * P::STAGE);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * P::STAGES + 4);
+  uint16_t* ones = reinterpret_cast<uint16_t*>(smem + P::STAGES * P::STAGE + 256);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = __ldg(prefix + ntask);
+  const int g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
+  const int g1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  const int ti0 = find_task(prefix, ntask, g0 < total ? g0 : total - 1);
+  const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
+  const uint32_t bar0 = tc::smem_u32(bars);
+  const uint32_t full = bar0, empty = bar0 + 8 * P::STAGES, acc_full = bar0 + 16 * P::STAGES, acc_empty = acc_full + 16;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P::STAGES; ++s) {
+      tc::mbar_init(full + 8 * s, 1);
+      tc::mbar_init(empty + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(acc_full + 8 * a, 1);
+      tc::mbar_init(acc_empty + 8 * a, 8);
+    }
+    tc::mbar_fence_init();
+  }
+  if (threadIdx.x < 64) ones[threadIdx.x] = 0x3F80;  // bf16 1.0
+  if (warp == 9) tc::tmem_alloc(tc::smem_u32(tmem_slot), P::TMEM_COLS);
+  tc::fence_proxy_async();  // the ones block is read by the tensor cores (async proxy)
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sb = tc::smem_u32(smem);
+  pdl_wait();
+
+  if (warp == 8) {
+    if (lane == 0) {  // ---------------- TMA producer: per tile the input halo and the dout tile
+      int s = 0, ti = ti0;
+      for (int g = g0; g < g1; ++g) {
+        ti = next_task(prefix, ntask, ti, g);
+        const Task tk = tasks[ti];
+        const ClientRec* c = recs + tk.rec;
+        const uint8_t* tm = reinterpret_cast<const uint8_t*>(c->tmaps);
+        const int r0 = (g - __ldg(prefix + ti)) * P::IPS, r1 = min(tk.rows, r0 + P::IPS);
+        for (int tile = r0 * P::TPI; tile < r1 * P::TPI; ++tile, ++s) {
+          const int buf = s % P::STAGES, r = tile / P::TPI, q = tile - r * P::TPI;
+          const int y0 = (q / (P::W / 8)) * 16, x0 = (q % (P::W / 8)) * 8;
+          const uint32_t st = sb + buf * P::STAGE;
+          if (s >= P::STAGES) tc::mbar_wait(empty + 8 * buf, ((s / P::STAGES) - 1) & 1);
+          tc::mbar_expect_tx(full + 8 * buf, P::G::HALO + P::DBYTES);
+          tc::tma_load_4d(st, tm + 128 * in_tm, full + 8 * buf, 0, x0 - 1, y0 - 1, r);
+          tc::tma_load_4d(st + P::HB, tm + 128 * dout_tm, full + 8 * buf, 0, x0, y0, r);
+        }
+      }
+    }
+  } else if (warp == 9) {  // ---------------- MMA issuer (whole warp, elected lane issues)
+    const uint32_t idesc = tc::idesc_bf16(128, C, true, true), idesc1 = tc::idesc_bf16(128, C, false, true);
+    const uint64_t d1 = tc::sdesc(tc::smem_u32(ones), 0, 0);
+    int s = 0, i = 0, ti = ti0;
+    for (int g = g0; g < g1; ++g, ++i) {
+      ti = next_task(prefix, ntask, ti, g);
+      const int rows = __ldg(&tasks[ti].rows);
+      const int r0 = (g - __ldg(prefix + ti)) * P::IPS, r1 = min(rows, r0 + P::IPS);
+      const int a = P::NACC == 2 ? (i & 1) : 0;
+      const uint32_t ta = tmem + a * P::COLS;
+      if (P::NACC == 2 ? i >= 2 : i >= 1)
+        tc::mbar_wait(acc_empty + 8 * a, (P::NACC == 2 ? (i >> 1) - 1 : i - 1) & 1);
+      tc::fence_after();
+      for (int tile = r0 * P::TPI; tile < r1 * P::TPI; ++tile, ++s) {
+        const int buf = s % P::STAGES;
+        const uint32_t hb = sb + buf * P::STAGE, db = hb + P::HB;
+        tc::mbar_wait(full + 8 * buf, (s / P::STAGES) & 1);
+        tc::fence_after();
+        const bool first = tile == r0 * P::TPI;
+        const uint64_t a0 = sdesc_swc(hb, P::PITCH, P::RB, P::RB);  // LBO = RB: the kx atoms one pixel apart
+        const uint64_t b0 = sdesc_swc(db, 8 * P::RB, P::RB);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {  // 16 pixels = 2 tile rows per K step
+          const uint64_t bk = tc::dadd(b0, ks * 16 * P::RB);
+#pragma unroll
+          for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+            for (int mh = 0; mh < P::MH; ++mh)
+              tc::mma_bf16_w(ta + (ky * P::MH + mh) * C, tc::dadd(a0, (ky + 2 * ks) * P::PITCH + mh * 2 * P::RB), bk,
+                             idesc, !(first && ks == 0));
+          tc::mma_bf16_w(ta + 3 * P::MH * C, d1, bk, idesc1, !(first && ks == 0));
+        }
+        tc::commit_w(empty + 8 * buf);
+      }
+      tc::commit_w(acc_full + 8 * a);
+    }
+    __syncwarp();
+  } else {  // ---------------- epilogue warps 0-7: lane quadrant warp % 4 = accumulator rows m
+    const int m = (warp & 3) * 32 + lane, half = warp >> 2;
+    int i = 0, ti = ti0;
+    for (int g = g0; g < g1; ++g, ++i) {
+      ti = next_task(prefix, ntask, ti, g);
+      const ClientRec* c = recs + tasks[ti].rec;
+      const int split = g - __ldg(prefix + ti);
+      const int a = P::NACC == 2 ? (i & 1) : 0;
+      const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + a * P::COLS;
+      tc::mbar_wait(acc_full + 8 * a, (P::NACC == 2 ? (i >> 1) : i) & 1);
+      tc::fence_after();
+      float* part = (float*)c->buf[B_R_WSP] + r8_wsp_off(layer, c->B) + (int64_t)split * C * P::N_PART;
+      // accumulator blocks (ky, mh) and the bias block; the two warp groups take alternate co chunks
+      // (C = 16: warp group 1 idles)
+      if (16 * half < C) {
+#pragma unroll
+        for (int blk = 0; blk <= 3 * P::MH; ++blk) {
+          const bool bias = blk == 3 * P::MH;
+          const int ky = bias ? 0 : blk / P::MH, mh = bias ? 0 : blk % P::MH;
+          const int kx = mh * (128 / C) + m / C, ci = m % C;
+          const bool ok = bias ? m == 0 : kx < 3;
+          const int n = bias ? 9 * C : (ky * 3 + kx) * C + ci;
+#pragma unroll
+          for (int cc = 0; cc < (C + 31) / 32; ++cc) {
+            const int c0 = 16 * half + 32 * cc;
+            float v[16];
+            tc::tmem_ld16(ta + blk * C + c0, v);
+            if (ok) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) part[(int64_t)(c0 + e) * P::N_PART + n] = v[e];
+            }
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty + 8 * a);
+    }
+  }
+  pdl_trigger();
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, P::TMEM_COLS);
+  }
+  if (threadIdx.x == 0 && g1 > g0) {  // K9: split this CTA's duration over its clients by item count
+    const uint64_t dt = globaltimer() - t_start;
+    int ti = ti0, lo = g0;
+    while (lo < g1) {
+      const int hi = min(g1, __ldg(prefix + ti + 1));
+      const ClientRec* c = recs + tasks[ti].rec;
+      if (c->sm_ns) atomicAdd((unsigned long long*)c->sm_ns, (unsigned long long)(dt * (hi - lo) / (g1 - g0)));
+      lo = hi;
+      ++ti;
+    }
+  }
+}
+
+}  // namespace protea

@@ -211,3 +211,17 @@ def test_resnet8_dgrad_wgrad_overlap_bitwise(torch):
     is unchanged, so the round is bitwise the serial one (PROTEA_R8_OVERLAP=0)."""
     wl = _resnet_one_step(16, k=3, epochs=2)
     assert np.array_equal(_bf16_round(wl), _bf16_round(wl, env={"PROTEA_R8_OVERLAP": "0"}))
+
+
+@pytest.mark.parametrize("mask", [1, 2, 4, 7])
+def test_resnet8_halo_passes_match_gathered(torch, mask):
+    """The halo kernels (kernels_resnet_halo.cuh) compute the same sums as the gathered kernels in a
+    different accumulation order: a round with the halo fwd (1), dgrad (2), wgrad (4) or all (7) agrees
+    with the all-gathered round (PROTEA_R8_HALO=0) to fp32-accumulation / bf16-storage rounding (the
+    oracle bars are checked by the tests above, which run the default = all halo)."""
+    wl = _resnet_one_step(64, k=3, epochs=1)  # B = 64: several tiles, 2048-pixel splits at every size
+    g0 = synth.init_weights(wl.model, 4, wl.classes, seed=0)
+    ref = _bf16_round(wl, env={"PROTEA_R8_HALO": "0"}) - g0
+    got = _bf16_round(wl, env={"PROTEA_R8_HALO": str(mask)}) - g0
+    assert np.all(np.isfinite(got))
+    assert rel_l2(got, ref) <= 2e-3, (mask, rel_l2(got, ref))  # on the round's UPDATE, not the weights
