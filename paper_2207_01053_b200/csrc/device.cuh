@@ -24,7 +24,7 @@ struct ClientRec {
   int32_t pad_;
   int64_t id;
   uint64_t* sm_ns;         // per-client device-time attribution (nullable)
-  const void* tmaps;       // bf16 CNN: TM_COUNT CUtensorMaps (128 B each, global memory), else nullptr
+  const void* tmaps;       // bf16 CNN / ResNet-8: kTmapSlots CUtensorMaps (128 B each, global memory), else nullptr
   float* mw;               // micro-client 0 of a batch > kMicroRows: the merge weights (P fp32), else nullptr
   // fp32 master weights of a [F][K] matrix at [sp_off, sp_off + sp_len) (sp_len = F K, sp_k = K, K a multiple
   // of 128) stored as 16-bit halves (bf16-mode CNN: fc1's W, the HBM-bound weight stream): per row f and

@@ -159,7 +159,7 @@ struct protea_ctx {
   bool have_partial = false;
   std::vector<int64_t> last_Ngroup;
   // TMA tensor maps per (client, slot offset, batch, group), reused across rounds
-  std::map<std::tuple<uint64_t, int, int, int64_t, int>, std::array<CUtensorMap, TM_COUNT>> tmap_cache;  // (offset, B, E, n, group): everything the slot layout depends on
+  std::map<std::tuple<uint64_t, int, int, int64_t, int>, std::array<CUtensorMap, kTmapSlots>> tmap_cache;  // (offset, B, E, n, group): everything the slot layout depends on
   DevArray<CUtensorMap> tmaps;
   DevArray<uint64_t> smns;  // K9 per-client SM-time counters of the current round
 };
@@ -273,6 +273,11 @@ int r8_halo_c(const Layer& l, int pass) {
   return ((c == 16 && l.hin == 32) || (c == 32 && l.hin == 16) || (c == 64 && l.hin == 8)) && l.win == l.hin ? c : 0;
 }
 int r8_halo_tiles(int c) { return c == 16 ? 8 : c == 32 ? 2 : 1; }
+// stride-2 fwd halo (RHaloS2): 16 -> 32 at 32x32 and 32 -> 64 at 16x16; returns Cin
+int r8_halo_s2(const Layer& l, int pass = R8H_FWD) {
+  if (!(g_r8_halo & pass) || l.kind != 0 || l.k != 3 || l.stride != 2 || l.cout != 2 * l.cin) return 0;
+  return ((l.cin == 16 && l.hin == 32) || (l.cin == 32 && l.hin == 16)) && l.win == l.hin ? l.cin : 0;
+}
 
 // The TMA tensor maps of one bf16-mode ResNet-8 client (RTmapId): the halo boxes (C, 10, 18, 1) of the
 // stride-1 layers' inputs (fwd) and output gradients (dgrad), and their weight taps (C, 1, C).
@@ -296,6 +301,23 @@ bool build_r8_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap* 
     const uint64_t dw[3] = {C, 9, C}, sw_[2] = {2 * C, 18 * C};
     const uint32_t bw[3] = {(uint32_t)C, 1, (uint32_t)C};
     ok &= tmap_encode(&out[RTM_W1 + k], (const uint8_t*)r.buf[B_WSH] + 2 * l.off_w, 3, dw, sw_, bw, sw);
+  }
+  static const int lay2[2] = {3, 5}, in2[2] = {B_R_O1, B_R_O2};
+  for (int k = 0; k < 2; ++k) {  // stride-2 fwd: the input as pixel pairs [B][H][W/2][2 Cin]
+    const Layer& l = m.layers[lay2[k]];
+    if (!r8_halo_s2(l, 7)) continue;
+    const uint64_t C = l.cin, H = l.hin, Co = l.cout;
+    const CUtensorMapSwizzle sw = C == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B;
+    const uint64_t d[4] = {2 * C, H / 2, H, (uint64_t)B}, st[3] = {4 * C, 2 * C * H, 2 * C * H * H};
+    const uint32_t box[4] = {(uint32_t)C, 9, 33, 1};
+    ok &= tmap_encode(&out[RTM_IN3 + k], r.buf[in2[k]], 4, d, st, box, sw);
+    const uint64_t dw[3] = {C, 9, Co}, sw_[2] = {2 * C, 18 * C};
+    const uint32_t bw[3] = {(uint32_t)C, 1, (uint32_t)Co};
+    ok &= tmap_encode(&out[RTM_W3 + k], (const uint8_t*)r.buf[B_WSH] + 2 * l.off_w, 3, dw, sw_, bw, sw);
+    const uint64_t Ho = H / 2, dd[4] = {Co, Ho, Ho, (uint64_t)B}, sd[3] = {2 * Co, 2 * Co * Ho, 2 * Co * Ho * Ho};
+    const uint32_t bd[4] = {(uint32_t)Co, 9, 17, 1};
+    ok &= tmap_encode(&out[RTM_DO3 + k], r.buf[k == 0 ? B_R_G0 : B_R_G1], 4, dd, sd, bd,
+                      Co == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
   }
   return ok;
 }
@@ -440,12 +462,14 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
     if (op < RI_HEAD) {
       const Layer& l = m.layers[op - RI_F0];
       if (tc && r8_halo_c(l, R8H_FWD)) return rows * r8_halo_tiles(l.cin);  // halo kernels: 16 x 8 pixel tiles
+      if (tc && r8_halo_s2(l)) return rows * (l.cin == 16 ? 2 : 1);
       if (tc) return cdiv(rows * l.hout * l.wout, 128);
       return cdiv(rows * l.hout * l.wout, R_BM) * cdiv(l.cout, R_BN);
     }
     if (op < RI_W0) {
       const Layer& l = m.layers[1 + op - RI_D1];
       if (tc && r8_halo_c(l, R8H_DGRAD)) return rows * r8_halo_tiles(l.cin);
+      if (tc && r8_halo_s2(l, R8H_DGRAD)) return rows * (l.cin == 16 ? 8 : 4);  // 4 parity classes
       if (tc) return cdiv(rows * l.hin * l.win, 128);
       return cdiv(rows * l.hin * l.win, R_BM) * cdiv(l.cin, R_BN);
     }
@@ -956,33 +980,43 @@ void launch_rtc(protea_ctx* ctx, const Op& op, const Launch& L, int opid, const 
     launch_rtc_bn<64>(ctx, op, L, opid, dtab, sm_cap);
 }
 
-// ResNet-8 stride-1 layer on the halo kernel (kernels_resnet_halo.cuh); sm_cap as launch_rtc
-template <int C, bool DGRAD>
-void launch_r8_halo_c(protea_ctx* ctx, RHalo<C, DGRAD> op, const Launch& L, int opid, const int32_t* dtab,
-                      int sm_cap) {
-  typedef RHalo<C, DGRAD> Op;
-  static bool attr = false;
-  if (!attr) {
+// Persistent conv op (k_conv_persistent) over min(tiles, resident CTAs per SM x SMs) CTAs; sm_cap as
+// launch_rtc (an SM share for concurrent streams)
+template <class Op>
+void launch_conv_op(protea_ctx* ctx, const Op& op, const Launch& L, int opid, const int32_t* dtab, int sm_cap) {
+  static int per_sm = 0;
+  if (!per_sm) {
     cudaFuncSetAttribute(k_conv_persistent<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
-    attr = true;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conv_persistent<Op>, kConvThreads, Op::SMEM) !=
+            cudaSuccess || per_sm < 1)
+      per_sm = 1;
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
-  const int grid = std::min(L.grid[opid], std::min(sm_cap > 0 ? sm_cap : g_num_sms, ctx->spin_cap));
+  const int grid = std::min(L.grid[opid], per_sm * std::min(sm_cap > 0 ? sm_cap : g_num_sms, ctx->spin_cap));
   const int ev = op_begin(ctx, op_class(opid), opid);
   launch_k(ctx, k_conv_persistent<Op>, grid, kConvThreads, Op::SMEM, op, tasks,
            (const int*)(dtab + L.prefix_off[opid]), L.ntask);
   op_end(ctx, ev);
 }
+// ResNet-8 stride-1 layer on the halo kernel (kernels_resnet_halo.cuh)
+template <int C, bool DGRAD>
+void launch_r8_halo_c(protea_ctx* ctx, RHalo<C, DGRAD> op, const Launch& L, int opid, const int32_t* dtab,
+                      int sm_cap) {
+  launch_conv_op(ctx, op, L, opid, dtab, sm_cap);
+}
 template <int C>
 void launch_r8_wgrad_halo_c(protea_ctx* ctx, const ClientRec* drecs, int i, int k, const Launch& L, int opid,
                             const int32_t* dtab, int sm_cap) {
-  static bool attr = false;
-  if (!attr) {
+  static int per_sm = 0;
+  if (!per_sm) {
     cudaFuncSetAttribute(k_r8_wgrad_halo<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, RWgHalo<C>::SMEM);
-    attr = true;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_r8_wgrad_halo<C>, kConvThreads, RWgHalo<C>::SMEM) !=
+            cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    per_sm = std::min(per_sm, 512 / RWgHalo<C>::TMEM_COLS);  // resident CTAs must fit their TMEM allocations
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
-  const int grid = std::min(L.grid[opid], sm_cap > 0 ? sm_cap : g_num_sms);
+  const int grid = std::min(L.grid[opid], per_sm * (sm_cap > 0 ? sm_cap : g_num_sms));
   const int ev = op_begin(ctx, op_class(opid), opid);
   launch_k(ctx, k_r8_wgrad_halo<C>, grid, kConvThreads, RWgHalo<C>::SMEM, drecs, tasks,
            (const int*)(dtab + L.prefix_off[opid]), L.ntask, (int)RTM_IN1 + k, (int)RTM_WD1 + k, i);
@@ -996,6 +1030,14 @@ void launch_r8_wgrad_halo(protea_ctx* ctx, const ClientRec* drecs, const Layer& 
   if (l.cin == 16) launch_r8_wgrad_halo_c<16>(ctx, drecs, i, k, L, opid, dtab, sm_cap);
   else if (l.cin == 32) launch_r8_wgrad_halo_c<32>(ctx, drecs, i, k, L, opid, dtab, sm_cap);
   else launch_r8_wgrad_halo_c<64>(ctx, drecs, i, k, L, opid, dtab, sm_cap);
+}
+void launch_r8_halo_s2(protea_ctx* ctx, const ClientRec* drecs, const Layer& l, int i, int out_buf, const Launch& L,
+                       int opid, const int32_t* dtab) {
+  const int k = i == 3 ? 0 : 1;
+  if (l.cin == 16)
+    launch_conv_op(ctx, RHaloS2<16>{drecs, RTM_IN3 + k, RTM_W3 + k, out_buf, l.off_b}, L, opid, dtab, 0);
+  else
+    launch_conv_op(ctx, RHaloS2<32>{drecs, RTM_IN3 + k, RTM_W3 + k, out_buf, l.off_b}, L, opid, dtab, 0);
 }
 template <bool DGRAD>
 void launch_r8_halo(protea_ctx* ctx, const ClientRec* drecs, const Layer& l, int i, int out_buf, int res_buf,
@@ -1052,7 +1094,9 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
         tf.in_buf = B_R_XS;
         tf.wbuf = B_R_W0P;
       }
-      if (r8_halo_c(m.layers[i], R8H_FWD))
+      if (r8_halo_s2(m.layers[i]))
+        launch_r8_halo_s2(ctx, drecs, m.layers[i], i, f.out_buf, L, RI_F0 + i, dtab);
+      else if (r8_halo_c(m.layers[i], R8H_FWD))
         launch_r8_halo<false>(ctx, drecs, m.layers[i], i, f.out_buf, f.res_buf, f.res_mode, f.Cres, -1, L, RI_F0 + i,
                               dtab);
       else
@@ -1110,7 +1154,15 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
       dg.Cadd = bw[i].cadd;
       if (TC) {
         RTcDgrad td{drecs, rtc(l), dg.dout_buf, dg.out_buf, dg.mask_buf, dg.add_buf, dg.add_mode, dg.Cadd};
-        if (r8_halo_c(l, R8H_DGRAD))  // (the dout halo maps follow this rotation: build_r8_tmaps)
+        if (r8_halo_s2(l, R8H_DGRAD)) {
+          const int k = i == 3 ? 0 : 1;
+          if (l.cin == 16)
+            launch_conv_op(ctx, RHaloS2D<16>{drecs, RTM_DO3 + k, RTM_W3 + k, dg.out_buf, dg.add_buf, dg.Cadd, dg.mask_buf},
+                           L, RI_D1 + i - 1, dtab, half);
+          else
+            launch_conv_op(ctx, RHaloS2D<32>{drecs, RTM_DO3 + k, RTM_W3 + k, dg.out_buf, dg.add_buf, dg.Cadd, dg.mask_buf},
+                           L, RI_D1 + i - 1, dtab, half);
+        } else if (r8_halo_c(l, R8H_DGRAD))  // (the dout halo maps follow this rotation: build_r8_tmaps)
           launch_r8_halo<true>(ctx, drecs, l, i, dg.out_buf, dg.add_buf, dg.add_mode, dg.Cadd, dg.mask_buf, L,
                                RI_D1 + i - 1, dtab, half);
         else
@@ -1798,7 +1850,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const floa
       auto key = std::make_tuple(rc[i].offset, rc[i].cap, rc[i].E, rc[i].n, rc[i].group);
       auto it = ctx->tmap_cache.find(key);
       if (it == ctx->tmap_cache.end()) {
-        std::array<CUtensorMap, TM_COUNT> a;
+        std::array<CUtensorMap, kTmapSlots> a;
         std::memset(a.data(), 0, sizeof(a));
         if (!(r8 ? build_r8_tmaps(m, recs[i], recs[i].B, a.data()) : build_cnn_tmaps(m, recs[i], recs[i].B, a.data())))
           return fail(ctx, PROTEA_ERR_CUDA, "run_round: cuTensorMapEncodeTiled failed for client " +
@@ -1812,7 +1864,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const floa
       CK(ctx->tmaps.reserve(maps.size()));
       CK(cudaMemcpyAsync(ctx->tmaps.p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice,
                          ctx->stream));
-      for (size_t k = 0; k < owner.size(); ++k) recs[owner[k]].tmaps = ctx->tmaps.p + k * TM_COUNT;
+      for (size_t k = 0; k < owner.size(); ++k) recs[owner[k]].tmaps = ctx->tmaps.p + k * kTmapSlots;
     }
   }
   // ---- lock-step lanes: within each (group, batch size) class the clients alternate between lanes, so

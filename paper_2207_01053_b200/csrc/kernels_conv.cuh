@@ -95,7 +95,7 @@ struct HaloConv2 {
                           DGRAD ? 2 - kx : kx - 2, y0 - 2, r);
     }
   }
-  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc) const {
+  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc, int = 0) const {
     const uint64_t a0 = G::SW64 ? tc::sdesc_sw64(hb, 16, 512) : tc::sdesc(hb, G::COPY, 128);
     const uint64_t b0 = !DGRAD ? tc::sdesc(sb + grp * G::NCC * N * 16, N * 16, 128)  // K chunk (tap, grp*NCC + 2cp)
                                : tc::sdesc(sb + grp * G::NCC * 128, 128, W::C2 * 16);  // k rows = co of tap
@@ -251,7 +251,7 @@ struct HaloConv2Q {
     const int r = tile >> 1, x0 = (tile & 1) * 8;
     tc::tma_load_4d(base, tmap_of(t, DGRAD ? TM_DZ2Q1 : TM_A1Q), bar, 32 * grp, x0 - 2, -2, r);
   }
-  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc) const {
+  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc, int = 0) const {
     const uint64_t a0 = tc::sdesc_sw64(hb, 16, 768);
     const uint64_t b0 = !DGRAD ? tc::sdesc_sw128(sb, 16, 1024) : tc::sdesc_sw64(sb, 16, 512);
 #pragma unroll
@@ -392,7 +392,7 @@ struct QuadConv1 {
   __device__ void load_halo(const TcTile& t, int tile, int grp, uint32_t base, uint32_t bar) const {
     tc::tma_load_4d(base, tmap_of(t, TM_XSH), bar, 64 * (tile & 1), 0, 0, tile >> 1);  // 10-pixel runs (160 B)
   }
-  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc) const {
+  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int grp, uint32_t idesc, int = 0) const {
     const uint64_t a0 = tc::sdesc(hb, 160, 640), b0 = tc::sdesc(sb, N * 16, 128);
 #pragma unroll
     for (int dy = 0; dy < 6; ++dy)
@@ -466,7 +466,7 @@ __device__ __forceinline__ int next_task(const int* __restrict__ prefix, int nta
 
 
 template <class Op>
-__global__ void __launch_bounds__(kConvThreads, 1)
+__global__ void __launch_bounds__(kConvThreads, min_blocks<Op>::value)
     k_conv_persistent(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
   constexpr int D0 = Op::DBG;  // PROTEA_DBG counter block
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           DBG_ADD(D0 + 3, tf);
           DBG_T0(tm);
           tc::fence_after();
-          op.mma_stage(sh + buf * Op::HSTRIDE, sb, tmem + acc * Op::N, grp, idesc);
+          op.mma_stage(sh + buf * Op::HSTRIDE, sb, tmem + acc * Op::N, grp, idesc, g - cur.lo);
           tc::commit_w(h_empty + 8 * buf);
           DBG_ADD(D0 + 4, tm);
         }

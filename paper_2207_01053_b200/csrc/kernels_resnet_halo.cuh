@@ -31,9 +31,12 @@ enum RTmapId : int {
   RTM_DO1, RTM_DO2, RTM_DO4, RTM_DO6,      // dgrad dout halos of layers 1, 2, 4, 6
   RTM_W1, RTM_W2, RTM_W4, RTM_W6,          // weight shadow of layers 1, 2, 4, 6 [co][9][ci]: box (C, 1, C)
   RTM_WD1, RTM_WD2, RTM_WD4, RTM_WD6,      // wgrad dout tiles of layers 1, 2, 4, 6: box (C, 8, 16, 1)
+  RTM_IN3, RTM_IN5,                        // stride-2 fwd input of layers 3, 5 as pixel pairs: box (Cin, 9, 33, 1)
+  RTM_W3, RTM_W5,                          // their weight taps [co][9][ci]: box (Cin, 1, Cout)
+  RTM_DO3, RTM_DO5,                        // stride-2 dgrad dout halos of layers 3, 5: box (Cout, 9, 17, 1)
   RTM_COUNT
 };
-static_assert((int)RTM_COUNT <= (int)TM_COUNT, "ResNet-8 maps share the CNN map array");
+static_assert((int)RTM_COUNT <= kTmapSlots, "ResNet-8 maps exceed the per-client map array");
 
 __device__ __forceinline__ uint64_t sdesc_swc(uint32_t saddr, uint32_t sbo, int rb, uint32_t lbo = 16) {
   // swizzle width = rb bytes (one pixel's channels): 32 -> SW32 (6), 64 -> SW64 (4), 128 -> SW128 (2)
@@ -56,8 +59,9 @@ struct RHalo {
   static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 128;
   static constexpr int SMEM = BSTRIDE + 2 * HSTRIDE + 256 + 1024;
   static constexpr int TX = W / 8, TY = (H + 15) / 16, TILES_PER_IMAGE = TX * TY;
-  static constexpr int NC = N / 2 < 16 ? 16 : N / 2;  // accumulator columns per epilogue warp group
-  static constexpr int NCH = NC / 16;
+  static constexpr int NC = N / 2;                  // accumulator columns per epilogue warp group
+  static constexpr int CW = NC < 16 ? NC : 16, NCH = NC / CW;  // tcgen05.ld width, loads per thread
+  static constexpr int MIN_BLOCKS = C == 64 ? 1 : C == 32 ? 2 : 3;  // resident CTAs per SM (C = 64: smem)
   static constexpr int DBG = 0;
   const ClientRec* recs;
   int in_tm, w_tm;       // tensor maps: input (fwd) / dout (dgrad) halo, weight taps
@@ -74,7 +78,7 @@ struct RHalo {
     const int y0 = (q / TX) * 16, x0 = (q % TX) * 8;
     tc::tma_load_4d(base, tmap_of(t, in_tm), bar, 0, x0 - 1, y0 - 1, r);
   }
-  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int, uint32_t idesc) const {
+  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int, uint32_t idesc, int = 0) const {
     const uint64_t a0 = sdesc_swc(hb, PITCH, RB), b0 = sdesc_swc(sb, 8 * RB, RB);
 #pragma unroll
     for (int ky = 0; ky < 3; ++ky)
@@ -92,6 +96,117 @@ struct RHalo {
   }
   struct EpiState {
     const ClientRec* c = nullptr;
+    float bias[NCH][CW];
+  };
+  struct Pre {};
+  __device__ void prefetch(const TcTile&, int, int, int, Pre&) const {}
+  __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
+                           int lane, EpiState& st, const Pre&) const {
+    const int g = warp >> 2, row = (warp & 3) * 32 + lane;  // warp group g: columns [g NC, (g + 1) NC)
+    const int r = tile / TILES_PER_IMAGE, q = tile - r * TILES_PER_IMAGE;
+    const int y = (q / TX) * 16 + (row >> 3), x = (q % TX) * 8 + (row & 7);
+    const bool valid = y < H;
+    const int64_t pix = ((int64_t)r * H + y) * W + x;
+    if (!DGRAD && st.c != t.c) {
+      st.c = t.c;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j)
+#pragma unroll
+        for (int e = 0; e < CW; ++e) st.bias[j][e] = t.c->params[b_off + g * NC + CW * j + e];
+    }
+    float pre[NCH][CW], msk[NCH][CW];  // residual / add and mask operands, fetched before the MMA wait
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c0 = g * NC + CW * j;
+#pragma unroll
+      for (int e = 0; e < CW; ++e) pre[j][e] = 0.f;
+      if (!valid) continue;
+      if (res_mode == 1) {
+        ld_bf16<CW>((const bf16*)t.c->buf[res_buf] + pix * C + c0, pre[j]);
+      } else if (!DGRAD && res_mode == 2 && c0 < Cres) {
+        ld_bf16<CW>((const bf16*)t.c->buf[res_buf] + (((int64_t)r * 2 * H + 2 * y) * 2 * W + 2 * x) * Cres + c0,
+                    pre[j]);
+      }
+      if (DGRAD) ld_bf16<CW>((const bf16*)t.c->buf[mask_buf] + pix * C + c0, msk[j]);
+    }
+    tc::mbar_wait(full_bar, parity);
+    tc::fence_after();
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c0 = g * NC + CW * j;
+      float v[CW];
+      const uint32_t ta = tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0;
+      if constexpr (CW == 16) tc::tmem_ld16(ta, v); else tc::tmem_ld8(ta, v);
+      if (!valid) continue;
+      float o[CW];
+      if (!DGRAD) {
+#pragma unroll
+        for (int e = 0; e < CW; ++e) o[e] = fmaxf(v[e] + st.bias[j][e] + pre[j][e], 0.f);
+      } else {
+#pragma unroll
+        for (int e = 0; e < CW; ++e) o[e] = msk[j][e] > 0.f ? v[e] + pre[j][e] : 0.f;
+      }
+      st_bf16<CW>((bf16*)t.c->buf[out_buf] + pix * C + c0, o);
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Stride-2 fwd (layers 3: 16 -> 32 ch, 32x32 -> 16x16; 5: 32 -> 64 ch, 16x16 -> 8x8).  Output tile =
+// 16 x 8 output pixels (8x8 outputs: rows 8-15 unused).  Output (yo, xo) reads input (2yo+ky-1,
+// 2xo+kx-1): the input rows are viewed as pixel PAIRS [H][W/2][2 Cin], so one TMA box of Cin channels
+// at channel offset 0 / Cin is the plane of even / odd input columns; two boxes [33 rows][9 pairs][Cin]
+// per tile.  Tap (ky, kx) reads plane kx == 1 ? even : odd at pair offset kx == 2, starting at row ky,
+// with 8-row core groups = 8 consecutive xo (consecutive pairs: RB bytes apart) and SBO = TWO plane
+// rows (yo -> 2 yo).  Epilogue bias + ReLU (the block's residual is added by its second conv).
+// ---------------------------------------------------------------------------
+template <int CIN>
+struct RHaloS2 {
+  static constexpr int H = CIN == 16 ? 32 : 16, W = H, HO = H / 2, WO = W / 2;
+  static constexpr int N = 2 * CIN, NOUT = N, COUT = N;
+  static constexpr bool B_MN = false;
+  static constexpr int GROUPS = 1;
+  static constexpr int RB = 2 * CIN;            // bytes of one input pixel = the swizzle width
+  static constexpr int PP = 9 * RB;             // one plane row (9 pixels of one parity)
+  static constexpr int PLANE = 33 * PP;         // TMA bytes of one plane
+  static constexpr int PSTRIDE = (PLANE + 1023) & ~1023;
+  static constexpr int HBYTES = 2 * PLANE, HSTRIDE = 2 * PSTRIDE;
+  static constexpr int TAPB = COUT * CIN * 2;   // one tap's weights [co][ci]
+  static constexpr int B_BYTES = 9 * TAPB, BSTRIDE = (B_BYTES + 1023) & ~1023;
+  static constexpr int TMEM_COLS = 2 * N <= 64 ? 64 : 128;
+  static constexpr int SMEM = BSTRIDE + 2 * HSTRIDE + 256 + 1024;
+  static constexpr int TX = WO / 8, TY = (HO + 15) / 16, TILES_PER_IMAGE = TX * TY;
+  static constexpr int NC = N / 2, NCH = NC / 16;
+  static constexpr int MIN_BLOCKS = CIN == 16 ? 2 : 1;  // (CIN = 32: shared memory)
+  static constexpr int DBG = 0;
+  const ClientRec* recs;
+  int in_tm, w_tm, out_buf;
+  int64_t b_off;
+
+  __device__ void load_b(const TcTile& t, uint32_t sb, uint32_t bar) const {
+    for (int tap = 0; tap < 9; ++tap) tc::tma_load_3d(sb + tap * TAPB, tmap_of(t, w_tm), bar, 0, tap, 0);
+  }
+  __device__ void load_halo(const TcTile& t, int tile, int, uint32_t base, uint32_t bar) const {
+    const int r = tile / TILES_PER_IMAGE, q = tile - r * TILES_PER_IMAGE;
+    const int y0 = (q / TX) * 16, x0 = (q % TX) * 8;
+    tc::tma_load_4d(base, tmap_of(t, in_tm), bar, 0, x0, 2 * y0 - 1, r);                // even columns 2 x0 ..
+    tc::tma_load_4d(base + PSTRIDE, tmap_of(t, in_tm), bar, CIN, x0 - 1, 2 * y0 - 1, r);  // odd columns 2 x0 - 1 ..
+  }
+  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int, uint32_t idesc, int = 0) const {
+    const uint64_t a0 = sdesc_swc(hb, 2 * PP, RB), b0 = sdesc_swc(sb, 8 * RB, RB);
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const int tap = ky * 3 + kx;
+        const uint32_t ao = (kx == 1 ? 0 : PSTRIDE) + ky * PP + (kx == 2 ? RB : 0);
+#pragma unroll
+        for (int ks = 0; ks < CIN / 16; ++ks)
+          tc::mma_bf16_w(dt, tc::dadd(a0, ao + 32 * ks), tc::dadd(b0, tap * TAPB + 32 * ks), idesc, (tap | ks) != 0);
+      }
+  }
+  struct EpiState {
+    const ClientRec* c = nullptr;
     float bias[NCH][16];
   };
   struct Pre {};
@@ -99,51 +214,137 @@ struct RHalo {
   __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
                            int lane, EpiState& st, const Pre&) const {
     const int g = warp >> 2, row = (warp & 3) * 32 + lane;
-    const bool active = g * NC < N;  // C = 16: one warp group holds all 16 columns
     const int r = tile / TILES_PER_IMAGE, q = tile - r * TILES_PER_IMAGE;
     const int y = (q / TX) * 16 + (row >> 3), x = (q % TX) * 8 + (row & 7);
-    const bool valid = active && y < H;
-    const int64_t pix = ((int64_t)r * H + y) * W + x;
-    if (!DGRAD && active && st.c != t.c) {
+    if (st.c != t.c) {
       st.c = t.c;
 #pragma unroll
       for (int j = 0; j < NCH; ++j)
 #pragma unroll
         for (int e = 0; e < 16; ++e) st.bias[j][e] = t.c->params[b_off + g * NC + 16 * j + e];
     }
-    float pre[NCH][16], msk[NCH][16];  // residual / add and mask operands, fetched before the MMA wait
-#pragma unroll
-    for (int j = 0; j < NCH; ++j) {
-      const int c0 = g * NC + 16 * j;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) pre[j][e] = 0.f;
-      if (!valid) continue;
-      if (res_mode == 1) {
-        ld_bf16<16>((const bf16*)t.c->buf[res_buf] + pix * C + c0, pre[j]);
-      } else if (!DGRAD && res_mode == 2 && c0 < Cres) {
-        ld_bf16<16>((const bf16*)t.c->buf[res_buf] + (((int64_t)r * 2 * H + 2 * y) * 2 * W + 2 * x) * Cres + c0,
-                    pre[j]);
-      }
-      if (DGRAD) ld_bf16<16>((const bf16*)t.c->buf[mask_buf] + pix * C + c0, msk[j]);
-    }
     tc::mbar_wait(full_bar, parity);
     tc::fence_after();
-    if (!active) return;
+    const int64_t pix = ((int64_t)r * HO + y) * WO + x;
 #pragma unroll
     for (int j = 0; j < NCH; ++j) {
       const int c0 = g * NC + 16 * j;
       float v[16];
       tc::tmem_ld16(tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
-      if (!valid) continue;
+      if (y >= HO) continue;
       float o[16];
-      if (!DGRAD) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) o[e] = fmaxf(v[e] + st.bias[j][e] + pre[j][e], 0.f);
-      } else {
+      for (int e = 0; e < 16; ++e) o[e] = fmaxf(v[e] + st.bias[j][e], 0.f);
+      st_bf16<16>((bf16*)t.c->buf[out_buf] + pix * COUT + c0, o);
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Stride-2 dgrad (layers 3, 5): dIn[y][x] = sum over the taps with y + 1 - ky and x + 1 - kx even of
+// dout[(y + 1 - ky) / 2][(x + 1 - kx) / 2] W[.][ky][kx].  The input pixels split into 4 parity classes
+// (py, px) = (y & 1, x & 1); inside a class every row of a tile uses the SAME taps: ky = 1 for py = 0,
+// ky in {0, 2} for py = 1 (likewise kx), at dout offset (py + 1 - ky) / 2 in {0, 1}.  A tile = 16 x 8
+// pixels (i, j) of one class (y = 2i + py, x = 2j + px); its A operands are descriptors into one dout
+// halo [17 rows][9 px][Cout] (offsets 0 / +1 row / +1 pixel; rows past the image are the TMA's zero
+// fill): 1, 2, 2 or 4 taps x Cout / 16 MMAs per tile.  B = the weight taps read MN-major (K = co,
+// N = ci), as RHalo<dgrad>.  Epilogue (+ option-A shortcut gradient at even (y, x), channels < Cin)
+// x ReLU mask -> bf16 (as RTcDgrad, add_mode 2).
+// ---------------------------------------------------------------------------
+template <int CIN>
+struct RHaloS2D {
+  static constexpr int H = CIN == 16 ? 32 : 16, W = H, HO = H / 2, WO = W / 2, COUT = 2 * CIN;
+  static constexpr int N = CIN, NOUT = N;
+  static constexpr bool B_MN = true;
+  static constexpr int GROUPS = 1;
+  static constexpr int RBO = 2 * COUT, RBI = 2 * CIN;  // dout pixel bytes (A swizzle), weight row bytes (B)
+  static constexpr int PITCH = 9 * RBO;
+  static constexpr int HALO = 17 * PITCH;
+  static constexpr int HBYTES = HALO, HSTRIDE = (HALO + 1023) & ~1023;
+  static constexpr int TAPB = COUT * CIN * 2;
+  static constexpr int B_BYTES = 9 * TAPB, BSTRIDE = (B_BYTES + 1023) & ~1023;
+  static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 64;
+  static constexpr int SMEM = BSTRIDE + 2 * HSTRIDE + 256 + 1024;
+  static constexpr int TX = WO / 8, TY = (HO + 15) / 16, TPC = TX * TY, TILES_PER_IMAGE = 4 * TPC;
+  static constexpr int NC = N / 2, CW = NC < 16 ? NC : 16, NCH = NC / CW;
+  static constexpr int MIN_BLOCKS = 2;
+  static constexpr int DBG = 0;
+  const ClientRec* recs;
+  int in_tm, w_tm, out_buf, add_buf, Cadd, mask_buf;
+
+  __device__ void load_b(const TcTile& t, uint32_t sb, uint32_t bar) const {
+    for (int tap = 0; tap < 9; ++tap) tc::tma_load_3d(sb + tap * TAPB, tmap_of(t, w_tm), bar, 0, tap, 0);
+  }
+  __device__ static void coords(int tile, int& r, int& cls, int& i0, int& j0) {
+    r = tile / TILES_PER_IMAGE;
+    const int q = tile - r * TILES_PER_IMAGE;
+    cls = q / TPC;
+    i0 = ((q % TPC) / TX) * 16;
+    j0 = (q % TX) * 8;
+  }
+  __device__ void load_halo(const TcTile& t, int tile, int, uint32_t base, uint32_t bar) const {
+    int r, cls, i0, j0;
+    coords(tile, r, cls, i0, j0);
+    tc::tma_load_4d(base, tmap_of(t, in_tm), bar, 0, j0, i0, r);
+  }
+  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int, uint32_t idesc, int tile = 0) const {
+    int r, cls, i0, j0;
+    coords(tile, r, cls, i0, j0);
+    const int py = cls >> 1, px = cls & 1;
+    const uint64_t a0 = sdesc_swc(hb, PITCH, RBO), b0 = sdesc_swc(sb, 8 * RBI, RBI);
+    bool acc = false;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) o[e] = msk[j][e] > 0.f ? v[e] + pre[j][e] : 0.f;
+    for (int ky = 0; ky < 3; ++ky) {
+      if ((ky == 1) != (py == 0)) continue;  // py = 0: ky = 1; py = 1: ky = 0, 2
+      const int dyo = (py + 1 - ky) / 2;
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        if ((kx == 1) != (px == 0)) continue;
+        const int dxo = (px + 1 - kx) / 2, tap = ky * 3 + kx;
+#pragma unroll
+        for (int ks = 0; ks < COUT / 16; ++ks) {
+          tc::mma_bf16_w(dt, tc::dadd(a0, dyo * PITCH + dxo * RBO + 32 * ks), tc::dadd(b0, tap * TAPB + ks * 16 * RBI),
+                         idesc, acc);
+          acc = true;
+        }
       }
-      st_bf16<16>((bf16*)t.c->buf[out_buf] + pix * C + c0, o);
+    }
+  }
+  struct EpiState {};
+  struct Pre {};
+  __device__ void prefetch(const TcTile&, int, int, int, Pre&) const {}
+  __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
+                           int lane, EpiState&, const Pre&) const {
+    const int g = warp >> 2, row = (warp & 3) * 32 + lane;
+    int r, cls, i0, j0;
+    coords(tile, r, cls, i0, j0);
+    const int i = i0 + (row >> 3), j = j0 + (row & 7), y = 2 * i + (cls >> 1), x = 2 * j + (cls & 1);
+    const bool valid = i < HO;
+    const int64_t pix = ((int64_t)r * H + y) * W + x;
+    float pre[NCH][CW], msk[NCH][CW];
+#pragma unroll
+    for (int jj = 0; jj < NCH; ++jj) {
+      const int c0 = g * NC + CW * jj;
+#pragma unroll
+      for (int e = 0; e < CW; ++e) pre[jj][e] = 0.f;
+      if (!valid) continue;
+      if (cls == 0 && c0 < Cadd)  // option-A shortcut gradient at even (y, x)
+        ld_bf16<CW>((const bf16*)t.c->buf[add_buf] + (((int64_t)r * HO + i) * WO + j) * Cadd + c0, pre[jj]);
+      ld_bf16<CW>((const bf16*)t.c->buf[mask_buf] + pix * CIN + c0, msk[jj]);
+    }
+    tc::mbar_wait(full_bar, parity);
+    tc::fence_after();
+#pragma unroll
+    for (int jj = 0; jj < NCH; ++jj) {
+      const int c0 = g * NC + CW * jj;
+      float v[CW];
+      const uint32_t ta = tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0;
+      if constexpr (CW == 16) tc::tmem_ld16(ta, v); else tc::tmem_ld8(ta, v);
+      if (!valid) continue;
+      float o[CW];
+#pragma unroll
+      for (int e = 0; e < CW; ++e) o[e] = msk[jj][e] > 0.f ? v[e] + pre[jj][e] : 0.f;
+      st_bf16<CW>((bf16*)t.c->buf[out_buf] + pix * CIN + c0, o);
     }
   }
 };
@@ -181,7 +382,7 @@ struct RWgHalo {
 };
 
 template <int C>
-__global__ void __launch_bounds__(kConvThreads, 1)
+__global__ void __launch_bounds__(kConvThreads, C == 64 ? 1 : 2)  // (C = 64: TMEM 512 columns)
     k_r8_wgrad_halo(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, const int* __restrict__ prefix,
                     int ntask, int in_tm, int dout_tm, int layer) {
   typedef RWgHalo<C> P;

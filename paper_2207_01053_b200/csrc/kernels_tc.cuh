@@ -755,6 +755,8 @@ enum TmapId : int {
   TM_W2DS,     // W2 shadow (32, 25, 64) box (32,1,64) 64B-swizzled conv2 dgrad weights (width 1)
   TM_COUNT
 };
+constexpr int kTmapSlots = 24;  // per-client map array (CNN: TmapId; ResNet-8: RTmapId, kernels_resnet_halo.cuh)
+static_assert((int)TM_COUNT <= kTmapSlots, "CNN maps exceed the per-client map array");
 
 __device__ __forceinline__ const void* tmap_of(const TcTile& t, int id) {
   return reinterpret_cast<const uint8_t*>(t.c->tmaps) + 128 * id;
