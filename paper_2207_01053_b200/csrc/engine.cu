@@ -318,6 +318,9 @@ bool build_r8_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap* 
     const uint32_t bd[4] = {(uint32_t)Co, 9, 17, 1};
     ok &= tmap_encode(&out[RTM_DO3 + k], r.buf[k == 0 ? B_R_G0 : B_R_G1], 4, dd, sd, bd,
                       Co == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
+    const uint32_t bt[4] = {(uint32_t)Co, 8, 16, 1};
+    ok &= tmap_encode(&out[RTM_WD3 + k], r.buf[k == 0 ? B_R_G0 : B_R_G1], 4, dd, sd, bt,
+                      Co == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
   }
   return ok;
 }
@@ -475,7 +478,8 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
     }
     if (op < RI_R0) {
       const Layer& l = m.layers[op - RI_W0];
-      if (tc && r8_halo_c(l, R8H_WGRAD)) return rsplits(l, rows);  // halo wgrad: one item per split
+      if (tc && (r8_halo_c(l, R8H_WGRAD) || r8_halo_s2(l, R8H_WGRAD)))
+        return rsplits(l, rows);  // halo wgrad: one item per split
       if (tc) return rsplits(l, rows) * cdiv(9 * (l.cin < 8 ? 8 : l.cin) + 1, 128);
       return rsplits(l, rows) * cdiv(l.cout, R_BM) * cdiv(9 * l.cin + 1, R_BN);
     }
@@ -1004,32 +1008,38 @@ void launch_r8_halo_c(protea_ctx* ctx, RHalo<C, DGRAD> op, const Launch& L, int 
                       int sm_cap) {
   launch_conv_op(ctx, op, L, opid, dtab, sm_cap);
 }
-template <int C>
-void launch_r8_wgrad_halo_c(protea_ctx* ctx, const ClientRec* drecs, int i, int k, const Launch& L, int opid,
-                            const int32_t* dtab, int sm_cap) {
+template <class P>
+void launch_r8_wgrad_halo_p(protea_ctx* ctx, const ClientRec* drecs, int i, int in_tm, int dout_tm, const Launch& L,
+                            int opid, const int32_t* dtab, int sm_cap) {
   static int per_sm = 0;
   if (!per_sm) {
-    cudaFuncSetAttribute(k_r8_wgrad_halo<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, RWgHalo<C>::SMEM);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_r8_wgrad_halo<C>, kConvThreads, RWgHalo<C>::SMEM) !=
+    cudaFuncSetAttribute(k_r8_wgrad_halo<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_r8_wgrad_halo<P>, kConvThreads, P::SMEM) !=
             cudaSuccess || per_sm < 1)
       per_sm = 1;
-    per_sm = std::min(per_sm, 512 / RWgHalo<C>::TMEM_COLS);  // resident CTAs must fit their TMEM allocations
+    per_sm = std::min(per_sm, 512 / P::TMEM_COLS);  // resident CTAs must fit their TMEM allocations
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[opid], per_sm * (sm_cap > 0 ? sm_cap : g_num_sms));
   const int ev = op_begin(ctx, op_class(opid), opid);
-  launch_k(ctx, k_r8_wgrad_halo<C>, grid, kConvThreads, RWgHalo<C>::SMEM, drecs, tasks,
-           (const int*)(dtab + L.prefix_off[opid]), L.ntask, (int)RTM_IN1 + k, (int)RTM_WD1 + k, i);
+  launch_k(ctx, k_r8_wgrad_halo<P>, grid, kConvThreads, P::SMEM, drecs, tasks, (const int*)(dtab + L.prefix_off[opid]),
+           L.ntask, in_tm, dout_tm, i);
   op_end(ctx, ev);
 }
 // layer index i in {1, 2, 4, 6}: map slot k = 0..3
 int r8_halo_slot(int i) { return i == 1 ? 0 : i == 2 ? 1 : i == 4 ? 2 : 3; }
 void launch_r8_wgrad_halo(protea_ctx* ctx, const ClientRec* drecs, const Layer& l, int i, const Launch& L, int opid,
                           const int32_t* dtab, int sm_cap = 0) {
+  if (l.stride == 2) {
+    const int k = i == 3 ? 0 : 1;
+    if (l.cin == 16) launch_r8_wgrad_halo_p<RWgHaloS2<16>>(ctx, drecs, i, RTM_IN3 + k, RTM_WD3 + k, L, opid, dtab, sm_cap);
+    else launch_r8_wgrad_halo_p<RWgHaloS2<32>>(ctx, drecs, i, RTM_IN3 + k, RTM_WD3 + k, L, opid, dtab, sm_cap);
+    return;
+  }
   const int k = r8_halo_slot(i);
-  if (l.cin == 16) launch_r8_wgrad_halo_c<16>(ctx, drecs, i, k, L, opid, dtab, sm_cap);
-  else if (l.cin == 32) launch_r8_wgrad_halo_c<32>(ctx, drecs, i, k, L, opid, dtab, sm_cap);
-  else launch_r8_wgrad_halo_c<64>(ctx, drecs, i, k, L, opid, dtab, sm_cap);
+  if (l.cin == 16) launch_r8_wgrad_halo_p<RWgHalo<16>>(ctx, drecs, i, RTM_IN1 + k, RTM_WD1 + k, L, opid, dtab, sm_cap);
+  else if (l.cin == 32) launch_r8_wgrad_halo_p<RWgHalo<32>>(ctx, drecs, i, RTM_IN1 + k, RTM_WD1 + k, L, opid, dtab, sm_cap);
+  else launch_r8_wgrad_halo_p<RWgHalo<64>>(ctx, drecs, i, RTM_IN1 + k, RTM_WD1 + k, L, opid, dtab, sm_cap);
 }
 void launch_r8_halo_s2(protea_ctx* ctx, const ClientRec* drecs, const Layer& l, int i, int out_buf, const Launch& L,
                        int opid, const int32_t* dtab) {
@@ -1178,7 +1188,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
         tw.L.lci = 3;
         tw.in_buf = B_R_XS;
       }
-      const bool hw = r8_halo_c(l, R8H_WGRAD) != 0;
+      const bool hw = r8_halo_c(l, R8H_WGRAD) != 0 || r8_halo_s2(l, R8H_WGRAD) != 0;
       if (ovl) {
         ctx->cur = ctx->wstream;
         cudaStreamWaitEvent(ctx->cur, ctx->r8ev[8 + i], 0);

@@ -34,6 +34,7 @@ enum RTmapId : int {
   RTM_IN3, RTM_IN5,                        // stride-2 fwd input of layers 3, 5 as pixel pairs: box (Cin, 9, 33, 1)
   RTM_W3, RTM_W5,                          // their weight taps [co][9][ci]: box (Cin, 1, Cout)
   RTM_DO3, RTM_DO5,                        // stride-2 dgrad dout halos of layers 3, 5: box (Cout, 9, 17, 1)
+  RTM_WD3, RTM_WD5,                        // stride-2 wgrad dout tiles of layers 3, 5: box (Cout, 8, 16, 1)
   RTM_COUNT
 };
 static_assert((int)RTM_COUNT <= kTmapSlots, "ResNet-8 maps exceed the per-client map array");
@@ -365,27 +366,89 @@ struct RHaloS2D {
 // Warp roles as k_conv_persistent: 0-7 epilogue, 8 TMA producer (lane 0), 9 MMA issuer.
 // ---------------------------------------------------------------------------
 template <int C>
-struct RWgHalo {
+struct RWgHalo {  // stride 1: C -> C
   typedef RHalo<C, false> G;
   static constexpr int H = G::H, W = G::W, RB = G::RB, PITCH = G::PITCH, TPI = G::TILES_PER_IMAGE;
+  static constexpr int COUT = C, CIN = C;
   static constexpr int IPS = kWgradChunkPx / (H * W);                       // images per split
   static constexpr int MH = C == 64 ? 2 : 1;                                 // M = (kx, ci) halves
-  static constexpr int DBYTES = 128 * RB;                                    // dout tile [16][8][C]
+  static constexpr int NBLK = 3 * MH;                                        // accumulator blocks (ky, mh)
+  static constexpr int RBO = 2 * COUT, DBYTES = 128 * RBO;                   // dout tile [16][8][Cout]
   static constexpr int HB = G::HSTRIDE, STAGE = HB + ((DBYTES + 1023) & ~1023);
+  static constexpr int TX_BYTES = G::HALO + DBYTES;
   static constexpr int STAGES = C == 64 ? 3 : 4;
-  static constexpr int COLS = 3 * MH * C + C;                                // + the bias accumulator
+  static constexpr int COLS = (NBLK + 1) * COUT;                             // + the bias accumulator
   static constexpr int NACC = 2 * COLS <= 512 ? 2 : 1;
   static constexpr int TMEM_COLS = NACC * COLS <= 32 ? 32 : NACC * COLS <= 64 ? 64 : NACC * COLS <= 128 ? 128
                                    : NACC * COLS <= 256 ? 256 : 512;
   static constexpr int SMEM = STAGES * STAGE + 256 + 128 + 1024;
-  static constexpr int N_PART = 9 * C + 1;                                   // partial row: 9 C weights + bias
+  static constexpr int N_PART = 9 * CIN + 1;                                 // partial row: 9 Cin weights + bias
+  __device__ static void load(uint32_t st, const uint8_t* tm, int in_tm, int dout_tm, int tile, uint32_t bar) {
+    const int r = tile / TPI, q = tile - r * TPI, y0 = (q / (W / 8)) * 16, x0 = (q % (W / 8)) * 8;
+    tc::tma_load_4d(st, tm + 128 * in_tm, bar, 0, x0 - 1, y0 - 1, r);
+    tc::tma_load_4d(st + HB, tm + 128 * dout_tm, bar, 0, x0, y0, r);
+  }
+  // K step ks = tile pixel rows 2 ks, 2 ks + 1; block (ky, mh) = D[(kx, ci)][co] of tap row ky
+  __device__ static void mma(uint32_t st, uint32_t ta, int ks, bool acc, uint32_t idesc, uint64_t bk) {
+    const uint64_t a0 = sdesc_swc(st, PITCH, RB, RB);  // LBO = RB: the kx atoms one pixel apart
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int mh = 0; mh < MH; ++mh)
+        tc::mma_bf16_w(ta + (ky * MH + mh) * COUT, tc::dadd(a0, (ky + 2 * ks) * PITCH + mh * 2 * RB), bk, idesc, acc);
+  }
+  __device__ static bool row_of(int blk, int m, int& n) {  // accumulator row m of block blk -> partial column
+    const int ky = blk / MH, kx = (blk % MH) * (128 / C) + m / C;
+    n = (ky * 3 + kx) * C + m % C;
+    return kx < 3;
+  }
 };
 
-template <int C>
-__global__ void __launch_bounds__(kConvThreads, C == 64 ? 1 : 2)  // (C = 64: TMEM 512 columns)
+template <int CIN>
+struct RWgHaloS2 {  // stride 2: CIN -> 2 CIN, over the pixel-pair planes of RHaloS2
+  typedef RHaloS2<CIN> G;
+  static constexpr int COUT = 2 * CIN, RB = G::RB, PP = G::PP, TPI = G::TILES_PER_IMAGE, HO = G::HO, WO = G::WO;
+  static constexpr int IPS = kWgradChunkPx / (HO * WO);
+  static constexpr int NBLK = 6;                                             // (ky, odd plane: kx 0, 2), (ky, even: kx 1)
+  static constexpr int RBO = 2 * COUT, DBYTES = 128 * RBO;
+  static constexpr int HB = G::HSTRIDE, STAGE = HB + ((DBYTES + 1023) & ~1023);
+  static constexpr int TX_BYTES = G::HBYTES + DBYTES;
+  static constexpr int STAGES = CIN == 16 ? 4 : 2;
+  static constexpr int COLS = (NBLK + 1) * COUT;
+  static constexpr int NACC = 2 * COLS <= 512 ? 2 : 1;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int SMEM = STAGES * STAGE + 256 + 128 + 1024;
+  static constexpr int N_PART = 9 * CIN + 1;
+  __device__ static void load(uint32_t st, const uint8_t* tm, int in_tm, int dout_tm, int tile, uint32_t bar) {
+    const int r = tile / TPI, q = tile - r * TPI, y0 = (q / G::TX) * 16, x0 = (q % G::TX) * 8;
+    tc::tma_load_4d(st, tm + 128 * in_tm, bar, 0, x0, 2 * y0 - 1, r);                    // even columns
+    tc::tma_load_4d(st + G::PSTRIDE, tm + 128 * in_tm, bar, CIN, x0 - 1, 2 * y0 - 1, r);  // odd columns
+    tc::tma_load_4d(st + HB, tm + 128 * dout_tm, bar, 0, x0, y0, r);
+  }
+  // output rows 2 ks, 2 ks + 1 read plane rows 4 ks + ky (+ 2): SBO = two plane rows
+  __device__ static void mma(uint32_t st, uint32_t ta, int ks, bool acc, uint32_t idesc, uint64_t bk) {
+    // odd plane: M atoms kx = 0 (pair offset 0) and kx = 2 (the next pair, RB bytes on): LBO = RB;
+    // even plane: atom 0 = kx = 1 (the others unused rows)
+    const uint64_t ae = sdesc_swc(st, 2 * PP, RB, RB), ao = sdesc_swc(st + G::PSTRIDE, 2 * PP, RB, RB);
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky) {
+      tc::mma_bf16_w(ta + (2 * ky) * COUT, tc::dadd(ao, (4 * ks + ky) * PP), bk, idesc, acc);
+      tc::mma_bf16_w(ta + (2 * ky + 1) * COUT, tc::dadd(ae, (4 * ks + ky) * PP), bk, idesc, acc);
+    }
+  }
+  __device__ static bool row_of(int blk, int m, int& n) {
+    const int ky = blk >> 1, a = m / CIN, odd = !(blk & 1);
+    const int kx = odd ? (a == 0 ? 0 : a == 1 ? 2 : 3) : (a == 0 ? 1 : 3);
+    n = (ky * 3 + kx) * CIN + m % CIN;
+    return kx < 3;
+  }
+};
+
+// Persistent weight-gradient kernel over one geometry P (RWgHalo / RWgHaloS2).
+template <class P>
+__global__ void __launch_bounds__(kConvThreads, P::TMEM_COLS <= 256 ? 2 : 1)
     k_r8_wgrad_halo(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, const int* __restrict__ prefix,
                     int ntask, int in_tm, int dout_tm, int layer) {
-  typedef RWgHalo<C> P;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + P::STAGES * P::STAGE);
@@ -421,7 +484,7 @@ __global__ void __launch_bounds__(kConvThreads, C == 64 ? 1 : 2)  // (C = 64: TM
   pdl_wait();
 
   if (warp == 8) {
-    if (lane == 0) {  // ---------------- TMA producer: per tile the input halo and the dout tile
+    if (lane == 0) {  // ---------------- TMA producer: per tile the input halo / planes and the dout tile
       int s = 0, ti = ti0;
       for (int g = g0; g < g1; ++g) {
         ti = next_task(prefix, ntask, ti, g);
@@ -430,18 +493,15 @@ __global__ void __launch_bounds__(kConvThreads, C == 64 ? 1 : 2)  // (C = 64: TM
         const uint8_t* tm = reinterpret_cast<const uint8_t*>(c->tmaps);
         const int r0 = (g - __ldg(prefix + ti)) * P::IPS, r1 = min(tk.rows, r0 + P::IPS);
         for (int tile = r0 * P::TPI; tile < r1 * P::TPI; ++tile, ++s) {
-          const int buf = s % P::STAGES, r = tile / P::TPI, q = tile - r * P::TPI;
-          const int y0 = (q / (P::W / 8)) * 16, x0 = (q % (P::W / 8)) * 8;
-          const uint32_t st = sb + buf * P::STAGE;
+          const int buf = s % P::STAGES;
           if (s >= P::STAGES) tc::mbar_wait(empty + 8 * buf, ((s / P::STAGES) - 1) & 1);
-          tc::mbar_expect_tx(full + 8 * buf, P::G::HALO + P::DBYTES);
-          tc::tma_load_4d(st, tm + 128 * in_tm, full + 8 * buf, 0, x0 - 1, y0 - 1, r);
-          tc::tma_load_4d(st + P::HB, tm + 128 * dout_tm, full + 8 * buf, 0, x0, y0, r);
+          tc::mbar_expect_tx(full + 8 * buf, P::TX_BYTES);
+          P::load(sb + buf * P::STAGE, tm, in_tm, dout_tm, tile, full + 8 * buf);
         }
       }
     }
   } else if (warp == 9) {  // ---------------- MMA issuer (whole warp, elected lane issues)
-    const uint32_t idesc = tc::idesc_bf16(128, C, true, true), idesc1 = tc::idesc_bf16(128, C, false, true);
+    const uint32_t idesc = tc::idesc_bf16(128, P::COUT, true, true), idesc1 = tc::idesc_bf16(128, P::COUT, false, true);
     const uint64_t d1 = tc::sdesc(tc::smem_u32(ones), 0, 0);
     int s = 0, i = 0, ti = ti0;
     for (int g = g0; g < g1; ++g, ++i) {
@@ -455,22 +515,16 @@ __global__ void __launch_bounds__(kConvThreads, C == 64 ? 1 : 2)  // (C = 64: TM
       tc::fence_after();
       for (int tile = r0 * P::TPI; tile < r1 * P::TPI; ++tile, ++s) {
         const int buf = s % P::STAGES;
-        const uint32_t hb = sb + buf * P::STAGE, db = hb + P::HB;
+        const uint32_t st = sb + buf * P::STAGE;
         tc::mbar_wait(full + 8 * buf, (s / P::STAGES) & 1);
         tc::fence_after();
         const bool first = tile == r0 * P::TPI;
-        const uint64_t a0 = sdesc_swc(hb, P::PITCH, P::RB, P::RB);  // LBO = RB: the kx atoms one pixel apart
-        const uint64_t b0 = sdesc_swc(db, 8 * P::RB, P::RB);
+        const uint64_t b0 = sdesc_swc(st + P::HB, 8 * P::RBO, P::RBO);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {  // 16 pixels = 2 tile rows per K step
-          const uint64_t bk = tc::dadd(b0, ks * 16 * P::RB);
-#pragma unroll
-          for (int ky = 0; ky < 3; ++ky)
-#pragma unroll
-            for (int mh = 0; mh < P::MH; ++mh)
-              tc::mma_bf16_w(ta + (ky * P::MH + mh) * C, tc::dadd(a0, (ky + 2 * ks) * P::PITCH + mh * 2 * P::RB), bk,
-                             idesc, !(first && ks == 0));
-          tc::mma_bf16_w(ta + 3 * P::MH * C, d1, bk, idesc1, !(first && ks == 0));
+          const uint64_t bk = tc::dadd(b0, ks * 16 * P::RBO);
+          P::mma(st, ta, ks, !(first && ks == 0), idesc, bk);
+          tc::mma_bf16_w(ta + P::NBLK * P::COUT, d1, bk, idesc1, !(first && ks == 0));
         }
         tc::commit_w(empty + 8 * buf);
       }
@@ -488,22 +542,21 @@ __global__ void __launch_bounds__(kConvThreads, C == 64 ? 1 : 2)  // (C = 64: TM
       const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + a * P::COLS;
       tc::mbar_wait(acc_full + 8 * a, (P::NACC == 2 ? (i >> 1) : i) & 1);
       tc::fence_after();
-      float* part = (float*)c->buf[B_R_WSP] + r8_wsp_off(layer, c->B) + (int64_t)split * C * P::N_PART;
-      // accumulator blocks (ky, mh) and the bias block; the two warp groups take alternate co chunks
-      // (C = 16: warp group 1 idles)
-      if (16 * half < C) {
+      float* part = (float*)c->buf[B_R_WSP] + r8_wsp_off(layer, c->B) + (int64_t)split * P::COUT * P::N_PART;
+      // accumulator blocks and the bias block; the two warp groups take alternate co chunks
+      // (Cout = 16: warp group 1 idles)
+      if (16 * half < P::COUT) {
 #pragma unroll
-        for (int blk = 0; blk <= 3 * P::MH; ++blk) {
-          const bool bias = blk == 3 * P::MH;
-          const int ky = bias ? 0 : blk / P::MH, mh = bias ? 0 : blk % P::MH;
-          const int kx = mh * (128 / C) + m / C, ci = m % C;
-          const bool ok = bias ? m == 0 : kx < 3;
-          const int n = bias ? 9 * C : (ky * 3 + kx) * C + ci;
+        for (int blk = 0; blk <= P::NBLK; ++blk) {
+          const bool bias = blk == P::NBLK;
+          int n = 0;
+          const bool ok = bias ? m == 0 : P::row_of(blk, m, n);
+          if (bias) n = P::N_PART - 1;
 #pragma unroll
-          for (int cc = 0; cc < (C + 31) / 32; ++cc) {
+          for (int cc = 0; cc < (P::COUT + 31) / 32; ++cc) {
             const int c0 = 16 * half + 32 * cc;
             float v[16];
-            tc::tmem_ld16(ta + blk * C + c0, v);
+            tc::tmem_ld16(ta + blk * P::COUT + c0, v);
             if (ok) {
 #pragma unroll
               for (int e = 0; e < 16; ++e) part[(int64_t)(c0 + e) * P::N_PART + n] = v[e];
