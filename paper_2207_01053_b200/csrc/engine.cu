@@ -263,9 +263,9 @@ bool build_cnn_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap*
 }
 
 // ResNet-8 layers run by the halo kernels (kernels_resnet_halo.cuh): stride 1, C -> C, with C = 16 / 32 / 64
-// at 32x32 / 16x16 / 8x8.  PROTEA_R8_HALO = bit mask 1 fwd, 2 dgrad, 4 wgrad (default 7; a cleared bit
-// runs that pass on the gathered kernels of kernels_resnet_tc.cuh).
-int g_r8_halo = 7;
+// at 32x32 / 16x16 / 8x8.  PROTEA_R8_HALO = bit mask 1 fwd, 2 dgrad, 4 wgrad, 8 conv0 too (default 15; a
+// cleared bit runs that pass on the gathered kernels of kernels_resnet_tc.cuh).
+int g_r8_halo = 15;
 enum { R8H_FWD = 1, R8H_DGRAD = 2, R8H_WGRAD = 4 };
 int r8_halo_c(const Layer& l, int pass) {
   if (!(g_r8_halo & pass) || l.kind != 0 || l.k != 3 || l.stride != 1 || l.cin != l.cout) return 0;
@@ -273,6 +273,11 @@ int r8_halo_c(const Layer& l, int pass) {
   return ((c == 16 && l.hin == 32) || (c == 32 && l.hin == 16) || (c == 64 && l.hin == 8)) && l.win == l.hin ? c : 0;
 }
 int r8_halo_tiles(int c) { return c == 16 ? 8 : c == 32 ? 2 : 1; }
+// conv0 (3 -> 16 at 32x32, on the staged input) on RHalo0 / RWgHalo0
+bool r8_halo0(const Layer& l, int pass) {
+  return (g_r8_halo & 8) && (g_r8_halo & pass) && l.kind == 0 && l.k == 3 && l.stride == 1 && l.cin == 3 &&
+         l.cout == 16 && l.hin == 32 && l.win == 32;
+}
 // stride-2 fwd halo (RHaloS2): 16 -> 32 at 32x32 and 32 -> 64 at 16x16; returns Cin
 int r8_halo_s2(const Layer& l, int pass = R8H_FWD) {
   if (!(g_r8_halo & pass) || l.kind != 0 || l.k != 3 || l.stride != 2 || l.cout != 2 * l.cin) return 0;
@@ -301,6 +306,17 @@ bool build_r8_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap* 
     const uint64_t dw[3] = {C, 9, C}, sw_[2] = {2 * C, 18 * C};
     const uint32_t bw[3] = {(uint32_t)C, 1, (uint32_t)C};
     ok &= tmap_encode(&out[RTM_W1 + k], (const uint8_t*)r.buf[B_WSH] + 2 * l.off_w, 3, dw, sw_, bw, sw);
+  }
+  if (r8_halo0(m.layers[0], R8H_FWD | R8H_WGRAD)) {  // conv0: staged input rows, padded weight taps, dz0 tiles
+    const uint64_t d[3] = {256, 32, (uint64_t)B}, st[2] = {512, 16384};
+    const uint32_t box[3] = {80, 18, 1};
+    ok &= tmap_encode(&out[RTM_IN0], r.buf[B_R_XS], 3, d, st, box);
+    const uint64_t dw[3] = {8, 9, 16}, sw_[2] = {16, 144};
+    const uint32_t bw[3] = {8, 1, 16};
+    ok &= tmap_encode(&out[RTM_W0], r.buf[B_R_W0P], 3, dw, sw_, bw);
+    const uint64_t dd[4] = {16, 32, 32, (uint64_t)B}, sd[3] = {32, 1024, 32768};
+    const uint32_t bt[4] = {16, 8, 16, 1};
+    ok &= tmap_encode(&out[RTM_WD0], r.buf[B_R_G0], 4, dd, sd, bt, CU_TENSOR_MAP_SWIZZLE_32B);
   }
   static const int lay2[2] = {3, 5}, in2[2] = {B_R_O1, B_R_O2};
   for (int k = 0; k < 2; ++k) {  // stride-2 fwd: the input as pixel pairs [B][H][W/2][2 Cin]
@@ -465,6 +481,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
     if (op < RI_HEAD) {
       const Layer& l = m.layers[op - RI_F0];
       if (tc && r8_halo_c(l, R8H_FWD)) return rows * r8_halo_tiles(l.cin);  // halo kernels: 16 x 8 pixel tiles
+      if (tc && r8_halo0(l, R8H_FWD)) return rows * 8;
       if (tc && r8_halo_s2(l)) return rows * (l.cin == 16 ? 2 : 1);
       if (tc) return cdiv(rows * l.hout * l.wout, 128);
       return cdiv(rows * l.hout * l.wout, R_BM) * cdiv(l.cout, R_BN);
@@ -478,7 +495,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
     }
     if (op < RI_R0) {
       const Layer& l = m.layers[op - RI_W0];
-      if (tc && (r8_halo_c(l, R8H_WGRAD) || r8_halo_s2(l, R8H_WGRAD)))
+      if (tc && (r8_halo_c(l, R8H_WGRAD) || r8_halo_s2(l, R8H_WGRAD) || r8_halo0(l, R8H_WGRAD)))
         return rsplits(l, rows);  // halo wgrad: one item per split
       if (tc) return rsplits(l, rows) * cdiv(9 * (l.cin < 8 ? 8 : l.cin) + 1, 128);
       return rsplits(l, rows) * cdiv(l.cout, R_BM) * cdiv(9 * l.cin + 1, R_BN);
@@ -1030,6 +1047,10 @@ void launch_r8_wgrad_halo_p(protea_ctx* ctx, const ClientRec* drecs, int i, int 
 int r8_halo_slot(int i) { return i == 1 ? 0 : i == 2 ? 1 : i == 4 ? 2 : 3; }
 void launch_r8_wgrad_halo(protea_ctx* ctx, const ClientRec* drecs, const Layer& l, int i, const Launch& L, int opid,
                           const int32_t* dtab, int sm_cap = 0) {
+  if (i == 0) {
+    launch_r8_wgrad_halo_p<RWgHalo0>(ctx, drecs, 0, RTM_IN0, RTM_WD0, L, opid, dtab, sm_cap);
+    return;
+  }
   if (l.stride == 2) {
     const int k = i == 3 ? 0 : 1;
     if (l.cin == 16) launch_r8_wgrad_halo_p<RWgHaloS2<16>>(ctx, drecs, i, RTM_IN3 + k, RTM_WD3 + k, L, opid, dtab, sm_cap);
@@ -1104,7 +1125,9 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
         tf.in_buf = B_R_XS;
         tf.wbuf = B_R_W0P;
       }
-      if (r8_halo_s2(m.layers[i]))
+      if (i == 0 && r8_halo0(m.layers[0], R8H_FWD))
+        launch_conv_op(ctx, RHalo0{drecs, f.out_buf, m.layers[0].off_b}, L, RI_F0, dtab, 0);
+      else if (r8_halo_s2(m.layers[i]))
         launch_r8_halo_s2(ctx, drecs, m.layers[i], i, f.out_buf, L, RI_F0 + i, dtab);
       else if (r8_halo_c(m.layers[i], R8H_FWD))
         launch_r8_halo<false>(ctx, drecs, m.layers[i], i, f.out_buf, f.res_buf, f.res_mode, f.Cres, -1, L, RI_F0 + i,
@@ -1122,7 +1145,13 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
   }
   RHeadArgs ha{drecs, m.classes, fc.off_w, fc.off_b, lr};
   int ev = op_begin(ctx, PROTEA_OPC_R_HEAD, RI_HEAD);
-  k_rhead<T><<<L.ntask, 256, 0, ctx->cur>>>(ha, tasks);
+  static bool rh_attr = false;
+  if (!rh_attr) {  // classes <= 64: up to 49.4 KB of dynamic shared memory
+    cudaFuncSetAttribute(k_rhead<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rhead_smem(64));
+    cudaFuncSetAttribute(k_rhead<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rhead_smem(64));
+    rh_attr = true;
+  }
+  k_rhead<T><<<L.ntask, 256, rhead_smem(m.classes), ctx->cur>>>(ha, tasks);
   op_end(ctx, ev);
   // backward, layer 6 (b3b) down to 1 (b1a): dgrad (dout, out, mask, add), then wgrad + reduce
   struct Bw { int dout, out, mask, add, add_mode, cadd; };
@@ -1135,7 +1164,8 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
       {B_R_G1, B_R_G2, B_R_O2, B_R_G0, 2, 64},         // b3a: ds2 = (convT_s2(dr3) + sc(ds3)) * (o2 > 0)
       {B_R_G0, B_R_G1, B_R_R3, -1, 0, 0}};             // b3b: dr3 = convT(ds3) * (r3 > 0)
   const int wg_dout[7] = {B_R_G0, B_R_G2, B_R_G1, B_R_G0, B_R_G2, B_R_G1, B_R_G0};
-  ReduceMulti rm;
+  ReduceMultiV rm;
+  rm.chunk_base[0] = 0;
   // bf16, one chain: wgrad(i) runs on ctx->wstream beside dgrad(i) (both only read dout(i)), each on half
   // the SMs; the gradient buffers rotate over three, so dgrad(i - 2) (which overwrites wgrad(i)'s dout)
   // waits for wgrad(i), and the merged reduce waits for all of them
@@ -1188,7 +1218,7 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
         tw.L.lci = 3;
         tw.in_buf = B_R_XS;
       }
-      const bool hw = r8_halo_c(l, R8H_WGRAD) != 0 || r8_halo_s2(l, R8H_WGRAD) != 0;
+      const bool hw = r8_halo_c(l, R8H_WGRAD) != 0 || r8_halo_s2(l, R8H_WGRAD) != 0 || r8_halo0(l, R8H_WGRAD);
       if (ovl) {
         ctx->cur = ctx->wstream;
         cudaStreamWaitEvent(ctx->cur, ctx->r8ev[8 + i], 0);
@@ -1213,14 +1243,13 @@ void launch_step_resnet(protea_ctx* ctx, const ModelDims& m, const Launch& L, co
     // backward (each layer's dgrad above has read its old weights; the next writer is the next step)
     rm.a[i] = ReduceArgs{drecs, B_R_WSP, l.cout, 9 * l.cin, l.off_w, l.off_b, l.hout * l.wout, lr,
                          TC ? (i == 0 ? 2 : 1) : 0, i};
-    rm.prefix[i] = dtab + L.prefix_off[RI_R0 + i];
   }
   if (ovl)
     for (int i = 0; i < 2; ++i) cudaStreamWaitEvent(main_s, ctx->r8ev[i], 0);  // wgrads 2..6 joined above
-  rm.base[0] = 0;
-  for (int i = 0; i < 7; ++i) rm.base[i + 1] = rm.base[i] + L.grid[RI_R0 + i];
+  for (int i = 0; i < 7; ++i)
+    rm.chunk_base[i + 1] = rm.chunk_base[i] + cdiv(m.layers[i].cout * (9 * m.layers[i].cin + 1), 4 * kReduceBlock);
   ev = op_begin(ctx, PROTEA_OPC_R_REDUCE, -1);
-  k_reduce_multi<<<rm.base[7], kReduceBlock, 0, ctx->cur>>>(rm, tasks, L.ntask);
+  k_reduce_multi_v4<<<dim3(rm.chunk_base[7], L.ntask), kReduceBlock, 0, ctx->cur>>>(rm, tasks);
   op_end(ctx, ev);
 }
 
@@ -1529,7 +1558,7 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
   if (const char* fs = std::getenv("PROTEA_F1W_SIDE_SMEM")) ctx->f1w_side_smem = std::max(0, std::min(220 * 1024, std::atoi(fs)));
   if (const char* dc = std::getenv("PROTEA_DEFER_C2R")) ctx->defer_c2r = std::atoi(dc) != 0;
   if (const char* ro = std::getenv("PROTEA_R8_OVERLAP")) ctx->r8_overlap = std::atoi(ro) != 0;
-  if (const char* rh = std::getenv("PROTEA_R8_HALO")) g_r8_halo = std::atoi(rh) & 7;
+  if (const char* rh = std::getenv("PROTEA_R8_HALO")) g_r8_halo = std::atoi(rh) & 15;
   if (const char* rr = std::getenv("PROTEA_R8_OVERLAP_ROWS")) ctx->r8_overlap_rows = std::atoll(rr);
   if (const char* ln = std::getenv("PROTEA_LANES")) ctx->lanes = std::max(1, std::min(4, std::atoi(ln)));
   if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio_least) != cudaSuccess ||

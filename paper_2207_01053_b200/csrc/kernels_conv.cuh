@@ -469,11 +469,12 @@ template <class Op>
 __global__ void __launch_bounds__(kConvThreads, min_blocks<Op>::value)
     k_conv_persistent(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
   constexpr int D0 = Op::DBG;  // PROTEA_DBG counter block
+  constexpr int HST = halo_stages<Op>::value;  // halo ring depth
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sH = smem + Op::BSTRIDE;  // (HBYTES / B_BYTES: the TMA transaction bytes; *STRIDE: the buffer pitch)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * Op::HSTRIDE);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + HST * Op::HSTRIDE);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * HST);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = __ldg(prefix + ntask);
   const int g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
@@ -482,14 +483,16 @@ __global__ void __launch_bounds__(kConvThreads, min_blocks<Op>::value)
   const uint64_t t_start = threadIdx.x == 0 ? globaltimer() : 0;
 
   const uint32_t bar0 = tc::smem_u32(bars);
-  const uint32_t b_full = bar0, b_empty = bar0 + 8, h_full = bar0 + 16, h_empty = bar0 + 32, acc_full = bar0 + 48,
-                 acc_empty = bar0 + 64;
+  const uint32_t b_full = bar0, b_empty = bar0 + 8, h_full = bar0 + 16, h_empty = h_full + 8 * HST,
+                 acc_full = h_empty + 8 * HST, acc_empty = acc_full + 16;
   if (threadIdx.x == 0) {
     tc::mbar_init(b_full, 1);
     tc::mbar_init(b_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < HST; ++i) {
       tc::mbar_init(h_full + 8 * i, 1);
       tc::mbar_init(h_empty + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       tc::mbar_init(acc_full + 8 * i, 1);
       tc::mbar_init(acc_empty + 8 * i, 8);
     }
@@ -533,9 +536,9 @@ __global__ void __launch_bounds__(kConvThreads, min_blocks<Op>::value)
         }
         const int tile = g - cur.lo;
         for (int grp = 0; grp < Op::GROUPS; ++grp, ++s) {
-          const int buf = s & 1;
+          const int buf = s % HST;
           DBG_T0(tw);
-          if (s >= 2) tc::mbar_wait(h_empty + 8 * buf, ((s >> 1) - 1) & 1);
+          if (s >= HST) tc::mbar_wait(h_empty + 8 * buf, ((s / HST) - 1) & 1);
           DBG_ADD(D0 + 0, tw);
           DBG_T0(ti);
           tc::mbar_expect_tx(h_full + 8 * buf, Op::HBYTES);
@@ -565,9 +568,9 @@ __global__ void __launch_bounds__(kConvThreads, min_blocks<Op>::value)
         DBG_ADD(D0 + 2, ta0);
         tc::fence_after();
         for (int grp = 0; grp < Op::GROUPS; ++grp, ++s) {
-          const int buf = s & 1;
+          const int buf = s % HST;
           DBG_T0(tf);
-          tc::mbar_wait(h_full + 8 * buf, (s >> 1) & 1);
+          tc::mbar_wait(h_full + 8 * buf, (s / HST) & 1);
           DBG_ADD(D0 + 3, tf);
           DBG_T0(tm);
           tc::fence_after();

@@ -191,29 +191,50 @@ struct RHeadArgs {
   int64_t w, b;
   float lr;
 };
+inline size_t rhead_smem(int classes) { return (size_t)(2 * 64 * 64 + 64 + classes * 64) * 4; }
 template <typename T>
 __global__ void __launch_bounds__(256) k_rhead(RHeadArgs a, const Task* __restrict__ tasks) {
-  __shared__ float gap[64 * 64];
-  __shared__ float dlog[64 * 64];  // rows x classes (<= 64 x 64)
-  __shared__ float lossr[64];
+  extern __shared__ float rh_smem[];  // rhead_smem(classes) bytes
   const Task tk = tasks[blockIdx.x];
   const ClientRec* c = a.recs + tk.rec;
   const int rows = tk.rows, C = a.classes;
+  float* gap = rh_smem;           // [rows][64]
+  float* dlog = gap + 64 * 64;    // [rows][C] (<= 64 x 64)
+  float* lossr = dlog + 64 * 64;  // [rows]
+  float* Ws = lossr + 64;         // the FC weights [C][64] (old W: logits and dgap)
   const T* o3 = (const T*)c->buf[B_R_O3];
   float* W = c->params + a.w;
   float* bias = c->params + a.b;
-  for (int idx = threadIdx.x; idx < rows * 64; idx += 256) {
-    const int r = idx >> 6, ch = idx & 63;
-    float s = 0.f;
-#pragma unroll 8
-    for (int p = 0; p < 64; ++p) s += ldv(o3 + ((int64_t)r * 64 + p) * 64 + ch);
-    gap[idx] = s * (1.f / 64.f);
+  for (int idx = threadIdx.x; idx < C * 64; idx += 256) Ws[idx] = W[idx];  // (offset not 16-byte aligned)
+  // GAP: one (row, 16-byte channel group) per item, the 64 pixels as independent 16-byte loads, summed
+  // per channel in pixel order (the same fp32 order as a scalar loop over p)
+  constexpr int V = 16 / sizeof(T), G = 64 / V;
+  for (int it = threadIdx.x; it < rows * G; it += 256) {
+    const int r = it / G, cg = it - r * G;
+    const uint4* src = reinterpret_cast<const uint4*>(o3 + (int64_t)r * 4096 + cg * V);
+    float s[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) s[j] = 0.f;
+#pragma unroll
+    for (int p0 = 0; p0 < 64; p0 += 16) {
+      uint4 v[16];
+#pragma unroll
+      for (int p = 0; p < 16; ++p) v[p] = src[(p0 + p) * G];
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        const T* e = reinterpret_cast<const T*>(&v[p]);
+#pragma unroll
+        for (int j = 0; j < V; ++j) s[j] += ldv(e + j);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) gap[r * 64 + cg * V + j] = s[j] * (1.f / 64.f);
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < rows * C; idx += 256) {
     const int r = idx / C, cc = idx - r * C;
     float s = bias[cc];
-    for (int f = 0; f < 64; ++f) s = fmaf(gap[r * 64 + f], W[cc * 64 + f], s);
+    for (int f = 0; f < 64; ++f) s = fmaf(gap[r * 64 + f], Ws[cc * 64 + f], s);
     dlog[idx] = s;
   }
   __syncthreads();
@@ -236,13 +257,13 @@ __global__ void __launch_bounds__(256) k_rhead(RHeadArgs a, const Task* __restri
   for (int idx = threadIdx.x; idx < rows * 64; idx += 256) {
     const int r = idx >> 6, ch = idx & 63;
     float dg = 0.f;
-    for (int cc = 0; cc < C; ++cc) dg = fmaf(dlog[r * C + cc], W[cc * 64 + ch], dg);
+    for (int cc = 0; cc < C; ++cc) dg = fmaf(dlog[r * C + cc], Ws[cc * 64 + ch], dg);
     dgap[idx] = dg;
   }
   __syncthreads();
   // ds3 = dgap / 64 * (o3 > 0)  -> g0
   T* g0 = (T*)c->buf[B_R_G0];
-  constexpr int V = 16 / sizeof(T);  // elements per 16-byte vector
+  // (V: elements per 16-byte vector, as above)
   for (int iv = threadIdx.x; iv < rows * 64 * 64 / V; iv += 256) {
     const int idx = iv * V, r = idx >> 12, ch = idx & 63;
     const uint4 ov = reinterpret_cast<const uint4*>(o3)[iv];

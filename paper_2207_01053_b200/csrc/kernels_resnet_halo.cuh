@@ -35,6 +35,9 @@ enum RTmapId : int {
   RTM_W3, RTM_W5,                          // their weight taps [co][9][ci]: box (Cin, 1, Cout)
   RTM_DO3, RTM_DO5,                        // stride-2 dgrad dout halos of layers 3, 5: box (Cout, 9, 17, 1)
   RTM_WD3, RTM_WD5,                        // stride-2 wgrad dout tiles of layers 3, 5: box (Cout, 8, 16, 1)
+  RTM_IN0,                                 // conv0: the staged input [r][32][32 x 8] as 160-byte halo rows: box (80, 18, 1)
+  RTM_W0,                                  // conv0: the padded weight taps [16][9][8]: box (8, 1, 16)
+  RTM_WD0,                                 // conv0 wgrad dout tile (dz0, 16 ch): box (16, 8, 16, 1)
   RTM_COUNT
 };
 static_assert((int)RTM_COUNT <= kTmapSlots, "ResNet-8 maps exceed the per-client map array");
@@ -58,7 +61,8 @@ struct RHalo {
   static constexpr int TAPB = C * C * 2;  // one tap's weights [co][ci]
   static constexpr int B_BYTES = 9 * TAPB, BSTRIDE = (B_BYTES + 1023) & ~1023;
   static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 128;
-  static constexpr int SMEM = BSTRIDE + 2 * HSTRIDE + 256 + 1024;
+  static constexpr int HSTAGES = C == 16 ? 6 : C == 32 ? 4 : 3;  // halo ring: TMA latency over small tiles
+  static constexpr int SMEM = BSTRIDE + HSTAGES * HSTRIDE + 256 + 1024;
   static constexpr int TX = W / 8, TY = (H + 15) / 16, TILES_PER_IMAGE = TX * TY;
   static constexpr int NC = N / 2;                  // accumulator columns per epilogue warp group
   static constexpr int CW = NC < 16 ? NC : 16, NCH = NC / CW;  // tcgen05.ld width, loads per thread
@@ -153,6 +157,78 @@ struct RHalo {
 };
 
 // ---------------------------------------------------------------------------
+// conv0 fwd (3 -> 16 ch at 32x32) on the staged input xs [r][32][32][8] bf16 (channels 3-7 zero) and the
+// padded weights w0p [16][9][8] (B_R_W0P).  A pixel is 16 bytes, so the halo [18 rows][10 px][8 ch] is
+// ONE 2-D TMA box of 160-byte rows (x viewed as 256 elements per image row; the conv's zero padding is
+// the out-of-bounds fill, also at element -8).  A is K-major without swizzle: core matrix = 8 pixels of
+// a halo row (16-byte rows), SBO = one halo row (160 B), LBO = 16 B = the NEXT pixel, so one K = 16 MMA
+// covers two horizontally adjacent taps (ky, kx) and (ky, kx + 1).  B = [ky][kx 0..3][co 16][ci 8] with
+// the (ky, 3) blocks zero: 6 MMAs (M = 128, N = 16, K = 16) per 16 x 8 tile.  Epilogue bias + ReLU -> a0.
+// ---------------------------------------------------------------------------
+struct RHalo0 {
+  static constexpr int H = 32, W = 32, N = 16, NOUT = 16;
+  static constexpr bool B_MN = false;
+  static constexpr int GROUPS = 1;
+  static constexpr int PITCH = 160, HBYTES = 18 * PITCH, HSTRIDE = 3072;
+  static constexpr int B_BYTES = 9 * 256, BSTRIDE = 12 * 256;  // 9 taps by TMA; (ky, 3) zero blocks
+  static constexpr int TMEM_COLS = 32;
+  static constexpr int HSTAGES = 6;
+  static constexpr int SMEM = BSTRIDE + HSTAGES * HSTRIDE + 256 + 1024;
+  static constexpr int TX = 4, TILES_PER_IMAGE = 8;
+  static constexpr int NC = 8;  // accumulator columns per epilogue warp group
+  static constexpr int MIN_BLOCKS = 3;
+  static constexpr int DBG = 0;
+  const ClientRec* recs;
+  int out_buf;
+  int64_t b_off;
+
+  __device__ void load_b(const TcTile& t, uint32_t sb, uint32_t bar) const {
+    for (int ky = 0; ky < 3; ++ky)  // the (ky, 3) blocks: zeros (generic stores, then visible to the async proxy)
+      for (int i = 0; i < 16; ++i) tc::st_shared_v4(sb + (ky * 4 + 3) * 256 + 16 * i, 0u, 0u, 0u, 0u);
+    tc::fence_proxy_async();
+    for (int tap = 0; tap < 9; ++tap)
+      tc::tma_load_3d(sb + ((tap / 3) * 4 + tap % 3) * 256, tmap_of(t, RTM_W0), bar, 0, tap, 0);
+  }
+  __device__ void load_halo(const TcTile& t, int tile, int, uint32_t base, uint32_t bar) const {
+    const int r = tile >> 3, q = tile & 7, y0 = (q >> 2) * 16, x0 = (q & 3) * 8;
+    tc::tma_load_3d(base, tmap_of(t, RTM_IN0), bar, 8 * (x0 - 1), y0 - 1, r);
+  }
+  __device__ void mma_stage(uint32_t hb, uint32_t sb, uint32_t dt, int, uint32_t idesc, int = 0) const {
+    const uint64_t a0 = tc::sdesc(hb, 16, PITCH), b0 = tc::sdesc(sb, 256, 128);
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+        tc::mma_bf16_w(dt, tc::dadd(a0, ky * PITCH + 32 * p), tc::dadd(b0, (ky * 4 + 2 * p) * 256), idesc,
+                       (ky | p) != 0);
+  }
+  struct EpiState {
+    const ClientRec* c = nullptr;
+    float bias[NC];
+  };
+  struct Pre {};
+  __device__ void prefetch(const TcTile&, int, int, int, Pre&) const {}
+  __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
+                           int lane, EpiState& st, const Pre&) const {
+    const int g = warp >> 2, row = (warp & 3) * 32 + lane;
+    const int r = tile >> 3, q = tile & 7;
+    const int y = (q >> 2) * 16 + (row >> 3), x = (q & 3) * 8 + (row & 7);
+    if (st.c != t.c) {
+      st.c = t.c;
+#pragma unroll
+      for (int e = 0; e < NC; ++e) st.bias[e] = t.c->params[b_off + g * NC + e];
+    }
+    tc::mbar_wait(full_bar, parity);
+    tc::fence_after();
+    float v[NC], o[NC];
+    tc::tmem_ld8(tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(g * NC), v);
+#pragma unroll
+    for (int e = 0; e < NC; ++e) o[e] = fmaxf(v[e] + st.bias[e], 0.f);
+    st_bf16<NC>((bf16*)t.c->buf[out_buf] + (((int64_t)r * H + y) * W + x) * 16 + g * NC, o);
+  }
+};
+
+// ---------------------------------------------------------------------------
 // Stride-2 fwd (layers 3: 16 -> 32 ch, 32x32 -> 16x16; 5: 32 -> 64 ch, 16x16 -> 8x8).  Output tile =
 // 16 x 8 output pixels (8x8 outputs: rows 8-15 unused).  Output (yo, xo) reads input (2yo+ky-1,
 // 2xo+kx-1): the input rows are viewed as pixel PAIRS [H][W/2][2 Cin], so one TMA box of Cin channels
@@ -175,7 +251,8 @@ struct RHaloS2 {
   static constexpr int TAPB = COUT * CIN * 2;   // one tap's weights [co][ci]
   static constexpr int B_BYTES = 9 * TAPB, BSTRIDE = (B_BYTES + 1023) & ~1023;
   static constexpr int TMEM_COLS = 2 * N <= 64 ? 64 : 128;
-  static constexpr int SMEM = BSTRIDE + 2 * HSTRIDE + 256 + 1024;
+  static constexpr int HSTAGES = CIN == 16 ? 4 : 3;
+  static constexpr int SMEM = BSTRIDE + HSTAGES * HSTRIDE + 256 + 1024;
   static constexpr int TX = WO / 8, TY = (HO + 15) / 16, TILES_PER_IMAGE = TX * TY;
   static constexpr int NC = N / 2, NCH = NC / 16;
   static constexpr int MIN_BLOCKS = CIN == 16 ? 2 : 1;  // (CIN = 32: shared memory)
@@ -265,7 +342,8 @@ struct RHaloS2D {
   static constexpr int TAPB = COUT * CIN * 2;
   static constexpr int B_BYTES = 9 * TAPB, BSTRIDE = (B_BYTES + 1023) & ~1023;
   static constexpr int TMEM_COLS = 2 * N <= 32 ? 32 : 64;
-  static constexpr int SMEM = BSTRIDE + 2 * HSTRIDE + 256 + 1024;
+  static constexpr int HSTAGES = CIN == 16 ? 4 : 3;
+  static constexpr int SMEM = BSTRIDE + HSTAGES * HSTRIDE + 256 + 1024;
   static constexpr int TX = WO / 8, TY = (HO + 15) / 16, TPC = TX * TY, TILES_PER_IMAGE = 4 * TPC;
   static constexpr int NC = N / 2, CW = NC < 16 ? NC : 16, NCH = NC / CW;
   static constexpr int MIN_BLOCKS = 2;
@@ -444,7 +522,49 @@ struct RWgHaloS2 {  // stride 2: CIN -> 2 CIN, over the pixel-pair planes of RHa
   }
 };
 
-// Persistent weight-gradient kernel over one geometry P (RWgHalo / RWgHaloS2).
+// conv0 (3 -> 16 at 32x32) over RHalo0's 160-byte-row halo of the staged input.  A = the halo read
+// MN-major without swizzle: core matrix = 8 channels of one pixel (16 B) x 8 consecutive pixels (K rows,
+// 16 B apart), M groups j at SBO = 16 B = the next pixel (kx = j), K groups at LBO = one halo row (the
+// tile's next pixel row).  A halo row is 10 pixels, so groups j = 10..12 are the NEXT halo row's pixels
+// 0..2: one MMA covers tap rows ky and ky + 1 (M rows 8 j + ci: j 0-2 -> (ky, kx = j), j 10-12 ->
+// (ky + 1, kx = j - 10), channels ci < 3 real); block 0 = ky 0 and 1, block 1 = ky 2, plus the bias
+// MMA.  B = the dz0 tile as RWgHalo<16>.  Partial rows [16][28] (9 x 3 weights + bias).
+struct RWgHalo0 {
+  static constexpr int COUT = 16, CIN = 3, TPI = 8, IPS = kWgradChunkPx / 1024;
+  static constexpr int PITCH = RHalo0::PITCH;
+  static constexpr int NBLK = 2;
+  static constexpr int RBO = 2 * COUT, DBYTES = 128 * RBO;
+  static constexpr int HB = 3072, STAGE = HB + DBYTES;
+  static constexpr int TX_BYTES = RHalo0::HBYTES + DBYTES;
+  static constexpr int STAGES = 6;
+  static constexpr int COLS = (NBLK + 1) * COUT;
+  static constexpr int NACC = 2;
+  static constexpr int TMEM_COLS = 128;
+  static constexpr int SMEM = STAGES * STAGE + 256 + 128 + 1024;
+  static constexpr int N_PART = 9 * CIN + 1;
+  __device__ static void load(uint32_t st, const uint8_t* tm, int in_tm, int dout_tm, int tile, uint32_t bar) {
+    const int r = tile >> 3, q = tile & 7, y0 = (q >> 2) * 16, x0 = (q & 3) * 8;
+    tc::tma_load_3d(st, tm + 128 * in_tm, bar, 8 * (x0 - 1), y0 - 1, r);
+    tc::tma_load_4d(st + HB, tm + 128 * dout_tm, bar, 0, x0, y0, r);
+  }
+  __device__ static void mma(uint32_t st, uint32_t ta, int ks, bool acc, uint32_t idesc, uint64_t bk) {
+    const uint64_t a0 = tc::sdesc(st, PITCH, 16);
+    tc::mma_bf16_w(ta, tc::dadd(a0, 2 * ks * PITCH), bk, idesc, acc);                // ky 0 and 1
+    tc::mma_bf16_w(ta + COUT, tc::dadd(a0, (2 * ks + 2) * PITCH), bk, idesc, acc);   // ky 2
+  }
+  __device__ static bool row_of(int blk, int m, int& n) {
+    const int j = m >> 3, ci = m & 7;
+    int ky, kx;
+    if (blk == 0 && j < 3) ky = 0, kx = j;
+    else if (blk == 0 && j >= 10 && j < 13) ky = 1, kx = j - 10;
+    else if (blk == 1 && j < 3) ky = 2, kx = j;
+    else return false;
+    n = (ky * 3 + kx) * CIN + ci;
+    return ci < CIN;
+  }
+};
+
+// Persistent weight-gradient kernel over one geometry P (RWgHalo / RWgHaloS2 / RWgHalo0).
 template <class P>
 __global__ void __launch_bounds__(kConvThreads, P::TMEM_COLS <= 256 ? 2 : 1)
     k_r8_wgrad_halo(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, const int* __restrict__ prefix,

@@ -522,6 +522,60 @@ __global__ void __launch_bounds__(kReduceBlock)
   reduce_update_block(r.a[l], tasks, r.prefix[l], ntask, blockIdx.x - r.base[l]);
 }
 
+// The same seven reduces with 4 consecutive partial elements per thread (float4 loads; every layer's
+// split stride M (Nw + 1) and region offset are multiples of 4 floats) and the client as blockIdx.y
+// (every client of a launch has the same layers: no task search).  Block x = (layer l, chunk of
+// kReduceBlock * 4 elements) with chunk_base[l] <= x < chunk_base[l + 1].  Per element the splits are
+// summed in split order from 0.f exactly as reduce_update_block: bitwise the same update.
+struct ReduceMultiV {
+  ReduceArgs a[7];
+  int chunk_base[8];
+};
+__global__ void __launch_bounds__(kReduceBlock)
+    k_reduce_multi_v4(ReduceMultiV r, const Task* __restrict__ tasks) {
+  int l = 0;
+  while (l < 6 && (int)blockIdx.x >= r.chunk_base[l + 1]) ++l;
+  const ReduceArgs& a = r.a[l];
+  const Task tk = tasks[blockIdx.y];
+  const ClientRec* c = a.recs + tk.rec;
+  const int N = a.Nw + 1, total = a.M * N;
+  const int e0 = ((blockIdx.x - r.chunk_base[l]) * kReduceBlock + threadIdx.x) * 4;
+  if (e0 >= total) return;
+  const int splits = cdiv(tk.rows * a.px_per_row, kWgradChunkPx);
+  const float* part = (const float*)c->buf[a.wsp_buf] + (a.layer >= 0 ? r8_wsp_off(a.layer, c->B) : 0) + e0;
+  float g[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int s0 = 0; s0 < splits; s0 += 4) {  // 4 float4 loads in flight
+    float4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      v[j] = s0 + j < splits ? __ldcg(reinterpret_cast<const float4*>(part + (int64_t)(s0 + j) * total))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (s0 + j < splits) {
+        g[0] += v[j].x;
+        g[1] += v[j].y;
+        g[2] += v[j].z;
+        g[3] += v[j].w;
+      }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int e = e0 + k;
+    if (e >= total) break;
+    const int m = e / N, n = e - m * N;
+    if (n < a.Nw) {
+      const int64_t idx = a.off_w + (int64_t)m * a.Nw + n;
+      const float nw = c->params[idx] - a.lr * g[k];
+      c->params[idx] = nw;
+      if (a.shadow) ((__nv_bfloat16*)c->buf[B_WSH])[idx] = __float2bfloat16_rn(nw);
+      if (a.shadow == 2) ((__nv_bfloat16*)c->buf[B_R_W0P])[m * 72 + (n / 3) * 8 + n % 3] = __float2bfloat16_rn(nw);
+    } else {
+      c->params[a.off_b + m] -= a.lr * g[k];
+    }
+  }
+}
+
 // --------------------------------------------------------------------------
 // MLP ops (784-64-10)
 // --------------------------------------------------------------------------

@@ -114,6 +114,15 @@ struct min_blocks {  // resident CTAs per SM the op is compiled for (register ca
   static constexpr int value = f<Op>(nullptr);
 };
 
+template <class Op>
+struct halo_stages {  // depth of k_conv_persistent's halo ring (Op::HSTAGES), default 2
+  template <class U>
+  static constexpr int f(decltype(U::HSTAGES)*) { return U::HSTAGES; }
+  template <class U>
+  static constexpr int f(...) { return 2; }
+  static constexpr int value = f<Op>(nullptr);
+};
+
 template <int BN, int STAGES, class Op>
 __global__ void __launch_bounds__(kTcThreads, min_blocks<Op>::value)
     k_gemm_tc(const Op op, const Task* __restrict__ tasks, const int* __restrict__ prefix, int ntask) {
@@ -755,7 +764,7 @@ enum TmapId : int {
   TM_W2DS,     // W2 shadow (32, 25, 64) box (32,1,64) 64B-swizzled conv2 dgrad weights (width 1)
   TM_COUNT
 };
-constexpr int kTmapSlots = 24;  // per-client map array (CNN: TmapId; ResNet-8: RTmapId, kernels_resnet_halo.cuh)
+constexpr int kTmapSlots = 28;  // per-client map array (CNN: TmapId; ResNet-8: RTmapId, kernels_resnet_halo.cuh)
 static_assert((int)TM_COUNT <= kTmapSlots, "CNN maps exceed the per-client map array");
 
 __device__ __forceinline__ const void* tmap_of(const TcTile& t, int id) {
