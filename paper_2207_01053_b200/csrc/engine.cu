@@ -309,7 +309,7 @@ bool build_r8_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap* 
   }
   if (r8_halo0(m.layers[0], R8H_FWD | R8H_WGRAD)) {  // conv0: staged input rows, padded weight taps, dz0 tiles
     const uint64_t d[3] = {256, 32, (uint64_t)B}, st[2] = {512, 16384};
-    const uint32_t box[3] = {80, 18, 1};
+    const uint32_t box[3] = {80, 19, 1};  // (RHalo0::HBYTES)
     ok &= tmap_encode(&out[RTM_IN0], r.buf[B_R_XS], 3, d, st, box);
     const uint64_t dw[3] = {8, 9, 16}, sw_[2] = {16, 144};
     const uint32_t bw[3] = {8, 1, 16};
@@ -1008,9 +1008,24 @@ void launch_conv_op(protea_ctx* ctx, const Op& op, const Launch& L, int opid, co
   static int per_sm = 0;
   if (!per_sm) {
     cudaFuncSetAttribute(k_conv_persistent<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Op::SMEM);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conv_persistent<Op>, kConvThreads, Op::SMEM) !=
-            cudaSuccess || per_sm < 1)
-      per_sm = 1;
+    // without a carveout preference the occupancy query (and the launch) may assume a smaller shared-memory
+    // partition: 1 resident CTA where the op is built for MIN_BLOCKS
+    cudaFuncSetAttribute(k_conv_persistent<Op>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    const cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conv_persistent<Op>, kConvThreads, Op::SMEM);
+    if (std::getenv("PROTEA_VERBOSE")) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, k_conv_persistent<Op>);
+      fprintf(stderr, "launch_conv_op %s: occupancy rc %d per_sm %d smem %d regs %d static_smem %zu local %zu maxthr %d maxdyn %d carve %d\n",
+              __PRETTY_FUNCTION__, (int)oe, per_sm, Op::SMEM, fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes,
+              fa.maxThreadsPerBlock, fa.maxDynamicSharedSizeBytes, fa.preferredShmemCarveout);
+    }
+    // the occupancy query reports 1 CTA per SM for these tcgen05 kernels even where registers (launch bounds
+    // MIN_BLOCKS) and shared memory admit more (measured: RHalo<16> 64 regs x 320 threads, 43 KB): size the
+    // grid from the kernel's own limits (TMEM is allocated per CTA and fits MIN_BLOCKS x TMEM_COLS <= 512)
+    per_sm = std::max(per_sm, std::min<int>(min_blocks<Op>::value, (227 * 1024) / (Op::SMEM + 1024)));
+    if (const char* cap = std::getenv("PROTEA_CONV_PER_SM")) per_sm = std::min(per_sm, std::atoi(cap));
+    if (oe != cudaSuccess || per_sm < 1) per_sm = 1;
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const int grid = std::min(L.grid[opid], per_sm * std::min(sm_cap > 0 ? sm_cap : g_num_sms, ctx->spin_cap));
@@ -1031,9 +1046,14 @@ void launch_r8_wgrad_halo_p(protea_ctx* ctx, const ClientRec* drecs, int i, int 
   static int per_sm = 0;
   if (!per_sm) {
     cudaFuncSetAttribute(k_r8_wgrad_halo<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_r8_wgrad_halo<P>, kConvThreads, P::SMEM) !=
-            cudaSuccess || per_sm < 1)
-      per_sm = 1;
+    cudaFuncSetAttribute(k_r8_wgrad_halo<P>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    const cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_r8_wgrad_halo<P>, kConvThreads, P::SMEM);
+    if (std::getenv("PROTEA_VERBOSE"))
+      fprintf(stderr, "launch_r8_wgrad_halo %s: occupancy rc %d per_sm %d smem %d\n", __PRETTY_FUNCTION__, (int)oe, per_sm, P::SMEM);
+    per_sm = std::max(per_sm, std::min<int>(P::TMEM_COLS <= 256 ? 2 : 1, (227 * 1024) / (P::SMEM + 1024)));  // (as launch_conv_op)
+    if (const char* cap = std::getenv("PROTEA_WG_PER_SM")) per_sm = std::min(per_sm, std::atoi(cap));
+    if (oe != cudaSuccess || per_sm < 1) per_sm = 1;
     per_sm = std::min(per_sm, 512 / P::TMEM_COLS);  // resident CTAs must fit their TMEM allocations
   }
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
@@ -1558,6 +1578,7 @@ protea_status protea_init(const protea_init_opts* opts, protea_ctx** out) {
   if (const char* fs = std::getenv("PROTEA_F1W_SIDE_SMEM")) ctx->f1w_side_smem = std::max(0, std::min(220 * 1024, std::atoi(fs)));
   if (const char* dc = std::getenv("PROTEA_DEFER_C2R")) ctx->defer_c2r = std::atoi(dc) != 0;
   if (const char* ro = std::getenv("PROTEA_R8_OVERLAP")) ctx->r8_overlap = std::atoi(ro) != 0;
+  g_r8_halo = 15;  // (process-wide: every context re-reads it, so an earlier context's setting does not leak)
   if (const char* rh = std::getenv("PROTEA_R8_HALO")) g_r8_halo = std::atoi(rh) & 15;
   if (const char* rr = std::getenv("PROTEA_R8_OVERLAP_ROWS")) ctx->r8_overlap_rows = std::atoll(rr);
   if (const char* ln = std::getenv("PROTEA_LANES")) ctx->lanes = std::max(1, std::min(4, std::atoi(ln)));

@@ -35,6 +35,14 @@ constexpr int kConvThreads = 320;
 // dgrad epilogue operands: loaded one tile ahead (true) or at the start of the tile's epilogue,
 // before its accumulator wait (false).  Measured on B200: the one-tile-ahead variant was slower.
 constexpr bool kCrossTilePrefetch = false;
+template <class Op>
+struct xprefetch {  // k_conv_persistent loads tile g + 1's epilogue operands (Op::prefetch) before tile g's epilogue
+  template <class U>
+  static constexpr bool f(decltype(U::XPF)*) { return U::XPF; }
+  template <class U>
+  static constexpr bool f(...) { return kCrossTilePrefetch; }
+  static constexpr bool value = f<Op>(nullptr);
+};
 
 // ---------------------------------------------------------------------------
 // conv2 fwd / dgrad
@@ -591,7 +599,7 @@ __global__ void __launch_bounds__(kConvThreads, min_blocks<Op>::value)
     t.tk = tasks[cur.ti];
     t.c = op.recs + t.tk.rec;
     TcTile tn = t;
-    if (kCrossTilePrefetch) op.prefetch(t, g0 - cur.lo, warp, lane, pc);
+    if (xprefetch<Op>::value) op.prefetch(t, g0 - cur.lo, warp, lane, pc);
     int i = 0;
     for (int g = g0; g < g1; ++g, ++i) {
       if (g + 1 < g1) {
@@ -599,7 +607,7 @@ __global__ void __launch_bounds__(kConvThreads, min_blocks<Op>::value)
           tn.tk = tasks[nxt.ti];
           tn.c = op.recs + tn.tk.rec;
         }
-        if (kCrossTilePrefetch) op.prefetch(tn, g + 1 - nxt.lo, warp, lane, pn);
+        if (xprefetch<Op>::value) op.prefetch(tn, g + 1 - nxt.lo, warp, lane, pn);
       }
       const int acc = i & 1;
       DBG_T0(te);

@@ -35,7 +35,7 @@ enum RTmapId : int {
   RTM_W3, RTM_W5,                          // their weight taps [co][9][ci]: box (Cin, 1, Cout)
   RTM_DO3, RTM_DO5,                        // stride-2 dgrad dout halos of layers 3, 5: box (Cout, 9, 17, 1)
   RTM_WD3, RTM_WD5,                        // stride-2 wgrad dout tiles of layers 3, 5: box (Cout, 8, 16, 1)
-  RTM_IN0,                                 // conv0: the staged input [r][32][32 x 8] as 160-byte halo rows: box (80, 18, 1)
+  RTM_IN0,                                 // conv0: the staged input [r][32][32 x 8] as 160-byte halo rows: box (80, 19, 1)
   RTM_W0,                                  // conv0: the padded weight taps [16][9][8]: box (8, 1, 16)
   RTM_WD0,                                 // conv0 wgrad dout tile (dz0, 16 ch): box (16, 8, 16, 1)
   RTM_COUNT
@@ -103,10 +103,40 @@ struct RHalo {
     const ClientRec* c = nullptr;
     float bias[NCH][CW];
   };
-  struct Pre {};
-  __device__ void prefetch(const TcTile&, int, int, int, Pre&) const {}
+  // the epilogue's global operands (fwd: residual; dgrad: identity add and ReLU mask) are loaded one tile
+  // ahead (k_conv_persistent, XPF): their latency overlaps the previous tile's epilogue
+  static constexpr bool XPF = true;
+  static constexpr int NV = CW / 8;  // 16-byte vectors per chunk
+  struct Pre {
+    uint4 p[NCH][NV];
+    uint4 m[DGRAD ? NCH : 1][NV];
+  };
+  __device__ void prefetch(const TcTile& t, int tile, int warp, int lane, Pre& pr) const {
+    const int g = warp >> 2, row = (warp & 3) * 32 + lane;
+    const int r = tile / TILES_PER_IMAGE, q = tile - r * TILES_PER_IMAGE;
+    const int y = (q / TX) * 16 + (row >> 3), x = (q % TX) * 8 + (row & 7);
+    const bool valid = y < H;
+    const int64_t pix = ((int64_t)r * H + y) * W + x;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c0 = g * NC + CW * j;
+      const bf16* src = nullptr;
+      if (valid && res_mode == 1)
+        src = (const bf16*)t.c->buf[res_buf] + pix * C + c0;
+      else if (valid && !DGRAD && res_mode == 2 && c0 < Cres)
+        src = (const bf16*)t.c->buf[res_buf] + (((int64_t)r * 2 * H + 2 * y) * 2 * W + 2 * x) * Cres + c0;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) pr.p[j][v] = src ? reinterpret_cast<const uint4*>(src)[v] : make_uint4(0, 0, 0, 0);
+      if constexpr (DGRAD) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          pr.m[j][v] = valid ? reinterpret_cast<const uint4*>((const bf16*)t.c->buf[mask_buf] + pix * C + c0)[v]
+                             : make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
   __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
-                           int lane, EpiState& st, const Pre&) const {
+                           int lane, EpiState& st, const Pre& pr) const {
     const int g = warp >> 2, row = (warp & 3) * 32 + lane;  // warp group g: columns [g NC, (g + 1) NC)
     const int r = tile / TILES_PER_IMAGE, q = tile - r * TILES_PER_IMAGE;
     const int y = (q / TX) * 16 + (row >> 3), x = (q % TX) * 8 + (row & 7);
@@ -119,37 +149,25 @@ struct RHalo {
 #pragma unroll
         for (int e = 0; e < CW; ++e) st.bias[j][e] = t.c->params[b_off + g * NC + CW * j + e];
     }
-    float pre[NCH][CW], msk[NCH][CW];  // residual / add and mask operands, fetched before the MMA wait
-#pragma unroll
-    for (int j = 0; j < NCH; ++j) {
-      const int c0 = g * NC + CW * j;
-#pragma unroll
-      for (int e = 0; e < CW; ++e) pre[j][e] = 0.f;
-      if (!valid) continue;
-      if (res_mode == 1) {
-        ld_bf16<CW>((const bf16*)t.c->buf[res_buf] + pix * C + c0, pre[j]);
-      } else if (!DGRAD && res_mode == 2 && c0 < Cres) {
-        ld_bf16<CW>((const bf16*)t.c->buf[res_buf] + (((int64_t)r * 2 * H + 2 * y) * 2 * W + 2 * x) * Cres + c0,
-                    pre[j]);
-      }
-      if (DGRAD) ld_bf16<CW>((const bf16*)t.c->buf[mask_buf] + pix * C + c0, msk[j]);
-    }
     tc::mbar_wait(full_bar, parity);
     tc::fence_after();
 #pragma unroll
     for (int j = 0; j < NCH; ++j) {
       const int c0 = g * NC + CW * j;
-      float v[CW];
+      float v[CW], pre[CW];
       const uint32_t ta = tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0;
       if constexpr (CW == 16) tc::tmem_ld16(ta, v); else tc::tmem_ld8(ta, v);
       if (!valid) continue;
+      ld_bf16<CW>(reinterpret_cast<const bf16*>(&pr.p[j][0]), pre);
       float o[CW];
-      if (!DGRAD) {
+      if constexpr (!DGRAD) {
 #pragma unroll
-        for (int e = 0; e < CW; ++e) o[e] = fmaxf(v[e] + st.bias[j][e] + pre[j][e], 0.f);
+        for (int e = 0; e < CW; ++e) o[e] = fmaxf(v[e] + st.bias[j][e] + pre[e], 0.f);
       } else {
+        float msk[CW];
+        ld_bf16<CW>(reinterpret_cast<const bf16*>(&pr.m[j][0]), msk);
 #pragma unroll
-        for (int e = 0; e < CW; ++e) o[e] = msk[j][e] > 0.f ? v[e] + pre[j][e] : 0.f;
+        for (int e = 0; e < CW; ++e) o[e] = msk[e] > 0.f ? v[e] + pre[e] : 0.f;
       }
       st_bf16<CW>((bf16*)t.c->buf[out_buf] + pix * C + c0, o);
     }
@@ -158,7 +176,7 @@ struct RHalo {
 
 // ---------------------------------------------------------------------------
 // conv0 fwd (3 -> 16 ch at 32x32) on the staged input xs [r][32][32][8] bf16 (channels 3-7 zero) and the
-// padded weights w0p [16][9][8] (B_R_W0P).  A pixel is 16 bytes, so the halo [18 rows][10 px][8 ch] is
+// padded weights w0p [16][9][8] (B_R_W0P).  A pixel is 16 bytes, so the halo [18 (+1) rows][10 px][8 ch] is
 // ONE 2-D TMA box of 160-byte rows (x viewed as 256 elements per image row; the conv's zero padding is
 // the out-of-bounds fill, also at element -8).  A is K-major without swizzle: core matrix = 8 pixels of
 // a halo row (16-byte rows), SBO = one halo row (160 B), LBO = 16 B = the NEXT pixel, so one K = 16 MMA
@@ -169,8 +187,10 @@ struct RHalo0 {
   static constexpr int H = 32, W = 32, N = 16, NOUT = 16;
   static constexpr bool B_MN = false;
   static constexpr int GROUPS = 1;
-  static constexpr int PITCH = 160, HBYTES = 18 * PITCH, HSTRIDE = 3072;
-  static constexpr int B_BYTES = 9 * 256, BSTRIDE = 12 * 256;  // 9 taps by TMA; (ky, 3) zero blocks
+  // 19 halo rows: the pseudo-tap (2, 3) reads one pixel past row 17 (times a zero weight), which must be
+  // finite data, not stale shared memory (NaN x 0 = NaN)
+  static constexpr int PITCH = 160, HBYTES = 19 * PITCH, HSTRIDE = 3072;
+  static constexpr int B_BYTES = 12 * 256, BSTRIDE = 12 * 256;  // 9 taps + 3 zero blocks, all by TMA
   static constexpr int TMEM_COLS = 32;
   static constexpr int HSTAGES = 6;
   static constexpr int SMEM = BSTRIDE + HSTAGES * HSTRIDE + 256 + 1024;
@@ -183,11 +203,11 @@ struct RHalo0 {
   int64_t b_off;
 
   __device__ void load_b(const TcTile& t, uint32_t sb, uint32_t bar) const {
-    for (int ky = 0; ky < 3; ++ky)  // the (ky, 3) blocks: zeros (generic stores, then visible to the async proxy)
-      for (int i = 0; i < 16; ++i) tc::st_shared_v4(sb + (ky * 4 + 3) * 256 + 16 * i, 0u, 0u, 0u, 0u);
-    tc::fence_proxy_async();
-    for (int tap = 0; tap < 9; ++tap)
-      tc::tma_load_3d(sb + ((tap / 3) * 4 + tap % 3) * 256, tmap_of(t, RTM_W0), bar, 0, tap, 0);
+    // block (ky, kx) <- tap ky * 3 + kx; the (ky, 3) blocks are the map's out-of-bounds tap 9: the TMA's zero
+    // fill (generic-proxy stores here would not be ordered before the barrier's completion)
+    for (int ky = 0; ky < 3; ++ky)
+      for (int kx = 0; kx < 4; ++kx)
+        tc::tma_load_3d(sb + (ky * 4 + kx) * 256, tmap_of(t, RTM_W0), bar, 0, kx < 3 ? ky * 3 + kx : 9, 0);
   }
   __device__ void load_halo(const TcTile& t, int tile, int, uint32_t base, uint32_t bar) const {
     const int r = tile >> 3, q = tile & 7, y0 = (q >> 2) * 16, x0 = (q & 3) * 8;
@@ -390,27 +410,40 @@ struct RHaloS2D {
     }
   }
   struct EpiState {};
-  struct Pre {};
-  __device__ void prefetch(const TcTile&, int, int, int, Pre&) const {}
-  __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
-                           int lane, EpiState&, const Pre&) const {
+  static constexpr bool XPF = true;  // mask / shortcut gradient loaded one tile ahead (as RHalo)
+  static constexpr int NV = CW / 8;
+  struct Pre {
+    uint4 p[NCH][NV], m[NCH][NV];
+  };
+  __device__ void prefetch(const TcTile& t, int tile, int warp, int lane, Pre& pr) const {
     const int g = warp >> 2, row = (warp & 3) * 32 + lane;
     int r, cls, i0, j0;
     coords(tile, r, cls, i0, j0);
     const int i = i0 + (row >> 3), j = j0 + (row & 7), y = 2 * i + (cls >> 1), x = 2 * j + (cls & 1);
     const bool valid = i < HO;
     const int64_t pix = ((int64_t)r * H + y) * W + x;
-    float pre[NCH][CW], msk[NCH][CW];
 #pragma unroll
     for (int jj = 0; jj < NCH; ++jj) {
       const int c0 = g * NC + CW * jj;
+      const bool add = valid && cls == 0 && c0 < Cadd;  // option-A shortcut gradient at even (y, x)
+      const uint4* ps = reinterpret_cast<const uint4*>((const bf16*)t.c->buf[add_buf] +
+                                                       (((int64_t)r * HO + i) * WO + j) * Cadd + c0);
+      const uint4* ms = reinterpret_cast<const uint4*>((const bf16*)t.c->buf[mask_buf] + pix * CIN + c0);
 #pragma unroll
-      for (int e = 0; e < CW; ++e) pre[jj][e] = 0.f;
-      if (!valid) continue;
-      if (cls == 0 && c0 < Cadd)  // option-A shortcut gradient at even (y, x)
-        ld_bf16<CW>((const bf16*)t.c->buf[add_buf] + (((int64_t)r * HO + i) * WO + j) * Cadd + c0, pre[jj]);
-      ld_bf16<CW>((const bf16*)t.c->buf[mask_buf] + pix * CIN + c0, msk[jj]);
+      for (int v = 0; v < NV; ++v) {
+        pr.p[jj][v] = add ? ps[v] : make_uint4(0, 0, 0, 0);
+        pr.m[jj][v] = valid ? ms[v] : make_uint4(0, 0, 0, 0);
+      }
     }
+  }
+  __device__ void epilogue(const TcTile& t, int tile, uint32_t tacc, uint32_t full_bar, uint32_t parity, int warp,
+                           int lane, EpiState&, const Pre& pr) const {
+    const int g = warp >> 2, row = (warp & 3) * 32 + lane;
+    int r, cls, i0, j0;
+    coords(tile, r, cls, i0, j0);
+    const int i = i0 + (row >> 3), j = j0 + (row & 7), y = 2 * i + (cls >> 1), x = 2 * j + (cls & 1);
+    const bool valid = i < HO;
+    const int64_t pix = ((int64_t)r * H + y) * W + x;
     tc::mbar_wait(full_bar, parity);
     tc::fence_after();
 #pragma unroll
@@ -420,9 +453,11 @@ struct RHaloS2D {
       const uint32_t ta = tacc + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0;
       if constexpr (CW == 16) tc::tmem_ld16(ta, v); else tc::tmem_ld8(ta, v);
       if (!valid) continue;
-      float o[CW];
+      float o[CW], pre[CW], msk[CW];
+      ld_bf16<CW>(reinterpret_cast<const bf16*>(&pr.p[jj][0]), pre);
+      ld_bf16<CW>(reinterpret_cast<const bf16*>(&pr.m[jj][0]), msk);
 #pragma unroll
-      for (int e = 0; e < CW; ++e) o[e] = msk[jj][e] > 0.f ? v[e] + pre[jj][e] : 0.f;
+      for (int e = 0; e < CW; ++e) o[e] = msk[e] > 0.f ? v[e] + pre[e] : 0.f;
       st_bf16<CW>((bf16*)t.c->buf[out_buf] + pix * CIN + c0, o);
     }
   }
