@@ -301,7 +301,7 @@ bool build_r8_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap* 
     const uint32_t box[4] = {(uint32_t)C, 10, 18, 1};
     ok &= tmap_encode(&out[RTM_IN1 + k], r.buf[in_buf[k]], 4, d, st, box, sw);
     ok &= tmap_encode(&out[RTM_DO1 + k], r.buf[dout_buf[k]], 4, d, st, box, sw);
-    const uint32_t tbox[4] = {(uint32_t)C, 8, 16, 1};
+    const uint32_t tbox[4] = {(uint32_t)C, 8, 18, 1};  // (RWgHalo: one dout row above and below the tile)
     ok &= tmap_encode(&out[RTM_WD1 + k], r.buf[dout_buf[k]], 4, d, st, tbox, sw);
     const uint64_t dw[3] = {C, 9, C}, sw_[2] = {2 * C, 18 * C};
     const uint32_t bw[3] = {(uint32_t)C, 1, (uint32_t)C};
@@ -315,7 +315,7 @@ bool build_r8_tmaps(const ModelDims& m, const ClientRec& r, int B, CUtensorMap* 
     const uint32_t bw[3] = {8, 1, 16};
     ok &= tmap_encode(&out[RTM_W0], r.buf[B_R_W0P], 3, dw, sw_, bw);
     const uint64_t dd[4] = {16, 32, 32, (uint64_t)B}, sd[3] = {32, 1024, 32768};
-    const uint32_t bt[4] = {16, 8, 16, 1};
+    const uint32_t bt[4] = {16, 8, 18, 1};
     ok &= tmap_encode(&out[RTM_WD0], r.buf[B_R_G0], 4, dd, sd, bt, CU_TENSOR_MAP_SWIZZLE_32B);
   }
   static const int lay2[2] = {3, 5}, in2[2] = {B_R_O1, B_R_O2};

@@ -30,14 +30,14 @@ enum RTmapId : int {
   RTM_IN1 = 0, RTM_IN2, RTM_IN4, RTM_IN6,  // fwd input halos of layers 1, 2, 4, 6: box (C, 10, 18, 1)
   RTM_DO1, RTM_DO2, RTM_DO4, RTM_DO6,      // dgrad dout halos of layers 1, 2, 4, 6
   RTM_W1, RTM_W2, RTM_W4, RTM_W6,          // weight shadow of layers 1, 2, 4, 6 [co][9][ci]: box (C, 1, C)
-  RTM_WD1, RTM_WD2, RTM_WD4, RTM_WD6,      // wgrad dout tiles of layers 1, 2, 4, 6: box (C, 8, 16, 1)
+  RTM_WD1, RTM_WD2, RTM_WD4, RTM_WD6,      // wgrad dout halos of layers 1, 2, 4, 6: box (C, 8, 18, 1)
   RTM_IN3, RTM_IN5,                        // stride-2 fwd input of layers 3, 5 as pixel pairs: box (Cin, 9, 33, 1)
   RTM_W3, RTM_W5,                          // their weight taps [co][9][ci]: box (Cin, 1, Cout)
   RTM_DO3, RTM_DO5,                        // stride-2 dgrad dout halos of layers 3, 5: box (Cout, 9, 17, 1)
   RTM_WD3, RTM_WD5,                        // stride-2 wgrad dout tiles of layers 3, 5: box (Cout, 8, 16, 1)
   RTM_IN0,                                 // conv0: the staged input [r][32][32 x 8] as 160-byte halo rows: box (80, 19, 1)
   RTM_W0,                                  // conv0: the padded weight taps [16][9][8]: box (8, 1, 16)
-  RTM_WD0,                                 // conv0 wgrad dout tile (dz0, 16 ch): box (16, 8, 16, 1)
+  RTM_WD0,                                 // conv0 wgrad dout halo (dz0, 16 ch): box (16, 8, 18, 1)
   RTM_COUNT
 };
 static_assert((int)RTM_COUNT <= kTmapSlots, "ResNet-8 maps exceed the per-client map array");
@@ -465,14 +465,18 @@ struct RHaloS2D {
 
 // ---------------------------------------------------------------------------
 // Weight gradient of the same layers, one work item per 2048-pixel split of a client (the split
-// partials of kernels_resnet_tc.cuh RTcWgrad, summed in split order + SGD by k_reduce_multi):
-//   D[(kx, ci)][co] (per ky) = sum_p in[p + (ky-1, kx-1)][ci] dout[p][co],   K = the split's pixels
-// Per 16 x 8 tile the TMA brings the input halo (as the fwd) and the dout tile [16][8][C].  A is the
-// halo read MN-major: M = (kx, ci) with the three kx "atoms" ONE pixel (RB bytes) apart (LBO = RB: the
-// same bytes serve the three column shifts), K = pixels (8 per halo row, SBO = one halo row), so one
-// MMA covers a whole tap row: M = 3C (<= 128; C = 64: kx 0-1 and kx 2 as two MMAs), N = co.
-// B = the dout tile, MN-major (N = co, K = pixels).  The bias gradient sum_p dout[p][co] is one more
-// MMA per K step with A = a 128-byte block of bf16 ones (LBO = SBO = 0: every core matrix aliases it).
+// partials of kernels_resnet_tc.cuh RTcWgrad, summed in split order + SGD by k_reduce_multi_v4):
+//   dW[co][ky][kx][ci] = sum_p in[p + (ky-1, kx-1)][ci] dout[p][co],   K = the split's pixels
+// Stride 1 (RWgHalo, RWgHalo0): per 16 x 8 tile the TMA brings the input halo (as the fwd) and the dout
+// tile WITH one halo row above and below [18][8][C].  Summing over the input pixels q of the tile instead
+// of the output pixels: dW[ky][kx] = sum_q in[q + (0, kx-1)][ci] dout[q - (ky-1, 0)][co]; the tiles'
+// input rows partition the image, so every (q, ky) pair is counted once (dout rows -1 / H are the
+// TMA's zero fill).  A = the input rows of the tile read MN-major: M = (kx, ci), the three kx "atoms"
+// ONE pixel (RB bytes) apart (LBO = RB: the same bytes serve the three column shifts), K = pixels
+// (8 per halo row, SBO = one halo row).  B = the dout halo read MN-major with N = (a, co): atom a = the
+// dout rows shifted by a (LBO = one dout row), i.e. tap row ky = 2 - a.  So ONE MMA covers all nine
+// taps (M = 3C <= 128, N = 3C; C = 64: kx 0-1 and kx 2 as two MMAs).  The bias gradient sum_p dout[p][co]
+// is one more MMA (N = C, the unshifted atom a = 1) with A = a 128-byte block of bf16 ones (LBO = SBO = 0).
 // Accumulators stay in TMEM over the split's tiles (double-buffered across items where TMEM allows);
 // the 8 epilogue warps write the partial [co][9 C + 1] rows (row m of the accumulator = (kx, ci):
 // consecutive lanes store consecutive weights).
@@ -485,8 +489,11 @@ struct RWgHalo {  // stride 1: C -> C
   static constexpr int COUT = C, CIN = C;
   static constexpr int IPS = kWgradChunkPx / (H * W);                       // images per split
   static constexpr int MH = C == 64 ? 2 : 1;                                 // M = (kx, ci) halves
-  static constexpr int NBLK = 3 * MH;                                        // accumulator blocks (ky, mh)
-  static constexpr int RBO = 2 * COUT, DBYTES = 128 * RBO;                   // dout tile [16][8][Cout]
+  static constexpr int NMMA = 3 * COUT;                                      // N = (a, co) of the tap MMAs
+  static constexpr int NBLK = 3 * MH;                                        // accumulator blocks (mh, a)
+  static constexpr int RBO = 2 * COUT, DBYTES = 144 * RBO;                   // dout halo [18][8][Cout]
+  static constexpr int B_LBO = 8 * RBO;                                      // N atoms: one dout row apart
+  static constexpr int BIAS_B = 8 * RBO;                                     // the unshifted atom (a = 1)
   static constexpr int HB = G::HSTRIDE, STAGE = HB + ((DBYTES + 1023) & ~1023);
   static constexpr int TX_BYTES = G::HALO + DBYTES;
   static constexpr int STAGES = C == 64 ? 3 : 4;
@@ -499,21 +506,53 @@ struct RWgHalo {  // stride 1: C -> C
   __device__ static void load(uint32_t st, const uint8_t* tm, int in_tm, int dout_tm, int tile, uint32_t bar) {
     const int r = tile / TPI, q = tile - r * TPI, y0 = (q / (W / 8)) * 16, x0 = (q % (W / 8)) * 8;
     tc::tma_load_4d(st, tm + 128 * in_tm, bar, 0, x0 - 1, y0 - 1, r);
-    tc::tma_load_4d(st + HB, tm + 128 * dout_tm, bar, 0, x0, y0, r);
+    tc::tma_load_4d(st + HB, tm + 128 * dout_tm, bar, 0, x0, y0 - 1, r);  // dout rows y0 - 1 .. y0 + 16
   }
-  // K step ks = tile pixel rows 2 ks, 2 ks + 1; block (ky, mh) = D[(kx, ci)][co] of tap row ky
+  // K step ks = tile pixel rows 2 ks, 2 ks + 1 (halo rows 2 ks + 1, + 2); block (mh, a) at columns (3 mh + a) C
   __device__ static void mma(uint32_t st, uint32_t ta, int ks, bool acc, uint32_t idesc, uint64_t bk) {
     const uint64_t a0 = sdesc_swc(st, PITCH, RB, RB);  // LBO = RB: the kx atoms one pixel apart
 #pragma unroll
-    for (int ky = 0; ky < 3; ++ky)
-#pragma unroll
-      for (int mh = 0; mh < MH; ++mh)
-        tc::mma_bf16_w(ta + (ky * MH + mh) * COUT, tc::dadd(a0, (ky + 2 * ks) * PITCH + mh * 2 * RB), bk, idesc, acc);
+    for (int mh = 0; mh < MH; ++mh)
+      tc::mma_bf16_w(ta + mh * NMMA, tc::dadd(a0, (1 + 2 * ks) * PITCH + mh * 2 * RB), bk, idesc, acc);
   }
   __device__ static bool row_of(int blk, int m, int& n) {  // accumulator row m of block blk -> partial column
-    const int ky = blk / MH, kx = (blk % MH) * (128 / C) + m / C;
+    const int mh = blk / 3, ky = 2 - blk % 3, kx = mh * (128 / C) + m / C;
     n = (ky * 3 + kx) * C + m % C;
     return kx < 3;
+  }
+};
+
+// conv0 (3 -> 16 at 32x32) over RHalo0's 160-byte-row halo of the staged input.  A = the tile's input rows
+// read MN-major without swizzle: core matrix = 8 channels of one pixel (16 B) x 8 consecutive pixels (K
+// rows, 16 B apart), M groups j at SBO = 16 B = the next pixel (kx = j, j < 3; channels ci < 3 real),
+// K groups at LBO = one halo row.  B = the dz0 halo with the tap rows as N atoms, as RWgHalo<16>.
+// Partial rows [16][28] (9 x 3 weights + bias).
+struct RWgHalo0 {
+  static constexpr int COUT = 16, CIN = 3, TPI = 8, IPS = kWgradChunkPx / 1024;
+  static constexpr int PITCH = RHalo0::PITCH;
+  static constexpr int NMMA = 3 * COUT, NBLK = 3;
+  static constexpr int RBO = 2 * COUT, DBYTES = 144 * RBO;
+  static constexpr int B_LBO = 8 * RBO, BIAS_B = 8 * RBO;
+  static constexpr int HB = 3072, STAGE = HB + ((DBYTES + 1023) & ~1023);
+  static constexpr int TX_BYTES = RHalo0::HBYTES + DBYTES;
+  static constexpr int STAGES = 6;
+  static constexpr int COLS = (NBLK + 1) * COUT;
+  static constexpr int NACC = 2;
+  static constexpr int TMEM_COLS = 128;
+  static constexpr int SMEM = STAGES * STAGE + 256 + 128 + 1024;
+  static constexpr int N_PART = 9 * CIN + 1;
+  __device__ static void load(uint32_t st, const uint8_t* tm, int in_tm, int dout_tm, int tile, uint32_t bar) {
+    const int r = tile >> 3, q = tile & 7, y0 = (q >> 2) * 16, x0 = (q & 3) * 8;
+    tc::tma_load_3d(st, tm + 128 * in_tm, bar, 8 * (x0 - 1), y0 - 1, r);
+    tc::tma_load_4d(st + HB, tm + 128 * dout_tm, bar, 0, x0, y0 - 1, r);
+  }
+  __device__ static void mma(uint32_t st, uint32_t ta, int ks, bool acc, uint32_t idesc, uint64_t bk) {
+    tc::mma_bf16_w(ta, tc::dadd(tc::sdesc(st, PITCH, 16), (1 + 2 * ks) * PITCH), bk, idesc, acc);
+  }
+  __device__ static bool row_of(int blk, int m, int& n) {
+    const int j = m >> 3, ci = m & 7, ky = 2 - blk;
+    n = (ky * 3 + j) * CIN + ci;
+    return j < 3 && ci < CIN;
   }
 };
 
@@ -523,6 +562,7 @@ struct RWgHaloS2 {  // stride 2: CIN -> 2 CIN, over the pixel-pair planes of RHa
   static constexpr int COUT = 2 * CIN, RB = G::RB, PP = G::PP, TPI = G::TILES_PER_IMAGE, HO = G::HO, WO = G::WO;
   static constexpr int IPS = kWgradChunkPx / (HO * WO);
   static constexpr int NBLK = 6;                                             // (ky, odd plane: kx 0, 2), (ky, even: kx 1)
+  static constexpr int NMMA = COUT, B_LBO = 16, BIAS_B = 0;                  // (one N atom: the dout tile itself)
   static constexpr int RBO = 2 * COUT, DBYTES = 128 * RBO;
   static constexpr int HB = G::HSTRIDE, STAGE = HB + ((DBYTES + 1023) & ~1023);
   static constexpr int TX_BYTES = G::HBYTES + DBYTES;
@@ -554,48 +594,6 @@ struct RWgHaloS2 {  // stride 2: CIN -> 2 CIN, over the pixel-pair planes of RHa
     const int kx = odd ? (a == 0 ? 0 : a == 1 ? 2 : 3) : (a == 0 ? 1 : 3);
     n = (ky * 3 + kx) * CIN + m % CIN;
     return kx < 3;
-  }
-};
-
-// conv0 (3 -> 16 at 32x32) over RHalo0's 160-byte-row halo of the staged input.  A = the halo read
-// MN-major without swizzle: core matrix = 8 channels of one pixel (16 B) x 8 consecutive pixels (K rows,
-// 16 B apart), M groups j at SBO = 16 B = the next pixel (kx = j), K groups at LBO = one halo row (the
-// tile's next pixel row).  A halo row is 10 pixels, so groups j = 10..12 are the NEXT halo row's pixels
-// 0..2: one MMA covers tap rows ky and ky + 1 (M rows 8 j + ci: j 0-2 -> (ky, kx = j), j 10-12 ->
-// (ky + 1, kx = j - 10), channels ci < 3 real); block 0 = ky 0 and 1, block 1 = ky 2, plus the bias
-// MMA.  B = the dz0 tile as RWgHalo<16>.  Partial rows [16][28] (9 x 3 weights + bias).
-struct RWgHalo0 {
-  static constexpr int COUT = 16, CIN = 3, TPI = 8, IPS = kWgradChunkPx / 1024;
-  static constexpr int PITCH = RHalo0::PITCH;
-  static constexpr int NBLK = 2;
-  static constexpr int RBO = 2 * COUT, DBYTES = 128 * RBO;
-  static constexpr int HB = 3072, STAGE = HB + DBYTES;
-  static constexpr int TX_BYTES = RHalo0::HBYTES + DBYTES;
-  static constexpr int STAGES = 6;
-  static constexpr int COLS = (NBLK + 1) * COUT;
-  static constexpr int NACC = 2;
-  static constexpr int TMEM_COLS = 128;
-  static constexpr int SMEM = STAGES * STAGE + 256 + 128 + 1024;
-  static constexpr int N_PART = 9 * CIN + 1;
-  __device__ static void load(uint32_t st, const uint8_t* tm, int in_tm, int dout_tm, int tile, uint32_t bar) {
-    const int r = tile >> 3, q = tile & 7, y0 = (q >> 2) * 16, x0 = (q & 3) * 8;
-    tc::tma_load_3d(st, tm + 128 * in_tm, bar, 8 * (x0 - 1), y0 - 1, r);
-    tc::tma_load_4d(st + HB, tm + 128 * dout_tm, bar, 0, x0, y0, r);
-  }
-  __device__ static void mma(uint32_t st, uint32_t ta, int ks, bool acc, uint32_t idesc, uint64_t bk) {
-    const uint64_t a0 = tc::sdesc(st, PITCH, 16);
-    tc::mma_bf16_w(ta, tc::dadd(a0, 2 * ks * PITCH), bk, idesc, acc);                // ky 0 and 1
-    tc::mma_bf16_w(ta + COUT, tc::dadd(a0, (2 * ks + 2) * PITCH), bk, idesc, acc);   // ky 2
-  }
-  __device__ static bool row_of(int blk, int m, int& n) {
-    const int j = m >> 3, ci = m & 7;
-    int ky, kx;
-    if (blk == 0 && j < 3) ky = 0, kx = j;
-    else if (blk == 0 && j >= 10 && j < 13) ky = 1, kx = j - 10;
-    else if (blk == 1 && j < 3) ky = 2, kx = j;
-    else return false;
-    n = (ky * 3 + kx) * CIN + ci;
-    return ci < CIN;
   }
 };
 
@@ -656,7 +654,7 @@ __global__ void __launch_bounds__(kConvThreads, P::TMEM_COLS <= 256 ? 2 : 1)
       }
     }
   } else if (warp == 9) {  // ---------------- MMA issuer (whole warp, elected lane issues)
-    const uint32_t idesc = tc::idesc_bf16(128, P::COUT, true, true), idesc1 = tc::idesc_bf16(128, P::COUT, false, true);
+    const uint32_t idesc = tc::idesc_bf16(128, P::NMMA, true, true), idesc1 = tc::idesc_bf16(128, P::COUT, false, true);
     const uint64_t d1 = tc::sdesc(tc::smem_u32(ones), 0, 0);
     int s = 0, i = 0, ti = ti0;
     for (int g = g0; g < g1; ++g, ++i) {
@@ -674,12 +672,12 @@ __global__ void __launch_bounds__(kConvThreads, P::TMEM_COLS <= 256 ? 2 : 1)
         tc::mbar_wait(full + 8 * buf, (s / P::STAGES) & 1);
         tc::fence_after();
         const bool first = tile == r0 * P::TPI;
-        const uint64_t b0 = sdesc_swc(st + P::HB, 8 * P::RBO, P::RBO);
+        const uint64_t b0 = sdesc_swc(st + P::HB, 8 * P::RBO, P::RBO, P::B_LBO);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {  // 16 pixels = 2 tile rows per K step
           const uint64_t bk = tc::dadd(b0, ks * 16 * P::RBO);
           P::mma(st, ta, ks, !(first && ks == 0), idesc, bk);
-          tc::mma_bf16_w(ta + P::NBLK * P::COUT, d1, bk, idesc1, !(first && ks == 0));
+          tc::mma_bf16_w(ta + P::NBLK * P::COUT, d1, tc::dadd(bk, P::BIAS_B), idesc1, !(first && ks == 0));
         }
         tc::commit_w(empty + 8 * buf);
       }
