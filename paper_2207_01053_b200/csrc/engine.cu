@@ -710,6 +710,7 @@ struct Launch {
   int64_t prefix_off[OP_COUNT];
   int grid[OP_COUNT];
   int c2w_groups;                       // width-1 conv2 wgrad: M-tile groups per split (1 or 7)
+  int max_rows;                         // largest batch of the launch (grids indexed by client: k_stage_x)
   uint64_t fl[OP_COUNT], by[OP_COUNT];  // algorithmic work of each op of this launch (op_work)
 };
 
@@ -770,7 +771,9 @@ void launch_conv_persistent(protea_ctx* ctx, const ClientRec* drecs, const CnnDi
   op.recs = drecs;
   op.d = d;
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
-  const int grid = std::min(L.grid[opid], ctx->spin_cap);  // one CTA per SM, each a contiguous tile range
+  // MIN_BLOCKS CTAs per SM (default 1), each a contiguous tile range
+  const int per_sm = std::max(1, std::min<int>(min_blocks<Op>::value, (227 * 1024) / (Op::SMEM + 1024)));
+  const int grid = std::min(L.grid[opid], per_sm * ctx->spin_cap);
   const int ev = op_begin(ctx, op_class(opid), opid);
   launch_k(ctx, k_conv_persistent<Op>, grid, kConvThreads, Op::SMEM, op, tasks, (const int*)(dtab + L.prefix_off[opid]),
            L.ntask);
@@ -867,8 +870,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const CnnDims d = cnn_dims(m);
   int ev = op_begin(ctx, OP_STAGE, OP_STAGE);
-  launch_k(ctx, k_stage_x, L.grid[OP_STAGE], kStageThreads, 0, drecs, tasks, (const int*)(dtab + L.prefix_off[OP_STAGE]),
-           L.ntask);
+  launch_k(ctx, k_stage_x, dim3(cdiv(L.max_rows * 1296, kStageThreads), L.ntask), kStageThreads, 0, drecs, tasks);
   op_end(ctx, ev);
   launch_conv_persistent<QuadConv1<WQ>>(ctx, drecs, d, L, OP_C1F, dtab);
   join_group(ctx, L.group);  // the previous step's deferred fc1 wgrad still reads a2
@@ -1978,6 +1980,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const floa
           const RunClient& c = *act[i];
           const int s = (int)(t - c.admit), ep = s / c.nb, j = s % c.nb;
           rows[i] = micro_rows(c, t);
+          L.max_rows = std::max(L.max_rows, rows[i]);
           tab.push_back(c.rec);
           tab.push_back((int32_t)std::min<int64_t>(c.B, c.n - (int64_t)j * c.B));  // |beta| of the whole batch
           tab.push_back(rows[i]);

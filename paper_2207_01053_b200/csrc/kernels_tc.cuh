@@ -950,16 +950,15 @@ struct TmaFc1Dgrad : TcFc1Dgrad<WQ> {
 // --------------------------------------------------------------------------
 constexpr int kStageThreads = 256;
 __global__ void __launch_bounds__(kStageThreads)
-    k_stage_x(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks, const int* __restrict__ prefix,
-              int ntask) {
+    k_stage_x(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks) {  // grid (blocks, task)
   __shared__ float lut[256];  // px01(u): the same fp32 values as the division, without one per channel
   lut[threadIdx.x] = px01((uint8_t)threadIdx.x);
   pdl_wait();  // xs is still read by the preceding conv1 wgrad
   pdl_trigger();
-  const int ti = find_task(prefix, ntask, blockIdx.x);
-  const Task tk = tasks[ti];
+  const Task tk = tasks[blockIdx.y];
+  if ((int)blockIdx.x * kStageThreads >= tk.rows * 1296) return;
   const ClientRec* c = recs + tk.rec;
-  const int e = (blockIdx.x - __ldg(prefix + ti)) * kStageThreads + threadIdx.x;  // staged pixel, storage order
+  const int e = blockIdx.x * kStageThreads + threadIdx.x;  // staged pixel, storage order
   const int r = e / 1296, rem = e - r * 1296, Y = rem / 36, rx = rem - Y * 36, X = 2 * (rx % 18) + rx / 18;
   const int y = Y - 2, x = X - 2;
   const bool in = e < tk.rows * 1296 && (unsigned)y < 32u && (unsigned)x < 32u;
