@@ -128,9 +128,11 @@ struct protea_ctx {
   std::vector<cudaEvent_t> gdone;
   std::vector<char> gpending;      // per model group: a deferred fc1 wgrad not yet joined
   bool overlap_now = false;        // current iteration defers fc1 wgrad (light iteration)
-  // programmatic dependent launch on the lock-step stream (PROTEA_PDL=1).  Off by default: measured on
-  // B200, config 2: 70.2 ms/round without, 71.5 ms with (early CTAs of the next kernel hold SM resources).
-  bool pdl = false;
+  // programmatic dependent launch on the lock-step stream (PROTEA_PDL=0 turns it off): the next kernel's
+  // prologue (barriers, TMEM, its first client's weights) overlaps the previous kernel's drain.  Round 1
+  // measured it slower (config 2: 70.2 -> 71.5 ms); with round 2's kernels it is faster: config 2
+  // 63.5 -> 62.0 ms, config 5 44.1 -> 42.5 ms (tools/env_sweep.sh)
+  bool pdl = true;
   int f1w_side_smem = 0;
   bool defer_c2r = true;
   bool single_chain = true;

@@ -191,7 +191,7 @@ struct RHeadArgs {
   int64_t w, b;
   float lr;
 };
-inline size_t rhead_smem(int classes) { return (size_t)(2 * 64 * 64 + 64 + classes * 64) * 4; }
+inline size_t rhead_smem(int classes) { return (size_t)(3 * 64 * 64 + 64 + classes * 64) * 4; }
 template <typename T>
 __global__ void __launch_bounds__(256) k_rhead(RHeadArgs a, const Task* __restrict__ tasks) {
   extern __shared__ float rh_smem[];  // rhead_smem(classes) bytes
@@ -201,7 +201,8 @@ __global__ void __launch_bounds__(256) k_rhead(RHeadArgs a, const Task* __restri
   float* gap = rh_smem;           // [rows][64]
   float* dlog = gap + 64 * 64;    // [rows][C] (<= 64 x 64)
   float* lossr = dlog + 64 * 64;  // [rows]
-  float* Ws = lossr + 64;         // the FC weights [C][64] (old W: logits and dgap)
+  float* dgs = lossr + 64;        // dgap [rows][64] (shared copy for the ds3 pass)
+  float* Ws = dgs + 64 * 64;      // the FC weights [C][64] (old W: logits and dgap)
   const T* o3 = (const T*)c->buf[B_R_O3];
   float* W = c->params + a.w;
   float* bias = c->params + a.b;
@@ -259,20 +260,32 @@ __global__ void __launch_bounds__(256) k_rhead(RHeadArgs a, const Task* __restri
     float dg = 0.f;
     for (int cc = 0; cc < C; ++cc) dg = fmaf(dlog[r * C + cc], Ws[cc * 64 + ch], dg);
     dgap[idx] = dg;
+    dgs[idx] = dg;
   }
   __syncthreads();
   // ds3 = dgap / 64 * (o3 > 0)  -> g0
   T* g0 = (T*)c->buf[B_R_G0];
   // (V: elements per 16-byte vector, as above)
-  for (int iv = threadIdx.x; iv < rows * 64 * 64 / V; iv += 256) {
-    const int idx = iv * V, r = idx >> 12, ch = idx & 63;
-    const uint4 ov = reinterpret_cast<const uint4*>(o3)[iv];
-    const T* o = reinterpret_cast<const T*>(&ov);
-    uint4 gv;
-    T* gq = reinterpret_cast<T*>(&gv);
+  const int nv = rows * 64 * 64 / V;
+  for (int b0 = 0; b0 < nv; b0 += 256 * 8) {  // 8 independent 16-byte loads in flight per thread
+    uint4 ov[8];
 #pragma unroll
-    for (int j = 0; j < V; ++j) stv(gq + j, ldv(o + j) > 0.f ? dgap[r * 64 + ch + j] * (1.f / 64.f) : 0.f);
-    reinterpret_cast<uint4*>(g0)[iv] = gv;
+    for (int u = 0; u < 8; ++u) {
+      const int iv = b0 + u * 256 + threadIdx.x;
+      if (iv < nv) ov[u] = reinterpret_cast<const uint4*>(o3)[iv];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int iv = b0 + u * 256 + threadIdx.x;
+      if (iv >= nv) break;
+      const int idx = iv * V, r = idx >> 12, ch = idx & 63;
+      const T* o = reinterpret_cast<const T*>(&ov[u]);
+      uint4 gv;
+      T* gq = reinterpret_cast<T*>(&gv);
+#pragma unroll
+      for (int j = 0; j < V; ++j) stv(gq + j, ldv(o + j) > 0.f ? dgs[r * 64 + ch + j] * (1.f / 64.f) : 0.f);
+      reinterpret_cast<uint4*>(g0)[iv] = gv;
+    }
   }
   for (int idx = threadIdx.x; idx < C * 64; idx += 256) {
     const int cc = idx >> 6, f = idx & 63;
