@@ -78,7 +78,13 @@ struct SlotLayout {
 
 // Split-K partition of the conv wgrad reductions (pixels per split).
 constexpr int kWgradChunkPx = 2048;
-constexpr int kW1QImages = 2;  // width-1 pool-quad conv1 wgrad: images per split (k_conv1_wgrad_q)
+// width-1 pool-quad conv1 wgrad (k_conv1_wgrad_q): images per split, a function of the client's own batch
+// rows only (client results must not depend on the cohort): 2 for the smallest batches (parallelism in
+// the light tail), 4 otherwise (half the per-split epilogues / partials in heavy iterations)
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int w1q_ips(int rows) { return rows >= 16 ? 4 : 2; }
 int cnn_conv1_splits(int rows);
 int cnn_conv2_splits(int rows);
 

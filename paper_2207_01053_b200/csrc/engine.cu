@@ -509,7 +509,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc) {
       case OP_STAGE: return cdiv(rows * 1296, kStageThreads);
       case OP_C1F: return rows * 2;  // persistent pool-quad kernel: 2 tiles of 128 pooled pixels per image
       case OP_C1W:  // width 1: persistent pool-quad kernel, one item per split; else 2 M tiles per split
-        return m.width_q == 4 ? cdiv(rows, kW1QImages) : 2 * cdiv(rows * 1024, kWgradChunkPx);
+        return m.width_q == 4 ? cdiv(rows, w1q_ips(rows)) : 2 * cdiv(rows * 1024, kWgradChunkPx);
       case OP_C1R: return cdiv(76 * m.c1, kReduceBlock);
       case OP_C2F: return rows * 2;  // halo kernel (width >= 1/2) or TmaConv2Fwd: both 128-pixel tiles
       case OP_F1F: return m.f / 128;
@@ -648,7 +648,7 @@ void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, u
   // image geometry (CIFAR 32x32x3: HW 1024, HW2 256, HW4 64; FEMNIST 28x28x1: 784, 196, 49)
   const uint64_t HW = (uint64_t)m.H * m.W, HW2 = HW / 4, HW4 = HW / 16, D = HW * m.C, KC = 25 * (uint64_t)m.C;
   const bool tcq = m.width_q == 4 && e == 2 && m.H == 32;
-  const uint64_t s1 = tcq ? cdiv((int)r, kW1QImages) : cdiv((int)(r * HW), kWgradChunkPx), s2 = cdiv((int)(r * HW2), kWgradChunkPx);
+  const uint64_t s1 = tcq ? cdiv((int)r, w1q_ips((int)r)) : cdiv((int)(r * HW), kWgradChunkPx), s2 = cdiv((int)(r * HW2), kWgradChunkPx);
   uint64_t F = 0, B = 0;
   switch (op) {
     case OP_C1F: F = 2 * r * HW * c1 * KC; B = r * D + 4 * c1 * (KC + 1) + r * HW2 * c1 * (e + 1); break;

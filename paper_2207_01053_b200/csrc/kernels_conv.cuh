@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(kConvThreads, min_blocks<Op>::value)
 //   D[(q,co)][(dy,dx,ci)] = sum_p g1[p][q][co] * xs[2py+dy][2px+dx][ci]     (one GEMM, K = pooled pixels)
 //   dW1[co][ky][kx][ci]   = sum_q D[(q,co)][(ky+qy, kx+qx, ci)]            (fold in the epilogue)
 //   db1[co]               = sum_q D[(q,co)][(2+qy, 2+qx, 3)]               (staged channel 3 = 1 in the image)
-// Work item = (client, split of kW1QImages images);
+// Work item = (client, split of w1q_ips(rows) images);
 // sub-tile = (image, column half) = 128 pooled pixels.  Per K step (16 pooled
 // pixels = 2 pooled rows): 6 MMAs (one per dy), M = 128 (q, co), N = 48 (dx, ci).
 // A = g1 sub-tile by TMA (two 64-row boxes, 128-byte swizzle, MN-major);
@@ -712,7 +712,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         TcTile t;
         t.tk = tasks[ti];
         t.c = recs + t.tk.rec;
-        const int r0 = kW1QImages * (g - __ldg(prefix + ti)), nsub = 2 * min(kW1QImages, t.tk.rows - r0);
+        const int ips = w1q_ips(t.tk.rows), r0 = ips * (g - __ldg(prefix + ti)), nsub = 2 * min(ips, t.tk.rows - r0);
         for (int sub = 0; sub < nsub; ++sub, ++s) {
           const int buf = s % kW1Stages, r = r0 + (sub >> 1), h = sub & 1;
           const uint32_t gb = sb + buf * kW1Stage;
@@ -732,7 +732,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       int ti = ti0, s = 0, i = 0;
       for (int g = g0; g < g1; ++g, ++i) {
         ti = next_task(prefix, ntask, ti, g);
-        const int r0 = kW1QImages * (g - __ldg(prefix + ti)), nsub = 2 * min(kW1QImages, __ldg(&tasks[ti].rows) - r0);
+        const int rows = __ldg(&tasks[ti].rows), ips = w1q_ips(rows);
+        const int r0 = ips * (g - __ldg(prefix + ti)), nsub = 2 * min(ips, rows - r0);
         if (i >= 1) tc::mbar_wait(acc_empty, (i - 1) & 1);
         tc::fence_after();
         for (int sub = 0; sub < nsub; ++sub, ++s) {
@@ -799,7 +800,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     for (int g = g0; g < g1; ++g) {
       rc.advance(prefix, g);
       const ClientRec* c = recs + tasks[rc.ti].rec;
-      const int splits = cdiv(tasks[rc.ti].rows, kW1QImages), item = g - rc.lo;
+      const int splits = cdiv(tasks[rc.ti].rows, w1q_ips(tasks[rc.ti].rows)), item = g - rc.lo;
       int* arrive = reinterpret_cast<int*>(c->stats) + 9;
       int* done = reinterpret_cast<int*>(c->stats) + 11;
       if (threadIdx.x == 0)
