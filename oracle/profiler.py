@@ -101,6 +101,16 @@ def conv_layers(model, width_q=4):
     return []
 
 
+def resnet8_wgrad_splits(hw, b):
+    """Weight-gradient splits of a ResNet-8 conv with an hw-pixel output map for a slot of b rows (DESIGN.md
+    §5): 2-image splits at 32x32; at 16x16 / 8x8 the larger of the 2048-pixel split count and
+    min(4, ceil(b / 2)) (never fewer than ~4 splits for small batches; non-decreasing in b).  Each split
+    then holds ceil(b / splits) whole images."""
+    if hw == 1024:
+        return math.ceil(b / 2)
+    return max(math.ceil(b * hw / WGRAD_CHUNK_PX), min(4, math.ceil(b / 2)))
+
+
 def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
     """[(buffer, bytes)] of one client's arena slot.
 
@@ -110,8 +120,9 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
     and per-row buffers are sized for it.
     wsp = split-K partials of the conv weight gradients: each conv layer's
     reduction over b*Hout*Wout pixels is cut into ceil(b*Hout*Wout / 2048)
-    splits, each holding cout rows of K+1 fp32 partials (the +1 is the bias
-    column); see the branches below for which layers keep partials where.
+    splits (ResNet-8: resnet8_wgrad_splits), each
+    holding cout rows of K+1 fp32 partials (the +1 is the bias column); see the
+    branches below for which layers keep partials where.
     """
     b, e = min(batch, n), elem_bytes  # a batch holds min(B, n) rows (SURVEY §8(c).2 step 3)
     P = n_params(model, width_q, classes)
@@ -150,6 +161,8 @@ def slot_layout(model, width_q, classes, batch, n, epochs, elem_bytes):
         raise ValueError(model)
     convs = conv_layers(model, width_q)
     splits = [math.ceil(b * hw / WGRAD_CHUNK_PX) for hw, _, _ in convs]
+    if model == RESNET8:
+        splits = [resnet8_wgrad_splits(hw, b) for hw, _, _ in convs]
     ceil4 = lambda k: -(-k // 4) * 4  # noqa: E731
     if model == RESNET18:  # one region reused layer by layer (reduced right after each wgrad), pitch K+1
         out.append(("wsp", max(4 * s * co * (K + 1) for s, (_, co, K) in zip(splits, convs))))

@@ -152,8 +152,10 @@ struct RWgrad {
     t.N = N;
     t.m0 = (rem / nt) * BM;
     t.n0 = (rem % nt) * BN;
-    t.kb = t.split * kWgradChunkPx;
-    t.ke = min(t.tk.rows * L.Ho * L.Wo, t.kb + kWgradChunkPx);
+    // ResNet-8 (layer >= 0): splits of r8_ips(layer, B) images (common.h); ResNet-18: 2048 pixels
+    const int chunk = layer >= 0 ? r8_ips(layer, t.c->B) * L.Ho * L.Wo : kWgradChunkPx;
+    t.kb = t.split * chunk;
+    t.ke = min(t.tk.rows * L.Ho * L.Wo, t.kb + chunk);
   }
   __device__ float A(const GemmTile& t, int m, int k) const {
     return ldv((const T*)t.c->buf[dout_buf] + (int64_t)k * L.Cout + m);

@@ -487,7 +487,6 @@ struct RWgHalo {  // stride 1: C -> C
   typedef RHalo<C, false> G;
   static constexpr int H = G::H, W = G::W, RB = G::RB, PITCH = G::PITCH, TPI = G::TILES_PER_IMAGE;
   static constexpr int COUT = C, CIN = C;
-  static constexpr int IPS = kWgradChunkPx / (H * W);                       // images per split
   static constexpr int MH = C == 64 ? 2 : 1;                                 // M = (kx, ci) halves
   static constexpr int NMMA = 3 * COUT;                                      // N = (a, co) of the tap MMAs
   static constexpr int NBLK = 3 * MH;                                        // accumulator blocks (mh, a)
@@ -528,7 +527,7 @@ struct RWgHalo {  // stride 1: C -> C
 // K groups at LBO = one halo row.  B = the dz0 halo with the tap rows as N atoms, as RWgHalo<16>.
 // Partial rows [16][28] (9 x 3 weights + bias).
 struct RWgHalo0 {
-  static constexpr int COUT = 16, CIN = 3, TPI = 8, IPS = kWgradChunkPx / 1024;
+  static constexpr int COUT = 16, CIN = 3, TPI = 8;
   static constexpr int PITCH = RHalo0::PITCH;
   static constexpr int NMMA = 3 * COUT, NBLK = 3;
   static constexpr int RBO = 2 * COUT, DBYTES = 144 * RBO;
@@ -560,7 +559,6 @@ template <int CIN>
 struct RWgHaloS2 {  // stride 2: CIN -> 2 CIN, over the pixel-pair planes of RHaloS2
   typedef RHaloS2<CIN> G;
   static constexpr int COUT = 2 * CIN, RB = G::RB, PP = G::PP, TPI = G::TILES_PER_IMAGE, HO = G::HO, WO = G::WO;
-  static constexpr int IPS = kWgradChunkPx / (HO * WO);
   static constexpr int NBLK = 6;                                             // (ky, odd plane: kx 0, 2), (ky, even: kx 1)
   static constexpr int NMMA = COUT, B_LBO = 16, BIAS_B = 0;                  // (one N atom: the dout tile itself)
   static constexpr int RBO = 2 * COUT, DBYTES = 128 * RBO;
@@ -644,7 +642,7 @@ __global__ void __launch_bounds__(kConvThreads, P::TMEM_COLS <= 256 ? 2 : 1)
         const Task tk = tasks[ti];
         const ClientRec* c = recs + tk.rec;
         const uint8_t* tm = reinterpret_cast<const uint8_t*>(c->tmaps);
-        const int r0 = (g - __ldg(prefix + ti)) * P::IPS, r1 = min(tk.rows, r0 + P::IPS);
+        const int ips = r8_ips(layer, c->B), r0 = (g - __ldg(prefix + ti)) * ips, r1 = min(tk.rows, r0 + ips);
         for (int tile = r0 * P::TPI; tile < r1 * P::TPI; ++tile, ++s) {
           const int buf = s % P::STAGES;
           if (s >= P::STAGES) tc::mbar_wait(empty + 8 * buf, ((s / P::STAGES) - 1) & 1);
@@ -659,8 +657,8 @@ __global__ void __launch_bounds__(kConvThreads, P::TMEM_COLS <= 256 ? 2 : 1)
     int s = 0, i = 0, ti = ti0;
     for (int g = g0; g < g1; ++g, ++i) {
       ti = next_task(prefix, ntask, ti, g);
-      const int rows = __ldg(&tasks[ti].rows);
-      const int r0 = (g - __ldg(prefix + ti)) * P::IPS, r1 = min(rows, r0 + P::IPS);
+      const int rows = __ldg(&tasks[ti].rows), ips = r8_ips(layer, recs[__ldg(&tasks[ti].rec)].B);
+      const int r0 = (g - __ldg(prefix + ti)) * ips, r1 = min(rows, r0 + ips);
       const int a = P::NACC == 2 ? (i & 1) : 0;
       const uint32_t ta = tmem + a * P::COLS;
       if (P::NACC == 2 ? i >= 2 : i >= 1)

@@ -541,17 +541,17 @@ __global__ void __launch_bounds__(kReduceBlock)
   const int N = a.Nw + 1, total = a.M * N;
   const int e0 = ((blockIdx.x - r.chunk_base[l]) * kReduceBlock + threadIdx.x) * 4;
   if (e0 >= total) return;
-  const int splits = cdiv(tk.rows * a.px_per_row, kWgradChunkPx);
-  const float* part = (const float*)c->buf[a.wsp_buf] + (a.layer >= 0 ? r8_wsp_off(a.layer, c->B) : 0) + e0;
+  const int splits = r8_splits(a.layer, tk.rows, c->B);  // (ResNet-8 only: layer >= 0)
+  const float* part = (const float*)c->buf[a.wsp_buf] + r8_wsp_off(a.layer, c->B) + e0;
   float g[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int s0 = 0; s0 < splits; s0 += 4) {  // 4 float4 loads in flight
-    float4 v[4];
+  for (int s0 = 0; s0 < splits; s0 += 8) {  // 8 float4 loads in flight
+    float4 v[8];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 8; ++j)
       v[j] = s0 + j < splits ? __ldcg(reinterpret_cast<const float4*>(part + (int64_t)(s0 + j) * total))
                              : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 8; ++j)
       if (s0 + j < splits) {
         g[0] += v[j].x;
         g[1] += v[j].y;

@@ -210,7 +210,7 @@ SlotLayout slot_layout(const ModelDims& m, int b, int64_t n, int epochs, int e) 
   } else if (m.arch == PROTEA_MODEL_RESNET8) {
     // a region per layer (all kept until the step's merged SGD reduce), regions placed at row pitch
     // ceil4(K+1) (r8_wsp_off); the last layer's rows are written at pitch K+1, so its last row ends the slot
-    wsp = 4ull * ((uint64_t)r8_wsp_off(6, rows) + (uint64_t)splits_for(m.layers[6], rows) * 64 * (9 * 64 + 1));
+    wsp = 4ull * ((uint64_t)r8_wsp_off(6, rows) + (uint64_t)r8_split_cap(6, rows) * 64 * (9 * 64 + 1));
   } else if (m.arch == PROTEA_MODEL_CNN && e == 2 && m.width_q == 4 && m.H == 32) {
     // width 1, bf16: conv1's partials live in dz2 (k_conv1_wgrad_q); conv2 writes partials (row pitch
     // ceil4(K+1) = 804) only when a client's rows need more than one split, else it updates from TMEM
