@@ -15,6 +15,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges visible to nsys / ncu --nvtx when a tool is attached
 
 #include <array>
 #include <tuple>
@@ -42,6 +43,13 @@
 #include "kernels_resnet18.cuh"
 
 namespace protea {
+// NVTX range for the enclosing scope (round phases and lock-step iterations; SURVEY §5 tracing)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 static std::mutex g_err_mu;
 static std::string g_err;
@@ -2095,7 +2103,13 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const floa
     for (uint64_t t = c.admit; t < c.release; ++t) {
       iter_rows[t] += micro_rows(c, t);
     }
+  NvtxRange nv_iters("protea: lock-step iterations");
   for (uint64_t t = 0; t < T; ++t) {
+    char nv_name[48];
+    std::snprintf(nv_name, sizeof(nv_name), "iteration %llu (%lld rows)", (unsigned long long)t,
+                  (long long)iter_rows[t]);
+    nvtxRangePushA(nv_name);
+    struct NvPop { ~NvPop() { nvtxRangePop(); } } nv_pop;
     // (several groups already overlap each other: no side-stream deferral then)
     ctx->overlap_now = tc_mode && !ctx->serialize && V == 1 && iter_rows[t] <= ctx->overlap_rows;
     ctx->rows_now = iter_rows[t];
@@ -2306,7 +2320,12 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
       }
     return PROTEA_OK;
   };
-  const protea_status vst = validate();
+  NvtxRange nv_round("protea_run_round");
+  protea_status vst;
+  {
+    NvtxRange nv("protea: validate");
+    vst = validate();
+  }
   if (ctx->comm) {
     // plan agreement + validation verdict: NCCL max over ranks of (h, ~h, failed) equals
     // (h, ~h, 0) iff every rank validated and all ranks hold the same client list and plan
@@ -2356,8 +2375,12 @@ protea_status protea_run_round(protea_ctx* ctx, const protea_round_opts* opts, c
   ExecExtras xx;
   xx.observe = opts->observe_hwm != 0;
   for (uint32_t i = 0; i < opts->n_trace; ++i) xx.trace[opts->trace_ids[i]] = (uint8_t*)opts->trace_bufs[i];
-  protea_status st =
-      execute(ctx, all, wg, ctx->acc.p, opts->lr, opts->seed, opts->round, opts->shuffle, &iters, loss_dev, &xx);
+  protea_status st;
+  {
+    NvtxRange nv("protea: execute (A2 local SGD, A3 profiles, A5 FedAvg accumulation)");
+    st = execute(ctx, all, wg, ctx->acc.p, opts->lr, opts->seed, opts->round, opts->shuffle, &iters, loss_dev, &xx);
+  }
+  NvtxRange nv_x("protea: exchange + finalise (K7)");
   if (ctx->comm && !opts->partial_only) {
     // every rank reaches the exchange; one that failed inside execute() says so first (NCCL max of a flag)
     const uint64_t f0 = st == PROTEA_OK ? 0 : 1;
