@@ -120,29 +120,28 @@ inline uint64_t w1q_bytes(int C1) { return 36ull * 4 * C1 * 8 * 2; }
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 // ResNet-8 weight-gradient splits (every wgrad kernel, the merged SGD reduce and the slot layout follow
-// this): layer l's reduction over a batch's output pixels is cut into splits of r8_ips(l, B) whole
-// images, B = the slot's batch capacity.  32x32 layers (0-2): 2 images (2048 pixels).  16x16 / 8x8 layers
-// (3-6): S(B) = max(ceil(B hw / 2048), min(4, ceil(B / 2))) splits of ceil(B / S) images: at most 2048
-// pixels, and at least ~4 splits so the light lock-step tail's few small-batch clients still spread
-// over many CTAs.  S(B) never decreases with B (the footprint stays monotone in the batch, reading R13)
-// and depends on the client's own B only (no cohort dependence).
+// this): layer l's reduction over a batch of `rows` images is cut into r8_split_cap(l, rows) splits of
+// whole images.  32x32 layers (0-2): ceil(rows / 2) splits of 2 images (2048 pixels).  16x16 / 8x8
+// layers (3-6): S = max(ceil(rows hw / 2048), min(4, ceil(rows / 2))) splits, split s holding images
+// [s rows / S, (s + 1) rows / S): at most 2048 pixels, and at least ~4 splits so the light lock-step
+// tail's few small-batch clients still spread over many CTAs.  S never decreases with rows, so a slot
+// sized for its capacity B (r8_wsp_off) holds every batch's partials, and a full batch touches all of
+// them (the observed high-water mark equals the layout, reading R2).  No cohort dependence.
 #if defined(__CUDACC__)
 __host__ __device__
 #endif
-inline int r8_split_cap(int layer, int B) {
-  if (layer < 3) return (B + 1) / 2;
-  const int hw = layer < 5 ? 256 : 64, full = (B * hw + kWgradChunkPx - 1) / kWgradChunkPx;
-  const int half = (B + 1) / 2, floor4 = half < 4 ? half : 4;
+inline int r8_split_cap(int layer, int rows) {
+  if (layer < 3) return (rows + 1) / 2;
+  const int hw = layer < 5 ? 256 : 64, full = (rows * hw + kWgradChunkPx - 1) / kWgradChunkPx;
+  const int half = (rows + 1) / 2, floor4 = half < 4 ? half : 4;
   return full > floor4 ? full : floor4;
 }
 #if defined(__CUDACC__)
 __host__ __device__
 #endif
-inline int r8_ips(int layer, int B) { return layer < 3 ? 2 : (B + r8_split_cap(layer, B) - 1) / r8_split_cap(layer, B); }
-#if defined(__CUDACC__)
-__host__ __device__
-#endif
-inline int r8_splits(int layer, int rows, int B) { return (rows + r8_ips(layer, B) - 1) / r8_ips(layer, B); }
+inline int r8_split_image(int layer, int rows, int s) {  // first image of split s (s = S: rows)
+  return layer < 3 ? (2 * s < rows ? 2 * s : rows) : (int)((int64_t)s * rows / r8_split_cap(layer, rows));
+}
 
 // ResNet-8 weight-gradient partials: one region per conv layer (all seven layers' partials are kept
 // until the step's single merged SGD reduce), region l = [r8_split_cap(l, B)][cout_l][9 cin_l + 1] fp32

@@ -463,7 +463,7 @@ void join_group(protea_ctx* ctx, int g) {
 const Layer& gconv(const ModelDims& m, int l) { return m.layers[2 * l]; }  // ResNet-18 conv layer l (0..16)
 const Layer& gnorm_of(const ModelDims& m, int l) { return m.layers[2 * l + 1]; }
 
-int tiles(const ModelDims& m, int op, int rows, bool tc, int cap = 0) {  // cap: the slot's batch capacity
+int tiles(const ModelDims& m, int op, int rows, bool tc) {
   if (op >= GI_F) {  // ResNet-18: SIMT kernels
     if (op == GI_HEAD) return 1;
     if (op < GI_N) {
@@ -505,7 +505,7 @@ int tiles(const ModelDims& m, int op, int rows, bool tc, int cap = 0) {  // cap:
     }
     if (op < RI_R0) {
       const Layer& l = m.layers[op - RI_W0];
-      const int sp = r8_splits(op - RI_W0, rows, cap > 0 ? cap : rows);  // (common.h: per-batch split rule)
+      const int sp = r8_split_cap(op - RI_W0, rows);  // (common.h: whole-image splits)
       if (tc && (r8_halo_c(l, R8H_WGRAD) || r8_halo_s2(l, R8H_WGRAD) || r8_halo0(l, R8H_WGRAD)))
         return sp;  // halo wgrad: one item per split
       if (tc) return sp * cdiv(9 * (l.cin < 8 ? 8 : l.cin) + 1, 128);
@@ -644,10 +644,10 @@ void op_work(const ModelDims& m, int op, uint64_t r, uint64_t e, uint64_t* fl, u
       const Layer& l = m.layers[op - RI_W0];
       F = 2 * r * l.hout * l.wout * l.cout * 9 * l.cin;
       B = r * (uint64_t)l.hin * l.win * l.cin * e + r * (uint64_t)l.hout * l.wout * l.cout * e +
-          4 * (uint64_t)r8_splits(op - RI_W0, (int)r, (int)r) * l.cout * (9 * l.cin + 1);
+          4 * (uint64_t)r8_split_cap(op - RI_W0, (int)r) * l.cout * (9 * l.cin + 1);
     } else {
       const Layer& l = m.layers[op - RI_R0];
-      B = 4 * (uint64_t)r8_splits(op - RI_R0, (int)r, (int)r) * l.cout * (9 * l.cin + 1) +
+      B = 4 * (uint64_t)r8_split_cap(op - RI_R0, (int)r) * l.cout * (9 * l.cin + 1) +
           8 * (uint64_t)l.cout * (9 * l.cin + 1);
     }
     *fl = F;
@@ -2011,7 +2011,7 @@ protea_status execute(protea_ctx* ctx, std::vector<RunClient>& rc_in, const floa
           int acc_t = 0;
           for (size_t i = 0; i < act.size(); ++i) {
             tab.push_back(acc_t);
-            acc_t += tiles(m, op, rows[i], tc_mode, act[i]->cap) * (op == OP_C2W ? L.c2w_groups : 1);
+            acc_t += tiles(m, op, rows[i], tc_mode) * (op == OP_C2W ? L.c2w_groups : 1);
             uint64_t fl, by;
             op_work(m, op, (uint64_t)rows[i], (uint64_t)e, &fl, &by);
             ctx->op_flops[op_class(op)] += fl;

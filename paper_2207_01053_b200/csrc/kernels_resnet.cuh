@@ -152,10 +152,13 @@ struct RWgrad {
     t.N = N;
     t.m0 = (rem / nt) * BM;
     t.n0 = (rem % nt) * BN;
-    // ResNet-8 (layer >= 0): splits of r8_ips(layer, B) images (common.h); ResNet-18: 2048 pixels
-    const int chunk = layer >= 0 ? r8_ips(layer, t.c->B) * L.Ho * L.Wo : kWgradChunkPx;
-    t.kb = t.split * chunk;
-    t.ke = min(t.tk.rows * L.Ho * L.Wo, t.kb + chunk);
+    if (layer >= 0) {  // ResNet-8: split = whole images [r8_split_image(s), r8_split_image(s + 1)) (common.h)
+      t.kb = r8_split_image(layer, t.tk.rows, t.split) * L.Ho * L.Wo;
+      t.ke = r8_split_image(layer, t.tk.rows, t.split + 1) * L.Ho * L.Wo;
+    } else {  // ResNet-18: 2048-pixel splits
+      t.kb = t.split * kWgradChunkPx;
+      t.ke = min(t.tk.rows * L.Ho * L.Wo, t.kb + kWgradChunkPx);
+    }
   }
   __device__ float A(const GemmTile& t, int m, int k) const {
     return ldv((const T*)t.c->buf[dout_buf] + (int64_t)k * L.Cout + m);

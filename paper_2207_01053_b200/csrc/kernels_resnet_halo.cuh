@@ -642,7 +642,8 @@ __global__ void __launch_bounds__(kConvThreads, P::TMEM_COLS <= 256 ? 2 : 1)
         const Task tk = tasks[ti];
         const ClientRec* c = recs + tk.rec;
         const uint8_t* tm = reinterpret_cast<const uint8_t*>(c->tmaps);
-        const int ips = r8_ips(layer, c->B), r0 = (g - __ldg(prefix + ti)) * ips, r1 = min(tk.rows, r0 + ips);
+        const int sp = g - __ldg(prefix + ti);
+        const int r0 = r8_split_image(layer, tk.rows, sp), r1 = r8_split_image(layer, tk.rows, sp + 1);
         for (int tile = r0 * P::TPI; tile < r1 * P::TPI; ++tile, ++s) {
           const int buf = s % P::STAGES;
           if (s >= P::STAGES) tc::mbar_wait(empty + 8 * buf, ((s / P::STAGES) - 1) & 1);
@@ -657,8 +658,8 @@ __global__ void __launch_bounds__(kConvThreads, P::TMEM_COLS <= 256 ? 2 : 1)
     int s = 0, i = 0, ti = ti0;
     for (int g = g0; g < g1; ++g, ++i) {
       ti = next_task(prefix, ntask, ti, g);
-      const int rows = __ldg(&tasks[ti].rows), ips = r8_ips(layer, recs[__ldg(&tasks[ti].rec)].B);
-      const int r0 = (g - __ldg(prefix + ti)) * ips, r1 = min(rows, r0 + ips);
+      const int rows = __ldg(&tasks[ti].rows), sp = g - __ldg(prefix + ti);
+      const int r0 = r8_split_image(layer, rows, sp), r1 = r8_split_image(layer, rows, sp + 1);
       const int a = P::NACC == 2 ? (i & 1) : 0;
       const uint32_t ta = tmem + a * P::COLS;
       if (P::NACC == 2 ? i >= 2 : i >= 1)

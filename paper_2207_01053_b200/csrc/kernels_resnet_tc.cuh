@@ -340,12 +340,13 @@ struct RTcWgrad {
   int cin_real;  // channels of the weight layout (conv0: 3 real of the 8 staged; else Cin)
   int layer;     // partial region of this layer (r8_wsp_off)
   __device__ int mtiles() const { return (9 * L.Cin + 1 + 127) / 128; }
-  __device__ int chunk(const TcTile& t) const { return r8_ips(layer, t.c->B) * L.Ho * L.Wo; }  // (common.h)
+  __device__ int p0(const TcTile& t) const { return r8_split_image(layer, t.tk.rows, t.n0) * L.Ho * L.Wo; }  // (common.h)
+  __device__ int p1(const TcTile& t) const { return r8_split_image(layer, t.tk.rows, t.n0 + 1) * L.Ho * L.Wo; }
   __device__ void setup(TcTile& t, int local) const {
-    const int mt = mtiles(), split = local / mt, ck = chunk(t), px = t.tk.rows * L.Ho * L.Wo - split * ck;
+    const int mt = mtiles(), split = local / mt;
     t.m0 = (local - split * mt) * 128;
-    t.n0 = split;  // the split index (K = this split's pixels)
-    t.nk = ((px < ck ? px : ck) + 63) / 64;
+    t.n0 = split;  // the split index (K = this split's pixels [p0, p1))
+    t.nk = (p1(t) - p0(t) + 63) / 64;
     t.n_mma = L.Cout;
   }
   __device__ const void* any(const TcTile& t) const { return t.c->params; }
@@ -356,11 +357,11 @@ struct RTcWgrad {
     const int tap = mg >> L.lci, ky = tap / 3, kx = tap - 3 * ky;
     return PA{i, ky - 1, kx - 1, mg & (L.Cin - 1), 0};
   }
-  __device__ KS a_ks(const TcTile& t, int j, int kb) const { return KS{t.n0 * chunk(t) + kb * 64}; }
+  __device__ KS a_ks(const TcTile& t, int j, int kb) const { return KS{p0(t) + kb * 64}; }
   __device__ const void* a_src(const TcTile& t, const PA& s, const KS& k) const {
     if (s.kind) return s.kind == 1 ? (const void*)kOneChunk : nullptr;
     const int hw = L.Ho * L.Wo, p = k.p0 + s.i;
-    if (p >= t.tk.rows * hw) return nullptr;
+    if (p >= p1(t)) return nullptr;
     const int r = p >> L.lhwo, rem = p & (hw - 1), yo = rem >> L.lwo, xo = rem & (L.Wo - 1);
     const int y = yo * L.s + s.dy, x = xo * L.s + s.dx;
     if ((unsigned)y >= (unsigned)L.H || (unsigned)x >= (unsigned)L.W) return nullptr;
@@ -368,8 +369,8 @@ struct RTcWgrad {
   }
   __device__ PB b_pre(const TcTile& t, int i, int j) const { return PB{i, 8 * j}; }
   __device__ const void* b_src(const TcTile& t, const PB& s, int kb) const {
-    const int p = t.n0 * chunk(t) + kb * 64 + s.i;
-    if (p >= t.tk.rows * L.Ho * L.Wo || s.n0 >= L.Cout) return nullptr;
+    const int p = p0(t) + kb * 64 + s.i;
+    if (p >= p1(t) || s.n0 >= L.Cout) return nullptr;
     return (const bf16*)t.c->buf[dout_buf] + (int64_t)p * L.Cout + s.n0;
   }
   __device__ void epilogue(const TcTile& t, int row, int c0, const float (&v)[16]) const {

@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kReduceBlock)
   const int N = a.Nw + 1, total = a.M * N;
   const int e0 = ((blockIdx.x - r.chunk_base[l]) * kReduceBlock + threadIdx.x) * 4;
   if (e0 >= total) return;
-  const int splits = r8_splits(a.layer, tk.rows, c->B);  // (ResNet-8 only: layer >= 0)
+  const int splits = r8_split_cap(a.layer, tk.rows);  // (ResNet-8 only: layer >= 0)
   const float* part = (const float*)c->buf[a.wsp_buf] + r8_wsp_off(a.layer, c->B) + e0;
   float g[4] = {0.f, 0.f, 0.f, 0.f};
   for (int s0 = 0; s0 < splits; s0 += 8) {  // 8 float4 loads in flight
