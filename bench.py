@@ -356,6 +356,9 @@ def main():
         dom_n += st["op_timed_launches"][dominant]
         if world == 1:  # A3 -> next A4: the latest in-run profile replaces the previous one (reading R7)
             profiles = meas  # (N > 1: each rank observes only its own clients; the plan keeps the footprints)
+            # a client whose every batch is partial (n < B) may leave the tail of its last buffers untouched, so
+            # its observed mark can sit below the slot layout run_round validates against: plan at least that
+            profiles["peak_bytes"] = np.maximum(profiles["peak_bytes"], foot["peak_bytes"])
     barrier()
     host_s = time.perf_counter() - host_t0
     clk = clocks.stop() if clocks else None
