@@ -702,31 +702,31 @@ struct TcFc1Wgrad {  // M = K1 (input features), N = F (outputs), K = rows; W <-
     load(0);
     tc::mbar_wait(done, 0);
     tc::fence_after();
+    // the staging buffer holds each weight as its fp32 value (hi/lo halves interleaved with byte permutes):
+    // the update pass is one conflict-free 4-byte load and store per weight instead of two 2-byte of each
     for (int cb = 0, buf = 0; cb < t.n_mma; cb += 32, buf ^= 1) {
-      uint16_t* sh = reinterpret_cast<uint16_t*>(smem) + buf * 8192;  // [32 columns][128 rows] x {hi, lo}
-      uint16_t* sl = sh + 4096;
+      uint32_t* sf = reinterpret_cast<uint32_t*>(smem) + buf * 4096;  // [32 columns][128 rows] fp32
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        *reinterpret_cast<uint2*>(sh + (4 * warp + i) * 128 + 4 * lane) = h[i];
-        *reinterpret_cast<uint2*>(sl + (4 * warp + i) * 128 + 4 * lane) = l[i];
-      }
+      for (int i = 0; i < 4; ++i)
+        *reinterpret_cast<uint4*>(sf + (4 * warp + i) * 128 + 4 * lane) =
+            make_uint4(__byte_perm(l[i].x, h[i].x, 0x5410), __byte_perm(l[i].x, h[i].x, 0x7632),
+                       __byte_perm(l[i].y, h[i].y, 0x5410), __byte_perm(l[i].y, h[i].y, 0x7632));
       if (cb + 32 < t.n_mma) load(cb + 32);
       asm volatile("bar.sync 1, 256;" ::: "memory");
       float v[16];
       tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(cb + cl), v);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const int idx = (cl + j) * 128 + row;
-        const uint32_t u = __float_as_uint(split_join(sh[idx], sl[idx]) - lr * v[j]);
-        sh[idx] = (uint16_t)(u >> 16);
-        sl[idx] = (uint16_t)(u & 0xFFFFu);
+        float* w = reinterpret_cast<float*>(sf) + (cl + j) * 128 + row;
+        *w = *w - lr * v[j];  // (= split_join(hi, lo) - lr * g, stored back as its two halves below)
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int64_t o = (int64_t)(t.n0 + cb + 4 * warp + i) * 2 * W::K1 + 4 * lane;
-        *reinterpret_cast<uint2*>(Hp + o) = *reinterpret_cast<const uint2*>(sh + (4 * warp + i) * 128 + 4 * lane);
-        *reinterpret_cast<uint2*>(Lp + o) = *reinterpret_cast<const uint2*>(sl + (4 * warp + i) * 128 + 4 * lane);
+        const uint4 q = *reinterpret_cast<const uint4*>(sf + (4 * warp + i) * 128 + 4 * lane);
+        *reinterpret_cast<uint2*>(Hp + o) = make_uint2(__byte_perm(q.x, q.y, 0x7632), __byte_perm(q.z, q.w, 0x7632));
+        *reinterpret_cast<uint2*>(Lp + o) = make_uint2(__byte_perm(q.x, q.y, 0x5410), __byte_perm(q.z, q.w, 0x5410));
       }
     }
   }
