@@ -874,6 +874,16 @@ OpT tma_op_lr(const ClientRec* recs, const CnnDims& d, float lr) {
   return op;
 }
 
+// fc1 wgrad op: operands by TMA (TmaFc1Wgrad)
+template <int WQ>
+TmaFc1Wgrad<WQ> f1w_op(const ClientRec* recs, const CnnDims& d, float lr) {
+  TmaFc1Wgrad<WQ> op;
+  op.recs = recs;
+  op.d = d;
+  op.lr = lr;
+  return op;
+}
+
 // bf16 mode, CNN: conv1, conv2 and fc1 (fwd / dgrad / wgrad) on tcgen05; the head on SIMT
 template <int WQ>
 void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, const ClientRec* drecs,
@@ -910,12 +920,12 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
     cudaStream_t main = ctx->cur;
     ctx->cur = ctx->side;
     // deferred: fewer resident CTAs (PROTEA_F1W_SIDE_SMEM) spread its HBM stream over the chain it overlaps
-    launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab, ctx->f1w_side_smem);
+    launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, f1w_op<WQ>(drecs, d, lr), L, OP_F1W, dtab, ctx->f1w_side_smem);
     cudaEventRecord(ctx->gjoin[L.group], ctx->side);
     ctx->gpending[L.group] = 1;
     ctx->cur = main;
   } else {
-    launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, TcFc1Wgrad<WQ>{drecs, d, lr}, L, OP_F1W, dtab);
+    launch_gemm_tc<TC_F1W_BN, TC_F1W_STAGES>(ctx, f1w_op<WQ>(drecs, d, lr), L, OP_F1W, dtab);
   }
   if constexpr (WQ == 4)
     launch_conv_persistent<HaloConv2Q<true>>(ctx, drecs, d, L, OP_C2D, dtab);

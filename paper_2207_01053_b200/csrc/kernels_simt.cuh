@@ -928,6 +928,7 @@ __global__ void __launch_bounds__(kHeadCnnThreads)
       stv(dh + (int64_t)r * F + f, s);
       gb += s;
     }
+    for (int r = rows; r < c->B; ++r) stv(dh + (int64_t)r * F + f, 0.f);  // (fc1 wgrad's TMA reads the slot's B rows)
     c->params[a.b_prev + f] -= a.lr * gb;
     for (int c0 = 0; c0 < C; c0 += 16) {
       float g[16];

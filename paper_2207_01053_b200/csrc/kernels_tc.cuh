@@ -115,6 +115,15 @@ struct min_blocks {  // resident CTAs per SM the op is compiled for (register ca
 };
 
 template <class Op>
+struct has_ksteps {  // the op's single K block holds fewer than 4 MMA K steps (Op::KSTEPS + op.ksteps(t))
+  template <class U>
+  static constexpr bool f(decltype(U::KSTEPS)*) { return U::KSTEPS; }
+  template <class U>
+  static constexpr bool f(...) { return false; }
+  static constexpr bool value = f<Op>(nullptr);
+};
+
+template <class Op>
 struct halo_stages {  // depth of k_conv_persistent's halo ring (Op::HSTAGES), default 2
   template <class U>
   static constexpr int f(decltype(U::HSTAGES)*) { return U::HSTAGES; }
@@ -256,9 +265,11 @@ __global__ void __launch_bounds__(kTcThreads, min_blocks<Op>::value)
         tc::mbar_wait(bar0 + 8 * s, (kb / STAGES) & 1);
         tc::fence_after();
         const uint64_t so = (uint64_t)(s * (STAGE >> 4));
+        int nks = 4;
+        if constexpr (has_ksteps<Op>::value) nks = op.ksteps(t);
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)
-          tc::mma_bf16_w(tmem, da0 + so + ks * dak, db0 + so + ks * dbk, idesc, (kb | ks) != 0);
+          if (ks < nks) tc::mma_bf16_w(tmem, da0 + so + ks * dak, db0 + so + ks * dbk, idesc, (kb | ks) != 0);
         tc::commit_w(bar0 + 8 * (STAGES + s));
       }
       tc::commit_w(done);
@@ -938,6 +949,31 @@ struct TmaFc1Dgrad : TcFc1Dgrad<WQ> {
   }
   __device__ uint64_t b_desc(const TcTile& t, uint32_t base, int ks) const {
     return tc::sdesc_sw128(base + 32 * ks, 16, 1024);
+  }
+};
+
+template <int WQ>
+struct TmaFc1Wgrad : TcFc1Wgrad<WQ> {
+  // Operands by TMA (no cp.async: its 16-byte chunk writes into the MN-major operand layout measured up to
+  // 28-way shared-memory bank conflicts, 43 % of the kernel's shared wavefronts): A = a2 [R rows][64 k1] x 2,
+  // B = dh [R rows][64 f] x 2 (128-byte swizzle, MN-major: K = rows at 128 B, 8-row groups 1 KB apart, the
+  // two 64-wide atoms 8 KB apart); R = the slot's rows rounded to 16 (rows past the slot are the TMA's zero
+  // fill; rows of a ragged batch past tk.rows are zero in dh: k_head_cnn).  K steps = R / 16.
+  static constexpr bool TMA = true, KSTEPS = true;
+  __device__ int ksteps(const TcTile& t) const { return ((t.c->B + 15) & ~15) >> 4; }
+  __device__ void init_stage(const TcTile&, uint8_t*, uint8_t*) const {}
+  __device__ uint32_t tx_bytes(const TcTile& t, int) const { return 512u * (uint32_t)((t.c->B + 15) & ~15); }
+  __device__ void tma_issue(const TcTile& t, int, uint32_t a, uint32_t b, uint32_t mbar) const {
+    tc::tma_load_2d(a, tmap_of(t, TM_A2), mbar, t.m0, 0);
+    tc::tma_load_2d(a + 8192, tmap_of(t, TM_A2), mbar, t.m0 + 64, 0);
+    tc::tma_load_2d(b, tmap_of(t, TM_DH), mbar, t.n0, 0);
+    tc::tma_load_2d(b + 8192, tmap_of(t, TM_DH), mbar, t.n0 + 64, 0);
+  }
+  __device__ uint64_t a_desc(const TcTile&, uint32_t base, int ks) const {
+    return tc::sdesc_sw128(base + 2048 * ks, 8192, 1024);
+  }
+  __device__ uint64_t b_desc(const TcTile&, uint32_t base, int ks) const {
+    return tc::sdesc_sw128(base + 2048 * ks, 8192, 1024);
   }
 };
 
