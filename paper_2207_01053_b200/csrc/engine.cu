@@ -892,7 +892,7 @@ void launch_step_tc_w(protea_ctx* ctx, const ModelDims& m, const Launch& L, cons
   const Task* tasks = reinterpret_cast<const Task*>(dtab + L.task_off);
   const CnnDims d = cnn_dims(m);
   int ev = op_begin(ctx, OP_STAGE, OP_STAGE);
-  launch_k(ctx, k_stage_x, dim3(cdiv(L.max_rows * 1296, kStageThreads), L.ntask), kStageThreads, 0, drecs, tasks);
+  launch_k(ctx, k_stage_x, dim3(cdiv(L.max_rows * 1296, kStageThreads * kStagePx), L.ntask), kStageThreads, 0, drecs, tasks);
   op_end(ctx, ev);
   launch_conv_persistent<QuadConv1<WQ>>(ctx, drecs, d, L, OP_C1F, dtab);
   join_group(ctx, L.group);  // the previous step's deferred fc1 wgrad still reads a2

@@ -989,33 +989,49 @@ struct TmaFc1Wgrad : TcFc1Wgrad<WQ> {
 // padded coordinates (Y, X) = (y + 2, x + 2).  Channel 3 is 1.0 inside the image
 // (0 in the border): the conv1 wgrad reads the bias gradient from it.
 // --------------------------------------------------------------------------
-constexpr int kStageThreads = 256;
+constexpr int kStageThreads = 256, kStagePx = 4;
 __global__ void __launch_bounds__(kStageThreads)
     k_stage_x(const ClientRec* __restrict__ recs, const Task* __restrict__ tasks) {  // grid (blocks, task)
+  // kStagePx staged pixels per thread (e = block base + k * 256 + thread): the task / record / permutation
+  // loads are paid once per thread and all pixel loads are in flight together
   __shared__ float lut[256];  // px01(u): the same fp32 values as the division, without one per channel
   lut[threadIdx.x] = px01((uint8_t)threadIdx.x);
   pdl_wait();  // xs is still read by the preceding conv1 wgrad
   pdl_trigger();
   const Task tk = tasks[blockIdx.y];
-  if ((int)blockIdx.x * kStageThreads >= tk.rows * 1296) return;
+  const int n_e = tk.rows * 1296, e0 = blockIdx.x * kStageThreads * kStagePx + threadIdx.x;
+  if ((int)blockIdx.x * kStageThreads * kStagePx >= n_e) return;
   const ClientRec* c = recs + tk.rec;
-  const int e = blockIdx.x * kStageThreads + threadIdx.x;  // staged pixel, storage order
-  const int r = e / 1296, rem = e - r * 1296, Y = rem / 36, rx = rem - Y * 36, X = 2 * (rx % 18) + rx / 18;
-  const int y = Y - 2, x = X - 2;
-  const bool in = e < tk.rows * 1296 && (unsigned)y < 32u && (unsigned)x < 32u;
-  const uint8_t* px = in ? c->x + (int64_t)__ldg(c->perm + tk.base + r) * 3072 + (y * 32 + x) * 3 : nullptr;
-  uint32_t u0 = 0, u1 = 0, u2 = 0;
-  if (in) u0 = __ldg(px), u1 = __ldg(px + 1), u2 = __ldg(px + 2);
-  __syncthreads();  // lut
-  if (e >= tk.rows * 1296) return;
-  uint4 out = make_uint4(0, 0, 0, 0);
-  if (in) {
-    const __nv_bfloat162 v01 = __floats2bfloat162_rn(lut[u0], lut[u1]);
-    const __nv_bfloat162 v23 = __floats2bfloat162_rn(lut[u2], 1.f);
-    out.x = *reinterpret_cast<const uint32_t*>(&v01);
-    out.y = *reinterpret_cast<const uint32_t*>(&v23);
+  const uint8_t* xbase = c->x;
+  uint4* xs = reinterpret_cast<uint4*>(c->buf[B_XS]);
+  uint32_t u[kStagePx][3];
+  bool in[kStagePx];
+#pragma unroll
+  for (int k = 0; k < kStagePx; ++k) {
+    const int e = e0 + k * kStageThreads;
+    const int r = e / 1296, rem = e - r * 1296, Y = rem / 36, rx = rem - Y * 36, X = 2 * (rx % 18) + rx / 18;
+    const int y = Y - 2, x = X - 2;
+    in[k] = e < n_e && (unsigned)y < 32u && (unsigned)x < 32u;
+    u[k][0] = u[k][1] = u[k][2] = 0;
+    if (in[k]) {
+      const uint8_t* px = xbase + (int64_t)__ldg(c->perm + tk.base + r) * 3072 + (y * 32 + x) * 3;
+      u[k][0] = __ldg(px), u[k][1] = __ldg(px + 1), u[k][2] = __ldg(px + 2);
+    }
   }
-  reinterpret_cast<uint4*>(c->buf[B_XS])[e] = out;
+  __syncthreads();  // lut
+#pragma unroll
+  for (int k = 0; k < kStagePx; ++k) {
+    const int e = e0 + k * kStageThreads;
+    if (e >= n_e) break;
+    uint4 out = make_uint4(0, 0, 0, 0);
+    if (in[k]) {
+      const __nv_bfloat162 v01 = __floats2bfloat162_rn(lut[u[k][0]], lut[u[k][1]]);
+      const __nv_bfloat162 v23 = __floats2bfloat162_rn(lut[u[k][2]], 1.f);
+      out.x = *reinterpret_cast<const uint32_t*>(&v01);
+      out.y = *reinterpret_cast<const uint32_t*>(&v23);
+    }
+    xs[e] = out;
+  }
 }
 __device__ __forceinline__ int64_t xs_index(int r, int Y, int X) {  // 8-element chunk index of padded (Y, X)
   return ((int64_t)(r * 36 + Y) * 2 + (X & 1)) * 18 + (X >> 1);
