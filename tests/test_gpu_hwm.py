@@ -106,3 +106,32 @@ def test_probe_guard_detects_nothing_and_oom_when_arena_small(torch):
         sim.profile(clients)
     assert e.value.name == "OOM"
     sim.close()
+
+
+def test_resnet8_small_shard_observed_hwm_equals_layout(torch):
+    """ResNet-8 clients whose shard is smaller than their batch (b = n < B: every batch is the whole shard)
+    and ragged ones: the whole-image weight-gradient splits (common.h r8_split_cap, a balanced partition)
+    touch every reserved partial, so the OBSERVED mark equals the layout exactly -- a plan from observed
+    profiles must never undersize the slot run_round validates against (bench.py feeds them back)."""
+    import dataclasses
+    wl = synth.build_workload(5, n_clients=300, k=6, samples=70)
+    shapes = [(5, 16), (9, 32), (13, 16), (7, 64), (21, 32), (45, 16)]  # (n, B)
+    tmpl = synth.class_templates(wl.shape, wl.classes, wl.seed)
+    wl.clients = [dataclasses.replace(c, n=n, batch=b, epochs=1) for c, (n, b) in zip(wl.clients, shapes)]
+    wl.shards = {c.id: synth.make_shard(tmpl, c.n, c.id, wl.seed) for c in wl.clients}
+    sim, clients = _sim(wl, 1)
+    prof = sim.profile(clients)
+    plan, _ = sim.plan(prof, margin_permille=1100)
+    g = torch.tensor(synth.init_weights(wl.model), device="cuda")
+    _, (st, meas) = sim.run_round(clients, plan, g, lr=0.05, seed=wl.seed, measured=True, observe_hwm=True)
+    bad = []
+    for p, c in zip(meas, wl.clients):
+        want = opf.hwm_bytes(c.model, c.width_q, c.classes, c.batch, c.n, c.epochs, 2)
+        if int(p["peak_bytes"]) != want:
+            bad.append((c.id, c.n, c.batch, int(p["peak_bytes"]), want))
+    for p, c in zip(prof, wl.clients):  # the one-step probe observes the same marks
+        want = opf.hwm_bytes(c.model, c.width_q, c.classes, c.batch, c.n, c.epochs, 2)
+        if int(p["peak_bytes"]) != want:
+            bad.append(("probe", c.id, c.n, c.batch, int(p["peak_bytes"]), want))
+    sim.close()
+    assert not bad, bad
