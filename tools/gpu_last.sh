@@ -1,6 +1,12 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -m gpu -q --timeout 300 -k "hwm or tc or teacher" > gpurun_out/last_tests.log 2>&1; echo "tests rc=$?"
+timeout 1500 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/last_tests.log 2>&1; echo "tests rc=$?"
 tail -n 2 gpurun_out/last_tests.log; grep -E "^FAILED|Error" gpurun_out/last_tests.log | head -5
-timeout 300 python tools/tail_probe.py 2>&1 | cut -c1-420
-timeout 300 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo "bench2 rc=$?"
-python -c "import json; d=json.loads(open('gpurun_out/bench_c2.json').read().strip().splitlines()[-1]); r=d['roofline']; print(d['value'], d['ms_per_step'], r['achieved'], r['frac'])"
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final_smoke.log 2>&1; echo "smoke rc=$?"
+timeout 300 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/final_bench_c2.json 2> gpurun_out/final_bench_c2.err; echo "bench c2 rc=$?"
+timeout 300 python bench.py --config 5 --scaling strong --steps 20 --warmup 5 > gpurun_out/final_bench_c5.json 2> gpurun_out/final_bench_c5.err; echo "bench c5 rc=$?"
+python -c "
+import json
+for f in ['gpurun_out/final_bench_c2.json','gpurun_out/final_bench_c5.json']:
+    d=json.loads(open(f).read().strip().splitlines()[-1]); r=d['roofline']
+    print(f, d['value'], d['ms_per_step'], d['e2e']['value'], r['kernel'], r['frac'], d['clocks'], d['detail']['op_ms_warmup'].get('admit'), d['detail']['op_ms_warmup'].get('fedavg'))
+"
