@@ -153,7 +153,7 @@ struct protea_ctx {
   int lanes = 1;     // lock-step lanes per model group (PROTEA_LANES): independent chains on own streams
   int spin_cap = 148;  // CTAs of a kernel whose CTAs spin-wait on each other (the width-1 CNN wgrad split
                        // reduces): g_num_sms / lanes, so concurrent lanes' instances are all co-resident
-  int64_t overlap_rows = 640;  // defer when the iteration has at most this many rows (PROTEA_OVERLAP_ROWS); measured best: 640
+  int64_t overlap_rows = 300;  // defer when the iteration has at most this many rows (PROTEA_OVERLAP_ROWS); round 2 sweep: 0 / 300 / 640 / 1000 / 1500 rows -> 57.50 / 57.52 / 58.36 / 58.45 / 58.89 ms
   // per-op-class accounting of the current round (protea_round_stats)
   uint32_t time_ops = 0;
   bool serialize = false;  // this round: no side-stream deferral (protea_round_opts.serialize)
