@@ -131,3 +131,25 @@ def test_survey_hwm_examples_reconciled(item):
     # every removed buffer is one of the survey's, every added one is in the built layout
     assert {n for n, _, _ in item["removed"]} <= {n for n, _ in item["survey_buffers"]}
     assert {n for n, _, _ in item["added"]} <= {n for n, _ in case["buffers"]}
+
+
+def test_resnet8_wgrad_split_rule():
+    """oracle.profiler.resnet8_wgrad_splits: every split holds whole images and at most 2048
+    output pixels; 32x32 layers use 2-image splits; 16x16 / 8x8 layers use at least min(4, ceil(b / 2))
+    splits; the count never decreases with b (so the footprint stays monotone in the batch, reading R13);
+    and b = 64 gives the hand-derived split counts of tests/golden/hwm.json (32 / 8 / 4)."""
+    import math
+    for hw in (1024, 256, 64):
+        prev = 0
+        for b in range(1, 65):
+            s = pf.resnet8_wgrad_splits(hw, b)
+            assert s >= prev
+            prev = s
+            ips = math.ceil(b / s)  # images in the largest split of a balanced partition
+            assert ips * hw <= pf.WGRAD_CHUNK_PX, (hw, b, s)
+            assert s <= b
+            if hw == 1024:
+                assert s == math.ceil(b / 2)
+            else:
+                assert s >= min(4, math.ceil(b / 2))
+    assert [pf.resnet8_wgrad_splits(hw, 64) for hw in (1024, 256, 64)] == [32, 8, 4]
