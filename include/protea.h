@@ -205,8 +205,10 @@ typedef struct {
   uint64_t op_timed_bytes[PROTEA_N_OPC];
 } protea_round_stats;
 
-/* Create a context on opts->device.  world > 1 bootstraps an NCCL communicator
- * from opts->nccl_id.  Errors: INVALID (bad field), CUDA, NCCL. */
+/* Create a context on opts->device: the simulation engine of one GPU (P:209 the VCE's per-GPU resource
+ * pool, here the caller-owned arena of capacity C_g = opts->arena_bytes that client slots are packed into,
+ * Eq. (1)).  world > 1 bootstraps an NCCL communicator from opts->nccl_id (multi-GPU placement,
+ * P:334).  Errors: INVALID (bad field), CUDA, NCCL. */
 protea_status protea_init(const protea_init_opts* opts, protea_ctx** out);
 
 /* Free the context, its device copies and workspace (not the caller's arena). */
@@ -215,14 +217,18 @@ void protea_finalize(protea_ctx* ctx);
 /* Message of the last failed call on ctx (or of the last failed context-free call when ctx == NULL). */
 const char* protea_last_error(const protea_ctx* ctx);
 
-/* Register a shape group.  Its global weights occupy [offset, offset + n_params)
- * of the concatenated global vector, groups in registration order; *n_params
- * receives P of this group.  Errors: INVALID. */
+/* Register a shape group (a model of P:304: MLP, CNN-w, ResNet-8 / ResNet-18, reading R11 / R26 / R27;
+ * the groups of HeteroFL-style widths are FedAvg'd independently, reading R12).  Its global weights occupy
+ * [offset, offset + n_params) of the concatenated global vector, groups in registration order; *n_params
+ * receives P of this group.  All groups of a context take one input size (INVALID otherwise).
+ * Errors: INVALID. */
 protea_status protea_register_model(protea_ctx* ctx, const protea_model_desc* desc, int32_t* model_id,
                                     uint64_t* n_params);
 
-/* Copy n shards to device (library-owned).  Re-registering an id replaces it.
- * Errors: INVALID (null, n_k <= 0, label out of range is not checked), CUDA. */
+/* Copy n shards to device (library-owned): each client's local data set (P:302 the per-client partitions;
+ * synthetic here).  Re-registering an id replaces it.  Labels are range-checked against the
+ * client's model when a round or profile uses the shard (INVALID there).
+ * Errors: INVALID (null, n_k <= 0), CUDA. */
 protea_status protea_register_shards(protea_ctx* ctx, const protea_shard* shards, size_t n);
 
 /* Profile n clients (shards must be registered): peak bytes, S_k, FLOPs, and the device time of one probe
